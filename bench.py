@@ -1,0 +1,369 @@
+"""Benchmark of the KK hot path (BASELINE.json metric: KK frames/s and
+pixel-pair samples/s, with the roofline fraction).
+
+Default workload: config 4 (functional-ultrasound ensemble, BASELINE.json
+configs[3]) — the configuration the metric is quoted on at 1/2/4/8 GPUs.
+A step = the whole hot path over one 400-frame ensemble per rank:
+real FFT -> per-bin element contraction -> inverse FFT -> kk pixel gather
+(+ fused |IQ|^2, per-frame max) -> dB map, every array in HBM.  The RF
+batch is 3.46 GB per rank (> 126 MB L2), so no L2 flush is needed between
+steps.  Multi-GPU: one process per GPU (torchrun), frames sharded by rank
+with no data-path collective (weak scaling: 400 frames per rank); the
+step time is the max over ranks of CUDA-event time.
+
+--impl reference: the CPU restatement of the reference path (oracle/:
+numpy/scipy stage 1 in the reference benchmark's complex64 form, C/OpenMP
+kk loop) on the host cores, bounded samples of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+METRIC = "KK frames/s (pixel-pair samples/s alongside), whole hot path"
+UNIT = "frames/s"
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def _workload(cfg: int, frames: int):
+    from paper_2603_22496_b200 import configs
+
+    if cfg == 4:
+        return configs.config4(frames=frames)
+    w = configs.CONFIGS[cfg]()
+    return w
+
+
+# ----------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], None, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax = float(parts[1])
+            except ValueError:
+                continue
+            for name, val in zip(names, parts[4:8]):
+                if val.lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------- CPU arms
+def cpu_pipeline_rate(w, seconds: float = 12.0, min_frames: int = 2, threads: int = 0):
+    """Oracle port of the reference path on the host: frames/s over a bounded
+    sample (>= min_frames, ~`seconds` of work)."""
+    from oracle import kkbeam_oracle as O
+    from paper_2603_22496_b200 import configs
+
+    O.build()
+    arr, p, rx, g = w.array, w.params, w.receive, w.grid
+    fs, c = arr.sampling_frequency, p.sound_speed
+    luts = O.kk_luts(g.x, g.z, p.transmit_angles, rx.angles, c)
+    rf = configs.noise_rf(p.num_transmits, arr.num_elements, p.num_samples, seed=0)
+    ones = np.ones(rx.num_angles)
+    shift = (0.0 - p.start_time) * fs
+
+    def frame():
+        tr = O.decompose_c64_staged(rf, fs, arr.positions, rx.angles, c)
+        img = O.kk_kernel(tr, *luts, ones, fs, shift, threads=threads)
+        return O.log_compress_db(O.intensity(img))
+
+    frame()  # warm-up (OpenMP pool, scipy planning)
+    n, t0 = 0, time.perf_counter()
+    while n < min_frames or time.perf_counter() - t0 < seconds:
+        frame()
+        n += 1
+    dt = time.perf_counter() - t0
+    return n / dt, n, dt
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    w = _workload(args.config, args.frames)
+    cores = os.cpu_count() or 1
+    # each step: a bounded sample of 2 frames of the same workload
+    per_step = []
+    for _ in range(args.warmup):
+        cpu_pipeline_rate(w, seconds=0.0, min_frames=1)
+    for _ in range(args.steps):
+        r, n, dt = cpu_pipeline_rate(w, seconds=0.0, min_frames=2)
+        per_step.append(dt)
+    t = sum(per_step)
+    value = 2 * args.steps / t
+    pp = w.grid.nx * w.grid.nz * w.pairs
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * t / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32/f64 (complex64 traces, float64 index math, complex128 image)",
+        "data": "synthetic (seeded noise RF, reference bench.noise_volume)",
+        "config": {"workload": w.name, "frames_per_step": 2, "pixel_pairs_per_frame": pp},
+        "pixel_pair_samples_per_s": value * pp,
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": "2 frames per step of the workload: numpy/scipy complex64 "
+                                   "stage 1 (bench.py:113-138 form) + C/OpenMP kk loop (all cores)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+# ----------------------------------------------------------------- GPU arm
+def run_gpu(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2603_22496_b200 as kb
+    from paper_2603_22496_b200 import _lib, configs
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    w = _workload(args.config, args.frames)
+    F = w.frames if args.config == 4 else args.frames
+    arr, p, rx, g = w.array, w.params, w.receive, w.grid
+    N, L, T, M = p.num_transmits, arr.num_elements, p.num_samples, rx.num_angles
+    P = g.nx * g.nz
+    pp_frame = P * N * M
+
+    # per-rank input: seeded noise frames (tiled from a few distinct frames to keep
+    # host generation short); each rank gets different seeds
+    distinct = min(F, 8)
+    base = np.stack([configs.noise_rf(N, L, T, seed=1000 * rank + s) for s in range(distinct)])
+    rf_dev = torch.empty((F, N, L, T), dtype=torch.float32, device="cuda")
+    src = torch.from_numpy(base).cuda()
+    for f0 in range(0, F, distinct):
+        n = min(distinct, F - f0)
+        rf_dev[f0:f0 + n].copy_(src[:n])
+    del src
+
+    eng = kb.KKEngine(arr, p, rx, g, frames=F, chunk_frames=args.chunk)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        eng.decompose(rf_dev)
+        e_mid.record(stream)
+        eng.gather()
+        e_g.record(stream)
+        eng.detect()
+
+    # warm-up
+    e_mid, e_g = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    mids = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    gs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    launches0 = _lib.launch_count()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    t_start.record(stream)
+    for i in range(args.steps):
+        starts[i].record(stream)
+        e_mid, e_g = mids[i], gs[i]
+        step()
+        ends[i].record(stream)
+    t_end.record(stream)
+    torch.cuda.synchronize()
+    launches = _lib.launch_count() - launches0
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    total_ms = t_start.elapsed_time(t_end)
+    if world > 1:
+        tt = torch.tensor([total_ms], device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        total_ms = float(tt.item())
+    ms_step = total_ms / args.steps
+    value = world * F / (total_ms / 1e3 / args.steps)
+
+    dec_ms = statistics.median(starts[i].elapsed_time(mids[i]) for i in range(args.steps))
+    kk_ms = statistics.median(mids[i].elapsed_time(gs[i]) for i in range(args.steps))
+    det_ms = statistics.median(gs[i].elapsed_time(ends[i]) for i in range(args.steps))
+
+    # ---- roofline of the dominant kernel (K5 gather, one launch per step) ----
+    hbm_peak, peak_kind = _peaks()
+    sm_count = torch.cuda.get_device_properties(local).multi_processor_count
+    gather_bytes_alg = 16.0 * pp_frame * F                     # 16 B x pp
+    compulsory = F * (N * M * T * 8 + P * (8 + 4)) + 8 * (g.nx + g.nz) * (N + M)
+    achieved_hbm = compulsory / (kk_ms / 1e3) / 1e9
+    sm_mhz = clk.get("sm_mhz") or 1965.0
+    smem_peak = sm_count * 128 * sm_mhz * 1e6 / 1e9           # GB/s, 128 B/clk/SM crossbar
+    achieved_taps = gather_bytes_alg / (kk_ms / 1e3) / 1e9
+
+    # ---- end to end through the public API: pinned host RF in, host IQ out ----
+    e2e = None
+    if not args.no_e2e:
+        host_rf = torch.empty((F, N, L, T), dtype=torch.float32).pin_memory()
+        for f0 in range(0, F, distinct):
+            n = min(distinct, F - f0)
+            host_rf[f0:f0 + n].copy_(torch.from_numpy(base[:n]))
+        host_iq = torch.empty((F, g.nx, g.nz), dtype=torch.complex64).pin_memory()
+        streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+        for _ in range(max(1, min(args.warmup, 2))):
+            eng.run_host(host_rf, host_iq, chunk_frames=args.e2e_chunk, streams=streams)
+        e2e_steps = max(1, min(args.steps, 5))
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            eng.run_host(host_rf, host_iq, chunk_frames=args.e2e_chunk, streams=streams)
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        if world > 1:
+            tt = torch.tensor([dt], device="cuda")
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            dt = float(tt.item())
+        e2e = {"value": world * F * e2e_steps / dt, "unit": UNIT,
+               "h2d_bytes_per_step": int(host_rf.numel() * 4),
+               "d2h_bytes_per_step": int(host_iq.numel() * 8),
+               "path": "KKEngine.run_host: pinned H2D RF, decompose+kk on 2 streams, D2H IQ"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        r, n, dt = cpu_pipeline_rate(w, seconds=args.cpu_seconds)
+        cpu = {"value": r, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
+               "sample": f"{n} frames of {w.name} in {dt:.1f} s: numpy/scipy complex64 stage 1 "
+                         "(reference bench.py:113-138 form) + C/OpenMP kk loop on all cores"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32 (complex64 traces/IQ; float64 delay-index math)",
+            "data": "synthetic (seeded noise RF, shapes of BASELINE config 4)",
+            "config": {"workload": w.name, "frames_per_rank": F, "N_tx": N, "M_rx": M,
+                       "L_el": L, "T": T, "grid": [g.nx, g.nz],
+                       "pixel_pairs_per_frame": pp_frame,
+                       "l2": "inputs larger than L2 (3.46 GB RF per rank), no flush",
+                       "parallelism": f"frame-sharded x{world}"},
+            "pixel_pair_samples_per_s": value * pp_frame,
+            "stage_ms": {"decompose(K1-K3)": dec_ms, "kk_gather(K5)": kk_ms, "db_map(K6)": det_ms},
+            "roofline": {"kernel": "k_kk_gather", "bound": "hbm",
+                         "achieved": achieved_hbm, "peak": hbm_peak, "unit": "GB/s",
+                         "frac": achieved_hbm / hbm_peak, "traffic": None,
+                         "peak_kind": peak_kind,
+                         "algorithmic_bytes": "compulsory HBM per launch: traces read + IQ/intensity "
+                                              "write + tables (SURVEY 8d)"},
+            "onchip_roofline": {"kernel": "k_kk_gather", "bound": "smem",
+                                "achieved": achieved_taps, "peak": smem_peak, "unit": "GB/s",
+                                "frac": achieved_taps / smem_peak,
+                                "algorithmic_bytes": "16 B of taps per pixel-pair (SURVEY 8d)",
+                                "pixel_pairs_per_s": pp_frame * F / (kk_ms / 1e3)},
+            "gpu_launches": int(launches),
+            "clocks": clk,
+        }
+        if e2e:
+            line["e2e"] = e2e
+        if cpu:
+            line["cpu_baseline"] = cpu
+        print(json.dumps(line))
+    eng.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="kkb", choices=["kkb", "reference"])
+    ap.add_argument("--config", type=int, default=4)
+    ap.add_argument("--frames", type=int, default=400)
+    ap.add_argument("--chunk", type=int, default=None, help="frames per decomposition pass")
+    ap.add_argument("--e2e-chunk", type=int, default=16)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "kkb":
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_gpu(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

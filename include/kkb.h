@@ -1,0 +1,172 @@
+/*
+ * kkb.h — C ABI of the B200-native KK beamforming hot path (libkkb.so).
+ *
+ * Drop-in boundary for the reference package `kkbeam` (arXiv 2603.22496).
+ * The reference has no FFI: its operator boundary is the flat-array numba
+ * kernels its Python wrappers look up at call time, plus the Python
+ * signatures around them.  Each entry point below names the reference
+ * interface it replaces (paths relative to /root/reference/pkg/src/kkbeam).
+ *
+ * Conventions (all entry points):
+ *   - Array pointers are DEVICE pointers unless the parameter name ends in
+ *     `_host`.  Layouts are C row-major, the reference's own (core.py:28-29,
+ *     beamform.py:83-93): RF float32 (N, L, T); analytic / decomposed data
+ *     complex64 interleaved (re, im) float pairs; LUTs float64 (X, N) etc.
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default).
+ *     Every call is asynchronous on that stream.
+ *   - Return 0 (KKB_OK) or a negative KKB_ERR_* code; kkb_last_error() gives
+ *     the message.  Kernels never raise: shape/geometry validation belongs
+ *     to the caller (the reference validates in Python before its kernels,
+ *     beamform.py:239-254,356-359; compress.py:110-119).
+ *   - Output buffers are caller-allocated and fully overwritten
+ *     (beamform.py:280,362 allocate `out` and the kernel writes every pixel).
+ */
+#ifndef KKB_H
+#define KKB_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define KKB_OK 0
+#define KKB_ERR_ARG (-1)          /* bad argument value          -> ConfigError   */
+#define KKB_ERR_SHAPE (-2)        /* inconsistent shapes/geometry -> GeometryError */
+#define KKB_ERR_CUDA (-3)         /* CUDA runtime failure                          */
+#define KKB_ERR_NOMEM (-4)        /* device allocation failed                      */
+#define KKB_ERR_UNSUPPORTED (-5)  /* size outside what the kernels support         */
+
+/* image output element type */
+#define KKB_OUT_C64 0   /* complex64  (throughput path, BASELINE config 5 "fp32 complex IQ") */
+#define KKB_OUT_C128 1  /* complex128 (ComplexImage dtype, core.py:232)                      */
+
+/* ------------------------------------------------------------ library */
+const char *kkb_version(void);
+const char *kkb_last_error(void);
+/* SM count and compute capability of the current device. */
+int kkb_device_info(int *sm_count, int *cc_major, int *cc_minor);
+/* Number of kernel launches this library issued since load (all threads). */
+long long kkb_launch_count(void);
+/* Reads and clears the device-side error word (synchronous). */
+int kkb_take_device_error(int *flag);
+
+/* ------------------------------------------------------------ K4: delay tables
+ * Replaces build_kk_luts / _tx_tables (beamform.py:121-126,159-175):
+ *   ltx[ix,n] = x[ix]*sin_tx[n]/c   ltz[iz,n] = z[iz]*cos_tx[n]/c
+ *   lrx[ix,m] = x[ix]*sin_rx[m]/c   lrz[iz,m] = z[iz]*cos_rx[m]/c
+ * with x = x0 + dx*ix, z = z0 + dz*iz (core.py:133-138), every product and
+ * quotient IEEE-rounded in that order -> bit-identical to the reference.
+ * sin/cos arrays are device copies of numpy's np.sin/np.cos values. */
+int kkb_build_kk_luts(double x0, double dx, int nx, double z0, double dz, int nz,
+                      const double *sin_tx, const double *cos_tx, int n_tx,
+                      const double *sin_rx, const double *cos_rx, int n_rx, double c,
+                      double *ltx, double *ltz, double *lrx, double *lrz, void *stream);
+
+/* ------------------------------------------------------------ K5: kk pixel gather
+ * Replaces _kk_kernel (beamform.py:212-236), called by kk (beamform.py:363-374):
+ *   out[f,ix,iz] = sum_n sum_m w[m] * lerp(data[f,n,m,:], fi)
+ *   fi = ((ltx[ix,n] + ltz[iz,n]) + lrz[iz,m] - lrx[ix,m]) * fs + shift
+ * linear (linear != 0): i0 = floor(fi), read iff 0 <= i0 && i0+1 <= T-1;
+ * nearest: j = floor(fi + 0.5), read iff 0 <= j <= T-1; else adds 0.
+ * fi is evaluated in float64 in exactly that order (tap indices and the
+ * in-window predicate are bit-identical to the reference); taps and the
+ * per-transmit partial sums are float32, the running sum float64.
+ * `weights` may be NULL (all ones, beamform.py:239-241).
+ * n_frames frames share the tables: data frame f at data + f*data_frame_stride
+ * (complex elements), out frame f at out + f*out_frame_stride (elements).
+ * `intensity` (may be NULL): also writes |out|^2 as float32, frame stride
+ * out_frame_stride (the detection of beamform.py:378-380, fused).
+ * `frame_max` (may be NULL, n_frames uint32, zeroed by the call): receives the bit
+ * pattern of max |out|^2 per frame for the dB epilogue. */
+int kkb_kk(const void *data, int n_tx, int n_rx, int n_t,
+           const double *ltx, const double *ltz, const double *lrx, const double *lrz,
+           int nx, int nz, const double *weights, double fs, double shift, int linear,
+           void *out, int out_kind, int n_frames, long long data_frame_stride,
+           long long out_frame_stride, float *intensity, unsigned int *frame_max,
+           void *stream);
+
+/* Plan form of K5 for repeated launches on fixed tables (the device-resident
+ * throughput path): copies the tables, builds depth-major copies of ltz/lrz,
+ * and sizes the shared-memory trace window once (synchronises `stream`). */
+typedef struct kkb_kk_plan kkb_kk_plan;
+int kkb_kk_plan_create(const double *ltx, const double *ltz, const double *lrx, const double *lrz,
+                       int n_tx, int n_rx, int n_t, int nx, int nz, const double *weights,
+                       double fs, double shift, int linear, void *stream, kkb_kk_plan **out);
+int kkb_kk_plan_run(kkb_kk_plan *p, const void *data, int n_frames, long long data_frame_stride,
+                    void *out, int out_kind, long long out_frame_stride, float *intensity,
+                    unsigned int *frame_max, void *stream);
+/* trace window (samples per pair) the plan stages in shared memory */
+int kkb_kk_plan_window(const kkb_kk_plan *p);
+int kkb_kk_plan_destroy(kkb_kk_plan *p);
+
+/* Diagnostic twin of K5's index math (same device function): writes the tap
+ * index of every (pixel, pair) as int32 idx[ix, iz, n, m], -1 when the read
+ * falls outside the window.  Used to prove the indices bit-identical to the
+ * reference's floor((((ltx+ltz)+lrz)-lrx)*fs+shift) (beamform.py:225-233). */
+int kkb_kk_taps(const double *ltx, const double *ltz, const double *lrx, const double *lrz,
+                int n_tx, int n_rx, int n_t, int nx, int nz, double fs, double shift, int linear,
+                int *idx, void *stream);
+
+/* ------------------------------------------------------------ K7: DAS comparison gather
+ * Replaces _das_kernel (beamform.py:178-209), called by das (beamform.py:281-297).
+ * hyp is (nx + l_eff, nz); base int64 (L,); frac (L,); xcoord (X,), zcoord
+ * (Z,), upos (L,); tan_max = +inf disables the receive gate (beamform.py:48). */
+int kkb_das(const void *data, int n_tx, int n_el, int n_t,
+            const double *ltx, const double *ltz, const double *hyp, int n_hyp_rows,
+            const long long *base, const double *frac, const double *xcoord,
+            const double *zcoord, const double *upos, double tan_max,
+            const double *weights, double fs, double shift, int linear,
+            int nx, int nz, void *out, int out_kind, void *stream);
+
+/* ------------------------------------------------------------ K1/K3: spectral
+ * Replaces analytic_signal (spectral.py:84-93): length-T FFT of each float32
+ * trace, one-sided weights (spectral.py:65-81), inverse FFT -> complex64.
+ * Any T >= 2 with T <= 8192 (mixed radix 2/3/4/5/8 plus direct odd radices). */
+int kkb_analytic_signal(const float *rf, long long n_traces, int n_t, void *out, void *stream);
+
+/* ------------------------------------------------------------ K1-K3: decomposition
+ * Replaces shear_and_sum (compress.py:54-82), the data path of compress
+ * (compress.py:120): complex (N, L, T) -> complex64 (N, M, T),
+ *   out[n,m] = IFFT( sum_l FFT(data[n,l]) * exp(2 pi i f tau_lm) ),
+ *   tau_lm = positions[l] * (sin(angles[m]) / c),  f = fftfreq(T, 1/fs).
+ * positions_host / angles_host are host arrays. */
+int kkb_shear_and_sum(const void *data, int n_tx, int n_el, int n_t,
+                      const double *positions_host, const double *angles_host, int n_rx,
+                      double fs, double c, void *out, void *stream);
+
+/* ------------------------------------------------------------ fused stage 1 plan
+ * Device-resident, batched form of analytic_signal + compress — the data
+ * flow of the reference's complex64 benchmark stages (bench.py:113-153):
+ * real FFT of the RF -> one-sided weights x cached ramps, contracted over
+ * elements per bin -> inverse FFT, for F frames at once.  Ramps (the
+ * reference caches them too, bench.py:124-125) and scratch live in the plan. */
+typedef struct kkb_decomposer kkb_decomposer;
+
+int kkb_decomposer_create(int n_tx, int n_el, int n_t, const double *positions_host,
+                          const double *angles_host, int n_rx, double fs, double c,
+                          int max_frames, kkb_decomposer **out);
+/* rf: (F, N, L, T) float32; traces: (F, N, M, T) complex64. */
+int kkb_decomposer_run(kkb_decomposer *p, const float *rf, int n_frames, void *traces,
+                       void *stream);
+/* bytes of device scratch held by the plan */
+long long kkb_decomposer_workspace_bytes(const kkb_decomposer *p);
+int kkb_decomposer_destroy(kkb_decomposer *p);
+
+/* ------------------------------------------------------------ K6: log-compression epilogue
+ * dB display map (new; the reference has no log compression):
+ * db[f,p] = max(10*log10(intensity[f,p] / max_f), floor_db), max_f from the
+ * frame_max array filled by kkb_kk. */
+int kkb_log_compress(const float *intensity, const unsigned int *frame_max, int n_frames,
+                     long long pixels_per_frame, float floor_db, float *db, void *stream);
+
+/* Element-wise compounding over J images (beamform.py:396-411):
+ * mode 0 coherent |sum_j B_j|^2, mode 1 incoherent sum_j |B_j|^2.
+ * images: J x P complex128; out: P float64. */
+int kkb_compound(const void *images, int n_images, long long n_pixels, int mode,
+                 double *out, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KKB_H */

@@ -1,0 +1,35 @@
+"""B200-native KK beamforming hot path (arXiv 2603.22496).
+
+Drop-in for the hot path of the reference package ``kkbeam``: the same
+public names, container types, sampling-scheme objects and error types for
+stage 1 (analytic signal + receive decomposition) and stage 2 (delay
+tables, kk / das image formation, detection and compounding), computed by
+hand-written sm_100a CUDA kernels in ``libkkb.so`` (``include/kkb.h``).
+``KKEngine`` is the device-resident batched pipeline for throughput.
+
+There is no CPU fallback: without the CUDA library or a GPU the compute
+entry points raise ``DeviceError``.
+"""
+
+from .beamform import (BeamformConfig, DelayLUTSet, build_das_luts, build_kk_luts,
+                       cache_model_entries, compound_coherent, compound_incoherent, das,
+                       intensity, kk)
+from .compress import compress, compression_ratio, guard_band_samples, shear_and_sum
+from .core import (AcquisitionParams, AnalyticRF, ComplexImage, CompressedRF, ImageGrid,
+                   IntensityImage, RFVolume, TransducerArray, element_positions, sample_index)
+from .errors import (ConfigError, DataError, DeviceError, GeometryError, GuardBandError,
+                     KKBeamError, WindowOverflowError)
+from .sampling import (ReceiveAngleSet, SupportSample, confocal_angles, explicit_angles, support,
+                       transmit_angles, uniform_vernier_angles)
+from .spectral import analytic_signal, one_sided_weights
+
+__version__ = "0.1.0"
+
+
+def __getattr__(name):
+    # lazy: importing the engine pulls in torch
+    if name == "KKEngine":
+        from .engine import KKEngine
+
+        return KKEngine
+    raise AttributeError(name)

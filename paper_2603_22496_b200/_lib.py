@@ -1,0 +1,98 @@
+"""ctypes binding of libkkb.so (include/kkb.h).
+
+The shared library is built in-tree by ``__graft_entry__.build()`` (nvcc,
+``-gencode arch=compute_100a,code=sm_100a``).  There is no CPU fallback:
+if the library or a CUDA device is missing, every product entry point
+raises ``DeviceError`` instead of computing something else.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+from .errors import DeviceError, raise_for_status
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libkkb.so")
+
+P = ctypes.c_void_p
+I = ctypes.c_int
+LL = ctypes.c_longlong
+D = ctypes.c_double
+F = ctypes.c_float
+
+# name -> argtypes (restype int unless listed in _RESTYPES)
+SIGNATURES = {
+    "kkb_version": [],
+    "kkb_last_error": [],
+    "kkb_device_info": [P, P, P],
+    "kkb_launch_count": [],
+    "kkb_take_device_error": [P],
+    "kkb_build_kk_luts": [D, D, I, D, D, I, P, P, I, P, P, I, D, P, P, P, P, P],
+    "kkb_kk": [P, I, I, I, P, P, P, P, I, I, P, D, D, I, P, I, I, LL, LL, P, P, P],
+    "kkb_kk_plan_create": [P, P, P, P, I, I, I, I, I, P, D, D, I, P, P],
+    "kkb_kk_plan_run": [P, P, I, LL, P, I, LL, P, P, P],
+    "kkb_kk_plan_window": [P],
+    "kkb_kk_plan_destroy": [P],
+    "kkb_kk_taps": [P, P, P, P, I, I, I, I, I, D, D, I, P, P],
+    "kkb_das": [P, I, I, I, P, P, P, I, P, P, P, P, P, D, P, D, D, I, I, I, P, I, P],
+    "kkb_analytic_signal": [P, LL, I, P, P],
+    "kkb_shear_and_sum": [P, I, I, I, P, P, I, D, D, P, P],
+    "kkb_decomposer_create": [I, I, I, P, P, I, D, D, I, P],
+    "kkb_decomposer_run": [P, P, I, P, P],
+    "kkb_decomposer_workspace_bytes": [P],
+    "kkb_decomposer_destroy": [P],
+    "kkb_log_compress": [P, P, I, LL, F, P, P],
+    "kkb_compound": [P, I, LL, I, P, P],
+}
+_RESTYPES = {
+    "kkb_version": ctypes.c_char_p,
+    "kkb_last_error": ctypes.c_char_p,
+    "kkb_launch_count": LL,
+    "kkb_decomposer_workspace_bytes": LL,
+}
+
+KKB_OUT_C64 = 0
+KKB_OUT_C128 = 1
+
+_lib = None
+
+
+def load() -> ctypes.CDLL:
+    """Load libkkb.so once; raise DeviceError if it is absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise DeviceError(
+            f"{LIB_PATH} is missing: run __graft_entry__.build() (nvcc, sm_100a); "
+            "this package has no CPU fallback")
+    lib = ctypes.CDLL(LIB_PATH)
+    for name, args in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = _RESTYPES.get(name, I)
+    _lib = lib
+    return lib
+
+
+def call(name: str, *args) -> None:
+    """Invoke a status-returning entry point and map failures to exceptions."""
+    lib = load()
+    st = getattr(lib, name)(*args)
+    if st != 0:
+        raise_for_status(st, name, lib.kkb_last_error().decode(errors="replace"))
+
+
+def last_error() -> str:
+    return load().kkb_last_error().decode(errors="replace")
+
+
+def launch_count() -> int:
+    """Kernel launches issued by libkkb in this process so far."""
+    return int(load().kkb_launch_count())
+
+
+def version() -> str:
+    return load().kkb_version().decode()

@@ -1,0 +1,264 @@
+"""Delay tables and image formation on the GPU (drop-in for kkbeam.beamform).
+
+Keeps the reference signatures, validation and error types
+(beamform.py:51-411):
+
+* ``build_kk_luts`` builds the four separable tables with the K4 kernel
+  (bit-identical to numpy's ``x*sin/c``), keeps device copies for ``kk``
+  and returns the host arrays in a ``DelayLUTSet``;
+* ``kk`` runs the K5 pixel-gather (replacing ``_kk_kernel``,
+  beamform.py:212-236) and returns a complex128 ``ComplexImage``;
+* ``das`` runs the K7 comparison gather (replacing ``_das_kernel``,
+  beamform.py:178-209) on tables from ``build_das_luts``;
+* ``intensity`` / ``compound_coherent`` / ``compound_incoherent`` run the
+  K6 element-wise kernel.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _device as dev
+from . import _lib
+from .core import AnalyticRF, ComplexImage, CompressedRF, ImageGrid, IntensityImage
+from .errors import ConfigError, GeometryError
+from .sampling import ReceiveAngleSet
+
+_NO_GATE = math.inf
+
+
+@dataclass(frozen=True)
+class BeamformConfig:
+    """Interpolation, pulse delay, receive gating (das) and channel weights
+    (beamform.py:51-72)."""
+
+    interpolation: str = "linear"
+    pulse_delay: float = 0.0
+    max_rx_angle: float | None = None
+    channel_weights: np.ndarray | None = None
+
+    def __post_init__(self):
+        if self.interpolation not in ("linear", "nearest"):
+            raise ConfigError(f"unknown interpolation {self.interpolation!r}")
+        if self.max_rx_angle is not None and not 0 < self.max_rx_angle < math.pi / 2:
+            raise ConfigError("max_rx_angle must be in (0, pi/2)")
+
+
+@dataclass(frozen=True, eq=False)
+class DelayLUTSet:
+    """Delay tables bound to one (grid, acquisition) pair (beamform.py:75-102).
+
+    ``device`` caches CUDA copies of the tables for the gather kernels."""
+
+    kind: str
+    grid: ImageGrid
+    sound_speed: float
+    transmit_angles: np.ndarray
+    lut_tx_x: np.ndarray
+    lut_tx_z: np.ndarray
+    element_positions: np.ndarray | None = None
+    lut_rx_hypot: np.ndarray | None = None
+    rx_base: np.ndarray | None = None
+    rx_frac: np.ndarray | None = None
+    receive_angles: np.ndarray | None = None
+    lut_rx_x: np.ndarray | None = None
+    lut_rx_z: np.ndarray | None = None
+    device: dict = field(default_factory=dict, repr=False)
+
+    @property
+    def entry_count(self) -> int:
+        n = self.lut_tx_x.size + self.lut_tx_z.size
+        for t in (self.lut_rx_hypot, self.lut_rx_x, self.lut_rx_z):
+            if t is not None:
+                n += t.size
+        return n
+
+    def dev(self, name: str):
+        """CUDA copy of a table (uploaded on first use)."""
+        if name not in self.device:
+            self.device[name] = dev.to_device(getattr(self, name))
+        return self.device[name]
+
+
+def cache_model_entries(grid: ImageGrid, num_transmits: int, num_channels: int, kind: str) -> int:
+    """Nominal delay-cache sizes: das (X+Z)N + (X+L)Z, kk (X+Z)(N+M)
+    (beamform.py:105-118)."""
+    x, z = grid.nx, grid.nz
+    if kind == "das":
+        return (x + z) * num_transmits + (x + num_channels) * z
+    if kind == "kk":
+        return (x + z) * (num_transmits + num_channels)
+    raise ConfigError(f"unknown beamformer kind {kind!r}")
+
+
+def _tx_tables_host(grid: ImageGrid, angles, c):
+    s, co = np.sin(angles), np.cos(angles)
+    return grid.x[:, None] * s[None, :] / c, grid.z[:, None] * co[None, :] / c
+
+
+def build_kk_luts_device(grid: ImageGrid, transmit_angles, receive_angles, c, stream=None):
+    """The four kk tables as CUDA tensors (K4 kernel)."""
+    ta = np.asarray(transmit_angles, dtype=np.float64)
+    ra = np.asarray(receive_angles, dtype=np.float64)
+    trig = dev.to_device(np.concatenate([np.sin(ta), np.cos(ta), np.sin(ra), np.cos(ra)]))
+    n, m = ta.size, ra.size
+    ltx = dev.empty((grid.nx, n), np.float64)
+    ltz = dev.empty((grid.nz, n), np.float64)
+    lrx = dev.empty((grid.nx, m), np.float64)
+    lrz = dev.empty((grid.nz, m), np.float64)
+    base = trig.data_ptr()
+    _lib.call("kkb_build_kk_luts", float(grid.x0), float(grid.dx), grid.nx, float(grid.z0),
+              float(grid.dz), grid.nz, base, base + 8 * n, n, base + 16 * n, base + 16 * n + 8 * m,
+              m, float(c), dev.ptr(ltx), dev.ptr(ltz), dev.ptr(lrx), dev.ptr(lrz),
+              dev.stream_handle(stream))
+    return {"lut_tx_x": ltx, "lut_tx_z": ltz, "lut_rx_x": lrx, "lut_rx_z": lrz, "_trig": trig}
+
+
+def build_kk_luts(grid: ImageGrid, params, receive: ReceiveAngleSet) -> DelayLUTSet:
+    """Separable transmit and receive plane-wave delay tables (beamform.py:159-175)."""
+    c = params.sound_speed
+    d = build_kk_luts_device(grid, params.transmit_angles, receive.angles, c)
+    dev.synchronize()
+    d.pop("_trig")
+    host = {k: dev.to_host(v) for k, v in d.items()}
+    return DelayLUTSet(
+        kind="kk", grid=grid, sound_speed=c,
+        transmit_angles=np.asarray(params.transmit_angles, dtype=np.float64),
+        lut_tx_x=host["lut_tx_x"], lut_tx_z=host["lut_tx_z"],
+        receive_angles=np.asarray(receive.angles, dtype=np.float64),
+        lut_rx_x=host["lut_rx_x"], lut_rx_z=host["lut_rx_z"], device=d)
+
+
+def build_das_luts(grid: ImageGrid, array, params) -> DelayLUTSet:
+    """das tables: transmit tables plus the offset-grid hypot table
+    (beamform.py:129-156).  Built on the host (comparison path, < 1 ms)."""
+    c = params.sound_speed
+    ltx, ltz = _tx_tables_host(grid, params.transmit_angles, c)
+    u = array.positions
+    l_eff = int(math.ceil(array.aperture / grid.dx))
+    offsets = grid.x0 - u[-1] + grid.dx * np.arange(grid.nx + l_eff)
+    hyp = np.sqrt(offsets[:, None] ** 2 + grid.z[None, :] ** 2) / c
+    shift = (u[-1] - u) / grid.dx
+    base = np.floor(shift).astype(np.int64)
+    return DelayLUTSet(
+        kind="das", grid=grid, sound_speed=c,
+        transmit_angles=np.asarray(params.transmit_angles, dtype=np.float64),
+        lut_tx_x=ltx, lut_tx_z=ltz, element_positions=np.asarray(u, dtype=np.float64),
+        lut_rx_hypot=hyp, rx_base=base, rx_frac=shift - base)
+
+
+def _resolve_weights(config: BeamformConfig, count: int, what: str):
+    if config.channel_weights is None:
+        return None
+    w = np.asarray(config.channel_weights, dtype=np.float64)
+    if w.shape != (count,):
+        raise GeometryError(f"channel_weights must have shape ({count},) for {what}")
+    return w
+
+
+def _check_common(luts: DelayLUTSet, params, kind: str):
+    if luts.kind != kind:
+        raise GeometryError(f"LUT set was built for {luts.kind!r}, not {kind!r}")
+    if luts.sound_speed != params.sound_speed:
+        raise GeometryError("LUT sound speed does not match the data")
+    if not np.array_equal(luts.transmit_angles, params.transmit_angles):
+        raise GeometryError("LUT transmit angles do not match the data")
+
+
+def kk_device(data, luts: DelayLUTSet, fs: float, shift: float, linear: bool = True,
+              weights=None, out_kind: int = _lib.KKB_OUT_C128, stream=None):
+    """K5 on a CUDA tensor (N, M, T) complex64 -> CUDA image (X, Z)."""
+    t = dev.require_cuda()
+    g = luts.grid
+    n, m, T = (int(s) for s in data.shape)
+    out = t.empty((g.nx, g.nz), dtype=t.complex128 if out_kind == _lib.KKB_OUT_C128 else t.complex64,
+                  device="cuda")
+    w = dev.to_device(weights) if weights is not None else None
+    _lib.call("kkb_kk", dev.ptr(data.contiguous()), n, m, T, dev.ptr(luts.dev("lut_tx_x")),
+              dev.ptr(luts.dev("lut_tx_z")), dev.ptr(luts.dev("lut_rx_x")),
+              dev.ptr(luts.dev("lut_rx_z")), g.nx, g.nz, dev.ptr(w), float(fs), float(shift),
+              int(bool(linear)), dev.ptr(out), out_kind, 1, 0, 0, None, None,
+              dev.stream_handle(stream))
+    return out
+
+
+def kk(rfc: CompressedRF, luts: DelayLUTSet, config: BeamformConfig = BeamformConfig()) -> ComplexImage:
+    """Beamform decomposed plane-wave traces onto the LUT grid (beamform.py:340-375)."""
+    _check_common(luts, rfc.params, "kk")
+    if not np.array_equal(luts.receive_angles, rfc.receive_angles.angles):
+        raise GeometryError("LUT receive angles do not match the data")
+    w = _resolve_weights(config, rfc.receive_angles.num_angles, "kk")
+    fs = rfc.sampling_frequency
+    shift = (config.pulse_delay - rfc.params.start_time) * fs
+    out = kk_device(dev.to_device(rfc.data), luts, fs, shift,
+                    linear=config.interpolation == "linear", weights=w)
+    dev.synchronize()
+    return ComplexImage(dev.to_host(out), luts.grid)
+
+
+def das(rf: AnalyticRF, luts: DelayLUTSet, config: BeamformConfig = BeamformConfig()) -> ComplexImage:
+    """Delay-and-sum the analytic element data onto the LUT grid (beamform.py:257-298)."""
+    _check_common(luts, rf.params, "das")
+    if not np.array_equal(luts.element_positions, rf.array.positions):
+        raise GeometryError("LUT element positions do not match the array")
+    w = _resolve_weights(config, rf.array.num_elements, "das")
+    tan_max = math.tan(config.max_rx_angle) if config.max_rx_angle is not None else _NO_GATE
+    fs = rf.array.sampling_frequency
+    shift = (config.pulse_delay - rf.params.start_time) * fs
+    g = luts.grid
+    t = dev.require_cuda()
+    data = dev.to_device(rf.data)
+    out = t.empty((g.nx, g.nz), dtype=t.complex128, device="cuda")
+    wd = dev.to_device(w) if w is not None else None
+    n, l, T = rf.data.shape
+    if "xz" not in luts.device:
+        luts.device["xz"] = (dev.to_device(g.x), dev.to_device(g.z))
+    xd, zd = luts.device["xz"]
+    _lib.call("kkb_das", dev.ptr(data), n, l, T, dev.ptr(luts.dev("lut_tx_x")),
+              dev.ptr(luts.dev("lut_tx_z")), dev.ptr(luts.dev("lut_rx_hypot")),
+              int(luts.lut_rx_hypot.shape[0]), dev.ptr(luts.dev("rx_base")),
+              dev.ptr(luts.dev("rx_frac")), dev.ptr(xd), dev.ptr(zd),
+              dev.ptr(luts.dev("element_positions")), float(tan_max), dev.ptr(wd), float(fs),
+              float(shift), int(config.interpolation == "linear"), g.nx, g.nz, dev.ptr(out),
+              _lib.KKB_OUT_C128, dev.stream_handle())
+    dev.synchronize()
+    return ComplexImage(dev.to_host(out), g)
+
+
+def _common_grid(images):
+    if not images:
+        raise ConfigError("need at least one image to compound")
+    grid = images[0].grid
+    for im in images[1:]:
+        if im.grid is not grid and im.grid.key() != grid.key():
+            raise GeometryError("cannot compound images on different grids")
+    return grid
+
+
+def _compound(images, mode: int) -> IntensityImage:
+    grid = _common_grid(images)
+    t = dev.require_cuda()
+    stack = dev.to_device(np.stack([im.pixels for im in images]))
+    out = t.empty((grid.nx, grid.nz), dtype=t.float64, device="cuda")
+    _lib.call("kkb_compound", dev.ptr(stack), len(images), grid.nx * grid.nz, mode, dev.ptr(out),
+              dev.stream_handle())
+    dev.synchronize()
+    return IntensityImage(dev.to_host(out), grid)
+
+
+def intensity(image: ComplexImage) -> IntensityImage:
+    """|B|^2 (beamform.py:378-380)."""
+    return _compound([image], 0)
+
+
+def compound_coherent(images) -> IntensityImage:
+    """|sum_j B_j|^2 (beamform.py:396-402)."""
+    return _compound(list(images), 0)
+
+
+def compound_incoherent(images) -> IntensityImage:
+    """sum_j |B_j|^2 (beamform.py:405-411)."""
+    return _compound(list(images), 1)

@@ -1,0 +1,452 @@
+// C ABI of libkkb (include/kkb.h): validation, temporaries, plans.
+#include <atomic>
+#include <cmath>
+#include <cstdarg>
+#include <cstring>
+#include <mutex>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "fft.cuh"
+#include "kk.cuh"
+
+#define KKB_VERSION_STR "kkb-b200 0.1.0 (sm_100a)"
+
+namespace kkb {
+
+static thread_local std::string t_last_error;
+static std::atomic<long long> g_launches{0};
+
+void set_error(const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    t_last_error = buf;
+}
+
+int cuda_status(cudaError_t e, const char *what) {
+    set_error("%s: %s", what, cudaGetErrorString(e));
+    return e == cudaErrorMemoryAllocation ? KKB_ERR_NOMEM : KKB_ERR_CUDA;
+}
+
+void count_launch(int n) { g_launches += n; }
+
+int sm_count() {
+    int dev = 0, n = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n;
+}
+
+// numpy.fft.fftfreq(T, 1/fs)[k]: integer bin times 1/(T*d), d = 1/fs
+static double fftfreq(int k, int T, double fs) {
+    double d = 1.0 / fs;
+    double val = 1.0 / (T * d);
+    int half = (T - 1) / 2 + 1;  // count of non-negative bins
+    int kk = k < half ? k : k - T;
+    return kk * val;
+}
+
+// one_sided_weights (spectral.py:65-81)
+static double one_sided(int k, int T) {
+    if (k == 0) return 1.0;
+    if (T % 2 == 0) {
+        if (k < T / 2) return 2.0;
+        if (k == T / 2) return 1.0;
+        return 0.0;
+    }
+    return k <= (T - 1) / 2 ? 2.0 : 0.0;
+}
+
+__global__ void k_scale_bins(float2 *X, long long ntr, long long ld, int K, const float *scale) {
+    const long long total = ntr * K;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+         i += (long long)gridDim.x * blockDim.x) {
+        long long r = i / K;
+        int k = (int)(i - r * K);
+        float2 v = X[r * ld + k];
+        float s = scale[k];
+        X[r * ld + k] = make_float2(v.x * s, v.y * s);
+    }
+}
+
+// RAII device scratch on a stream (stream-ordered allocator)
+struct Scratch {
+    void *p = nullptr;
+    cudaStream_t s;
+    explicit Scratch(cudaStream_t st) : s(st) {}
+    int alloc(size_t bytes) {
+        if (bytes == 0) bytes = 16;
+        cudaError_t e = cudaMallocAsync(&p, bytes, s);
+        if (e != cudaSuccess) return cuda_status(e, "cudaMallocAsync");
+        return KKB_OK;
+    }
+    ~Scratch() {
+        if (p) cudaFreeAsync(p, s);
+    }
+};
+
+}  // namespace kkb
+
+using namespace kkb;
+
+// =====================================================================
+// library
+extern "C" const char *kkb_version(void) { return KKB_VERSION_STR; }
+extern "C" const char *kkb_last_error(void) { return t_last_error.c_str(); }
+extern "C" long long kkb_launch_count(void) { return g_launches.load(); }
+
+extern "C" int kkb_device_info(int *sms, int *major, int *minor) {
+    int dev = 0;
+    KKB_TRY_CUDA(cudaGetDevice(&dev), "cudaGetDevice");
+    cudaDeviceProp prop;
+    KKB_TRY_CUDA(cudaGetDeviceProperties(&prop, dev), "cudaGetDeviceProperties");
+    if (sms) *sms = prop.multiProcessorCount;
+    if (major) *major = prop.major;
+    if (minor) *minor = prop.minor;
+    return KKB_OK;
+}
+
+extern "C" int kkb_take_device_error(int *flag) { return take_device_error(flag); }
+
+// =====================================================================
+// K4
+extern "C" int kkb_build_kk_luts(double x0, double dx, int nx, double z0, double dz, int nz,
+                                 const double *sin_tx, const double *cos_tx, int n_tx,
+                                 const double *sin_rx, const double *cos_rx, int n_rx, double c,
+                                 double *ltx, double *ltz, double *lrx, double *lrz, void *stream) {
+    if (nx < 1 || nz < 1 || n_tx < 1 || n_rx < 1 || !(c > 0)) {
+        set_error("build_kk_luts: bad sizes");
+        return KKB_ERR_ARG;
+    }
+    return build_kk_luts(x0, dx, nx, z0, dz, nz, sin_tx, cos_tx, n_tx, sin_rx, cos_rx, n_rx, c, ltx,
+                         ltz, lrx, lrz, as_stream(stream));
+}
+
+// =====================================================================
+// K5 (stateless): transposes the z tables, sizes the window, gathers
+static int check_kk_args(int n_tx, int n_rx, int n_t, int nx, int nz, int out_kind) {
+    if (n_tx < 1 || n_rx < 1 || n_t < 2 || nx < 1 || nz < 1) {
+        set_error("kk: bad sizes N=%d M=%d T=%d X=%d Z=%d", n_tx, n_rx, n_t, nx, nz);
+        return KKB_ERR_ARG;
+    }
+    if (out_kind != KKB_OUT_C64 && out_kind != KKB_OUT_C128) {
+        set_error("kk: unknown out_kind %d", out_kind);
+        return KKB_ERR_ARG;
+    }
+    return KKB_OK;
+}
+
+struct kkb_kk_plan {
+    int N, M, T, nx, nz, linear, W;
+    double fs, shift;
+    double *ltx, *ltzT, *lrx, *lrzT, *w;  // one allocation
+};
+
+extern "C" int kkb_kk_plan_create(const double *ltx, const double *ltz, const double *lrx,
+                                  const double *lrz, int n_tx, int n_rx, int n_t, int nx, int nz,
+                                  const double *weights, double fs, double shift, int linear,
+                                  void *stream, kkb_kk_plan **out) {
+    int st = check_kk_args(n_tx, n_rx, n_t, nx, nz, KKB_OUT_C64);
+    if (st) return st;
+    cudaStream_t s = as_stream(stream);
+    kkb_kk_plan *p = new (std::nothrow) kkb_kk_plan();
+    if (!p) return KKB_ERR_NOMEM;
+    p->N = n_tx;
+    p->M = n_rx;
+    p->T = n_t;
+    p->nx = nx;
+    p->nz = nz;
+    p->linear = linear;
+    p->fs = fs;
+    p->shift = shift;
+    size_t n_ltx = (size_t)nx * n_tx, n_ltz = (size_t)nz * n_tx, n_lrx = (size_t)nx * n_rx,
+           n_lrz = (size_t)nz * n_rx;
+    double *buf = nullptr;
+    cudaError_t e = cudaMalloc(&buf, sizeof(double) * (n_ltx + n_ltz + n_lrx + n_lrz + n_rx));
+    if (e != cudaSuccess) {
+        delete p;
+        return cuda_status(e, "cudaMalloc(kk plan)");
+    }
+    p->ltx = buf;
+    p->ltzT = buf + n_ltx;
+    p->lrx = p->ltzT + n_ltz;
+    p->lrzT = p->lrx + n_lrx;
+    p->w = weights ? p->lrzT + n_lrz : nullptr;
+    auto fail = [&](int code) {
+        cudaFree(buf);
+        delete p;
+        return code;
+    };
+    if ((e = cudaMemcpyAsync(p->ltx, ltx, sizeof(double) * n_ltx, cudaMemcpyDeviceToDevice, s)))
+        return fail(cuda_status(e, "copy ltx"));
+    if ((e = cudaMemcpyAsync(p->lrx, lrx, sizeof(double) * n_lrx, cudaMemcpyDeviceToDevice, s)))
+        return fail(cuda_status(e, "copy lrx"));
+    if (weights &&
+        (e = cudaMemcpyAsync(p->w, weights, sizeof(double) * n_rx, cudaMemcpyDeviceToDevice, s)))
+        return fail(cuda_status(e, "copy weights"));
+    if ((st = transpose_f64(ltz, nz, n_tx, p->ltzT, s))) return fail(st);
+    if ((st = transpose_f64(lrz, nz, n_rx, p->lrzT, s))) return fail(st);
+    if ((st = kk_window(ltx, ltz, lrx, lrz, n_tx, n_rx, nx, nz, fs, shift, &p->W, s))) return fail(st);
+    *out = p;
+    return KKB_OK;
+}
+
+extern "C" int kkb_kk_plan_window(const kkb_kk_plan *p) { return p ? p->W : -1; }
+
+extern "C" int kkb_kk_plan_run(kkb_kk_plan *p, const void *data, int n_frames,
+                               long long data_frame_stride, void *out, int out_kind,
+                               long long out_frame_stride, float *intensity,
+                               unsigned int *frame_max, void *stream) {
+    if (!p) return KKB_ERR_ARG;
+    int st = check_kk_args(p->N, p->M, p->T, p->nx, p->nz, out_kind);
+    if (st) return st;
+    if (frame_max)
+        KKB_TRY_CUDA(cudaMemsetAsync(frame_max, 0, sizeof(unsigned) * (size_t)n_frames, as_stream(stream)),
+                     "zero frame_max");
+    return kk_gather(reinterpret_cast<const float2 *>(data), p->N, p->M, p->T, p->ltx, p->ltzT,
+                     p->lrx, p->lrzT, p->nx, p->nz, p->w, p->fs, p->shift, p->linear, out,
+                     out_kind, n_frames, data_frame_stride, out_frame_stride, intensity, frame_max,
+                     p->W, as_stream(stream));
+}
+
+extern "C" int kkb_kk_plan_destroy(kkb_kk_plan *p) {
+    if (!p) return KKB_OK;
+    cudaFree(p->ltx);
+    delete p;
+    return KKB_OK;
+}
+
+extern "C" int kkb_kk(const void *data, int n_tx, int n_rx, int n_t, const double *ltx,
+                      const double *ltz, const double *lrx, const double *lrz, int nx, int nz,
+                      const double *weights, double fs, double shift, int linear, void *out,
+                      int out_kind, int n_frames, long long data_frame_stride,
+                      long long out_frame_stride, float *intensity, unsigned int *frame_max,
+                      void *stream) {
+    int st = check_kk_args(n_tx, n_rx, n_t, nx, nz, out_kind);
+    if (st) return st;
+    kkb_kk_plan *p = nullptr;
+    st = kkb_kk_plan_create(ltx, ltz, lrx, lrz, n_tx, n_rx, n_t, nx, nz, weights, fs, shift, linear,
+                            stream, &p);
+    if (st) return st;
+    st = kkb_kk_plan_run(p, data, n_frames, data_frame_stride, out, out_kind, out_frame_stride,
+                         intensity, frame_max, stream);
+    cudaStreamSynchronize(as_stream(stream));
+    kkb_kk_plan_destroy(p);
+    return st;
+}
+
+extern "C" int kkb_kk_taps(const double *ltx, const double *ltz, const double *lrx,
+                           const double *lrz, int n_tx, int n_rx, int n_t, int nx, int nz,
+                           double fs, double shift, int linear, int *idx, void *stream) {
+    int st = check_kk_args(n_tx, n_rx, n_t, nx, nz, KKB_OUT_C64);
+    if (st) return st;
+    return kk_taps(ltx, ltz, lrx, lrz, n_tx, n_rx, n_t, nx, nz, fs, shift, linear, idx,
+                   as_stream(stream));
+}
+
+// =====================================================================
+// K7
+extern "C" int kkb_das(const void *data, int n_tx, int n_el, int n_t, const double *ltx,
+                       const double *ltz, const double *hyp, int n_hyp_rows, const long long *base,
+                       const double *frac, const double *xcoord, const double *zcoord,
+                       const double *upos, double tan_max, const double *weights, double fs,
+                       double shift, int linear, int nx, int nz, void *out, int out_kind,
+                       void *stream) {
+    if (n_tx < 1 || n_el < 1 || n_t < 2 || nx < 1 || nz < 1 || n_hyp_rows < nx) {
+        set_error("das: bad sizes");
+        return KKB_ERR_ARG;
+    }
+    if (out_kind != KKB_OUT_C64 && out_kind != KKB_OUT_C128) {
+        set_error("das: unknown out_kind %d", out_kind);
+        return KKB_ERR_ARG;
+    }
+    return das_gather(reinterpret_cast<const float2 *>(data), n_tx, n_el, n_t, ltx, ltz, hyp,
+                      n_hyp_rows, base, frac, xcoord, zcoord, upos, tan_max, weights, fs, shift,
+                      linear, nx, nz, out, out_kind, as_stream(stream));
+}
+
+// =====================================================================
+// K1/K3: analytic_signal
+extern "C" int kkb_analytic_signal(const float *rf, long long n_traces, int n_t, void *out,
+                                   void *stream) {
+    if (n_traces < 0 || n_t < 1 || n_t > KKB_FFT_MAX_T) {
+        set_error("analytic_signal: unsupported T=%d", n_t);
+        return n_t > KKB_FFT_MAX_T ? KKB_ERR_UNSUPPORTED : KKB_ERR_ARG;
+    }
+    if (n_traces == 0) return KKB_OK;
+    cudaStream_t s = as_stream(stream);
+    const int T = n_t, K = T / 2 + 1;
+    std::vector<float> sc(K);
+    for (int k = 0; k < K; ++k) sc[k] = (float)(one_sided(k, T) / T);
+    FftPlan plan;
+    int st = get_fft_plan(T, &plan);
+    if (st) return st;
+    Scratch spec(s), scale(s), promo(s);
+    if ((st = spec.alloc(sizeof(float2) * (size_t)n_traces * K))) return st;
+    if ((st = scale.alloc(sizeof(float) * K))) return st;
+    KKB_TRY_CUDA(cudaMemcpyAsync(scale.p, sc.data(), sizeof(float) * K, cudaMemcpyHostToDevice, s),
+                 "copy weights");
+    float2 *X = (float2 *)spec.p;
+    if (plan.direct) {
+        if ((st = promo.alloc(sizeof(float2) * (size_t)n_traces * T))) return st;
+        if ((st = fft_r2c(rf, n_traces, T, X, K, K, nullptr, s, (float2 *)promo.p))) return st;
+        long long total = n_traces * K;
+        k_scale_bins<<<(unsigned)std::min<long long>(ceil_div(total, 256), 4096), 256, 0, s>>>(
+            X, n_traces, K, K, (const float *)scale.p);
+        KKB_CHECK_LAUNCH("k_scale_bins");
+    } else {
+        if ((st = fft_r2c(rf, n_traces, T, X, K, K, (const float *)scale.p, s, nullptr))) return st;
+    }
+    st = fft_c2c(X, K, K, (float2 *)out, T, T, n_traces, T, true, 1.0f, s);
+    cudaStreamSynchronize(s);  // host weights vector dies here
+    return st;
+}
+
+// =====================================================================
+// K1-K3: shear_and_sum on complex input, all T bins
+extern "C" int kkb_shear_and_sum(const void *data, int n_tx, int n_el, int n_t,
+                                 const double *positions_host, const double *angles_host, int n_rx,
+                                 double fs, double c, void *out, void *stream) {
+    if (n_tx < 1 || n_el < 1 || n_rx < 1 || n_t < 1 || n_t > KKB_FFT_MAX_T || !(c > 0)) {
+        set_error("shear_and_sum: bad sizes");
+        return KKB_ERR_ARG;
+    }
+    cudaStream_t s = as_stream(stream);
+    const int T = n_t;
+    const long long ntr = (long long)n_tx * n_el;
+    std::vector<double> tau((size_t)n_el * n_rx), freq(T), scale(T, 1.0 / T);
+    for (int m = 0; m < n_rx; ++m) {
+        double q = sin(angles_host[m]) / c;  // compress.py:79  positions * (sin(theta) / c)
+        for (int l = 0; l < n_el; ++l) tau[(size_t)l * n_rx + m] = positions_host[l] * q;
+    }
+    for (int k = 0; k < T; ++k) freq[k] = fftfreq(k, T, fs);
+    Scratch xs(s), ys(s), rs(s);
+    int st;
+    if ((st = xs.alloc(sizeof(float2) * (size_t)ntr * T))) return st;
+    if ((st = ys.alloc(sizeof(float2) * (size_t)n_tx * n_rx * T))) return st;
+    if ((st = rs.alloc(sizeof(float2) * (size_t)n_rx * n_el * T))) return st;
+    if ((st = build_ramps(tau.data(), n_el, n_rx, freq.data(), scale.data(), T, (float2 *)rs.p, s)))
+        return st;
+    float2 *X = (float2 *)xs.p, *Y = (float2 *)ys.p;
+    if ((st = fft_c2c((const float2 *)data, T, T, X, T, T, ntr, T, false, 1.0f, s))) return st;
+    if ((st = contract(X, T, (const float2 *)rs.p, T, Y, T, n_tx, n_el, n_rx, T, s))) return st;
+    st = fft_c2c(Y, T, T, (float2 *)out, T, T, (long long)n_tx * n_rx, T, true, 1.0f, s);
+    return st;
+}
+
+// =====================================================================
+// fused stage-1 plan
+struct kkb_decomposer {
+    int N, L, T, M, K, chunk;
+    float2 *ramps = nullptr;
+    float2 *X = nullptr;
+    float2 *Y = nullptr;
+    long long bytes = 0;
+};
+
+extern "C" int kkb_decomposer_create(int n_tx, int n_el, int n_t, const double *positions_host,
+                                     const double *angles_host, int n_rx, double fs, double c,
+                                     int max_frames, kkb_decomposer **out) {
+    if (n_tx < 1 || n_el < 1 || n_rx < 1 || n_t < 2 || n_t > KKB_FFT_MAX_T || max_frames < 1 ||
+        !(c > 0)) {
+        set_error("decomposer: bad sizes");
+        return KKB_ERR_ARG;
+    }
+    FftPlan plan;
+    int st = get_fft_plan(n_t, &plan);
+    if (st) return st;
+    if (plan.direct) {
+        set_error("decomposer: T=%d has a prime factor > 31 (use kkb_shear_and_sum)", n_t);
+        return KKB_ERR_UNSUPPORTED;
+    }
+    kkb_decomposer *p = new (std::nothrow) kkb_decomposer();
+    if (!p) return KKB_ERR_NOMEM;
+    p->N = n_tx;
+    p->L = n_el;
+    p->T = n_t;
+    p->M = n_rx;
+    p->K = n_t / 2 + 1;
+    p->chunk = max_frames;
+    const int K = p->K;
+    std::vector<double> tau((size_t)n_el * n_rx), freq(K), scale(K);
+    for (int m = 0; m < n_rx; ++m) {
+        double q = sin(angles_host[m]) / c;
+        for (int l = 0; l < n_el; ++l) tau[(size_t)l * n_rx + m] = positions_host[l] * q;
+    }
+    for (int k = 0; k < K; ++k) {
+        freq[k] = fftfreq(k, n_t, fs);
+        scale[k] = one_sided(k, n_t) / n_t;
+    }
+    size_t rb = sizeof(float2) * (size_t)n_rx * n_el * K;
+    size_t xb = sizeof(float2) * (size_t)max_frames * n_tx * n_el * K;
+    size_t yb = sizeof(float2) * (size_t)max_frames * n_tx * n_rx * K;
+    cudaError_t e;
+    if ((e = cudaMalloc(&p->ramps, rb)) || (e = cudaMalloc(&p->X, xb)) || (e = cudaMalloc(&p->Y, yb))) {
+        cudaFree(p->ramps);
+        cudaFree(p->X);
+        cudaFree(p->Y);
+        delete p;
+        return cuda_status(e, "cudaMalloc(decomposer)");
+    }
+    p->bytes = (long long)(rb + xb + yb);
+    st = build_ramps(tau.data(), n_el, n_rx, freq.data(), scale.data(), K, p->ramps, 0);
+    if (st) {
+        cudaFree(p->ramps);
+        cudaFree(p->X);
+        cudaFree(p->Y);
+        delete p;
+        return st;
+    }
+    *out = p;
+    return KKB_OK;
+}
+
+extern "C" long long kkb_decomposer_workspace_bytes(const kkb_decomposer *p) { return p ? p->bytes : 0; }
+
+extern "C" int kkb_decomposer_run(kkb_decomposer *p, const float *rf, int n_frames, void *traces,
+                                  void *stream) {
+    if (!p || n_frames < 0) return KKB_ERR_ARG;
+    cudaStream_t s = as_stream(stream);
+    const int N = p->N, L = p->L, T = p->T, M = p->M, K = p->K;
+    for (int f0 = 0; f0 < n_frames; f0 += p->chunk) {
+        int F = std::min(p->chunk, n_frames - f0);
+        const float *rf_c = rf + (size_t)f0 * N * L * T;
+        float2 *tr_c = (float2 *)traces + (size_t)f0 * N * M * T;
+        int st;
+        if ((st = fft_r2c(rf_c, (long long)F * N * L, T, p->X, K, K, nullptr, s, nullptr))) return st;
+        if ((st = contract(p->X, K, p->ramps, K, p->Y, K, (long long)F * N, L, M, K, s))) return st;
+        if ((st = fft_c2c(p->Y, K, K, tr_c, T, T, (long long)F * N * M, T, true, 1.0f, s))) return st;
+    }
+    return KKB_OK;
+}
+
+extern "C" int kkb_decomposer_destroy(kkb_decomposer *p) {
+    if (!p) return KKB_OK;
+    cudaFree(p->ramps);
+    cudaFree(p->X);
+    cudaFree(p->Y);
+    delete p;
+    return KKB_OK;
+}
+
+// =====================================================================
+// K6
+extern "C" int kkb_log_compress(const float *intensity, const unsigned int *frame_max, int n_frames,
+                                long long pixels_per_frame, float floor_db, float *db, void *stream) {
+    return log_compress(intensity, frame_max, n_frames, pixels_per_frame, floor_db, db,
+                        as_stream(stream));
+}
+
+extern "C" int kkb_compound(const void *images, int n_images, long long n_pixels, int mode,
+                            double *out, void *stream) {
+    if (n_images < 1 || (mode != 0 && mode != 1)) {
+        set_error("compound: need >= 1 image and mode 0/1");
+        return KKB_ERR_ARG;
+    }
+    return compound(images, n_images, n_pixels, mode, out, as_stream(stream));
+}

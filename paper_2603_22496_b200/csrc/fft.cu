@@ -1,0 +1,427 @@
+// K1 / K3: batched length-T FFTs along time, in shared memory (sm_100a).
+//
+// Replaces the numpy/scipy pocketfft calls of the reference hot path
+// (spectral.py:90,92; compress.py:75,81; bench.py:128,138): full-length DFTs,
+// no padding — the circular-shear wrap position depends on T exactly
+// (compress.py:21-26, spectral.py:8-10).
+//
+// Algorithm: Stockham autosort, mixed radix (8, 4, 2, 3, 5, direct odd
+// radices <= 31), ping-pong between two shared-memory buffers, one or more
+// traces per CTA.  Stage s with radix R and sub-transform length Ns:
+//   j in [0, T/R):  k = j mod Ns
+//   v[r] = a[j + r T/R] * W_T^{r k T/(Ns R)}        (r = 0..R-1)
+//   b[(j/Ns) Ns R + k + r Ns] = DFT_R(v)[r]
+// Twiddles W_T^i = exp(-2 pi i/T) are computed in float64 on the host and
+// rounded once to float32, so the float32 transform error stays ~eps*log T.
+// Inverse transforms run the forward stages on conj(x) and conjugate again.
+// Lengths whose largest prime factor exceeds 31 use a direct O(T^2) DFT
+// kernel (still on the GPU; correctness path for odd sizes only).
+
+#include <map>
+#include <mutex>
+#include <vector>
+#include <cmath>
+
+#include "common.cuh"
+#include "fft.cuh"
+
+namespace kkb {
+
+namespace {
+
+std::mutex g_fft_mu;
+std::map<int, FftPlan> g_fft_plans;  // per device 0 only; libkkb is one-device-per-process
+
+}  // namespace
+
+int get_fft_plan(int T, FftPlan *out) {
+    std::lock_guard<std::mutex> lock(g_fft_mu);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int key = T * 64 + dev;
+    auto it = g_fft_plans.find(key);
+    if (it != g_fft_plans.end()) {
+        *out = it->second;
+        return KKB_OK;
+    }
+    if (T < 1 || T > KKB_FFT_MAX_T) {
+        set_error("FFT length %d outside [1, %d]", T, KKB_FFT_MAX_T);
+        return KKB_ERR_UNSUPPORTED;
+    }
+    FftPlan p{};
+    p.T = T;
+    int t = T;
+    const int order[] = {8, 4, 2, 3, 5, 7, 11, 13, 17, 19, 23, 29, 31};
+    for (int r : order) {
+        while (t % r == 0) {
+            if (p.nstages >= KKB_FFT_MAX_STAGES) break;
+            p.radix[p.nstages++] = r;
+            t /= r;
+        }
+    }
+    p.direct = (t != 1) ? 1 : 0;
+    if (p.direct) p.nstages = 0;
+    std::vector<float2> tw(T);
+    for (int k = 0; k < T; ++k) {
+        // exp(-2 pi i k / T) in double, reduced exactly by symmetry
+        double a = -2.0 * M_PI * (double)k / (double)T;
+        tw[k] = make_float2((float)cos(a), (float)sin(a));
+    }
+    KKB_TRY_CUDA(cudaMalloc(&p.tw, sizeof(float2) * T), "cudaMalloc(twiddles)");
+    KKB_TRY_CUDA(cudaMemcpy(p.tw, tw.data(), sizeof(float2) * T, cudaMemcpyHostToDevice),
+                 "cudaMemcpy(twiddles)");
+    g_fft_plans[key] = p;
+    *out = p;
+    return KKB_OK;
+}
+
+// ------------------------------------------------------------- small DFTs
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+    return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__device__ __forceinline__ float2 mul_mi(float2 a) { return make_float2(a.y, -a.x); }  // * (-i)
+
+__device__ __forceinline__ void dft2(float2 &a, float2 &b) {
+    float2 t = a;
+    a = cadd(t, b);
+    b = csub(t, b);
+}
+
+__device__ __forceinline__ void dft4(float2 *v) {
+    float2 a0 = cadd(v[0], v[2]), a1 = csub(v[0], v[2]);
+    float2 a2 = cadd(v[1], v[3]), a3 = mul_mi(csub(v[1], v[3]));
+    v[0] = cadd(a0, a2);
+    v[2] = csub(a0, a2);
+    v[1] = cadd(a1, a3);
+    v[3] = csub(a1, a3);
+}
+
+__device__ __forceinline__ void dft8(float2 *v) {
+    const float r = 0.70710678118654752440f;
+    float2 e[4] = {v[0], v[2], v[4], v[6]};
+    float2 o[4] = {v[1], v[3], v[5], v[7]};
+    dft4(e);
+    dft4(o);
+    // twiddle o[k] by W8^k
+    o[1] = make_float2(r * (o[1].x + o[1].y), r * (o[1].y - o[1].x));
+    o[2] = mul_mi(o[2]);
+    o[3] = make_float2(r * (o[3].y - o[3].x), -r * (o[3].x + o[3].y));
+    for (int k = 0; k < 4; ++k) {
+        v[k] = cadd(e[k], o[k]);
+        v[k + 4] = csub(e[k], o[k]);
+    }
+}
+
+__device__ __forceinline__ void dft3(float2 *v) {
+    const float s = 0.86602540378443864676f;  // sin(2pi/3)
+    float2 t1 = cadd(v[1], v[2]);
+    float2 t2 = make_float2(v[0].x - 0.5f * t1.x, v[0].y - 0.5f * t1.y);
+    float2 t3 = csub(v[1], v[2]);
+    // -i*s*t3
+    float2 t4 = make_float2(s * t3.y, -s * t3.x);
+    v[0] = cadd(v[0], t1);
+    v[1] = cadd(t2, t4);
+    v[2] = csub(t2, t4);
+}
+
+__device__ __forceinline__ void dft5(float2 *v) {
+    const float c1 = 0.30901699437494742410f;   // cos(2pi/5)
+    const float c2 = -0.80901699437494742410f;  // cos(4pi/5)
+    const float s1 = 0.95105651629515357212f;   // sin(2pi/5)
+    const float s2 = 0.58778525229247312917f;   // sin(4pi/5)
+    float2 a1 = cadd(v[1], v[4]), b1 = csub(v[1], v[4]);
+    float2 a2 = cadd(v[2], v[3]), b2 = csub(v[2], v[3]);
+    float2 x0 = v[0];
+    float2 p1 = make_float2(x0.x + c1 * a1.x + c2 * a2.x, x0.y + c1 * a1.y + c2 * a2.y);
+    float2 p2 = make_float2(x0.x + c2 * a1.x + c1 * a2.x, x0.y + c2 * a1.y + c1 * a2.y);
+    // q = -i (s1 b1 + s2 b2),  r = -i (s2 b1 - s1 b2)
+    float2 q1 = make_float2(s1 * b1.x + s2 * b2.x, s1 * b1.y + s2 * b2.y);
+    float2 q2 = make_float2(s2 * b1.x - s1 * b2.x, s2 * b1.y - s1 * b2.y);
+    q1 = mul_mi(q1);
+    q2 = mul_mi(q2);
+    v[0] = make_float2(x0.x + a1.x + a2.x, x0.y + a1.y + a2.y);
+    v[1] = cadd(p1, q1);
+    v[4] = csub(p1, q1);
+    v[2] = cadd(p2, q2);
+    v[3] = csub(p2, q2);
+}
+
+// generic odd radix (<= 31) by direct summation with table twiddles
+__device__ __noinline__ void dft_generic(float2 *v, int R, const float2 *__restrict__ tw, int T) {
+    float2 out[KKB_FFT_MAX_RADIX];
+    int step = T / R;
+    for (int p = 0; p < R; ++p) {
+        float2 acc = make_float2(0.f, 0.f);
+        for (int q = 0; q < R; ++q) {
+            float2 w = tw[(size_t)step * ((p * q) % R)];
+            acc = cadd(acc, cmul(v[q], w));
+        }
+        out[p] = acc;
+    }
+    for (int p = 0; p < R; ++p) v[p] = out[p];
+}
+
+// Run every Stockham stage on G traces laid out back to back (stride T) in
+// buffer `a`; `b` is scratch of the same size.  Returns the buffer holding
+// the result.  Must be called by all threads of the CTA.
+__device__ float2 *stockham(float2 *a, float2 *b, int G, const FftPlan &p) {
+    const int T = p.T;
+    const float2 *__restrict__ tw = p.tw;
+    int Ns = 1;
+    for (int s = 0; s < p.nstages; ++s) {
+        const int R = p.radix[s];
+        const int TR = T / R;
+        const int tws = T / (Ns * R);
+        for (int idx = threadIdx.x; idx < G * TR; idx += blockDim.x) {
+            const int g = idx / TR;
+            const int j = idx - g * TR;
+            const int k = j % Ns;
+            const float2 *src = a + g * T;
+            float2 *dst = b + g * T;
+            if (R == 8) {
+                float2 v[8];
+#pragma unroll
+                for (int r = 0; r < 8; ++r) v[r] = src[j + r * TR];
+                if (Ns > 1) {
+#pragma unroll
+                    for (int r = 1; r < 8; ++r) v[r] = cmul(v[r], __ldg(tw + r * k * tws));
+                }
+                dft8(v);
+                const int base = (j - k) * 8 + k;
+#pragma unroll
+                for (int r = 0; r < 8; ++r) dst[base + r * Ns] = v[r];
+            } else if (R == 4) {
+                float2 v[4];
+#pragma unroll
+                for (int r = 0; r < 4; ++r) v[r] = src[j + r * TR];
+                if (Ns > 1) {
+#pragma unroll
+                    for (int r = 1; r < 4; ++r) v[r] = cmul(v[r], __ldg(tw + r * k * tws));
+                }
+                dft4(v);
+                const int base = (j - k) * 4 + k;
+#pragma unroll
+                for (int r = 0; r < 4; ++r) dst[base + r * Ns] = v[r];
+            } else if (R == 2) {
+                float2 v[2];
+                v[0] = src[j];
+                v[1] = src[j + TR];
+                if (Ns > 1) v[1] = cmul(v[1], __ldg(tw + k * tws));
+                dft2(v[0], v[1]);
+                const int base = (j - k) * 2 + k;
+                dst[base] = v[0];
+                dst[base + Ns] = v[1];
+            } else if (R == 3) {
+                float2 v[3];
+#pragma unroll
+                for (int r = 0; r < 3; ++r) v[r] = src[j + r * TR];
+                if (Ns > 1) {
+#pragma unroll
+                    for (int r = 1; r < 3; ++r) v[r] = cmul(v[r], __ldg(tw + r * k * tws));
+                }
+                dft3(v);
+                const int base = (j - k) * 3 + k;
+#pragma unroll
+                for (int r = 0; r < 3; ++r) dst[base + r * Ns] = v[r];
+            } else if (R == 5) {
+                float2 v[5];
+#pragma unroll
+                for (int r = 0; r < 5; ++r) v[r] = src[j + r * TR];
+                if (Ns > 1) {
+#pragma unroll
+                    for (int r = 1; r < 5; ++r) v[r] = cmul(v[r], __ldg(tw + r * k * tws));
+                }
+                dft5(v);
+                const int base = (j - k) * 5 + k;
+#pragma unroll
+                for (int r = 0; r < 5; ++r) dst[base + r * Ns] = v[r];
+            } else {
+                float2 v[KKB_FFT_MAX_RADIX];
+                for (int r = 0; r < R; ++r) v[r] = src[j + r * TR];
+                if (Ns > 1)
+                    for (int r = 1; r < R; ++r) v[r] = cmul(v[r], __ldg(tw + r * k * tws));
+                dft_generic(v, R, tw, T);
+                const int base = (j - k) * R + k;
+                for (int r = 0; r < R; ++r) dst[base + r * Ns] = v[r];
+            }
+        }
+        __syncthreads();
+        float2 *t = a;
+        a = b;
+        b = t;
+        Ns *= R;
+    }
+    return a;
+}
+
+// ------------------------------------------------------------- kernels
+// Complex-to-complex FFT of `ntraces` rows.  Input row i: in + i*in_stride,
+// first in_len bins read, the rest treated as zero (one-sided spectra).
+// Output row i: out + i*out_stride, first out_len bins written, times scale.
+__global__ void __launch_bounds__(KKB_FFT_THREADS)
+k_fft_c2c(const float2 *__restrict__ in, long long in_stride, int in_len,
+          float2 *__restrict__ out, long long out_stride, int out_len,
+          long long ntraces, int G, int inverse, float scale, FftPlan p) {
+    extern __shared__ float2 smem[];
+    const int T = p.T;
+    float2 *a = smem;
+    float2 *b = smem + G * T;
+    const long long t0 = (long long)blockIdx.x * G;
+    for (int idx = threadIdx.x; idx < G * T; idx += blockDim.x) {
+        int g = idx / T;
+        int t = idx - g * T;
+        long long tr = t0 + g;
+        float2 v = make_float2(0.f, 0.f);
+        if (tr < ntraces && t < in_len) v = in[tr * in_stride + t];
+        if (inverse) v.y = -v.y;
+        a[idx] = v;
+    }
+    __syncthreads();
+    float2 *res = stockham(a, b, G, p);
+    for (int idx = threadIdx.x; idx < G * out_len; idx += blockDim.x) {
+        int g = idx / out_len;
+        int t = idx - g * out_len;
+        long long tr = t0 + g;
+        if (tr >= ntraces) continue;
+        float2 v = res[g * T + t];
+        if (inverse) v.y = -v.y;
+        out[tr * out_stride + t] = make_float2(v.x * scale, v.y * scale);
+    }
+}
+
+// Real-input FFT of `ntraces` float rows (stride T), two rows packed as one
+// complex row per transform.  Writes bins [0, K) of each row's spectrum to
+// out + row*out_stride, each multiplied by bin_scale[k] (NULL = 1).
+__global__ void __launch_bounds__(KKB_FFT_THREADS)
+k_fft_r2c_pairs(const float *__restrict__ in, long long ntraces, float2 *__restrict__ out,
+                long long out_stride, int K, const float *__restrict__ bin_scale, int G,
+                FftPlan p) {
+    extern __shared__ float2 smem[];
+    const int T = p.T;
+    float2 *a = smem;
+    float2 *b = smem + G * T;
+    const long long pair0 = (long long)blockIdx.x * G;
+    for (int idx = threadIdx.x; idx < G * T; idx += blockDim.x) {
+        int g = idx / T;
+        int t = idx - g * T;
+        long long r0 = 2 * (pair0 + g);
+        float re = (r0 < ntraces) ? in[r0 * T + t] : 0.f;
+        float im = (r0 + 1 < ntraces) ? in[(r0 + 1) * T + t] : 0.f;
+        a[idx] = make_float2(re, im);
+    }
+    __syncthreads();
+    float2 *res = stockham(a, b, G, p);
+    for (int idx = threadIdx.x; idx < G * K; idx += blockDim.x) {
+        int g = idx / K;
+        int k = idx - g * K;
+        long long r0 = 2 * (pair0 + g);
+        if (r0 >= ntraces) continue;
+        float2 zk = res[g * T + k];
+        float2 zn = res[g * T + (k == 0 ? 0 : T - k)];
+        float s = bin_scale ? bin_scale[k] : 1.0f;
+        // X0 = (Z_k + conj(Z_-k)) / 2 ; X1 = (Z_k - conj(Z_-k)) / (2i)
+        float2 x0 = make_float2(0.5f * (zk.x + zn.x), 0.5f * (zk.y - zn.y));
+        float dx = zk.x - zn.x, dy = zk.y + zn.y;
+        float2 x1 = make_float2(0.5f * dy, -0.5f * dx);
+        out[r0 * out_stride + k] = make_float2(x0.x * s, x0.y * s);
+        if (r0 + 1 < ntraces) out[(r0 + 1) * out_stride + k] = make_float2(x1.x * s, x1.y * s);
+    }
+}
+
+// Direct DFT fallback for lengths with a prime factor > 31.
+__global__ void k_dft_direct(const float2 *__restrict__ in, long long in_stride, int in_len,
+                             float2 *__restrict__ out, long long out_stride, int out_len,
+                             long long ntraces, int inverse, float scale, FftPlan p) {
+    const int T = p.T;
+    long long tr = blockIdx.y;
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < out_len; k += gridDim.x * blockDim.x) {
+        double ar = 0.0, ai = 0.0;
+        for (int t = 0; t < in_len; ++t) {
+            float2 v = in[tr * in_stride + t];
+            float2 w = p.tw[(long long)k * t % T];
+            if (inverse) w.y = -w.y;
+            ar += (double)v.x * w.x - (double)v.y * w.y;
+            ai += (double)v.x * w.y + (double)v.y * w.x;
+        }
+        out[tr * out_stride + k] = make_float2((float)ar * scale, (float)ai * scale);
+    }
+}
+
+__global__ void k_real_to_complex(const float *__restrict__ in, long long n, float2 *__restrict__ out) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x)
+        out[i] = make_float2(in[i], 0.f);
+}
+
+// ------------------------------------------------------------- host launchers
+static int traces_per_cta(int T) {
+    int G = KKB_FFT_TARGET_ELEMS / T;
+    return G < 1 ? 1 : G;
+}
+
+static int smem_bytes(int T, int G) { return 2 * G * T * (int)sizeof(float2); }
+
+static int ensure_smem(const void *fn, int bytes) {
+    if (bytes > 48 * 1024) {
+        KKB_TRY_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes),
+                     "cudaFuncSetAttribute(fft smem)");
+    }
+    return KKB_OK;
+}
+
+int fft_c2c(const float2 *in, long long in_stride, int in_len, float2 *out, long long out_stride,
+            int out_len, long long ntraces, int T, bool inverse, float scale, cudaStream_t s) {
+    if (ntraces <= 0) return KKB_OK;
+    FftPlan p;
+    int st = get_fft_plan(T, &p);
+    if (st) return st;
+    if (p.direct) {
+        dim3 grid((unsigned)ceil_div(out_len, 256), (unsigned)ntraces);
+        k_dft_direct<<<grid, 256, 0, s>>>(in, in_stride, in_len, out, out_stride, out_len, ntraces,
+                                          inverse ? 1 : 0, scale, p);
+        KKB_CHECK_LAUNCH("k_dft_direct");
+        return KKB_OK;
+    }
+    int G = traces_per_cta(T);
+    int sm = smem_bytes(T, G);
+    st = ensure_smem((const void *)k_fft_c2c, sm);
+    if (st) return st;
+    k_fft_c2c<<<(unsigned)ceil_div(ntraces, G), KKB_FFT_THREADS, sm, s>>>(
+        in, in_stride, in_len, out, out_stride, out_len, ntraces, G, inverse ? 1 : 0, scale, p);
+    KKB_CHECK_LAUNCH("k_fft_c2c");
+    return KKB_OK;
+}
+
+int fft_r2c(const float *in, long long ntraces, int T, float2 *out, long long out_stride, int K,
+            const float *bin_scale, cudaStream_t s, float2 *scratch_c2c) {
+    if (ntraces <= 0) return KKB_OK;
+    FftPlan p;
+    int st = get_fft_plan(T, &p);
+    if (st) return st;
+    if (p.direct) {
+        // promote to complex (scratch holds ntraces*T) then direct DFT; scaling
+        // by bin_scale is not supported here (callers fold it elsewhere)
+        if (!scratch_c2c || bin_scale) {
+            set_error("direct-DFT r2c path needs scratch and no bin scale");
+            return KKB_ERR_UNSUPPORTED;
+        }
+        long long n = ntraces * (long long)T;
+        k_real_to_complex<<<(unsigned)std::min<long long>(ceil_div(n, 256), 65535), 256, 0, s>>>(
+            in, n, scratch_c2c);
+        KKB_CHECK_LAUNCH("k_real_to_complex");
+        return fft_c2c(scratch_c2c, T, T, out, out_stride, K, ntraces, T, false, 1.0f, s);
+    }
+    int G = traces_per_cta(T);
+    int sm = smem_bytes(T, G);
+    st = ensure_smem((const void *)k_fft_r2c_pairs, sm);
+    if (st) return st;
+    long long npairs = (ntraces + 1) / 2;
+    k_fft_r2c_pairs<<<(unsigned)ceil_div(npairs, G), KKB_FFT_THREADS, sm, s>>>(
+        in, ntraces, out, out_stride, K, bin_scale, G, p);
+    KKB_CHECK_LAUNCH("k_fft_r2c_pairs");
+    return KKB_OK;
+}
+
+}  // namespace kkb

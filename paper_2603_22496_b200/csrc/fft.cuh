@@ -1,0 +1,32 @@
+// FFT plan and launchers shared by the spectral / decomposition paths.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#define KKB_FFT_MAX_STAGES 16
+#define KKB_FFT_MAX_RADIX 32
+#define KKB_FFT_MAX_T 8192
+#define KKB_FFT_THREADS 256
+#define KKB_FFT_TARGET_ELEMS 4096  // traces per CTA = max(1, this / T)
+
+namespace kkb {
+
+struct FftPlan {
+    int T;
+    int nstages;
+    int direct;                      // 1: largest prime factor > 31 -> O(T^2) kernel
+    int radix[KKB_FFT_MAX_STAGES];
+    float2 *tw;                      // exp(-2 pi i k / T), k < T (device)
+};
+
+int get_fft_plan(int T, FftPlan *out);
+
+// Batched C2C (forward exp(-), inverse exp(+) unnormalised, times `scale`).
+int fft_c2c(const float2 *in, long long in_stride, int in_len, float2 *out, long long out_stride,
+            int out_len, long long ntraces, int T, bool inverse, float scale, cudaStream_t s);
+
+// Batched real-input FFT: bins [0, K) of each row, times bin_scale[k].
+int fft_r2c(const float *in, long long ntraces, int T, float2 *out, long long out_stride, int K,
+            const float *bin_scale, cudaStream_t s, float2 *scratch_c2c);
+
+}  // namespace kkb

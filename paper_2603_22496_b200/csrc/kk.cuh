@@ -1,0 +1,54 @@
+// Internal declarations of the gather / LUT / epilogue / decomposition kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+
+// kk gather tile: TZ = 32*WZ depth rows x TX = WX*PX lateral columns per CTA
+#define KKB_KK_WZ 4
+#define KKB_KK_WX 2
+#define KKB_KK_PX 4
+#define KKB_KK_TZ (32 * KKB_KK_WZ)
+#define KKB_KK_TX (KKB_KK_WX * KKB_KK_PX)
+
+namespace kkb {
+
+int take_device_error(int *out);
+
+int build_kk_luts(double x0, double dx, int nx, double z0, double dz, int nz, const double *sin_tx,
+                  const double *cos_tx, int n_tx, const double *sin_rx, const double *cos_rx,
+                  int n_rx, double c, double *ltx, double *ltz, double *lrx, double *lrz,
+                  cudaStream_t s);
+
+int transpose_f64(const double *in, int rows, int cols, double *out, cudaStream_t s);
+
+// Synchronises `s`: returns the shared-memory window length (samples) one
+// gather tile needs for these tables.
+int kk_window(const double *ltx, const double *ltz, const double *lrx, const double *lrz, int N,
+              int M, int nx, int nz, double fs, double shift, int *window_out, cudaStream_t s);
+
+int kk_gather(const float2 *data, int N, int M, int T, const double *ltx, const double *ltzT,
+              const double *lrx, const double *lrzT, int nx, int nz, const double *w, double fs,
+              double shift, int linear, void *out, int out_kind, int n_frames, long long data_fs,
+              long long out_fs, float *inten, unsigned *fmax, int W, cudaStream_t s);
+
+int kk_taps(const double *ltx, const double *ltz, const double *lrx, const double *lrz, int N, int M,
+            int T, int nx, int nz, double fs, double shift, int linear, int *idx, cudaStream_t s);
+
+int log_compress(const float *inten, const unsigned *fmax, int n_frames, long long P, float floor_db,
+                 float *db, cudaStream_t s);
+
+int compound(const void *images, int J, long long P, int mode, double *out, cudaStream_t s);
+
+int das_gather(const float2 *data, int n_tx, int n_el, int n_t, const double *ltx, const double *ltz,
+               const double *hyp, int n_hyp_rows, const long long *base, const double *frac,
+               const double *xcoord, const double *zcoord, const double *upos, double tan_max,
+               const double *weights, double fs, double shift, int linear, int nx, int nz,
+               void *out, int out_kind, cudaStream_t s);
+
+// decomposition (ramps + per-bin contraction)
+int build_ramps(const double *tau_host, int L, int M, const double *freq_host,
+                const double *scale_host, int Kb, float2 *ramps, cudaStream_t s);
+int contract(const float2 *X, long long ldx, const float2 *R, long long ldr, float2 *Y,
+             long long ldy, long long B, int L, int M, int Kb, cudaStream_t s);
+
+}  // namespace kkb

@@ -1,0 +1,203 @@
+"""Device-resident, batched KK pipeline (the throughput path).
+
+One ``KKEngine`` owns the plans for a fixed geometry — the decomposition
+ramps, the four delay tables and the gather window — plus the per-batch
+buffers, and runs the whole hot path for F frames with every array in HBM:
+
+    RF (F, N, L, T) float32
+      -> K1  real-pair FFT of every element trace            (spectral.py:90)
+      -> K2  per-bin contraction over elements x ramps        (compress.py:78-81)
+      -> K3  inverse FFT over the non-negative bins           (compress.py:81)
+         traces (F, N, M, T) complex64
+      -> K5  pixel gather over the N x M coarray pairs        (beamform.py:212-236)
+         IQ (F, X, Z) complex64 + fused |IQ|^2 + per-frame max
+      -> K6  10 log10(I / max I) display map (new; not in the reference)
+
+This is the reference's own staged data flow (bench.py:113-153 for stage 1,
+kk for stage 2) for a batch of frames; the reference times it per frame on
+the CPU.  ``run_host`` is the end-to-end form: pinned host RF in, IQ out,
+with host<->device copies overlapped with compute on two streams.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _device as dev
+from . import _lib
+from .beamform import build_kk_luts_device
+from .core import AcquisitionParams, ImageGrid, TransducerArray
+from .errors import ConfigError
+from .sampling import ReceiveAngleSet
+
+
+class KKEngine:
+    def __init__(self, array: TransducerArray, params: AcquisitionParams,
+                 receive: ReceiveAngleSet, grid: ImageGrid, frames: int, *,
+                 chunk_frames: int | None = None, interpolation: str = "linear",
+                 pulse_delay: float = 0.0, channel_weights=None, floor_db: float = -60.0,
+                 want_db: bool = True):
+        t = dev.require_cuda()
+        self.t = t
+        self.array, self.params, self.receive, self.grid = array, params, receive, grid
+        self.F = int(frames)
+        if self.F < 1:
+            raise ConfigError("frames must be >= 1")
+        self.N = params.num_transmits
+        self.L = array.num_elements
+        self.M = receive.num_angles
+        self.T = params.num_samples
+        self.fs = array.sampling_frequency
+        self.c = params.sound_speed
+        self.shift = (pulse_delay - params.start_time) * self.fs
+        self.linear = interpolation == "linear"
+        self.floor_db = float(floor_db)
+        self.want_db = want_db
+        self.chunk = int(chunk_frames or self.F)
+        lib = _lib.load()
+
+        self._dec = self._new_decomposer(self.chunk)
+        self._stream_decs = []  # one per stream of run_host (scratch is per plan)
+
+        self.luts = build_kk_luts_device(grid, params.transmit_angles, receive.angles, self.c)
+        w = None
+        if channel_weights is not None:
+            w = np.asarray(channel_weights, dtype=np.float64)
+            if w.shape != (self.M,):
+                raise ConfigError(f"channel_weights must have shape ({self.M},)")
+        self._w = dev.to_device(w) if w is not None else None
+        kp = ctypes.c_void_p()
+        _lib.call("kkb_kk_plan_create", dev.ptr(self.luts["lut_tx_x"]), dev.ptr(self.luts["lut_tx_z"]),
+                  dev.ptr(self.luts["lut_rx_x"]), dev.ptr(self.luts["lut_rx_z"]), self.N, self.M,
+                  self.T, grid.nx, grid.nz, dev.ptr(self._w), float(self.fs), float(self.shift),
+                  int(self.linear), dev.stream_handle(), ctypes.byref(kp))
+        self._kk = kp
+        self.window = int(lib.kkb_kk_plan_window(kp))
+
+        F, N, M, T, X, Z = self.F, self.N, self.M, self.T, grid.nx, grid.nz
+        self.traces = t.empty((F, N, M, T), dtype=t.complex64, device="cuda")
+        self.iq = t.empty((F, X, Z), dtype=t.complex64, device="cuda")
+        self.inten = t.empty((F, X, Z), dtype=t.float32, device="cuda")
+        self.fmax = t.zeros((F,), dtype=t.int32, device="cuda")
+        self.db = t.empty((F, X, Z), dtype=t.float32, device="cuda") if want_db else None
+        self._closed = False
+
+    def _new_decomposer(self, chunk: int):
+        pos = np.ascontiguousarray(self.array.positions, dtype=np.float64)
+        ang = np.ascontiguousarray(self.receive.angles, dtype=np.float64)
+        h = ctypes.c_void_p()
+        _lib.call("kkb_decomposer_create", self.N, self.L, self.T, pos.ctypes.data, ang.ctypes.data,
+                  self.M, float(self.fs), float(self.c), int(chunk), ctypes.byref(h))
+        return h
+
+    # ------------------------------------------------------------------ info
+    @property
+    def pixel_pairs_per_frame(self) -> int:
+        return self.grid.nx * self.grid.nz * self.N * self.M
+
+    def workspace_bytes(self) -> int:
+        lib = _lib.load()
+        own = sum(x.numel() * x.element_size() for x in
+                  (self.traces, self.iq, self.inten, self.fmax) + ((self.db,) if self.db is not None else ()))
+        return int(lib.kkb_decomposer_workspace_bytes(self._dec)) + own
+
+    # ------------------------------------------------------------------ device path
+    def decompose(self, rf, n_frames: int | None = None, stream=None):
+        F = self.F if n_frames is None else n_frames
+        _lib.call("kkb_decomposer_run", self._dec, dev.ptr(rf), F, dev.ptr(self.traces),
+                  dev.stream_handle(stream))
+        return self.traces[:F]
+
+    def beamform(self, traces=None, n_frames: int | None = None, stream=None, out_offset: int = 0):
+        F = self.F if n_frames is None else n_frames
+        traces = self.traces if traces is None else traces
+        P = self.grid.nx * self.grid.nz
+        s = dev.stream_handle(stream)
+        iq = self.iq[out_offset:out_offset + F]
+        inten = self.inten[out_offset:out_offset + F]
+        fmax = self.fmax[out_offset:out_offset + F]
+        _lib.call("kkb_kk_plan_run", self._kk, dev.ptr(traces), F, self.N * self.M * self.T,
+                  dev.ptr(iq), _lib.KKB_OUT_C64, P, dev.ptr(inten), dev.ptr(fmax), s)
+        if self.want_db:
+            db = self.db[out_offset:out_offset + F]
+            _lib.call("kkb_log_compress", dev.ptr(inten), dev.ptr(fmax), F, P, self.floor_db,
+                      dev.ptr(db), s)
+        return iq
+
+    def gather(self, n_frames: int | None = None, stream=None):
+        """K5 alone on self.traces (bench instrumentation)."""
+        F = self.F if n_frames is None else n_frames
+        P = self.grid.nx * self.grid.nz
+        fmax = self.fmax[:F]
+        _lib.call("kkb_kk_plan_run", self._kk, dev.ptr(self.traces), F, self.N * self.M * self.T,
+                  dev.ptr(self.iq), _lib.KKB_OUT_C64, P, dev.ptr(self.inten), dev.ptr(fmax),
+                  dev.stream_handle(stream))
+        return self.iq[:F]
+
+    def detect(self, n_frames: int | None = None, stream=None):
+        """K6 dB map alone (bench instrumentation)."""
+        F = self.F if n_frames is None else n_frames
+        P = self.grid.nx * self.grid.nz
+        _lib.call("kkb_log_compress", dev.ptr(self.inten), dev.ptr(self.fmax), F, P, self.floor_db,
+                  dev.ptr(self.db), dev.stream_handle(stream))
+        return self.db[:F]
+
+    def run(self, rf, stream=None):
+        """Whole hot path for a (F, N, L, T) float32 CUDA tensor; asynchronous.
+        Returns the complex64 IQ images (F, X, Z) (``self.inten`` / ``self.db``
+        hold the detected and log-compressed images)."""
+        t = self.t
+        if rf.dtype != t.float32 or tuple(rf.shape) != (self.F, self.N, self.L, self.T):
+            raise ConfigError(f"expected float32 RF of shape {(self.F, self.N, self.L, self.T)}")
+        if not rf.is_contiguous():
+            raise ConfigError("RF must be contiguous")
+        self.decompose(rf, stream=stream)
+        return self.beamform(stream=stream)
+
+    # ------------------------------------------------------------------ end-to-end path
+    def run_host(self, rf_host, iq_host, chunk_frames: int = 16, streams=None, staging=None):
+        """Pinned host RF (F, N, L, T) float32 -> pinned host IQ (F, X, Z) complex64.
+
+        Chunks of frames are copied in, processed and copied out on alternating
+        streams so that H2D, kernels and D2H overlap."""
+        t = self.t
+        F = self.F
+        C = max(1, min(chunk_frames, self.chunk, F))
+        if streams is None:
+            streams = [t.cuda.Stream(), t.cuda.Stream()]
+        while len(self._stream_decs) < len(streams):
+            self._stream_decs.append(self._new_decomposer(C))
+        if staging is None:
+            staging = [t.empty((C, self.N, self.L, self.T), dtype=t.float32, device="cuda")
+                       for _ in streams]
+        for i, f0 in enumerate(range(0, F, C)):
+            n = min(C, F - f0)
+            s = streams[i % len(streams)]
+            buf = staging[i % len(staging)]
+            with t.cuda.stream(s):
+                buf[:n].copy_(rf_host[f0:f0 + n], non_blocking=True)
+                tr = self.traces[f0:f0 + n]
+                _lib.call("kkb_decomposer_run", self._stream_decs[i % len(streams)], dev.ptr(buf),
+                          n, dev.ptr(tr), s.cuda_stream)
+                self.beamform(traces=tr, n_frames=n, stream=s, out_offset=f0)
+                iq_host[f0:f0 + n].copy_(self.iq[f0:f0 + n], non_blocking=True)
+        for s in streams:
+            s.synchronize()
+        return iq_host
+
+    def close(self):
+        if not self._closed:
+            lib = _lib.load()
+            lib.kkb_decomposer_destroy(self._dec)
+            for h in self._stream_decs:
+                lib.kkb_decomposer_destroy(h)
+            lib.kkb_kk_plan_destroy(self._kk)
+            self._closed = True
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

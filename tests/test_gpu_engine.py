@@ -1,0 +1,155 @@
+"""GPU parity of the device-resident batched pipeline (KKEngine) on the five
+workloads.  Tolerances: traces and IQ rel L2 <= 1e-5 vs the oracle /
+reference goldens; batch/rerun results bit-identical."""
+
+import numpy as np
+import pytest
+
+from conftest import C, golden, rel_l2, sha
+
+pytestmark = pytest.mark.gpu
+
+import paper_2603_22496_b200 as kb  # noqa: E402
+from paper_2603_22496_b200 import configs  # noqa: E402
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+def _engine(w, frames, **kw):
+    return kb.KKEngine(w.array, w.params, w.receive, w.grid, frames=frames, **kw)
+
+
+def test_engine_config1_point_targets(oracle, config1_rf):
+    torch = _torch()
+    w, rf = config1_rf
+    g = golden("config1")
+    eng = _engine(w, 1)
+    iq = eng.run(torch.from_numpy(rf[None]).cuda())
+    torch.cuda.synchronize()
+    assert rel_l2(eng.traces[0].cpu().numpy(), g["compressed"]) <= 1e-5
+    assert rel_l2(iq[0].cpu().numpy(), g["image"]) <= 1e-5
+    # fused detection + dB map
+    inten = eng.inten[0].cpu().numpy().astype(np.float64)
+    ref_i = oracle.intensity(g["image"])
+    assert rel_l2(inten, ref_i) <= 1e-5
+    db = eng.db[0].cpu().numpy()
+    ref_db = oracle.log_compress_db(ref_i, floor_db=-60.0)
+    assert np.abs(db - ref_db).max() <= 1e-3
+    eng.close()
+
+
+@pytest.mark.parametrize("name,cfg", [("config2_noise", 2), ("config4_noise", 4)])
+def test_engine_noise_configs_match_reference(oracle, name, cfg):
+    torch = _torch()
+    w = configs.CONFIGS[cfg]()
+    g = golden(name)
+    p, arr = w.params, w.array
+    rf = configs.noise_rf(p.num_transmits, arr.num_elements, p.num_samples, seed=cfg)
+    assert sha(rf) == str(g["rf_sha"])
+    eng = _engine(w, 1)
+    iq = eng.run(torch.from_numpy(rf[None]).cuda())
+    torch.cuda.synchronize()
+    assert rel_l2(eng.traces[0].cpu().numpy(), g["compressed"]) <= 1e-5
+    assert rel_l2(iq[0].cpu().numpy(), g["image"]) <= 1e-5
+    eng.close()
+
+
+def test_engine_batch_equals_single_frames_and_is_deterministic():
+    torch = _torch()
+    w = configs.config4(frames=6)
+    p, arr = w.params, w.array
+    rf = np.stack([configs.noise_rf(p.num_transmits, arr.num_elements, p.num_samples, seed=s)
+                   for s in range(6)])
+    rf_d = torch.from_numpy(rf).cuda()
+    eng = _engine(w, 6, chunk_frames=4)
+    a = eng.run(rf_d).clone()
+    b = eng.run(rf_d).clone()
+    torch.cuda.synchronize()
+    assert torch.equal(a, b)
+    one = _engine(w, 1)
+    for f in (0, 5):
+        s = one.run(rf_d[f:f + 1].contiguous()).clone()
+        torch.cuda.synchronize()
+        assert torch.equal(s[0], a[f])
+    eng.close()
+    one.close()
+
+
+def test_engine_run_host_equals_device_path():
+    torch = _torch()
+    w = configs.config4(frames=5)
+    p, arr = w.params, w.array
+    rf = np.stack([configs.noise_rf(p.num_transmits, arr.num_elements, p.num_samples, seed=10 + s)
+                   for s in range(5)])
+    eng = _engine(w, 5)
+    ref = eng.run(torch.from_numpy(rf).cuda()).clone()
+    torch.cuda.synchronize()
+    host_in = torch.from_numpy(rf).pin_memory()
+    host_out = torch.empty((5, w.grid.nx, w.grid.nz), dtype=torch.complex64).pin_memory()
+    eng.run_host(host_in, host_out, chunk_frames=2)
+    assert torch.equal(host_out, ref.cpu())
+    eng.close()
+
+
+@pytest.mark.parametrize("scheme", ["dense_vernier", "shifted_vernier", "confocal", "hybrid"])
+def test_engine_config3_schemes(oracle, scheme):
+    torch = _torch()
+    w3 = configs.config3()
+    params, rx = w3.extra_receive[scheme]
+    arr, grid = w3.array, w3.grid
+    rf = configs.noise_rf(params.num_transmits, arr.num_elements, params.num_samples, seed=3)
+    eng = kb.KKEngine(arr, params, rx, grid, frames=1)
+    iq = eng.run(torch.from_numpy(rf[None]).cuda())
+    torch.cuda.synchronize()
+    fs = arr.sampling_frequency
+    ref_tr = oracle.decompose_f64(rf, fs, arr.positions, rx.angles, C)
+    assert rel_l2(eng.traces[0].cpu().numpy(), ref_tr) <= 1e-5
+    luts = oracle.kk_luts(grid.x, grid.z, params.transmit_angles, rx.angles, C)
+    ref = oracle.kk_kernel(ref_tr, *luts, np.ones(rx.num_angles), fs, 0.0)
+    assert rel_l2(iq[0].cpu().numpy(), ref) <= 1e-5
+    eng.close()
+
+
+def test_engine_config5_full_size(oracle):
+    """Config 5 at full size (961 pairs, 2048 x 1024 px, T = 4096): traces vs the
+    float64 oracle over the whole frame, IQ vs the oracle on a row block, and
+    linearity over the whole image (size-independent property)."""
+    torch = _torch()
+    w = configs.config5()
+    p, arr, grid = w.params, w.array, w.grid
+    rf = configs.noise_rf(p.num_transmits, arr.num_elements, p.num_samples, seed=5)
+    eng = _engine(w, 1)
+    iq = eng.run(torch.from_numpy(rf[None]).cuda()).clone()
+    torch.cuda.synchronize()
+    fs = arr.sampling_frequency
+    ref_tr = oracle.decompose_f64(rf, fs, arr.positions, w.receive.angles, C)
+    got_tr = eng.traces[0].cpu().numpy()
+    assert rel_l2(got_tr, ref_tr) <= 1e-5
+    luts = oracle.kk_luts(grid.x, grid.z, p.transmit_angles, w.receive.angles, C)
+    rows = (500 * grid.nz, 502 * grid.nz)  # two lateral columns x all depths
+    ref = oracle.kk_kernel(ref_tr, *luts, np.ones(31), fs, 0.0, p_range=rows)
+    got = iq[0].cpu().numpy().ravel()[rows[0]:rows[1]]
+    assert rel_l2(got, ref) <= 1e-5
+    # linearity: IQ(2 rf + rf') = 2 IQ(rf) + IQ(rf')
+    rf2 = configs.noise_rf(p.num_transmits, arr.num_elements, p.num_samples, seed=55)
+    b = eng.run(torch.from_numpy(rf2[None]).cuda()).clone()
+    mix = eng.run(torch.from_numpy((2 * rf + rf2)[None]).cuda()).clone()
+    torch.cuda.synchronize()
+    assert rel_l2(mix.cpu().numpy(), (2 * iq + b).cpu().numpy()) <= 1e-5
+    eng.close()
+
+
+def test_engine_weights_and_nearest(oracle, config1_rf):
+    torch = _torch()
+    w, rf = config1_rf
+    g = golden("config1")
+    eng = kb.KKEngine(w.array, w.params, w.receive, w.grid, frames=1, interpolation="nearest",
+                      pulse_delay=0.3e-6, channel_weights=g["weights"])
+    iq = eng.run(torch.from_numpy(rf[None]).cuda())
+    torch.cuda.synchronize()
+    assert rel_l2(iq[0].cpu().numpy(), g["image_nearest"]) <= 1e-5
+    eng.close()
