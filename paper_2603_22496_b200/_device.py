@@ -42,6 +42,7 @@ def _dtype(np_dtype):
         np.dtype(np.complex128): t.complex128,
         np.dtype(np.int64): t.int64,
         np.dtype(np.int16): t.int16,
+        np.dtype(np.int32): t.int32,
         np.dtype(np.uint32): t.int32,
     }
     return table[np.dtype(np_dtype)]

@@ -12,10 +12,11 @@
 // the phase reaches ~68 cycles and a float32 phase would cost 3-6e-6 of
 // relative error.
 //
-// Contraction: each thread owns one bin k and a register tile of NB rows x
-// MC receive angles (complex accumulators), streaming l; X and R loads are
-// coalesced along k, every X value feeds MC FMAs and every R value NB.  FP32
-// FMA (4 per complex MAC): exact enough for the 1e-6 max-abs reference tests.
+// Contraction: a CTA owns KT bins x BT rows; element chunks of X and R stream
+// through shared memory (cp.async, double-buffered, coalesced along k), and
+// each thread keeps an NB x MC register tile of complex accumulators, so each
+// shared X value feeds MC FMAs and each R value NB.  FP32 FMA (4 per complex
+// MAC): within the 1e-6 max-abs bound of the reference's compress tests.
 
 #include <algorithm>
 #include <vector>
@@ -64,35 +65,81 @@ int build_ramps(const double *tau_host, int L, int M, const double *freq_host,
     return KKB_OK;
 }
 
-#define KKB_CT_KX 64  // bins per CTA (threads along x)
-#define KKB_CT_BY 4   // row groups per CTA (threads along y)
+// Tile: KT bins x BT rows per CTA, all (<= MC) receive angles; the element
+// axis streams through shared memory in chunks of LC with cp.async double
+// buffering.  Thread (kx, bg) owns bin k0+kx and rows b0 + bg*NB .. +NB-1.
+#define KKB_CT_KT 32
+#define KKB_CT_BT 32
+#define KKB_CT_NB 4
+#define KKB_CT_LC 4
+#define KKB_CT_THREADS (KKB_CT_KT * (KKB_CT_BT / KKB_CT_NB))
 
-template <int NB, int MC>
-__global__ void __launch_bounds__(KKB_CT_KX *KKB_CT_BY)
+__device__ __forceinline__ void cp_async8z(void *smem_dst, const void *gsrc, bool valid) {
+    unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
+    int sz = valid ? 8 : 0;
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(gsrc), "r"(sz)
+                 : "memory");
+}
+
+template <int MC>
+__global__ void __launch_bounds__(KKB_CT_THREADS)
 k_contract(const float2 *__restrict__ X, long long ldx, const float2 *__restrict__ R,
            long long ldr, float2 *__restrict__ Y, long long ldy, long long B, int L, int M, int Kb) {
-    const int k = blockIdx.x * KKB_CT_KX + threadIdx.x;
-    const long long b0 = ((long long)blockIdx.y * KKB_CT_BY + threadIdx.y) * NB;
+    constexpr int KT = KKB_CT_KT, BT = KKB_CT_BT, NB = KKB_CT_NB, LC = KKB_CT_LC;
+    extern __shared__ __align__(16) float2 csm[];
+    float2 *Xs = csm;                       // [2][LC][BT][KT]
+    float2 *Rs = csm + 2 * LC * BT * KT;    // [2][LC][MC][KT]
+    const int tid = threadIdx.x;
+    const int kx = tid % KT, bg = tid / KT;
+    const int k0 = blockIdx.x * KT;
+    const long long b0 = (long long)blockIdx.y * BT;
     const int m0 = blockIdx.z * MC;
-    if (k >= Kb || b0 >= B) return;
+    const int nlc = (L + LC - 1) / LC;
+
+    auto stage = [&](int c, int buf) {
+        const int l0 = c * LC;
+        for (int i = tid; i < LC * BT * KT; i += KKB_CT_THREADS) {
+            int kk = i % KT, r = i / KT, bb = r % BT, ll = r / BT;
+            long long b = b0 + bb;
+            int l = l0 + ll, k = k0 + kk;
+            bool ok = b < B && l < L && k < Kb;
+            const float2 *src = ok ? X + (b * L + l) * ldx + k : X;
+            cp_async8z(&Xs[((buf * LC + ll) * BT + bb) * KT + kk], src, ok);
+        }
+        for (int i = tid; i < LC * MC * KT; i += KKB_CT_THREADS) {
+            int kk = i % KT, r = i / KT, j = r % MC, ll = r / MC;
+            int m = m0 + j, l = l0 + ll, k = k0 + kk;
+            bool ok = m < M && l < L && k < Kb;
+            const float2 *src = ok ? R + ((long long)m * L + l) * ldr + k : R;
+            cp_async8z(&Rs[((buf * LC + ll) * MC + j) * KT + kk], src, ok);
+        }
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+    };
+
     float2 acc[NB][MC];
 #pragma unroll
     for (int i = 0; i < NB; ++i)
 #pragma unroll
         for (int j = 0; j < MC; ++j) acc[i][j] = make_float2(0.f, 0.f);
-    const int nb = (int)min((long long)NB, B - b0);
-    const int mc = min(MC, M - m0);
-    const float2 *xp = X + b0 * L * ldx + k;
-    const float2 *rp = R + (long long)m0 * L * ldr + k;
-    for (int l = 0; l < L; ++l) {
-        float2 xv[NB];
+
+    stage(0, 0);
+    for (int c = 0; c < nlc; ++c) {
+        const int buf = c & 1;
+        if (c + 1 < nlc) {
+            stage(c + 1, buf ^ 1);
+            asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+        } else {
+            asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+        }
+        __syncthreads();
 #pragma unroll
-        for (int i = 0; i < NB; ++i)
-            xv[i] = (i < nb) ? __ldg(xp + ((long long)i * L + l) * ldx) : make_float2(0.f, 0.f);
+        for (int ll = 0; ll < LC; ++ll) {
+            float2 xv[NB];
 #pragma unroll
-        for (int j = 0; j < MC; ++j) {
-            if (j < mc) {
-                const float2 r = __ldg(rp + ((long long)j * L + l) * ldr);
+            for (int i = 0; i < NB; ++i) xv[i] = Xs[((buf * LC + ll) * BT + bg * NB + i) * KT + kx];
+#pragma unroll
+            for (int j = 0; j < MC; ++j) {
+                const float2 r = Rs[((buf * LC + ll) * MC + j) * KT + kx];
 #pragma unroll
                 for (int i = 0; i < NB; ++i) {
                     acc[i][j].x = fmaf(xv[i].x, r.x, acc[i][j].x);
@@ -102,27 +149,33 @@ k_contract(const float2 *__restrict__ X, long long ldx, const float2 *__restrict
                 }
             }
         }
+        __syncthreads();  // buffer `buf` is refilled by the next iteration's stage()
     }
+    const int k = k0 + kx;
+    if (k >= Kb) return;
 #pragma unroll
     for (int i = 0; i < NB; ++i) {
-        if (i >= nb) break;
+        const long long b = b0 + bg * NB + i;
+        if (b >= B) break;
 #pragma unroll
         for (int j = 0; j < MC; ++j)
-            if (j < mc) Y[((b0 + i) * M + m0 + j) * ldy + k] = acc[i][j];
+            if (m0 + j < M) Y[(b * M + m0 + j) * ldy + k] = acc[i][j];
     }
 }
 
-template <int NB, int MC>
+template <int MC>
 static int launch_contract(const float2 *X, long long ldx, const float2 *R, long long ldr, float2 *Y,
                            long long ldy, long long B, int L, int M, int Kb, cudaStream_t s) {
-    dim3 block(KKB_CT_KX, KKB_CT_BY);
-    dim3 grid((unsigned)ceil_div(Kb, KKB_CT_KX), (unsigned)ceil_div(B, (long long)NB * KKB_CT_BY),
+    dim3 grid((unsigned)ceil_div(Kb, KKB_CT_KT), (unsigned)ceil_div(B, KKB_CT_BT),
               (unsigned)ceil_div(M, MC));
     if (grid.y > 65535u) {
         set_error("contraction batch too large (%lld rows)", B);
         return KKB_ERR_UNSUPPORTED;
     }
-    k_contract<NB, MC><<<grid, block, 0, s>>>(X, ldx, R, ldr, Y, ldy, B, L, M, Kb);
+    const int sm = (int)sizeof(float2) * 2 * KKB_CT_LC * KKB_CT_KT * (KKB_CT_BT + MC);
+    KKB_TRY_CUDA(cudaFuncSetAttribute(k_contract<MC>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm),
+                 "smem attr contract");
+    k_contract<MC><<<grid, KKB_CT_THREADS, sm, s>>>(X, ldx, R, ldr, Y, ldy, B, L, M, Kb);
     KKB_CHECK_LAUNCH("k_contract");
     return KKB_OK;
 }
@@ -130,10 +183,10 @@ static int launch_contract(const float2 *X, long long ldx, const float2 *R, long
 int contract(const float2 *X, long long ldx, const float2 *R, long long ldr, float2 *Y,
              long long ldy, long long B, int L, int M, int Kb, cudaStream_t s) {
     if (B <= 0 || Kb <= 0) return KKB_OK;
-    if (M <= 4) return launch_contract<8, 4>(X, ldx, R, ldr, Y, ldy, B, L, M, Kb, s);
-    if (M <= 8) return launch_contract<6, 8>(X, ldx, R, ldr, Y, ldy, B, L, M, Kb, s);
-    if (M <= 12) return launch_contract<4, 12>(X, ldx, R, ldr, Y, ldy, B, L, M, Kb, s);
-    return launch_contract<4, 16>(X, ldx, R, ldr, Y, ldy, B, L, M, Kb, s);
+    if (M <= 4) return launch_contract<4>(X, ldx, R, ldr, Y, ldy, B, L, M, Kb, s);
+    if (M <= 8) return launch_contract<8>(X, ldx, R, ldr, Y, ldy, B, L, M, Kb, s);
+    if (M <= 12) return launch_contract<12>(X, ldx, R, ldr, Y, ldy, B, L, M, Kb, s);
+    return launch_contract<16>(X, ldx, R, ldr, Y, ldy, B, L, M, Kb, s);
 }
 
 }  // namespace kkb

@@ -164,87 +164,99 @@ __device__ __noinline__ void dft_generic(float2 *v, int R, const float2 *__restr
 }
 
 // Run every Stockham stage on G traces laid out back to back (stride T) in
-// buffer `a`; `b` is scratch of the same size.  Returns the buffer holding
-// the result.  Must be called by all threads of the CTA.
-__device__ float2 *stockham(float2 *a, float2 *b, int G, const FftPlan &p) {
+// buffer `a`; `b` is scratch of the same size; `tw` is the twiddle table in
+// shared memory.  Each thread walks butterfly indices j and applies them to
+// all G traces, so a twiddle is fetched once per j.  Ns is a power of two in
+// every stage that precedes the first odd radix (radices run 8,4,2 first),
+// so k = j mod Ns is a mask there.  Returns the buffer holding the result.
+__device__ float2 *stockham(float2 *a, float2 *b, int G, const FftPlan &p, const float2 *tw) {
     const int T = p.T;
-    const float2 *__restrict__ tw = p.tw;
     int Ns = 1;
     for (int s = 0; s < p.nstages; ++s) {
         const int R = p.radix[s];
         const int TR = T / R;
         const int tws = T / (Ns * R);
-        for (int idx = threadIdx.x; idx < G * TR; idx += blockDim.x) {
-            const int g = idx / TR;
-            const int j = idx - g * TR;
-            const int k = j % Ns;
-            const float2 *src = a + g * T;
-            float2 *dst = b + g * T;
+        const bool pow2 = (Ns & (Ns - 1)) == 0;
+        for (int j = threadIdx.x; j < TR; j += blockDim.x) {
+            const int k = pow2 ? (j & (Ns - 1)) : (j % Ns);
+            const int base = (j - k) * R + k;
             if (R == 8) {
-                float2 v[8];
+                float2 w[8];
 #pragma unroll
-                for (int r = 0; r < 8; ++r) v[r] = src[j + r * TR];
-                if (Ns > 1) {
+                for (int r = 1; r < 8; ++r) w[r] = tw[r * k * tws];
+                for (int g = 0; g < G; ++g) {
+                    const float2 *src = a + g * T;
+                    float2 *dst = b + g * T;
+                    float2 v[8];
 #pragma unroll
-                    for (int r = 1; r < 8; ++r) v[r] = cmul(v[r], __ldg(tw + r * k * tws));
+                    for (int r = 0; r < 8; ++r) v[r] = src[j + r * TR];
+#pragma unroll
+                    for (int r = 1; r < 8; ++r) v[r] = cmul(v[r], w[r]);
+                    dft8(v);
+#pragma unroll
+                    for (int r = 0; r < 8; ++r) dst[base + r * Ns] = v[r];
                 }
-                dft8(v);
-                const int base = (j - k) * 8 + k;
-#pragma unroll
-                for (int r = 0; r < 8; ++r) dst[base + r * Ns] = v[r];
             } else if (R == 4) {
-                float2 v[4];
+                float2 w[4];
 #pragma unroll
-                for (int r = 0; r < 4; ++r) v[r] = src[j + r * TR];
-                if (Ns > 1) {
+                for (int r = 1; r < 4; ++r) w[r] = tw[r * k * tws];
+                for (int g = 0; g < G; ++g) {
+                    const float2 *src = a + g * T;
+                    float2 *dst = b + g * T;
+                    float2 v[4];
 #pragma unroll
-                    for (int r = 1; r < 4; ++r) v[r] = cmul(v[r], __ldg(tw + r * k * tws));
+                    for (int r = 0; r < 4; ++r) v[r] = src[j + r * TR];
+#pragma unroll
+                    for (int r = 1; r < 4; ++r) v[r] = cmul(v[r], w[r]);
+                    dft4(v);
+#pragma unroll
+                    for (int r = 0; r < 4; ++r) dst[base + r * Ns] = v[r];
                 }
-                dft4(v);
-                const int base = (j - k) * 4 + k;
-#pragma unroll
-                for (int r = 0; r < 4; ++r) dst[base + r * Ns] = v[r];
             } else if (R == 2) {
-                float2 v[2];
-                v[0] = src[j];
-                v[1] = src[j + TR];
-                if (Ns > 1) v[1] = cmul(v[1], __ldg(tw + k * tws));
-                dft2(v[0], v[1]);
-                const int base = (j - k) * 2 + k;
-                dst[base] = v[0];
-                dst[base + Ns] = v[1];
+                const float2 w1 = tw[k * tws];
+                for (int g = 0; g < G; ++g) {
+                    const float2 *src = a + g * T;
+                    float2 *dst = b + g * T;
+                    float2 v0 = src[j], v1 = cmul(src[j + TR], w1);
+                    dft2(v0, v1);
+                    dst[base] = v0;
+                    dst[base + Ns] = v1;
+                }
             } else if (R == 3) {
-                float2 v[3];
+                const float2 w1 = tw[k * tws], w2 = tw[2 * k * tws];
+                for (int g = 0; g < G; ++g) {
+                    const float2 *src = a + g * T;
+                    float2 *dst = b + g * T;
+                    float2 v[3] = {src[j], cmul(src[j + TR], w1), cmul(src[j + 2 * TR], w2)};
+                    dft3(v);
 #pragma unroll
-                for (int r = 0; r < 3; ++r) v[r] = src[j + r * TR];
-                if (Ns > 1) {
-#pragma unroll
-                    for (int r = 1; r < 3; ++r) v[r] = cmul(v[r], __ldg(tw + r * k * tws));
+                    for (int r = 0; r < 3; ++r) dst[base + r * Ns] = v[r];
                 }
-                dft3(v);
-                const int base = (j - k) * 3 + k;
-#pragma unroll
-                for (int r = 0; r < 3; ++r) dst[base + r * Ns] = v[r];
             } else if (R == 5) {
-                float2 v[5];
+                float2 w[5];
 #pragma unroll
-                for (int r = 0; r < 5; ++r) v[r] = src[j + r * TR];
-                if (Ns > 1) {
+                for (int r = 1; r < 5; ++r) w[r] = tw[r * k * tws];
+                for (int g = 0; g < G; ++g) {
+                    const float2 *src = a + g * T;
+                    float2 *dst = b + g * T;
+                    float2 v[5];
 #pragma unroll
-                    for (int r = 1; r < 5; ++r) v[r] = cmul(v[r], __ldg(tw + r * k * tws));
+                    for (int r = 0; r < 5; ++r) v[r] = src[j + r * TR];
+#pragma unroll
+                    for (int r = 1; r < 5; ++r) v[r] = cmul(v[r], w[r]);
+                    dft5(v);
+#pragma unroll
+                    for (int r = 0; r < 5; ++r) dst[base + r * Ns] = v[r];
                 }
-                dft5(v);
-                const int base = (j - k) * 5 + k;
-#pragma unroll
-                for (int r = 0; r < 5; ++r) dst[base + r * Ns] = v[r];
             } else {
-                float2 v[KKB_FFT_MAX_RADIX];
-                for (int r = 0; r < R; ++r) v[r] = src[j + r * TR];
-                if (Ns > 1)
-                    for (int r = 1; r < R; ++r) v[r] = cmul(v[r], __ldg(tw + r * k * tws));
-                dft_generic(v, R, tw, T);
-                const int base = (j - k) * R + k;
-                for (int r = 0; r < R; ++r) dst[base + r * Ns] = v[r];
+                for (int g = 0; g < G; ++g) {
+                    const float2 *src = a + g * T;
+                    float2 *dst = b + g * T;
+                    float2 v[KKB_FFT_MAX_RADIX];
+                    for (int r = 0; r < R; ++r) v[r] = cmul(src[j + r * TR], tw[r * k * tws]);
+                    dft_generic(v, R, tw, T);
+                    for (int r = 0; r < R; ++r) dst[base + r * Ns] = v[r];
+                }
             }
         }
         __syncthreads();
@@ -257,6 +269,10 @@ __device__ float2 *stockham(float2 *a, float2 *b, int G, const FftPlan &p) {
 }
 
 // ------------------------------------------------------------- kernels
+__device__ __forceinline__ void load_twiddles(float2 *tw_s, const FftPlan &p) {
+    for (int i = threadIdx.x; i < p.T; i += blockDim.x) tw_s[i] = p.tw[i];
+}
+
 // Complex-to-complex FFT of `ntraces` rows.  Input row i: in + i*in_stride,
 // first in_len bins read, the rest treated as zero (one-sided spectra).
 // Output row i: out + i*out_stride, first out_len bins written, times scale.
@@ -268,26 +284,31 @@ k_fft_c2c(const float2 *__restrict__ in, long long in_stride, int in_len,
     const int T = p.T;
     float2 *a = smem;
     float2 *b = smem + G * T;
+    float2 *tw = smem + 2 * G * T;
+    load_twiddles(tw, p);
     const long long t0 = (long long)blockIdx.x * G;
-    for (int idx = threadIdx.x; idx < G * T; idx += blockDim.x) {
-        int g = idx / T;
-        int t = idx - g * T;
-        long long tr = t0 + g;
-        float2 v = make_float2(0.f, 0.f);
-        if (tr < ntraces && t < in_len) v = in[tr * in_stride + t];
-        if (inverse) v.y = -v.y;
-        a[idx] = v;
+    const float sgn = inverse ? -1.f : 1.f;
+    for (int g = 0; g < G; ++g) {
+        const long long tr = t0 + g;
+        const bool live = tr < ntraces;
+        const float2 *row = in + (live ? tr : 0) * in_stride;
+        for (int t = threadIdx.x; t < T; t += blockDim.x) {
+            float2 v = make_float2(0.f, 0.f);
+            if (live && t < in_len) v = row[t];
+            a[g * T + t] = make_float2(v.x, sgn * v.y);
+        }
     }
     __syncthreads();
-    float2 *res = stockham(a, b, G, p);
-    for (int idx = threadIdx.x; idx < G * out_len; idx += blockDim.x) {
-        int g = idx / out_len;
-        int t = idx - g * out_len;
-        long long tr = t0 + g;
-        if (tr >= ntraces) continue;
-        float2 v = res[g * T + t];
-        if (inverse) v.y = -v.y;
-        out[tr * out_stride + t] = make_float2(v.x * scale, v.y * scale);
+    float2 *res = stockham(a, b, G, p, tw);
+    const float sy = sgn * scale;
+    for (int g = 0; g < G; ++g) {
+        const long long tr = t0 + g;
+        if (tr >= ntraces) break;
+        float2 *row = out + tr * out_stride;
+        for (int t = threadIdx.x; t < out_len; t += blockDim.x) {
+            const float2 v = res[g * T + t];
+            row[t] = make_float2(v.x * scale, v.y * sy);
+        }
     }
 }
 
@@ -302,31 +323,46 @@ k_fft_r2c_pairs(const float *__restrict__ in, long long ntraces, float2 *__restr
     const int T = p.T;
     float2 *a = smem;
     float2 *b = smem + G * T;
+    float2 *tw = smem + 2 * G * T;
+    load_twiddles(tw, p);
     const long long pair0 = (long long)blockIdx.x * G;
-    for (int idx = threadIdx.x; idx < G * T; idx += blockDim.x) {
-        int g = idx / T;
-        int t = idx - g * T;
-        long long r0 = 2 * (pair0 + g);
-        float re = (r0 < ntraces) ? in[r0 * T + t] : 0.f;
-        float im = (r0 + 1 < ntraces) ? in[(r0 + 1) * T + t] : 0.f;
-        a[idx] = make_float2(re, im);
+    const bool vec4 = (T & 3) == 0;
+    for (int g = 0; g < G; ++g) {
+        const long long r0 = 2 * (pair0 + g);
+        const bool l0 = r0 < ntraces, l1 = r0 + 1 < ntraces;
+        const float *x0 = in + (l0 ? r0 : 0) * T;
+        const float *x1 = in + (l1 ? r0 + 1 : 0) * T;
+        if (vec4) {
+            for (int t = 4 * threadIdx.x; t < T; t += 4 * blockDim.x) {
+                float4 u = l0 ? __ldg(reinterpret_cast<const float4 *>(x0 + t)) : make_float4(0, 0, 0, 0);
+                float4 w = l1 ? __ldg(reinterpret_cast<const float4 *>(x1 + t)) : make_float4(0, 0, 0, 0);
+                float2 *d = a + g * T + t;
+                d[0] = make_float2(u.x, w.x);
+                d[1] = make_float2(u.y, w.y);
+                d[2] = make_float2(u.z, w.z);
+                d[3] = make_float2(u.w, w.w);
+            }
+        } else {
+            for (int t = threadIdx.x; t < T; t += blockDim.x)
+                a[g * T + t] = make_float2(l0 ? x0[t] : 0.f, l1 ? x1[t] : 0.f);
+        }
     }
     __syncthreads();
-    float2 *res = stockham(a, b, G, p);
-    for (int idx = threadIdx.x; idx < G * K; idx += blockDim.x) {
-        int g = idx / K;
-        int k = idx - g * K;
-        long long r0 = 2 * (pair0 + g);
-        if (r0 >= ntraces) continue;
-        float2 zk = res[g * T + k];
-        float2 zn = res[g * T + (k == 0 ? 0 : T - k)];
-        float s = bin_scale ? bin_scale[k] : 1.0f;
-        // X0 = (Z_k + conj(Z_-k)) / 2 ; X1 = (Z_k - conj(Z_-k)) / (2i)
-        float2 x0 = make_float2(0.5f * (zk.x + zn.x), 0.5f * (zk.y - zn.y));
-        float dx = zk.x - zn.x, dy = zk.y + zn.y;
-        float2 x1 = make_float2(0.5f * dy, -0.5f * dx);
-        out[r0 * out_stride + k] = make_float2(x0.x * s, x0.y * s);
-        if (r0 + 1 < ntraces) out[(r0 + 1) * out_stride + k] = make_float2(x1.x * s, x1.y * s);
+    float2 *res = stockham(a, b, G, p, tw);
+    for (int g = 0; g < G; ++g) {
+        const long long r0 = 2 * (pair0 + g);
+        if (r0 >= ntraces) break;
+        const bool has1 = r0 + 1 < ntraces;
+        float2 *o0 = out + r0 * out_stride;
+        float2 *o1 = out + (r0 + 1) * out_stride;
+        for (int k = threadIdx.x; k < K; k += blockDim.x) {
+            const float2 zk = res[g * T + k];
+            const float2 zn = res[g * T + (k == 0 ? 0 : T - k)];
+            const float s = bin_scale ? bin_scale[k] : 1.0f;
+            // X0 = (Z_k + conj(Z_-k)) / 2 ; X1 = (Z_k - conj(Z_-k)) / (2i)
+            o0[k] = make_float2(0.5f * s * (zk.x + zn.x), 0.5f * s * (zk.y - zn.y));
+            if (has1) o1[k] = make_float2(0.5f * s * (zk.y + zn.y), -0.5f * s * (zk.x - zn.x));
+        }
     }
 }
 
@@ -361,7 +397,7 @@ static int traces_per_cta(int T) {
     return G < 1 ? 1 : G;
 }
 
-static int smem_bytes(int T, int G) { return 2 * G * T * (int)sizeof(float2); }
+static int smem_bytes(int T, int G) { return (2 * G + 1) * T * (int)sizeof(float2); }
 
 static int ensure_smem(const void *fn, int bytes) {
     if (bytes > 48 * 1024) {

@@ -3,12 +3,13 @@
 
 #include <cuda_runtime.h>
 
-// kk gather tile: TZ = 32*WZ depth rows x TX = WX*PX lateral columns per CTA
+// kk gather tile: TZ = 8*WZ depth rows x TX = 16*WX lateral columns per CTA
+// (a warp covers 8 x 16 pixels, 2 x 2 per lane)
 #define KKB_KK_WZ 4
 #define KKB_KK_WX 2
-#define KKB_KK_PX 4
-#define KKB_KK_TZ (32 * KKB_KK_WZ)
-#define KKB_KK_TX (KKB_KK_WX * KKB_KK_PX)
+#define KKB_KK_TZ (8 * KKB_KK_WZ)
+#define KKB_KK_TX (16 * KKB_KK_WX)
+#define KKB_KK_STAGE_ELEMS 2048  // window entries staged per pipeline stage
 
 namespace kkb {
 

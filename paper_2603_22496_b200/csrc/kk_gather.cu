@@ -1,25 +1,31 @@
 // K4 delay tables, K5 kk pixel gather, K6 detection / log-compression epilogue.
 //
 // K5 replaces _kk_kernel (beamform.py:212-236).  Work decomposition:
-//   * CTA = one TZ x TX pixel tile of one frame (TZ = 32*WZ rows along depth,
-//     lanes along z so a warp reads neighbouring samples; TX = WX*PX columns,
-//     each thread owns PX pixels of one row).
+//   * CTA = one 32 x 32 pixel tile of one frame; a warp covers 8 depth rows x
+//     16 columns with each lane owning 2 x 2 pixels, so for each of its four
+//     pixel slots the warp is a 4 x 8 block whose delays span only a few
+//     samples: tap reads from shared memory are mostly broadcasts.
 //   * The (transmit n, receive-chunk) stages are pipelined: while stage s is
-//     summed, the per-pair trace windows of stage s+1 stream from L2/HBM into
-//     the other shared-memory buffer with cp.async (LDGSTS, zero-fill outside
-//     [0, T)).  A window covers every tap the tile can read for that pair
-//     (tile-corner delays +-1 sample: the delay is affine in (ix, iz)).
+//     summed, the trace windows of stage s+1 are loaded into registers and
+//     written to the other shared-memory buffer as (2 d0 - d1, d1 - d0)
+//     float4 entries (one 16 B read per linear tap pair).  A window covers
+//     every tap the tile can read for that pair (tile-corner delays +-1
+//     sample: the delay is affine in (ix, iz)); window starts for all pairs
+//     are computed once per CTA.
 //   * Per pixel-pair: fi = ((ltx+ltz)+lrz-lrx)*fs+shift in float64 with
 //     explicit _rn intrinsics (no FMA contraction: the exact IEEE sequence
-//     of beamform.py:223,225), floor via RD(fi + 1.5*2^52) (no F2I), the
-//     in-window predicate on the integer, the lerp weight from the mantissa
-//     of fi - (floor(fi) - 1).  Taps and partial sums over receive angles
-//     are float32; each transmit's partial is folded into a float64 total,
-//     in fixed order (deterministic; no atomics).
+//     of beamform.py:223,225), then ONE round-down add of 1.5*2^20 whose high
+//     word minus 0x41380000 is floor(fi) and whose low word is frac*2^32 —
+//     the in-window predicate is an unsigned compare, the lerp weight is
+//     (low >> 9) | 1.0f.  No branches: out-of-window taps get weight 0.
+//     Taps and partial sums over receive angles are float32; each transmit's
+//     partial is folded into a float64 total in fixed order (deterministic,
+//     no atomics).
 // Output complex64 or complex128, plus optional fused |IQ|^2 and per-frame
 // max for the dB epilogue (K6).
 
 #include <algorithm>
+#include <type_traits>
 #include <vector>
 
 #include "common.cuh"
@@ -212,17 +218,13 @@ int kk_window(const double *ltx, const double *ltz, const double *lrx, const dou
 }
 
 // ------------------------------------------------------------- K5 kernel
-__device__ __forceinline__ void cp_async8(void *smem_dst, const void *gsrc, bool valid) {
-    unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
-    int sz = valid ? 8 : 0;
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(gsrc), "r"(sz)
-                 : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-template <int Nw>
-__device__ __forceinline__ void cp_async_wait() {
-    asm volatile("cp.async.wait_group %0;\n" ::"n"(Nw) : "memory");
-}
+// Tile: TZ = 8*WZ depth rows x TX = 16*WX lateral columns.  A warp covers an
+// 8 x 16 patch; lane (zt, xt) = (lane % 4, lane / 4) owns the 2 x 2 pixels
+// rows zt + {0, 4}, columns xt + {0, 8} of it.  For a fixed (a, b) the 32
+// lanes form a 4 x 8 block whose delays span only ~3*dfi/dz + 7*dfi/dx
+// samples, so their tap reads hit a few shared-memory words (broadcast).
+#define KKB_FLOOR_MAGIC2 1572864.0   // 1.5 * 2^20: ulp 2^-32, |fi| < 2^19
+#define KKB_MAGIC2_HI 0x41380000     // high word of 1.5*2^20 + 0
 
 struct KKArgs {
     const float2 *data;
@@ -244,194 +246,229 @@ struct KKArgs {
     unsigned *fmax;
 };
 
-template <int WZ, int WX, int PX, bool LINEAR>
+// packed LUT index: tile row r -> (r/8)*4 + r%4 pair slot, a = (r/4)&1
+__device__ __forceinline__ int prow(int r) { return ((r >> 3) << 3) + ((r & 3) << 1) + ((r >> 2) & 1); }
+// tile column c -> (c/16)*8 + c%8 pair slot, b = (c/8)&1
+__device__ __forceinline__ int pcol(int c) { return ((c >> 4) << 4) + ((c & 7) << 1) + ((c >> 3) & 1); }
+
+template <int WZ, int WX, bool LINEAR>
 __global__ void __launch_bounds__(WZ *WX * 32)
 k_kk_gather(const KKArgs a) {
-    constexpr int TZ = 32 * WZ;
-    constexpr int TX = WX * PX;
+    constexpr int TZ = 8 * WZ;
+    constexpr int TX = 16 * WX;
     constexpr int NT = WZ * WX * 32;
+    constexpr int EPT = KKB_KK_STAGE_ELEMS / NT;  // staged window entries per thread
+    using Entry = typename std::conditional<LINEAR, float4, float2>::type;
     const int N = a.N, M = a.M, T = a.T, W = a.W, MCH = a.MCH, nx = a.nx, nz = a.nz;
     const int nchunk = (M + MCH - 1) / MCH;
     const int nstage = N * nchunk;
 
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    float2 *win = reinterpret_cast<float2 *>(smem_raw);              // [2][MCH][W]
-    double *lrz_s = reinterpret_cast<double *>(win + 2 * MCH * W);    // [M][TZ]
-    double *lrx_s = lrz_s + M * TZ;                                   // [M][TX]
-    double *ltx_s = lrx_s + M * TX;                                   // [N][TX]
-    float *w_s = reinterpret_cast<float *>(ltx_s + N * TX);           // [M]
-    int *lo_s = reinterpret_cast<int *>(w_s + M);                     // [3][MCH] (slot s % 3)
+    Entry *win = reinterpret_cast<Entry *>(smem_raw);                  // [2][MCH][W]
+    double *lrz_p = reinterpret_cast<double *>(win + 2 * MCH * W);     // [M][TZ] packed rows
+    double *lrx_p = lrz_p + M * TZ;                                    // [M][TX] packed cols
+    double *ltz_p = lrx_p + M * TX;                                    // [N][TZ]
+    double *ltx_p = ltz_p + N * TZ;                                    // [N][TX]
+    float *w_s = reinterpret_cast<float *>(ltx_p + N * TX);            // [M]
+    int *lo_s = reinterpret_cast<int *>(w_s + M);                      // [N][M]
 
     const int tid = threadIdx.x;
     const int f = blockIdx.z;
     const int ix0 = blockIdx.y * TX, iz0 = blockIdx.x * TZ;
     const int lane = tid & 31, warp = tid >> 5;
     const int wz = warp % WZ, wx = warp / WZ;
-    const int rz = wz * 32 + lane;
-    const int iz = iz0 + rz;
-    const int izc = min(iz, nz - 1);
-    const int cx = wx * PX;
-    const int cxb = min(TX - 1, nx - 1 - ix0);   // last valid local column
-    const int rzb = min(TZ - 1, nz - 1 - iz0);   // last valid local row
+    const int zt = lane & 3, xt = lane >> 2;
+    const int zq = wz * 4 + zt;   // packed row-pair slot (rows zq-> r, r+4)
+    const int xq = wx * 8 + xt;   // packed col-pair slot (cols c, c+8)
+    const int rzb = min(TZ - 1, nz - 1 - iz0);
+    const int cxb = min(TX - 1, nx - 1 - ix0);
 
     for (int i = tid; i < M * TZ; i += NT) {
         int m = i / TZ, r = i - m * TZ;
-        lrz_s[i] = a.lrzT[(long long)m * nz + min(iz0 + r, nz - 1)];
+        lrz_p[m * TZ + prow(r)] = a.lrzT[(long long)m * nz + min(iz0 + r, nz - 1)];
+    }
+    for (int i = tid; i < N * TZ; i += NT) {
+        int n = i / TZ, r = i - n * TZ;
+        ltz_p[n * TZ + prow(r)] = a.ltzT[(long long)n * nz + min(iz0 + r, nz - 1)];
     }
     for (int i = tid; i < M * TX; i += NT) {
         int m = i / TX, c = i - m * TX;
-        lrx_s[i] = a.lrx[(long long)min(ix0 + c, nx - 1) * M + m];
+        lrx_p[m * TX + pcol(c)] = a.lrx[(long long)min(ix0 + c, nx - 1) * M + m];
     }
     for (int i = tid; i < N * TX; i += NT) {
         int n = i / TX, c = i - n * TX;
-        ltx_s[i] = a.ltx[(long long)min(ix0 + c, nx - 1) * N + n];
+        ltx_p[n * TX + pcol(c)] = a.ltx[(long long)min(ix0 + c, nx - 1) * N + n];
     }
     for (int i = tid; i < M; i += NT) w_s[i] = a.w ? (float)a.w[i] : 1.0f;
     __syncthreads();
 
-    const float2 *dframe = a.data + (long long)f * a.data_fs;
     const double fs = a.fs, shift = a.shift;
-
-    // window start of stage s for its chunk-local receive index q (thread q computes)
-    auto stage_lo = [&](int s, int q) -> int {
-        int n = s / nchunk, m = (s - n * nchunk) * MCH + q;
+    // window start of every (n, m): floor of the smallest corner delay, minus 1
+    for (int i = tid; i < N * M; i += NT) {
+        const int n = i / M, m = i - n * M;
         double lo = 1e300;
-        double tza = a.ltzT[(long long)n * nz + iz0];
-        double tzb = a.ltzT[(long long)n * nz + iz0 + rzb];
-        double t1[4] = {__dadd_rn(ltx_s[n * TX], tza), __dadd_rn(ltx_s[n * TX], tzb),
-                        __dadd_rn(ltx_s[n * TX + cxb], tza), __dadd_rn(ltx_s[n * TX + cxb], tzb)};
-        double lz[4] = {lrz_s[m * TZ], lrz_s[m * TZ + rzb], lrz_s[m * TZ], lrz_s[m * TZ + rzb]};
-        double lx[4] = {lrx_s[m * TX], lrx_s[m * TX], lrx_s[m * TX + cxb], lrx_s[m * TX + cxb]};
 #pragma unroll
-        for (int c = 0; c < 4; ++c) lo = fmin(lo, kk_delay(t1[c], lz[c], lx[c], fs, shift));
-        lo = floor(lo) - 1.0;
-        lo = fmax(fmin(lo, 1.0e9), -1.0e9);
-        return (int)lo;
-    };
-    auto issue = [&](int s, int buf) {
-        int n = s / nchunk, m0 = (s - n * nchunk) * MCH;
-        int mc = min(MCH, M - m0);
-        const int *lo_q = lo_s + (s % 3) * MCH;
-        for (int i = tid; i < mc * W; i += NT) {
-            int q = i / W, e = i - q * W;
-            int smp = lo_q[q] + e;
-            bool ok = (unsigned)smp < (unsigned)T;
-            const float2 *src = dframe + ((long long)n * M + m0 + q) * T + (ok ? smp : 0);
-            cp_async8(&win[(buf * MCH + q) * W + e], src, ok);
-        }
-        cp_async_commit();
-    };
-
-    if (tid < min(MCH, M)) lo_s[tid] = stage_lo(0, tid);
-    __syncthreads();
-    issue(0, 0);
-
-    double accd_r[PX], accd_i[PX];
-    float accr[PX], acci[PX];
-    double t1[PX];
+        for (int cr = 0; cr < 2; ++cr)
 #pragma unroll
-    for (int j = 0; j < PX; ++j) {
-        accd_r[j] = accd_i[j] = 0.0;
-        accr[j] = acci[j] = 0.f;
+            for (int cc = 0; cc < 2; ++cc) {
+                const int r = cr ? rzb : 0, c = cc ? cxb : 0;
+                const double t1 = __dadd_rn(ltx_p[n * TX + pcol(c)], ltz_p[n * TZ + prow(r)]);
+                lo = fmin(lo, kk_delay(t1, lrz_p[m * TZ + prow(r)], lrx_p[m * TX + pcol(c)], fs, shift));
+            }
+        lo = fmax(fmin(floor(lo) - 1.0, 1.0e9), -1.0e9);
+        lo_s[i] = (int)lo;
     }
+    __syncthreads();
 
+    const float2 *dframe = a.data + (long long)f * a.data_fs;
+    // register-staged window entries of one stage
+    float2 s0[EPT], s1[EPT];
+    auto load_stage = [&](int s) {
+        const int n = s / nchunk, m0 = (s - n * nchunk) * MCH;
+        const int cnt = min(MCH, M - m0) * W;
+#pragma unroll
+        for (int i = 0; i < EPT; ++i) {
+            const int idx = tid + i * NT;
+            s0[i] = s1[i] = make_float2(0.f, 0.f);
+            if (idx < cnt) {
+                const int q = idx / W, e = idx - q * W;
+                const int smp = lo_s[n * M + m0 + q] + e;
+                const float2 *tr = dframe + ((long long)n * M + m0 + q) * T;
+                if ((unsigned)smp < (unsigned)T) s0[i] = __ldg(tr + smp);
+                if (LINEAR && (unsigned)(smp + 1) < (unsigned)T) s1[i] = __ldg(tr + smp + 1);
+            }
+        }
+    };
+    auto store_stage = [&](int s, int buf) {
+        const int n = s / nchunk, m0 = (s - n * nchunk) * MCH;
+        const int cnt = min(MCH, M - m0) * W;
+        Entry *wb = win + buf * MCH * W;
+#pragma unroll
+        for (int i = 0; i < EPT; ++i) {
+            const int idx = tid + i * NT;
+            if (idx < cnt) {
+                if constexpr (LINEAR) {
+                    // (2 d0 - d1, d1 - d0): the lerp becomes e0 + (1 + frac) * diff
+                    wb[idx] = make_float4(fmaf(2.f, s0[i].x, -s1[i].x), fmaf(2.f, s0[i].y, -s1[i].y),
+                                          s1[i].x - s0[i].x, s1[i].y - s0[i].y);
+                } else {
+                    wb[idx] = s0[i];
+                }
+            }
+        }
+    };
+
+    double accd_r[2][2], accd_i[2][2];
+    float accr[2][2], acci[2][2];
+    double t1[2][2];
+#pragma unroll
+    for (int p = 0; p < 2; ++p)
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+            accd_r[p][q] = accd_i[p][q] = 0.0;
+            accr[p][q] = acci[p][q] = 0.f;
+        }
+
+    load_stage(0);
+    store_stage(0, 0);
+    __syncthreads();
     for (int s = 0; s < nstage; ++s) {
         const int buf = s & 1;
         const int n = s / nchunk, ch = s - n * nchunk, m0 = ch * MCH;
         const int mc = min(MCH, M - m0);
-        // window starts of stage s+1 go to slot (s+1)%3: slot (s-2)%3 was last read
-        // before the previous iteration's first barrier, so no reader remains
-        if (s + 1 < nstage) {
-            int n1 = (s + 1) / nchunk, m1 = ((s + 1) - n1 * nchunk) * MCH;
-            if (tid < min(MCH, M - m1)) lo_s[((s + 1) % 3) * MCH + tid] = stage_lo(s + 1, tid);
-        }
-        __syncthreads();
-        if (s + 1 < nstage) {
-            issue(s + 1, buf ^ 1);
-            cp_async_wait<1>();
-        } else {
-            cp_async_wait<0>();
-        }
-        __syncthreads();
-
+        if (s + 1 < nstage) load_stage(s + 1);  // in flight during this stage's sums
         if (ch == 0) {
-            double tz = a.ltzT[(long long)n * nz + izc];
-#pragma unroll
-            for (int j = 0; j < PX; ++j) t1[j] = __dadd_rn(ltx_s[n * TX + min(cx + j, cxb)], tz);
+            const double2 tz = reinterpret_cast<const double2 *>(ltz_p + n * TZ)[zq];
+            const double2 tx = reinterpret_cast<const double2 *>(ltx_p + n * TX)[xq];
+            t1[0][0] = __dadd_rn(tx.x, tz.x);
+            t1[0][1] = __dadd_rn(tx.y, tz.x);
+            t1[1][0] = __dadd_rn(tx.x, tz.y);
+            t1[1][1] = __dadd_rn(tx.y, tz.y);
         }
-        const float2 *wb = win + buf * MCH * W;
+        const Entry *wb = win + buf * MCH * W;
+        const int *lo_n = lo_s + n * M + m0;
         for (int q = 0; q < mc; ++q) {
             const int m = m0 + q;
-            const double lz = lrz_s[m * TZ + min(rz, rzb)];
+            const double2 lz = reinterpret_cast<const double2 *>(lrz_p + m * TZ)[zq];
+            const double2 lx = reinterpret_cast<const double2 *>(lrx_p + m * TX)[xq];
             const float wm = w_s[m];
-            const int lo = lo_s[(s % 3) * MCH + q];
-            const float2 *wv = wb + q * W;
+            const int lo = lo_n[q];
+            const Entry *wv = wb + q * W;
 #pragma unroll
-            for (int j = 0; j < PX; ++j) {
-                const double lx = lrx_s[m * TX + min(cx + j, cxb)];
-                const double fi = kk_delay(t1[j], lz, lx, fs, shift);
-                int F;
-                double y;
-                if (tap_index<LINEAR>(fi, T, F, y)) {
-                    if (LINEAR) {
-                        const int e = min(max(F - lo, 0), W - 2);
-                        const float2 d0 = wv[e], d1 = wv[e + 1];
-                        const float fr = frac_from_floor(fi, y);
-                        const float vr = fmaf(fr, d1.x - d0.x, d0.x);
-                        const float vi = fmaf(fr, d1.y - d0.y, d0.y);
-                        accr[j] = fmaf(wm, vr, accr[j]);
-                        acci[j] = fmaf(wm, vi, acci[j]);
+            for (int p = 0; p < 2; ++p) {
+#pragma unroll
+                for (int r = 0; r < 2; ++r) {
+                    const double fi = kk_delay(t1[p][r], p ? lz.y : lz.x, r ? lx.y : lx.x, fs, shift);
+                    // s = RD(arg + 1.5*2^20): high word - 0x41380000 = floor(arg), low word = frac * 2^32
+                    const double sv = __dadd_rd(LINEAR ? fi : __dadd_rn(fi, 0.5), KKB_FLOOR_MAGIC2);
+                    const int F = __double2hiint(sv) - KKB_MAGIC2_HI;
+                    const bool ok = (unsigned)F <= (unsigned)(LINEAR ? T - 2 : T - 1);
+                    const unsigned e = min((unsigned)(F - lo), (unsigned)(LINEAR ? W - 2 : W - 1));
+                    const float we = ok ? wm : 0.f;
+                    if constexpr (LINEAR) {
+                        const float4 v = wv[e];
+                        const float f1 = __uint_as_float(((unsigned)__double2loint(sv) >> 9) + 0x3F800000u);
+                        accr[p][r] = fmaf(we, fmaf(f1, v.z, v.x), accr[p][r]);
+                        acci[p][r] = fmaf(we, fmaf(f1, v.w, v.y), acci[p][r]);
                     } else {
-                        const float2 d = wv[min(max(F - lo, 0), W - 1)];
-                        accr[j] = fmaf(wm, d.x, accr[j]);
-                        acci[j] = fmaf(wm, d.y, acci[j]);
+                        const float2 v = wv[e];
+                        accr[p][r] = fmaf(we, v.x, accr[p][r]);
+                        acci[p][r] = fmaf(we, v.y, acci[p][r]);
                     }
                 }
             }
         }
         if (ch == nchunk - 1) {
 #pragma unroll
-            for (int j = 0; j < PX; ++j) {
-                accd_r[j] += (double)accr[j];
-                accd_i[j] += (double)acci[j];
-                accr[j] = acci[j] = 0.f;
-            }
+            for (int p = 0; p < 2; ++p)
+#pragma unroll
+                for (int r = 0; r < 2; ++r) {
+                    accd_r[p][r] += (double)accr[p][r];
+                    accd_i[p][r] += (double)acci[p][r];
+                    accr[p][r] = acci[p][r] = 0.f;
+                }
         }
+        // buffer buf^1 was last read in stage s-1, which every thread finished
+        // before the barrier that ended it
+        if (s + 1 < nstage) store_stage(s + 1, buf ^ 1);
+        __syncthreads();
     }
 
     // epilogue: IQ (+ fused intensity and frame max)
     float fmx = 0.f;
-    if (iz < nz) {
 #pragma unroll
-        for (int j = 0; j < PX; ++j) {
-            const int ix = ix0 + cx + j;
-            if (ix < nx) {
-                const long long p = (long long)f * a.out_fs + (long long)ix * nz + iz;
+    for (int p = 0; p < 2; ++p) {
+        const int iz = iz0 + wz * 8 + p * 4 + zt;
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+            const int ix = ix0 + wx * 16 + r * 8 + xt;
+            if (iz < nz && ix < nx) {
+                const long long px = (long long)f * a.out_fs + (long long)ix * nz + iz;
                 if (a.out_kind == KKB_OUT_C128) {
-                    reinterpret_cast<double2 *>(a.out)[p] = make_double2(accd_r[j], accd_i[j]);
+                    reinterpret_cast<double2 *>(a.out)[px] = make_double2(accd_r[p][r], accd_i[p][r]);
                 } else {
-                    reinterpret_cast<float2 *>(a.out)[p] =
-                        make_float2((float)accd_r[j], (float)accd_i[j]);
+                    reinterpret_cast<float2 *>(a.out)[px] =
+                        make_float2((float)accd_r[p][r], (float)accd_i[p][r]);
                 }
                 if (a.inten) {
-                    float I = (float)(accd_r[j] * accd_r[j] + accd_i[j] * accd_i[j]);
-                    a.inten[p] = I;
+                    float I = (float)(accd_r[p][r] * accd_r[p][r] + accd_i[p][r] * accd_i[p][r]);
+                    a.inten[px] = I;
                     fmx = fmaxf(fmx, I);
                 }
             }
         }
     }
     if (a.fmax) {
-        // warp max, then one atomic per warp (non-negative floats order as uints)
         for (int o = 16; o > 0; o >>= 1) fmx = fmaxf(fmx, __shfl_xor_sync(0xffffffffu, fmx, o));
         if (lane == 0) atomicMax(a.fmax + f, __float_as_uint(fmx));
     }
 }
 
-static size_t kk_smem_bytes(int N, int M, int W, int MCH) {
-    return sizeof(float2) * 2 * MCH * W + sizeof(double) * ((size_t)M * KKB_KK_TZ + (size_t)M * KKB_KK_TX +
-                                                            (size_t)N * KKB_KK_TX) +
-           sizeof(float) * M + sizeof(int) * 3 * MCH;
+static size_t kk_smem_bytes(int N, int M, int W, int MCH, bool linear) {
+    size_t entry = linear ? sizeof(float4) : sizeof(float2);
+    return entry * 2 * MCH * W +
+           sizeof(double) * ((size_t)(M + N) * KKB_KK_TZ + (size_t)(M + N) * KKB_KK_TX) +
+           sizeof(float) * M + sizeof(int) * (size_t)N * M;
 }
 
 int kk_gather(const float2 *data, int N, int M, int T, const double *ltx, const double *ltzT,
@@ -440,11 +477,15 @@ int kk_gather(const float2 *data, int N, int M, int T, const double *ltx, const 
               long long out_fs, float *inten, unsigned *fmax, int W, cudaStream_t s) {
     if (n_frames <= 0 || nx <= 0 || nz <= 0) return KKB_OK;
     if (W < 2) W = 2;
-    // receive angles per stage: as many as fit a ~96 KB double buffer
-    const size_t budget = 200 * 1024;
-    int MCH = M;
-    while (MCH > 1 && kk_smem_bytes(N, M, W, MCH) > budget) MCH = (MCH + 1) / 2;
-    size_t sm = kk_smem_bytes(N, M, W, MCH);
+    if (W > KKB_KK_STAGE_ELEMS) {
+        set_error("kk: trace window of %d samples per tile exceeds %d (delay tables too steep "
+                  "for the %dx%d tile)", W, KKB_KK_STAGE_ELEMS, KKB_KK_TZ, KKB_KK_TX);
+        return KKB_ERR_UNSUPPORTED;
+    }
+    // receive angles per stage: bounded by the register staging and shared memory
+    int MCH = std::max(1, std::min(M, KKB_KK_STAGE_ELEMS / W));
+    while (MCH > 1 && kk_smem_bytes(N, M, W, MCH, linear) > 200 * 1024) MCH = (MCH + 1) / 2;
+    size_t sm = kk_smem_bytes(N, M, W, MCH, linear);
     if (sm > 227 * 1024) {
         set_error("kk tile needs %zu B of shared memory (N=%d M=%d window=%d)", sm, N, M, W);
         return KKB_ERR_UNSUPPORTED;
@@ -454,12 +495,12 @@ int kk_gather(const float2 *data, int N, int M, int T, const double *ltx, const 
     dim3 grid((unsigned)ceil_div(nz, KKB_KK_TZ), (unsigned)ceil_div(nx, KKB_KK_TX), (unsigned)n_frames);
     dim3 block(KKB_KK_WZ * KKB_KK_WX * 32);
     if (linear) {
-        auto fn = k_kk_gather<KKB_KK_WZ, KKB_KK_WX, KKB_KK_PX, true>;
+        auto fn = k_kk_gather<KKB_KK_WZ, KKB_KK_WX, true>;
         KKB_TRY_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm),
                      "smem attr kk");
         fn<<<grid, block, sm, s>>>(a);
     } else {
-        auto fn = k_kk_gather<KKB_KK_WZ, KKB_KK_WX, KKB_KK_PX, false>;
+        auto fn = k_kk_gather<KKB_KK_WZ, KKB_KK_WX, false>;
         KKB_TRY_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm),
                      "smem attr kk");
         fn<<<grid, block, sm, s>>>(a);
