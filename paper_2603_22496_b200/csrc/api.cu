@@ -342,7 +342,7 @@ extern "C" int kkb_shear_and_sum(const void *data, int n_tx, int n_el, int n_t,
 // =====================================================================
 // fused stage-1 plan
 struct kkb_decomposer {
-    int N, L, T, M, K, chunk;
+    int N, L, T, M, K, ldk, chunk;  // ldk: spectral row stride (K rounded up to even)
     float2 *ramps = nullptr;
     float2 *X = nullptr;
     float2 *Y = nullptr;
@@ -371,8 +371,9 @@ extern "C" int kkb_decomposer_create(int n_tx, int n_el, int n_t, const double *
     p->T = n_t;
     p->M = n_rx;
     p->K = n_t / 2 + 1;
+    p->ldk = p->K + (p->K & 1);
     p->chunk = max_frames;
-    const int K = p->K;
+    const int K = p->K, ldk = p->ldk;
     std::vector<double> tau((size_t)n_el * n_rx), freq(K), scale(K);
     for (int m = 0; m < n_rx; ++m) {
         double q = sin(angles_host[m]) / c;
@@ -382,9 +383,9 @@ extern "C" int kkb_decomposer_create(int n_tx, int n_el, int n_t, const double *
         freq[k] = fftfreq(k, n_t, fs);
         scale[k] = one_sided(k, n_t) / n_t;
     }
-    size_t rb = sizeof(float2) * (size_t)n_rx * n_el * K;
-    size_t xb = sizeof(float2) * (size_t)max_frames * n_tx * n_el * K;
-    size_t yb = sizeof(float2) * (size_t)max_frames * n_tx * n_rx * K;
+    size_t rb = sizeof(float2) * (size_t)n_rx * n_el * ldk;
+    size_t xb = sizeof(float2) * (size_t)max_frames * n_tx * n_el * ldk;
+    size_t yb = sizeof(float2) * (size_t)max_frames * n_tx * n_rx * ldk;
     cudaError_t e;
     if ((e = cudaMalloc(&p->ramps, rb)) || (e = cudaMalloc(&p->X, xb)) || (e = cudaMalloc(&p->Y, yb))) {
         cudaFree(p->ramps);
@@ -394,7 +395,10 @@ extern "C" int kkb_decomposer_create(int n_tx, int n_el, int n_t, const double *
         return cuda_status(e, "cudaMalloc(decomposer)");
     }
     p->bytes = (long long)(rb + xb + yb);
-    st = build_ramps(tau.data(), n_el, n_rx, freq.data(), scale.data(), K, p->ramps, 0);
+    // ramps at row stride ldk: build K bins (+1 zero pad bin when K is odd)
+    freq.resize(ldk, 0.0);
+    scale.resize(ldk, 0.0);
+    st = build_ramps(tau.data(), n_el, n_rx, freq.data(), scale.data(), ldk, p->ramps, 0);
     if (st) {
         cudaFree(p->ramps);
         cudaFree(p->X);
@@ -412,15 +416,15 @@ extern "C" int kkb_decomposer_run(kkb_decomposer *p, const float *rf, int n_fram
                                   void *stream) {
     if (!p || n_frames < 0) return KKB_ERR_ARG;
     cudaStream_t s = as_stream(stream);
-    const int N = p->N, L = p->L, T = p->T, M = p->M, K = p->K;
+    const int N = p->N, L = p->L, T = p->T, M = p->M, K = p->K, ldk = p->ldk;
     for (int f0 = 0; f0 < n_frames; f0 += p->chunk) {
         int F = std::min(p->chunk, n_frames - f0);
         const float *rf_c = rf + (size_t)f0 * N * L * T;
         float2 *tr_c = (float2 *)traces + (size_t)f0 * N * M * T;
         int st;
-        if ((st = fft_r2c(rf_c, (long long)F * N * L, T, p->X, K, K, nullptr, s, nullptr))) return st;
-        if ((st = contract(p->X, K, p->ramps, K, p->Y, K, (long long)F * N, L, M, K, s))) return st;
-        if ((st = fft_c2c(p->Y, K, K, tr_c, T, T, (long long)F * N * M, T, true, 1.0f, s))) return st;
+        if ((st = fft_r2c(rf_c, (long long)F * N * L, T, p->X, ldk, K, nullptr, s, nullptr))) return st;
+        if ((st = contract(p->X, ldk, p->ramps, ldk, p->Y, ldk, (long long)F * N, L, M, K, s))) return st;
+        if ((st = fft_c2c(p->Y, ldk, K, tr_c, T, T, (long long)F * N * M, T, true, 1.0f, s))) return st;
     }
     return KKB_OK;
 }

@@ -81,8 +81,15 @@ __device__ __forceinline__ void cp_async8z(void *smem_dst, const void *gsrc, boo
                  : "memory");
 }
 
+__device__ __forceinline__ void cp_async16z(void *smem_dst, const void *gsrc, bool valid) {
+    unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
+    int sz = valid ? 16 : 0;
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(gsrc), "r"(sz)
+                 : "memory");
+}
+
 template <int MC>
-__global__ void __launch_bounds__(KKB_CT_THREADS)
+__global__ void __launch_bounds__(KKB_CT_THREADS, MC <= 12 ? 2 : 1)
 k_contract(const float2 *__restrict__ X, long long ldx, const float2 *__restrict__ R,
            long long ldr, float2 *__restrict__ Y, long long ldy, long long B, int L, int M, int Kb) {
     constexpr int KT = KKB_CT_KT, BT = KKB_CT_BT, NB = KKB_CT_NB, LC = KKB_CT_LC;
@@ -96,22 +103,56 @@ k_contract(const float2 *__restrict__ X, long long ldx, const float2 *__restrict
     const int m0 = blockIdx.z * MC;
     const int nlc = (L + LC - 1) / LC;
 
+    // 16-byte copies (2 bins) when the row strides are even; otherwise 8-byte
+    const bool wide = ((ldx | ldr) & 1) == 0;
+    // wide path: thread copies bins (2kc, 2kc+1) of rows bbA = tid/16 and bbA+16 for
+    // each of the LC elements, and of R rows (j, ll) = divmod(tid/16 + 16*it, LC)
+    constexpr int RROWS = LC * MC;                       // R rows per stage
+    constexpr int RIT = (RROWS + 15) / 16;               // R copies per thread
+    const int kc = tid & 15, bbA = tid >> 4;
+    const int kw = k0 + 2 * kc;
+    const bool kok = kw < Kb;
+    const float2 *xA = X + ((b0 + bbA) * L) * ldx + kw;
+    const float2 *xB = xA + (long long)16 * L * ldx;
+    const bool okA = kok && b0 + bbA < B, okB = kok && b0 + bbA + 16 < B;
     auto stage = [&](int c, int buf) {
         const int l0 = c * LC;
-        for (int i = tid; i < LC * BT * KT; i += KKB_CT_THREADS) {
-            int kk = i % KT, r = i / KT, bb = r % BT, ll = r / BT;
-            long long b = b0 + bb;
-            int l = l0 + ll, k = k0 + kk;
-            bool ok = b < B && l < L && k < Kb;
-            const float2 *src = ok ? X + (b * L + l) * ldx + k : X;
-            cp_async8z(&Xs[((buf * LC + ll) * BT + bb) * KT + kk], src, ok);
-        }
-        for (int i = tid; i < LC * MC * KT; i += KKB_CT_THREADS) {
-            int kk = i % KT, r = i / KT, j = r % MC, ll = r / MC;
-            int m = m0 + j, l = l0 + ll, k = k0 + kk;
-            bool ok = m < M && l < L && k < Kb;
-            const float2 *src = ok ? R + ((long long)m * L + l) * ldr + k : R;
-            cp_async8z(&Rs[((buf * LC + ll) * MC + j) * KT + kk], src, ok);
+        if (wide) {
+            float2 *xs = Xs + buf * LC * BT * KT + bbA * KT + 2 * kc;
+#pragma unroll
+            for (int ll = 0; ll < LC; ++ll) {
+                const bool lok = l0 + ll < L;
+                const long long off = (long long)(l0 + ll) * ldx;
+                cp_async16z(xs + ll * BT * KT, okA && lok ? xA + off : X, okA && lok);
+                cp_async16z(xs + ll * BT * KT + 16 * KT, okB && lok ? xB + off : X, okB && lok);
+            }
+#pragma unroll
+            for (int it = 0; it < RIT; ++it) {
+                const int rr = bbA + 16 * it;
+                if (rr < RROWS) {
+                    const int ll = rr / MC, j = rr - ll * MC;
+                    const int m = m0 + j, l = l0 + ll;
+                    const bool ok = kok && m < M && l < L;
+                    const float2 *src = ok ? R + ((long long)m * L + l) * ldr + kw : R;
+                    cp_async16z(&Rs[((buf * LC + ll) * MC + j) * KT + 2 * kc], src, ok);
+                }
+            }
+        } else {
+            for (int i = tid; i < LC * BT * KT; i += KKB_CT_THREADS) {
+                const int kk = i % KT, rr = i / KT, bb = rr % BT, ll = rr / BT;
+                const long long b = b0 + bb;
+                const int l = l0 + ll, k = k0 + kk;
+                const bool ok = b < B && l < L && k < Kb;
+                const float2 *src = ok ? X + (b * L + l) * ldx + k : X;
+                cp_async8z(&Xs[((buf * LC + ll) * BT + bb) * KT + kk], src, ok);
+            }
+            for (int i = tid; i < LC * MC * KT; i += KKB_CT_THREADS) {
+                const int kk = i % KT, rr = i / KT, j = rr % MC, ll = rr / MC;
+                const int m = m0 + j, l = l0 + ll, k = k0 + kk;
+                const bool ok = m < M && l < L && k < Kb;
+                const float2 *src = ok ? R + ((long long)m * L + l) * ldr + k : R;
+                cp_async8z(&Rs[((buf * LC + ll) * MC + j) * KT + kk], src, ok);
+            }
         }
         asm volatile("cp.async.commit_group;\n" ::: "memory");
     };

@@ -171,6 +171,8 @@ __device__ __noinline__ void dft_generic(float2 *v, int R, const float2 *__restr
 // so k = j mod Ns is a mask there.  Returns the buffer holding the result.
 __device__ float2 *stockham(float2 *a, float2 *b, int G, const FftPlan &p, const float2 *tw) {
     const int T = p.T;
+    const int sw = (T & 15) == 0 ? 15 : 0;  // XOR swizzle of the low 4 index bits (bank spread)
+#define SW(e) ((e) ^ (((e) >> 3) & sw))
     int Ns = 1;
     for (int s = 0; s < p.nstages; ++s) {
         const int R = p.radix[s];
@@ -189,12 +191,12 @@ __device__ float2 *stockham(float2 *a, float2 *b, int G, const FftPlan &p, const
                     float2 *dst = b + g * T;
                     float2 v[8];
 #pragma unroll
-                    for (int r = 0; r < 8; ++r) v[r] = src[j + r * TR];
+                    for (int r = 0; r < 8; ++r) v[r] = src[SW(j + r * TR)];
 #pragma unroll
                     for (int r = 1; r < 8; ++r) v[r] = cmul(v[r], w[r]);
                     dft8(v);
 #pragma unroll
-                    for (int r = 0; r < 8; ++r) dst[base + r * Ns] = v[r];
+                    for (int r = 0; r < 8; ++r) dst[SW(base + r * Ns)] = v[r];
                 }
             } else if (R == 4) {
                 float2 w[4];
@@ -205,32 +207,32 @@ __device__ float2 *stockham(float2 *a, float2 *b, int G, const FftPlan &p, const
                     float2 *dst = b + g * T;
                     float2 v[4];
 #pragma unroll
-                    for (int r = 0; r < 4; ++r) v[r] = src[j + r * TR];
+                    for (int r = 0; r < 4; ++r) v[r] = src[SW(j + r * TR)];
 #pragma unroll
                     for (int r = 1; r < 4; ++r) v[r] = cmul(v[r], w[r]);
                     dft4(v);
 #pragma unroll
-                    for (int r = 0; r < 4; ++r) dst[base + r * Ns] = v[r];
+                    for (int r = 0; r < 4; ++r) dst[SW(base + r * Ns)] = v[r];
                 }
             } else if (R == 2) {
                 const float2 w1 = tw[k * tws];
                 for (int g = 0; g < G; ++g) {
                     const float2 *src = a + g * T;
                     float2 *dst = b + g * T;
-                    float2 v0 = src[j], v1 = cmul(src[j + TR], w1);
+                    float2 v0 = src[SW(j)], v1 = cmul(src[SW(j + TR)], w1);
                     dft2(v0, v1);
-                    dst[base] = v0;
-                    dst[base + Ns] = v1;
+                    dst[SW(base)] = v0;
+                    dst[SW(base + Ns)] = v1;
                 }
             } else if (R == 3) {
                 const float2 w1 = tw[k * tws], w2 = tw[2 * k * tws];
                 for (int g = 0; g < G; ++g) {
                     const float2 *src = a + g * T;
                     float2 *dst = b + g * T;
-                    float2 v[3] = {src[j], cmul(src[j + TR], w1), cmul(src[j + 2 * TR], w2)};
+                    float2 v[3] = {src[SW(j)], cmul(src[SW(j + TR)], w1), cmul(src[SW(j + 2 * TR)], w2)};
                     dft3(v);
 #pragma unroll
-                    for (int r = 0; r < 3; ++r) dst[base + r * Ns] = v[r];
+                    for (int r = 0; r < 3; ++r) dst[SW(base + r * Ns)] = v[r];
                 }
             } else if (R == 5) {
                 float2 w[5];
@@ -241,21 +243,21 @@ __device__ float2 *stockham(float2 *a, float2 *b, int G, const FftPlan &p, const
                     float2 *dst = b + g * T;
                     float2 v[5];
 #pragma unroll
-                    for (int r = 0; r < 5; ++r) v[r] = src[j + r * TR];
+                    for (int r = 0; r < 5; ++r) v[r] = src[SW(j + r * TR)];
 #pragma unroll
                     for (int r = 1; r < 5; ++r) v[r] = cmul(v[r], w[r]);
                     dft5(v);
 #pragma unroll
-                    for (int r = 0; r < 5; ++r) dst[base + r * Ns] = v[r];
+                    for (int r = 0; r < 5; ++r) dst[SW(base + r * Ns)] = v[r];
                 }
             } else {
                 for (int g = 0; g < G; ++g) {
                     const float2 *src = a + g * T;
                     float2 *dst = b + g * T;
                     float2 v[KKB_FFT_MAX_RADIX];
-                    for (int r = 0; r < R; ++r) v[r] = cmul(src[j + r * TR], tw[r * k * tws]);
+                    for (int r = 0; r < R; ++r) v[r] = cmul(src[SW(j + r * TR)], tw[r * k * tws]);
                     dft_generic(v, R, tw, T);
-                    for (int r = 0; r < R; ++r) dst[base + r * Ns] = v[r];
+                    for (int r = 0; r < R; ++r) dst[SW(base + r * Ns)] = v[r];
                 }
             }
         }
@@ -265,8 +267,12 @@ __device__ float2 *stockham(float2 *a, float2 *b, int G, const FftPlan &p, const
         b = t;
         Ns *= R;
     }
+#undef SW
     return a;
 }
+
+// Index of logical element t of a trace buffer (the swizzle stockham uses).
+__device__ __forceinline__ int fft_sw(int t, int T) { return (T & 15) == 0 ? t ^ ((t >> 3) & 15) : t; }
 
 // ------------------------------------------------------------- kernels
 __device__ __forceinline__ void load_twiddles(float2 *tw_s, const FftPlan &p) {
@@ -295,7 +301,7 @@ k_fft_c2c(const float2 *__restrict__ in, long long in_stride, int in_len,
         for (int t = threadIdx.x; t < T; t += blockDim.x) {
             float2 v = make_float2(0.f, 0.f);
             if (live && t < in_len) v = row[t];
-            a[g * T + t] = make_float2(v.x, sgn * v.y);
+            a[g * T + fft_sw(t, T)] = make_float2(v.x, sgn * v.y);
         }
     }
     __syncthreads();
@@ -306,7 +312,7 @@ k_fft_c2c(const float2 *__restrict__ in, long long in_stride, int in_len,
         if (tr >= ntraces) break;
         float2 *row = out + tr * out_stride;
         for (int t = threadIdx.x; t < out_len; t += blockDim.x) {
-            const float2 v = res[g * T + t];
+            const float2 v = res[g * T + fft_sw(t, T)];
             row[t] = make_float2(v.x * scale, v.y * sy);
         }
     }
@@ -336,15 +342,15 @@ k_fft_r2c_pairs(const float *__restrict__ in, long long ntraces, float2 *__restr
             for (int t = 4 * threadIdx.x; t < T; t += 4 * blockDim.x) {
                 float4 u = l0 ? __ldg(reinterpret_cast<const float4 *>(x0 + t)) : make_float4(0, 0, 0, 0);
                 float4 w = l1 ? __ldg(reinterpret_cast<const float4 *>(x1 + t)) : make_float4(0, 0, 0, 0);
-                float2 *d = a + g * T + t;
-                d[0] = make_float2(u.x, w.x);
-                d[1] = make_float2(u.y, w.y);
-                d[2] = make_float2(u.z, w.z);
-                d[3] = make_float2(u.w, w.w);
+                float2 *d = a + g * T;
+                d[fft_sw(t, T)] = make_float2(u.x, w.x);
+                d[fft_sw(t + 1, T)] = make_float2(u.y, w.y);
+                d[fft_sw(t + 2, T)] = make_float2(u.z, w.z);
+                d[fft_sw(t + 3, T)] = make_float2(u.w, w.w);
             }
         } else {
             for (int t = threadIdx.x; t < T; t += blockDim.x)
-                a[g * T + t] = make_float2(l0 ? x0[t] : 0.f, l1 ? x1[t] : 0.f);
+                a[g * T + fft_sw(t, T)] = make_float2(l0 ? x0[t] : 0.f, l1 ? x1[t] : 0.f);
         }
     }
     __syncthreads();
@@ -356,8 +362,8 @@ k_fft_r2c_pairs(const float *__restrict__ in, long long ntraces, float2 *__restr
         float2 *o0 = out + r0 * out_stride;
         float2 *o1 = out + (r0 + 1) * out_stride;
         for (int k = threadIdx.x; k < K; k += blockDim.x) {
-            const float2 zk = res[g * T + k];
-            const float2 zn = res[g * T + (k == 0 ? 0 : T - k)];
+            const float2 zk = res[g * T + fft_sw(k, T)];
+            const float2 zn = res[g * T + fft_sw(k == 0 ? 0 : T - k, T)];
             const float s = bin_scale ? bin_scale[k] : 1.0f;
             // X0 = (Z_k + conj(Z_-k)) / 2 ; X1 = (Z_k - conj(Z_-k)) / (2i)
             o0[k] = make_float2(0.5f * s * (zk.x + zn.x), 0.5f * s * (zk.y - zn.y));

@@ -9,7 +9,8 @@
 #define KKB_KK_WX 2
 #define KKB_KK_TZ (8 * KKB_KK_WZ)
 #define KKB_KK_TX (16 * KKB_KK_WX)
-#define KKB_KK_STAGE_ELEMS 2048  // window entries staged per pipeline stage
+#define KKB_KK_STAGE_ELEMS 1024  // window entries staged per pipeline stage
+#define KKB_KK_MIN_CTAS 3        // occupancy target (caps registers at 85)
 
 namespace kkb {
 

@@ -122,13 +122,18 @@ __device__ __forceinline__ double kk_delay(double t1, double lz, double lx, doub
 
 // Tap index of one (pixel, pair): linear i0 = floor(fi) valid iff 0 <= i0 <= T-2,
 // nearest j = floor(fi + 0.5) valid iff 0 <= j <= T-1 (beamform.py:226-235).
-// y = RD(arg + 1.5*2^52) is returned for the lerp weight.
+// sv = RD(arg + 1.5*2^20) (arg = fi, or RN(fi + 0.5) for nearest): for
+// |arg| < 2^19 its high word minus 0x41380000 is floor(arg) exactly (the
+// round-down never crosses an integer) and its low word is frac(arg)*2^32;
+// any larger |arg| gives F >= 2^19 or F < 0, i.e. out of window.  This one
+// function is the index math of the K5 gather and of kkb_kk_taps.
+#define KKB_FLOOR_MAGIC2 1572864.0   // 1.5 * 2^20: ulp 2^-32
+#define KKB_MAGIC2_HI 0x41380000     // high word of 1.5*2^20 + 0
 template <bool LINEAR>
-__device__ __forceinline__ bool tap_index(double fi, int T, int &F, double &y) {
-    y = __dadd_rd(LINEAR ? fi : __dadd_rn(fi, 0.5), KKB_FLOOR_MAGIC);
-    F = __double2loint(y);
-    return (__double2hiint(y) == KKB_MAGIC_HI) &&
-           ((unsigned)F <= (unsigned)(LINEAR ? T - 2 : T - 1));
+__device__ __forceinline__ bool tap_index(double fi, int T, int &F, double &sv) {
+    sv = __dadd_rd(LINEAR ? fi : __dadd_rn(fi, 0.5), KKB_FLOOR_MAGIC2);
+    F = __double2hiint(sv) - KKB_MAGIC2_HI;
+    return (unsigned)F <= (unsigned)(LINEAR ? T - 2 : T - 1);
 }
 
 // Diagnostic twin of the gather's index math: idx[ix, iz, n, m] = tap index or -1.
@@ -223,9 +228,6 @@ int kk_window(const double *ltx, const double *ltz, const double *lrx, const dou
 // rows zt + {0, 4}, columns xt + {0, 8} of it.  For a fixed (a, b) the 32
 // lanes form a 4 x 8 block whose delays span only ~3*dfi/dz + 7*dfi/dx
 // samples, so their tap reads hit a few shared-memory words (broadcast).
-#define KKB_FLOOR_MAGIC2 1572864.0   // 1.5 * 2^20: ulp 2^-32, |fi| < 2^19
-#define KKB_MAGIC2_HI 0x41380000     // high word of 1.5*2^20 + 0
-
 struct KKArgs {
     const float2 *data;
     long long data_fs;  // frame stride, complex elements
@@ -252,7 +254,7 @@ __device__ __forceinline__ int prow(int r) { return ((r >> 3) << 3) + ((r & 3) <
 __device__ __forceinline__ int pcol(int c) { return ((c >> 4) << 4) + ((c & 7) << 1) + ((c >> 3) & 1); }
 
 template <int WZ, int WX, bool LINEAR>
-__global__ void __launch_bounds__(WZ *WX * 32)
+__global__ void __launch_bounds__(WZ *WX * 32, KKB_KK_MIN_CTAS)
 k_kk_gather(const KKArgs a) {
     constexpr int TZ = 8 * WZ;
     constexpr int TX = 16 * WX;
@@ -321,26 +323,34 @@ k_kk_gather(const KKArgs a) {
     __syncthreads();
 
     const float2 *dframe = a.data + (long long)f * a.data_fs;
-    // register-staged window entries of one stage
+    // register-staged window entries of one stage; entry tid + i*NT of a stage
+    // is (receive q, sample e) = divmod(tid + i*NT, W), the same every stage
     float2 s0[EPT], s1[EPT];
-    auto load_stage = [&](int s) {
-        const int n = s / nchunk, m0 = (s - n * nchunk) * MCH;
+    int qe[EPT];
+#pragma unroll
+    for (int i = 0; i < EPT; ++i) {
+        const int idx = tid + i * NT, q = idx / W;
+        qe[i] = (q << 16) | (idx - q * W);
+    }
+    // stage (n, m0): receive angles m0 .. m0+mc-1 of transmit n
+    auto load_stage = [&](int n, int m0) {
         const int cnt = min(MCH, M - m0) * W;
+        const float2 *base = dframe + (long long)(n * M + m0) * T;
+        const int *lo_q = lo_s + n * M + m0;
 #pragma unroll
         for (int i = 0; i < EPT; ++i) {
             const int idx = tid + i * NT;
             s0[i] = s1[i] = make_float2(0.f, 0.f);
             if (idx < cnt) {
-                const int q = idx / W, e = idx - q * W;
-                const int smp = lo_s[n * M + m0 + q] + e;
-                const float2 *tr = dframe + ((long long)n * M + m0 + q) * T;
+                const int q = qe[i] >> 16, e = qe[i] & 0xFFFF;
+                const int smp = lo_q[q] + e;
+                const float2 *tr = base + q * T;
                 if ((unsigned)smp < (unsigned)T) s0[i] = __ldg(tr + smp);
                 if (LINEAR && (unsigned)(smp + 1) < (unsigned)T) s1[i] = __ldg(tr + smp + 1);
             }
         }
     };
-    auto store_stage = [&](int s, int buf) {
-        const int n = s / nchunk, m0 = (s - n * nchunk) * MCH;
+    auto store_stage = [&](int m0, int buf) {
         const int cnt = min(MCH, M - m0) * W;
         Entry *wb = win + buf * MCH * W;
 #pragma unroll
@@ -369,14 +379,22 @@ k_kk_gather(const KKArgs a) {
             accr[p][q] = acci[p][q] = 0.f;
         }
 
-    load_stage(0);
+    load_stage(0, 0);
     store_stage(0, 0);
     __syncthreads();
+    int n = 0, ch = 0;           // current stage
+    int n1 = 0, ch1 = 0;         // next stage
     for (int s = 0; s < nstage; ++s) {
         const int buf = s & 1;
-        const int n = s / nchunk, ch = s - n * nchunk, m0 = ch * MCH;
+        const int m0 = ch * MCH;
         const int mc = min(MCH, M - m0);
-        if (s + 1 < nstage) load_stage(s + 1);  // in flight during this stage's sums
+        n1 = n;
+        ch1 = ch + 1;
+        if (ch1 == nchunk) {
+            ch1 = 0;
+            ++n1;
+        }
+        if (s + 1 < nstage) load_stage(n1, ch1 * MCH);  // in flight during this stage's sums
         if (ch == 0) {
             const double2 tz = reinterpret_cast<const double2 *>(ltz_p + n * TZ)[zq];
             const double2 tx = reinterpret_cast<const double2 *>(ltx_p + n * TX)[xq];
@@ -399,10 +417,9 @@ k_kk_gather(const KKArgs a) {
 #pragma unroll
                 for (int r = 0; r < 2; ++r) {
                     const double fi = kk_delay(t1[p][r], p ? lz.y : lz.x, r ? lx.y : lx.x, fs, shift);
-                    // s = RD(arg + 1.5*2^20): high word - 0x41380000 = floor(arg), low word = frac * 2^32
-                    const double sv = __dadd_rd(LINEAR ? fi : __dadd_rn(fi, 0.5), KKB_FLOOR_MAGIC2);
-                    const int F = __double2hiint(sv) - KKB_MAGIC2_HI;
-                    const bool ok = (unsigned)F <= (unsigned)(LINEAR ? T - 2 : T - 1);
+                    int F;
+                    double sv;
+                    const bool ok = tap_index<LINEAR>(fi, T, F, sv);
                     const unsigned e = min((unsigned)(F - lo), (unsigned)(LINEAR ? W - 2 : W - 1));
                     const float we = ok ? wm : 0.f;
                     if constexpr (LINEAR) {
@@ -430,8 +447,10 @@ k_kk_gather(const KKArgs a) {
         }
         // buffer buf^1 was last read in stage s-1, which every thread finished
         // before the barrier that ended it
-        if (s + 1 < nstage) store_stage(s + 1, buf ^ 1);
+        if (s + 1 < nstage) store_stage(ch1 * MCH, buf ^ 1);
         __syncthreads();
+        n = n1;
+        ch = ch1;
     }
 
     // epilogue: IQ (+ fused intensity and frame max)
