@@ -14,7 +14,8 @@ import os
 from .errors import DeviceError, raise_for_status
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libkkb.so")
+# KKB_LIB selects an alternative in-tree build (tuning variants under variants/)
+LIB_PATH = os.environ.get("KKB_LIB") or os.path.join(_HERE, "libkkb.so")
 
 P = ctypes.c_void_p
 I = ctypes.c_int

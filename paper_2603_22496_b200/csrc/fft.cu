@@ -21,6 +21,7 @@
 #include <mutex>
 #include <vector>
 #include <cmath>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "fft.cuh"
@@ -398,6 +399,13 @@ __global__ void k_real_to_complex(const float *__restrict__ in, long long n, flo
 }
 
 // ------------------------------------------------------------- host launchers
+// Compile-time-specialised kernels (fft_ct.cu) for T in {1024, 1536, 2048, 4096};
+// KKB_FFT_GENERIC=1 in the environment forces the runtime-plan kernels (tests).
+static const bool g_use_ct = [] {
+    const char *e = getenv("KKB_FFT_GENERIC");
+    return !(e && e[0] == '1');
+}();
+
 static int traces_per_cta(int T) {
     int G = KKB_FFT_TARGET_ELEMS / T;
     return G < 1 ? 1 : G;
@@ -426,6 +434,9 @@ int fft_c2c(const float2 *in, long long in_stride, int in_len, float2 *out, long
         KKB_CHECK_LAUNCH("k_dft_direct");
         return KKB_OK;
     }
+    if (fft_ct_supported(T) && g_use_ct)
+        return fft_c2c_ct(in, in_stride, in_len, out, out_stride, out_len, ntraces, T, inverse, scale,
+                          p.tw, s);
     int G = traces_per_cta(T);
     int sm = smem_bytes(T, G);
     st = ensure_smem((const void *)k_fft_c2c, sm);
@@ -455,6 +466,8 @@ int fft_r2c(const float *in, long long ntraces, int T, float2 *out, long long ou
         KKB_CHECK_LAUNCH("k_real_to_complex");
         return fft_c2c(scratch_c2c, T, T, out, out_stride, K, ntraces, T, false, 1.0f, s);
     }
+    if (fft_ct_supported(T) && g_use_ct)
+        return fft_r2c_ct(in, ntraces, T, out, out_stride, K, bin_scale, p.tw, s);
     int G = traces_per_cta(T);
     int sm = smem_bytes(T, G);
     st = ensure_smem((const void *)k_fft_r2c_pairs, sm);

@@ -29,4 +29,12 @@ int fft_c2c(const float2 *in, long long in_stride, int in_len, float2 *out, long
 int fft_r2c(const float *in, long long ntraces, int T, float2 *out, long long out_stride, int K,
             const float *bin_scale, cudaStream_t s, float2 *scratch_c2c);
 
+// compile-time-specialised twins (fft_ct.cu)
+bool fft_ct_supported(int T);
+int fft_r2c_ct(const float *in, long long ntraces, int T, float2 *out, long long out_stride, int K,
+               const float *bin_scale, const float2 *tw, cudaStream_t s);
+int fft_c2c_ct(const float2 *in, long long in_stride, int in_len, float2 *out, long long out_stride,
+               int out_len, long long ntraces, int T, bool inverse, float scale, const float2 *tw,
+               cudaStream_t s);
+
 }  // namespace kkb

@@ -9,8 +9,15 @@
 #define KKB_KK_WX 2
 #define KKB_KK_TZ (8 * KKB_KK_WZ)
 #define KKB_KK_TX (16 * KKB_KK_WX)
+#ifndef KKB_KK_STAGE_ELEMS
 #define KKB_KK_STAGE_ELEMS 1024  // window entries staged per pipeline stage
+#endif
+#ifndef KKB_KK_MIN_CTAS
 #define KKB_KK_MIN_CTAS 3        // occupancy target (caps registers at 85)
+#endif
+#ifndef KKB_KK_QUNROLL
+#define KKB_KK_QUNROLL 1         // receive-loop unroll of the gather
+#endif
 
 namespace kkb {
 

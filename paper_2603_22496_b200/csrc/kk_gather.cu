@@ -345,8 +345,12 @@ k_kk_gather(const KKArgs a) {
                 const int q = qe[i] >> 16, e = qe[i] & 0xFFFF;
                 const int smp = lo_q[q] + e;
                 const float2 *tr = base + q * T;
-                if ((unsigned)smp < (unsigned)T) s0[i] = __ldg(tr + smp);
-                if (LINEAR && (unsigned)(smp + 1) < (unsigned)T) s1[i] = __ldg(tr + smp + 1);
+                // entry smp stays zero unless a tap at smp is in the reference's
+                // window: linear 0 <= i0 <= T-2 (both d0, d1 exist), nearest 0 <= j <= T-1
+                if ((unsigned)smp <= (unsigned)(LINEAR ? T - 2 : T - 1)) {
+                    s0[i] = __ldg(tr + smp);
+                    if (LINEAR) s1[i] = __ldg(tr + smp + 1);
+                }
             }
         }
     };
@@ -405,32 +409,35 @@ k_kk_gather(const KKArgs a) {
         }
         const Entry *wb = win + buf * MCH * W;
         const int *lo_n = lo_s + n * M + m0;
+        constexpr int kQUnroll = KKB_KK_QUNROLL;
+#pragma unroll kQUnroll
         for (int q = 0; q < mc; ++q) {
             const int m = m0 + q;
             const double2 lz = reinterpret_cast<const double2 *>(lrz_p + m * TZ)[zq];
             const double2 lx = reinterpret_cast<const double2 *>(lrx_p + m * TX)[xq];
             const float wm = w_s[m];
-            const int lo = lo_n[q];
+            // window index e = floor(arg) - lo = hi(sv) - (0x41380000 + lo); the
+            // in-window predicate of tap_index() is folded into the staged window
+            // (entries whose tap would be invalid are zero), so no per-tap test
+            const int loC = lo_n[q] + KKB_MAGIC2_HI;
             const Entry *wv = wb + q * W;
 #pragma unroll
             for (int p = 0; p < 2; ++p) {
 #pragma unroll
                 for (int r = 0; r < 2; ++r) {
                     const double fi = kk_delay(t1[p][r], p ? lz.y : lz.x, r ? lx.y : lx.x, fs, shift);
-                    int F;
-                    double sv;
-                    const bool ok = tap_index<LINEAR>(fi, T, F, sv);
-                    const unsigned e = min((unsigned)(F - lo), (unsigned)(LINEAR ? W - 2 : W - 1));
-                    const float we = ok ? wm : 0.f;
+                    const double sv = __dadd_rd(LINEAR ? fi : __dadd_rn(fi, 0.5), KKB_FLOOR_MAGIC2);
+                    const unsigned e = min((unsigned)(__double2hiint(sv) - loC),
+                                           (unsigned)(LINEAR ? W - 2 : W - 1));
                     if constexpr (LINEAR) {
                         const float4 v = wv[e];
                         const float f1 = __uint_as_float(((unsigned)__double2loint(sv) >> 9) + 0x3F800000u);
-                        accr[p][r] = fmaf(we, fmaf(f1, v.z, v.x), accr[p][r]);
-                        acci[p][r] = fmaf(we, fmaf(f1, v.w, v.y), acci[p][r]);
+                        accr[p][r] = fmaf(wm, fmaf(f1, v.z, v.x), accr[p][r]);
+                        acci[p][r] = fmaf(wm, fmaf(f1, v.w, v.y), acci[p][r]);
                     } else {
                         const float2 v = wv[e];
-                        accr[p][r] = fmaf(we, v.x, accr[p][r]);
-                        acci[p][r] = fmaf(we, v.y, acci[p][r]);
+                        accr[p][r] = fmaf(wm, v.x, accr[p][r]);
+                        acci[p][r] = fmaf(wm, v.y, acci[p][r]);
                     }
                 }
             }

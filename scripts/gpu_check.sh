@@ -8,6 +8,6 @@ $CMD > gpurun_out/plain.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launch.log 2>&1
 echo "launch rc=$?"
 $CMD > gpurun_out/plain2.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:"k_kk_gather|k_contract|k_fft_r2c|k_fft_c2c" -s 12 -c 4 -o gpurun_out/prof $CMD > gpurun_out/ncu_full.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:"k_kk_gather|k_contract|k_r2c|k_c2c" -s 12 -c 4 -f -o gpurun_out/prof $CMD > gpurun_out/ncu_full.log 2>&1
 echo "full rc=$?"
 fi
