@@ -46,6 +46,19 @@ def _peaks():
         return 6650.0, "fallback"
 
 
+def _gather_traffic(frames: int):
+    """dram read+write bytes of one k_kk_gather launch from the newest committed
+    ncu --set full capture (profiles/r*_gather_traffic.json), scaled to `frames`."""
+    import glob
+
+    paths = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_gather_traffic.json")))
+    if not paths:
+        return None
+    with open(paths[-1]) as f:
+        d = json.load(f)
+    return d["dram_bytes_per_launch"] * frames / d["frames_per_launch"]
+
+
 def _workload(cfg: int, frames: int):
     from paper_2603_22496_b200 import configs
 
@@ -321,7 +334,8 @@ def run_gpu(args):
             "stage_ms": {"decompose(K1-K3)": dec_ms, "kk_gather(K5)": kk_ms, "db_map(K6)": det_ms},
             "roofline": {"kernel": "k_kk_gather", "bound": "hbm",
                          "achieved": achieved_hbm, "peak": hbm_peak, "unit": "GB/s",
-                         "frac": achieved_hbm / hbm_peak, "traffic": None,
+                         "frac": achieved_hbm / hbm_peak, "traffic": _gather_traffic(F),
+                         "algorithmic_bytes_per_launch": compulsory,
                          "peak_kind": peak_kind,
                          "algorithmic_bytes": "compulsory HBM per launch: traces read + IQ/intensity "
                                               "write + tables (SURVEY 8d)"},
@@ -339,6 +353,73 @@ def run_gpu(args):
             line["cpu_baseline"] = cpu
         print(json.dumps(line))
     eng.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def run_gpu_rowblock(args):
+    """Config 5: one large frame per step, image row-blocks sharded over ranks,
+    stage 1 replicated, NCCL all-gather of the complex64 blocks (strong scaling)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2603_22496_b200 import _lib, configs, shard
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    w = configs.config5()
+    arr, p, rx, g = w.array, w.params, w.receive, w.grid
+    rf = torch.from_numpy(configs.noise_rf(p.num_transmits, arr.num_elements, p.num_samples,
+                                           seed=5)).cuda()
+    rb = shard.RowBlockKK(arr, p, rx, g, rank, world)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        rb.beamform_block(rf)
+        if world > 1:
+            rb.gather()
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    launches0 = _lib.launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    launches = _lib.launch_count() - launches0
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        tt = torch.tensor([ms], device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    ms_step = ms / args.steps
+    pp = g.nx * g.nz * w.pairs
+    if rank == 0:
+        print(json.dumps({
+            "metric": METRIC, "value": 1e3 / ms_step, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f32 (complex64 traces/IQ; float64 delay-index math)",
+            "data": "synthetic (seeded noise RF, shapes of BASELINE config 5)",
+            "config": {"workload": w.name, "frames_per_step": 1, "pixel_pairs_per_frame": pp,
+                       "parallelism": f"row-block x{world}, stage 1 replicated, NCCL all-gather"},
+            "pixel_pair_samples_per_s": pp * 1e3 / ms_step, "gpu_launches": int(launches),
+            "clocks": clk}))
+    rb.close()
     if world > 1:
         dist.destroy_process_group()
     return 0
@@ -362,6 +443,8 @@ def main():
         args.warmup = 3
     if args.impl == "reference":
         return run_reference(args)
+    if args.config == 5:
+        return run_gpu_rowblock(args)
     return run_gpu(args)
 
 

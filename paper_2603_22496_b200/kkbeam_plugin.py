@@ -1,0 +1,102 @@
+"""Reference-side binding: route the reference package's own kernels to libkkb.
+
+The reference (`kkbeam`) has no FFI; its wrappers look up three module
+globals at call time:
+
+* ``kkbeam.beamform._kk_kernel``   (beamform.py:212-236, called at 363-374)
+* ``kkbeam.beamform._das_kernel``  (beamform.py:178-209, called at 281-297)
+* ``kkbeam.compress.shear_and_sum`` (compress.py:54-82, called at 120)
+
+The shims below have exactly those signatures (flat numpy arrays in, the
+caller's ``out`` array filled in place) and run the sm_100a kernels through
+the C ABI.  ``install(kkbeam)`` rebinds the globals, so ``kkbeam.kk``,
+``kkbeam.das`` and ``kkbeam.compress`` — and the reference's own test suite,
+via ``-p paper_2603_22496_b200.pytest_kkbeam_gpu`` — run on the GPU with no
+change to the reference source.  See INTEGRATION.md.
+"""
+
+from __future__ import annotations
+
+import sys
+
+import numpy as np
+
+from . import _device as dev
+from . import _lib
+
+
+def _launch_kk(data, ltx, ltz, lrx, lrz, weights, fs, shift, linear, out):
+    t = dev.require_cuda()
+    d = [dev.to_device(np.ascontiguousarray(a)) for a in (data, ltx, ltz, lrx, lrz)]
+    n, m, T = data.shape
+    nx, nz = out.shape
+    w = dev.to_device(np.ascontiguousarray(weights, dtype=np.float64))
+    o = t.empty((nx, nz), dtype=t.complex128, device="cuda")
+    _lib.call("kkb_kk", dev.ptr(d[0]), n, m, T, dev.ptr(d[1]), dev.ptr(d[2]), dev.ptr(d[3]),
+              dev.ptr(d[4]), nx, nz, dev.ptr(w), float(fs), float(shift), int(bool(linear)),
+              dev.ptr(o), _lib.KKB_OUT_C128, 1, 0, 0, None, None, dev.stream_handle())
+    dev.synchronize()
+    out[...] = dev.to_host(o)
+
+
+def kk_kernel(data, ltx, ltz, lrx, lrz, weights, fs, shift, linear, out):
+    """Drop-in for kkbeam.beamform._kk_kernel (same arguments, fills `out`)."""
+    _launch_kk(np.asarray(data, dtype=np.complex64), ltx, ltz, lrx, lrz, weights, fs, shift,
+               linear, out)
+
+
+def das_kernel(data, ltx, ltz, hyp, base, frac, xcoord, zcoord, upos, tan_max, weights, fs,
+               shift, linear, out):
+    """Drop-in for kkbeam.beamform._das_kernel (same arguments, fills `out`)."""
+    t = dev.require_cuda()
+    arrs = [dev.to_device(np.ascontiguousarray(a)) for a in
+            (np.asarray(data, dtype=np.complex64), ltx, ltz, hyp)]
+    bd = dev.to_device(np.ascontiguousarray(base, dtype=np.int64))
+    rest = [dev.to_device(np.ascontiguousarray(a, dtype=np.float64)) for a in
+            (frac, xcoord, zcoord, upos, weights)]
+    n, l, T = data.shape
+    nx, nz = out.shape
+    o = t.empty((nx, nz), dtype=t.complex128, device="cuda")
+    _lib.call("kkb_das", dev.ptr(arrs[0]), n, l, T, dev.ptr(arrs[1]), dev.ptr(arrs[2]),
+              dev.ptr(arrs[3]), int(hyp.shape[0]), dev.ptr(bd), dev.ptr(rest[0]), dev.ptr(rest[1]),
+              dev.ptr(rest[2]), dev.ptr(rest[3]), float(tan_max), dev.ptr(rest[4]), float(fs),
+              float(shift), int(bool(linear)), nx, nz, dev.ptr(o), _lib.KKB_OUT_C128,
+              dev.stream_handle())
+    dev.synchronize()
+    out[...] = dev.to_host(o)
+
+
+def shear_and_sum(data, sampling_frequency, positions, angles, sound_speed):
+    """Drop-in for kkbeam.compress.shear_and_sum (complex128 (N, M, T) out)."""
+    from .compress import shear_and_sum as gpu_shear
+
+    return gpu_shear(data, sampling_frequency, positions, angles, sound_speed)
+
+
+class Installed:
+    """Handle returned by install(); ``restore()`` puts the originals back."""
+
+    def __init__(self, saved):
+        self._saved = saved
+
+    def restore(self):
+        for (mod, name), value in self._saved.items():
+            setattr(mod, name, value)
+        self._saved = {}
+
+
+def install(kkbeam_pkg=None) -> Installed:
+    """Rebind the reference's kernel globals to the GPU shims.
+
+    Note kkbeam/__init__.py:34 binds ``kkbeam.compress`` to the *function*,
+    so the submodule is taken from sys.modules."""
+    if kkbeam_pkg is None:
+        import kkbeam as kkbeam_pkg  # noqa: F401  (the reference package)
+    bf = sys.modules["kkbeam.beamform"]
+    cp = sys.modules["kkbeam.compress"]
+    saved = {(bf, "_kk_kernel"): bf._kk_kernel, (bf, "_das_kernel"): bf._das_kernel,
+             (cp, "shear_and_sum"): cp.shear_and_sum}
+    bf._kk_kernel = kk_kernel
+    bf._das_kernel = das_kernel
+    cp.shear_and_sum = shear_and_sum
+    return Installed(saved)

@@ -186,6 +186,34 @@ def test_workload_sizes_match_survey():
         "dense_vernier": 81, "shifted_vernier": 75, "confocal": 75, "hybrid": 125}
 
 
+def test_plugin_install_on_the_real_reference():
+    """install() rebinds the reference's own kernel globals (no kernel runs)."""
+    import sys
+
+    src = "/root/reference/pkg/src"
+    if not os.path.isdir(src):
+        pytest.skip("reference package not present (GPU box)")
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache")
+    sys.path.insert(0, src)
+    try:
+        import kkbeam
+
+        from paper_2603_22496_b200 import kkbeam_plugin
+
+        bf, cp = sys.modules["kkbeam.beamform"], sys.modules["kkbeam.compress"]
+        orig = (bf._kk_kernel, bf._das_kernel, cp.shear_and_sum)
+        h = kkbeam_plugin.install(kkbeam)
+        assert bf._kk_kernel is kkbeam_plugin.kk_kernel
+        assert bf._das_kernel is kkbeam_plugin.das_kernel
+        assert cp.shear_and_sum is kkbeam_plugin.shear_and_sum
+        # the package-level name keeps the float64 original (oracle stays intact)
+        assert kkbeam.shear_and_sum is orig[2]
+        h.restore()
+        assert (bf._kk_kernel, bf._das_kernel, cp.shear_and_sum) == orig
+    finally:
+        sys.path.remove(src)
+
+
 def test_no_device_means_loud_failure(monkeypatch):
     # the product path refuses to run without CUDA instead of falling back
     from paper_2603_22496_b200 import _device
