@@ -283,7 +283,7 @@ def run_gpu(args):
     achieved_taps = gather_bytes_alg / (kk_ms / 1e3) / 1e9
 
     # ---- end to end through the public API: pinned host RF in, host IQ out ----
-    e2e = None
+    e2e = e2e_i16 = None
     if not args.no_e2e:
         host_rf = torch.empty((F, N, L, T), dtype=torch.float32).pin_memory()
         for f0 in range(0, F, distinct):
@@ -291,25 +291,42 @@ def run_gpu(args):
             host_rf[f0:f0 + n].copy_(torch.from_numpy(base[:n]))
         host_iq = torch.empty((F, g.nx, g.nz), dtype=torch.complex64).pin_memory()
         streams = [torch.cuda.Stream(), torch.cuda.Stream()]
-        for _ in range(max(1, min(args.warmup, 2))):
-            eng.run_host(host_rf, host_iq, chunk_frames=args.e2e_chunk, streams=streams)
         e2e_steps = max(1, min(args.steps, 5))
-        torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-        t0 = time.perf_counter()
-        for _ in range(e2e_steps):
-            eng.run_host(host_rf, host_iq, chunk_frames=args.e2e_chunk, streams=streams)
-        torch.cuda.synchronize()
-        dt = time.perf_counter() - t0
-        if world > 1:
-            tt = torch.tensor([dt], device="cuda")
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            dt = float(tt.item())
-        e2e = {"value": world * F * e2e_steps / dt, "unit": UNIT,
+
+        def e2e_rate(host_in):
+            for _ in range(max(1, min(args.warmup, 2))):
+                eng.run_host(host_in, host_iq, chunk_frames=args.e2e_chunk, streams=streams)
+            torch.cuda.synchronize()
+            if world > 1:
+                dist.barrier()
+            t0 = time.perf_counter()
+            for _ in range(e2e_steps):
+                eng.run_host(host_in, host_iq, chunk_frames=args.e2e_chunk, streams=streams)
+            torch.cuda.synchronize()
+            dt = time.perf_counter() - t0
+            if world > 1:
+                tt = torch.tensor([dt], device="cuda")
+                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+                dt = float(tt.item())
+            return world * F * e2e_steps / dt
+
+        e2e = {"value": e2e_rate(host_rf), "unit": UNIT,
                "h2d_bytes_per_step": int(host_rf.numel() * 4),
                "d2h_bytes_per_step": int(host_iq.numel() * 8),
-               "path": "KKEngine.run_host: pinned H2D RF, decompose+kk on 2 streams, D2H IQ"}
+               "path": "KKEngine.run_host: pinned H2D float32 RF, decompose+kk on 2 streams, D2H IQ"}
+        # same path fed int16-quantised RF (BASELINE config 2 sample format; exact)
+        del host_rf
+        scale = float(np.abs(base).max()) / 32767.0
+        q = np.clip(np.round(base / scale), -32767, 32767).astype(np.int16)
+        host_q = torch.empty((F, N, L, T), dtype=torch.int16).pin_memory()
+        for f0 in range(0, F, distinct):
+            n = min(distinct, F - f0)
+            host_q[f0:f0 + n].copy_(torch.from_numpy(q[:n]))
+        e2e_i16 = {"value": e2e_rate(host_q), "unit": UNIT,
+                   "h2d_bytes_per_step": int(host_q.numel() * 2),
+                   "d2h_bytes_per_step": int(host_iq.numel() * 8),
+                   "path": "KKEngine.run_host with int16 RF (converted exactly on device)"}
+        del host_q
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -349,6 +366,7 @@ def run_gpu(args):
         }
         if e2e:
             line["e2e"] = e2e
+            line["e2e_int16_ingest"] = e2e_i16
         if cpu:
             line["cpu_baseline"] = cpu
         print(json.dumps(line))

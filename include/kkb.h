@@ -149,6 +149,12 @@ int kkb_decomposer_create(int n_tx, int n_el, int n_t, const double *positions_h
 /* rf: (F, N, L, T) float32; traces: (F, N, M, T) complex64. */
 int kkb_decomposer_run(kkb_decomposer *p, const float *rf, int n_frames, void *traces,
                        void *stream);
+/* int16-quantised RF ingest: rf is
+ * (F, N, L, T) int16; each sample is converted exactly to float32 inside the
+ * FFT load, identical to running the float32 path on rf.astype(float32).
+ * Needs T in {1024, 1536, 2048, 4096}. */
+int kkb_decomposer_run_i16(kkb_decomposer *p, const short *rf, int n_frames, void *traces,
+                           void *stream);
 /* bytes of device scratch held by the plan */
 long long kkb_decomposer_workspace_bytes(const kkb_decomposer *p);
 int kkb_decomposer_destroy(kkb_decomposer *p);

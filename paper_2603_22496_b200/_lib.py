@@ -42,6 +42,7 @@ SIGNATURES = {
     "kkb_shear_and_sum": [P, I, I, I, P, P, I, D, D, P, P],
     "kkb_decomposer_create": [I, I, I, P, P, I, D, D, I, P],
     "kkb_decomposer_run": [P, P, I, P, P],
+    "kkb_decomposer_run_i16": [P, P, I, P, P],
     "kkb_decomposer_workspace_bytes": [P],
     "kkb_decomposer_destroy": [P],
     "kkb_log_compress": [P, P, I, LL, F, P, P],

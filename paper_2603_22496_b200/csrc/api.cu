@@ -412,21 +412,43 @@ extern "C" int kkb_decomposer_create(int n_tx, int n_el, int n_t, const double *
 
 extern "C" long long kkb_decomposer_workspace_bytes(const kkb_decomposer *p) { return p ? p->bytes : 0; }
 
-extern "C" int kkb_decomposer_run(kkb_decomposer *p, const float *rf, int n_frames, void *traces,
-                                  void *stream) {
+static int decomposer_run(kkb_decomposer *p, const void *rf, int in_kind, int n_frames,
+                          void *traces, void *stream) {
     if (!p || n_frames < 0) return KKB_ERR_ARG;
     cudaStream_t s = as_stream(stream);
     const int N = p->N, L = p->L, T = p->T, M = p->M, K = p->K, ldk = p->ldk;
+    if (in_kind && !fft_ct_supported(T)) {
+        set_error("int16 RF ingest needs T in {1024, 1536, 2048, 4096} (got %d)", T);
+        return KKB_ERR_UNSUPPORTED;
+    }
+    const size_t esz = in_kind ? sizeof(short) : sizeof(float);
+    FftPlan plan;
+    int st = get_fft_plan(T, &plan);
+    if (st) return st;
     for (int f0 = 0; f0 < n_frames; f0 += p->chunk) {
         int F = std::min(p->chunk, n_frames - f0);
-        const float *rf_c = rf + (size_t)f0 * N * L * T;
+        const char *rf_c = (const char *)rf + (size_t)f0 * N * L * T * esz;
         float2 *tr_c = (float2 *)traces + (size_t)f0 * N * M * T;
-        int st;
-        if ((st = fft_r2c(rf_c, (long long)F * N * L, T, p->X, ldk, K, nullptr, s, nullptr))) return st;
+        if (in_kind)
+            st = fft_r2c_ct(rf_c, 1, (long long)F * N * L, T, p->X, ldk, K, nullptr, plan.tw, s);
+        else
+            st = fft_r2c((const float *)rf_c, (long long)F * N * L, T, p->X, ldk, K, nullptr, s,
+                         nullptr);
+        if (st) return st;
         if ((st = contract(p->X, ldk, p->ramps, ldk, p->Y, ldk, (long long)F * N, L, M, K, s))) return st;
         if ((st = fft_c2c(p->Y, ldk, K, tr_c, T, T, (long long)F * N * M, T, true, 1.0f, s))) return st;
     }
     return KKB_OK;
+}
+
+extern "C" int kkb_decomposer_run(kkb_decomposer *p, const float *rf, int n_frames, void *traces,
+                                  void *stream) {
+    return decomposer_run(p, rf, 0, n_frames, traces, stream);
+}
+
+extern "C" int kkb_decomposer_run_i16(kkb_decomposer *p, const short *rf, int n_frames,
+                                      void *traces, void *stream) {
+    return decomposer_run(p, rf, 1, n_frames, traces, stream);
 }
 
 extern "C" int kkb_decomposer_destroy(kkb_decomposer *p) {

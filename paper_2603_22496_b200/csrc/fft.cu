@@ -467,7 +467,7 @@ int fft_r2c(const float *in, long long ntraces, int T, float2 *out, long long ou
         return fft_c2c(scratch_c2c, T, T, out, out_stride, K, ntraces, T, false, 1.0f, s);
     }
     if (fft_ct_supported(T) && g_use_ct)
-        return fft_r2c_ct(in, ntraces, T, out, out_stride, K, bin_scale, p.tw, s);
+        return fft_r2c_ct(in, 0, ntraces, T, out, out_stride, K, bin_scale, p.tw, s);
     int G = traces_per_cta(T);
     int sm = smem_bytes(T, G);
     st = ensure_smem((const void *)k_fft_r2c_pairs, sm);

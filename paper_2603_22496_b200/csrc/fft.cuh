@@ -31,8 +31,10 @@ int fft_r2c(const float *in, long long ntraces, int T, float2 *out, long long ou
 
 // compile-time-specialised twins (fft_ct.cu)
 bool fft_ct_supported(int T);
-int fft_r2c_ct(const float *in, long long ntraces, int T, float2 *out, long long out_stride, int K,
-               const float *bin_scale, const float2 *tw, cudaStream_t s);
+// in_kind 0: float32 rows, 1: int16 rows (converted exactly to float32)
+int fft_r2c_ct(const void *in, int in_kind, long long ntraces, int T, float2 *out,
+               long long out_stride, int K, const float *bin_scale, const float2 *tw,
+               cudaStream_t s);
 int fft_c2c_ct(const float2 *in, long long in_stride, int in_len, float2 *out, long long out_stride,
                int out_len, long long ntraces, int T, bool inverse, float scale, const float2 *tw,
                cudaStream_t s);

@@ -11,6 +11,12 @@
 // shared-memory banks from neighbouring lanes write through an XOR swizzle
 // (index ^ ((index >> 3) & 15)), which the next stage reads back.
 // Twiddles exp(-2 pi i k / T): float64-accurate table in global memory (L1).
+//
+// Measured (r1, config 4): a persistent cp.async-pipelined variant of the
+// real FFT was 22% slower than one CTA per pair (register cap -> fewer
+// resident CTAs), so the simple form is the one kept.
+
+#include <algorithm>
 
 #include "common.cuh"
 #include "fft.cuh"
@@ -150,23 +156,32 @@ __device__ __forceinline__ void run_fft(float2 *buf, const float2 *tw) {
     fft<T, P::NT, P::R0, P::R1, P::R2, P::R3>(buf, tw);
 }
 
-// Real-pair forward FFT: rows 2p, 2p+1 of `in` (float32, length T) -> bins
-// [0, K) of each row's spectrum at out + row*out_stride, times bin_scale[k].
-template <int T>
+// four consecutive samples as float (float32 rows: one 16 B load; int16 rows:
+// one 8 B load, converted exactly — the reference consumes q.astype(float32))
+__device__ __forceinline__ float4 load4(const float *p) { return __ldg(reinterpret_cast<const float4 *>(p)); }
+__device__ __forceinline__ float4 load4(const short *p) {
+    const int2 u = __ldg(reinterpret_cast<const int2 *>(p));
+    return make_float4((float)(short)(u.x & 0xFFFF), (float)(short)(u.x >> 16),
+                       (float)(short)(u.y & 0xFFFF), (float)(short)(u.y >> 16));
+}
+
+// Real-pair forward FFT: rows 2p, 2p+1 of `in` (length T) -> bins [0, K) of
+// each row's spectrum at out + row*out_stride, times bin_scale[k].
+template <int T, typename InT>
 __global__ void __launch_bounds__(Plan<T>::NT)
-k_r2c(const float *__restrict__ in, long long ntraces, float2 *__restrict__ out,
+k_r2c(const InT *__restrict__ in, long long ntraces, float2 *__restrict__ out,
       long long out_stride, int K, const float *__restrict__ bin_scale,
       const float2 *__restrict__ tw) {
     constexpr int NT = Plan<T>::NT;
     __shared__ __align__(16) float2 buf[T];
     const long long r0 = 2 * (long long)blockIdx.x;
     const bool l1 = r0 + 1 < ntraces;
-    const float4 *x0 = reinterpret_cast<const float4 *>(in + r0 * T);
-    const float4 *x1 = reinterpret_cast<const float4 *>(in + (l1 ? r0 + 1 : r0) * T);
+    const InT *x0 = in + r0 * T;
+    const InT *x1 = in + (l1 ? r0 + 1 : r0) * T;
 #pragma unroll
     for (int i = threadIdx.x; i < T / 4; i += NT) {
-        const float4 u = __ldg(x0 + i);
-        float4 w = __ldg(x1 + i);
+        const float4 u = load4(x0 + 4 * i);
+        float4 w = load4(x1 + 4 * i);
         if (!l1) w = make_float4(0.f, 0.f, 0.f, 0.f);
         buf[4 * i] = make_float2(u.x, w.x);
         buf[4 * i + 1] = make_float2(u.y, w.y);
@@ -220,11 +235,16 @@ k_c2c(const float2 *__restrict__ in, long long in_stride, int in_len, float2 *__
 bool fft_ct_supported(int T) { return T == 1024 || T == 1536 || T == 2048 || T == 4096; }
 
 template <int T>
-static int launch_r2c(const float *in, long long ntraces, float2 *out, long long out_stride, int K,
-                      const float *bin_scale, const float2 *tw, cudaStream_t s) {
-    long long npairs = (ntraces + 1) / 2;
-    ct::k_r2c<T><<<(unsigned)npairs, ct::Plan<T>::NT, 0, s>>>(in, ntraces, out, out_stride, K,
-                                                              bin_scale, tw);
+static int launch_r2c(const void *in, int in_kind, long long ntraces, float2 *out,
+                      long long out_stride, int K, const float *bin_scale, const float2 *tw,
+                      cudaStream_t s) {
+    const unsigned npairs = (unsigned)((ntraces + 1) / 2);
+    if (in_kind)
+        ct::k_r2c<T, short><<<npairs, ct::Plan<T>::NT, 0, s>>>(
+            reinterpret_cast<const short *>(in), ntraces, out, out_stride, K, bin_scale, tw);
+    else
+        ct::k_r2c<T, float><<<npairs, ct::Plan<T>::NT, 0, s>>>(
+            reinterpret_cast<const float *>(in), ntraces, out, out_stride, K, bin_scale, tw);
     KKB_CHECK_LAUNCH("k_fft_r2c_ct");
     return KKB_OK;
 }
@@ -243,15 +263,16 @@ static int launch_c2c(const float2 *in, long long in_stride, int in_len, float2 
     return KKB_OK;
 }
 
-int fft_r2c_ct(const float *in, long long ntraces, int T, float2 *out, long long out_stride, int K,
-               const float *bin_scale, const float2 *tw, cudaStream_t s) {
+int fft_r2c_ct(const void *in, int in_kind, long long ntraces, int T, float2 *out,
+               long long out_stride, int K, const float *bin_scale, const float2 *tw,
+               cudaStream_t s) {
     if (ntraces <= 0) return KKB_OK;
     if ((ntraces + 1) / 2 > 0x7fffffffLL) return KKB_ERR_UNSUPPORTED;
     switch (T) {
-        case 1024: return launch_r2c<1024>(in, ntraces, out, out_stride, K, bin_scale, tw, s);
-        case 1536: return launch_r2c<1536>(in, ntraces, out, out_stride, K, bin_scale, tw, s);
-        case 2048: return launch_r2c<2048>(in, ntraces, out, out_stride, K, bin_scale, tw, s);
-        case 4096: return launch_r2c<4096>(in, ntraces, out, out_stride, K, bin_scale, tw, s);
+        case 1024: return launch_r2c<1024>(in, in_kind, ntraces, out, out_stride, K, bin_scale, tw, s);
+        case 1536: return launch_r2c<1536>(in, in_kind, ntraces, out, out_stride, K, bin_scale, tw, s);
+        case 2048: return launch_r2c<2048>(in, in_kind, ntraces, out, out_stride, K, bin_scale, tw, s);
+        case 4096: return launch_r2c<4096>(in, in_kind, ntraces, out, out_stride, K, bin_scale, tw, s);
     }
     return KKB_ERR_UNSUPPORTED;
 }

@@ -104,10 +104,14 @@ class KKEngine:
         return int(lib.kkb_decomposer_workspace_bytes(self._dec)) + own
 
     # ------------------------------------------------------------------ device path
+    def _run_decomposer(self, handle, rf, n_frames, traces, stream_handle):
+        # float32 RF, or int16-quantised RF converted exactly inside the FFT load
+        name = "kkb_decomposer_run_i16" if rf.dtype == self.t.int16 else "kkb_decomposer_run"
+        _lib.call(name, handle, dev.ptr(rf), n_frames, dev.ptr(traces), stream_handle)
+
     def decompose(self, rf, n_frames: int | None = None, stream=None):
         F = self.F if n_frames is None else n_frames
-        _lib.call("kkb_decomposer_run", self._dec, dev.ptr(rf), F, dev.ptr(self.traces),
-                  dev.stream_handle(stream))
+        self._run_decomposer(self._dec, rf, F, self.traces, dev.stream_handle(stream))
         return self.traces[:F]
 
     def beamform(self, traces=None, n_frames: int | None = None, stream=None, out_offset: int = 0):
@@ -149,8 +153,8 @@ class KKEngine:
         Returns the complex64 IQ images (F, X, Z) (``self.inten`` / ``self.db``
         hold the detected and log-compressed images)."""
         t = self.t
-        if rf.dtype != t.float32 or tuple(rf.shape) != (self.F, self.N, self.L, self.T):
-            raise ConfigError(f"expected float32 RF of shape {(self.F, self.N, self.L, self.T)}")
+        if rf.dtype not in (t.float32, t.int16) or tuple(rf.shape) != (self.F, self.N, self.L, self.T):
+            raise ConfigError(f"expected float32 or int16 RF of shape {(self.F, self.N, self.L, self.T)}")
         if not rf.is_contiguous():
             raise ConfigError("RF must be contiguous")
         self.decompose(rf, stream=stream)
@@ -170,7 +174,7 @@ class KKEngine:
         while len(self._stream_decs) < len(streams):
             self._stream_decs.append(self._new_decomposer(C))
         if staging is None:
-            staging = [t.empty((C, self.N, self.L, self.T), dtype=t.float32, device="cuda")
+            staging = [t.empty((C, self.N, self.L, self.T), dtype=rf_host.dtype, device="cuda")
                        for _ in streams]
         for i, f0 in enumerate(range(0, F, C)):
             n = min(C, F - f0)
@@ -179,8 +183,8 @@ class KKEngine:
             with t.cuda.stream(s):
                 buf[:n].copy_(rf_host[f0:f0 + n], non_blocking=True)
                 tr = self.traces[f0:f0 + n]
-                _lib.call("kkb_decomposer_run", self._stream_decs[i % len(streams)], dev.ptr(buf),
-                          n, dev.ptr(tr), s.cuda_stream)
+                self._run_decomposer(self._stream_decs[i % len(streams)], buf[:n], n, tr,
+                                     s.cuda_stream)
                 self.beamform(traces=tr, n_frames=n, stream=s, out_offset=f0)
                 iq_host[f0:f0 + n].copy_(self.iq[f0:f0 + n], non_blocking=True)
         for s in streams:
