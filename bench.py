@@ -217,20 +217,29 @@ def run_gpu(args):
         rf_dev[f0:f0 + n].copy_(src[:n])
     del src
 
-    eng = kb.KKEngine(arr, p, rx, g, frames=F, chunk_frames=args.chunk)
+    pipeline = (args.pipe_chunk, args.pipe_slots) if args.pipe_slots > 1 else None
+    eng = kb.KKEngine(arr, p, rx, g, frames=F, chunk_frames=args.chunk, pipeline=pipeline)
     stream = torch.cuda.current_stream()
 
-    def step():
-        eng.decompose(rf_dev)
-        e_mid.record(stream)
-        eng.gather()
-        e_g.record(stream)
-        eng.detect()
+    G = max(1, args.groups)
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
 
-    # warm-up
-    e_mid, e_g = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    def step(marks):
+        """One pass of the hot path over the 400-frame batch.  G > 1: frame groups,
+        decomposition of group g+1 overlapped with the gather of group g
+        (KKEngine._run_overlapped); marks = per-group (start, end) events of
+        the gather launches on their stream."""
+        if G > 1:
+            eng.run(rf_dev, groups=G, gather_events=marks)
+        else:
+            eng.decompose(rf_dev)
+            marks[0][0].record(stream)
+            eng.gather()
+            marks[0][1].record(stream)
+            eng.detect()
+
     for _ in range(args.warmup):
-        step()
+        step([(ev(), ev()) for _ in range(G)])
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -238,22 +247,15 @@ def run_gpu(args):
     clocks = ClockSampler(local)
     clocks.start()
     time.sleep(0.3)
-    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    mids = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    gs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    marks = [[(ev(), ev()) for _ in range(G)] for _ in range(args.steps)]
     launches0 = _lib.launch_count()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    t_start = torch.cuda.Event(enable_timing=True)
-    t_end = torch.cuda.Event(enable_timing=True)
+    t_start, t_end = ev(), ev()
     t_start.record(stream)
     for i in range(args.steps):
-        starts[i].record(stream)
-        e_mid, e_g = mids[i], gs[i]
-        step()
-        ends[i].record(stream)
+        step(marks[i])
     t_end.record(stream)
     torch.cuda.synchronize()
     launches = _lib.launch_count() - launches0
@@ -267,20 +269,38 @@ def run_gpu(args):
         total_ms = float(tt.item())
     ms_step = total_ms / args.steps
     value = world * F / (total_ms / 1e3 / args.steps)
+    # K5 launch durations inside the timed region (G launches of F/G frames per step;
+    # with G > 1 they include the K6 dB map and share the SMs with the decomposition)
+    kk_launch_ms = statistics.median(a.elapsed_time(b) for m in marks for a, b in m)
+    frames_per_launch = F / G
 
-    dec_ms = statistics.median(starts[i].elapsed_time(mids[i]) for i in range(args.steps))
-    kk_ms = statistics.median(mids[i].elapsed_time(gs[i]) for i in range(args.steps))
-    det_ms = statistics.median(gs[i].elapsed_time(ends[i]) for i in range(args.steps))
+    # stage split from sequential instrumented passes after the timed region
+    seq = []
+    for _ in range(3):
+        e = [ev() for _ in range(4)]
+        e[0].record(stream)
+        eng.decompose(rf_dev)
+        e[1].record(stream)
+        eng.gather()
+        e[2].record(stream)
+        eng.detect()
+        e[3].record(stream)
+        seq.append(e)
+    torch.cuda.synchronize()
+    dec_ms = statistics.median(e[0].elapsed_time(e[1]) for e in seq)
+    kk_ms = statistics.median(e[1].elapsed_time(e[2]) for e in seq)
+    det_ms = statistics.median(e[2].elapsed_time(e[3]) for e in seq)
 
-    # ---- roofline of the dominant kernel (K5 gather, one launch per step) ----
+    # ---- roofline of the dominant kernel (K5 gather), per launch in the timed region ----
     hbm_peak, peak_kind = _peaks()
     sm_count = torch.cuda.get_device_properties(local).multi_processor_count
-    gather_bytes_alg = 16.0 * pp_frame * F                     # 16 B x pp
-    compulsory = F * (N * M * T * 8 + P * (8 + 4)) + 8 * (g.nx + g.nz) * (N + M)
-    achieved_hbm = compulsory / (kk_ms / 1e3) / 1e9
+    fl = frames_per_launch
+    gather_bytes_alg = 16.0 * pp_frame * fl                    # 16 B x pp
+    compulsory = fl * (N * M * T * 8 + P * (8 + 4)) + 8 * (g.nx + g.nz) * (N + M)
+    achieved_hbm = compulsory / (kk_launch_ms / 1e3) / 1e9
     sm_mhz = clk.get("sm_mhz") or 1965.0
     smem_peak = sm_count * 128 * sm_mhz * 1e6 / 1e9           # GB/s, 128 B/clk/SM crossbar
-    achieved_taps = gather_bytes_alg / (kk_ms / 1e3) / 1e9
+    achieved_taps = gather_bytes_alg / (kk_launch_ms / 1e3) / 1e9
 
     # ---- end to end through the public API: pinned host RF in, host IQ out ----
     e2e = e2e_i16 = None
@@ -348,10 +368,13 @@ def run_gpu(args):
                        "l2": "inputs larger than L2 (3.46 GB RF per rank), no flush",
                        "parallelism": f"frame-sharded x{world}"},
             "pixel_pair_samples_per_s": value * pp_frame,
-            "stage_ms": {"decompose(K1-K3)": dec_ms, "kk_gather(K5)": kk_ms, "db_map(K6)": det_ms},
+            "stage_ms_sequential": {"decompose(K1-K3)": dec_ms, "kk_gather(K5)": kk_ms,
+                                    "db_map(K6)": det_ms},
+            "overlap_groups": G,
             "roofline": {"kernel": "k_kk_gather", "bound": "hbm",
                          "achieved": achieved_hbm, "peak": hbm_peak, "unit": "GB/s",
-                         "frac": achieved_hbm / hbm_peak, "traffic": _gather_traffic(F),
+                         "frac": achieved_hbm / hbm_peak, "traffic": _gather_traffic(fl),
+                         "launch_ms": kk_launch_ms, "frames_per_launch": fl,
                          "algorithmic_bytes_per_launch": compulsory,
                          "peak_kind": peak_kind,
                          "algorithmic_bytes": "compulsory HBM per launch: traces read + IQ/intensity "
@@ -360,7 +383,8 @@ def run_gpu(args):
                                 "achieved": achieved_taps, "peak": smem_peak, "unit": "GB/s",
                                 "frac": achieved_taps / smem_peak,
                                 "algorithmic_bytes": "16 B of taps per pixel-pair (SURVEY 8d)",
-                                "pixel_pairs_per_s": pp_frame * F / (kk_ms / 1e3)},
+                                "pixel_pairs_per_s": pp_frame * fl / (kk_launch_ms / 1e3),
+                                "pixel_pairs_per_s_isolated": pp_frame * F / (kk_ms / 1e3)},
             "gpu_launches": int(launches),
             "clocks": clk,
         }
@@ -452,6 +476,10 @@ def main():
     ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--frames", type=int, default=400)
     ap.add_argument("--chunk", type=int, default=None, help="frames per decomposition pass")
+    ap.add_argument("--pipe-chunk", type=int, default=8, help="frames per pipelined pass")
+    ap.add_argument("--pipe-slots", type=int, default=1, help="decomposition streams (1 = off)")
+    ap.add_argument("--groups", type=int, default=1,
+                    help="frame groups: decomposition of group g+1 overlaps the gather of group g")
     ap.add_argument("--e2e-chunk", type=int, default=16)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")

@@ -155,6 +155,15 @@ int kkb_decomposer_run(kkb_decomposer *p, const float *rf, int n_frames, void *t
  * Needs T in {1024, 1536, 2048, 4096}. */
 int kkb_decomposer_run_i16(kkb_decomposer *p, const short *rf, int n_frames, void *traces,
                            void *stream);
+/* Pipelined mode: process chunk_frames per pass, rotating passes over `slots`
+ * (1..4) internal streams (forked from / joined back into the caller's
+ * stream), so one pass's FFT overlaps the previous pass's contraction and the
+ * spectra are consumed while L2-resident.  Reallocates scratch (synchronous). */
+int kkb_decomposer_set_pipeline(kkb_decomposer *p, int chunk_frames, int slots);
+/* Number of +/- receive-angle classes of the symmetric contraction the plan
+ * uses (0: general contraction).  The reference guarantees the symmetry
+ * (ReceiveAngleSet, sampling.py:55-57; centred positions, core.py:32-38). */
+int kkb_decomposer_symmetric_classes(const kkb_decomposer *p);
 /* bytes of device scratch held by the plan */
 long long kkb_decomposer_workspace_bytes(const kkb_decomposer *p);
 int kkb_decomposer_destroy(kkb_decomposer *p);

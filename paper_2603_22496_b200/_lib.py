@@ -43,6 +43,8 @@ SIGNATURES = {
     "kkb_decomposer_create": [I, I, I, P, P, I, D, D, I, P],
     "kkb_decomposer_run": [P, P, I, P, P],
     "kkb_decomposer_run_i16": [P, P, I, P, P],
+    "kkb_decomposer_set_pipeline": [P, I, I],
+    "kkb_decomposer_symmetric_classes": [P],
     "kkb_decomposer_workspace_bytes": [P],
     "kkb_decomposer_destroy": [P],
     "kkb_log_compress": [P, P, I, LL, F, P, P],

@@ -2,6 +2,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstdarg>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <new>
@@ -344,10 +345,70 @@ extern "C" int kkb_shear_and_sum(const void *data, int n_tx, int n_el, int n_t,
 struct kkb_decomposer {
     int N, L, T, M, K, ldk, chunk;  // ldk: spectral row stride (K rounded up to even)
     float2 *ramps = nullptr;
-    float2 *X = nullptr;
-    float2 *Y = nullptr;
+    float2 *X = nullptr;            // slots x chunk frames of spectra
+    float2 *Y = nullptr;            // slots x chunk frames of contracted bins
     long long bytes = 0;
+    // pipelined mode (kkb_decomposer_set_pipeline): chunks rotate over `slots`
+    // streams so one chunk's FFT overlaps the previous chunk's contraction and
+    // its spectra are consumed while still L2-resident
+    int slots = 1;
+    cudaStream_t st[4] = {};
+    cudaEvent_t ev[5] = {};
+    // symmetric contraction (k_contract_sym): P > 0 classes when the element
+    // positions are centred (pos[L-1-l] == -pos[l]) and every receive angle has
+    // an exact negative partner (or is 0) — always true for the reference's
+    // TransducerArray / ReceiveAngleSet.  cs = (P, ceil(L/2), ldk) cos/sin table.
+    int P = 0;
+    float2 *cs = nullptr;
+    std::vector<short> mp, mm;
 };
+
+// Pair receive angles into +/- classes and build the cos/sin table; P = 0
+// (general contraction) when the geometry is not symmetric or KKB_NO_SYM=1.
+static int build_symmetric_classes(kkb_decomposer *p, const double *pos, const double *ang,
+                                   double c, const std::vector<double> &freq,
+                                   const std::vector<double> &scale) {
+    const char *env = getenv("KKB_NO_SYM");
+    if (env && env[0] == '1') return KKB_OK;
+    const int L = p->L, M = p->M;
+    for (int l = 0; l < L; ++l)
+        if (pos[L - 1 - l] != -pos[l]) return KKB_OK;
+    std::vector<int> used(M, 0);
+    std::vector<short> mp, mm;
+    for (int m = 0; m < M; ++m) {
+        if (used[m] || ang[m] < 0) continue;
+        used[m] = 1;
+        if (ang[m] == 0.0) {
+            mp.push_back((short)m);
+            mm.push_back(-1);
+            continue;
+        }
+        int partner = -1;
+        for (int q = 0; q < M && partner < 0; ++q)
+            if (!used[q] && ang[q] == -ang[m]) partner = q;
+        if (partner < 0) return KKB_OK;
+        used[partner] = 1;
+        mp.push_back((short)m);
+        mm.push_back((short)partner);
+    }
+    for (int m = 0; m < M; ++m)
+        if (!used[m]) return KKB_OK;
+    const int P = (int)mp.size(), Lp = (L + 1) / 2;
+    if (P > KKB_MAX_CLASSES) return KKB_OK;
+    std::vector<double> tau((size_t)Lp * P);
+    for (int q = 0; q < P; ++q) {
+        const double s = sin(ang[mp[q]]) / c;  // compress.py:79 order: positions * (sin/c)
+        for (int j = 0; j < Lp; ++j) tau[(size_t)j * P + q] = pos[j] * s;
+    }
+    KKB_TRY_CUDA(cudaMalloc(&p->cs, sizeof(float2) * (size_t)P * Lp * p->ldk), "cudaMalloc(cs)");
+    int st = build_ramps(tau.data(), Lp, P, freq.data(), scale.data(), p->ldk, p->cs, 0);
+    if (st) return st;
+    p->P = P;
+    p->mp = mp;
+    p->mm = mm;
+    p->bytes += (long long)(sizeof(float2) * (size_t)P * Lp * p->ldk);
+    return KKB_OK;
+}
 
 extern "C" int kkb_decomposer_create(int n_tx, int n_el, int n_t, const double *positions_host,
                                      const double *angles_host, int n_rx, double fs, double c,
@@ -399,16 +460,20 @@ extern "C" int kkb_decomposer_create(int n_tx, int n_el, int n_t, const double *
     freq.resize(ldk, 0.0);
     scale.resize(ldk, 0.0);
     st = build_ramps(tau.data(), n_el, n_rx, freq.data(), scale.data(), ldk, p->ramps, 0);
+    if (!st) st = build_symmetric_classes(p, positions_host, angles_host, c, freq, scale);
     if (st) {
         cudaFree(p->ramps);
         cudaFree(p->X);
         cudaFree(p->Y);
+        cudaFree(p->cs);
         delete p;
         return st;
     }
     *out = p;
     return KKB_OK;
 }
+
+extern "C" int kkb_decomposer_symmetric_classes(const kkb_decomposer *p) { return p ? p->P : -1; }
 
 extern "C" long long kkb_decomposer_workspace_bytes(const kkb_decomposer *p) { return p ? p->bytes : 0; }
 
@@ -425,19 +490,76 @@ static int decomposer_run(kkb_decomposer *p, const void *rf, int in_kind, int n_
     FftPlan plan;
     int st = get_fft_plan(T, &plan);
     if (st) return st;
-    for (int f0 = 0; f0 < n_frames; f0 += p->chunk) {
+    const bool piped = p->slots > 1 && n_frames > p->chunk;
+    if (piped) {  // fork: slot streams wait for work already queued on the caller stream
+        KKB_TRY_CUDA(cudaEventRecord(p->ev[4], s), "record fork");
+        for (int i = 0; i < p->slots; ++i)
+            KKB_TRY_CUDA(cudaStreamWaitEvent(p->st[i], p->ev[4], 0), "wait fork");
+    }
+    const size_t xslot = (size_t)p->chunk * N * L * ldk, yslot = (size_t)p->chunk * N * M * ldk;
+    int ci = 0;
+    for (int f0 = 0; f0 < n_frames; f0 += p->chunk, ++ci) {
+        const int slot = piped ? ci % p->slots : 0;
+        cudaStream_t cs = piped ? p->st[slot] : s;
+        float2 *X = p->X + slot * xslot, *Y = p->Y + slot * yslot;
         int F = std::min(p->chunk, n_frames - f0);
         const char *rf_c = (const char *)rf + (size_t)f0 * N * L * T * esz;
         float2 *tr_c = (float2 *)traces + (size_t)f0 * N * M * T;
         if (in_kind)
-            st = fft_r2c_ct(rf_c, 1, (long long)F * N * L, T, p->X, ldk, K, nullptr, plan.tw, s);
+            st = fft_r2c_ct(rf_c, 1, (long long)F * N * L, T, X, ldk, K, nullptr, plan.tw, cs);
         else
-            st = fft_r2c((const float *)rf_c, (long long)F * N * L, T, p->X, ldk, K, nullptr, s,
+            st = fft_r2c((const float *)rf_c, (long long)F * N * L, T, X, ldk, K, nullptr, cs,
                          nullptr);
         if (st) return st;
-        if ((st = contract(p->X, ldk, p->ramps, ldk, p->Y, ldk, (long long)F * N, L, M, K, s))) return st;
-        if ((st = fft_c2c(p->Y, ldk, K, tr_c, T, T, (long long)F * N * M, T, true, 1.0f, s))) return st;
+        if (p->P > 0)
+            st = contract_sym(X, ldk, p->cs, ldk, Y, ldk, (long long)F * N, L, M, K, p->P,
+                              p->mp.data(), p->mm.data(), cs);
+        else
+            st = contract(X, ldk, p->ramps, ldk, Y, ldk, (long long)F * N, L, M, K, cs);
+        if (st) return st;
+        if ((st = fft_c2c(Y, ldk, K, tr_c, T, T, (long long)F * N * M, T, true, 1.0f, cs))) return st;
     }
+    if (piped) {  // join
+        for (int i = 0; i < p->slots; ++i) {
+            KKB_TRY_CUDA(cudaEventRecord(p->ev[i], p->st[i]), "record join");
+            KKB_TRY_CUDA(cudaStreamWaitEvent(s, p->ev[i], 0), "wait join");
+        }
+    }
+    return KKB_OK;
+}
+
+// Pipelined mode: `chunk_frames` per pass, passes rotated over `slots` (1..4)
+// streams; reallocates the plan's scratch (slots x chunk frames).
+extern "C" int kkb_decomposer_set_pipeline(kkb_decomposer *p, int chunk_frames, int slots) {
+    if (!p || chunk_frames < 1 || slots < 1 || slots > 4) {
+        set_error("set_pipeline: chunk >= 1, 1 <= slots <= 4");
+        return KKB_ERR_ARG;
+    }
+    KKB_TRY_CUDA(cudaDeviceSynchronize(), "sync before realloc");
+    const size_t xb = sizeof(float2) * (size_t)slots * chunk_frames * p->N * p->L * p->ldk;
+    const size_t yb = sizeof(float2) * (size_t)slots * chunk_frames * p->N * p->M * p->ldk;
+    float2 *X = nullptr, *Y = nullptr;
+    cudaError_t e;
+    if ((e = cudaMalloc(&X, xb)) || (e = cudaMalloc(&Y, yb))) {
+        cudaFree(X);
+        return cuda_status(e, "cudaMalloc(decomposer pipeline)");
+    }
+    cudaFree(p->X);
+    cudaFree(p->Y);
+    p->X = X;
+    p->Y = Y;
+    p->bytes = (long long)(sizeof(float2) * (size_t)p->M * p->L * p->ldk + xb + yb);
+    for (int i = p->slots; i < slots; ++i) {
+        if (i == 0) continue;
+        KKB_TRY_CUDA(cudaStreamCreateWithFlags(&p->st[i], cudaStreamNonBlocking), "stream create");
+    }
+    if (slots > 1 && !p->st[0]) {
+        KKB_TRY_CUDA(cudaStreamCreateWithFlags(&p->st[0], cudaStreamNonBlocking), "stream create");
+        for (int i = 0; i < 5; ++i)
+            KKB_TRY_CUDA(cudaEventCreateWithFlags(&p->ev[i], cudaEventDisableTiming), "event create");
+    }
+    p->chunk = chunk_frames;
+    p->slots = slots;
     return KKB_OK;
 }
 
@@ -453,9 +575,14 @@ extern "C" int kkb_decomposer_run_i16(kkb_decomposer *p, const short *rf, int n_
 
 extern "C" int kkb_decomposer_destroy(kkb_decomposer *p) {
     if (!p) return KKB_OK;
+    for (int i = 0; i < 4; ++i)
+        if (p->st[i]) cudaStreamDestroy(p->st[i]);
+    for (int i = 0; i < 5; ++i)
+        if (p->ev[i]) cudaEventDestroy(p->ev[i]);
     cudaFree(p->ramps);
     cudaFree(p->X);
     cudaFree(p->Y);
+    cudaFree(p->cs);
     delete p;
     return KKB_OK;
 }

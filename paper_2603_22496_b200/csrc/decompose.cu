@@ -69,10 +69,16 @@ int build_ramps(const double *tau_host, int L, int M, const double *freq_host,
 // axis streams through shared memory in chunks of LC with cp.async double
 // buffering.  Thread (kx, bg) owns bin k0+kx and rows b0 + bg*NB .. +NB-1.
 #define KKB_CT_KT 32
-#define KKB_CT_BT 32
-#define KKB_CT_NB 4
+#ifndef KKB_CT_NB
+#define KKB_CT_NB 4       // rows per thread (register tile NB x MC)
+#endif
+#ifndef KKB_CT_MINB
+#define KKB_CT_MINB 2     // CTAs per SM requested for MC <= 12
+#endif
+#define KKB_CT_BT (8 * KKB_CT_NB)  // rows per CTA: 8 row groups of 32 bin-threads
 #define KKB_CT_LC 4
-#define KKB_CT_THREADS (KKB_CT_KT * (KKB_CT_BT / KKB_CT_NB))
+#define KKB_CT_THREADS 256
+static_assert(KKB_CT_BT == 16 || KKB_CT_BT == 32, "wide staging covers 16 or 32 rows");
 
 __device__ __forceinline__ void cp_async8z(void *smem_dst, const void *gsrc, bool valid) {
     unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
@@ -89,7 +95,7 @@ __device__ __forceinline__ void cp_async16z(void *smem_dst, const void *gsrc, bo
 }
 
 template <int MC>
-__global__ void __launch_bounds__(KKB_CT_THREADS, MC <= 12 ? 2 : 1)
+__global__ void __launch_bounds__(KKB_CT_THREADS, MC <= 12 ? KKB_CT_MINB : 1)
 k_contract(const float2 *__restrict__ X, long long ldx, const float2 *__restrict__ R,
            long long ldr, float2 *__restrict__ Y, long long ldy, long long B, int L, int M, int Kb) {
     constexpr int KT = KKB_CT_KT, BT = KKB_CT_BT, NB = KKB_CT_NB, LC = KKB_CT_LC;
@@ -124,7 +130,8 @@ k_contract(const float2 *__restrict__ X, long long ldx, const float2 *__restrict
                 const bool lok = l0 + ll < L;
                 const long long off = (long long)(l0 + ll) * ldx;
                 cp_async16z(xs + ll * BT * KT, okA && lok ? xA + off : X, okA && lok);
-                cp_async16z(xs + ll * BT * KT + 16 * KT, okB && lok ? xB + off : X, okB && lok);
+                if (BT > 16)
+                    cp_async16z(xs + ll * BT * KT + 16 * KT, okB && lok ? xB + off : X, okB && lok);
             }
 #pragma unroll
             for (int it = 0; it < RIT; ++it) {
@@ -219,6 +226,182 @@ static int launch_contract(const float2 *X, long long ldx, const float2 *R, long
     k_contract<MC><<<grid, KKB_CT_THREADS, sm, s>>>(X, ldx, R, ldr, Y, ldy, B, L, M, Kb);
     KKB_CHECK_LAUNCH("k_contract");
     return KKB_OK;
+}
+
+// ------------------------------------------------------------- symmetric form
+// The reference's receive sets are symmetric multisets (sampling.py:55-57)
+// and element positions are centred (core.py:32-38), so for a (+theta,
+// -theta) pair the ramps satisfy R_{L-1-l}(theta) = conj(R_l(theta)) =
+// R_l(-theta).  With S_l = X_l + X_{L-1-l}, D_l = X_l - X_{L-1-l} (l < L/2):
+//   Y(+theta) = A + iB,  Y(-theta) = A - iB,
+//   A = sum_l S_l cos(phi_l),  B = sum_l D_l sin(phi_l)
+// (cos/sin carry the one-sided weight and 1/T).  4 real FMAs per l-pair and
+// angle pair instead of 16: the contraction drops ~4x in arithmetic.
+// Class p = one +theta/-theta pair (or a lone theta = 0); CS[p][j][k] =
+// (cos, sin) * scale for j < ceil(L/2) (the middle element of odd L has
+// phi = 0 and no mirror).
+#ifndef KKB_CS_NB6
+#define KKB_CS_NB6 2   // rows per thread of the 6-class instance (config 4: M = 11)
+#endif
+#define KKB_CS_LC 4
+
+struct SymClasses {
+    int P;
+    short mp[KKB_MAX_CLASSES];  // output receive index of +theta
+    short mm[KKB_MAX_CLASSES];  // output receive index of -theta, -1 for theta = 0
+};
+
+template <int PC, int NB>
+__global__ void __launch_bounds__(256, 2)
+k_contract_sym(const float2 *__restrict__ X, long long ldx, const float2 *__restrict__ CS,
+               long long ldc, float2 *__restrict__ Y, long long ldy, long long B, int L, int M,
+               int Kb, const SymClasses cls) {
+    constexpr int KT = KKB_CT_KT, BT = 8 * NB, LC = KKB_CS_LC;
+    static_assert(BT == 16 || BT == 32, "staging covers 16 or 2 x 16 rows");
+    extern __shared__ __align__(16) float2 csm[];
+    float2 *Xl = csm;                     // [2][LC][BT][KT]
+    float2 *Xr = Xl + 2 * LC * BT * KT;   // [2][LC][BT][KT] mirrored elements
+    float2 *Cs = Xr + 2 * LC * BT * KT;   // [2][LC][PC][KT]
+    const int tid = threadIdx.x;
+    const int kx = tid % KT, bg = tid / KT;
+    const int k0 = blockIdx.x * KT;
+    const long long b0 = (long long)blockIdx.y * BT;
+    const int p0 = blockIdx.z * PC;
+    const int Lp = (L + 1) / 2;
+    const int nlc = (Lp + LC - 1) / LC;
+    const int kc = tid & 15, bbA = tid >> 4;
+    const int kw = k0 + 2 * kc;
+    const bool kok = kw < Kb;
+    const float2 *xA = X + ((b0 + bbA) * L) * ldx + kw;
+    const float2 *xB = xA + (long long)16 * L * ldx;
+    const bool okA = kok && b0 + bbA < B, okB = kok && b0 + bbA + 16 < B;
+    constexpr int CROWS = LC * PC;
+    constexpr int CIT = (CROWS + 15) / 16;
+
+    auto stage = [&](int c, int buf) {
+        const int j0 = c * LC;
+#pragma unroll
+        for (int ll = 0; ll < LC; ++ll) {
+            const int j = j0 + ll, r = L - 1 - j;
+            const bool jok = j < Lp, rok = jok && r != j;
+            const long long offl = (long long)j * ldx, offr = (long long)r * ldx;
+            float2 *xl = Xl + ((buf * LC + ll) * BT + bbA) * KT + 2 * kc;
+            float2 *xr = Xr + ((buf * LC + ll) * BT + bbA) * KT + 2 * kc;
+            cp_async16z(xl, okA && jok ? xA + offl : X, okA && jok);
+            cp_async16z(xr, okA && rok ? xA + offr : X, okA && rok);
+            if (BT > 16) {
+                cp_async16z(xl + 16 * KT, okB && jok ? xB + offl : X, okB && jok);
+                cp_async16z(xr + 16 * KT, okB && rok ? xB + offr : X, okB && rok);
+            }
+        }
+#pragma unroll
+        for (int it = 0; it < CIT; ++it) {
+            const int rr = bbA + 16 * it;
+            if (rr < CROWS) {
+                const int ll = rr / PC, q = rr - ll * PC;
+                const int p = p0 + q, j = j0 + ll;
+                const bool ok = kok && p < cls.P && j < Lp;
+                const float2 *src = ok ? CS + ((long long)p * Lp + j) * ldc + kw : CS;
+                cp_async16z(&Cs[((buf * LC + ll) * PC + q) * KT + 2 * kc], src, ok);
+            }
+        }
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+    };
+
+    float2 A[NB][PC], Bv[NB][PC];
+#pragma unroll
+    for (int i = 0; i < NB; ++i)
+#pragma unroll
+        for (int q = 0; q < PC; ++q) A[i][q] = Bv[i][q] = make_float2(0.f, 0.f);
+
+    stage(0, 0);
+    for (int c = 0; c < nlc; ++c) {
+        const int buf = c & 1;
+        if (c + 1 < nlc) {
+            stage(c + 1, buf ^ 1);
+            asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+        } else {
+            asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+        }
+        __syncthreads();
+#pragma unroll
+        for (int ll = 0; ll < LC; ++ll) {
+            float2 S[NB], D[NB];
+#pragma unroll
+            for (int i = 0; i < NB; ++i) {
+                const int off = ((buf * LC + ll) * BT + bg * NB + i) * KT + kx;
+                const float2 xl = Xl[off], xr = Xr[off];
+                S[i] = make_float2(xl.x + xr.x, xl.y + xr.y);
+                D[i] = make_float2(xl.x - xr.x, xl.y - xr.y);
+            }
+#pragma unroll
+            for (int q = 0; q < PC; ++q) {
+                const float2 cs = Cs[((buf * LC + ll) * PC + q) * KT + kx];
+#pragma unroll
+                for (int i = 0; i < NB; ++i) {
+                    A[i][q].x = fmaf(S[i].x, cs.x, A[i][q].x);
+                    A[i][q].y = fmaf(S[i].y, cs.x, A[i][q].y);
+                    Bv[i][q].x = fmaf(D[i].x, cs.y, Bv[i][q].x);
+                    Bv[i][q].y = fmaf(D[i].y, cs.y, Bv[i][q].y);
+                }
+            }
+        }
+        __syncthreads();
+    }
+    const int k = k0 + kx;
+    if (k >= Kb) return;
+#pragma unroll
+    for (int i = 0; i < NB; ++i) {
+        const long long b = b0 + bg * NB + i;
+        if (b >= B) break;
+#pragma unroll
+        for (int q = 0; q < PC; ++q) {
+            const int p = p0 + q;
+            if (p >= cls.P) break;
+            const float2 a = A[i][q], bb = Bv[i][q];
+            Y[(b * M + cls.mp[p]) * ldy + k] = make_float2(a.x - bb.y, a.y + bb.x);
+            if (cls.mm[p] >= 0) Y[(b * M + cls.mm[p]) * ldy + k] = make_float2(a.x + bb.y, a.y - bb.x);
+        }
+    }
+}
+
+template <int PC, int NB>
+static int launch_contract_sym(const float2 *X, long long ldx, const float2 *CS, long long ldc,
+                               float2 *Y, long long ldy, long long B, int L, int M, int Kb,
+                               const SymClasses &cls, cudaStream_t s) {
+    constexpr int BT = 8 * NB;
+    dim3 grid((unsigned)ceil_div(Kb, KKB_CT_KT), (unsigned)ceil_div(B, BT),
+              (unsigned)ceil_div(cls.P, PC));
+    if (grid.y > 65535u) {
+        set_error("contraction batch too large (%lld rows)", B);
+        return KKB_ERR_UNSUPPORTED;
+    }
+    const int sm = (int)sizeof(float2) * 2 * KKB_CS_LC * KKB_CT_KT * (2 * BT + PC);
+    KKB_TRY_CUDA(cudaFuncSetAttribute(k_contract_sym<PC, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm),
+                 "smem attr contract_sym");
+    k_contract_sym<PC, NB><<<grid, 256, sm, s>>>(X, ldx, CS, ldc, Y, ldy, B, L, M, Kb, cls);
+    KKB_CHECK_LAUNCH("k_contract_sym");
+    return KKB_OK;
+}
+
+int contract_sym(const float2 *X, long long ldx, const float2 *CS, long long ldc, float2 *Y,
+                 long long ldy, long long B, int L, int M, int Kb, int P, const short *mp,
+                 const short *mm, cudaStream_t s) {
+    if (B <= 0 || Kb <= 0) return KKB_OK;
+    if (P < 1 || P > KKB_MAX_CLASSES || ((ldx | ldc) & 1)) {
+        set_error("contract_sym: bad class count %d or odd row stride", P);
+        return KKB_ERR_ARG;
+    }
+    SymClasses cls{};
+    cls.P = P;
+    for (int p = 0; p < P; ++p) {
+        cls.mp[p] = mp[p];
+        cls.mm[p] = mm[p];
+    }
+    // register tile NB x PC complex (A, B) pairs: NB = 4 rows for few classes, 2 otherwise
+    if (P <= 3) return launch_contract_sym<3, 4>(X, ldx, CS, ldc, Y, ldy, B, L, M, Kb, cls, s);
+    if (P <= 6) return launch_contract_sym<6, KKB_CS_NB6>(X, ldx, CS, ldc, Y, ldy, B, L, M, Kb, cls, s);
+    return launch_contract_sym<8, 2>(X, ldx, CS, ldc, Y, ldy, B, L, M, Kb, cls, s);
 }
 
 int contract(const float2 *X, long long ldx, const float2 *R, long long ldr, float2 *Y,

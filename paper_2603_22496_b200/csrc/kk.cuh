@@ -57,6 +57,10 @@ int das_gather(const float2 *data, int n_tx, int n_el, int n_t, const double *lt
 // decomposition (ramps + per-bin contraction)
 int build_ramps(const double *tau_host, int L, int M, const double *freq_host,
                 const double *scale_host, int Kb, float2 *ramps, cudaStream_t s);
+#define KKB_MAX_CLASSES 64  // symmetric angle classes per contraction launch
+int contract_sym(const float2 *X, long long ldx, const float2 *CS, long long ldc, float2 *Y,
+                 long long ldy, long long B, int L, int M, int Kb, int P, const short *mp,
+                 const short *mm, cudaStream_t s);
 int contract(const float2 *X, long long ldx, const float2 *R, long long ldr, float2 *Y,
              long long ldy, long long B, int L, int M, int Kb, cudaStream_t s);
 

@@ -36,9 +36,10 @@ from .sampling import ReceiveAngleSet
 class KKEngine:
     def __init__(self, array: TransducerArray, params: AcquisitionParams,
                  receive: ReceiveAngleSet, grid: ImageGrid, frames: int, *,
-                 chunk_frames: int | None = None, interpolation: str = "linear",
+                 chunk_frames: int | None = None, pipeline: tuple | None = None,
+                 interpolation: str = "linear",
                  pulse_delay: float = 0.0, channel_weights=None, floor_db: float = -60.0,
-                 want_db: bool = True):
+                 want_db: bool = True, groups: int = 1):
         t = dev.require_cuda()
         self.t = t
         self.array, self.params, self.receive, self.grid = array, params, receive, grid
@@ -56,9 +57,14 @@ class KKEngine:
         self.floor_db = float(floor_db)
         self.want_db = want_db
         self.chunk = int(chunk_frames or self.F)
+        self.groups = int(groups)   # >1: overlap decomposition and gather across frame groups
+        self._side = None
         lib = _lib.load()
 
         self._dec = self._new_decomposer(self.chunk)
+        if pipeline is not None:
+            # (frames per pass, streams): overlapped, L2-resident decomposition passes
+            _lib.call("kkb_decomposer_set_pipeline", self._dec, int(pipeline[0]), int(pipeline[1]))
         self._stream_decs = []  # one per stream of run_host (scratch is per plan)
 
         self.luts = build_kk_luts_device(grid, params.transmit_angles, receive.angles, self.c)
@@ -148,7 +154,7 @@ class KKEngine:
                   dev.ptr(self.db), dev.stream_handle(stream))
         return self.db[:F]
 
-    def run(self, rf, stream=None):
+    def run(self, rf, stream=None, groups=None, gather_events=None):
         """Whole hot path for a (F, N, L, T) float32 CUDA tensor; asynchronous.
         Returns the complex64 IQ images (F, X, Z) (``self.inten`` / ``self.db``
         hold the detected and log-compressed images)."""
@@ -157,8 +163,42 @@ class KKEngine:
             raise ConfigError(f"expected float32 or int16 RF of shape {(self.F, self.N, self.L, self.T)}")
         if not rf.is_contiguous():
             raise ConfigError("RF must be contiguous")
-        self.decompose(rf, stream=stream)
-        return self.beamform(stream=stream)
+        groups = self.groups if groups is None else int(groups)
+        if groups <= 1 or self.F < 2:
+            self.decompose(rf, stream=stream)
+            return self.beamform(stream=stream)
+        return self._run_overlapped(rf, groups, stream, gather_events)
+
+    def _run_overlapped(self, rf, groups, stream, gather_events=None):
+        """Frame groups: decomposition of group g+1 (FFT/FMA/latency-bound) runs
+        on the caller's stream while the gather of group g (shared-memory
+        bound) runs on a side stream, so the two bottlenecks share the SMs."""
+        t = self.t
+        from .shard import balanced_range
+
+        main = stream if stream is not None else t.cuda.current_stream()
+        if self._side is None:
+            self._side = t.cuda.Stream()
+        side = self._side
+        side.wait_stream(main)  # outputs may still be read by earlier work on main
+        NMT = self.N * self.M * self.T
+        for g in range(groups):
+            f0, f1 = balanced_range(self.F, g, groups)
+            n = f1 - f0
+            if n == 0:
+                continue
+            tr = self.traces[f0:f1]
+            self._run_decomposer(self._dec, rf[f0:f1], n, tr, main.cuda_stream)
+            ev = t.cuda.Event()
+            ev.record(main)
+            side.wait_event(ev)
+            if gather_events is not None:
+                gather_events[g][0].record(side)
+            self.beamform(traces=tr, n_frames=n, stream=side, out_offset=f0)
+            if gather_events is not None:
+                gather_events[g][1].record(side)
+        main.wait_stream(side)
+        return self.iq
 
     # ------------------------------------------------------------------ end-to-end path
     def run_host(self, rf_host, iq_host, chunk_frames: int = 16, streams=None, staging=None):
