@@ -372,7 +372,7 @@ k_kk_gather(const KKArgs a) {
         }
     };
 
-    double accd_r[2][2], accd_i[2][2];
+    kk_total_t accd_r[2][2], accd_i[2][2];
     float accr[2][2], acci[2][2];
     double t1[2][2];
 #pragma unroll
@@ -447,8 +447,8 @@ k_kk_gather(const KKArgs a) {
             for (int p = 0; p < 2; ++p)
 #pragma unroll
                 for (int r = 0; r < 2; ++r) {
-                    accd_r[p][r] += (double)accr[p][r];
-                    accd_i[p][r] += (double)acci[p][r];
+                    accd_r[p][r] += (kk_total_t)accr[p][r];
+                    accd_i[p][r] += (kk_total_t)acci[p][r];
                     accr[p][r] = acci[p][r] = 0.f;
                 }
         }

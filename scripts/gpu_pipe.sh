@@ -4,6 +4,6 @@ for cs in "8 1" "4 2" "4 3" "8 2" "8 3" "16 2" "16 3" "32 2" "2 4"; do
   python - "$1" "$2" <<'PY'
 import json,sys
 d=json.loads(open("gpurun_out/pipe.json").read().strip().splitlines()[-1])
-print("chunk", sys.argv[1], "slots", sys.argv[2], "frames/s %.0f"%d["value"], {k: round(v,3) for k,v in d["stage_ms"].items()})
+print("chunk", sys.argv[1], "slots", sys.argv[2], "frames/s %.0f"%d["value"], {k: round(v,3) for k,v in d["stage_ms_sequential"].items()})
 PY
 done

@@ -4,6 +4,6 @@ for c in 4 8 16 32 400; do
   python - "$c" <<'PY'
 import json,sys
 d=json.loads(open(f"gpurun_out/sweep_{sys.argv[1]}.json").read().strip().splitlines()[-1])
-print("chunk", sys.argv[1], "frames/s %.0f"%d["value"], {k: round(v,3) for k,v in d["stage_ms"].items()})
+print("chunk", sys.argv[1], "frames/s %.0f"%d["value"], {k: round(v,3) for k,v in d["stage_ms_sequential"].items()})
 PY
 done

@@ -4,6 +4,6 @@ for lib in paper_2603_22496_b200/libkkb.so paper_2603_22496_b200/variants/libkkb
   python - "$lib" <<'PY'
 import json,sys
 d=json.loads(open("gpurun_out/var.json").read().strip().splitlines()[-1])
-print(sys.argv[1].split('/')[-1], "frames/s %.0f"%d["value"], {k: round(v,3) for k,v in d["stage_ms"].items()})
+print(sys.argv[1].split('/')[-1], "frames/s %.0f"%d["value"], {k: round(v,3) for k,v in d["stage_ms_sequential"].items()})
 PY
 done
