@@ -506,7 +506,7 @@ static int decomposer_run(kkb_decomposer *p, const void *rf, int in_kind, int n_
         const char *rf_c = (const char *)rf + (size_t)f0 * N * L * T * esz;
         float2 *tr_c = (float2 *)traces + (size_t)f0 * N * M * T;
         if (in_kind)
-            st = fft_r2c_ct(rf_c, 1, (long long)F * N * L, T, X, ldk, K, nullptr, plan.tw, cs);
+            st = fft_r2c_ct(rf_c, 1, (long long)F * N * L, T, X, ldk, K, nullptr, plan.tws, cs);
         else
             st = fft_r2c((const float *)rf_c, (long long)F * N * L, T, X, ldk, K, nullptr, cs,
                          nullptr);

@@ -71,6 +71,14 @@ int get_fft_plan(int T, FftPlan *out) {
     KKB_TRY_CUDA(cudaMalloc(&p.tw, sizeof(float2) * T), "cudaMalloc(twiddles)");
     KKB_TRY_CUDA(cudaMemcpy(p.tw, tw.data(), sizeof(float2) * T, cudaMemcpyHostToDevice),
                  "cudaMemcpy(twiddles)");
+    if (fft_ct_supported(T)) {
+        std::vector<float2> tws;
+        fft_ct_twiddles(T, tws);
+        KKB_TRY_CUDA(cudaMalloc(&p.tws, sizeof(float2) * tws.size()), "cudaMalloc(stage twiddles)");
+        KKB_TRY_CUDA(cudaMemcpy(p.tws, tws.data(), sizeof(float2) * tws.size(),
+                                cudaMemcpyHostToDevice),
+                     "cudaMemcpy(stage twiddles)");
+    }
     g_fft_plans[key] = p;
     *out = p;
     return KKB_OK;
@@ -436,7 +444,7 @@ int fft_c2c(const float2 *in, long long in_stride, int in_len, float2 *out, long
     }
     if (fft_ct_supported(T) && g_use_ct)
         return fft_c2c_ct(in, in_stride, in_len, out, out_stride, out_len, ntraces, T, inverse, scale,
-                          p.tw, s);
+                          p.tws, s);
     int G = traces_per_cta(T);
     int sm = smem_bytes(T, G);
     st = ensure_smem((const void *)k_fft_c2c, sm);
@@ -467,7 +475,7 @@ int fft_r2c(const float *in, long long ntraces, int T, float2 *out, long long ou
         return fft_c2c(scratch_c2c, T, T, out, out_stride, K, ntraces, T, false, 1.0f, s);
     }
     if (fft_ct_supported(T) && g_use_ct)
-        return fft_r2c_ct(in, 0, ntraces, T, out, out_stride, K, bin_scale, p.tw, s);
+        return fft_r2c_ct(in, 0, ntraces, T, out, out_stride, K, bin_scale, p.tws, s);
     int G = traces_per_cta(T);
     int sm = smem_bytes(T, G);
     st = ensure_smem((const void *)k_fft_r2c_pairs, sm);

@@ -3,6 +3,8 @@
 
 #include <cuda_runtime.h>
 
+#include <vector>
+
 #define KKB_FFT_MAX_STAGES 16
 #define KKB_FFT_MAX_RADIX 32
 #define KKB_FFT_MAX_T 8192
@@ -17,6 +19,7 @@ struct FftPlan {
     int direct;                      // 1: largest prime factor > 31 -> O(T^2) kernel
     int radix[KKB_FFT_MAX_STAGES];
     float2 *tw;                      // exp(-2 pi i k / T), k < T (device)
+    float2 *tws;                     // stage-ordered twiddles of the compile-time plan (device; fft_ct_supported T only)
 };
 
 int get_fft_plan(int T, FftPlan *out);
@@ -31,9 +34,11 @@ int fft_r2c(const float *in, long long ntraces, int T, float2 *out, long long ou
 
 // compile-time-specialised twins (fft_ct.cu)
 bool fft_ct_supported(int T);
+// host copy of the stage-ordered twiddle table the *_ct kernels read
+void fft_ct_twiddles(int T, std::vector<float2> &out);
 // in_kind 0: float32 rows, 1: int16 rows (converted exactly to float32)
 int fft_r2c_ct(const void *in, int in_kind, long long ntraces, int T, float2 *out,
-               long long out_stride, int K, const float *bin_scale, const float2 *tw,
+               long long out_stride, int K, const float *bin_scale, const float2 *tws,
                cudaStream_t s);
 int fft_c2c_ct(const float2 *in, long long in_stride, int in_len, float2 *out, long long out_stride,
                int out_len, long long ntraces, int T, bool inverse, float scale, const float2 *tw,

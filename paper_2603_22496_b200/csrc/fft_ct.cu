@@ -19,6 +19,8 @@
 // so the simple form is the one kept.
 
 #include <algorithm>
+#include <cmath>
+#include <vector>
 
 #include "common.cuh"
 #include "fft.cuh"
@@ -85,11 +87,14 @@ __device__ __forceinline__ int swz(int e) {
 }
 
 // One Stockham stage, in place: radix R, input sub-transform length NS.
-template <int T, int NT, int R, int NS, bool SW_IN, bool SW_OUT>
+// Twiddles come from the stage-ordered table (see stage_twiddles): entry
+// OFF + (r-1)*NS + k = exp(-2 pi i r k / (NS R)), so the lanes of a warp read
+// consecutive k for each r (two 128 B wavefronts) instead of r*k-strided
+// entries of a length-T table (up to 32 wavefronts per load).
+template <int T, int NT, int R, int NS, int OFF, bool SW_IN, bool SW_OUT>
 __device__ __forceinline__ void stage(float2 *buf, const float2 *__restrict__ tw) {
     constexpr int TR = T / R;
     constexpr int ITER = (TR + NT - 1) / NT;
-    constexpr int TWS = T / (NS * R);
     float2 v[ITER][R];
 #pragma unroll
     for (int t = 0; t < ITER; ++t) {
@@ -107,7 +112,7 @@ __device__ __forceinline__ void stage(float2 *buf, const float2 *__restrict__ tw
             const int k = j % NS;
             if (NS > 1) {
 #pragma unroll
-                for (int r = 1; r < R; ++r) v[t][r] = cmul(v[t][r], __ldg(tw + r * k * TWS));
+                for (int r = 1; r < R; ++r) v[t][r] = cmul(v[t][r], __ldg(tw + OFF + (r - 1) * NS + k));
             }
             dft<R>(v[t]);
             const int base = (j - k) * R + k;
@@ -122,17 +127,18 @@ __device__ __forceinline__ void stage(float2 *buf, const float2 *__restrict__ tw
 template <int T, int NT, int R0, int R1, int R2, int R3>
 __device__ __forceinline__ void fft(float2 *buf, const float2 *__restrict__ tw) {
     constexpr int N1 = R0, N2 = R0 * R1, N3 = R0 * R1 * R2;
+    constexpr int O2 = (R1 - 1) * N1, O3 = O2 + (R2 - 1) * N2;
     static_assert(R0 * R1 * R2 * R3 == T, "radix plan must multiply to T");
     // stage s writes at stride NS_s: swizzle its output when NS_s < 16
-    stage<T, NT, R0, 1, false, true>(buf, tw);
-    stage<T, NT, R1, N1, true, (N1 < 16)>(buf, tw);
+    stage<T, NT, R0, 1, 0, false, true>(buf, tw);
+    stage<T, NT, R1, N1, 0, true, (N1 < 16)>(buf, tw);
     if constexpr (R3 == 1) {
         static_assert(N2 >= 16, "last stage must write in natural order");
-        stage<T, NT, R2, N2, (N1 < 16), false>(buf, tw);
+        stage<T, NT, R2, N2, O2, (N1 < 16), false>(buf, tw);
     } else {
-        stage<T, NT, R2, N2, (N1 < 16), (N2 < 16)>(buf, tw);
+        stage<T, NT, R2, N2, O2, (N1 < 16), (N2 < 16)>(buf, tw);
         static_assert(N3 >= 16, "last stage must write in natural order");
-        stage<T, NT, R3, N3, (N2 < 16), false>(buf, tw);
+        stage<T, NT, R3, N3, O3, (N2 < 16), false>(buf, tw);
     }
 }
 
@@ -235,6 +241,35 @@ k_c2c(const float2 *__restrict__ in, long long in_stride, int in_len, float2 *__
 }  // namespace ct
 
 bool fft_ct_supported(int T) { return T == 1024 || T == 1536 || T == 2048 || T == 4096; }
+
+// Stage-ordered twiddle table of plan P, in the order fft<> reads it:
+// for stages 1.. (input length NS, radix R): (R-1) x NS entries
+// exp(-2 pi i r k / (NS R)), evaluated in double as the length-T table was.
+template <int T>
+static void stage_twiddles(std::vector<float2> &out) {
+    using P = ct::Plan<T>;
+    const int radix[4] = {P::R0, P::R1, P::R2, P::R3};
+    int ns = radix[0];
+    for (int s = 1; s < 4 && radix[s] > 1; ++s) {
+        const int R = radix[s];
+        for (int r = 1; r < R; ++r)
+            for (int k = 0; k < ns; ++k) {
+                const double a = -2.0 * M_PI * (double)(r * k * (T / (ns * R))) / (double)T;
+                out.push_back(make_float2((float)cos(a), (float)sin(a)));
+            }
+        ns *= R;
+    }
+}
+
+void fft_ct_twiddles(int T, std::vector<float2> &out) {
+    out.clear();
+    switch (T) {
+        case 1024: stage_twiddles<1024>(out); break;
+        case 1536: stage_twiddles<1536>(out); break;
+        case 2048: stage_twiddles<2048>(out); break;
+        case 4096: stage_twiddles<4096>(out); break;
+    }
+}
 
 template <int T>
 static int launch_r2c(const void *in, int in_kind, long long ntraces, float2 *out,
