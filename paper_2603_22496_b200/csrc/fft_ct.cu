@@ -3,20 +3,27 @@
 // are compile-time constants, so the Stockham stages are straight-line code.
 //
 // One CTA = one complex transform of length T (two real traces packed as
-// re/im for the forward real FFT).  The transform lives in ONE shared buffer;
-// each stage reads all of a thread's butterfly inputs into registers, barriers,
-// then writes the outputs in place (no ping-pong buffer: 8 B x T of shared
-// memory per CTA, so many CTAs per SM overlap their global loads with other
-// CTAs' arithmetic).  Stages whose output stride Ns < 16 would hit the same
-// shared-memory banks from neighbouring lanes write through an XOR swizzle
-// (index ^ ((index >> 3) & 15)), which the next stage reads back.
-// Twiddles exp(-2 pi i k / T): float64-accurate table in global memory (L1).
+// re/im for the forward real FFT), three Stockham stages R0 x R1 x R2 with
+// R0 = 16 (composite butterflies 16 = 4x4, 12 = 4x3, 8, 6 = 2x3 in registers).
+// The transform is bound by L1/shared-memory wavefronts (ncu, r1: LSU data
+// pipe 91-94% busy), so the layout minimises passes through shared memory:
+//   - stage 0 reads its butterfly inputs straight from global memory (lane j
+//     reads sample j + r T/R0: coalesced), no staging copy;
+//   - stages 0 and 1 write in place into ONE shared buffer (8 B x T); stage 0
+//     writes at stride 1 and goes through an XOR swizzle e ^ ((e >> 4) & 15)
+//     that stage 1 reads back; from stage 1 on, output strides are >= 16;
+//   - the last stage keeps its outputs in registers (natural order: lane j
+//     holds bins j + r T/R2): the complex transform stores them to global
+//     directly; the real-pair split writes them once to shared memory and
+//     reads back only the mirrored bin T - k it needs.
+// Twiddles: stage-ordered float32 table (stage_twiddles) so that lanes read
+// consecutive entries; butterfly-internal twiddles are compile-time constants.
 //
-// Measured (r1, config 4): a persistent cp.async-pipelined variant of the
-// real FFT was 22% slower than one CTA per pair (register cap -> fewer
-// resident CTAs), and a multi-pair CTA with cp.async double-buffered input
-// staging was 53% slower (237 registers uncapped; 64 capped -> 512 B spills),
-// so the simple form is the one kept.
+// Measured (r1, config 4, T = 1536, 28160 pairs): the previous four-stage
+// radix-8 form with a staging pass and a length-T twiddle table took 224 us
+// (177 us with the stage-ordered table); a persistent cp.async-pipelined
+// variant was 22% slower and a multi-pair CTA with cp.async double-buffered
+// staging 53% slower (register pressure), so one CTA per transform is kept.
 
 #include <algorithm>
 #include <cmath>
@@ -35,143 +42,219 @@ __device__ __forceinline__ float2 cmul(float2 a, float2 b) {
 }
 __device__ __forceinline__ float2 mul_mi(float2 a) { return make_float2(a.y, -a.x); }
 
+// compile-time exp(-2 pi i m / N), evaluated in double (Taylor series on the
+// angle reduced to [-pi, pi]) and rounded once to float
+__host__ __device__ constexpr double cx_cos(double x) {
+    double term = 1.0, sum = 1.0;
+    for (int n = 1; n < 40; ++n) {
+        term *= -x * x / ((2.0 * n - 1.0) * (2.0 * n));
+        sum += term;
+    }
+    return sum;
+}
+__host__ __device__ constexpr double cx_sin(double x) {
+    double term = x, sum = x;
+    for (int n = 1; n < 40; ++n) {
+        term *= -x * x / ((2.0 * n) * (2.0 * n + 1.0));
+        sum += term;
+    }
+    return sum;
+}
+template <int N>
+struct TwTab {
+    float re[N], im[N];
+    __host__ __device__ constexpr TwTab() : re(), im() {
+        constexpr double pi = 3.14159265358979323846;
+        for (int m = 0; m < N; ++m) {
+            double a = 2.0 * pi * (double)m / (double)N;  // [0, 2 pi)
+            if (a > pi) a -= 2.0 * pi;
+            re[m] = (float)cx_cos(a);
+            im[m] = (float)(-cx_sin(a));
+        }
+    }
+};
+
+// x * exp(-2 pi i m / N) with m a compile-time constant after unrolling
+template <int N>
+__device__ __forceinline__ float2 twc(float2 x, int m) {
+    constexpr TwTab<N> tab{};
+    m %= N;
+    if (m == 0) return x;
+    if (4 * m == N) return mul_mi(x);
+    if (2 * m == N) return make_float2(-x.x, -x.y);
+    if (4 * m == 3 * N) return make_float2(-x.y, x.x);
+    return cmul(x, make_float2(tab.re[m], tab.im[m]));
+}
+
 template <int R>
-__device__ __forceinline__ void dft(float2 *v);
+struct Dft;
 
 template <>
-__device__ __forceinline__ void dft<2>(float2 *v) {
-    float2 t = v[0];
-    v[0] = cadd(t, v[1]);
-    v[1] = csub(t, v[1]);
-}
-template <>
-__device__ __forceinline__ void dft<4>(float2 *v) {
-    float2 a0 = cadd(v[0], v[2]), a1 = csub(v[0], v[2]);
-    float2 a2 = cadd(v[1], v[3]), a3 = mul_mi(csub(v[1], v[3]));
-    v[0] = cadd(a0, a2);
-    v[2] = csub(a0, a2);
-    v[1] = cadd(a1, a3);
-    v[3] = csub(a1, a3);
-}
-template <>
-__device__ __forceinline__ void dft<8>(float2 *v) {
-    const float r = 0.70710678118654752440f;
-    float2 e[4] = {v[0], v[2], v[4], v[6]};
-    float2 o[4] = {v[1], v[3], v[5], v[7]};
-    dft<4>(e);
-    dft<4>(o);
-    o[1] = make_float2(r * (o[1].x + o[1].y), r * (o[1].y - o[1].x));
-    o[2] = mul_mi(o[2]);
-    o[3] = make_float2(r * (o[3].y - o[3].x), -r * (o[3].x + o[3].y));
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        v[k] = cadd(e[k], o[k]);
-        v[k + 4] = csub(e[k], o[k]);
+struct Dft<2> {
+    __device__ __forceinline__ static void run(float2 *v) {
+        float2 t = v[0];
+        v[0] = cadd(t, v[1]);
+        v[1] = csub(t, v[1]);
     }
-}
+};
 template <>
-__device__ __forceinline__ void dft<3>(float2 *v) {
-    const float s = 0.86602540378443864676f;
-    float2 t1 = cadd(v[1], v[2]);
-    float2 t2 = make_float2(fmaf(-0.5f, t1.x, v[0].x), fmaf(-0.5f, t1.y, v[0].y));
-    float2 t3 = csub(v[1], v[2]);
-    float2 t4 = make_float2(s * t3.y, -s * t3.x);
-    v[0] = cadd(v[0], t1);
-    v[1] = cadd(t2, t4);
-    v[2] = csub(t2, t4);
-}
-
-template <bool SW>
-__device__ __forceinline__ int swz(int e) {
-    return SW ? (e ^ ((e >> 3) & 15)) : e;
-}
-
-// One Stockham stage, in place: radix R, input sub-transform length NS.
-// Twiddles come from the stage-ordered table (see stage_twiddles): entry
-// OFF + (r-1)*NS + k = exp(-2 pi i r k / (NS R)), so the lanes of a warp read
-// consecutive k for each r (two 128 B wavefronts) instead of r*k-strided
-// entries of a length-T table (up to 32 wavefronts per load).
-template <int T, int NT, int R, int NS, int OFF, bool SW_IN, bool SW_OUT>
-__device__ __forceinline__ void stage(float2 *buf, const float2 *__restrict__ tw) {
-    constexpr int TR = T / R;
-    constexpr int ITER = (TR + NT - 1) / NT;
-    float2 v[ITER][R];
+struct Dft<3> {
+    __device__ __forceinline__ static void run(float2 *v) {
+        const float s = 0.86602540378443864676f;
+        float2 t1 = cadd(v[1], v[2]);
+        float2 t2 = make_float2(fmaf(-0.5f, t1.x, v[0].x), fmaf(-0.5f, t1.y, v[0].y));
+        float2 t3 = csub(v[1], v[2]);
+        float2 t4 = make_float2(s * t3.y, -s * t3.x);
+        v[0] = cadd(v[0], t1);
+        v[1] = cadd(t2, t4);
+        v[2] = csub(t2, t4);
+    }
+};
+template <>
+struct Dft<4> {
+    __device__ __forceinline__ static void run(float2 *v) {
+        float2 a0 = cadd(v[0], v[2]), a1 = csub(v[0], v[2]);
+        float2 a2 = cadd(v[1], v[3]), a3 = mul_mi(csub(v[1], v[3]));
+        v[0] = cadd(a0, a2);
+        v[2] = csub(a0, a2);
+        v[1] = cadd(a1, a3);
+        v[3] = csub(a1, a3);
+    }
+};
+template <>
+struct Dft<8> {
+    __device__ __forceinline__ static void run(float2 *v) {
+        const float r = 0.70710678118654752440f;
+        float2 e[4] = {v[0], v[2], v[4], v[6]};
+        float2 o[4] = {v[1], v[3], v[5], v[7]};
+        Dft<4>::run(e);
+        Dft<4>::run(o);
+        o[1] = make_float2(r * (o[1].x + o[1].y), r * (o[1].y - o[1].x));
+        o[2] = mul_mi(o[2]);
+        o[3] = make_float2(r * (o[3].y - o[3].x), -r * (o[3].x + o[3].y));
 #pragma unroll
-    for (int t = 0; t < ITER; ++t) {
-        const int j = threadIdx.x + t * NT;
-        if (TR % NT == 0 || j < TR) {
-#pragma unroll
-            for (int r = 0; r < R; ++r) v[t][r] = buf[swz<SW_IN>(j + r * TR)];
+        for (int k = 0; k < 4; ++k) {
+            v[k] = cadd(e[k], o[k]);
+            v[k + 4] = csub(e[k], o[k]);
         }
     }
-    __syncthreads();
+};
+// composite N = N1 x N2 (Cooley-Tukey, n = N2 n1 + n2, k = k1 + N1 k2)
+template <int N1, int N2>
+struct DftComp {
+    __device__ __forceinline__ static void run(float2 *v) {
+        constexpr int N = N1 * N2;
+        float2 a[N2][N1];
 #pragma unroll
-    for (int t = 0; t < ITER; ++t) {
-        const int j = threadIdx.x + t * NT;
-        if (TR % NT == 0 || j < TR) {
-            const int k = j % NS;
-            if (NS > 1) {
+        for (int n2 = 0; n2 < N2; ++n2) {
 #pragma unroll
-                for (int r = 1; r < R; ++r) v[t][r] = cmul(v[t][r], __ldg(tw + OFF + (r - 1) * NS + k));
-            }
-            dft<R>(v[t]);
-            const int base = (j - k) * R + k;
+            for (int n1 = 0; n1 < N1; ++n1) a[n2][n1] = v[N2 * n1 + n2];
+            Dft<N1>::run(a[n2]);
 #pragma unroll
-            for (int r = 0; r < R; ++r) buf[swz<SW_OUT>(base + r * NS)] = v[t][r];
+            for (int k1 = 0; k1 < N1; ++k1) a[n2][k1] = twc<N>(a[n2][k1], n2 * k1);
+        }
+#pragma unroll
+        for (int k1 = 0; k1 < N1; ++k1) {
+            float2 t[N2];
+#pragma unroll
+            for (int n2 = 0; n2 < N2; ++n2) t[n2] = a[n2][k1];
+            Dft<N2>::run(t);
+#pragma unroll
+            for (int k2 = 0; k2 < N2; ++k2) v[k1 + N1 * k2] = t[k2];
         }
     }
-    __syncthreads();
-}
-
-// Full transform: radices R0..R3 (R3 == 1: three stages).  Output natural order.
-template <int T, int NT, int R0, int R1, int R2, int R3>
-__device__ __forceinline__ void fft(float2 *buf, const float2 *__restrict__ tw) {
-    constexpr int N1 = R0, N2 = R0 * R1, N3 = R0 * R1 * R2;
-    constexpr int O2 = (R1 - 1) * N1, O3 = O2 + (R2 - 1) * N2;
-    static_assert(R0 * R1 * R2 * R3 == T, "radix plan must multiply to T");
-    // stage s writes at stride NS_s: swizzle its output when NS_s < 16
-    stage<T, NT, R0, 1, 0, false, true>(buf, tw);
-    stage<T, NT, R1, N1, 0, true, (N1 < 16)>(buf, tw);
-    if constexpr (R3 == 1) {
-        static_assert(N2 >= 16, "last stage must write in natural order");
-        stage<T, NT, R2, N2, O2, (N1 < 16), false>(buf, tw);
-    } else {
-        stage<T, NT, R2, N2, O2, (N1 < 16), (N2 < 16)>(buf, tw);
-        static_assert(N3 >= 16, "last stage must write in natural order");
-        stage<T, NT, R3, N3, O3, (N2 < 16), false>(buf, tw);
-    }
-}
+};
+template <>
+struct Dft<6> : DftComp<2, 3> {};
+template <>
+struct Dft<12> : DftComp<4, 3> {};
+template <>
+struct Dft<16> : DftComp<4, 4> {};
 
 template <int T>
 struct Plan;
 template <>
-struct Plan<1024> { static constexpr int NT = 64, R0 = 8, R1 = 8, R2 = 4, R3 = 4; };
+struct Plan<1024> { static constexpr int NT = 64, R0 = 16, R1 = 8, R2 = 8, R3 = 1; };
 template <>
-struct Plan<1536> {
-#ifndef KKB_FFT1536_NT
-#define KKB_FFT1536_NT 128  // measured: 128 threads beat 64 / 192 (fewer registers, more CTAs)
-#endif
-    static constexpr int NT = KKB_FFT1536_NT, R0 = 8, R1 = 8, R2 = 8, R3 = 3;
+struct Plan<1536> { static constexpr int NT = 128, R0 = 16, R1 = 12, R2 = 8, R3 = 1; };
+template <>
+struct Plan<2048> { static constexpr int NT = 128, R0 = 16, R1 = 16, R2 = 8, R3 = 1; };
+template <>
+struct Plan<4096> { static constexpr int NT = 256, R0 = 16, R1 = 16, R2 = 16, R3 = 1; };
+
+// registers of one stage: lane j handles butterflies j, j + NT, ... (< T/R);
+// butterfly j reads inputs j + r T/R and writes outputs base + r NS,
+// base = (j - j % NS) R + j % NS (Stockham, natural order after the last stage)
+template <int T, int NT, int R>
+struct Stage {
+    static constexpr int TR = T / R;
+    static constexpr int ITER = (TR + NT - 1) / NT;
+    float2 v[ITER][R];
+
+    __device__ __forceinline__ static int lane_j(int t) { return (int)threadIdx.x + t * NT; }
+    __device__ __forceinline__ static bool ok(int j) { return TR % NT == 0 || j < TR; }
+    __device__ __forceinline__ static int swz(int e) { return e ^ ((e >> 4) & 15); }
+
+    template <bool SW>
+    __device__ __forceinline__ void load(const float2 *buf) {
+#pragma unroll
+        for (int t = 0; t < ITER; ++t) {
+            const int j = lane_j(t);
+            if (ok(j)) {
+#pragma unroll
+                for (int r = 0; r < R; ++r) v[t][r] = buf[SW ? swz(j + r * TR) : j + r * TR];
+            }
+        }
+    }
+    // twiddles from the stage-ordered table (entry OFF + (r-1) NS + k), then DFT_R
+    template <int NS, int OFF>
+    __device__ __forceinline__ void compute(const float2 *__restrict__ tw) {
+#pragma unroll
+        for (int t = 0; t < ITER; ++t) {
+            const int j = lane_j(t);
+            if (ok(j)) {
+                if (NS > 1) {
+                    const int k = j % NS;
+#pragma unroll
+                    for (int r = 1; r < R; ++r)
+                        v[t][r] = cmul(v[t][r], __ldg(tw + OFF + (r - 1) * NS + k));
+                }
+                Dft<R>::run(v[t]);
+            }
+        }
+    }
+    template <int NS, bool SW>
+    __device__ __forceinline__ void store(float2 *buf) const {
+#pragma unroll
+        for (int t = 0; t < ITER; ++t) {
+            const int j = lane_j(t);
+            if (ok(j)) {
+                const int k = j % NS;
+                const int base = (j - k) * R + k;
+#pragma unroll
+                for (int r = 0; r < R; ++r) buf[SW ? swz(base + r * NS) : base + r * NS] = v[t][r];
+            }
+        }
+    }
 };
-template <>
-struct Plan<2048> { static constexpr int NT = 128, R0 = 8, R1 = 8, R2 = 8, R3 = 4; };
-template <>
-struct Plan<4096> { static constexpr int NT = 192, R0 = 8, R1 = 8, R2 = 8, R3 = 8; };
 
-template <int T>
-__device__ __forceinline__ void run_fft(float2 *buf, const float2 *tw) {
+// stages 1 and 2 of the plan on `buf` holding stage 0's swizzled output;
+// returns with stage 2's outputs (bins j + r T/R2) in `c`
+template <int T, typename S2>
+__device__ __forceinline__ void stages12(float2 *buf, const float2 *__restrict__ tw, S2 &c) {
     using P = Plan<T>;
-    fft<T, P::NT, P::R0, P::R1, P::R2, P::R3>(buf, tw);
+    Stage<T, P::NT, P::R1> b;
+    b.template load<true>(buf);
+    __syncthreads();
+    b.template compute<P::R0, 0>(tw);
+    b.template store<P::R0, false>(buf);
+    __syncthreads();
+    c.template load<false>(buf);
+    c.template compute<P::R0 * P::R1, (P::R1 - 1) * P::R0>(tw);
 }
 
-// four consecutive samples as float (float32 rows: one 16 B load; int16 rows:
-// one 8 B load, converted exactly — the reference consumes q.astype(float32))
-__device__ __forceinline__ float4 load4(const float *p) { return __ldg(reinterpret_cast<const float4 *>(p)); }
-__device__ __forceinline__ float4 load4(const short *p) {
-    const int2 u = __ldg(reinterpret_cast<const int2 *>(p));
-    return make_float4((float)(short)(u.x & 0xFFFF), (float)(short)(u.x >> 16),
-                       (float)(short)(u.y & 0xFFFF), (float)(short)(u.y >> 16));
-}
+__device__ __forceinline__ float to_f(float x) { return x; }
+__device__ __forceinline__ float to_f(short x) { return (float)x; }  // exact
 
 // Real-pair forward FFT: rows 2p, 2p+1 of `in` (length T) -> bins [0, K) of
 // each row's spectrum at out + row*out_stride, times bin_scale[k].
@@ -180,33 +263,59 @@ __global__ void __launch_bounds__(Plan<T>::NT)
 k_r2c(const InT *__restrict__ in, long long ntraces, float2 *__restrict__ out,
       long long out_stride, int K, const float *__restrict__ bin_scale,
       const float2 *__restrict__ tw) {
-    constexpr int NT = Plan<T>::NT;
+    using P = Plan<T>;
     __shared__ __align__(16) float2 buf[T];
     const long long r0 = 2 * (long long)blockIdx.x;
     const bool l1 = r0 + 1 < ntraces;
     const InT *x0 = in + r0 * T;
     const InT *x1 = in + (l1 ? r0 + 1 : r0) * T;
+    using S0 = Stage<T, P::NT, P::R0>;
+    S0 a;
 #pragma unroll
-    for (int i = threadIdx.x; i < T / 4; i += NT) {
-        const float4 u = load4(x0 + 4 * i);
-        float4 w = load4(x1 + 4 * i);
-        if (!l1) w = make_float4(0.f, 0.f, 0.f, 0.f);
-        buf[4 * i] = make_float2(u.x, w.x);
-        buf[4 * i + 1] = make_float2(u.y, w.y);
-        buf[4 * i + 2] = make_float2(u.z, w.z);
-        buf[4 * i + 3] = make_float2(u.w, w.w);
+    for (int t = 0; t < S0::ITER; ++t) {
+        const int j = S0::lane_j(t);
+        if (S0::ok(j)) {
+#pragma unroll
+            for (int r = 0; r < P::R0; ++r) {
+                const int e = j + r * S0::TR;
+                const float im = to_f(__ldg(x1 + e));
+                a.v[t][r] = make_float2(to_f(__ldg(x0 + e)), l1 ? im : 0.f);
+            }
+        }
+    }
+    a.template compute<1, 0>(tw);
+    a.template store<1, true>(buf);
+    __syncthreads();
+    using S2 = Stage<T, P::NT, P::R2>;
+    S2 c;
+    stages12<T>(buf, tw, c);
+    __syncthreads();  // every stage-2 input read before the bins overwrite buf
+#pragma unroll
+    for (int t = 0; t < S2::ITER; ++t) {
+        const int j = S2::lane_j(t);
+        if (S2::ok(j)) {
+#pragma unroll
+            for (int r = 0; r < P::R2; ++r) buf[j + r * S2::TR] = c.v[t][r];
+        }
     }
     __syncthreads();
-    run_fft<T>(buf, tw);
     float2 *o0 = out + r0 * out_stride;
     float2 *o1 = out + (r0 + 1) * out_stride;
-    for (int k = threadIdx.x; k < K; k += NT) {
-        const float2 zk = buf[k];
-        const float2 zn = buf[k == 0 ? 0 : T - k];
-        const float s = 0.5f * (bin_scale ? bin_scale[k] : 1.0f);
-        // X0 = (Z_k + conj(Z_-k)) / 2 ; X1 = (Z_k - conj(Z_-k)) / (2i)
-        o0[k] = make_float2(s * (zk.x + zn.x), s * (zk.y - zn.y));
-        if (l1) o1[k] = make_float2(s * (zk.y + zn.y), -s * (zk.x - zn.x));
+#pragma unroll
+    for (int t = 0; t < S2::ITER; ++t) {
+        const int j = S2::lane_j(t);
+#pragma unroll
+        for (int r = 0; r < P::R2; ++r) {
+            const int k = j + r * S2::TR;
+            if (S2::ok(j) && k < K) {
+                const float2 zk = c.v[t][r];
+                const float2 zn = buf[k == 0 ? 0 : T - k];
+                const float s = 0.5f * (bin_scale ? __ldg(bin_scale + k) : 1.0f);
+                // X0 = (Z_k + conj(Z_-k)) / 2 ; X1 = (Z_k - conj(Z_-k)) / (2i)
+                o0[k] = make_float2(s * (zk.x + zn.x), s * (zk.y - zn.y));
+                if (l1) o1[k] = make_float2(s * (zk.y + zn.y), -s * (zk.x - zn.x));
+            }
+        }
     }
 }
 
@@ -216,25 +325,42 @@ template <int T, bool INV>
 __global__ void __launch_bounds__(Plan<T>::NT)
 k_c2c(const float2 *__restrict__ in, long long in_stride, int in_len, float2 *__restrict__ out,
       long long out_stride, int out_len, float scale, const float2 *__restrict__ tw) {
-    constexpr int NT = Plan<T>::NT;
+    using P = Plan<T>;
     __shared__ __align__(16) float2 buf[T];
     const long long row = blockIdx.x;
     const float2 *src = in + row * in_stride;
     const float sg = INV ? -1.f : 1.f;
+    using S0 = Stage<T, P::NT, P::R0>;
+    S0 a;
 #pragma unroll
-    for (int t = threadIdx.x; t < T; t += NT) {
-        float2 v = make_float2(0.f, 0.f);
-        if (t < in_len) v = __ldg(src + t);
-        buf[t] = make_float2(v.x, sg * v.y);
+    for (int t = 0; t < S0::ITER; ++t) {
+        const int j = S0::lane_j(t);
+        if (S0::ok(j)) {
+#pragma unroll
+            for (int r = 0; r < P::R0; ++r) {
+                const int e = j + r * S0::TR;
+                float2 v = make_float2(0.f, 0.f);
+                if (e < in_len) v = __ldg(src + e);
+                a.v[t][r] = make_float2(v.x, sg * v.y);
+            }
+        }
     }
+    a.template compute<1, 0>(tw);
+    a.template store<1, true>(buf);
     __syncthreads();
-    run_fft<T>(buf, tw);
+    using S2 = Stage<T, P::NT, P::R2>;
+    S2 c;
+    stages12<T>(buf, tw, c);
     float2 *dst = out + row * out_stride;
     const float sy = sg * scale;
 #pragma unroll
-    for (int t = threadIdx.x; t < out_len; t += NT) {
-        const float2 v = buf[t];
-        dst[t] = make_float2(v.x * scale, v.y * sy);
+    for (int t = 0; t < S2::ITER; ++t) {
+        const int j = S2::lane_j(t);
+#pragma unroll
+        for (int r = 0; r < P::R2; ++r) {
+            const int k = j + r * S2::TR;
+            if (S2::ok(j) && k < out_len) dst[k] = make_float2(c.v[t][r].x * scale, c.v[t][r].y * sy);
+        }
     }
 }
 
