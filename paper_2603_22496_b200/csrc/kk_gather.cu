@@ -536,25 +536,44 @@ int kk_gather(const float2 *data, int N, int M, int T, const double *ltx, const 
 }
 
 // ------------------------------------------------------------- K6 epilogues
-__global__ void k_log_compress(const float *__restrict__ inten, const unsigned *__restrict__ fmax,
-                               int n_frames, long long P, float floor_db, float *db) {
-    const long long total = (long long)n_frames * P;
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
-         i += (long long)gridDim.x * blockDim.x) {
-        int f = (int)(i / P);
-        float mx = __uint_as_float(fmax[f]);
-        float v = inten[i];
-        float d = (mx > 0.f && v > 0.f) ? 10.0f * log10f(v / mx) : floor_db;
-        db[i] = fmaxf(d, floor_db);
+// one CTA row per frame (blockIdx.y); float4 body when P % 4 == 0 and both
+// buffers are 16 B aligned
+__device__ __forceinline__ float db_of(float v, float mx, float floor_db) {
+    const float d = (mx > 0.f && v > 0.f) ? 10.0f * log10f(v / mx) : floor_db;
+    return fmaxf(d, floor_db);
+}
+
+__global__ void __launch_bounds__(256)
+k_log_compress(const float *__restrict__ inten, const unsigned *__restrict__ fmax, long long P,
+               float floor_db, float *db, bool vec) {
+    const int f = blockIdx.y;
+    const float mx = __uint_as_float(fmax[f]);
+    const float *src = inten + (long long)f * P;
+    float *dst = db + (long long)f * P;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    const long long t0 = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (vec) {
+        const float4 *s4 = reinterpret_cast<const float4 *>(src);
+        float4 *d4 = reinterpret_cast<float4 *>(dst);
+        for (long long i = t0; i < P / 4; i += stride) {
+            const float4 v = __ldcs(s4 + i);  // read once: stream past L2
+            __stcs(d4 + i, make_float4(db_of(v.x, mx, floor_db), db_of(v.y, mx, floor_db),
+                                       db_of(v.z, mx, floor_db), db_of(v.w, mx, floor_db)));
+        }
+    } else {
+        for (long long i = t0; i < P; i += stride) dst[i] = db_of(src[i], mx, floor_db);
     }
 }
 
 int log_compress(const float *inten, const unsigned *fmax, int n_frames, long long P, float floor_db,
                  float *db, cudaStream_t s) {
-    long long total = (long long)n_frames * P;
-    if (total <= 0) return KKB_OK;
-    int blocks = (int)std::min<long long>(ceil_div(total, 256), 148 * 16);
-    k_log_compress<<<blocks, 256, 0, s>>>(inten, fmax, n_frames, P, floor_db, db);
+    if ((long long)n_frames * P <= 0) return KKB_OK;
+    if (n_frames > 65535) return KKB_ERR_UNSUPPORTED;
+    const bool vec = (P & 3) == 0 && (((uintptr_t)inten | (uintptr_t)db) & 15) == 0;
+    const long long per = vec ? P / 4 : P;
+    const int bx = (int)std::max<long long>(1, std::min<long long>(ceil_div(per, 256),
+                                                                   std::max(1, 148 * 8 / n_frames)));
+    k_log_compress<<<dim3(bx, n_frames), 256, 0, s>>>(inten, fmax, P, floor_db, db, vec);
     KKB_CHECK_LAUNCH("k_log_compress");
     return KKB_OK;
 }

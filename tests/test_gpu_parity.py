@@ -67,6 +67,17 @@ def test_analytic_signal_odd_and_prime_lengths(oracle):
         assert rel_l2(out, ref) <= 1e-5, T
 
 
+@pytest.mark.parametrize("T", [1024, 1536, 2048, 4096])
+def test_compile_time_fft_lengths(oracle, T):
+    # the compile-time radix plans (fft_ct.cu) against numpy, odd trace count
+    # so the last real pair is half-empty
+    x = np.random.default_rng(T).standard_normal((1, 7, T)).astype(np.float32)
+    arr = kb.TransducerArray(7, 0.23e-3, 5.2e6, 20.83e6, 0.67)
+    out = kb.analytic_signal(kb.RFVolume(x, arr, kb.AcquisitionParams(C, [0.0], T))).data
+    ref = oracle.analytic_signal(x)
+    assert rel_l2(out, ref) <= 1e-6, T
+
+
 def test_analytic_real_part_preserves_input():
     x = np.random.default_rng(0).standard_normal((1, 4, 128)).astype(np.float32)
     arr = kb.TransducerArray(4, 0.23e-3, 5.2e6, 20.83e6, 0.67)
