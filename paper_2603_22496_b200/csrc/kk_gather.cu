@@ -271,8 +271,8 @@ k_kk_gather(const KKArgs a) {
     double *lrx_p = lrz_p + M * TZ;                                    // [M][TX] packed cols
     double *ltz_p = lrx_p + M * TX;                                    // [N][TZ]
     double *ltx_p = ltz_p + N * TZ;                                    // [N][TX]
-    float *w_s = reinterpret_cast<float *>(ltx_p + N * TX);            // [M]
-    int *lo_s = reinterpret_cast<int *>(w_s + M);                      // [N][M]
+    // per (n, m): window start lo and weight w[m] (bits), one 8 B read per receive
+    int2 *lw_s = reinterpret_cast<int2 *>(ltx_p + N * TX);             // [N][M]
 
     const int tid = threadIdx.x;
     const int f = blockIdx.z;
@@ -301,7 +301,6 @@ k_kk_gather(const KKArgs a) {
         int n = i / TX, c = i - n * TX;
         ltx_p[n * TX + pcol(c)] = a.ltx[(long long)min(ix0 + c, nx - 1) * N + n];
     }
-    for (int i = tid; i < M; i += NT) w_s[i] = a.w ? (float)a.w[i] : 1.0f;
     __syncthreads();
 
     const double fs = a.fs, shift = a.shift;
@@ -318,7 +317,7 @@ k_kk_gather(const KKArgs a) {
                 lo = fmin(lo, kk_delay(t1, lrz_p[m * TZ + prow(r)], lrx_p[m * TX + pcol(c)], fs, shift));
             }
         lo = fmax(fmin(floor(lo) - 1.0, 1.0e9), -1.0e9);
-        lo_s[i] = (int)lo;
+        lw_s[i] = make_int2((int)lo, __float_as_int(a.w ? (float)a.w[m] : 1.0f));
     }
     __syncthreads();
 
@@ -336,14 +335,14 @@ k_kk_gather(const KKArgs a) {
     auto load_stage = [&](int n, int m0) {
         const int cnt = min(MCH, M - m0) * W;
         const float2 *base = dframe + (long long)(n * M + m0) * T;
-        const int *lo_q = lo_s + n * M + m0;
+        const int2 *lo_q = lw_s + n * M + m0;
 #pragma unroll
         for (int i = 0; i < EPT; ++i) {
             const int idx = tid + i * NT;
             s0[i] = s1[i] = make_float2(0.f, 0.f);
             if (idx < cnt) {
                 const int q = qe[i] >> 16, e = qe[i] & 0xFFFF;
-                const int smp = lo_q[q] + e;
+                const int smp = lo_q[q].x + e;
                 const float2 *tr = base + q * T;
                 // entry smp stays zero unless a tap at smp is in the reference's
                 // window: linear 0 <= i0 <= T-2 (both d0, d1 exist), nearest 0 <= j <= T-1
@@ -408,18 +407,19 @@ k_kk_gather(const KKArgs a) {
             t1[1][1] = __dadd_rn(tx.y, tz.y);
         }
         const Entry *wb = win + buf * MCH * W;
-        const int *lo_n = lo_s + n * M + m0;
+        const int2 *lw_n = lw_s + n * M + m0;
         constexpr int kQUnroll = KKB_KK_QUNROLL;
 #pragma unroll kQUnroll
         for (int q = 0; q < mc; ++q) {
             const int m = m0 + q;
             const double2 lz = reinterpret_cast<const double2 *>(lrz_p + m * TZ)[zq];
             const double2 lx = reinterpret_cast<const double2 *>(lrx_p + m * TX)[xq];
-            const float wm = w_s[m];
+            const int2 lw = lw_n[q];
+            const float wm = __int_as_float(lw.y);
             // window index e = floor(arg) - lo = hi(sv) - (0x41380000 + lo); the
             // in-window predicate of tap_index() is folded into the staged window
             // (entries whose tap would be invalid are zero), so no per-tap test
-            const int loC = lo_n[q] + KKB_MAGIC2_HI;
+            const int loC = lw.x + KKB_MAGIC2_HI;
             const Entry *wv = wb + q * W;
 #pragma unroll
             for (int p = 0; p < 2; ++p) {
@@ -442,6 +442,7 @@ k_kk_gather(const KKArgs a) {
                 }
             }
         }
+#if KKB_KK_F64_TOTAL
         if (ch == nchunk - 1) {
 #pragma unroll
             for (int p = 0; p < 2; ++p)
@@ -452,6 +453,7 @@ k_kk_gather(const KKArgs a) {
                     accr[p][r] = acci[p][r] = 0.f;
                 }
         }
+#endif
         // buffer buf^1 was last read in stage s-1, which every thread finished
         // before the barrier that ended it
         if (s + 1 < nstage) store_stage(ch1 * MCH, buf ^ 1);
@@ -469,15 +471,20 @@ k_kk_gather(const KKArgs a) {
         for (int r = 0; r < 2; ++r) {
             const int ix = ix0 + wx * 16 + r * 8 + xt;
             if (iz < nz && ix < nx) {
+#if KKB_KK_F64_TOTAL
+                const kk_total_t vr = accd_r[p][r], vi = accd_i[p][r];
+#else
+                const float vr = accr[p][r], vi = acci[p][r];  // float32 totals: one accumulator
+#endif
                 const long long px = (long long)f * a.out_fs + (long long)ix * nz + iz;
                 if (a.out_kind == KKB_OUT_C128) {
-                    reinterpret_cast<double2 *>(a.out)[px] = make_double2(accd_r[p][r], accd_i[p][r]);
+                    reinterpret_cast<double2 *>(a.out)[px] = make_double2(vr, vi);
                 } else {
                     reinterpret_cast<float2 *>(a.out)[px] =
-                        make_float2((float)accd_r[p][r], (float)accd_i[p][r]);
+                        make_float2((float)vr, (float)vi);
                 }
                 if (a.inten) {
-                    float I = (float)(accd_r[p][r] * accd_r[p][r] + accd_i[p][r] * accd_i[p][r]);
+                    float I = (float)(vr * vr + vi * vi);
                     a.inten[px] = I;
                     fmx = fmaxf(fmx, I);
                 }
@@ -494,7 +501,7 @@ static size_t kk_smem_bytes(int N, int M, int W, int MCH, bool linear) {
     size_t entry = linear ? sizeof(float4) : sizeof(float2);
     return entry * 2 * MCH * W +
            sizeof(double) * ((size_t)(M + N) * KKB_KK_TZ + (size_t)(M + N) * KKB_KK_TX) +
-           sizeof(float) * M + sizeof(int) * (size_t)N * M;
+           sizeof(int2) * (size_t)N * M;
 }
 
 int kk_gather(const float2 *data, int N, int M, int T, const double *ltx, const double *ltzT,
