@@ -3,8 +3,8 @@
 
 #include <cuda_runtime.h>
 
-// kk gather tile: TZ = 8*WZ depth rows x TX = 16*WX lateral columns per CTA
-// (a warp covers 8 x 16 pixels, 2 x 2 per lane)
+// kk gather tile: TZ = 8*WZ depth rows x TX = 8*CX*WX lateral columns per CTA
+// (a warp covers 8 x 8CX pixels, 2 x CX per lane)
 #ifndef KKB_KK_WZ
 #define KKB_KK_WZ 4   // warps along depth
 #endif
@@ -20,13 +20,16 @@ typedef double kk_total_t;
 #else
 typedef float kk_total_t;
 #endif
+#ifndef KKB_KK_CX
+#define KKB_KK_CX 4   // pixel columns per lane (measured r1: 4 beats 2 by 14%, 8 spills)
+#endif
 #define KKB_KK_TZ (8 * KKB_KK_WZ)
-#define KKB_KK_TX (16 * KKB_KK_WX)
+#define KKB_KK_TX (8 * KKB_KK_CX * KKB_KK_WX)
 #ifndef KKB_KK_STAGE_ELEMS
 #define KKB_KK_STAGE_ELEMS 1024  // window entries staged per pipeline stage
 #endif
 #ifndef KKB_KK_MIN_CTAS
-#define KKB_KK_MIN_CTAS 3        // occupancy target (caps registers at 85)
+#define KKB_KK_MIN_CTAS 2        // occupancy target (caps registers at 128)
 #endif
 #ifndef KKB_KK_QUNROLL
 #define KKB_KK_QUNROLL 1         // receive-loop unroll of the gather

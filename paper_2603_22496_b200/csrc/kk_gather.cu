@@ -223,9 +223,9 @@ int kk_window(const double *ltx, const double *ltz, const double *lrx, const dou
 }
 
 // ------------------------------------------------------------- K5 kernel
-// Tile: TZ = 8*WZ depth rows x TX = 16*WX lateral columns.  A warp covers an
-// 8 x 16 patch; lane (zt, xt) = (lane % 4, lane / 4) owns the 2 x 2 pixels
-// rows zt + {0, 4}, columns xt + {0, 8} of it.  For a fixed (a, b) the 32
+// Tile: TZ = 8*WZ depth rows x TX = 8*CX*WX lateral columns.  A warp covers an
+// 8 x 8CX patch; lane (zt, xt) = (lane % 4, lane / 4) owns the 2 x CX pixels
+// rows zt + {0, 4}, columns xt + 8j (j < CX) of it.  For a fixed (a, b) the 32
 // lanes form a 4 x 8 block whose delays span only ~3*dfi/dz + 7*dfi/dx
 // samples, so their tap reads hit a few shared-memory words (broadcast).
 struct KKArgs {
@@ -250,14 +250,18 @@ struct KKArgs {
 
 // packed LUT index: tile row r -> (r/8)*4 + r%4 pair slot, a = (r/4)&1
 __device__ __forceinline__ int prow(int r) { return ((r >> 3) << 3) + ((r & 3) << 1) + ((r >> 2) & 1); }
-// tile column c -> (c/16)*8 + c%8 pair slot, b = (c/8)&1
-__device__ __forceinline__ int pcol(int c) { return ((c >> 4) << 4) + ((c & 7) << 1) + ((c >> 3) & 1); }
+// tile column c -> warp block c/(8CX), lane slot c%8, column j = (c/8)%CX: the
+// CX columns of one lane are contiguous (CX/2 16-byte reads)
+template <int CX>
+__device__ __forceinline__ int pcol(int c) {
+    return (c / (8 * CX)) * (8 * CX) + (c & 7) * CX + ((c >> 3) % CX);
+}
 
-template <int WZ, int WX, bool LINEAR>
+template <int WZ, int WX, int CX, bool LINEAR>
 __global__ void __launch_bounds__(WZ *WX * 32, KKB_KK_MIN_CTAS)
 k_kk_gather(const KKArgs a) {
     constexpr int TZ = 8 * WZ;
-    constexpr int TX = 16 * WX;
+    constexpr int TX = 8 * CX * WX;
     constexpr int NT = WZ * WX * 32;
     constexpr int EPT = KKB_KK_STAGE_ELEMS / NT;  // staged window entries per thread
     using Entry = typename std::conditional<LINEAR, float4, float2>::type;
@@ -281,7 +285,7 @@ k_kk_gather(const KKArgs a) {
     const int wz = warp % WZ, wx = warp / WZ;
     const int zt = lane & 3, xt = lane >> 2;
     const int zq = wz * 4 + zt;   // packed row-pair slot (rows zq-> r, r+4)
-    const int xq = wx * 8 + xt;   // packed col-pair slot (cols c, c+8)
+    const int xq = wx * 8 + xt;   // packed column slot (cols c + 8j, j < CX)
     const int rzb = min(TZ - 1, nz - 1 - iz0);
     const int cxb = min(TX - 1, nx - 1 - ix0);
 
@@ -295,11 +299,11 @@ k_kk_gather(const KKArgs a) {
     }
     for (int i = tid; i < M * TX; i += NT) {
         int m = i / TX, c = i - m * TX;
-        lrx_p[m * TX + pcol(c)] = a.lrx[(long long)min(ix0 + c, nx - 1) * M + m];
+        lrx_p[m * TX + pcol<CX>(c)] = a.lrx[(long long)min(ix0 + c, nx - 1) * M + m];
     }
     for (int i = tid; i < N * TX; i += NT) {
         int n = i / TX, c = i - n * TX;
-        ltx_p[n * TX + pcol(c)] = a.ltx[(long long)min(ix0 + c, nx - 1) * N + n];
+        ltx_p[n * TX + pcol<CX>(c)] = a.ltx[(long long)min(ix0 + c, nx - 1) * N + n];
     }
     __syncthreads();
 
@@ -313,8 +317,8 @@ k_kk_gather(const KKArgs a) {
 #pragma unroll
             for (int cc = 0; cc < 2; ++cc) {
                 const int r = cr ? rzb : 0, c = cc ? cxb : 0;
-                const double t1 = __dadd_rn(ltx_p[n * TX + pcol(c)], ltz_p[n * TZ + prow(r)]);
-                lo = fmin(lo, kk_delay(t1, lrz_p[m * TZ + prow(r)], lrx_p[m * TX + pcol(c)], fs, shift));
+                const double t1 = __dadd_rn(ltx_p[n * TX + pcol<CX>(c)], ltz_p[n * TZ + prow(r)]);
+                lo = fmin(lo, kk_delay(t1, lrz_p[m * TZ + prow(r)], lrx_p[m * TX + pcol<CX>(c)], fs, shift));
             }
         lo = fmax(fmin(floor(lo) - 1.0, 1.0e9), -1.0e9);
         lw_s[i] = make_int2((int)lo, __float_as_int(a.w ? (float)a.w[m] : 1.0f));
@@ -371,13 +375,13 @@ k_kk_gather(const KKArgs a) {
         }
     };
 
-    kk_total_t accd_r[2][2], accd_i[2][2];
-    float accr[2][2], acci[2][2];
-    double t1[2][2];
+    kk_total_t accd_r[2][CX], accd_i[2][CX];
+    float accr[2][CX], acci[2][CX];
+    double t1[2][CX];
 #pragma unroll
     for (int p = 0; p < 2; ++p)
 #pragma unroll
-        for (int q = 0; q < 2; ++q) {
+        for (int q = 0; q < CX; ++q) {
             accd_r[p][q] = accd_i[p][q] = 0.0;
             accr[p][q] = acci[p][q] = 0.f;
         }
@@ -400,11 +404,18 @@ k_kk_gather(const KKArgs a) {
         if (s + 1 < nstage) load_stage(n1, ch1 * MCH);  // in flight during this stage's sums
         if (ch == 0) {
             const double2 tz = reinterpret_cast<const double2 *>(ltz_p + n * TZ)[zq];
-            const double2 tx = reinterpret_cast<const double2 *>(ltx_p + n * TX)[xq];
-            t1[0][0] = __dadd_rn(tx.x, tz.x);
-            t1[0][1] = __dadd_rn(tx.y, tz.x);
-            t1[1][0] = __dadd_rn(tx.x, tz.y);
-            t1[1][1] = __dadd_rn(tx.y, tz.y);
+            double txv[CX];
+#pragma unroll
+            for (int j = 0; j < CX / 2; ++j) {
+                const double2 tx = reinterpret_cast<const double2 *>(ltx_p + n * TX + xq * CX)[j];
+                txv[2 * j] = tx.x;
+                txv[2 * j + 1] = tx.y;
+            }
+#pragma unroll
+            for (int j = 0; j < CX; ++j) {
+                t1[0][j] = __dadd_rn(txv[j], tz.x);
+                t1[1][j] = __dadd_rn(txv[j], tz.y);
+            }
         }
         const Entry *wb = win + buf * MCH * W;
         const int2 *lw_n = lw_s + n * M + m0;
@@ -413,7 +424,13 @@ k_kk_gather(const KKArgs a) {
         for (int q = 0; q < mc; ++q) {
             const int m = m0 + q;
             const double2 lz = reinterpret_cast<const double2 *>(lrz_p + m * TZ)[zq];
-            const double2 lx = reinterpret_cast<const double2 *>(lrx_p + m * TX)[xq];
+            double lxv[CX];
+#pragma unroll
+            for (int j = 0; j < CX / 2; ++j) {
+                const double2 lx = reinterpret_cast<const double2 *>(lrx_p + m * TX + xq * CX)[j];
+                lxv[2 * j] = lx.x;
+                lxv[2 * j + 1] = lx.y;
+            }
             const int2 lw = lw_n[q];
             const float wm = __int_as_float(lw.y);
             // window index e = floor(arg) - lo = hi(sv) - (0x41380000 + lo); the
@@ -424,8 +441,8 @@ k_kk_gather(const KKArgs a) {
 #pragma unroll
             for (int p = 0; p < 2; ++p) {
 #pragma unroll
-                for (int r = 0; r < 2; ++r) {
-                    const double fi = kk_delay(t1[p][r], p ? lz.y : lz.x, r ? lx.y : lx.x, fs, shift);
+                for (int r = 0; r < CX; ++r) {
+                    const double fi = kk_delay(t1[p][r], p ? lz.y : lz.x, lxv[r], fs, shift);
                     const double sv = __dadd_rd(LINEAR ? fi : __dadd_rn(fi, 0.5), KKB_FLOOR_MAGIC2);
                     const unsigned e = min((unsigned)(__double2hiint(sv) - loC),
                                            (unsigned)(LINEAR ? W - 2 : W - 1));
@@ -447,7 +464,7 @@ k_kk_gather(const KKArgs a) {
 #pragma unroll
             for (int p = 0; p < 2; ++p)
 #pragma unroll
-                for (int r = 0; r < 2; ++r) {
+                for (int r = 0; r < CX; ++r) {
                     accd_r[p][r] += (kk_total_t)accr[p][r];
                     accd_i[p][r] += (kk_total_t)acci[p][r];
                     accr[p][r] = acci[p][r] = 0.f;
@@ -468,8 +485,8 @@ k_kk_gather(const KKArgs a) {
     for (int p = 0; p < 2; ++p) {
         const int iz = iz0 + wz * 8 + p * 4 + zt;
 #pragma unroll
-        for (int r = 0; r < 2; ++r) {
-            const int ix = ix0 + wx * 16 + r * 8 + xt;
+        for (int r = 0; r < CX; ++r) {
+            const int ix = ix0 + wx * 8 * CX + r * 8 + xt;
             if (iz < nz && ix < nx) {
 #if KKB_KK_F64_TOTAL
                 const kk_total_t vr = accd_r[p][r], vi = accd_i[p][r];
@@ -528,12 +545,12 @@ int kk_gather(const float2 *data, int N, int M, int T, const double *ltx, const 
     dim3 grid((unsigned)ceil_div(nz, KKB_KK_TZ), (unsigned)ceil_div(nx, KKB_KK_TX), (unsigned)n_frames);
     dim3 block(KKB_KK_WZ * KKB_KK_WX * 32);
     if (linear) {
-        auto fn = k_kk_gather<KKB_KK_WZ, KKB_KK_WX, true>;
+        auto fn = k_kk_gather<KKB_KK_WZ, KKB_KK_WX, KKB_KK_CX, true>;
         KKB_TRY_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm),
                      "smem attr kk");
         fn<<<grid, block, sm, s>>>(a);
     } else {
-        auto fn = k_kk_gather<KKB_KK_WZ, KKB_KK_WX, false>;
+        auto fn = k_kk_gather<KKB_KK_WZ, KKB_KK_WX, KKB_KK_CX, false>;
         KKB_TRY_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm),
                      "smem attr kk");
         fn<<<grid, block, sm, s>>>(a);

@@ -1,0 +1,71 @@
+// Microbenchmark: shared-memory wavefront cost of a 128-bit warp load as a
+// function of the lane -> address pattern (informs the K5 lane layout).
+#include <cstdio>
+#include <cuda_runtime.h>
+
+__device__ __forceinline__ int pat(int p, int lane) {
+    switch (p) {
+        case 0: return lane;              // 32 distinct, consecutive
+        case 1: return 0;                 // broadcast
+        case 2: return lane & 3;          // 4 distinct, cycling
+        case 3: return lane >> 2;         // 8 distinct, groups of 4
+        case 4: return lane >> 3;         // 4 distinct, groups of 8
+        case 5: return lane & 7;          // 8 distinct, cycling
+        case 6: return lane >> 1;         // 16 distinct, pairs
+        case 7: return lane & 15;         // 16 distinct, cycling
+        case 8: return (lane * 7) & 15;   // 16 distinct, shuffled
+        case 9: return (lane >> 2) + 8 * (lane & 1);  // mixed
+        case 10: return lane >> 4;        // 2 distinct, halves
+        case 11: return (lane & 1) * 8;   // 2 distinct, 128 B apart
+        case 12: return (lane >> 2) * 2;  // 8 distinct, stride 32 B
+        case 13: return lane * 2;         // 32 distinct, stride 32 B
+    }
+    return 0;
+}
+
+__global__ void k(int p, int iters, float *out) {
+    __shared__ __align__(16) float4 s[2048];
+    for (int i = threadIdx.x; i < 2048; i += blockDim.x) s[i] = make_float4(i, i, i, i);
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    unsigned a = (unsigned)__cvta_generic_to_shared(&s[(pat(p, lane) + warp * 32) & 127]);
+    float acc = 0.f;
+    for (int i = 0; i < iters; ++i) {
+        float x, y, z, w;
+        const unsigned ai = a ^ ((i & 7) << 11);
+        asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(x), "=f"(y), "=f"(z), "=f"(w) : "r"(ai) : "memory");
+        acc += (x + y) * (z + w);
+        asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4+16];" : "=f"(x), "=f"(y), "=f"(z), "=f"(w) : "r"(ai) : "memory");
+        acc += (x + z) * (y + w);
+    }
+    if (acc == -1.f) out[0] = acc;
+}
+
+int main() {
+    float *out;
+    cudaMalloc(&out, 4);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    int sms;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    const int iters = 4096, threads = 512, blocks = sms * 4;
+    const char *names[] = {"lane", "bcast", "lane&3", "lane>>2", "lane>>3", "lane&7", "lane>>1",
+                           "lane&15", "(lane*7)&15", "mixed", "lane>>4", "(lane&1)*8", "(lane>>2)*2", "lane*2"};
+    for (int p = 0; p < 14; ++p) {
+        k<<<blocks, threads>>>(p, iters, out);
+        cudaEventRecord(e0);
+        k<<<blocks, threads>>>(p, iters, out);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float ms;
+        cudaEventElapsedTime(&ms, e0, e1);
+        double warp_loads = (double)blocks * threads / 32 * iters * 2;
+        int clk;
+        cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
+        double cyc = ms * 1e-3 * clk * 1e3 * sms;  // SM-cycles (at the nominal clock)
+        printf("%-14s %.3f SM-cycles per warp LDS.128 (%.3f ms, %s)\n", names[p], cyc / warp_loads, ms,
+               cudaGetErrorString(cudaGetLastError()));
+    }
+    return 0;
+}
