@@ -181,6 +181,21 @@ int kkb_log_compress(const float *intensity, const unsigned int *frame_max, int 
 int kkb_compound(const void *images, int n_images, long long n_pixels, int mode,
                  double *out, void *stream);
 
+/* ------------------------------------------------------------ K8: forward RF simulator
+ * Replaces _render_traces (simulate.py:187-220), the kernel of simulate_rf
+ * (simulate.py:223-296): adds the pulse echo of every scatterer (input order)
+ * to out (n_tx, n_el, n_t) float32 (accumulates: simulate_rf passes zeros).
+ * sx, sz, refl: (n_sc,) float64; upos (n_el,); sin_t, cos_t (n_tx,) numpy's
+ * np.sin/np.cos of the transmit angles; wave (n_w,) the pulse waveform; half =
+ * its peak index; spread != 0 divides by sqrt(distance).  All arrays device
+ * pointers.  Bit-identical to the reference (float64 in its operation order,
+ * float32 accumulation in scatterer order).  The caller performs the
+ * window-overflow check (simulate.py:246-264). */
+int kkb_render_traces(float *out, int n_tx, int n_el, int n_t, const double *sx, const double *sz,
+                      const double *refl, long long n_sc, const double *upos, const double *sin_t,
+                      const double *cos_t, double inv_c, double fs, double t0, const double *wave,
+                      int n_w, double half, int spread, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -21,6 +21,8 @@ from .errors import (ConfigError, DataError, DeviceError, GeometryError, GuardBa
                      KKBeamError, WindowOverflowError)
 from .sampling import (ReceiveAngleSet, SupportSample, confocal_angles, explicit_angles, support,
                        transmit_angles, uniform_vernier_angles)
+from .simulate import (Phantom, Pulse, Scatterer, make_pulse, merge_phantoms, render_rf_device,
+                       simulate_rf, speckle_phantom, wire_phantom)
 from .spectral import analytic_signal, one_sided_weights
 
 __version__ = "0.1.0"

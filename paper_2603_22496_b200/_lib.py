@@ -49,6 +49,7 @@ SIGNATURES = {
     "kkb_decomposer_destroy": [P],
     "kkb_log_compress": [P, P, I, LL, F, P, P],
     "kkb_compound": [P, I, LL, I, P, P],
+    "kkb_render_traces": [P, I, I, I, P, P, P, LL, P, P, P, D, D, D, P, I, D, I, P],
 }
 _RESTYPES = {
     "kkb_version": ctypes.c_char_p,

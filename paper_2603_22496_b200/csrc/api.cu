@@ -603,3 +603,20 @@ extern "C" int kkb_compound(const void *images, int n_images, long long n_pixels
     }
     return compound(images, n_images, n_pixels, mode, out, as_stream(stream));
 }
+
+extern "C" int kkb_render_traces(float *out, int n_tx, int n_el, int n_t, const double *sx,
+                                 const double *sz, const double *refl, long long n_sc,
+                                 const double *upos, const double *sin_t, const double *cos_t,
+                                 double inv_c, double fs, double t0, const double *wave, int n_w,
+                                 double half, int spread, void *stream) {
+    if (n_tx < 0 || n_el < 0 || n_t < 0 || n_sc < 0 || n_w < 1 || !(fs > 0.0) || !(inv_c > 0.0)) {
+        set_error("render_traces: bad sizes or nonpositive fs / 1/c");
+        return KKB_ERR_ARG;
+    }
+    if (!out || (n_sc > 0 && (!sx || !sz || !refl)) || !upos || !sin_t || !cos_t || !wave) {
+        set_error("render_traces: null array");
+        return KKB_ERR_ARG;
+    }
+    return render_traces(out, n_tx, n_el, n_t, sx, sz, refl, n_sc, upos, sin_t, cos_t, inv_c, fs,
+                         t0, wave, n_w, half, spread, as_stream(stream));
+}

@@ -80,4 +80,10 @@ int contract_sym(const float2 *X, long long ldx, const float2 *CS, long long ldc
 int contract(const float2 *X, long long ldx, const float2 *R, long long ldr, float2 *Y,
              long long ldy, long long B, int L, int M, int Kb, cudaStream_t s);
 
+// K8 forward simulator (simulate.cu)
+int render_traces(float *out, int n_tx, int n_el, int n_t, const double *sx, const double *sz,
+                  const double *refl, long long n_sc, const double *upos, const double *sin_t,
+                  const double *cos_t, double inv_c, double fs, double t0, const double *wave,
+                  int n_w, double half, int spread, cudaStream_t s);
+
 }  // namespace kkb
