@@ -108,43 +108,29 @@ k_render_traces(float *__restrict__ out, int n_tx, int n_el, int n_t, const doub
             } else {
                 my_rng[lane] = make_int4(j0, j1, 0, 0);
             }
-            const bool all_fast = __all_sync(0xffffffffu, fast || j0 > j1) && n_w <= 255;
+            const bool all_fast = __all_sync(0xffffffffu, fast || j0 > j1) && n_w <= 32;
             __syncwarp();
             const int kmax = min(32, cnt - b);
             if (all_fast) {
-                // derive 8 echoes' (sample, amp * v) independently, then apply the
-                // 8 read-add-round-writes in scatterer order (a lane owns j = lane
-                // mod 32: a pulse longer than 32 samples loops)
+                // pulse <= 32 samples: each lane owns at most one sample of an echo
+                // (j = lane mod 32).  Derive 8 echoes' (sample, amp * v) branch-free,
+                // then apply the 8 read-add-round-writes in scatterer order.
                 for (int k0 = 0; k0 < kmax; k0 += 8) {
                     int jj[8];
                     double vv[8];
 #pragma unroll
                     for (int v8 = 0; v8 < 8; ++v8) {
-                        const int k = k0 + v8;
-                        jj[v8] = -1;
-                        vv[v8] = 0.0;
-                        if (k < kmax) {
-                            const int4 r = my_rng[k];
-                            const int j = r.x + ((lane - r.x) & 31);
-                            if (j <= r.y && n_w <= 32) {
-                                const double2 fa = my_fa[k];
-                                const int i0 = j + r.z;  // in [0, n_w - 1] by construction
-                                const double2 w = w_s[i0];
-                                const double lerp = __dadd_rn(w.x, __dmul_rn(fa.x, __dadd_rn(w.y, -w.x)));
-                                const double v = (fa.x > 0.0 && i0 + 1 < n_w) ? lerp : w.x;
-                                vv[v8] = __dmul_rn(fa.y, v);
-                                jj[v8] = j - seg0;
-                            } else if (j <= r.y) {
-                                const double2 fa = my_fa[k];
-                                for (int jl = j; jl <= r.y; jl += 32) {
-                                    const int i0 = jl + r.z;
-                                    const double2 w = w_s[i0];
-                                    const double lerp = __dadd_rn(w.x, __dmul_rn(fa.x, __dadd_rn(w.y, -w.x)));
-                                    const double v = (fa.x > 0.0 && i0 + 1 < n_w) ? lerp : w.x;
-                                    seg[jl - seg0] = (float)__dadd_rn((double)seg[jl - seg0], __dmul_rn(fa.y, v));
-                                }
-                            }
-                        }
+                        const int k = (k0 + v8) & 31;
+                        const int4 r = my_rng[k];
+                        const int j = r.x + ((lane - r.x) & 31);
+                        const bool ok = k0 + v8 < kmax && j <= r.y;
+                        const double2 fa = my_fa[k];
+                        const int i0 = ok ? j + r.z : 0;  // in [0, n_w - 1] by construction
+                        const double2 w = w_s[i0];
+                        const double lerp = __dadd_rn(w.x, __dmul_rn(fa.x, __dadd_rn(w.y, -w.x)));
+                        const double v = (fa.x > 0.0 && i0 + 1 < n_w) ? lerp : w.x;
+                        vv[v8] = __dmul_rn(fa.y, v);
+                        jj[v8] = ok ? j - seg0 : -1;
                     }
 #pragma unroll
                     for (int v8 = 0; v8 < 8; ++v8)
