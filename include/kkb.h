@@ -36,6 +36,8 @@ extern "C" {
 #define KKB_ERR_CUDA (-3)         /* CUDA runtime failure                          */
 #define KKB_ERR_NOMEM (-4)        /* device allocation failed                      */
 #define KKB_ERR_UNSUPPORTED (-5)  /* size outside what the kernels support         */
+#define KKB_ERR_FORMAT (-6)       /* malformed KKRF container     -> FileFormatError */
+#define KKB_ERR_IO (-7)           /* operating-system I/O failure -> OSError         */
 
 /* image output element type */
 #define KKB_OUT_C64 0   /* complex64  (throughput path, BASELINE config 5 "fp32 complex IQ") */
@@ -195,6 +197,37 @@ int kkb_render_traces(float *out, int n_tx, int n_el, int n_t, const double *sx,
                       const double *refl, long long n_sc, const double *upos, const double *sin_t,
                       const double *cos_t, double inv_c, double fs, double t0, const double *wave,
                       int n_w, double half, int spread, void *stream);
+
+/* ------------------------------------------------------------ KKRF container I/O
+ * The reference's binary RF container (rffile.py:1-26): 59-byte little-endian
+ * head "<4sHB3I5d", N f64 transmit angles, M f64 receive angles (kind 2), then
+ * the C-order payload (float32 kind 0, complex64 kinds 1/2).  These calls move
+ * bytes; the reference's validation rules and messages (read_container,
+ * rffile.py:116-178) live in the Python mirror.  Payload transfers to/from
+ * DEVICE memory stream through two pinned 16 MiB buffers so disk and PCIe
+ * overlap; they return with the copies complete. */
+typedef struct kkb_kkrf_header {
+    char magic[4];
+    uint16_t version;
+    uint8_t kind;                /* 0 real RF, 1 analytic RF, 2 compressed RF */
+    uint32_t num_transmits;
+    uint32_t num_channels;       /* elements L (kinds 0/1) or receive angles M (kind 2) */
+    uint32_t num_samples;
+    double sampling_frequency, center_frequency, sound_speed, pitch, start_time;
+    long long head_bytes;        /* 59 */
+    long long file_bytes;        /* file size (filled by kkb_kkrf_read_header) */
+} kkb_kkrf_header;
+
+/* Parses the fixed head (no validation beyond its length: KKB_ERR_FORMAT). */
+int kkb_kkrf_read_header(const char *path, kkb_kkrf_header *header);
+/* Reads `bytes` at `offset` into dst (host, or device when dst_is_device). */
+int kkb_kkrf_read_bytes(const char *path, long long offset, long long bytes, void *dst,
+                        int dst_is_device, void *stream);
+/* Writes head, angle tables (rx_host only for kind 2) and the payload
+ * (host, or device when payload_is_device), replacing `path`. */
+int kkb_kkrf_write(const char *path, const kkb_kkrf_header *header, const double *tx_host,
+                   const double *rx_host, const void *payload, long long payload_bytes,
+                   int payload_is_device, void *stream);
 
 #ifdef __cplusplus
 }

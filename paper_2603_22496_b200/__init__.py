@@ -17,8 +17,9 @@ from .beamform import (BeamformConfig, DelayLUTSet, build_das_luts, build_kk_lut
 from .compress import compress, compression_ratio, guard_band_samples, shear_and_sum
 from .core import (AcquisitionParams, AnalyticRF, ComplexImage, CompressedRF, ImageGrid,
                    IntensityImage, RFVolume, TransducerArray, element_positions, sample_index)
-from .errors import (ConfigError, DataError, DeviceError, GeometryError, GuardBandError,
-                     KKBeamError, WindowOverflowError)
+from .errors import (ConfigError, DataError, DeviceError, FileFormatError, GeometryError,
+                     GuardBandError, KKBeamError, MetricError, RoiError, WindowOverflowError)
+from .rffile import read_container, write_container
 from .sampling import (ReceiveAngleSet, SupportSample, confocal_angles, explicit_angles, support,
                        transmit_angles, uniform_vernier_angles)
 from .simulate import (Phantom, Pulse, Scatterer, make_pulse, merge_phantoms, render_rf_device,

@@ -50,6 +50,9 @@ SIGNATURES = {
     "kkb_log_compress": [P, P, I, LL, F, P, P],
     "kkb_compound": [P, I, LL, I, P, P],
     "kkb_render_traces": [P, I, I, I, P, P, P, LL, P, P, P, D, D, D, P, I, D, I, P],
+    "kkb_kkrf_read_header": [ctypes.c_char_p, P],
+    "kkb_kkrf_read_bytes": [ctypes.c_char_p, LL, LL, P, I, P],
+    "kkb_kkrf_write": [ctypes.c_char_p, P, P, P, P, LL, I, P],
 }
 _RESTYPES = {
     "kkb_version": ctypes.c_char_p,
@@ -57,6 +60,27 @@ _RESTYPES = {
     "kkb_launch_count": LL,
     "kkb_decomposer_workspace_bytes": LL,
 }
+
+
+class KKRFHeader(ctypes.Structure):
+    """kkb_kkrf_header (include/kkb.h), natural C alignment."""
+
+    _fields_ = [
+        ("magic", ctypes.c_char * 4),
+        ("version", ctypes.c_uint16),
+        ("kind", ctypes.c_uint8),
+        ("num_transmits", ctypes.c_uint32),
+        ("num_channels", ctypes.c_uint32),
+        ("num_samples", ctypes.c_uint32),
+        ("sampling_frequency", ctypes.c_double),
+        ("center_frequency", ctypes.c_double),
+        ("sound_speed", ctypes.c_double),
+        ("pitch", ctypes.c_double),
+        ("start_time", ctypes.c_double),
+        ("head_bytes", ctypes.c_longlong),
+        ("file_bytes", ctypes.c_longlong),
+    ]
+
 
 KKB_OUT_C64 = 0
 KKB_OUT_C128 = 1

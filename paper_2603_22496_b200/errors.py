@@ -33,6 +33,18 @@ class GeometryError(DataError):
     """Data geometry disagrees with the delay tables or grid (errors.py:28)."""
 
 
+class RoiError(DataError):
+    """Region of interest is unusable (errors.py:32)."""
+
+
+class MetricError(DataError):
+    """A quality metric cannot be evaluated on this image (errors.py:36)."""
+
+
+class FileFormatError(DataError):
+    """A container file violates the binary format (errors.py:40)."""
+
+
 class DeviceError(KKBeamError):
     """The CUDA library reported a failure (no reference counterpart: the
     reference never leaves the host)."""
@@ -45,6 +57,8 @@ _STATUS = {
     -3: DeviceError,      # KKB_ERR_CUDA
     -4: DeviceError,      # KKB_ERR_NOMEM
     -5: ConfigError,      # KKB_ERR_UNSUPPORTED
+    -6: FileFormatError,  # KKB_ERR_FORMAT
+    -7: OSError,          # KKB_ERR_IO
 }
 
 
