@@ -229,6 +229,27 @@ int kkb_kkrf_write(const char *path, const kkb_kkrf_header *header, const double
                    const double *rx_host, const void *payload, long long payload_bytes,
                    int payload_is_device, void *stream);
 
+/* ------------------------------------------------------------ display / budgeting
+ * Max of a float64 device array (synchronous; result on the host). */
+int kkb_max_f64(const double *x, long long n, double *max_host, void *stream);
+/* Replaces gamma_match (metrics.py:175-202): normalise `image` (n float64,
+ * device) by its max and golden-section search (metrics.py:156-172, same
+ * steps) the exponent g in [lo, hi] (tolerance tol) whose mean (I/max)^g
+ * matches mean((R/maxR)^0.5) of `reference`.  Every objective evaluation is
+ * a deterministic device reduction.  gamma -> *gamma_host; `mapped` (device,
+ * may be NULL) receives (I/max)^gamma.  KKB_ERR_SHAPE if either max <= 0. */
+int kkb_gamma_match(const double *image, const double *reference, long long n, double lo,
+                    double hi, double tol, double *gamma_host, double *mapped, void *stream);
+/* The maximum over the (nx, nz) grid of max_n(x sin_n + z cos_n) +
+ * max_m(z cos_m - x sin_m): the delay numerator of the last sample the kk
+ * gather reads (cli.py:110-128, the compress guard-band budget).  Arrays are
+ * device float64 (x: nx, z: nz, sin/cos of the transmit and receive angles);
+ * bit-identical to the reference's numpy expression. */
+int kkb_last_read_sample_max(const double *x, int nx, const double *z, int nz,
+                             const double *sin_t, const double *cos_t, int n_tx,
+                             const double *sin_r, const double *cos_r, int n_rx,
+                             double *max_host, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -53,6 +53,9 @@ SIGNATURES = {
     "kkb_kkrf_read_header": [ctypes.c_char_p, P],
     "kkb_kkrf_read_bytes": [ctypes.c_char_p, LL, LL, P, I, P],
     "kkb_kkrf_write": [ctypes.c_char_p, P, P, P, P, LL, I, P],
+    "kkb_max_f64": [P, LL, P, P],
+    "kkb_gamma_match": [P, P, LL, D, D, D, P, P, P],
+    "kkb_last_read_sample_max": [P, I, P, I, P, P, I, P, P, I, P, P],
 }
 _RESTYPES = {
     "kkb_version": ctypes.c_char_p,

@@ -620,3 +620,108 @@ extern "C" int kkb_render_traces(float *out, int n_tx, int n_el, int n_t, const 
     return render_traces(out, n_tx, n_el, n_t, sx, sz, refl, n_sc, upos, sin_t, cos_t, inv_c, fs,
                          t0, wave, n_w, half, spread, as_stream(stream));
 }
+
+// ------------------------------------------------------------- display / budgeting
+namespace {
+struct DevScratch {
+    double *p = nullptr;
+    ~DevScratch() {
+        if (p) cudaFree(p);
+    }
+};
+}  // namespace
+
+extern "C" int kkb_max_f64(const double *x, long long n, double *max_host, void *stream) {
+    if (!x || n <= 0 || !max_host) {
+        set_error("max_f64: empty input");
+        return KKB_ERR_ARG;
+    }
+    DevScratch sc;
+    KKB_TRY_CUDA(cudaMalloc(&sc.p, sizeof(double) * 304), "cudaMalloc(scratch)");
+    cudaStream_t s = as_stream(stream);
+    int st = device_max(x, n, sc.p, sc.p + 300, s);
+    if (st) return st;
+    KKB_TRY_CUDA(cudaMemcpyAsync(max_host, sc.p + 300, sizeof(double), cudaMemcpyDeviceToHost, s), "D2H max");
+    KKB_TRY_CUDA(cudaStreamSynchronize(s), "sync max");
+    return KKB_OK;
+}
+
+extern "C" int kkb_gamma_match(const double *image, const double *reference, long long n, double lo,
+                               double hi, double tol, double *gamma_host, double *mapped,
+                               void *stream) {
+    if (!image || !reference || n <= 0 || !gamma_host || !(tol > 0.0)) {
+        set_error("gamma_match: bad arguments");
+        return KKB_ERR_ARG;
+    }
+    DevScratch sc;
+    KKB_TRY_CUDA(cudaMalloc(&sc.p, sizeof(double) * 304), "cudaMalloc(scratch)");
+    cudaStream_t s = as_stream(stream);
+    double *imax = sc.p + 300, *rmax = sc.p + 301, *tmp = sc.p + 302;
+    int st = device_max(image, n, sc.p, imax, s);
+    if (!st) st = device_max(reference, n, sc.p, rmax, s);
+    double h[2];
+    if (!st) {
+        KKB_TRY_CUDA(cudaMemcpyAsync(h, imax, 2 * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H max");
+        KKB_TRY_CUDA(cudaStreamSynchronize(s), "sync max");
+        if (!(h[0] > 0.0) || !(h[1] > 0.0)) {
+            set_error("gamma matching needs nonzero images");
+            return KKB_ERR_SHAPE;
+        }
+    }
+    double target = 0.0;
+    if (!st) st = device_pow_mean(reference, n, rmax, 0.5, sc.p, tmp, &target, s);
+    if (st) return st;
+    int err = KKB_OK;
+    auto objective = [&](double g) {
+        double m = 0.0;
+        if (!err) err = device_pow_mean(image, n, imax, g, sc.p, tmp, &m, s);
+        return fabs(m - target);
+    };
+    // golden-section search of metrics.py:156-172, step for step
+    const double invphi = (sqrt(5.0) - 1.0) / 2.0;
+    double a = lo, b = hi;
+    double c = b - invphi * (b - a), d = a + invphi * (b - a);
+    double fc = objective(c), fd = objective(d);
+    while (b - a > tol && !err) {
+        if (fc < fd) {
+            b = d;
+            d = c;
+            fd = fc;
+            c = b - invphi * (b - a);
+            fc = objective(c);
+        } else {
+            a = c;
+            c = d;
+            fc = fd;
+            d = a + invphi * (b - a);
+            fd = objective(d);
+        }
+    }
+    if (err) return err;
+    const double gamma = 0.5 * (a + b);
+    *gamma_host = gamma;
+    if (mapped) {
+        st = pow_map(image, n, imax, gamma, mapped, s);
+        if (st) return st;
+        KKB_TRY_CUDA(cudaStreamSynchronize(s), "sync map");  // scratch (imax) freed on return
+    }
+    return KKB_OK;
+}
+
+extern "C" int kkb_last_read_sample_max(const double *x, int nx, const double *z, int nz,
+                                        const double *sin_t, const double *cos_t, int n_tx,
+                                        const double *sin_r, const double *cos_r, int n_rx,
+                                        double *max_host, void *stream) {
+    if (!x || !z || nx <= 0 || nz <= 0 || n_tx <= 0 || n_rx <= 0 || !max_host) {
+        set_error("last_read_sample: empty grid or angle set");
+        return KKB_ERR_ARG;
+    }
+    DevScratch sc;
+    KKB_TRY_CUDA(cudaMalloc(&sc.p, sizeof(double) * 304), "cudaMalloc(scratch)");
+    cudaStream_t s = as_stream(stream);
+    int st = last_read_max(x, nx, z, nz, sin_t, cos_t, n_tx, sin_r, cos_r, n_rx, sc.p, sc.p + 300, s);
+    if (st) return st;
+    KKB_TRY_CUDA(cudaMemcpyAsync(max_host, sc.p + 300, sizeof(double), cudaMemcpyDeviceToHost, s), "D2H");
+    KKB_TRY_CUDA(cudaStreamSynchronize(s), "sync last read");
+    return KKB_OK;
+}

@@ -86,4 +86,13 @@ int render_traces(float *out, int n_tx, int n_el, int n_t, const double *sx, con
                   const double *cos_t, double inv_c, double fs, double t0, const double *wave,
                   int n_w, double half, int spread, cudaStream_t s);
 
+// display / budgeting epilogues (display.cu); scratch >= 300 doubles (device)
+int device_max(const double *x, long long n, double *scratch, double *out, cudaStream_t s);
+int device_pow_mean(const double *x, long long n, const double *maxv, double g, double *scratch,
+                    double *out_dev, double *out_host, cudaStream_t s);
+int pow_map(const double *x, long long n, const double *maxv, double g, double *out, cudaStream_t s);
+int last_read_max(const double *x, int nx, const double *z, int nz, const double *sin_t,
+                  const double *cos_t, int n_tx, const double *sin_r, const double *cos_r, int n_rx,
+                  double *scratch, double *out, cudaStream_t s);
+
 }  // namespace kkb
