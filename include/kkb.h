@@ -98,6 +98,14 @@ int kkb_kk_plan_create(const double *ltx, const double *ltz, const double *lrx, 
 int kkb_kk_plan_run(kkb_kk_plan *p, const void *data, int n_frames, long long data_frame_stride,
                     void *out, int out_kind, long long out_frame_stride, float *intensity,
                     unsigned int *frame_max, void *stream);
+/* kkb_kk_plan_run with flags: KKB_RUN_ACCUMULATE_INTENSITY adds |IQ|^2 to
+ * `intensity` instead of overwriting it -- incoherent compounding of receive
+ * sets (compound_incoherent, beamform.py:405-411; cli.py:257-266), one call
+ * per set; frame_max (zeroed by each call) then holds the max of the sum. */
+#define KKB_RUN_ACCUMULATE_INTENSITY 1
+int kkb_kk_plan_run_ex(kkb_kk_plan *p, const void *data, int n_frames, long long data_frame_stride,
+                       void *out, int out_kind, long long out_frame_stride, float *intensity,
+                       unsigned int *frame_max, int flags, void *stream);
 /* trace window (samples per pair) the plan stages in shared memory */
 int kkb_kk_plan_window(const kkb_kk_plan *p);
 int kkb_kk_plan_destroy(kkb_kk_plan *p);

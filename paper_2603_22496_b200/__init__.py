@@ -31,8 +31,8 @@ __version__ = "0.1.0"
 
 def __getattr__(name):
     # lazy: importing the engine pulls in torch
-    if name == "KKEngine":
-        from .engine import KKEngine
+    if name in ("KKEngine", "MultiSetEngine"):
+        from . import engine
 
-        return KKEngine
+        return getattr(engine, name)
     raise AttributeError(name)

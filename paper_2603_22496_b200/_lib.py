@@ -34,6 +34,7 @@ SIGNATURES = {
     "kkb_kk": [P, I, I, I, P, P, P, P, I, I, P, D, D, I, P, I, I, LL, LL, P, P, P],
     "kkb_kk_plan_create": [P, P, P, P, I, I, I, I, I, P, D, D, I, P, P],
     "kkb_kk_plan_run": [P, P, I, LL, P, I, LL, P, P, P],
+    "kkb_kk_plan_run_ex": [P, P, I, LL, P, I, LL, P, P, I, P],
     "kkb_kk_plan_window": [P],
     "kkb_kk_plan_destroy": [P],
     "kkb_kk_taps": [P, P, P, P, I, I, I, I, I, D, D, I, P, P],
@@ -86,6 +87,7 @@ class KKRFHeader(ctypes.Structure):
 
 
 KKB_OUT_C64 = 0
+KKB_RUN_ACCUMULATE_INTENSITY = 1
 KKB_OUT_C128 = 1
 
 _lib = None

@@ -54,7 +54,8 @@ int kk_window(const double *ltx, const double *ltz, const double *lrx, const dou
 int kk_gather(const float2 *data, int N, int M, int T, const double *ltx, const double *ltzT,
               const double *lrx, const double *lrzT, int nx, int nz, const double *w, double fs,
               double shift, int linear, void *out, int out_kind, int n_frames, long long data_fs,
-              long long out_fs, float *inten, unsigned *fmax, int W, cudaStream_t s);
+              long long out_fs, float *inten, unsigned *fmax, int W, cudaStream_t s,
+              int accum = 0);
 
 int kk_taps(const double *ltx, const double *ltz, const double *lrx, const double *lrz, int N, int M,
             int T, int nx, int nz, double fs, double shift, int linear, int *idx, cudaStream_t s);

@@ -246,6 +246,7 @@ struct KKArgs {
     long long out_fs;
     float *inten;
     unsigned *fmax;
+    int accum;  // 1: intensity += |IQ|^2 (incoherent multi-set compounding)
 };
 
 // packed LUT index: tile row r -> (r/8)*4 + r%4 pair slot, a = (r/4)&1
@@ -502,6 +503,7 @@ k_kk_gather(const KKArgs a) {
                 }
                 if (a.inten) {
                     float I = (float)(vr * vr + vi * vi);
+                    if (a.accum) I += a.inten[px];  // sets compounded in call order
                     a.inten[px] = I;
                     fmx = fmaxf(fmx, I);
                 }
@@ -524,7 +526,7 @@ static size_t kk_smem_bytes(int N, int M, int W, int MCH, bool linear) {
 int kk_gather(const float2 *data, int N, int M, int T, const double *ltx, const double *ltzT,
               const double *lrx, const double *lrzT, int nx, int nz, const double *w, double fs,
               double shift, int linear, void *out, int out_kind, int n_frames, long long data_fs,
-              long long out_fs, float *inten, unsigned *fmax, int W, cudaStream_t s) {
+              long long out_fs, float *inten, unsigned *fmax, int W, cudaStream_t s, int accum) {
     if (n_frames <= 0 || nx <= 0 || nz <= 0) return KKB_OK;
     if (W < 2) W = 2;
     if (W > KKB_KK_STAGE_ELEMS) {
@@ -541,7 +543,7 @@ int kk_gather(const float2 *data, int N, int M, int T, const double *ltx, const 
         return KKB_ERR_UNSUPPORTED;
     }
     KKArgs a{data, data_fs, N, M, T, ltx, ltzT, lrx, lrzT, w, fs, shift, nx, nz, W, MCH,
-             out, out_kind, out_fs, inten, fmax};
+             out, out_kind, out_fs, inten, fmax, accum};
     dim3 grid((unsigned)ceil_div(nz, KKB_KK_TZ), (unsigned)ceil_div(nx, KKB_KK_TX), (unsigned)n_frames);
     dim3 block(KKB_KK_WZ * KKB_KK_WX * 32);
     if (linear) {

@@ -120,17 +120,22 @@ class KKEngine:
         self._run_decomposer(self._dec, rf, F, self.traces, dev.stream_handle(stream))
         return self.traces[:F]
 
-    def beamform(self, traces=None, n_frames: int | None = None, stream=None, out_offset: int = 0):
+    def beamform(self, traces=None, n_frames: int | None = None, stream=None, out_offset: int = 0,
+                 inten=None, fmax=None, accumulate: bool = False, want_db: bool | None = None):
+        """K5 (+ fused detection) and K6 on decomposed traces.  `inten` / `fmax`
+        redirect the detection to caller buffers; `accumulate` adds |IQ|^2 to
+        `inten` (incoherent compounding, see MultiSetEngine)."""
         F = self.F if n_frames is None else n_frames
         traces = self.traces if traces is None else traces
         P = self.grid.nx * self.grid.nz
         s = dev.stream_handle(stream)
         iq = self.iq[out_offset:out_offset + F]
-        inten = self.inten[out_offset:out_offset + F]
-        fmax = self.fmax[out_offset:out_offset + F]
-        _lib.call("kkb_kk_plan_run", self._kk, dev.ptr(traces), F, self.N * self.M * self.T,
-                  dev.ptr(iq), _lib.KKB_OUT_C64, P, dev.ptr(inten), dev.ptr(fmax), s)
-        if self.want_db:
+        inten = (self.inten if inten is None else inten)[out_offset:out_offset + F]
+        fmax = None if fmax is False else (self.fmax if fmax is None else fmax)[out_offset:out_offset + F]
+        _lib.call("kkb_kk_plan_run_ex", self._kk, dev.ptr(traces), F, self.N * self.M * self.T,
+                  dev.ptr(iq), _lib.KKB_OUT_C64, P, dev.ptr(inten), dev.ptr(fmax),
+                  _lib.KKB_RUN_ACCUMULATE_INTENSITY if accumulate else 0, s)
+        if self.want_db if want_db is None else want_db:
             db = self.db[out_offset:out_offset + F]
             _lib.call("kkb_log_compress", dev.ptr(inten), dev.ptr(fmax), F, P, self.floor_db,
                       dev.ptr(db), s)
@@ -245,3 +250,65 @@ class KKEngine:
             self.close()
         except Exception:
             pass
+
+
+class MultiSetEngine:
+    """Several receive-angle sets over one RF batch, compounded on the device
+    (the reference's hybrid / multi-j acquisitions: cli.py:93-107, 250-266;
+    compound_coherent / compound_incoherent, beamform.py:396-411).
+
+    mode "incoherent": one decomposition + gather per set; every gather adds
+      its |IQ_j|^2 to one shared intensity buffer (KKB_RUN_ACCUMULATE_INTENSITY),
+      so sum_j |B_j|^2 and its per-frame max come out of the last launch.
+    mode "coherent": |sum_j B_j|^2 is the kk image over the concatenated angle
+      list (kk sums over every receive angle), so it is ONE engine on the union.
+    """
+
+    def __init__(self, array: TransducerArray, params: AcquisitionParams, receive_sets,
+                 grid: ImageGrid, frames: int, mode: str = "incoherent", want_db: bool = True,
+                 floor_db: float = -60.0, **kw):
+        from .sampling import explicit_angles
+
+        sets = [rs[1] if isinstance(rs, tuple) else rs for rs in receive_sets]
+        if not sets:
+            raise ConfigError("need at least one receive set")
+        if mode not in ("incoherent", "coherent"):
+            raise ConfigError(f"unknown compounding mode {mode!r}")
+        self.mode, self.want_db, self.floor_db = mode, want_db, float(floor_db)
+        if mode == "coherent":
+            union = explicit_angles(np.concatenate([s.angles for s in sets]), sets[0].delta_theta_i)
+            self.engines = [KKEngine(array, params, union, grid, frames, want_db=want_db,
+                                     floor_db=floor_db, **kw)]
+            e = self.engines[0]
+            self.inten, self.fmax, self.db = e.inten, e.fmax, e.db
+            return
+        self.engines = [KKEngine(array, params, rs, grid, frames, want_db=False, **kw) for rs in sets]
+        e = self.engines[0]
+        self.inten, self.fmax = e.inten, e.fmax
+        self.db = e.t.empty_like(e.inten) if want_db else None
+
+    @property
+    def pixel_pairs_per_frame(self) -> int:
+        return sum(e.pixel_pairs_per_frame for e in self.engines)
+
+    def run(self, rf, stream=None):
+        """Compounded intensity (F, X, Z) float32 for a (F, N, L, T) RF batch;
+        per-set IQ stays in engines[j].iq.  Asynchronous."""
+        if self.mode == "coherent":
+            self.engines[0].run(rf, stream=stream, groups=1)
+            return self.inten
+        last = len(self.engines) - 1
+        for j, e in enumerate(self.engines):
+            e.decompose(rf, stream=stream)
+            e.beamform(stream=stream, inten=self.inten, fmax=self.fmax if j == last else False,
+                       accumulate=j > 0, want_db=False)
+        if self.want_db:
+            e = self.engines[0]
+            P = e.grid.nx * e.grid.nz
+            _lib.call("kkb_log_compress", dev.ptr(self.inten), dev.ptr(self.fmax), e.F, P,
+                      self.floor_db, dev.ptr(self.db), dev.stream_handle(stream))
+        return self.inten
+
+    def close(self):
+        for e in self.engines:
+            e.close()
