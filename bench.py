@@ -301,6 +301,13 @@ def run_gpu(args):
     sm_mhz = clk.get("sm_mhz") or 1965.0
     smem_peak = sm_count * 128 * sm_mhz * 1e6 / 1e9           # GB/s, 128 B/clk/SM crossbar
     achieved_taps = gather_bytes_alg / (kk_launch_ms / 1e3) / 1e9
+    # stage 1 (K1-K3) is HBM-bound: bytes its three kernels must move per batch
+    # (RF in, spectra written then read, contracted bins written then read,
+    # traces out) and the two-array compulsory minimum (RF in + traces out)
+    ldk = (T // 2 + 1 + 1) & ~1
+    s1_bytes = F * (4.0 * N * L * T + 2 * 8.0 * N * L * ldk + 2 * 8.0 * N * M * ldk + 8.0 * N * M * T)
+    s1_min = F * (4.0 * N * L * T + 8.0 * N * M * T)
+    s1_achieved = s1_bytes / (dec_ms / 1e3) / 1e9
 
     # ---- end to end through the public API: pinned host RF in, host IQ out ----
     e2e = e2e_i16 = None
@@ -385,6 +392,15 @@ def run_gpu(args):
                                 "algorithmic_bytes": "16 B of taps per pixel-pair (SURVEY 8d)",
                                 "pixel_pairs_per_s": pp_frame * fl / (kk_launch_ms / 1e3),
                                 "pixel_pairs_per_s_isolated": pp_frame * F / (kk_ms / 1e3)},
+            "stage1_roofline": {"kernels": "k_r2c + k_contract_sym + k_c2c", "bound": "hbm",
+                                "achieved": s1_achieved, "peak": hbm_peak, "unit": "GB/s",
+                                "frac": s1_achieved / hbm_peak, "ms": dec_ms,
+                                "bytes_per_step": s1_bytes,
+                                "compulsory_frac": s1_min / (dec_ms / 1e3) / 1e9 / hbm_peak,
+                                "algorithmic_bytes": "RF in + spectra write/read + contracted "
+                                                     "bins write/read + traces out (three-kernel "
+                                                     "structure); compulsory_frac counts RF in + "
+                                                     "traces out only"},
             "gpu_launches": int(launches),
             "clocks": clk,
         }

@@ -23,19 +23,36 @@ __device__ __forceinline__ int pat(int p, int lane) {
     return 0;
 }
 
+template <int WB>
 __global__ void k(int p, int iters, float *out) {
     __shared__ __align__(16) float4 s[2048];
     for (int i = threadIdx.x; i < 2048; i += blockDim.x) s[i] = make_float4(i, i, i, i);
     __syncthreads();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    unsigned a = (unsigned)__cvta_generic_to_shared(&s[(pat(p, lane) + warp * 32) & 127]);
+    unsigned a = (unsigned)__cvta_generic_to_shared(s) + ((pat(p, lane) + warp * 32) & 127) * WB;
     float acc = 0.f;
     for (int i = 0; i < iters; ++i) {
         float x, y, z, w;
         const unsigned ai = a ^ ((i & 7) << 11);
-        asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(x), "=f"(y), "=f"(z), "=f"(w) : "r"(ai) : "memory");
+        if (WB == 16) {
+            asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(x), "=f"(y), "=f"(z), "=f"(w) : "r"(ai) : "memory");
+        } else if (WB == 8) {
+            asm volatile("ld.shared.v2.f32 {%0,%1}, [%2];" : "=f"(x), "=f"(y) : "r"(ai) : "memory");
+            z = x; w = y;
+        } else {
+            asm volatile("ld.shared.f32 %0, [%1];" : "=f"(x) : "r"(ai) : "memory");
+            y = z = w = x;
+        }
         acc += (x + y) * (z + w);
-        asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4+16];" : "=f"(x), "=f"(y), "=f"(z), "=f"(w) : "r"(ai) : "memory");
+        if (WB == 16) {
+            asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4+16];" : "=f"(x), "=f"(y), "=f"(z), "=f"(w) : "r"(ai) : "memory");
+        } else if (WB == 8) {
+            asm volatile("ld.shared.v2.f32 {%0,%1}, [%2+16];" : "=f"(x), "=f"(y) : "r"(ai) : "memory");
+            z = x; w = y;
+        } else {
+            asm volatile("ld.shared.f32 %0, [%1+16];" : "=f"(x) : "r"(ai) : "memory");
+            y = z = w = x;
+        }
         acc += (x + z) * (y + w);
     }
     if (acc == -1.f) out[0] = acc;
@@ -52,10 +69,12 @@ int main() {
     const int iters = 4096, threads = 512, blocks = sms * 4;
     const char *names[] = {"lane", "bcast", "lane&3", "lane>>2", "lane>>3", "lane&7", "lane>>1",
                            "lane&15", "(lane*7)&15", "mixed", "lane>>4", "(lane&1)*8", "(lane>>2)*2", "lane*2"};
+    for (int wb = 16; wb >= 4; wb /= 2)
     for (int p = 0; p < 14; ++p) {
-        k<<<blocks, threads>>>(p, iters, out);
+        auto fn = wb == 16 ? k<16> : (wb == 8 ? k<8> : k<4>);
+        fn<<<blocks, threads>>>(p, iters, out);
         cudaEventRecord(e0);
-        k<<<blocks, threads>>>(p, iters, out);
+        fn<<<blocks, threads>>>(p, iters, out);
         cudaEventRecord(e1);
         cudaEventSynchronize(e1);
         float ms;
@@ -64,7 +83,7 @@ int main() {
         int clk;
         cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
         double cyc = ms * 1e-3 * clk * 1e3 * sms;  // SM-cycles (at the nominal clock)
-        printf("%-14s %.3f SM-cycles per warp LDS.128 (%.3f ms, %s)\n", names[p], cyc / warp_loads, ms,
+        printf("LDS%-3d %-14s %.3f SM-cycles per warp load (%.3f ms, %s)\n", wb * 8, names[p], cyc / warp_loads, ms,
                cudaGetErrorString(cudaGetLastError()));
     }
     return 0;
