@@ -19,6 +19,13 @@ __device__ __forceinline__ int pat(int p, int lane) {
         case 11: return (lane & 1) * 8;   // 2 distinct, 128 B apart
         case 12: return (lane >> 2) * 2;  // 8 distinct, stride 32 B
         case 13: return lane * 2;         // 32 distinct, stride 32 B
+        case 14: return lane < 16 ? (lane >> 1) : 8 + lane;          // half-warp 0 pair-uniform
+        case 15: return lane < 8 ? (lane >> 1) : 8 + lane;           // quarter 0 pair-uniform
+        case 16: return lane < 4 ? (lane >> 1) : 8 + lane;           // 2 pairs uniform
+        case 17: return lane < 2 ? 0 : 8 + lane;                     // 1 pair uniform
+        case 18: return lane < 30 ? (lane >> 1) : 16 + lane;         // all but the last pair
+        case 19: return (lane & 8) ? 16 + lane : (lane >> 1);        // quarters 0, 2 pair-uniform
+        case 20: return (lane & 16) ? (lane >> 1) : 8 + lane;        // half-warp 1 pair-uniform
     }
     return 0;
 }
@@ -68,9 +75,10 @@ int main() {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     const int iters = 4096, threads = 512, blocks = sms * 4;
     const char *names[] = {"lane", "bcast", "lane&3", "lane>>2", "lane>>3", "lane&7", "lane>>1",
-                           "lane&15", "(lane*7)&15", "mixed", "lane>>4", "(lane&1)*8", "(lane>>2)*2", "lane*2"};
+                           "lane&15", "(lane*7)&15", "mixed", "lane>>4", "(lane&1)*8", "(lane>>2)*2", "lane*2", "hw0 pairs", "q0 pairs", "2 pairs", "1 pair",
+                           "all-but-1", "q0,q2 pairs", "hw1 pairs"};
     for (int wb = 16; wb >= 4; wb /= 2)
-    for (int p = 0; p < 14; ++p) {
+    for (int p = 0; p < 21; ++p) {
         auto fn = wb == 16 ? k<16> : (wb == 8 ? k<8> : k<4>);
         fn<<<blocks, threads>>>(p, iters, out);
         cudaEventRecord(e0);
