@@ -14,6 +14,7 @@
 // (a warp's 32 depth neighbours touch one or two 128 B lines per element).
 
 #include <algorithm>
+#include <cstdlib>
 #include <type_traits>
 
 #include "common.cuh"
@@ -476,6 +477,10 @@ int das_gather(const float2 *data, int n_tx, int n_el, int n_t, const double *lt
                void *out, int out_kind, cudaStream_t s) {
     (void)n_hyp_rows;
     if ((long long)nx * nz <= 0) return KKB_OK;
+    const char *force = getenv("KKB_DAS_DIRECT");  // test hook: the per-pixel fallback kernel
+    if (force && force[0] == '1')
+        return das_gather_direct(data, n_tx, n_el, n_t, ltx, ltz, hyp, base, frac, xcoord, zcoord,
+                                 upos, tan_max, weights, fs, shift, linear, nx, nz, out, out_kind, s);
     DasArgs a{data, n_tx, n_el, n_t, ltx, ltz, hyp, base, frac, xcoord, zcoord, upos, tan_max,
               weights, fs, shift, nx, nz, 0, 0, out, out_kind, 1, nullptr};
     const int tiles = (int)(ceil_div(nx, KKB_DAS_TX) * ceil_div(nz, KKB_DAS_TZ));

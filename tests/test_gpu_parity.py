@@ -354,3 +354,28 @@ def test_intensity_and_compounding(oracle):
         kb.compound_coherent([im, other])
     with pytest.raises(kb.ConfigError):
         kb.compound_incoherent([])
+
+
+@pytest.mark.parametrize("direct", ["0", "1"])
+def test_das_odd_grid_gated_weighted_vs_oracle(oracle, small_array, monkeypatch, direct):
+    # partial tiles, element groups, the per-tile gate skip, and (direct=1) the
+    # per-pixel fallback kernel, against the C restatement of _das_kernel
+    monkeypatch.setenv("KKB_DAS_DIRECT", direct)
+    rng = np.random.default_rng(21)
+    params = kb.AcquisitionParams(C, kb.transmit_angles(7, 12 * DEG), 1024, start_time=1e-6)
+    data = (rng.standard_normal((7, 64, 1024)) + 1j * rng.standard_normal((7, 64, 1024))).astype(np.complex64)
+    grid = kb.ImageGrid(-3e-3, 5e-3, 0.07e-3, 0.09e-3, 45, 37)
+    an = kb.AnalyticRF(data, small_array, params)
+    luts = kb.build_das_luts(grid, small_array, params)
+    w = rng.uniform(0.5, 1.5, 64)
+    fs = small_array.sampling_frequency
+    for cfg, linear in ((kb.BeamformConfig(max_rx_angle=0.25, channel_weights=w), True),
+                        (kb.BeamformConfig(interpolation="nearest", pulse_delay=0.2e-6), False)):
+        got = kb.das(an, luts, cfg).pixels
+        tan_max = np.tan(cfg.max_rx_angle) if cfg.max_rx_angle is not None else np.inf
+        wts = cfg.channel_weights if cfg.channel_weights is not None else np.ones(64)
+        shift = (cfg.pulse_delay - params.start_time) * fs
+        ref = oracle.das_kernel(data, luts.lut_tx_x, luts.lut_tx_z, luts.lut_rx_hypot, luts.rx_base,
+                                luts.rx_frac, grid.x, grid.z, small_array.positions, tan_max, wts,
+                                fs, shift, linear=linear)
+        assert rel_l2(got, ref) <= 1e-5, (direct, linear)
