@@ -25,6 +25,7 @@
 // max for the dB epilogue (K6).
 
 #include <algorithm>
+#include <cstdlib>
 #include <type_traits>
 #include <vector>
 
@@ -516,6 +517,61 @@ k_kk_gather(const KKArgs a) {
     }
 }
 
+// Per-pixel fallback of K5 for geometries whose per-tile trace window does not
+// fit the staging buffer (very coarse grids / steep delays): one thread per
+// (frame, pixel), taps read through L1, the same index math (kk_delay +
+// tap_index), lerp, accumulation order and epilogue as the tiled kernel.
+template <bool LINEAR>
+__global__ void __launch_bounds__(256)
+k_kk_direct(const KKArgs a) {
+    const long long P = (long long)a.nx * a.nz;
+    const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    const int f = blockIdx.y;
+    float fmx = 0.f;
+    if (i < P) {
+        const int ix = (int)(i / a.nz), iz = (int)(i % a.nz);
+        const float2 *dframe = a.data + (long long)f * a.data_fs;
+        float ar = 0.f, ai = 0.f;
+        for (int n = 0; n < a.N; ++n) {
+            const double t1 = __dadd_rn(a.ltx[(long long)ix * a.N + n], a.ltzT[(long long)n * a.nz + iz]);
+            for (int m = 0; m < a.M; ++m) {
+                const double fi = kk_delay(t1, a.lrzT[(long long)m * a.nz + iz], a.lrx[(long long)ix * a.M + m],
+                                           a.fs, a.shift);
+                int F;
+                double sv;
+                if (!tap_index<LINEAR>(fi, a.T, F, sv)) continue;
+                const float wm = a.w ? (float)a.w[m] : 1.0f;
+                const float2 *tr = dframe + (long long)(n * a.M + m) * a.T;
+                const float2 d0 = __ldg(tr + F);
+                if (LINEAR) {
+                    const float2 d1 = __ldg(tr + F + 1);
+                    const float fr = __uint_as_float(((unsigned)__double2loint(sv) >> 9) | 0x3F800000u) - 1.0f;
+                    ar = fmaf(wm, fmaf(fr, d1.x - d0.x, d0.x), ar);
+                    ai = fmaf(wm, fmaf(fr, d1.y - d0.y, d0.y), ai);
+                } else {
+                    ar = fmaf(wm, d0.x, ar);
+                    ai = fmaf(wm, d0.y, ai);
+                }
+            }
+        }
+        const long long px = (long long)f * a.out_fs + i;
+        if (a.out_kind == KKB_OUT_C128)
+            reinterpret_cast<double2 *>(a.out)[px] = make_double2(ar, ai);
+        else
+            reinterpret_cast<float2 *>(a.out)[px] = make_float2(ar, ai);
+        if (a.inten) {
+            float I = ar * ar + ai * ai;
+            if (a.accum) I += a.inten[px];
+            a.inten[px] = I;
+            fmx = I;
+        }
+    }
+    if (a.fmax) {
+        for (int o = 16; o > 0; o >>= 1) fmx = fmaxf(fmx, __shfl_xor_sync(0xffffffffu, fmx, o));
+        if ((threadIdx.x & 31) == 0) atomicMax(a.fmax + f, __float_as_uint(fmx));
+    }
+}
+
 static size_t kk_smem_bytes(int N, int M, int W, int MCH, bool linear) {
     size_t entry = linear ? sizeof(float4) : sizeof(float2);
     return entry * 2 * MCH * W +
@@ -529,10 +585,18 @@ int kk_gather(const float2 *data, int N, int M, int T, const double *ltx, const 
               long long out_fs, float *inten, unsigned *fmax, int W, cudaStream_t s, int accum) {
     if (n_frames <= 0 || nx <= 0 || nz <= 0) return KKB_OK;
     if (W < 2) W = 2;
-    if (W > KKB_KK_STAGE_ELEMS) {
-        set_error("kk: trace window of %d samples per tile exceeds %d (delay tables too steep "
-                  "for the %dx%d tile)", W, KKB_KK_STAGE_ELEMS, KKB_KK_TZ, KKB_KK_TX);
-        return KKB_ERR_UNSUPPORTED;
+    const char *force = getenv("KKB_KK_DIRECT");  // test hook: the per-pixel fallback
+    if (W > KKB_KK_STAGE_ELEMS || (force && force[0] == '1')) {
+        // steep geometry: the tile's trace window would not fit the staging buffer
+        KKArgs a{data, data_fs, N, M, T, ltx, ltzT, lrx, lrzT, w, fs, shift, nx, nz, W, 0,
+                 out, out_kind, out_fs, inten, fmax, accum};
+        dim3 grid((unsigned)ceil_div((long long)nx * nz, 256), (unsigned)n_frames);
+        if (linear)
+            k_kk_direct<true><<<grid, 256, 0, s>>>(a);
+        else
+            k_kk_direct<false><<<grid, 256, 0, s>>>(a);
+        KKB_CHECK_LAUNCH("k_kk_direct");
+        return KKB_OK;
     }
     // receive angles per stage: bounded by the register staging and shared memory
     int MCH = std::max(1, std::min(M, KKB_KK_STAGE_ELEMS / W));

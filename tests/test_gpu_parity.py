@@ -379,3 +379,38 @@ def test_das_odd_grid_gated_weighted_vs_oracle(oracle, small_array, monkeypatch,
                                 luts.rx_frac, grid.x, grid.z, small_array.positions, tan_max, wts,
                                 fs, shift, linear=linear)
         assert rel_l2(got, ref) <= 1e-5, (direct, linear)
+
+
+def test_kk_steep_geometry_falls_back_to_per_pixel_kernel(oracle, small_array):
+    # a coarse grid (1 mm pixels): a 32 x 64 tile spans > 1024 samples, so the
+    # tiled kernel cannot stage its windows and the per-pixel kernel runs
+    rng = np.random.default_rng(17)
+    params = kb.AcquisitionParams(C, kb.transmit_angles(5, 12 * DEG), 4096)
+    rx = kb.uniform_vernier_angles(5, 5, 12 * DEG, 0)
+    data = (rng.standard_normal((5, 5, 4096)) + 1j * rng.standard_normal((5, 5, 4096))).astype(np.complex64)
+    grid = kb.ImageGrid(-20e-3, 2e-3, 1e-3, 1.5e-3, 41, 50)
+    rfc = kb.CompressedRF(data, rx, params, small_array)
+    luts = kb.build_kk_luts(grid, params, rx)
+    d = [dev.to_device(a) for a in (luts.lut_tx_x, luts.lut_tx_z, luts.lut_rx_x, luts.lut_rx_z)]
+    import ctypes
+
+    h = ctypes.c_void_p()
+    _lib.call("kkb_kk_plan_create", *[x.data_ptr() for x in d], 5, 5, 4096, 41, 50, None,
+              small_array.sampling_frequency, 0.0, 1, dev.stream_handle(), ctypes.byref(h))
+    assert _lib.load().kkb_kk_plan_window(h) > 1024
+    _lib.load().kkb_kk_plan_destroy(h)
+    ref = oracle.kk_kernel(data, luts.lut_tx_x, luts.lut_tx_z, luts.lut_rx_x, luts.lut_rx_z,
+                           np.ones(5), small_array.sampling_frequency, 0.0)
+    assert rel_l2(kb.kk(rfc, luts).pixels, ref) <= 1e-5
+
+
+def test_kk_per_pixel_kernel_matches_reference(monkeypatch):
+    monkeypatch.setenv("KKB_KK_DIRECT", "1")
+    g = golden("config1")
+    w = configs.config1()
+    rfc = _c1_rfc(w, g)
+    luts = kb.build_kk_luts(w.grid, w.params, w.receive)
+    assert rel_l2(kb.kk(rfc, luts).pixels, g["image"]) <= 1e-5
+    near = kb.kk(rfc, luts, kb.BeamformConfig(interpolation="nearest", pulse_delay=0.3e-6,
+                                              channel_weights=g["weights"])).pixels
+    assert rel_l2(near, g["image_nearest"]) <= 1e-5
