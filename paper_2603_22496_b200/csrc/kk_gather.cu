@@ -531,8 +531,9 @@ k_kk_direct(const KKArgs a) {
     if (i < P) {
         const int ix = (int)(i / a.nz), iz = (int)(i % a.nz);
         const float2 *dframe = a.data + (long long)f * a.data_fs;
-        float ar = 0.f, ai = 0.f;
+        double tr_ = 0.0, ti_ = 0.0;  // per-transmit float32 partials, float64 total
         for (int n = 0; n < a.N; ++n) {
+            float ar = 0.f, ai = 0.f;
             const double t1 = __dadd_rn(a.ltx[(long long)ix * a.N + n], a.ltzT[(long long)n * a.nz + iz]);
             for (int m = 0; m < a.M; ++m) {
                 const double fi = kk_delay(t1, a.lrzT[(long long)m * a.nz + iz], a.lrx[(long long)ix * a.M + m],
@@ -553,10 +554,13 @@ k_kk_direct(const KKArgs a) {
                     ai = fmaf(wm, d0.y, ai);
                 }
             }
+            tr_ += (double)ar;
+            ti_ += (double)ai;
         }
+        const float ar = (float)tr_, ai = (float)ti_;
         const long long px = (long long)f * a.out_fs + i;
         if (a.out_kind == KKB_OUT_C128)
-            reinterpret_cast<double2 *>(a.out)[px] = make_double2(ar, ai);
+            reinterpret_cast<double2 *>(a.out)[px] = make_double2(tr_, ti_);
         else
             reinterpret_cast<float2 *>(a.out)[px] = make_float2(ar, ai);
         if (a.inten) {
@@ -586,7 +590,9 @@ int kk_gather(const float2 *data, int N, int M, int T, const double *ltx, const 
     if (n_frames <= 0 || nx <= 0 || nz <= 0) return KKB_OK;
     if (W < 2) W = 2;
     const char *force = getenv("KKB_KK_DIRECT");  // test hook: the per-pixel fallback
-    if (W > KKB_KK_STAGE_ELEMS || (force && force[0] == '1')) {
+    // tables of very many pairs (N*M in the thousands) outgrow shared memory too
+    const bool too_big = kk_smem_bytes(N, M, std::max(W, 2), 1, linear) > 227 * 1024;
+    if (W > KKB_KK_STAGE_ELEMS || too_big || (force && force[0] == '1')) {
         // steep geometry: the tile's trace window would not fit the staging buffer
         KKArgs a{data, data_fs, N, M, T, ltx, ltzT, lrx, lrzT, w, fs, shift, nx, nz, W, 0,
                  out, out_kind, out_fs, inten, fmax, accum};
@@ -602,10 +608,6 @@ int kk_gather(const float2 *data, int N, int M, int T, const double *ltx, const 
     int MCH = std::max(1, std::min(M, KKB_KK_STAGE_ELEMS / W));
     while (MCH > 1 && kk_smem_bytes(N, M, W, MCH, linear) > 200 * 1024) MCH = (MCH + 1) / 2;
     size_t sm = kk_smem_bytes(N, M, W, MCH, linear);
-    if (sm > 227 * 1024) {
-        set_error("kk tile needs %zu B of shared memory (N=%d M=%d window=%d)", sm, N, M, W);
-        return KKB_ERR_UNSUPPORTED;
-    }
     KKArgs a{data, data_fs, N, M, T, ltx, ltzT, lrx, lrzT, w, fs, shift, nx, nz, W, MCH,
              out, out_kind, out_fs, inten, fmax, accum};
     dim3 grid((unsigned)ceil_div(nz, KKB_KK_TZ), (unsigned)ceil_div(nx, KKB_KK_TX), (unsigned)n_frames);

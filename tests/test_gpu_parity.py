@@ -414,3 +414,18 @@ def test_kk_per_pixel_kernel_matches_reference(monkeypatch):
     near = kb.kk(rfc, luts, kb.BeamformConfig(interpolation="nearest", pulse_delay=0.3e-6,
                                               channel_weights=g["weights"])).pixels
     assert rel_l2(near, g["image_nearest"]) <= 1e-5
+
+
+def test_kk_ten_thousand_pairs(oracle, small_array):
+    # 100 x 100 pairs: the per-tile pair tables outgrow shared memory, so the
+    # per-pixel kernel takes over (no size limit on the pair set)
+    rng = np.random.default_rng(23)
+    params = kb.AcquisitionParams(C, np.linspace(-0.2, 0.2, 100), 512)
+    rx = kb.explicit_angles(np.linspace(-0.25, 0.25, 100))
+    data = (rng.standard_normal((100, 100, 512)) + 1j * rng.standard_normal((100, 100, 512))).astype(np.complex64)
+    grid = kb.ImageGrid(-1e-3, 3e-3, 0.1e-3, 0.08e-3, 21, 19)
+    rfc = kb.CompressedRF(data, rx, params, small_array)
+    luts = kb.build_kk_luts(grid, params, rx)
+    ref = oracle.kk_kernel(data, luts.lut_tx_x, luts.lut_tx_z, luts.lut_rx_x, luts.lut_rx_z,
+                           np.ones(100), small_array.sampling_frequency, 0.0)
+    assert rel_l2(kb.kk(rfc, luts).pixels, ref) <= 1e-5
