@@ -452,7 +452,9 @@ def run_gpu(args):
 
 def run_gpu_rowblock(args):
     """Config 5: one large frame per step, image row-blocks sharded over ranks,
-    stage 1 replicated, NCCL all-gather of the complex64 blocks (strong scaling)."""
+    stage 1 replicated; the gather kernel stores its rows into every rank's
+    image over NVLink (P2P, CUDA IPC), NCCL all-gather as the fallback
+    (strong scaling)."""
     import torch
     import torch.distributed as dist
 
@@ -508,7 +510,9 @@ def run_gpu_rowblock(args):
             "dtype": "f32 (complex64 traces/IQ; float64 delay-index math)",
             "data": "synthetic (seeded noise RF, shapes of BASELINE config 5)",
             "config": {"workload": w.name, "frames_per_step": 1, "pixel_pairs_per_frame": pp,
-                       "parallelism": f"row-block x{world}, stage 1 replicated, NCCL all-gather"},
+                       "parallelism": f"row-block x{world}, stage 1 replicated, "
+                                      + ("P2P stores from the gather epilogue (CUDA IPC over NVLink)"
+                                         if rb.transport == "p2p" else "NCCL all-gather")},
             "pixel_pair_samples_per_s": pp * 1e3 / ms_step, "gpu_launches": int(launches),
             "clocks": clk}))
     rb.close()

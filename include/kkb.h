@@ -106,6 +106,17 @@ int kkb_kk_plan_run(kkb_kk_plan *p, const void *data, int n_frames, long long da
 int kkb_kk_plan_run_ex(kkb_kk_plan *p, const void *data, int n_frames, long long data_frame_stride,
                        void *out, int out_kind, long long out_frame_stride, float *intensity,
                        unsigned int *frame_max, int flags, void *stream);
+/* Fused row-block all-gather: run the plan (whose
+ * tables are this rank's lateral rows) and store every IQ pixel straight into
+ * each of the n_dst (<= 8) full-image buffers dst_host[d] (device pointers:
+ * this rank's own buffer and the peers' buffers mapped with CUDA IPC over
+ * NVLink) at dst_offset + ix*nz + iz (+ f*out_frame_stride).  The P2P stores
+ * from the gather epilogue replace the NCCL all-gather; the caller orders
+ * completion (stream sync + a barrier) before reading its image. */
+int kkb_kk_plan_run_scatter(kkb_kk_plan *p, const void *data, int n_frames,
+                            long long data_frame_stride, void *const *dst_host, int n_dst,
+                            long long dst_offset, int out_kind, long long out_frame_stride,
+                            void *stream);
 /* trace window (samples per pair) the plan stages in shared memory */
 int kkb_kk_plan_window(const kkb_kk_plan *p);
 int kkb_kk_plan_destroy(kkb_kk_plan *p);
@@ -257,6 +268,15 @@ int kkb_last_read_sample_max(const double *x, int nx, const double *z, int nz,
                              const double *sin_t, const double *cos_t, int n_tx,
                              const double *sin_r, const double *cos_r, int n_rx,
                              double *max_host, void *stream);
+
+/* ------------------------------------------------------------ CUDA IPC for row-block P2P
+ * A plain cudaMalloc buffer (IPC handles need allocation base pointers), its
+ * 64-byte handle, and mapping / unmapping a peer process's handle. */
+int kkb_ipc_alloc(long long bytes, void **ptr);
+int kkb_ipc_free(void *ptr);
+int kkb_ipc_get_handle(const void *ptr, void *handle64);
+int kkb_ipc_open_handle(const void *handle64, void **ptr);
+int kkb_ipc_close_handle(void *ptr);
 
 #ifdef __cplusplus
 }

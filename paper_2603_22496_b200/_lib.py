@@ -35,6 +35,7 @@ SIGNATURES = {
     "kkb_kk_plan_create": [P, P, P, P, I, I, I, I, I, P, D, D, I, P, P],
     "kkb_kk_plan_run": [P, P, I, LL, P, I, LL, P, P, P],
     "kkb_kk_plan_run_ex": [P, P, I, LL, P, I, LL, P, P, I, P],
+    "kkb_kk_plan_run_scatter": [P, P, I, LL, P, I, LL, I, LL, P],
     "kkb_kk_plan_window": [P],
     "kkb_kk_plan_destroy": [P],
     "kkb_kk_taps": [P, P, P, P, I, I, I, I, I, D, D, I, P, P],
@@ -57,6 +58,11 @@ SIGNATURES = {
     "kkb_max_f64": [P, LL, P, P],
     "kkb_gamma_match": [P, P, LL, D, D, D, P, P, P],
     "kkb_last_read_sample_max": [P, I, P, I, P, P, I, P, P, I, P, P],
+    "kkb_ipc_alloc": [LL, P],
+    "kkb_ipc_free": [P],
+    "kkb_ipc_get_handle": [P, P],
+    "kkb_ipc_open_handle": [P, P],
+    "kkb_ipc_close_handle": [P],
 }
 _RESTYPES = {
     "kkb_version": ctypes.c_char_p,
@@ -88,6 +94,7 @@ class KKRFHeader(ctypes.Structure):
 
 KKB_OUT_C64 = 0
 KKB_RUN_ACCUMULATE_INTENSITY = 1
+KKB_MAX_DST = 8  # destinations of kkb_kk_plan_run_scatter
 KKB_OUT_C128 = 1
 
 _lib = None

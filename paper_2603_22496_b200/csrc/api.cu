@@ -215,6 +215,71 @@ extern "C" int kkb_kk_plan_run_ex(kkb_kk_plan *p, const void *data, int n_frames
                      p->W, as_stream(stream), (flags & KKB_RUN_ACCUMULATE_INTENSITY) ? 1 : 0);
 }
 
+extern "C" int kkb_kk_plan_run_scatter(kkb_kk_plan *p, const void *data, int n_frames,
+                                       long long data_frame_stride, void *const *dst_host,
+                                       int n_dst, long long dst_offset, int out_kind,
+                                       long long out_frame_stride, void *stream) {
+    if (!p || n_dst < 1 || n_dst > KKB_MAX_DST || !dst_host || dst_offset < 0) {
+        set_error("kk_plan_run_scatter: 1 <= n_dst <= %d destinations, offset >= 0", KKB_MAX_DST);
+        return KKB_ERR_ARG;
+    }
+    int st = check_kk_args(p->N, p->M, p->T, p->nx, p->nz, out_kind);
+    if (st) return st;
+    KKScatter sc{};
+    sc.ndst = n_dst;
+    sc.dst_off = dst_offset;
+    for (int d = 0; d < n_dst; ++d) {
+        if (!dst_host[d]) {
+            set_error("kk_plan_run_scatter: null destination %d", d);
+            return KKB_ERR_ARG;
+        }
+        sc.dst[d] = dst_host[d];
+    }
+    return kk_gather(reinterpret_cast<const float2 *>(data), p->N, p->M, p->T, p->ltx, p->ltzT,
+                     p->lrx, p->lrzT, p->nx, p->nz, p->w, p->fs, p->shift, p->linear, nullptr,
+                     out_kind, n_frames, data_frame_stride, out_frame_stride, nullptr, nullptr,
+                     p->W, as_stream(stream), 0, &sc);
+}
+
+// ------------------------------------------------------------- CUDA IPC (row-block P2P)
+extern "C" int kkb_ipc_alloc(long long bytes, void **ptr) {
+    if (bytes <= 0 || !ptr) {
+        set_error("ipc_alloc: bad size");
+        return KKB_ERR_ARG;
+    }
+    *ptr = nullptr;
+    KKB_TRY_CUDA(cudaMalloc(ptr, (size_t)bytes), "cudaMalloc(ipc buffer)");
+    return KKB_OK;
+}
+
+extern "C" int kkb_ipc_free(void *ptr) {
+    if (ptr) KKB_TRY_CUDA(cudaFree(ptr), "cudaFree(ipc buffer)");
+    return KKB_OK;
+}
+
+extern "C" int kkb_ipc_get_handle(const void *ptr, void *handle64) {
+    if (!ptr || !handle64) return KKB_ERR_ARG;
+    cudaIpcMemHandle_t h;
+    KKB_TRY_CUDA(cudaIpcGetMemHandle(&h, const_cast<void *>(ptr)), "cudaIpcGetMemHandle");
+    static_assert(sizeof(h) == 64, "CUDA IPC handles are 64 bytes");
+    memcpy(handle64, &h, sizeof(h));
+    return KKB_OK;
+}
+
+extern "C" int kkb_ipc_open_handle(const void *handle64, void **ptr) {
+    if (!handle64 || !ptr) return KKB_ERR_ARG;
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle64, sizeof(h));
+    *ptr = nullptr;
+    KKB_TRY_CUDA(cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+    return KKB_OK;
+}
+
+extern "C" int kkb_ipc_close_handle(void *ptr) {
+    if (ptr) KKB_TRY_CUDA(cudaIpcCloseMemHandle(ptr), "cudaIpcCloseMemHandle");
+    return KKB_OK;
+}
+
 extern "C" int kkb_kk_plan_run(kkb_kk_plan *p, const void *data, int n_frames,
                                long long data_frame_stride, void *out, int out_kind,
                                long long out_frame_stride, float *intensity,

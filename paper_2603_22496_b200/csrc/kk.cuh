@@ -51,11 +51,19 @@ int transpose_f64(const double *in, int rows, int cols, double *out, cudaStream_
 int kk_window(const double *ltx, const double *ltz, const double *lrx, const double *lrz, int N,
               int M, int nx, int nz, double fs, double shift, int *window_out, cudaStream_t s);
 
+#define KKB_MAX_DST 8
+// fused row-block all-gather targets of the gather epilogue (device pointers)
+struct KKScatter {
+    int ndst;
+    long long dst_off;
+    void *dst[KKB_MAX_DST];
+};
+
 int kk_gather(const float2 *data, int N, int M, int T, const double *ltx, const double *ltzT,
               const double *lrx, const double *lrzT, int nx, int nz, const double *w, double fs,
               double shift, int linear, void *out, int out_kind, int n_frames, long long data_fs,
               long long out_fs, float *inten, unsigned *fmax, int W, cudaStream_t s,
-              int accum = 0);
+              int accum = 0, const KKScatter *sc = nullptr);
 
 int kk_taps(const double *ltx, const double *ltz, const double *lrx, const double *lrz, int N, int M,
             int T, int nx, int nz, double fs, double shift, int linear, int *idx, cudaStream_t s);

@@ -248,6 +248,12 @@ struct KKArgs {
     float *inten;
     unsigned *fmax;
     int accum;  // 1: intensity += |IQ|^2 (incoherent multi-set compounding)
+    // fused row-block all-gather: when ndst > 0 every IQ pixel is also stored
+    // at dst[d] + dst_off + ix*nz + iz for d < ndst (peers' image buffers
+    // mapped over NVLink with CUDA IPC; the stores are the collective)
+    int ndst;
+    long long dst_off;
+    void *dst[KKB_MAX_DST];
 };
 
 // packed LUT index: tile row r -> (r/8)*4 + r%4 pair slot, a = (r/4)&1
@@ -496,11 +502,17 @@ k_kk_gather(const KKArgs a) {
                 const float vr = accr[p][r], vi = acci[p][r];  // float32 totals: one accumulator
 #endif
                 const long long px = (long long)f * a.out_fs + (long long)ix * nz + iz;
-                if (a.out_kind == KKB_OUT_C128) {
-                    reinterpret_cast<double2 *>(a.out)[px] = make_double2(vr, vi);
-                } else {
-                    reinterpret_cast<float2 *>(a.out)[px] =
-                        make_float2((float)vr, (float)vi);
+                if (a.out) {
+                    if (a.out_kind == KKB_OUT_C128)
+                        reinterpret_cast<double2 *>(a.out)[px] = make_double2(vr, vi);
+                    else
+                        reinterpret_cast<float2 *>(a.out)[px] = make_float2((float)vr, (float)vi);
+                }
+                for (int d = 0; d < a.ndst; ++d) {
+                    if (a.out_kind == KKB_OUT_C128)
+                        reinterpret_cast<double2 *>(a.dst[d])[a.dst_off + px] = make_double2(vr, vi);
+                    else
+                        reinterpret_cast<float2 *>(a.dst[d])[a.dst_off + px] = make_float2((float)vr, (float)vi);
                 }
                 if (a.inten) {
                     float I = (float)(vr * vr + vi * vi);
@@ -559,10 +571,18 @@ k_kk_direct(const KKArgs a) {
         }
         const float ar = (float)tr_, ai = (float)ti_;
         const long long px = (long long)f * a.out_fs + i;
-        if (a.out_kind == KKB_OUT_C128)
-            reinterpret_cast<double2 *>(a.out)[px] = make_double2(tr_, ti_);
-        else
-            reinterpret_cast<float2 *>(a.out)[px] = make_float2(ar, ai);
+        if (a.out) {
+            if (a.out_kind == KKB_OUT_C128)
+                reinterpret_cast<double2 *>(a.out)[px] = make_double2(tr_, ti_);
+            else
+                reinterpret_cast<float2 *>(a.out)[px] = make_float2(ar, ai);
+        }
+        for (int d = 0; d < a.ndst; ++d) {
+            if (a.out_kind == KKB_OUT_C128)
+                reinterpret_cast<double2 *>(a.dst[d])[a.dst_off + px] = make_double2(tr_, ti_);
+            else
+                reinterpret_cast<float2 *>(a.dst[d])[a.dst_off + px] = make_float2(ar, ai);
+        }
         if (a.inten) {
             float I = ar * ar + ai * ai;
             if (a.accum) I += a.inten[px];
@@ -586,7 +606,8 @@ static size_t kk_smem_bytes(int N, int M, int W, int MCH, bool linear) {
 int kk_gather(const float2 *data, int N, int M, int T, const double *ltx, const double *ltzT,
               const double *lrx, const double *lrzT, int nx, int nz, const double *w, double fs,
               double shift, int linear, void *out, int out_kind, int n_frames, long long data_fs,
-              long long out_fs, float *inten, unsigned *fmax, int W, cudaStream_t s, int accum) {
+              long long out_fs, float *inten, unsigned *fmax, int W, cudaStream_t s, int accum,
+              const KKScatter *sc) {
     if (n_frames <= 0 || nx <= 0 || nz <= 0) return KKB_OK;
     if (W < 2) W = 2;
     const char *force = getenv("KKB_KK_DIRECT");  // test hook: the per-pixel fallback
@@ -595,7 +616,12 @@ int kk_gather(const float2 *data, int N, int M, int T, const double *ltx, const 
     if (W > KKB_KK_STAGE_ELEMS || too_big || (force && force[0] == '1')) {
         // steep geometry: the tile's trace window would not fit the staging buffer
         KKArgs a{data, data_fs, N, M, T, ltx, ltzT, lrx, lrzT, w, fs, shift, nx, nz, W, 0,
-                 out, out_kind, out_fs, inten, fmax, accum};
+                 out, out_kind, out_fs, inten, fmax, accum, 0, 0, {}};
+        if (sc) {
+            a.ndst = sc->ndst;
+            a.dst_off = sc->dst_off;
+            for (int d = 0; d < sc->ndst; ++d) a.dst[d] = sc->dst[d];
+        }
         dim3 grid((unsigned)ceil_div((long long)nx * nz, 256), (unsigned)n_frames);
         if (linear)
             k_kk_direct<true><<<grid, 256, 0, s>>>(a);
@@ -609,7 +635,12 @@ int kk_gather(const float2 *data, int N, int M, int T, const double *ltx, const 
     while (MCH > 1 && kk_smem_bytes(N, M, W, MCH, linear) > 200 * 1024) MCH = (MCH + 1) / 2;
     size_t sm = kk_smem_bytes(N, M, W, MCH, linear);
     KKArgs a{data, data_fs, N, M, T, ltx, ltzT, lrx, lrzT, w, fs, shift, nx, nz, W, MCH,
-             out, out_kind, out_fs, inten, fmax, accum};
+             out, out_kind, out_fs, inten, fmax, accum, 0, 0, {}};
+    if (sc) {
+        a.ndst = sc->ndst;
+        a.dst_off = sc->dst_off;
+        for (int d = 0; d < sc->ndst; ++d) a.dst[d] = sc->dst[d];
+    }
     dim3 grid((unsigned)ceil_div(nz, KKB_KK_TZ), (unsigned)ceil_div(nx, KKB_KK_TX), (unsigned)n_frames);
     dim3 block(KKB_KK_WZ * KKB_KK_WX * 32);
     if (linear) {

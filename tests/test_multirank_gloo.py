@@ -54,6 +54,9 @@ def _worker(rank, world, port, out_dir):
                            p_range=(ix0 * nz, ix1 * nz), threads=1)
         block = torch.from_numpy(part.astype(np.complex64).reshape(ix1 - ix0, nz))
         full = shard.gather_row_blocks(block, nx, nz)
+        # P2P transport plumbing: every rank receives all 64-byte handles in rank order
+        hs = shard.exchange_handles(bytes([rank]) * 64)
+        assert hs == [bytes([r]) * 64 for r in range(world)]
         np.save(os.path.join(out_dir, f"rank{rank}.npy"), full.numpy())
         # frame sharding: each rank sums its frames' ids; all-reduce checks coverage
         b, e = shard.frame_range(400, rank, world)
