@@ -1,10 +1,11 @@
 // K4 delay tables, K5 kk pixel gather, K6 detection / log-compression epilogue.
 //
 // K5 replaces _kk_kernel (beamform.py:212-236).  Work decomposition:
-//   * CTA = one 32 x 32 pixel tile of one frame; a warp covers 8 depth rows x
-//     16 columns with each lane owning 2 x 2 pixels, so for each of its four
-//     pixel slots the warp is a 4 x 8 block whose delays span only a few
-//     samples: tap reads from shared memory are mostly broadcasts.
+//   * CTA = one TZ x TX = 32 x 64 pixel tile of one frame (8 warps); a warp
+//     covers 8 depth rows x 32 columns and lane (zt, xt) = (lane % 4, lane / 4)
+//     owns the 2 x 4 pixels rows zt + {0, 4}, columns xt + {0, 8, 16, 24}, so
+//     the per-receive table reads (row delays, column delays, window start +
+//     weight) are shared by 8 taps.
 //   * The (transmit n, receive-chunk) stages are pipelined: while stage s is
 //     summed, the trace windows of stage s+1 are loaded into registers and
 //     written to the other shared-memory buffer as (2 d0 - d1, d1 - d0)
@@ -16,13 +17,16 @@
 //     explicit _rn intrinsics (no FMA contraction: the exact IEEE sequence
 //     of beamform.py:223,225), then ONE round-down add of 1.5*2^20 whose high
 //     word minus 0x41380000 is floor(fi) and whose low word is frac*2^32 —
-//     the in-window predicate is an unsigned compare, the lerp weight is
-//     (low >> 9) | 1.0f.  No branches: out-of-window taps get weight 0.
-//     Taps and partial sums over receive angles are float32; each transmit's
-//     partial is folded into a float64 total in fixed order (deterministic,
-//     no atomics).
-// Output complex64 or complex128, plus optional fused |IQ|^2 and per-frame
-// max for the dB epilogue (K6).
+//     the in-window predicate is folded into the staged window (entries of
+//     out-of-trace samples are zero), the lerp weight is (low >> 9) | 1.0f.
+//     Taps and the per-pixel sum are float32, accumulated in fixed order
+//     (deterministic, no atomics; KKB_KK_F64_TOTAL=1 keeps float64 totals).
+//   * Geometries whose window or pair tables do not fit shared memory run the
+//     per-pixel kernel k_kk_direct (same index math, lerp and epilogue).
+// Output complex64 or complex128, plus optional fused |IQ|^2 (optionally
+// accumulated across receive sets) and per-frame max for the dB epilogue
+// (K6), and optional P2P stores of every pixel into peers' image buffers
+// (fused row-block all-gather, kkb_kk_plan_run_scatter).
 
 #include <algorithm>
 #include <cstdlib>
