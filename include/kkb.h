@@ -73,7 +73,8 @@ int kkb_build_kk_luts(double x0, double dx, int nx, double z0, double dz, int nz
  * nearest: j = floor(fi + 0.5), read iff 0 <= j <= T-1; else adds 0.
  * fi is evaluated in float64 in exactly that order (tap indices and the
  * in-window predicate are bit-identical to the reference); taps and the
- * per-transmit partial sums are float32, the running sum float64.
+ * per-pixel sum are float32 in a fixed order (the reference's c64 pixel
+ * accumulation differs from its c128 image by ~2e-7).
  * `weights` may be NULL (all ones, beamform.py:239-241).
  * n_frames frames share the tables: data frame f at data + f*data_frame_stride
  * (complex elements), out frame f at out + f*out_frame_stride (elements).

@@ -7,7 +7,8 @@
 //   fi = ((ltx + ltz) + h) * fs + shift                   (beamform.py:189,198)
 // all in float64 with explicit IEEE round-to-nearest steps, so tap indices
 // and gating are bit-identical to the reference; taps are float32 lerps,
-// element partials float32, transmit totals float64.
+// element partials float32, transmit totals float64 (per-pixel kernel; the
+// tiled kernel below sums per-element float32 partials into float64).
 //
 // One thread per pixel, consecutive threads along depth (the reference's
 // flattened p = ix*nz + iz order), hyp rows and traces read through L1
