@@ -126,6 +126,9 @@ static int das_gather_direct(const float2 *data, int n_tx, int n_el, int n_t, co
 #define KKB_DAS_TX 32
 #define KKB_DAS_NT 256
 #define KKB_DAS_STAGE 1024
+#ifndef KKB_DAS_MINB
+#define KKB_DAS_MINB 2  // CTAs per SM (register cap 128)
+#endif
 
 __device__ __forceinline__ int das_prow(int r) { return ((r >> 3) << 3) + ((r & 3) << 1) + ((r >> 2) & 1); }
 __device__ __forceinline__ int das_pcol(int c) { return ((c >> 4) << 4) + ((c & 7) << 1) + ((c >> 3) & 1); }
@@ -196,7 +199,7 @@ k_das_window(const DasArgs a, int *wmax) {
 }
 
 template <bool LINEAR>
-__global__ void __launch_bounds__(KKB_DAS_NT, 2)
+__global__ void __launch_bounds__(KKB_DAS_NT, KKB_DAS_MINB)
 k_das_tile(const DasArgs a) {
     constexpr int TZ = KKB_DAS_TZ, TX = KKB_DAS_TX, NT = KKB_DAS_NT;
     constexpr int EPT = KKB_DAS_STAGE / NT;
