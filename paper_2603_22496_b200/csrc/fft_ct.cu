@@ -176,7 +176,10 @@ struct Plan;
 template <>
 struct Plan<1024> { static constexpr int NT = 64, R0 = 16, R1 = 8, R2 = 8, R3 = 1; };
 template <>
-struct Plan<1536> { static constexpr int NT = 128, R0 = 16, R1 = 12, R2 = 8, R3 = 1; };
+#ifndef KKB_FFT1536_NT
+#define KKB_FFT1536_NT 128
+#endif
+struct Plan<1536> { static constexpr int NT = KKB_FFT1536_NT, R0 = 16, R1 = 12, R2 = 8, R3 = 1; };
 template <>
 struct Plan<2048> { static constexpr int NT = 128, R0 = 16, R1 = 16, R2 = 8, R3 = 1; };
 template <>
