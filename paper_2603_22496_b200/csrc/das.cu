@@ -123,7 +123,15 @@ static int das_gather_direct(const float2 *data, int n_tx, int n_el, int n_t, co
 // window is sized for floor(fi_max) + 2.  Entries of out-of-trace samples are
 // zero, so the reference's in-window test needs no per-tap predicate.
 #define KKB_DAS_TZ 32
-#define KKB_DAS_TX 32
+#ifndef KKB_DAS_CX
+#define KKB_DAS_CX 2  // pixel columns per lane
+#endif
+#define KKB_DAS_TX (16 * KKB_DAS_CX)
+#if KKB_DAS_CX > 2
+typedef float das_total_t;  // 8 pixels per lane: float totals keep registers < 128
+#else
+typedef double das_total_t;
+#endif
 #define KKB_DAS_NT 256
 #define KKB_DAS_STAGE 1024
 #ifndef KKB_DAS_MINB
@@ -131,7 +139,12 @@ static int das_gather_direct(const float2 *data, int n_tx, int n_el, int n_t, co
 #endif
 
 __device__ __forceinline__ int das_prow(int r) { return ((r >> 3) << 3) + ((r & 3) << 1) + ((r >> 2) & 1); }
-__device__ __forceinline__ int das_pcol(int c) { return ((c >> 4) << 4) + ((c & 7) << 1) + ((c >> 3) & 1); }
+// tile column c -> warp block c/(8CX), lane slot c%8, column j = (c/8)%CX (a lane's CX
+// columns contiguous)
+__device__ __forceinline__ int das_pcol(int c) {
+    constexpr int CX = KKB_DAS_CX;
+    return (c / (8 * CX)) * (8 * CX) + (c & 7) * CX + ((c >> 3) % CX);
+}
 
 struct DasArgs {
     const float2 *data;
@@ -316,21 +329,22 @@ k_das_tile(const DasArgs a) {
         if (tid < min(NCH, N - n0)) lo_s[buf * NCH + tid] = lo_of(n0 + tid, l) + KKB_MAGIC2_HI_DAS;
     };
 
-    // this lane's pixels: rows zq -> r, r + 4 of the packed slot, cols c, c + 8
-    int ixp[2], izp[2];
+    // this lane's pixels: rows zq -> r, r + 4 of the packed slot, cols c + 8j
+    constexpr int CX = KKB_DAS_CX;
+    int ixp[CX], izp[2];
 #pragma unroll
-    for (int j = 0; j < 2; ++j) {
-        ixp[j] = min(ix0 + wx * 16 + j * 8 + xt, nx - 1);
-        izp[j] = min(iz0 + wz * 8 + j * 4 + zt, nz - 1);
-    }
-    double accr[2][2], acci[2][2], h[2][2], hn[2][2];
-    float pr[2][2], pi[2][2];
-    unsigned gate = 0, gaten = 0;  // bit (p * 2 + r): pixel skips this element
+    for (int j = 0; j < CX; ++j) ixp[j] = min(ix0 + wx * 8 * CX + j * 8 + xt, nx - 1);
+#pragma unroll
+    for (int j = 0; j < 2; ++j) izp[j] = min(iz0 + wz * 8 + j * 4 + zt, nz - 1);
+    das_total_t accr[2][CX], acci[2][CX];
+    double h[2][CX], hn[2][CX];
+    float pr[2][CX], pi[2][CX];
+    unsigned gate = 0, gaten = 0;  // bit (p * CX + r): pixel skips this element
     float wl = 1.f, wln = 1.f;
 #pragma unroll
     for (int p = 0; p < 2; ++p)
 #pragma unroll
-        for (int r = 0; r < 2; ++r) {
+        for (int r = 0; r < CX; ++r) {
             accr[p][r] = acci[p][r] = 0.0;
             pr[p][r] = pi[p][r] = 0.f;
             h[p][r] = hn[p][r] = 0.0;
@@ -345,13 +359,13 @@ k_das_tile(const DasArgs a) {
 #pragma unroll
         for (int p = 0; p < 2; ++p)
 #pragma unroll
-            for (int r = 0; r < 2; ++r) {
+            for (int r = 0; r < CX; ++r) {
                 const long long row = ixp[r] + bl;
                 double hv = a.hyp[row * nz + izp[p]];
                 if (fr > 0.0) hv = __dadd_rn(hv, __dmul_rn(fr, __dsub_rn(a.hyp[(row + 1) * nz + izp[p]], hv)));
                 hn[p][r] = hv;
                 if (fabs(__dsub_rn(a.xcoord[ixp[r]], ul)) > __dmul_rn(a.zcoord[izp[p]], a.tan_max))
-                    gaten |= 1u << (p * 2 + r);
+                    gaten |= 1u << (p * CX + r);
             }
     };
 
@@ -374,7 +388,7 @@ k_das_tile(const DasArgs a) {
 #pragma unroll
             for (int p = 0; p < 2; ++p)
 #pragma unroll
-                for (int r = 0; r < 2; ++r) h[p][r] = hn[p][r];
+                for (int r = 0; r < CX; ++r) h[p][r] = hn[p][r];
             gate = gaten;
             wl = wln;
         }
@@ -389,20 +403,26 @@ k_das_tile(const DasArgs a) {
         for (int q = 0; q < nc; ++q) {
             const int n = n0 + q;
             const double2 tz = reinterpret_cast<const double2 *>(ltz_p + n * TZ)[zq];
-            const double2 tx = reinterpret_cast<const double2 *>(ltx_p + n * TX)[xq];
+            double txv[CX];
+#pragma unroll
+            for (int j = 0; j < CX / 2; ++j) {
+                const double2 tx = reinterpret_cast<const double2 *>(ltx_p + n * TX + xq * CX)[j];
+                txv[2 * j] = tx.x;
+                txv[2 * j + 1] = tx.y;
+            }
             const int loC = lo_b[q];
             const Entry *wv = wb + q * W;
 #pragma unroll
             for (int p = 0; p < 2; ++p) {
 #pragma unroll
-                for (int r = 0; r < 2; ++r) {
-                    const double t = __dadd_rn(r ? tx.y : tx.x, p ? tz.y : tz.x);
+                for (int r = 0; r < CX; ++r) {
+                    const double t = __dadd_rn(txv[r], p ? tz.y : tz.x);
                     const double fi = das_fi(t, h[p][r], fs, shift);
                     const double sv = __dadd_rd(LINEAR ? fi : __dadd_rn(fi, 0.5), KKB_FLOOR_MAGIC2_DAS);
                     const unsigned e = min((unsigned)(__double2hiint(sv) - loC),
                                            (unsigned)(LINEAR ? W - 2 : W - 1));
                     // gated pixels weigh 0 (the reference skips them, beamform.py:191)
-                    const float m = ((gate >> (p * 2 + r)) & 1u) ? 0.f : wl;
+                    const float m = ((gate >> (p * CX + r)) & 1u) ? 0.f : wl;
                     if constexpr (LINEAR) {
                         const float4 v = wv[e];
                         const float f1 = __uint_as_float(((unsigned)__double2loint(sv) >> 9) + 0x3F800000u);
@@ -420,9 +440,9 @@ k_das_tile(const DasArgs a) {
 #pragma unroll
             for (int p = 0; p < 2; ++p)
 #pragma unroll
-                for (int r = 0; r < 2; ++r) {
-                    accr[p][r] += (double)pr[p][r];
-                    acci[p][r] += (double)pi[p][r];
+                for (int r = 0; r < CX; ++r) {
+                    accr[p][r] += (das_total_t)pr[p][r];
+                    acci[p][r] += (das_total_t)pi[p][r];
                     pr[p][r] = pi[p][r] = 0.f;
                 }
         }
@@ -435,8 +455,8 @@ k_das_tile(const DasArgs a) {
     for (int p = 0; p < 2; ++p) {
         const int iz = iz0 + wz * 8 + p * 4 + zt;
 #pragma unroll
-        for (int r = 0; r < 2; ++r) {
-            const int ix = ix0 + wx * 16 + r * 8 + xt;
+        for (int r = 0; r < CX; ++r) {
+            const int ix = ix0 + wx * 8 * CX + r * 8 + xt;
             if (iz < nz && ix < nx) {
                 const long long px = (long long)ix * nz + iz;
                 if (a.groups > 1)
