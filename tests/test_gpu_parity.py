@@ -429,3 +429,21 @@ def test_kk_ten_thousand_pairs(oracle, small_array):
     ref = oracle.kk_kernel(data, luts.lut_tx_x, luts.lut_tx_z, luts.lut_rx_x, luts.lut_rx_z,
                            np.ones(100), small_array.sampling_frequency, 0.0)
     assert rel_l2(kb.kk(rfc, luts).pixels, ref) <= 1e-5
+
+
+@pytest.mark.parametrize("T", [8192, 4099])
+def test_analytic_signal_largest_and_prime_above_radix_lengths(oracle, T):
+    # the maximum supported length (KKB_FFT_MAX_T) and a length with a prime
+    # factor > 31 (4099 is prime: direct DFT kernel)
+    x = np.random.default_rng(T).standard_normal((1, 3, T)).astype(np.float32)
+    arr = kb.TransducerArray(3, 0.23e-3, 5.2e6, 20.83e6, 0.67)
+    out = kb.analytic_signal(kb.RFVolume(x, arr, kb.AcquisitionParams(C, [0.0], T))).data
+    assert rel_l2(out, oracle.analytic_signal(x)) <= 1e-5, T
+
+
+def test_analytic_signal_rejects_too_long_traces():
+    T = 8193
+    arr = kb.TransducerArray(2, 0.23e-3, 5.2e6, 20.83e6, 0.67)
+    vol = kb.RFVolume(np.zeros((1, 2, T), np.float32), arr, kb.AcquisitionParams(C, [0.0], T))
+    with pytest.raises(kb.KKBeamError):
+        kb.analytic_signal(vol)
