@@ -339,6 +339,7 @@ def run_gpu(args):
     s1_bytes = F * (4.0 * N * L * T + 2 * 8.0 * N * L * ldk + 2 * 8.0 * N * M * ldk + 8.0 * N * M * T)
     s1_min = F * (4.0 * N * L * T + 8.0 * N * M * T)
     s1_achieved = s1_bytes / (dec_ms / 1e3) / 1e9
+    frame_bytes = 4.0 * N * L * T + 2 * 8.0 * N * M * T + 8.0 * P + 8.0 * (g.nx + g.nz) * (N + M)
 
     # ---- end to end through the public API: pinned host RF in, host IQ out ----
     e2e = e2e_i16 = None
@@ -426,6 +427,11 @@ def run_gpu(args):
                                 "algorithmic_bytes": "16 B of taps per pixel-pair (SURVEY 8d)",
                                 "pixel_pairs_per_s": pp_frame * fl / (kk_launch_ms / 1e3),
                                 "pixel_pairs_per_s_isolated": pp_frame * F / (kk_ms / 1e3)},
+            "frame_roofline": {"bound": "hbm", "bytes_per_frame": frame_bytes,
+                               "achieved": value / world * frame_bytes / 1e9, "peak": hbm_peak,
+                               "unit": "GB/s", "frac": value / world * frame_bytes / 1e9 / hbm_peak,
+                               "algorithmic_bytes": "SURVEY 8(d) compulsory HBM per frame: RF in "
+                                                    "+ traces write/read + IQ out + tables"},
             "stage1_roofline": {"kernels": "k_r2c + k_contract_sym + k_c2c", "bound": "hbm",
                                 "achieved": s1_achieved, "peak": hbm_peak, "unit": "GB/s",
                                 "frac": s1_achieved / hbm_peak, "ms": dec_ms,
