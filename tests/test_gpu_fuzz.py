@@ -1,0 +1,114 @@
+"""Seeded random geometries through kk / das / compress against the oracle:
+pair counts, trace lengths, grid shapes and spacings, shifts, interpolation
+modes and weights drawn at random (edge sizes included: 1 transmit, 1 receive
+angle, 1-pixel rows), so the tiled kernels, their fallbacks and the window
+sizing meet geometries the fixed configs do not."""
+
+import numpy as np
+import pytest
+
+from conftest import C, rel_l2
+
+pytestmark = pytest.mark.gpu
+
+import paper_2603_22496_b200 as kb  # noqa: E402
+
+
+def _sym(rng, m, amax):
+    half = np.sort(rng.uniform(0.0, amax, m // 2))
+    ang = np.concatenate([-half[::-1], [0.0] if m % 2 else [], half])
+    return ang
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_kk_random_geometry(oracle, seed):
+    rng = np.random.default_rng(1000 + seed)
+    n_tx = int(rng.integers(1, 10))
+    m_rx = int(rng.integers(1, 13))
+    T = int(rng.choice([64, 100, 256, 777, 1024, 1536, 2048]))
+    nx, nz = int(rng.integers(1, 90)), int(rng.integers(1, 90))
+    fs = float(rng.uniform(10e6, 40e6))
+    arr = kb.TransducerArray(16, 0.3e-3, fs / 4, fs, 0.6)
+    tx = _sym(rng, n_tx, 0.3) if n_tx > 1 else np.array([float(rng.uniform(-0.2, 0.2))])
+    params = kb.AcquisitionParams(C, tx, T, start_time=float(rng.uniform(0, 3e-6)))
+    rx = kb.explicit_angles(_sym(rng, m_rx, 0.35))
+    dx, dz = float(rng.uniform(0.02e-3, 0.6e-3)), float(rng.uniform(0.02e-3, 0.6e-3))
+    grid = kb.ImageGrid(float(rng.uniform(-5e-3, 0)), float(rng.uniform(1e-3, 10e-3)), dx, dz, nx, nz)
+    data = (rng.standard_normal((n_tx, m_rx, T)) + 1j * rng.standard_normal((n_tx, m_rx, T))).astype(np.complex64)
+    rfc = kb.CompressedRF(data, rx, params, arr)
+    luts = kb.build_kk_luts(grid, params, rx)
+    linear = bool(rng.integers(0, 2))
+    pd = float(rng.uniform(-0.5e-6, 0.5e-6))
+    w = rng.uniform(0.2, 2.0, m_rx) if rng.integers(0, 2) else None
+    cfg = kb.BeamformConfig(interpolation="linear" if linear else "nearest", pulse_delay=pd,
+                            channel_weights=w)
+    got = kb.kk(rfc, luts, cfg).pixels
+    shift = (pd - params.start_time) * fs
+    ref = oracle.kk_kernel(data, luts.lut_tx_x, luts.lut_tx_z, luts.lut_rx_x, luts.lut_rx_z,
+                           w if w is not None else np.ones(m_rx), fs, shift, linear=linear)
+    if np.abs(ref).max() == 0:
+        assert np.abs(got).max() == 0
+    else:
+        assert rel_l2(got, ref) <= 1e-5, (seed, n_tx, m_rx, T, nx, nz)
+
+
+@pytest.mark.parametrize("seed", range(20))
+def test_das_random_geometry(oracle, seed):
+    rng = np.random.default_rng(2000 + seed)
+    n_tx = int(rng.integers(1, 8))
+    L = int(rng.integers(2, 40))
+    T = int(rng.choice([128, 512, 1000, 2048]))
+    nx, nz = int(rng.integers(1, 70)), int(rng.integers(1, 70))
+    fs = float(rng.uniform(10e6, 40e6))
+    arr = kb.TransducerArray(L, float(rng.uniform(0.1e-3, 0.4e-3)), fs / 4, fs, 0.6)
+    tx = _sym(rng, n_tx, 0.3) if n_tx > 1 else np.array([0.1])
+    params = kb.AcquisitionParams(C, tx, T, start_time=float(rng.uniform(0, 2e-6)))
+    grid = kb.ImageGrid(float(rng.uniform(-4e-3, 0)), float(rng.uniform(1e-3, 8e-3)),
+                        float(rng.uniform(0.03e-3, 0.4e-3)), float(rng.uniform(0.03e-3, 0.4e-3)), nx, nz)
+    data = (rng.standard_normal((n_tx, L, T)) + 1j * rng.standard_normal((n_tx, L, T))).astype(np.complex64)
+    an = kb.AnalyticRF(data, arr, params)
+    luts = kb.build_das_luts(grid, arr, params)
+    gate = float(rng.uniform(0.1, 0.8)) if rng.integers(0, 2) else None
+    linear = bool(rng.integers(0, 2))
+    w = rng.uniform(0.2, 2.0, L) if rng.integers(0, 2) else None
+    cfg = kb.BeamformConfig(interpolation="linear" if linear else "nearest", max_rx_angle=gate,
+                            channel_weights=w)
+    got = kb.das(an, luts, cfg).pixels
+    ref = oracle.das_kernel(data, luts.lut_tx_x, luts.lut_tx_z, luts.lut_rx_hypot, luts.rx_base,
+                            luts.rx_frac, grid.x, grid.z, arr.positions,
+                            np.tan(gate) if gate is not None else np.inf,
+                            w if w is not None else np.ones(L), fs, -params.start_time * fs,
+                            linear=linear)
+    if np.abs(ref).max() == 0:
+        assert np.abs(got).max() == 0
+    else:
+        assert rel_l2(got, ref) <= 1e-5, (seed, n_tx, L, T, nx, nz)
+
+
+@pytest.mark.parametrize("seed", range(10))
+def test_decomposition_random_geometry(oracle, seed):
+    # analytic_signal + compress (the accuracy path) and the batched engine
+    # decomposition on random element counts, lengths and angle sets
+    import torch
+
+    rng = np.random.default_rng(3000 + seed)
+    n_tx = int(rng.integers(1, 6))
+    L = int(rng.integers(2, 70))
+    T = int(rng.choice([96, 250, 512, 1024, 1536, 2048]))
+    m_rx = int(rng.integers(1, 12))
+    fs = float(rng.uniform(10e6, 40e6))
+    arr = kb.TransducerArray(L, float(rng.uniform(0.1e-3, 0.4e-3)), fs / 4, fs, 0.6)
+    params = kb.AcquisitionParams(C, np.linspace(-0.1, 0.1, n_tx), T)
+    rx = kb.explicit_angles(_sym(rng, m_rx, 0.3))
+    rf = rng.standard_normal((n_tx, L, T)).astype(np.float32)
+    ref = oracle.decompose_f64(rf, fs, arr.positions, rx.angles, C)
+    an = kb.analytic_signal(kb.RFVolume(rf, arr, params))
+    got = kb.compress(an, rx, last_used_sample=0).data
+    assert rel_l2(got, ref) <= 1e-5, (seed, n_tx, L, T, m_rx)
+    grid = kb.ImageGrid(-1e-3, 2e-3, 0.1e-3, 0.1e-3, 4, 4)
+    eng = kb.KKEngine(arr, params, rx, grid, frames=2, want_db=False)
+    eng.decompose(torch.from_numpy(np.stack([rf, rf])).cuda())
+    torch.cuda.synchronize()
+    tr = eng.traces.cpu().numpy()
+    assert rel_l2(tr[0], ref) <= 1e-5 and np.array_equal(tr[0], tr[1]), (seed, n_tx, L, T, m_rx)
+    eng.close()
