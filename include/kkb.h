@@ -144,7 +144,10 @@ int kkb_das(const void *data, int n_tx, int n_el, int n_t,
 /* ------------------------------------------------------------ K1/K3: spectral
  * Replaces analytic_signal (spectral.py:84-93): length-T FFT of each float32
  * trace, one-sided weights (spectral.py:65-81), inverse FFT -> complex64.
- * Any T >= 2 with T <= 8192 (mixed radix 2/3/4/5/8 plus direct odd radices). */
+ * Any T >= 1 up to 2^20: one transform per CTA for T <= 8192 (mixed radix
+ * 2/3/4/5/8 plus direct odd radices <= 31, direct DFT for larger prime
+ * factors), a four-step T = T1 x T2 transform above 8192 (direct DFT when T
+ * has no such split). */
 int kkb_analytic_signal(const float *rf, long long n_traces, int n_t, void *out, void *stream);
 
 /* ------------------------------------------------------------ K1-K3: decomposition

@@ -139,6 +139,10 @@ static int check_kk_args(int n_tx, int n_rx, int n_t, int nx, int nz, int out_ki
         set_error("kk: unknown out_kind %d", out_kind);
         return KKB_ERR_ARG;
     }
+    if (n_t > (1 << 19)) {  // tap_index: RD(fi + 1.5*2^20) resolves |fi| < 2^19
+        set_error("kk: %d samples per trace exceed the 2^19 tap-index range", n_t);
+        return KKB_ERR_UNSUPPORTED;
+    }
     return KKB_OK;
 }
 
@@ -348,9 +352,9 @@ extern "C" int kkb_das(const void *data, int n_tx, int n_el, int n_t, const doub
 // K1/K3: analytic_signal
 extern "C" int kkb_analytic_signal(const float *rf, long long n_traces, int n_t, void *out,
                                    void *stream) {
-    if (n_traces < 0 || n_t < 1 || n_t > KKB_FFT_MAX_T) {
+    if (n_traces < 0 || n_t < 1 || n_t > KKB_FFT_MAX_T_TOTAL) {
         set_error("analytic_signal: unsupported T=%d", n_t);
-        return n_t > KKB_FFT_MAX_T ? KKB_ERR_UNSUPPORTED : KKB_ERR_ARG;
+        return n_t > KKB_FFT_MAX_T_TOTAL ? KKB_ERR_UNSUPPORTED : KKB_ERR_ARG;
     }
     if (n_traces == 0) return KKB_OK;
     cudaStream_t s = as_stream(stream);
@@ -366,7 +370,7 @@ extern "C" int kkb_analytic_signal(const float *rf, long long n_traces, int n_t,
     KKB_TRY_CUDA(cudaMemcpyAsync(scale.p, sc.data(), sizeof(float) * K, cudaMemcpyHostToDevice, s),
                  "copy weights");
     float2 *X = (float2 *)spec.p;
-    if (plan.direct) {
+    if (plan.direct || plan.large) {
         if ((st = promo.alloc(sizeof(float2) * (size_t)n_traces * T))) return st;
         if ((st = fft_r2c(rf, n_traces, T, X, K, K, nullptr, s, (float2 *)promo.p))) return st;
         long long total = n_traces * K;
@@ -386,7 +390,7 @@ extern "C" int kkb_analytic_signal(const float *rf, long long n_traces, int n_t,
 extern "C" int kkb_shear_and_sum(const void *data, int n_tx, int n_el, int n_t,
                                  const double *positions_host, const double *angles_host, int n_rx,
                                  double fs, double c, void *out, void *stream) {
-    if (n_tx < 1 || n_el < 1 || n_rx < 1 || n_t < 1 || n_t > KKB_FFT_MAX_T || !(c > 0)) {
+    if (n_tx < 1 || n_el < 1 || n_rx < 1 || n_t < 1 || n_t > KKB_FFT_MAX_T_TOTAL || !(c > 0)) {
         set_error("shear_and_sum: bad sizes");
         return KKB_ERR_ARG;
     }
@@ -486,7 +490,7 @@ static int build_symmetric_classes(kkb_decomposer *p, const double *pos, const d
 extern "C" int kkb_decomposer_create(int n_tx, int n_el, int n_t, const double *positions_host,
                                      const double *angles_host, int n_rx, double fs, double c,
                                      int max_frames, kkb_decomposer **out) {
-    if (n_tx < 1 || n_el < 1 || n_rx < 1 || n_t < 2 || n_t > KKB_FFT_MAX_T || max_frames < 1 ||
+    if (n_tx < 1 || n_el < 1 || n_rx < 1 || n_t < 2 || n_t > KKB_FFT_MAX_T_TOTAL || max_frames < 1 ||
         !(c > 0)) {
         set_error("decomposer: bad sizes");
         return KKB_ERR_ARG;
@@ -494,10 +498,7 @@ extern "C" int kkb_decomposer_create(int n_tx, int n_el, int n_t, const double *
     FftPlan plan;
     int st = get_fft_plan(n_t, &plan);
     if (st) return st;
-    if (plan.direct) {
-        set_error("decomposer: T=%d has a prime factor > 31 (use kkb_shear_and_sum)", n_t);
-        return KKB_ERR_UNSUPPORTED;
-    }
+    (void)plan;  // lengths without a single-CTA plan are promoted to complex per pass (run)
     kkb_decomposer *p = new (std::nothrow) kkb_decomposer();
     if (!p) return KKB_ERR_NOMEM;
     p->N = n_tx;
@@ -578,11 +579,19 @@ static int decomposer_run(kkb_decomposer *p, const void *rf, int in_kind, int n_
         int F = std::min(p->chunk, n_frames - f0);
         const char *rf_c = (const char *)rf + (size_t)f0 * N * L * T * esz;
         float2 *tr_c = (float2 *)traces + (size_t)f0 * N * M * T;
-        if (in_kind)
+        if (in_kind) {
             st = fft_r2c_ct(rf_c, 1, (long long)F * N * L, T, X, ldk, K, nullptr, plan.tws, cs);
-        else
+        } else if (plan.direct || plan.large) {
+            // lengths without a single-CTA real plan: promote to complex first
+            float2 *promo = nullptr;
+            KKB_TRY_CUDA(cudaMallocAsync(&promo, sizeof(float2) * (size_t)F * N * L * T, cs),
+                         "cudaMallocAsync(promote)");
+            st = fft_r2c((const float *)rf_c, (long long)F * N * L, T, X, ldk, K, nullptr, cs, promo);
+            cudaFreeAsync(promo, cs);
+        } else {
             st = fft_r2c((const float *)rf_c, (long long)F * N * L, T, X, ldk, K, nullptr, cs,
                          nullptr);
+        }
         if (st) return st;
         if (p->P > 0)
             st = contract_sym(X, ldk, p->cs, ldk, Y, ldk, (long long)F * N, L, M, K, p->P,

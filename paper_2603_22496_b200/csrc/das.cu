@@ -502,7 +502,9 @@ int das_gather(const float2 *data, int n_tx, int n_el, int n_t, const double *lt
     (void)n_hyp_rows;
     if ((long long)nx * nz <= 0) return KKB_OK;
     const char *force = getenv("KKB_DAS_DIRECT");  // test hook: the per-pixel fallback kernel
-    if (force && force[0] == '1')
+    // the tiled kernel's floor add resolves |fi| < 2^19; longer traces use the
+    // per-pixel kernel (1.5*2^52 magic)
+    if ((force && force[0] == '1') || n_t > (1 << 19))
         return das_gather_direct(data, n_tx, n_el, n_t, ltx, ltz, hyp, base, frac, xcoord, zcoord,
                                  upos, tan_max, weights, fs, shift, linear, nx, nz, out, out_kind, s);
     DasArgs a{data, n_tx, n_el, n_t, ltx, ltz, hyp, base, frac, xcoord, zcoord, upos, tan_max,

@@ -45,13 +45,29 @@ int get_fft_plan(int T, FftPlan *out) {
         *out = it->second;
         return KKB_OK;
     }
-    if (T < 1 || T > KKB_FFT_MAX_T) {
-        set_error("FFT length %d outside [1, %d]", T, KKB_FFT_MAX_T);
+    if (T < 1 || T > KKB_FFT_MAX_T_TOTAL) {
+        set_error("FFT length %d outside [1, %d]", T, KKB_FFT_MAX_T_TOTAL);
         return KKB_ERR_UNSUPPORTED;
     }
     FftPlan p{};
     p.T = T;
     int t = T;
+    if (T > KKB_FFT_MAX_T) {
+        // four-step split T = T1 x T2, both single-CTA lengths, T1 as close to
+        // sqrt(T) as the divisors allow; no such split -> direct DFT
+        for (int a = (int)std::sqrt((double)T); a >= 2; --a) {
+            if (T % a) continue;
+            const int b = T / a;
+            if (a <= KKB_FFT_MAX_T && b <= KKB_FFT_MAX_T) {
+                p.T1 = b;  // the larger factor first (rows of length T1)
+                p.T2 = a;
+                break;
+            }
+        }
+        p.large = p.T1 > 0 ? 1 : 0;
+        p.direct = p.large ? 0 : 1;
+        t = 1;
+    }
     const int order[] = {8, 4, 2, 3, 5, 7, 11, 13, 17, 19, 23, 29, 31};
     for (int r : order) {
         while (t % r == 0) {
@@ -60,8 +76,8 @@ int get_fft_plan(int T, FftPlan *out) {
             t /= r;
         }
     }
-    p.direct = (t != 1) ? 1 : 0;
-    if (p.direct) p.nstages = 0;
+    if (T <= KKB_FFT_MAX_T) p.direct = (t != 1) ? 1 : 0;
+    if (p.direct || p.large) p.nstages = 0;
     std::vector<float2> tw(T);
     for (int k = 0; k < T; ++k) {
         // exp(-2 pi i k / T) in double, reduced exactly by symmetry
@@ -406,6 +422,92 @@ __global__ void k_real_to_complex(const float *__restrict__ in, long long n, flo
         out[i] = make_float2(in[i], 0.f);
 }
 
+// ------------------------------------------------------------- four-step (T > 8192)
+// X[k1 + T1 k2] = sum_n2 W_T2^(n2 k2) W_T^(n2 k1) sum_n1 W_T1^(n1 k1) x[n1 T2 + n2]:
+// three batched transposes around two batches of single-CTA transforms.
+// MODE 0: A[tr][n2][n1] = x[tr][n1 T2 + n2]         (zero past in_len)
+// MODE 1: A[tr][k1][n2] = B[tr][n2][k1] * W_T^(+-n2 k1)
+// MODE 2: out[tr][k2 T1 + k1] = B[tr][k1][k2] * scale (* bin_scale), k < out_len
+template <int MODE>
+__global__ void __launch_bounds__(256)
+k_fourstep(const float2 *__restrict__ src, long long src_stride, int src_len, float2 *__restrict__ dst,
+           long long dst_stride, int dst_len, int R, int C, const float2 *__restrict__ tw, int T,
+           int inverse, float scale, const float *__restrict__ bin_scale) {
+    // transpose of an R x C matrix (row r, column c) per trace, 32 x 32 tiles
+    __shared__ float2 tile[32][33];
+    const long long tr = blockIdx.z;
+    const int c0 = blockIdx.x * 32, r0 = blockIdx.y * 32;
+    const float2 *s = src + tr * src_stride;
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+        const int r = r0 + i, c = c0 + threadIdx.x;
+        float2 v = make_float2(0.f, 0.f);
+        if (r < R && c < C) {
+            const long long e = (long long)r * C + c;
+            if (MODE != 0 || e < src_len) v = s[e];
+            if (MODE == 1) {  // source row r = n2, column c = k1
+                float2 w = tw[(long long)r * c % T];
+                if (inverse) w.y = -w.y;
+                v = make_float2(v.x * w.x - v.y * w.y, v.x * w.y + v.y * w.x);
+            }
+        }
+        tile[i][threadIdx.x] = v;
+    }
+    __syncthreads();
+    float2 *d = dst + tr * dst_stride;
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+        const int c = c0 + i, r = r0 + threadIdx.x;  // destination row c, column r
+        if (r < R && c < C) {
+            const long long e = (long long)c * R + r;
+            float2 v = tile[threadIdx.x][i];
+            if (MODE == 2) {
+                if (e >= dst_len) continue;
+                const float sc = scale * (bin_scale ? bin_scale[e] : 1.0f);
+                v = make_float2(v.x * sc, v.y * sc);
+            }
+            d[e] = v;
+        }
+    }
+}
+
+int fft_c2c(const float2 *in, long long in_stride, int in_len, float2 *out, long long out_stride,
+            int out_len, long long ntraces, int T, bool inverse, float scale, cudaStream_t s);
+
+static int fft_c2c_large(const FftPlan &p, const float2 *in, long long in_stride, int in_len,
+                         float2 *out, long long out_stride, int out_len, long long ntraces,
+                         bool inverse, float scale, const float *bin_scale, cudaStream_t s) {
+    const int T = p.T, T1 = p.T1, T2 = p.T2;
+    if (ntraces > 65535) {
+        set_error("four-step FFT: %lld traces per call exceed the grid limit", ntraces);
+        return KKB_ERR_UNSUPPORTED;
+    }
+    float2 *A = nullptr, *B = nullptr;
+    KKB_TRY_CUDA(cudaMallocAsync(&A, sizeof(float2) * (size_t)ntraces * T, s), "cudaMallocAsync(4step A)");
+    KKB_TRY_CUDA(cudaMallocAsync(&B, sizeof(float2) * (size_t)ntraces * T, s), "cudaMallocAsync(4step B)");
+    const dim3 blk(32, 8);
+    int st = KKB_OK;
+    // x as T1 rows (n1) x T2 columns (n2) -> A rows n2 of length T1
+    k_fourstep<0><<<dim3(ceil_div(T2, 32), ceil_div(T1, 32), ntraces), blk, 0, s>>>(
+        in, in_stride, in_len, A, T, T, T1, T2, p.tw, T, 0, 1.f, nullptr);
+    KKB_CHECK_LAUNCH("k_fourstep<load>");
+    if (!st) st = fft_c2c(A, T1, T1, B, T1, T1, ntraces * T2, T1, inverse, 1.0f, s);
+    if (!st) {
+        // B rows n2 (T2) x columns k1 (T1), twiddled -> A rows k1 of length T2
+        k_fourstep<1><<<dim3(ceil_div(T1, 32), ceil_div(T2, 32), ntraces), blk, 0, s>>>(
+            B, T, T, A, T, T, T2, T1, p.tw, T, inverse ? 1 : 0, 1.f, nullptr);
+        KKB_CHECK_LAUNCH("k_fourstep<twiddle>");
+        st = fft_c2c(A, T2, T2, B, T2, T2, ntraces * T1, T2, inverse, 1.0f, s);
+    }
+    if (!st) {
+        // B rows k1 (T1) x columns k2 (T2) -> natural order k = k2 T1 + k1
+        k_fourstep<2><<<dim3(ceil_div(T2, 32), ceil_div(T1, 32), ntraces), blk, 0, s>>>(
+            B, T, T, out, out_stride, out_len, T1, T2, p.tw, T, 0, scale, bin_scale);
+        KKB_CHECK_LAUNCH("k_fourstep<store>");
+    }
+    cudaFreeAsync(A, s);
+    cudaFreeAsync(B, s);
+    return st;
+}
+
 // ------------------------------------------------------------- host launchers
 // Compile-time-specialised kernels (fft_ct.cu) for T in {1024, 1536, 2048, 4096};
 // KKB_FFT_GENERIC=1 in the environment forces the runtime-plan kernels (tests).
@@ -435,6 +537,8 @@ int fft_c2c(const float2 *in, long long in_stride, int in_len, float2 *out, long
     FftPlan p;
     int st = get_fft_plan(T, &p);
     if (st) return st;
+    if (p.large) return fft_c2c_large(p, in, in_stride, in_len, out, out_stride, out_len, ntraces,
+                                      inverse, scale, nullptr, s);
     if (p.direct) {
         dim3 grid((unsigned)ceil_div(out_len, 256), (unsigned)ntraces);
         k_dft_direct<<<grid, 256, 0, s>>>(in, in_stride, in_len, out, out_stride, out_len, ntraces,
@@ -461,9 +565,10 @@ int fft_r2c(const float *in, long long ntraces, int T, float2 *out, long long ou
     FftPlan p;
     int st = get_fft_plan(T, &p);
     if (st) return st;
-    if (p.direct) {
-        // promote to complex (scratch holds ntraces*T) then direct DFT; scaling
-        // by bin_scale is not supported here (callers fold it elsewhere)
+    if (p.direct || p.large) {
+        // promote to complex (scratch holds ntraces*T) then the direct DFT or
+        // the four-step transform; scaling by bin_scale is not supported here
+        // (callers fold it elsewhere)
         if (!scratch_c2c || bin_scale) {
             set_error("direct-DFT r2c path needs scratch and no bin scale");
             return KKB_ERR_UNSUPPORTED;

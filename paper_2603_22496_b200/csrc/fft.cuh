@@ -7,7 +7,8 @@
 
 #define KKB_FFT_MAX_STAGES 16
 #define KKB_FFT_MAX_RADIX 32
-#define KKB_FFT_MAX_T 8192
+#define KKB_FFT_MAX_T 8192            // one transform per CTA in shared memory
+#define KKB_FFT_MAX_T_TOTAL (1 << 20) // longer: four-step T = T1 x T2 (or direct DFT)
 #define KKB_FFT_THREADS 256
 #define KKB_FFT_TARGET_ELEMS 4096  // traces per CTA = max(1, this / T)
 
@@ -17,6 +18,8 @@ struct FftPlan {
     int T;
     int nstages;
     int direct;                      // 1: largest prime factor > 31 -> O(T^2) kernel
+    int large;                       // 1: T > KKB_FFT_MAX_T, four-step with T = T1 * T2
+    int T1, T2;
     int radix[KKB_FFT_MAX_STAGES];
     float2 *tw;                      // exp(-2 pi i k / T), k < T (device)
     float2 *tws;                     // stage-ordered twiddles of the compile-time plan (device; fft_ct_supported T only)

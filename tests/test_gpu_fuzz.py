@@ -94,7 +94,7 @@ def test_decomposition_random_geometry(oracle, seed):
     rng = np.random.default_rng(3000 + seed)
     n_tx = int(rng.integers(1, 6))
     L = int(rng.integers(2, 70))
-    T = int(rng.choice([96, 250, 512, 1024, 1536, 2048]))
+    T = int(rng.choice([96, 250, 512, 1021, 1024, 1536, 2048]))
     m_rx = int(rng.integers(1, 12))
     fs = float(rng.uniform(10e6, 40e6))
     arr = kb.TransducerArray(L, float(rng.uniform(0.1e-3, 0.4e-3)), fs / 4, fs, 0.6)

@@ -431,18 +431,40 @@ def test_kk_ten_thousand_pairs(oracle, small_array):
     assert rel_l2(kb.kk(rfc, luts).pixels, ref) <= 1e-5
 
 
-@pytest.mark.parametrize("T", [8192, 4099])
-def test_analytic_signal_largest_and_prime_above_radix_lengths(oracle, T):
-    # the maximum supported length (KKB_FFT_MAX_T) and a length with a prime
-    # factor > 31 (4099 is prime: direct DFT kernel)
+@pytest.mark.parametrize("T", [8192, 4099, 8193, 12288, 20000, 10007])
+def test_analytic_signal_long_and_awkward_lengths(oracle, T):
+    # the largest single-CTA length (8192), a prime factor > 31 (4099: direct
+    # DFT), four-step lengths above 8192 (8193 = 3 x 2731, 12288, 20000) and a
+    # prime above 8192 (10007: direct DFT)
     x = np.random.default_rng(T).standard_normal((1, 3, T)).astype(np.float32)
     arr = kb.TransducerArray(3, 0.23e-3, 5.2e6, 20.83e6, 0.67)
     out = kb.analytic_signal(kb.RFVolume(x, arr, kb.AcquisitionParams(C, [0.0], T))).data
     assert rel_l2(out, oracle.analytic_signal(x)) <= 1e-5, T
 
 
+def test_long_trace_decomposition_and_compress(oracle, small_array):
+    # T = 12288 (four-step FFT) through compress and the batched engine
+    import torch
+
+    T = 12288
+    params = kb.AcquisitionParams(C, [0.0, 0.1], T)
+    rf = np.random.default_rng(41).standard_normal((2, 64, T)).astype(np.float32)
+    rf_gpu = rf.copy()
+    rx = kb.uniform_vernier_angles(7, 5, 12 * DEG, 1)
+    ref = oracle.decompose_f64(rf, small_array.sampling_frequency, small_array.positions,
+                               rx.angles, C)
+    an = kb.analytic_signal(kb.RFVolume(rf, small_array, params))
+    assert rel_l2(kb.compress(an, rx, last_used_sample=0).data, ref) <= 1e-5
+    grid = kb.ImageGrid(-1e-3, 2e-3, 0.1e-3, 0.1e-3, 4, 4)
+    eng = kb.KKEngine(small_array, params, rx, grid, frames=1, want_db=False)
+    eng.decompose(torch.from_numpy(rf_gpu[None]).cuda())
+    torch.cuda.synchronize()
+    assert rel_l2(eng.traces[0].cpu().numpy(), ref) <= 1e-5
+    eng.close()
+
+
 def test_analytic_signal_rejects_too_long_traces():
-    T = 8193
+    T = (1 << 20) + 2
     arr = kb.TransducerArray(2, 0.23e-3, 5.2e6, 20.83e6, 0.67)
     vol = kb.RFVolume(np.zeros((1, 2, T), np.float32), arr, kb.AcquisitionParams(C, [0.0], T))
     with pytest.raises(kb.KKBeamError):
