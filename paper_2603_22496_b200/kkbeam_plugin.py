@@ -1,11 +1,13 @@
 """Reference-side binding: route the reference package's own kernels to libkkb.
 
-The reference (`kkbeam`) has no FFI; its wrappers look up three module
+The reference (`kkbeam`) has no FFI; its wrappers look up these module
 globals at call time:
 
 * ``kkbeam.beamform._kk_kernel``   (beamform.py:212-236, called at 363-374)
 * ``kkbeam.beamform._das_kernel``  (beamform.py:178-209, called at 281-297)
 * ``kkbeam.compress.shear_and_sum`` (compress.py:54-82, called at 120)
+* ``kkbeam.simulate._render_traces`` (simulate.py:187-220, called at 280-293;
+  the forward simulator, §8(f) row 4 — bit-identical on the GPU)
 
 The shims below have exactly those signatures (flat numpy arrays in, the
 caller's ``out`` array filled in place) and run the sm_100a kernels through
@@ -73,6 +75,22 @@ def shear_and_sum(data, sampling_frequency, positions, angles, sound_speed):
     return gpu_shear(data, sampling_frequency, positions, angles, sound_speed)
 
 
+def render_traces(out, sx, sz, refl, upos, sin_t, cos_t, inv_c, fs, t0, wave, half, spread):
+    """Drop-in for kkbeam.simulate._render_traces: adds the echoes to `out`
+    (float32 (N, L, T), in place), bit-identical to the numba kernel."""
+    n_tx, n_el, n_t = out.shape
+    d_out = dev.to_device(np.ascontiguousarray(out, dtype=np.float32))
+    arrs = [dev.to_device(np.ascontiguousarray(a, dtype=np.float64)) for a in
+            (sx, sz, refl, upos, sin_t, cos_t, wave)]
+    _lib.call("kkb_render_traces", dev.ptr(d_out), n_tx, n_el, n_t, dev.ptr(arrs[0]),
+              dev.ptr(arrs[1]), dev.ptr(arrs[2]), int(np.asarray(sx).size), dev.ptr(arrs[3]),
+              dev.ptr(arrs[4]), dev.ptr(arrs[5]), float(inv_c), float(fs), float(t0),
+              dev.ptr(arrs[6]), int(np.asarray(wave).size), float(half), int(bool(spread)),
+              dev.stream_handle())
+    dev.synchronize()
+    out[...] = dev.to_host(d_out)
+
+
 class Installed:
     """Handle returned by install(); ``restore()`` puts the originals back."""
 
@@ -99,4 +117,8 @@ def install(kkbeam_pkg=None) -> Installed:
     bf._kk_kernel = kk_kernel
     bf._das_kernel = das_kernel
     cp.shear_and_sum = shear_and_sum
+    sim = sys.modules.get("kkbeam.simulate")
+    if sim is not None and hasattr(sim, "_render_traces"):
+        saved[(sim, "_render_traces")] = sim._render_traces
+        sim._render_traces = render_traces
     return Installed(saved)

@@ -201,15 +201,17 @@ def test_plugin_install_on_the_real_reference():
         from paper_2603_22496_b200 import kkbeam_plugin
 
         bf, cp = sys.modules["kkbeam.beamform"], sys.modules["kkbeam.compress"]
-        orig = (bf._kk_kernel, bf._das_kernel, cp.shear_and_sum)
+        sim = sys.modules["kkbeam.simulate"]
+        orig = (bf._kk_kernel, bf._das_kernel, cp.shear_and_sum, sim._render_traces)
         h = kkbeam_plugin.install(kkbeam)
         assert bf._kk_kernel is kkbeam_plugin.kk_kernel
         assert bf._das_kernel is kkbeam_plugin.das_kernel
         assert cp.shear_and_sum is kkbeam_plugin.shear_and_sum
+        assert sim._render_traces is kkbeam_plugin.render_traces
         # the package-level name keeps the float64 original (oracle stays intact)
         assert kkbeam.shear_and_sum is orig[2]
         h.restore()
-        assert (bf._kk_kernel, bf._das_kernel, cp.shear_and_sum) == orig
+        assert (bf._kk_kernel, bf._das_kernel, cp.shear_and_sum, sim._render_traces) == orig
     finally:
         sys.path.remove(src)
 

@@ -60,3 +60,24 @@ def test_install_rebinds_and_restores():
                 sys.modules.pop(k, None)
             else:
                 sys.modules[k] = v
+
+
+def test_render_traces_shim_is_bit_identical(oracle):
+    # the numba signature of _render_traces (simulate.py:187-220): the shim adds
+    # the echoes into the caller's float32 array, like the reference
+    from conftest import sha
+
+    import paper_2603_22496_b200 as kb
+    from paper_2603_22496_b200 import configs
+
+    w = configs.config1()
+    g = golden("config1")
+    arr, p = w.array, w.params
+    out = np.zeros((p.num_transmits, arr.num_elements, p.num_samples), np.float32)
+    kkbeam_plugin.render_traces(out, g["phantom_x"], g["phantom_z"], np.ones(5), arr.positions,
+                                np.sin(p.transmit_angles), np.cos(p.transmit_angles),
+                                1.0 / p.sound_speed, arr.sampling_frequency, p.start_time,
+                                g["pulse"], float((g["pulse"].size - 1) // 2), False)
+    out += 1e-3 * np.random.default_rng(0).standard_normal(out.shape, dtype=np.float32)
+    assert sha(out) == str(g["rf_sha"])
+    assert kb.simulate_rf is not None
