@@ -8,6 +8,9 @@ globals at call time:
 * ``kkbeam.compress.shear_and_sum`` (compress.py:54-82, called at 120)
 * ``kkbeam.simulate._render_traces`` (simulate.py:187-220, called at 280-293;
   the forward simulator, §8(f) row 4 — bit-identical on the GPU)
+* ``kkbeam.metrics.gamma_match`` and the CLI's imported name
+  ``kkbeam.cli.gamma_match`` (metrics.py:175-202, called at cli.py:167; the
+  display map, §8(f) row 2)
 
 The shims below have exactly those signatures (flat numpy arrays in, the
 caller's ``out`` array filled in place) and run the sm_100a kernels through
@@ -91,6 +94,21 @@ def render_traces(out, sx, sz, refl, upos, sin_t, cos_t, inv_c, fs, t0, wave, ha
     out[...] = dev.to_host(d_out)
 
 
+def gamma_match(image, reference, lo=0.1, hi=1.0, tol=1e-3):
+    """Drop-in for kkbeam.metrics.gamma_match: the golden-section search with
+    every objective evaluated on the device; raises the reference's own
+    MetricError for all-zero images."""
+    if image.pixels.max() <= 0 or reference.pixels.max() <= 0:
+        err = sys.modules.get("kkbeam.errors")
+        exc = getattr(err, "MetricError", None) if err is not None else None
+        if exc is None:
+            from .errors import MetricError as exc
+        raise exc("gamma matching needs nonzero images")
+    from .display import gamma_match as device_gamma_match
+
+    return device_gamma_match(image, reference, lo, hi, tol)
+
+
 class Installed:
     """Handle returned by install(); ``restore()`` puts the originals back."""
 
@@ -121,4 +139,9 @@ def install(kkbeam_pkg=None) -> Installed:
     if sim is not None and hasattr(sim, "_render_traces"):
         saved[(sim, "_render_traces")] = sim._render_traces
         sim._render_traces = render_traces
+    for name in ("kkbeam.metrics", "kkbeam.cli"):
+        mod = sys.modules.get(name)
+        if mod is not None and hasattr(mod, "gamma_match"):
+            saved[(mod, "gamma_match")] = mod.gamma_match
+            mod.gamma_match = gamma_match
     return Installed(saved)

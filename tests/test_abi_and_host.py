@@ -202,8 +202,14 @@ def test_plugin_install_on_the_real_reference():
 
         bf, cp = sys.modules["kkbeam.beamform"], sys.modules["kkbeam.compress"]
         sim = sys.modules["kkbeam.simulate"]
+        import kkbeam.cli  # noqa: F401  (the CLI imports gamma_match by name)
+
+        met, cli = sys.modules["kkbeam.metrics"], sys.modules["kkbeam.cli"]
         orig = (bf._kk_kernel, bf._das_kernel, cp.shear_and_sum, sim._render_traces)
+        orig_g = (met.gamma_match, cli.gamma_match)
         h = kkbeam_plugin.install(kkbeam)
+        assert met.gamma_match is kkbeam_plugin.gamma_match
+        assert cli.gamma_match is kkbeam_plugin.gamma_match
         assert bf._kk_kernel is kkbeam_plugin.kk_kernel
         assert bf._das_kernel is kkbeam_plugin.das_kernel
         assert cp.shear_and_sum is kkbeam_plugin.shear_and_sum
@@ -212,6 +218,7 @@ def test_plugin_install_on_the_real_reference():
         assert kkbeam.shear_and_sum is orig[2]
         h.restore()
         assert (bf._kk_kernel, bf._das_kernel, cp.shear_and_sum, sim._render_traces) == orig
+        assert (met.gamma_match, cli.gamma_match) == orig_g
     finally:
         sys.path.remove(src)
 

@@ -81,3 +81,19 @@ def test_render_traces_shim_is_bit_identical(oracle):
     out += 1e-3 * np.random.default_rng(0).standard_normal(out.shape, dtype=np.float32)
     assert sha(out) == str(g["rf_sha"])
     assert kb.simulate_rf is not None
+
+
+def test_gamma_match_shim_matches_reference():
+    import os
+
+    sys.path.insert(0, os.path.join(os.path.dirname(__file__), "golden"))
+    from make_display_golden import images
+
+    import paper_2603_22496_b200 as kb
+
+    G = np.load(os.path.join(os.path.dirname(__file__), "golden", "display.npz"))
+    grid, a, b = images(kb, 0)
+    g, m = kkbeam_plugin.gamma_match(kb.IntensityImage(a, grid), kb.IntensityImage(b, grid))
+    assert abs(g - float(G["gamma_0"])) <= 1e-12
+    with pytest.raises(kb.MetricError):
+        kkbeam_plugin.gamma_match(kb.IntensityImage(np.zeros_like(a), grid), kb.IntensityImage(b, grid))
