@@ -147,7 +147,7 @@ static int check_kk_args(int n_tx, int n_rx, int n_t, int nx, int nz, int out_ki
 }
 
 struct kkb_kk_plan {
-    int N, M, T, nx, nz, linear, W;
+    int N, M, T, nx, nz, linear, W, W_small;  // trace windows of the big / small tiles
     double fs, shift;
     double *ltx, *ltzT, *lrx, *lrzT, *w;  // one allocation
 };
@@ -197,6 +197,9 @@ extern "C" int kkb_kk_plan_create(const double *ltx, const double *ltz, const do
     if ((st = transpose_f64(ltz, nz, n_tx, p->ltzT, s))) return fail(st);
     if ((st = transpose_f64(lrz, nz, n_rx, p->lrzT, s))) return fail(st);
     if ((st = kk_window(ltx, ltz, lrx, lrz, n_tx, n_rx, nx, nz, fs, shift, &p->W, s))) return fail(st);
+    if ((st = kk_window(ltx, ltz, lrx, lrz, n_tx, n_rx, nx, nz, fs, shift, &p->W_small, s,
+                        KKB_KK_S_TX, KKB_KK_S_TZ)))
+        return fail(st);
     *out = p;
     return KKB_OK;
 }
@@ -216,7 +219,8 @@ extern "C" int kkb_kk_plan_run_ex(kkb_kk_plan *p, const void *data, int n_frames
     return kk_gather(reinterpret_cast<const float2 *>(data), p->N, p->M, p->T, p->ltx, p->ltzT,
                      p->lrx, p->lrzT, p->nx, p->nz, p->w, p->fs, p->shift, p->linear, out,
                      out_kind, n_frames, data_frame_stride, out_frame_stride, intensity, frame_max,
-                     p->W, as_stream(stream), (flags & KKB_RUN_ACCUMULATE_INTENSITY) ? 1 : 0);
+                     p->W, as_stream(stream), (flags & KKB_RUN_ACCUMULATE_INTENSITY) ? 1 : 0,
+                     nullptr, p->W_small);
 }
 
 extern "C" int kkb_kk_plan_run_scatter(kkb_kk_plan *p, const void *data, int n_frames,
@@ -242,7 +246,7 @@ extern "C" int kkb_kk_plan_run_scatter(kkb_kk_plan *p, const void *data, int n_f
     return kk_gather(reinterpret_cast<const float2 *>(data), p->N, p->M, p->T, p->ltx, p->ltzT,
                      p->lrx, p->lrzT, p->nx, p->nz, p->w, p->fs, p->shift, p->linear, nullptr,
                      out_kind, n_frames, data_frame_stride, out_frame_stride, nullptr, nullptr,
-                     p->W, as_stream(stream), 0, &sc);
+                     p->W, as_stream(stream), 0, &sc, p->W_small);
 }
 
 // ------------------------------------------------------------- CUDA IPC (row-block P2P)

@@ -25,6 +25,14 @@ typedef float kk_total_t;
 #endif
 #define KKB_KK_TZ (8 * KKB_KK_WZ)
 #define KKB_KK_TX (8 * KKB_KK_CX * KKB_KK_WX)
+// small-tile instance for batches whose big-tile grid cannot fill the SMs (a
+// single small frame): 16 x 16 pixels, 2 warps; the per-pixel sums run in the
+// same (n, m) order, so both instances give bit-identical images
+#define KKB_KK_S_WZ 2
+#define KKB_KK_S_WX 1
+#define KKB_KK_S_CX 2
+#define KKB_KK_S_TZ (8 * KKB_KK_S_WZ)
+#define KKB_KK_S_TX (8 * KKB_KK_S_CX * KKB_KK_S_WX)
 #ifndef KKB_KK_STAGE_ELEMS
 #define KKB_KK_STAGE_ELEMS 1024  // window entries staged per pipeline stage
 #endif
@@ -49,7 +57,8 @@ int transpose_f64(const double *in, int rows, int cols, double *out, cudaStream_
 // Synchronises `s`: returns the shared-memory window length (samples) one
 // gather tile needs for these tables.
 int kk_window(const double *ltx, const double *ltz, const double *lrx, const double *lrz, int N,
-              int M, int nx, int nz, double fs, double shift, int *window_out, cudaStream_t s);
+              int M, int nx, int nz, double fs, double shift, int *window_out, cudaStream_t s,
+              int tile_x = KKB_KK_TX, int tile_z = KKB_KK_TZ);
 
 #define KKB_MAX_DST 8
 // fused row-block all-gather targets of the gather epilogue (device pointers)
@@ -63,7 +72,7 @@ int kk_gather(const float2 *data, int N, int M, int T, const double *ltx, const 
               const double *lrx, const double *lrzT, int nx, int nz, const double *w, double fs,
               double shift, int linear, void *out, int out_kind, int n_frames, long long data_fs,
               long long out_fs, float *inten, unsigned *fmax, int W, cudaStream_t s,
-              int accum = 0, const KKScatter *sc = nullptr);
+              int accum = 0, const KKScatter *sc = nullptr, int W_small = 0);
 
 int kk_taps(const double *ltx, const double *ltz, const double *lrx, const double *lrz, int N, int M,
             int T, int nx, int nz, double fs, double shift, int linear, int *idx, cudaStream_t s);

@@ -211,11 +211,12 @@ __global__ void k_kk_window(const double *__restrict__ ltx, const double *__rest
 }
 
 int kk_window(const double *ltx, const double *ltz, const double *lrx, const double *lrz, int N,
-              int M, int nx, int nz, double fs, double shift, int *window_out, cudaStream_t s) {
+              int M, int nx, int nz, double fs, double shift, int *window_out, cudaStream_t s,
+              int tile_x, int tile_z) {
     int *d = nullptr;
     KKB_TRY_CUDA(cudaMallocAsync(&d, sizeof(int), s), "cudaMallocAsync(window)");
     KKB_TRY_CUDA(cudaMemsetAsync(d, 0, sizeof(int), s), "memset(window)");
-    k_kk_window<<<512, 256, 0, s>>>(ltx, ltz, lrx, lrz, N, M, nx, nz, KKB_KK_TX, KKB_KK_TZ, fs, shift,
+    k_kk_window<<<512, 256, 0, s>>>(ltx, ltz, lrx, lrz, N, M, nx, nz, tile_x, tile_z, fs, shift,
                                     d);
     KKB_CHECK_LAUNCH("k_kk_window");
     int h = 0;
@@ -275,7 +276,8 @@ k_kk_gather(const KKArgs a) {
     constexpr int TZ = 8 * WZ;
     constexpr int TX = 8 * CX * WX;
     constexpr int NT = WZ * WX * 32;
-    constexpr int EPT = KKB_KK_STAGE_ELEMS / NT;  // staged window entries per thread
+    // staged window entries per thread (the big instance stages KKB_KK_STAGE_ELEMS)
+    constexpr int EPT = KKB_KK_STAGE_ELEMS / (32 * KKB_KK_WZ * KKB_KK_WX);
     using Entry = typename std::conditional<LINEAR, float4, float2>::type;
     const int N = a.N, M = a.M, T = a.T, W = a.W, MCH = a.MCH, nx = a.nx, nz = a.nz;
     const int nchunk = (M + MCH - 1) / MCH;
@@ -600,32 +602,61 @@ k_kk_direct(const KKArgs a) {
     }
 }
 
-static size_t kk_smem_bytes(int N, int M, int W, int MCH, bool linear) {
+static size_t kk_smem_bytes(int N, int M, int W, int MCH, bool linear, int tz = KKB_KK_TZ,
+                            int tx = KKB_KK_TX) {
     size_t entry = linear ? sizeof(float4) : sizeof(float2);
-    return entry * 2 * MCH * W +
-           sizeof(double) * ((size_t)(M + N) * KKB_KK_TZ + (size_t)(M + N) * KKB_KK_TX) +
+    return entry * 2 * MCH * W + sizeof(double) * ((size_t)(M + N) * tz + (size_t)(M + N) * tx) +
            sizeof(int2) * (size_t)N * M;
+}
+
+template <int WZ, int WX, int CX>
+static int launch_tiled(const KKArgs &a, int n_frames, size_t sm, bool linear, cudaStream_t s) {
+    constexpr int TZ = 8 * WZ, TX = 8 * CX * WX;
+    dim3 grid((unsigned)ceil_div(a.nz, TZ), (unsigned)ceil_div(a.nx, TX), (unsigned)n_frames);
+    dim3 block(WZ * WX * 32);
+    if (linear) {
+        auto fn = k_kk_gather<WZ, WX, CX, true>;
+        KKB_TRY_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm),
+                     "smem attr kk");
+        fn<<<grid, block, sm, s>>>(a);
+    } else {
+        auto fn = k_kk_gather<WZ, WX, CX, false>;
+        KKB_TRY_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm),
+                     "smem attr kk");
+        fn<<<grid, block, sm, s>>>(a);
+    }
+    KKB_CHECK_LAUNCH("k_kk_gather");
+    return KKB_OK;
 }
 
 int kk_gather(const float2 *data, int N, int M, int T, const double *ltx, const double *ltzT,
               const double *lrx, const double *lrzT, int nx, int nz, const double *w, double fs,
               double shift, int linear, void *out, int out_kind, int n_frames, long long data_fs,
               long long out_fs, float *inten, unsigned *fmax, int W, cudaStream_t s, int accum,
-              const KKScatter *sc) {
+              const KKScatter *sc, int W_small) {
     if (n_frames <= 0 || nx <= 0 || nz <= 0) return KKB_OK;
     if (W < 2) W = 2;
-    const char *force = getenv("KKB_KK_DIRECT");  // test hook: the per-pixel fallback
-    // tables of very many pairs (N*M in the thousands) outgrow shared memory too
-    const bool too_big = kk_smem_bytes(N, M, std::max(W, 2), 1, linear) > 227 * 1024;
-    if (W > KKB_KK_STAGE_ELEMS || too_big || (force && force[0] == '1')) {
-        // steep geometry: the tile's trace window would not fit the staging buffer
-        KKArgs a{data, data_fs, N, M, T, ltx, ltzT, lrx, lrzT, w, fs, shift, nx, nz, W, 0,
-                 out, out_kind, out_fs, inten, fmax, accum, 0, 0, {}};
-        if (sc) {
-            a.ndst = sc->ndst;
-            a.dst_off = sc->dst_off;
-            for (int d = 0; d < sc->ndst; ++d) a.dst[d] = sc->dst[d];
-        }
+    KKArgs a{data, data_fs, N, M, T, ltx, ltzT, lrx, lrzT, w, fs, shift, nx, nz, W, 0,
+             out, out_kind, out_fs, inten, fmax, accum, 0, 0, {}};
+    if (sc) {
+        a.ndst = sc->ndst;
+        a.dst_off = sc->dst_off;
+        for (int d = 0; d < sc->ndst; ++d) a.dst[d] = sc->dst[d];
+    }
+    // instance: big tiles; small tiles when the big grid cannot fill the SMs
+    // (or the big tile's window overflows its stage); else the per-pixel kernel
+    constexpr int EPT = KKB_KK_STAGE_ELEMS / (32 * KKB_KK_WZ * KKB_KK_WX);
+    constexpr int STAGE_S = EPT * 32 * KKB_KK_S_WZ * KKB_KK_S_WX;
+    const long long tiles_big = ceil_div(nz, KKB_KK_TZ) * ceil_div(nx, KKB_KK_TX);
+    const bool small_ok = W_small >= 2 && W_small <= STAGE_S &&
+                          kk_smem_bytes(N, M, W_small, 1, linear, KKB_KK_S_TZ, KKB_KK_S_TX) <= 200 * 1024;
+    const bool big_ok = W <= KKB_KK_STAGE_ELEMS && kk_smem_bytes(N, M, W, 1, linear) <= 227 * 1024;
+    const char *force = getenv("KKB_KK_DIRECT");  // test hooks: per-pixel / small-tile kernels
+    const char *fsmall = getenv("KKB_KK_SMALL");
+    bool use_small = small_ok && (!big_ok || tiles_big * n_frames < 2LL * sm_count() ||
+                                  (fsmall && fsmall[0] == '1'));
+    if ((force && force[0] == '1') || (!big_ok && !use_small)) {
+        // steep geometry or huge pair tables: per-pixel kernel
         dim3 grid((unsigned)ceil_div((long long)nx * nz, 256), (unsigned)n_frames);
         if (linear)
             k_kk_direct<true><<<grid, 256, 0, s>>>(a);
@@ -634,32 +665,17 @@ int kk_gather(const float2 *data, int N, int M, int T, const double *ltx, const 
         KKB_CHECK_LAUNCH("k_kk_direct");
         return KKB_OK;
     }
+    const int Wc = use_small ? W_small : W;
+    const int stage = use_small ? STAGE_S : KKB_KK_STAGE_ELEMS;
+    const int tz = use_small ? KKB_KK_S_TZ : KKB_KK_TZ, tx = use_small ? KKB_KK_S_TX : KKB_KK_TX;
     // receive angles per stage: bounded by the register staging and shared memory
-    int MCH = std::max(1, std::min(M, KKB_KK_STAGE_ELEMS / W));
-    while (MCH > 1 && kk_smem_bytes(N, M, W, MCH, linear) > 200 * 1024) MCH = (MCH + 1) / 2;
-    size_t sm = kk_smem_bytes(N, M, W, MCH, linear);
-    KKArgs a{data, data_fs, N, M, T, ltx, ltzT, lrx, lrzT, w, fs, shift, nx, nz, W, MCH,
-             out, out_kind, out_fs, inten, fmax, accum, 0, 0, {}};
-    if (sc) {
-        a.ndst = sc->ndst;
-        a.dst_off = sc->dst_off;
-        for (int d = 0; d < sc->ndst; ++d) a.dst[d] = sc->dst[d];
-    }
-    dim3 grid((unsigned)ceil_div(nz, KKB_KK_TZ), (unsigned)ceil_div(nx, KKB_KK_TX), (unsigned)n_frames);
-    dim3 block(KKB_KK_WZ * KKB_KK_WX * 32);
-    if (linear) {
-        auto fn = k_kk_gather<KKB_KK_WZ, KKB_KK_WX, KKB_KK_CX, true>;
-        KKB_TRY_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm),
-                     "smem attr kk");
-        fn<<<grid, block, sm, s>>>(a);
-    } else {
-        auto fn = k_kk_gather<KKB_KK_WZ, KKB_KK_WX, KKB_KK_CX, false>;
-        KKB_TRY_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm),
-                     "smem attr kk");
-        fn<<<grid, block, sm, s>>>(a);
-    }
-    KKB_CHECK_LAUNCH("k_kk_gather");
-    return KKB_OK;
+    int MCH = std::max(1, std::min(M, stage / Wc));
+    while (MCH > 1 && kk_smem_bytes(N, M, Wc, MCH, linear, tz, tx) > 200 * 1024) MCH = (MCH + 1) / 2;
+    const size_t sm = kk_smem_bytes(N, M, Wc, MCH, linear, tz, tx);
+    a.W = Wc;
+    a.MCH = MCH;
+    if (use_small) return launch_tiled<KKB_KK_S_WZ, KKB_KK_S_WX, KKB_KK_S_CX>(a, n_frames, sm, linear != 0, s);
+    return launch_tiled<KKB_KK_WZ, KKB_KK_WX, KKB_KK_CX>(a, n_frames, sm, linear != 0, s);
 }
 
 // ------------------------------------------------------------- K6 epilogues

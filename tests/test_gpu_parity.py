@@ -469,3 +469,21 @@ def test_analytic_signal_rejects_too_long_traces():
     vol = kb.RFVolume(np.zeros((1, 2, T), np.float32), arr, kb.AcquisitionParams(C, [0.0], T))
     with pytest.raises(kb.KKBeamError):
         kb.analytic_signal(vol)
+
+
+def test_small_and_big_tile_instances_are_bit_identical(monkeypatch):
+    # a single small frame runs the 16 x 16 tile instance, a batch the 32 x 64
+    # one; the per-pixel sums run in the same order, so the images agree bit for bit
+    import torch
+
+    w = configs.config4(frames=4)
+    p, arr = w.params, w.array
+    rf = np.stack([configs.noise_rf(p.num_transmits, arr.num_elements, p.num_samples, seed=s)
+                   for s in range(4)])
+    eng = kb.KKEngine(arr, p, w.receive, w.grid, frames=4, want_db=False)
+    big = eng.run(torch.from_numpy(rf).cuda()).clone()
+    monkeypatch.setenv("KKB_KK_SMALL", "1")
+    small = eng.run(torch.from_numpy(rf).cuda()).clone()
+    torch.cuda.synchronize()
+    assert torch.equal(big, small)
+    eng.close()
