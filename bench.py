@@ -123,6 +123,19 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------- CPU arms
+def cpu_model() -> str:
+    """Host CPU model name (/proc/cpuinfo), for the CPU-baseline record."""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+
+    return platform.processor() or "unknown"
+
+
 def cpu_pipeline_rate(w, seconds: float = 12.0, min_frames: int = 2, threads: int = 0):
     """Oracle port of the reference path on the host: frames/s over a bounded
     sample (>= min_frames, ~`seconds` of work)."""
@@ -175,7 +188,7 @@ def run_reference(args):
         "data": "synthetic (seeded noise RF, reference bench.noise_volume)",
         "config": {"workload": w.name, "frames_per_step": 2, "pixel_pairs_per_frame": pp},
         "pixel_pair_samples_per_s": value * pp,
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "cpu": cpu_model(),
                          "sample": "2 frames per step of the workload: numpy/scipy complex64 "
                                    "stage 1 (bench.py:113-138 form) + C/OpenMP kk loop (all cores)"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -390,7 +403,7 @@ def run_gpu(args):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         r, n, dt = cpu_pipeline_rate(w, seconds=args.cpu_seconds)
-        cpu = {"value": r, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
+        cpu = {"value": r, "unit": UNIT, "cores": os.cpu_count(), "kind": "port", "cpu": cpu_model(),
                "sample": f"{n} frames of {w.name} in {dt:.1f} s: numpy/scipy complex64 stage 1 "
                          "(reference bench.py:113-138 form) + C/OpenMP kk loop on all cores"}
 
