@@ -11,15 +11,6 @@
 #ifndef KKB_KK_WX
 #define KKB_KK_WX 2   // warps along x
 #endif
-// running per-pixel total over transmits (the per-transmit partials are float32)
-#ifndef KKB_KK_F64_TOTAL
-#define KKB_KK_F64_TOTAL 0   // measured: float32 totals 4.5% faster, IQ still ~2e-7 rel L2
-#endif
-#if KKB_KK_F64_TOTAL
-typedef double kk_total_t;
-#else
-typedef float kk_total_t;
-#endif
 #ifndef KKB_KK_CX
 #define KKB_KK_CX 4   // pixel columns per lane (measured r1: 4 beats 2 by 14%, 8 spills)
 #endif
@@ -38,6 +29,9 @@ typedef float kk_total_t;
 #endif
 #ifndef KKB_KK_MIN_CTAS
 #define KKB_KK_MIN_CTAS 2        // occupancy target (caps registers at 128)
+#endif
+#ifndef KKB_KK_FR
+#define KKB_KK_FR 2              // frames per CTA of the batched (big-tile) gather
 #endif
 #ifndef KKB_KK_QUNROLL
 #define KKB_KK_QUNROLL 1         // receive-loop unroll of the gather

@@ -20,7 +20,9 @@
 //     the in-window predicate is folded into the staged window (entries of
 //     out-of-trace samples are zero), the lerp weight is (low >> 9) | 1.0f.
 //     Taps and the per-pixel sum are float32, accumulated in fixed order
-//     (deterministic, no atomics; KKB_KK_F64_TOTAL=1 keeps float64 totals).
+//     (deterministic, no atomics).  A batch runs KKB_KK_FR frames per CTA: the
+//     tables and every tap's index math are shared, only the window reads
+//     and the accumulators are per frame.
 //   * Geometries whose window or pair tables do not fit shared memory run the
 //     per-pixel kernel k_kk_direct (same index math, lerp and epilogue).
 // Output complex64 or complex128, plus optional fused |IQ|^2 (optionally
@@ -259,6 +261,7 @@ struct KKArgs {
     int ndst;
     long long dst_off;
     void *dst[KKB_MAX_DST];
+    int n_frames;  // frames in the batch (the multi-frame instance skips the tail)
 };
 
 // packed LUT index: tile row r -> (r/8)*4 + r%4 pair slot, a = (r/4)&1
@@ -270,7 +273,7 @@ __device__ __forceinline__ int pcol(int c) {
     return (c / (8 * CX)) * (8 * CX) + (c & 7) * CX + ((c >> 3) % CX);
 }
 
-template <int WZ, int WX, int CX, bool LINEAR>
+template <int WZ, int WX, int CX, bool LINEAR, int FR>
 __global__ void __launch_bounds__(WZ *WX * 32, KKB_KK_MIN_CTAS)
 k_kk_gather(const KKArgs a) {
     constexpr int TZ = 8 * WZ;
@@ -284,8 +287,8 @@ k_kk_gather(const KKArgs a) {
     const int nstage = N * nchunk;
 
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    Entry *win = reinterpret_cast<Entry *>(smem_raw);                  // [2][MCH][W]
-    double *lrz_p = reinterpret_cast<double *>(win + 2 * MCH * W);     // [M][TZ] packed rows
+    Entry *win = reinterpret_cast<Entry *>(smem_raw);                  // [2][FR][MCH][W]
+    double *lrz_p = reinterpret_cast<double *>(win + 2 * FR * MCH * W);  // [M][TZ] packed rows
     double *lrx_p = lrz_p + M * TZ;                                    // [M][TX] packed cols
     double *ltz_p = lrx_p + M * TX;                                    // [N][TZ]
     double *ltx_p = ltz_p + N * TZ;                                    // [N][TX]
@@ -293,7 +296,9 @@ k_kk_gather(const KKArgs a) {
     int2 *lw_s = reinterpret_cast<int2 *>(ltx_p + N * TX);             // [N][M]
 
     const int tid = threadIdx.x;
-    const int f = blockIdx.z;
+    // FR frames per CTA share the tables and every tap's index math; the
+    // taps of frame fr come from its own window block
+    const int f0 = blockIdx.z * FR;
     const int ix0 = blockIdx.y * TX, iz0 = blockIdx.x * TZ;
     const int lane = tid & 31, warp = tid >> 5;
     const int wz = warp % WZ, wx = warp / WZ;
@@ -339,27 +344,28 @@ k_kk_gather(const KKArgs a) {
     }
     __syncthreads();
 
-    const float2 *dframe = a.data + (long long)f * a.data_fs;
     // register-staged window entries of one stage; entry tid + i*NT of a stage
-    // is (receive q, sample e) = divmod(tid + i*NT, W), the same every stage
+    // is (frame fr, receive q, sample e) of the [FR][MCH][W] window block,
+    // the same every stage
     float2 s0[EPT], s1[EPT];
     int qe[EPT];
 #pragma unroll
     for (int i = 0; i < EPT; ++i) {
-        const int idx = tid + i * NT, q = idx / W;
-        qe[i] = (q << 16) | (idx - q * W);
+        const int idx = tid + i * NT, fr = idx / (MCH * W), rem = idx - fr * MCH * W, q = rem / W;
+        qe[i] = (fr << 26) | (q << 16) | (rem - q * W);
     }
-    // stage (n, m0): receive angles m0 .. m0+mc-1 of transmit n
+    // stage (n, m0): receive angles m0 .. m0+mc-1 of transmit n, all FR frames
     auto load_stage = [&](int n, int m0) {
-        const int cnt = min(MCH, M - m0) * W;
-        const float2 *base = dframe + (long long)(n * M + m0) * T;
+        const int mc = min(MCH, M - m0);
         const int2 *lo_q = lw_s + n * M + m0;
 #pragma unroll
         for (int i = 0; i < EPT; ++i) {
-            const int idx = tid + i * NT;
             s0[i] = s1[i] = make_float2(0.f, 0.f);
-            if (idx < cnt) {
-                const int q = qe[i] >> 16, e = qe[i] & 0xFFFF;
+            const int fr = qe[i] >> 26, q = (qe[i] >> 16) & 1023, e = qe[i] & 0xFFFF;
+            if (tid + i * NT < FR * MCH * W && q < mc) {
+                // frames past the batch re-read the first frame (results discarded)
+                const int fe = f0 + fr < a.n_frames ? f0 + fr : f0;
+                const float2 *base = a.data + (long long)fe * a.data_fs + (long long)(n * M + m0) * T;
                 const int smp = lo_q[q].x + e;
                 const float2 *tr = base + q * T;
                 // entry smp stays zero unless a tap at smp is in the reference's
@@ -372,12 +378,12 @@ k_kk_gather(const KKArgs a) {
         }
     };
     auto store_stage = [&](int m0, int buf) {
-        const int cnt = min(MCH, M - m0) * W;
-        Entry *wb = win + buf * MCH * W;
+        const int mc = min(MCH, M - m0);
+        Entry *wb = win + buf * FR * MCH * W;
 #pragma unroll
         for (int i = 0; i < EPT; ++i) {
             const int idx = tid + i * NT;
-            if (idx < cnt) {
+            if (idx < FR * MCH * W && ((qe[i] >> 16) & 1023) < mc) {
                 if constexpr (LINEAR) {
                     // (2 d0 - d1, d1 - d0): the lerp becomes e0 + (1 + frac) * diff
                     wb[idx] = make_float4(fmaf(2.f, s0[i].x, -s1[i].x), fmaf(2.f, s0[i].y, -s1[i].y),
@@ -389,16 +395,14 @@ k_kk_gather(const KKArgs a) {
         }
     };
 
-    kk_total_t accd_r[2][CX], accd_i[2][CX];
-    float accr[2][CX], acci[2][CX];
+    float accr[FR][2][CX], acci[FR][2][CX];  // float32 per-pixel sums, fixed order
     double t1[2][CX];
 #pragma unroll
-    for (int p = 0; p < 2; ++p)
+    for (int fr = 0; fr < FR; ++fr)
 #pragma unroll
-        for (int q = 0; q < CX; ++q) {
-            accd_r[p][q] = accd_i[p][q] = 0.0;
-            accr[p][q] = acci[p][q] = 0.f;
-        }
+        for (int p = 0; p < 2; ++p)
+#pragma unroll
+            for (int q = 0; q < CX; ++q) accr[fr][p][q] = acci[fr][p][q] = 0.f;
 
     load_stage(0, 0);
     store_stage(0, 0);
@@ -431,7 +435,7 @@ k_kk_gather(const KKArgs a) {
                 t1[1][j] = __dadd_rn(txv[j], tz.y);
             }
         }
-        const Entry *wb = win + buf * MCH * W;
+        const Entry *wb = win + buf * FR * MCH * W;
         const int2 *lw_n = lw_s + n * M + m0;
         constexpr int kQUnroll = KKB_KK_QUNROLL;
 #pragma unroll kQUnroll
@@ -451,7 +455,6 @@ k_kk_gather(const KKArgs a) {
             // in-window predicate of tap_index() is folded into the staged window
             // (entries whose tap would be invalid are zero), so no per-tap test
             const int loC = lw.x + KKB_MAGIC2_HI;
-            const Entry *wv = wb + q * W;
 #pragma unroll
             for (int p = 0; p < 2; ++p) {
 #pragma unroll
@@ -460,31 +463,23 @@ k_kk_gather(const KKArgs a) {
                     const double sv = __dadd_rd(LINEAR ? fi : __dadd_rn(fi, 0.5), KKB_FLOOR_MAGIC2);
                     const unsigned e = min((unsigned)(__double2hiint(sv) - loC),
                                            (unsigned)(LINEAR ? W - 2 : W - 1));
-                    if constexpr (LINEAR) {
-                        const float4 v = wv[e];
-                        const float f1 = __uint_as_float(((unsigned)__double2loint(sv) >> 9) + 0x3F800000u);
-                        accr[p][r] = fmaf(wm, fmaf(f1, v.z, v.x), accr[p][r]);
-                        acci[p][r] = fmaf(wm, fmaf(f1, v.w, v.y), acci[p][r]);
-                    } else {
-                        const float2 v = wv[e];
-                        accr[p][r] = fmaf(wm, v.x, accr[p][r]);
-                        acci[p][r] = fmaf(wm, v.y, acci[p][r]);
+                    const float f1 = __uint_as_float(((unsigned)__double2loint(sv) >> 9) + 0x3F800000u);
+#pragma unroll
+                    for (int fr = 0; fr < FR; ++fr) {
+                        const Entry *wv = wb + (fr * MCH + q) * W;
+                        if constexpr (LINEAR) {
+                            const float4 v = wv[e];
+                            accr[fr][p][r] = fmaf(wm, fmaf(f1, v.z, v.x), accr[fr][p][r]);
+                            acci[fr][p][r] = fmaf(wm, fmaf(f1, v.w, v.y), acci[fr][p][r]);
+                        } else {
+                            const float2 v = wv[e];
+                            accr[fr][p][r] = fmaf(wm, v.x, accr[fr][p][r]);
+                            acci[fr][p][r] = fmaf(wm, v.y, acci[fr][p][r]);
+                        }
                     }
                 }
             }
         }
-#if KKB_KK_F64_TOTAL
-        if (ch == nchunk - 1) {
-#pragma unroll
-            for (int p = 0; p < 2; ++p)
-#pragma unroll
-                for (int r = 0; r < CX; ++r) {
-                    accd_r[p][r] += (kk_total_t)accr[p][r];
-                    accd_i[p][r] += (kk_total_t)acci[p][r];
-                    accr[p][r] = acci[p][r] = 0.f;
-                }
-        }
-#endif
         // buffer buf^1 was last read in stage s-1, which every thread finished
         // before the barrier that ended it
         if (s + 1 < nstage) store_stage(ch1 * MCH, buf ^ 1);
@@ -493,45 +488,46 @@ k_kk_gather(const KKArgs a) {
         ch = ch1;
     }
 
-    // epilogue: IQ (+ fused intensity and frame max)
-    float fmx = 0.f;
+    // epilogue: IQ (+ fused intensity and frame max), per frame
 #pragma unroll
-    for (int p = 0; p < 2; ++p) {
-        const int iz = iz0 + wz * 8 + p * 4 + zt;
+    for (int fr = 0; fr < FR; ++fr) {
+        const int f = f0 + fr;
+        if (f >= a.n_frames) break;
+        float fmx = 0.f;
 #pragma unroll
-        for (int r = 0; r < CX; ++r) {
-            const int ix = ix0 + wx * 8 * CX + r * 8 + xt;
-            if (iz < nz && ix < nx) {
-#if KKB_KK_F64_TOTAL
-                const kk_total_t vr = accd_r[p][r], vi = accd_i[p][r];
-#else
-                const float vr = accr[p][r], vi = acci[p][r];  // float32 totals: one accumulator
-#endif
-                const long long px = (long long)f * a.out_fs + (long long)ix * nz + iz;
-                if (a.out) {
-                    if (a.out_kind == KKB_OUT_C128)
-                        reinterpret_cast<double2 *>(a.out)[px] = make_double2(vr, vi);
-                    else
-                        reinterpret_cast<float2 *>(a.out)[px] = make_float2((float)vr, (float)vi);
-                }
-                for (int d = 0; d < a.ndst; ++d) {
-                    if (a.out_kind == KKB_OUT_C128)
-                        reinterpret_cast<double2 *>(a.dst[d])[a.dst_off + px] = make_double2(vr, vi);
-                    else
-                        reinterpret_cast<float2 *>(a.dst[d])[a.dst_off + px] = make_float2((float)vr, (float)vi);
-                }
-                if (a.inten) {
-                    float I = (float)(vr * vr + vi * vi);
-                    if (a.accum) I += a.inten[px];  // sets compounded in call order
-                    a.inten[px] = I;
-                    fmx = fmaxf(fmx, I);
+        for (int p = 0; p < 2; ++p) {
+            const int iz = iz0 + wz * 8 + p * 4 + zt;
+#pragma unroll
+            for (int r = 0; r < CX; ++r) {
+                const int ix = ix0 + wx * 8 * CX + r * 8 + xt;
+                if (iz < nz && ix < nx) {
+                    const float vr = accr[fr][p][r], vi = acci[fr][p][r];
+                    const long long px = (long long)f * a.out_fs + (long long)ix * nz + iz;
+                    if (a.out) {
+                        if (a.out_kind == KKB_OUT_C128)
+                            reinterpret_cast<double2 *>(a.out)[px] = make_double2(vr, vi);
+                        else
+                            reinterpret_cast<float2 *>(a.out)[px] = make_float2(vr, vi);
+                    }
+                    for (int d = 0; d < a.ndst; ++d) {
+                        if (a.out_kind == KKB_OUT_C128)
+                            reinterpret_cast<double2 *>(a.dst[d])[a.dst_off + px] = make_double2(vr, vi);
+                        else
+                            reinterpret_cast<float2 *>(a.dst[d])[a.dst_off + px] = make_float2(vr, vi);
+                    }
+                    if (a.inten) {
+                        float I = vr * vr + vi * vi;
+                        if (a.accum) I += a.inten[px];  // sets compounded in call order
+                        a.inten[px] = I;
+                        fmx = fmaxf(fmx, I);
+                    }
                 }
             }
         }
-    }
-    if (a.fmax) {
-        for (int o = 16; o > 0; o >>= 1) fmx = fmaxf(fmx, __shfl_xor_sync(0xffffffffu, fmx, o));
-        if (lane == 0) atomicMax(a.fmax + f, __float_as_uint(fmx));
+        if (a.fmax) {
+            for (int o = 16; o > 0; o >>= 1) fmx = fmaxf(fmx, __shfl_xor_sync(0xffffffffu, fmx, o));
+            if (lane == 0) atomicMax(a.fmax + f, __float_as_uint(fmx));
+        }
     }
 }
 
@@ -603,24 +599,25 @@ k_kk_direct(const KKArgs a) {
 }
 
 static size_t kk_smem_bytes(int N, int M, int W, int MCH, bool linear, int tz = KKB_KK_TZ,
-                            int tx = KKB_KK_TX) {
+                            int tx = KKB_KK_TX, int fr = 1) {
     size_t entry = linear ? sizeof(float4) : sizeof(float2);
-    return entry * 2 * MCH * W + sizeof(double) * ((size_t)(M + N) * tz + (size_t)(M + N) * tx) +
+    return entry * 2 * fr * MCH * W + sizeof(double) * ((size_t)(M + N) * tz + (size_t)(M + N) * tx) +
            sizeof(int2) * (size_t)N * M;
 }
 
-template <int WZ, int WX, int CX>
+template <int WZ, int WX, int CX, int FR>
 static int launch_tiled(const KKArgs &a, int n_frames, size_t sm, bool linear, cudaStream_t s) {
     constexpr int TZ = 8 * WZ, TX = 8 * CX * WX;
-    dim3 grid((unsigned)ceil_div(a.nz, TZ), (unsigned)ceil_div(a.nx, TX), (unsigned)n_frames);
+    dim3 grid((unsigned)ceil_div(a.nz, TZ), (unsigned)ceil_div(a.nx, TX),
+              (unsigned)ceil_div(n_frames, FR));
     dim3 block(WZ * WX * 32);
     if (linear) {
-        auto fn = k_kk_gather<WZ, WX, CX, true>;
+        auto fn = k_kk_gather<WZ, WX, CX, true, FR>;
         KKB_TRY_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm),
                      "smem attr kk");
         fn<<<grid, block, sm, s>>>(a);
     } else {
-        auto fn = k_kk_gather<WZ, WX, CX, false>;
+        auto fn = k_kk_gather<WZ, WX, CX, false, FR>;
         KKB_TRY_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm),
                      "smem attr kk");
         fn<<<grid, block, sm, s>>>(a);
@@ -637,7 +634,7 @@ int kk_gather(const float2 *data, int N, int M, int T, const double *ltx, const 
     if (n_frames <= 0 || nx <= 0 || nz <= 0) return KKB_OK;
     if (W < 2) W = 2;
     KKArgs a{data, data_fs, N, M, T, ltx, ltzT, lrx, lrzT, w, fs, shift, nx, nz, W, 0,
-             out, out_kind, out_fs, inten, fmax, accum, 0, 0, {}};
+             out, out_kind, out_fs, inten, fmax, accum, 0, 0, {}, n_frames};
     if (sc) {
         a.ndst = sc->ndst;
         a.dst_off = sc->dst_off;
@@ -668,14 +665,22 @@ int kk_gather(const float2 *data, int N, int M, int T, const double *ltx, const 
     const int Wc = use_small ? W_small : W;
     const int stage = use_small ? STAGE_S : KKB_KK_STAGE_ELEMS;
     const int tz = use_small ? KKB_KK_S_TZ : KKB_KK_TZ, tx = use_small ? KKB_KK_S_TX : KKB_KK_TX;
+    // big tiles over a batch: KKB_KK_FR frames per CTA share the tables and the
+    // index math of every tap (when a window block of FR frames fits a stage)
+    const char *ffr = getenv("KKB_KK_FR1");  // test hook: one frame per CTA
+    const int FR = (!use_small && n_frames > 1 && KKB_KK_FR > 1 && KKB_KK_FR * Wc <= stage &&
+                    !(ffr && ffr[0] == '1')) ? KKB_KK_FR : 1;
     // receive angles per stage: bounded by the register staging and shared memory
-    int MCH = std::max(1, std::min(M, stage / Wc));
-    while (MCH > 1 && kk_smem_bytes(N, M, Wc, MCH, linear, tz, tx) > 200 * 1024) MCH = (MCH + 1) / 2;
-    const size_t sm = kk_smem_bytes(N, M, Wc, MCH, linear, tz, tx);
+    int MCH = std::max(1, std::min(M, stage / (FR * Wc)));
+    while (MCH > 1 && kk_smem_bytes(N, M, Wc, MCH, linear, tz, tx, FR) > 200 * 1024) MCH = (MCH + 1) / 2;
+    const size_t sm = kk_smem_bytes(N, M, Wc, MCH, linear, tz, tx, FR);
     a.W = Wc;
     a.MCH = MCH;
-    if (use_small) return launch_tiled<KKB_KK_S_WZ, KKB_KK_S_WX, KKB_KK_S_CX>(a, n_frames, sm, linear != 0, s);
-    return launch_tiled<KKB_KK_WZ, KKB_KK_WX, KKB_KK_CX>(a, n_frames, sm, linear != 0, s);
+    if (use_small)
+        return launch_tiled<KKB_KK_S_WZ, KKB_KK_S_WX, KKB_KK_S_CX, 1>(a, n_frames, sm, linear != 0, s);
+    if (FR > 1)
+        return launch_tiled<KKB_KK_WZ, KKB_KK_WX, KKB_KK_CX, KKB_KK_FR>(a, n_frames, sm, linear != 0, s);
+    return launch_tiled<KKB_KK_WZ, KKB_KK_WX, KKB_KK_CX, 1>(a, n_frames, sm, linear != 0, s);
 }
 
 // ------------------------------------------------------------- K6 epilogues
