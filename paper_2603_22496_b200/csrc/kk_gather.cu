@@ -358,14 +358,18 @@ k_kk_gather(const KKArgs a) {
     auto load_stage = [&](int n, int m0) {
         const int mc = min(MCH, M - m0);
         const int2 *lo_q = lw_s + n * M + m0;
+        const float2 *base0 = a.data + (long long)f0 * a.data_fs + (long long)(n * M + m0) * T;
 #pragma unroll
         for (int i = 0; i < EPT; ++i) {
             s0[i] = s1[i] = make_float2(0.f, 0.f);
             const int fr = qe[i] >> 26, q = (qe[i] >> 16) & 1023, e = qe[i] & 0xFFFF;
             if (tid + i * NT < FR * MCH * W && q < mc) {
-                // frames past the batch re-read the first frame (results discarded)
-                const int fe = f0 + fr < a.n_frames ? f0 + fr : f0;
-                const float2 *base = a.data + (long long)fe * a.data_fs + (long long)(n * M + m0) * T;
+                const float2 *base = base0;
+                if constexpr (FR > 1) {
+                    // frames past the batch re-read the first frame (results discarded)
+                    const int fe = f0 + fr < a.n_frames ? f0 + fr : f0;
+                    base = a.data + (long long)fe * a.data_fs + (long long)(n * M + m0) * T;
+                }
                 const int smp = lo_q[q].x + e;
                 const float2 *tr = base + q * T;
                 // entry smp stays zero unless a tap at smp is in the reference's
