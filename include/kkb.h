@@ -175,9 +175,9 @@ int kkb_decomposer_create(int n_tx, int n_el, int n_t, const double *positions_h
 int kkb_decomposer_run(kkb_decomposer *p, const float *rf, int n_frames, void *traces,
                        void *stream);
 /* int16-quantised RF ingest: rf is
- * (F, N, L, T) int16; each sample is converted exactly to float32 inside the
- * FFT load, identical to running the float32 path on rf.astype(float32).
- * Needs T in {1024, 1536, 2048, 4096}. */
+ * (F, N, L, T) int16; each sample is converted exactly to float32 (inside the
+ * FFT load for T in {1024, 1536, 2048, 4096}, by a widening pass otherwise),
+ * identical to running the float32 path on rf.astype(float32). */
 int kkb_decomposer_run_i16(kkb_decomposer *p, const short *rf, int n_frames, void *traces,
                            void *stream);
 /* Pipelined mode: process chunk_frames per pass, rotating passes over `slots`

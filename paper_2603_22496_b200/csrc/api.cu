@@ -555,15 +555,21 @@ extern "C" int kkb_decomposer_symmetric_classes(const kkb_decomposer *p) { retur
 
 extern "C" long long kkb_decomposer_workspace_bytes(const kkb_decomposer *p) { return p ? p->bytes : 0; }
 
+// exact int16 -> float32 widening (the reference consumes q.astype(float32))
+__global__ void k_i16_to_f32(const short *__restrict__ in, long long n, float *__restrict__ out) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x)
+        out[i] = (float)in[i];
+}
+
 static int decomposer_run(kkb_decomposer *p, const void *rf, int in_kind, int n_frames,
                           void *traces, void *stream) {
     if (!p || n_frames < 0) return KKB_ERR_ARG;
     cudaStream_t s = as_stream(stream);
     const int N = p->N, L = p->L, T = p->T, M = p->M, K = p->K, ldk = p->ldk;
-    if (in_kind && !fft_ct_supported(T)) {
-        set_error("int16 RF ingest needs T in {1024, 1536, 2048, 4096} (got %d)", T);
-        return KKB_ERR_UNSUPPORTED;
-    }
+    // int16 RF: converted exactly inside the compile-time real FFT's load; other
+    // lengths convert each chunk to float32 first (k_i16_to_f32)
+    const bool i16_direct = in_kind && fft_ct_supported(T);
     const size_t esz = in_kind ? sizeof(short) : sizeof(float);
     FftPlan plan;
     int st = get_fft_plan(T, &plan);
@@ -583,7 +589,16 @@ static int decomposer_run(kkb_decomposer *p, const void *rf, int in_kind, int n_
         int F = std::min(p->chunk, n_frames - f0);
         const char *rf_c = (const char *)rf + (size_t)f0 * N * L * T * esz;
         float2 *tr_c = (float2 *)traces + (size_t)f0 * N * M * T;
-        if (in_kind) {
+        float *conv = nullptr;
+        if (in_kind && !i16_direct) {
+            const long long n = (long long)F * N * L * T;
+            KKB_TRY_CUDA(cudaMallocAsync(&conv, sizeof(float) * (size_t)n, cs), "cudaMallocAsync(i16 convert)");
+            k_i16_to_f32<<<(unsigned)std::min<long long>(ceil_div(n, 256), 148 * 32), 256, 0, cs>>>(
+                (const short *)rf_c, n, conv);
+            KKB_CHECK_LAUNCH("k_i16_to_f32");
+            rf_c = (const char *)conv;
+        }
+        if (i16_direct) {
             st = fft_r2c_ct(rf_c, 1, (long long)F * N * L, T, X, ldk, K, nullptr, plan.tws, cs);
         } else if (plan.direct || plan.large) {
             // lengths without a single-CTA real plan: promote to complex first
@@ -596,6 +611,7 @@ static int decomposer_run(kkb_decomposer *p, const void *rf, int in_kind, int n_
             st = fft_r2c((const float *)rf_c, (long long)F * N * L, T, X, ldk, K, nullptr, cs,
                          nullptr);
         }
+        if (conv) cudaFreeAsync(conv, cs);
         if (st) return st;
         if (p->P > 0)
             st = contract_sym(X, ldk, p->cs, ldk, Y, ldk, (long long)F * N, L, M, K, p->P,

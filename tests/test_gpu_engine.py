@@ -155,6 +155,23 @@ def test_engine_weights_and_nearest(oracle, config1_rf):
     eng.close()
 
 
+def test_engine_int16_ingest_other_lengths():
+    # lengths without a compile-time FFT plan widen int16 to float32 first
+    torch = _torch()
+    arr = kb.TransducerArray(32, 0.3e-3, 5.2e6, 20.8e6, 0.6)
+    rx = kb.uniform_vernier_angles(3, 3, 0.1, 0)
+    grid = kb.ImageGrid(-1e-3, 3e-3, 0.1e-3, 0.1e-3, 16, 16)
+    for T in (777, 1021, 3000):
+        p = kb.AcquisitionParams(C, kb.transmit_angles(3, 0.1), T)
+        q = np.random.default_rng(T).integers(-30000, 30000, (2, 3, 32, T)).astype(np.int16)
+        eng = kb.KKEngine(arr, p, rx, grid, frames=2, want_db=False)
+        a = eng.run(torch.from_numpy(q.astype(np.float32)).cuda()).clone()
+        b = eng.run(torch.from_numpy(q).cuda()).clone()
+        torch.cuda.synchronize()
+        assert torch.equal(a, b), T
+        eng.close()
+
+
 @pytest.mark.parametrize("cfg", [1, 2, 4, 5])
 def test_engine_int16_ingest_is_exact(cfg):
     """int16-quantised RF (BASELINE config 2) through the int16 ingest path is
