@@ -118,6 +118,14 @@ int kkb_kk_plan_run_scatter(kkb_kk_plan *p, const void *data, int n_frames,
                             long long data_frame_stride, void *const *dst_host, int n_dst,
                             long long dst_offset, int out_kind, long long out_frame_stride,
                             void *stream);
+/* kkb_kk_plan_run_ex on a receive subset of a larger trace array: transmit n's
+ * traces start at data + n*data_tx_stride (complex elements; 0 = M*T), so a
+ * plan over M receive angles can read M consecutive rows of (N, M_total, T)
+ * traces decomposed once for several receive sets (multi-set compounding). */
+int kkb_kk_plan_run_strided(kkb_kk_plan *p, const void *data, int n_frames,
+                            long long data_frame_stride, long long data_tx_stride, void *out,
+                            int out_kind, long long out_frame_stride, float *intensity,
+                            unsigned int *frame_max, int flags, void *stream);
 /* trace window (samples per pair) the plan stages in shared memory */
 int kkb_kk_plan_window(const kkb_kk_plan *p);
 int kkb_kk_plan_destroy(kkb_kk_plan *p);

@@ -35,6 +35,7 @@ SIGNATURES = {
     "kkb_kk_plan_create": [P, P, P, P, I, I, I, I, I, P, D, D, I, P, P],
     "kkb_kk_plan_run": [P, P, I, LL, P, I, LL, P, P, P],
     "kkb_kk_plan_run_ex": [P, P, I, LL, P, I, LL, P, P, I, P],
+    "kkb_kk_plan_run_strided": [P, P, I, LL, LL, P, I, LL, P, P, I, P],
     "kkb_kk_plan_run_scatter": [P, P, I, LL, P, I, LL, I, LL, P],
     "kkb_kk_plan_window": [P],
     "kkb_kk_plan_destroy": [P],

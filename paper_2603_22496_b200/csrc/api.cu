@@ -206,11 +206,16 @@ extern "C" int kkb_kk_plan_create(const double *ltx, const double *ltz, const do
 
 extern "C" int kkb_kk_plan_window(const kkb_kk_plan *p) { return p ? p->W : -1; }
 
-extern "C" int kkb_kk_plan_run_ex(kkb_kk_plan *p, const void *data, int n_frames,
-                                  long long data_frame_stride, void *out, int out_kind,
-                                  long long out_frame_stride, float *intensity,
-                                  unsigned int *frame_max, int flags, void *stream) {
-    if (!p || (flags & ~KKB_RUN_ACCUMULATE_INTENSITY)) return KKB_ERR_ARG;
+extern "C" int kkb_kk_plan_run_strided(kkb_kk_plan *p, const void *data, int n_frames,
+                                       long long data_frame_stride, long long data_tx_stride,
+                                       void *out, int out_kind, long long out_frame_stride,
+                                       float *intensity, unsigned int *frame_max, int flags,
+                                       void *stream) {
+    if (!p || (flags & ~KKB_RUN_ACCUMULATE_INTENSITY) ||
+        (data_tx_stride != 0 && data_tx_stride < (long long)p->M * p->T)) {
+        set_error("kk_plan_run: bad flags or transmit stride");
+        return KKB_ERR_ARG;
+    }
     int st = check_kk_args(p->N, p->M, p->T, p->nx, p->nz, out_kind);
     if (st) return st;
     if (frame_max)
@@ -220,7 +225,15 @@ extern "C" int kkb_kk_plan_run_ex(kkb_kk_plan *p, const void *data, int n_frames
                      p->lrx, p->lrzT, p->nx, p->nz, p->w, p->fs, p->shift, p->linear, out,
                      out_kind, n_frames, data_frame_stride, out_frame_stride, intensity, frame_max,
                      p->W, as_stream(stream), (flags & KKB_RUN_ACCUMULATE_INTENSITY) ? 1 : 0,
-                     nullptr, p->W_small);
+                     nullptr, p->W_small, data_tx_stride);
+}
+
+extern "C" int kkb_kk_plan_run_ex(kkb_kk_plan *p, const void *data, int n_frames,
+                                  long long data_frame_stride, void *out, int out_kind,
+                                  long long out_frame_stride, float *intensity,
+                                  unsigned int *frame_max, int flags, void *stream) {
+    return kkb_kk_plan_run_strided(p, data, n_frames, data_frame_stride, 0, out, out_kind,
+                                   out_frame_stride, intensity, frame_max, flags, stream);
 }
 
 extern "C" int kkb_kk_plan_run_scatter(kkb_kk_plan *p, const void *data, int n_frames,

@@ -66,7 +66,8 @@ int kk_gather(const float2 *data, int N, int M, int T, const double *ltx, const 
               const double *lrx, const double *lrzT, int nx, int nz, const double *w, double fs,
               double shift, int linear, void *out, int out_kind, int n_frames, long long data_fs,
               long long out_fs, float *inten, unsigned *fmax, int W, cudaStream_t s,
-              int accum = 0, const KKScatter *sc = nullptr, int W_small = 0);
+              int accum = 0, const KKScatter *sc = nullptr, int W_small = 0,
+              long long data_ns = 0);  // 0: M*T (dense (N, M, T) traces)
 
 int kk_taps(const double *ltx, const double *ltz, const double *lrx, const double *lrz, int N, int M,
             int T, int nx, int nz, double fs, double shift, int linear, int *idx, cudaStream_t s);

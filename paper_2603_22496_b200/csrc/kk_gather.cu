@@ -239,6 +239,7 @@ int kk_window(const double *ltx, const double *ltz, const double *lrx, const dou
 struct KKArgs {
     const float2 *data;
     long long data_fs;  // frame stride, complex elements
+    long long data_ns;  // transmit stride (M*T, or wider for a receive subset of a larger trace set)
     int N, M, T;
     const double *ltx;   // (X, N)
     const double *ltzT;  // (N, Z)
@@ -358,7 +359,7 @@ k_kk_gather(const KKArgs a) {
     auto load_stage = [&](int n, int m0) {
         const int mc = min(MCH, M - m0);
         const int2 *lo_q = lw_s + n * M + m0;
-        const float2 *base0 = a.data + (long long)f0 * a.data_fs + (long long)(n * M + m0) * T;
+        const float2 *base0 = a.data + (long long)f0 * a.data_fs + n * a.data_ns + (long long)m0 * T;
 #pragma unroll
         for (int i = 0; i < EPT; ++i) {
             s0[i] = s1[i] = make_float2(0.f, 0.f);
@@ -368,7 +369,7 @@ k_kk_gather(const KKArgs a) {
                 if constexpr (FR > 1) {
                     // frames past the batch re-read the first frame (results discarded)
                     const int fe = f0 + fr < a.n_frames ? f0 + fr : f0;
-                    base = a.data + (long long)fe * a.data_fs + (long long)(n * M + m0) * T;
+                    base = a.data + (long long)fe * a.data_fs + n * a.data_ns + (long long)m0 * T;
                 }
                 const int smp = lo_q[q].x + e;
                 const float2 *tr = base + q * T;
@@ -560,7 +561,7 @@ k_kk_direct(const KKArgs a) {
                 double sv;
                 if (!tap_index<LINEAR>(fi, a.T, F, sv)) continue;
                 const float wm = a.w ? (float)a.w[m] : 1.0f;
-                const float2 *tr = dframe + (long long)(n * a.M + m) * a.T;
+                const float2 *tr = dframe + n * a.data_ns + (long long)m * a.T;
                 const float2 d0 = __ldg(tr + F);
                 if (LINEAR) {
                     const float2 d1 = __ldg(tr + F + 1);
@@ -634,10 +635,11 @@ int kk_gather(const float2 *data, int N, int M, int T, const double *ltx, const 
               const double *lrx, const double *lrzT, int nx, int nz, const double *w, double fs,
               double shift, int linear, void *out, int out_kind, int n_frames, long long data_fs,
               long long out_fs, float *inten, unsigned *fmax, int W, cudaStream_t s, int accum,
-              const KKScatter *sc, int W_small) {
+              const KKScatter *sc, int W_small, long long data_ns) {
     if (n_frames <= 0 || nx <= 0 || nz <= 0) return KKB_OK;
     if (W < 2) W = 2;
-    KKArgs a{data, data_fs, N, M, T, ltx, ltzT, lrx, lrzT, w, fs, shift, nx, nz, W, 0,
+    KKArgs a{data, data_fs, data_ns > 0 ? data_ns : (long long)M * T, N, M, T, ltx, ltzT, lrx,
+             lrzT, w, fs, shift, nx, nz, W, 0,
              out, out_kind, out_fs, inten, fmax, accum, 0, 0, {}, n_frames};
     if (sc) {
         a.ndst = sc->ndst;

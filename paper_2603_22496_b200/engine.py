@@ -257,16 +257,22 @@ class MultiSetEngine:
     (the reference's hybrid / multi-j acquisitions: cli.py:93-107, 250-266;
     compound_coherent / compound_incoherent, beamform.py:396-411).
 
-    mode "incoherent": one decomposition + gather per set; every gather adds
-      its |IQ_j|^2 to one shared intensity buffer (KKB_RUN_ACCUMULATE_INTENSITY),
-      so sum_j |B_j|^2 and its per-frame max come out of the last launch.
-    mode "coherent": |sum_j B_j|^2 is the kk image over the concatenated angle
-      list (kk sums over every receive angle), so it is ONE engine on the union.
+    The RF is decomposed ONCE over the concatenated angle list (the sets laid
+    out one after another along the receive axis), so the element FFTs are
+    shared by all sets.
+    mode "incoherent": one gather per set over its rows of the shared traces
+      (``kkb_kk_plan_run_strided``); each adds its |IQ_j|^2 to one intensity
+      buffer (KKB_RUN_ACCUMULATE_INTENSITY), so sum_j |B_j|^2 and its per-frame
+      max come out of the last launch; per-set IQ in ``iq[j]``.
+    mode "coherent": |sum_j B_j|^2 is the kk image over the whole list (kk sums
+      over every receive angle): one gather over all rows.
     """
 
     def __init__(self, array: TransducerArray, params: AcquisitionParams, receive_sets,
                  grid: ImageGrid, frames: int, mode: str = "incoherent", want_db: bool = True,
                  floor_db: float = -60.0, **kw):
+        import ctypes
+
         from .sampling import explicit_angles
 
         sets = [rs[1] if isinstance(rs, tuple) else rs for rs in receive_sets]
@@ -275,40 +281,67 @@ class MultiSetEngine:
         if mode not in ("incoherent", "coherent"):
             raise ConfigError(f"unknown compounding mode {mode!r}")
         self.mode, self.want_db, self.floor_db = mode, want_db, float(floor_db)
+        union = explicit_angles(np.concatenate([s.angles for s in sets]), sets[0].delta_theta_i)
+        # the union engine: shared decomposition; in coherent mode also the gather
+        self.engine = KKEngine(array, params, union, grid, frames,
+                               want_db=want_db and mode == "coherent", floor_db=floor_db, **kw)
+        self.engines = [self.engine]
+        e = self.engine
         if mode == "coherent":
-            union = explicit_angles(np.concatenate([s.angles for s in sets]), sets[0].delta_theta_i)
-            self.engines = [KKEngine(array, params, union, grid, frames, want_db=want_db,
-                                     floor_db=floor_db, **kw)]
-            e = self.engines[0]
             self.inten, self.fmax, self.db = e.inten, e.fmax, e.db
             return
-        self.engines = [KKEngine(array, params, rs, grid, frames, want_db=False, **kw) for rs in sets]
-        e = self.engines[0]
+        t = e.t
         self.inten, self.fmax = e.inten, e.fmax
-        self.db = e.t.empty_like(e.inten) if want_db else None
+        self.db = t.empty_like(e.inten) if want_db else None
+        self.sets = sets
+        self._plans, self._luts, self.iq = [], [], []
+        self._m_off = np.concatenate([[0], np.cumsum([s.num_angles for s in sets])[:-1]]).astype(int)
+        w_all = kw.get("channel_weights")
+        for j, rs in enumerate(sets):
+            luts = build_kk_luts_device(grid, params.transmit_angles, rs.angles, e.c)
+            w = None
+            if w_all is not None:
+                w = dev.to_device(np.asarray(w_all, dtype=np.float64)[
+                    self._m_off[j]:self._m_off[j] + rs.num_angles])
+            kp = ctypes.c_void_p()
+            _lib.call("kkb_kk_plan_create", dev.ptr(luts["lut_tx_x"]), dev.ptr(luts["lut_tx_z"]),
+                      dev.ptr(luts["lut_rx_x"]), dev.ptr(luts["lut_rx_z"]), e.N, rs.num_angles,
+                      e.T, grid.nx, grid.nz, dev.ptr(w), float(e.fs), float(e.shift),
+                      int(e.linear), dev.stream_handle(), ctypes.byref(kp))
+            self._plans.append(kp)
+            self._luts.append((luts, w))
+            self.iq.append(t.empty((e.F, grid.nx, grid.nz), dtype=t.complex64, device="cuda"))
 
     @property
     def pixel_pairs_per_frame(self) -> int:
-        return sum(e.pixel_pairs_per_frame for e in self.engines)
+        return self.engine.pixel_pairs_per_frame
 
     def run(self, rf, stream=None):
         """Compounded intensity (F, X, Z) float32 for a (F, N, L, T) RF batch;
-        per-set IQ stays in engines[j].iq.  Asynchronous."""
+        asynchronous."""
+        e = self.engine
         if self.mode == "coherent":
-            self.engines[0].run(rf, stream=stream, groups=1)
+            e.run(rf, stream=stream, groups=1)
             return self.inten
-        last = len(self.engines) - 1
-        for j, e in enumerate(self.engines):
-            e.decompose(rf, stream=stream)
-            e.beamform(stream=stream, inten=self.inten, fmax=self.fmax if j == last else False,
-                       accumulate=j > 0, want_db=False)
+        e.decompose(rf, stream=stream)
+        s = dev.stream_handle(stream)
+        P = e.grid.nx * e.grid.nz
+        Mu = e.M
+        last = len(self.sets) - 1
+        for j, (rs, kp) in enumerate(zip(self.sets, self._plans)):
+            base = dev.ptr(e.traces) + int(self._m_off[j]) * e.T * 8  # complex64 rows m_off..
+            _lib.call("kkb_kk_plan_run_strided", kp, base, e.F, e.N * Mu * e.T, Mu * e.T,
+                      dev.ptr(self.iq[j]), _lib.KKB_OUT_C64, P, dev.ptr(self.inten),
+                      dev.ptr(self.fmax) if j == last else None,
+                      _lib.KKB_RUN_ACCUMULATE_INTENSITY if j > 0 else 0, s)
         if self.want_db:
-            e = self.engines[0]
-            P = e.grid.nx * e.grid.nz
             _lib.call("kkb_log_compress", dev.ptr(self.inten), dev.ptr(self.fmax), e.F, P,
-                      self.floor_db, dev.ptr(self.db), dev.stream_handle(stream))
+                      self.floor_db, dev.ptr(self.db), s)
         return self.inten
 
     def close(self):
-        for e in self.engines:
-            e.close()
+        lib = _lib.load()
+        for kp in getattr(self, "_plans", []):
+            lib.kkb_kk_plan_destroy(kp)
+        self._plans = []
+        self.engine.close()

@@ -225,4 +225,7 @@ def test_multiset_compounding_matches_oracle(oracle, config1_rf, mode):
     assert np.isclose(float(got[0].max()), float(eng.fmax[0].cpu().numpy().view(np.float32)), rtol=0)
     db = eng.db[0].cpu().numpy()
     assert np.abs(db - oracle.log_compress_db(ref, floor_db=-60.0)).max() <= 1e-3
+    if mode == "incoherent":  # per-set images from rows of the shared decomposition
+        for j, img in enumerate(imgs):
+            assert rel_l2(eng.iq[j][1].cpu().numpy(), img) <= 1e-5, j
     eng.close()
