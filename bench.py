@@ -471,7 +471,8 @@ def run_gpu(args):
 
 def run_gpu_rowblock(args):
     """Config 5: one large frame per step, image row-blocks sharded over ranks,
-    stage 1 replicated; the gather kernel stores its rows into every rank's
+    stage 1 replicated (or, --stage1 sharded, split by transmit with the
+    trace all-gather fused into the inverse FFT's P2P stores); the gather kernel stores its rows into every rank's
     image over NVLink (P2P, CUDA IPC), NCCL all-gather as the fallback
     (strong scaling)."""
     import torch
@@ -489,7 +490,10 @@ def run_gpu_rowblock(args):
     arr, p, rx, g = w.array, w.params, w.receive, w.grid
     rf = torch.from_numpy(configs.noise_rf(p.num_transmits, arr.num_elements, p.num_samples,
                                            seed=5)).cuda()
-    rb = shard.RowBlockKK(arr, p, rx, g, rank, world)
+    rb = shard.RowBlockKK(arr, p, rx, g, rank, world, stage1=args.stage1)
+    if args.stage1 == "sharded":  # each rank holds only its transmits' RF
+        n0, n1 = shard.balanced_range(p.num_transmits, rank, world)
+        rf = rf[n0:n1].contiguous()
     stream = torch.cuda.current_stream()
 
     def step():
@@ -529,7 +533,10 @@ def run_gpu_rowblock(args):
             "dtype": "f32 (complex64 traces/IQ; float64 delay-index math)",
             "data": "synthetic (seeded noise RF, shapes of BASELINE config 5)",
             "config": {"workload": w.name, "frames_per_step": 1, "pixel_pairs_per_frame": pp,
-                       "parallelism": f"row-block x{world}, stage 1 replicated, "
+                       "parallelism": f"row-block x{world}, stage 1 {args.stage1}"
+                                      + (" (trace all-gather fused into the inverse FFT)"
+                                         if args.stage1 == "sharded" and rb.transport == "p2p" else "")
+                                      + ", "
                                       + ("P2P stores from the gather epilogue (CUDA IPC over NVLink)"
                                          if rb.transport == "p2p" else "NCCL all-gather")},
             "pixel_pair_samples_per_s": pp * 1e3 / ms_step, "gpu_launches": int(launches),
@@ -554,6 +561,9 @@ def main():
     ap.add_argument("--groups", type=int, default=1,
                     help="frame groups: decomposition of group g+1 overlaps the gather of group g")
     ap.add_argument("--e2e-chunk", type=int, default=16)
+    ap.add_argument("--stage1", default="replicated", choices=["replicated", "sharded"],
+                    help="config 5: decompose the whole frame on every rank, or only the "
+                         "rank's transmits with a fused trace all-gather")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)

@@ -193,6 +193,20 @@ int kkb_decomposer_run_i16(kkb_decomposer *p, const short *rf, int n_frames, voi
  * stream), so one pass's FFT overlaps the previous pass's contraction and the
  * spectra are consumed while L2-resident.  Reallocates scratch (synchronous). */
 int kkb_decomposer_set_pipeline(kkb_decomposer *p, int chunk_frames, int slots);
+/* Transmit-sharded stage 1 with a fused trace all-gather (SURVEY §8(e),
+ * config 5 alternative): a plan created for this rank's n_tx transmits
+ * decomposes rf ((F, n_tx, L, T), float32, or int16 if rf_is_i16) and the
+ * inverse FFT's epilogue stores trace (f, n, m) into each of the ndst (<= 8)
+ * buffers dsts_host[d] (device pointers: this rank's full (F, N, M, T) trace
+ * buffer and the peers' buffers mapped with CUDA IPC over NVLink) at complex64
+ * element dst_offset + f*frame_stride + (n*M + m)*T — dst_offset = n0*M*T for
+ * a rank holding transmits [n0, n0 + n_tx), frame_stride = N*M*T.  Per-row
+ * arithmetic is independent of the transmit split, so the assembled traces
+ * equal a single plan's bit for bit.  The caller orders completion (stream
+ * sync + a barrier) before any rank reads its traces. */
+int kkb_decomposer_run_scatter(kkb_decomposer *p, const void *rf, int rf_is_i16, int n_frames,
+                               void *const *dsts_host, int ndst, long long dst_offset,
+                               long long frame_stride, void *stream);
 /* Number of +/- receive-angle classes of the symmetric contraction the plan
  * uses (0: general contraction).  The reference guarantees the symmetry
  * (ReceiveAngleSet, sampling.py:55-57; centred positions, core.py:32-38). */

@@ -46,6 +46,7 @@ SIGNATURES = {
     "kkb_decomposer_create": [I, I, I, P, P, I, D, D, I, P],
     "kkb_decomposer_run": [P, P, I, P, P],
     "kkb_decomposer_run_i16": [P, P, I, P, P],
+    "kkb_decomposer_run_scatter": [P, P, I, I, P, I, LL, LL, P],
     "kkb_decomposer_set_pipeline": [P, I, I],
     "kkb_decomposer_symmetric_classes": [P],
     "kkb_decomposer_workspace_bytes": [P],

@@ -576,7 +576,7 @@ __global__ void k_i16_to_f32(const short *__restrict__ in, long long n, float *_
 }
 
 static int decomposer_run(kkb_decomposer *p, const void *rf, int in_kind, int n_frames,
-                          void *traces, void *stream) {
+                          void *traces, void *stream, const RowScatter *scatter = nullptr) {
     if (!p || n_frames < 0) return KKB_ERR_ARG;
     cudaStream_t s = as_stream(stream);
     const int N = p->N, L = p->L, T = p->T, M = p->M, K = p->K, ldk = p->ldk;
@@ -632,7 +632,15 @@ static int decomposer_run(kkb_decomposer *p, const void *rf, int in_kind, int n_
         else
             st = contract(X, ldk, p->ramps, ldk, Y, ldk, (long long)F * N, L, M, K, cs);
         if (st) return st;
-        if ((st = fft_c2c(Y, ldk, K, tr_c, T, T, (long long)F * N * M, T, true, 1.0f, cs))) return st;
+        if (scatter) {  // fused all-gather: rows land in every rank's full trace buffer
+            RowScatter sc = *scatter;
+            sc.off += (long long)f0 * sc.frame_stride;
+            sc.rows_per_frame = N * M;
+            st = fft_c2c_scatter(Y, ldk, K, T, (long long)F * N * M, T, true, 1.0f, sc, cs);
+        } else {
+            st = fft_c2c(Y, ldk, K, tr_c, T, T, (long long)F * N * M, T, true, 1.0f, cs);
+        }
+        if (st) return st;
     }
     if (piped) {  // join
         for (int i = 0; i < p->slots; ++i) {
@@ -686,6 +694,30 @@ extern "C" int kkb_decomposer_run(kkb_decomposer *p, const float *rf, int n_fram
 extern "C" int kkb_decomposer_run_i16(kkb_decomposer *p, const short *rf, int n_frames,
                                       void *traces, void *stream) {
     return decomposer_run(p, rf, 1, n_frames, traces, stream);
+}
+
+extern "C" int kkb_decomposer_run_scatter(kkb_decomposer *p, const void *rf, int rf_is_i16,
+                                          int n_frames, void *const *dsts, int ndst,
+                                          long long dst_offset, long long frame_stride,
+                                          void *stream) {
+    if (!p || !dsts || ndst < 1 || ndst > KKB_ROW_SCATTER_MAX || n_frames < 0 || dst_offset < 0 ||
+        frame_stride < (long long)p->N * p->M * p->T) {
+        set_error("decomposer_run_scatter: 1 <= ndst <= %d, frame_stride >= n_tx*M*T",
+                  KKB_ROW_SCATTER_MAX);
+        return KKB_ERR_ARG;
+    }
+    RowScatter sc;
+    sc.ndst = ndst;
+    sc.frame_stride = frame_stride;
+    sc.off = dst_offset;
+    for (int d = 0; d < ndst; ++d) {
+        if (!dsts[d]) {
+            set_error("decomposer_run_scatter: null destination %d", d);
+            return KKB_ERR_ARG;
+        }
+        sc.dst[d] = (float2 *)dsts[d];
+    }
+    return decomposer_run(p, rf, rf_is_i16 ? 1 : 0, n_frames, nullptr, stream, &sc);
 }
 
 extern "C" int kkb_decomposer_destroy(kkb_decomposer *p) {

@@ -559,6 +559,35 @@ int fft_c2c(const float2 *in, long long in_stride, int in_len, float2 *out, long
     return KKB_OK;
 }
 
+int fft_c2c_scatter(const float2 *in, long long in_stride, int in_len, int out_len,
+                    long long ntraces, int T, bool inverse, float scale, const RowScatter &sc,
+                    cudaStream_t s) {
+    if (ntraces <= 0) return KKB_OK;
+    if (sc.ndst < 1 || sc.ndst > KKB_ROW_SCATTER_MAX || sc.rows_per_frame < 1) return KKB_ERR_ARG;
+    if (fft_ct_supported(T) && g_use_ct && ntraces <= 0x7fffffffLL) {
+        FftPlan p;
+        int st = get_fft_plan(T, &p);
+        if (st) return st;
+        return fft_c2c_ct(in, in_stride, in_len, nullptr, out_len, out_len, ntraces, T, inverse,
+                          scale, p.tws, s, &sc);
+    }
+    // other lengths: transform into scratch, then one strided copy per destination
+    float2 *tmp = nullptr;
+    KKB_TRY_CUDA(cudaMallocAsync(&tmp, sizeof(float2) * (size_t)ntraces * out_len, s),
+                 "cudaMallocAsync(scatter scratch)");
+    int st = fft_c2c(in, in_stride, in_len, tmp, out_len, out_len, ntraces, T, inverse, scale, s);
+    const long long frames = ntraces / sc.rows_per_frame;
+    const size_t row_bytes = sizeof(float2) * (size_t)sc.rows_per_frame * out_len;
+    for (int d = 0; d < sc.ndst && !st; ++d) {
+        cudaError_t e = cudaMemcpy2DAsync(sc.dst[d] + sc.off, sizeof(float2) * (size_t)sc.frame_stride,
+                                          tmp, row_bytes, row_bytes, (size_t)frames,
+                                          cudaMemcpyDeviceToDevice, s);
+        if (e != cudaSuccess) st = cuda_status(e, "scatter copy");
+    }
+    cudaFreeAsync(tmp, s);
+    return st;
+}
+
 int fft_r2c(const float *in, long long ntraces, int T, float2 *out, long long out_stride, int K,
             const float *bin_scale, cudaStream_t s, float2 *scratch_c2c) {
     if (ntraces <= 0) return KKB_OK;

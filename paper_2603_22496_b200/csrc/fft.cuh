@@ -14,6 +14,18 @@
 
 namespace kkb {
 
+// Row-wise multi-destination store of a batched transform (fused trace
+// all-gather): row r goes to dst[d] + off + (r / rows_per_frame) * frame_stride
+// + (r % rows_per_frame) * out_stride for every d < ndst (complex64 elements).
+#define KKB_ROW_SCATTER_MAX 8
+struct RowScatter {
+    int ndst = 0;
+    int rows_per_frame = 1;
+    long long frame_stride = 0;
+    long long off = 0;
+    float2 *dst[KKB_ROW_SCATTER_MAX] = {};
+};
+
 struct FftPlan {
     int T;
     int nstages;
@@ -45,6 +57,12 @@ int fft_r2c_ct(const void *in, int in_kind, long long ntraces, int T, float2 *ou
                cudaStream_t s);
 int fft_c2c_ct(const float2 *in, long long in_stride, int in_len, float2 *out, long long out_stride,
                int out_len, long long ntraces, int T, bool inverse, float scale, const float2 *tw,
-               cudaStream_t s);
+               cudaStream_t s, const RowScatter *sc = nullptr);
+// fft_c2c whose rows are stored through `sc` (out_stride = row pitch inside a
+// frame): fused into the compile-time kernels' epilogue, otherwise one
+// transform into scratch followed by a strided copy per destination.
+int fft_c2c_scatter(const float2 *in, long long in_stride, int in_len, int out_len,
+                    long long ntraces, int T, bool inverse, float scale, const RowScatter &sc,
+                    cudaStream_t s);
 
 }  // namespace kkb

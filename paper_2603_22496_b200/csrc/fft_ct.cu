@@ -323,11 +323,16 @@ k_r2c(const InT *__restrict__ in, long long ntraces, float2 *__restrict__ out,
 }
 
 // Complex FFT of rows: input bins [0, in_len) (rest zero), output the first
-// out_len points times `scale`; INV selects exp(+) via conjugation.
-template <int T, bool INV>
+// out_len points times `scale`; INV selects exp(+) via conjugation.  SC: the
+// epilogue stores every row into each of sc.ndst buffers (peers' trace
+// buffers mapped over NVLink) at sc.off + (row / rpf) * frame_stride +
+// (row % rpf) * out_stride instead of `out` -- the fused trace all-gather of
+// transmit-sharded stage 1.
+template <int T, bool INV, bool SC = false>
 __global__ void __launch_bounds__(Plan<T>::NT)
 k_c2c(const float2 *__restrict__ in, long long in_stride, int in_len, float2 *__restrict__ out,
-      long long out_stride, int out_len, float scale, const float2 *__restrict__ tw) {
+      long long out_stride, int out_len, float scale, const float2 *__restrict__ tw,
+      RowScatter sc = RowScatter{}) {
     using P = Plan<T>;
     __shared__ __align__(16) float2 buf[T];
     const long long row = blockIdx.x;
@@ -354,15 +359,33 @@ k_c2c(const float2 *__restrict__ in, long long in_stride, int in_len, float2 *__
     using S2 = Stage<T, P::NT, P::R2>;
     S2 c;
     stages12<T>(buf, tw, c);
-    float2 *dst = out + row * out_stride;
     const float sy = sg * scale;
+    if constexpr (SC) {
+        const long long o = sc.off + (row / sc.rows_per_frame) * sc.frame_stride +
+                            (row % sc.rows_per_frame) * out_stride;
+#pragma unroll 1
+        for (int d = 0; d < sc.ndst; ++d) {
+            float2 *dst = sc.dst[d] + o;
 #pragma unroll
-    for (int t = 0; t < S2::ITER; ++t) {
-        const int j = S2::lane_j(t);
+            for (int t = 0; t < S2::ITER; ++t) {
+                const int j = S2::lane_j(t);
 #pragma unroll
-        for (int r = 0; r < P::R2; ++r) {
-            const int k = j + r * S2::TR;
-            if (S2::ok(j) && k < out_len) dst[k] = make_float2(c.v[t][r].x * scale, c.v[t][r].y * sy);
+                for (int r = 0; r < P::R2; ++r) {
+                    const int k = j + r * S2::TR;
+                    if (S2::ok(j) && k < out_len) dst[k] = make_float2(c.v[t][r].x * scale, c.v[t][r].y * sy);
+                }
+            }
+        }
+    } else {
+        float2 *dst = out + row * out_stride;
+#pragma unroll
+        for (int t = 0; t < S2::ITER; ++t) {
+            const int j = S2::lane_j(t);
+#pragma unroll
+            for (int r = 0; r < P::R2; ++r) {
+                const int k = j + r * S2::TR;
+                if (S2::ok(j) && k < out_len) dst[k] = make_float2(c.v[t][r].x * scale, c.v[t][r].y * sy);
+            }
         }
     }
 }
@@ -418,8 +441,15 @@ static int launch_r2c(const void *in, int in_kind, long long ntraces, float2 *ou
 template <int T>
 static int launch_c2c(const float2 *in, long long in_stride, int in_len, float2 *out,
                       long long out_stride, int out_len, long long ntraces, bool inverse,
-                      float scale, const float2 *tw, cudaStream_t s) {
-    if (inverse)
+                      float scale, const float2 *tw, cudaStream_t s, const RowScatter *sc) {
+    if (sc) {
+        if (inverse)
+            ct::k_c2c<T, true, true><<<(unsigned)ntraces, ct::Plan<T>::NT, 0, s>>>(
+                in, in_stride, in_len, out, out_stride, out_len, scale, tw, *sc);
+        else
+            ct::k_c2c<T, false, true><<<(unsigned)ntraces, ct::Plan<T>::NT, 0, s>>>(
+                in, in_stride, in_len, out, out_stride, out_len, scale, tw, *sc);
+    } else if (inverse)
         ct::k_c2c<T, true><<<(unsigned)ntraces, ct::Plan<T>::NT, 0, s>>>(
             in, in_stride, in_len, out, out_stride, out_len, scale, tw);
     else
@@ -445,14 +475,14 @@ int fft_r2c_ct(const void *in, int in_kind, long long ntraces, int T, float2 *ou
 
 int fft_c2c_ct(const float2 *in, long long in_stride, int in_len, float2 *out, long long out_stride,
                int out_len, long long ntraces, int T, bool inverse, float scale, const float2 *tw,
-               cudaStream_t s) {
+               cudaStream_t s, const RowScatter *sc) {
     if (ntraces <= 0) return KKB_OK;
     if (ntraces > 0x7fffffffLL) return KKB_ERR_UNSUPPORTED;
     switch (T) {
-        case 1024: return launch_c2c<1024>(in, in_stride, in_len, out, out_stride, out_len, ntraces, inverse, scale, tw, s);
-        case 1536: return launch_c2c<1536>(in, in_stride, in_len, out, out_stride, out_len, ntraces, inverse, scale, tw, s);
-        case 2048: return launch_c2c<2048>(in, in_stride, in_len, out, out_stride, out_len, ntraces, inverse, scale, tw, s);
-        case 4096: return launch_c2c<4096>(in, in_stride, in_len, out, out_stride, out_len, ntraces, inverse, scale, tw, s);
+        case 1024: return launch_c2c<1024>(in, in_stride, in_len, out, out_stride, out_len, ntraces, inverse, scale, tw, s, sc);
+        case 1536: return launch_c2c<1536>(in, in_stride, in_len, out, out_stride, out_len, ntraces, inverse, scale, tw, s, sc);
+        case 2048: return launch_c2c<2048>(in, in_stride, in_len, out, out_stride, out_len, ntraces, inverse, scale, tw, s, sc);
+        case 4096: return launch_c2c<4096>(in, in_stride, in_len, out, out_stride, out_len, ntraces, inverse, scale, tw, s, sc);
     }
     return KKB_ERR_UNSUPPORTED;
 }

@@ -115,8 +115,20 @@ class KKEngine:
         name = "kkb_decomposer_run_i16" if rf.dtype == self.t.int16 else "kkb_decomposer_run"
         _lib.call(name, handle, dev.ptr(rf), n_frames, dev.ptr(traces), stream_handle)
 
+    def _check_rf(self, rf, n_frames: int):
+        t = self.t
+        if not (0 <= n_frames <= self.F):
+            raise ConfigError(f"n_frames must be in [0, {self.F}]")
+        if (rf.dtype not in (t.float32, t.int16) or rf.dim() != 4 or rf.shape[0] < n_frames
+                or tuple(rf.shape[1:]) != (self.N, self.L, self.T)):
+            raise ConfigError(f"expected float32 or int16 RF of shape (>= {n_frames}, {self.N}, "
+                              f"{self.L}, {self.T}), got {rf.dtype} {tuple(rf.shape)}")
+        if not rf.is_cuda or not rf.is_contiguous():
+            raise ConfigError("RF must be a contiguous CUDA tensor")
+
     def decompose(self, rf, n_frames: int | None = None, stream=None):
         F = self.F if n_frames is None else n_frames
+        self._check_rf(rf, F)
         self._run_decomposer(self._dec, rf, F, self.traces, dev.stream_handle(stream))
         return self.traces[:F]
 
@@ -163,11 +175,9 @@ class KKEngine:
         """Whole hot path for a (F, N, L, T) float32 CUDA tensor; asynchronous.
         Returns the complex64 IQ images (F, X, Z) (``self.inten`` / ``self.db``
         hold the detected and log-compressed images)."""
-        t = self.t
-        if rf.dtype not in (t.float32, t.int16) or tuple(rf.shape) != (self.F, self.N, self.L, self.T):
+        if tuple(rf.shape[:1]) != (self.F,):
             raise ConfigError(f"expected float32 or int16 RF of shape {(self.F, self.N, self.L, self.T)}")
-        if not rf.is_contiguous():
-            raise ConfigError("RF must be contiguous")
+        self._check_rf(rf, self.F)
         groups = self.groups if groups is None else int(groups)
         if groups <= 1 or self.F < 2:
             self.decompose(rf, stream=stream)
@@ -213,9 +223,18 @@ class KKEngine:
         streams so that H2D, kernels and D2H overlap."""
         t = self.t
         F = self.F
+        if rf_host.is_cuda or tuple(rf_host.shape) != (F, self.N, self.L, self.T) or \
+                rf_host.dtype not in (t.float32, t.int16):
+            raise ConfigError(f"expected host float32 or int16 RF of shape {(F, self.N, self.L, self.T)}")
+        if iq_host.is_cuda or tuple(iq_host.shape) != (F, self.grid.nx, self.grid.nz) or \
+                iq_host.dtype != t.complex64:
+            raise ConfigError(f"expected a host complex64 IQ buffer of shape {(F, self.grid.nx, self.grid.nz)}")
         C = max(1, min(chunk_frames, self.chunk, F))
         if streams is None:
             streams = [t.cuda.Stream(), t.cuda.Stream()]
+        cur = t.cuda.current_stream()
+        for s in streams:  # earlier work on the caller's stream may still use the buffers
+            s.wait_stream(cur)
         while len(self._stream_decs) < len(streams):
             self._stream_decs.append(self._new_decomposer(C))
         if staging is None:
@@ -323,6 +342,8 @@ class MultiSetEngine:
         if self.mode == "coherent":
             e.run(rf, stream=stream, groups=1)
             return self.inten
+        if tuple(rf.shape[:1]) != (e.F,):
+            raise ConfigError(f"expected RF of shape {(e.F, e.N, e.L, e.T)}")
         e.decompose(rf, stream=stream)
         s = dev.stream_handle(stream)
         P = e.grid.nx * e.grid.nz
@@ -345,3 +366,9 @@ class MultiSetEngine:
             lib.kkb_kk_plan_destroy(kp)
         self._plans = []
         self.engine.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -95,6 +95,31 @@ def test_engine_run_host_equals_device_path():
     eng.close()
 
 
+def test_engine_rejects_malformed_inputs():
+    """Wrong dtype / shape / device / layout raise ConfigError before any launch."""
+    torch = _torch()
+    from paper_2603_22496_b200.errors import ConfigError
+
+    w = configs.config1()
+    p, arr = w.params, w.array
+    eng = _engine(w, 2)
+    shape = (2, p.num_transmits, arr.num_elements, p.num_samples)
+    good = torch.zeros(shape, dtype=torch.float32, device="cuda")
+    for bad in (good.double(), good[:, :, :-1], good.cpu(), good.transpose(2, 3).contiguous().transpose(2, 3),
+                good[:1]):
+        with pytest.raises(ConfigError):
+            eng.run(bad)
+    with pytest.raises(ConfigError):
+        eng.decompose(good, n_frames=3)
+    with pytest.raises(ConfigError):
+        eng.run_host(good, torch.empty((2, w.grid.nx, w.grid.nz), dtype=torch.complex64))
+    with pytest.raises(ConfigError):
+        eng.run_host(good.cpu(), torch.empty((2, w.grid.nx, w.grid.nz), dtype=torch.complex128))
+    eng.run(good)
+    torch.cuda.synchronize()
+    eng.close()
+
+
 @pytest.mark.parametrize("scheme", ["dense_vernier", "shifted_vernier", "confocal", "hybrid"])
 def test_engine_config3_schemes(oracle, scheme):
     torch = _torch()

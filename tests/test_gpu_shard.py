@@ -84,3 +84,95 @@ def test_p2p_transport_single_rank_is_the_full_image():
     assert torch.equal(rb.gather(), full)
     rb.close()
     full_eng.close()
+
+
+def _full_traces(w, rf, frames):
+    eng = kb.KKEngine(w.array, w.params, w.receive, w.grid, frames=frames, want_db=False)
+    tr = eng.decompose(rf).clone()
+    eng.close()
+    return tr
+
+
+@pytest.mark.parametrize("cfg,T,frames,world", [(4, None, 2, 3), (5, None, 1, 8), (1, 1000, 2, 3)])
+def test_transmit_sharded_stage1_scatter_assembles_every_trace_buffer(cfg, T, frames, world):
+    # transmit-sharded stage 1 on one GPU: `world` "ranks" each decompose their
+    # transmit block and the inverse FFT's epilogue stores the rows into all
+    # ranks' full trace buffers (fused for the compile-time lengths, strided
+    # copies after the transform for T = 1000); every buffer must equal the
+    # single-plan decomposition bit for bit
+    import ctypes
+
+    import torch
+
+    from paper_2603_22496_b200 import _device as dev
+    from paper_2603_22496_b200 import _lib
+
+    w = configs.CONFIGS[cfg]()
+    p, arr = w.params, w.array
+    if T is not None:
+        p = kb.AcquisitionParams(p.sound_speed, p.transmit_angles, T, start_time=p.start_time)
+        w = configs.Workload(w.name, arr, p, w.receive, w.grid)
+    N, M, L, TT = p.num_transmits, w.receive.num_angles, arr.num_elements, p.num_samples
+    rf = torch.from_numpy(np.stack([configs.noise_rf(N, L, TT, seed=30 + f)
+                                    for f in range(frames)])).cuda()
+    full = _full_traces(w, rf, frames)
+    bufs = [torch.full((frames, N, M, TT), complex(5, 5), dtype=torch.complex64, device="cuda")
+            for _ in range(world)]
+    dsts = (ctypes.c_void_p * world)(*[b.data_ptr() for b in bufs])
+    pos = np.ascontiguousarray(arr.positions, dtype=np.float64)
+    ang = np.ascontiguousarray(w.receive.angles, dtype=np.float64)
+    for r in range(world):
+        n0, n1 = shard.balanced_range(N, r, world)
+        h = ctypes.c_void_p()
+        _lib.call("kkb_decomposer_create", n1 - n0, L, TT, pos.ctypes.data, ang.ctypes.data, M,
+                  float(arr.sampling_frequency), float(p.sound_speed), frames, ctypes.byref(h))
+        sub = rf[:, n0:n1].contiguous()
+        _lib.call("kkb_decomposer_run_scatter", h, dev.ptr(sub), 0, frames, dsts, world,
+                  n0 * M * TT, N * M * TT, dev.stream_handle())
+        torch.cuda.synchronize()
+        _lib.load().kkb_decomposer_destroy(h)
+    for b in bufs:
+        assert torch.equal(b, full)
+
+
+def test_decomposer_scatter_rejects_bad_arguments():
+    import ctypes
+
+    from paper_2603_22496_b200 import _lib
+    from paper_2603_22496_b200.errors import ConfigError
+
+    w = configs.config1()
+    p, arr = w.params, w.array
+    pos = np.ascontiguousarray(arr.positions, dtype=np.float64)
+    ang = np.ascontiguousarray(w.receive.angles, dtype=np.float64)
+    h = ctypes.c_void_p()
+    N, M, T = p.num_transmits, w.receive.num_angles, p.num_samples
+    _lib.call("kkb_decomposer_create", N, arr.num_elements, T, pos.ctypes.data, ang.ctypes.data, M,
+              float(arr.sampling_frequency), float(p.sound_speed), 1, ctypes.byref(h))
+    one = (ctypes.c_void_p * 1)(16)
+    nine = (ctypes.c_void_p * 9)(*([16] * 9))
+    for dsts, n, stride in ((one, 0, N * M * T), (nine, 9, N * M * T), (one, 1, N * M * T - 1)):
+        with pytest.raises(ConfigError):
+            _lib.call("kkb_decomposer_run_scatter", h, None, 0, 1, dsts, n, 0, stride, None)
+    _lib.load().kkb_decomposer_destroy(h)
+
+
+@pytest.mark.parametrize("transport", ["p2p", "nccl"])
+@pytest.mark.parametrize("cfg", [1, 5])
+def test_sharded_stage1_single_rank_is_the_full_image(cfg, transport):
+    import torch
+
+    w = configs.CONFIGS[cfg]()
+    p, arr = w.params, w.array
+    rf = torch.from_numpy(configs.noise_rf(p.num_transmits, arr.num_elements, p.num_samples,
+                                           seed=6)).cuda()
+    full_eng = kb.KKEngine(arr, p, w.receive, w.grid, frames=1, want_db=False)
+    full = full_eng.run(rf[None]).clone()[0]
+    rb = shard.RowBlockKK(arr, p, w.receive, w.grid, 0, 1, transport=transport, stage1="sharded")
+    assert rb.transport == transport and rb.engine is None
+    rb.beamform_block(rf)
+    assert torch.equal(rb.gather(), full)
+    rb.beamform_block(rf)  # rerun: identical
+    assert torch.equal(rb.gather(), full)
+    rb.close()
+    full_eng.close()

@@ -1,5 +1,6 @@
 """Multi-rank host logic on the CPU (gloo, world size 2 and 3): partitions,
-the row-block all-gather and its bit-identity with the single-rank image.
+the row-block all-gather and its bit-identity with the single-rank image,
+the transmit-block trace all-gather of sharded stage 1.
 The per-rank compute is the oracle here (no GPU in this container); on the
 GPU the same partition drives the K5 kernel (tests/test_gpu_shard.py)."""
 
@@ -58,6 +59,12 @@ def _worker(rank, world, port, out_dir):
         hs = shard.exchange_handles(bytes([rank]) * 64)
         assert hs == [bytes([r]) * 64 for r in range(world)]
         np.save(os.path.join(out_dir, f"rank{rank}.npy"), full.numpy())
+        # transmit-sharded stage 1 (NCCL-form fallback): each rank holds the
+        # traces of its transmit block; the all-gather rebuilds (N, M, T)
+        comp = g["compressed"].astype(np.complex64)
+        n0, n1 = shard.balanced_range(comp.shape[0], rank, world)
+        tr = shard.gather_transmit_blocks(torch.from_numpy(comp[n0:n1].copy()), comp.shape[0])
+        assert np.array_equal(tr.numpy(), comp)
         # frame sharding: each rank sums its frames' ids; all-reduce checks coverage
         b, e = shard.frame_range(400, rank, world)
         t = torch.tensor([float(sum(range(b, e)))])
