@@ -107,6 +107,22 @@ int kkb_kk_plan_run(kkb_kk_plan *p, const void *data, int n_frames, long long da
 int kkb_kk_plan_run_ex(kkb_kk_plan *p, const void *data, int n_frames, long long data_frame_stride,
                        void *out, int out_kind, long long out_frame_stride, float *intensity,
                        unsigned int *frame_max, int flags, void *stream);
+/* Incoherent multi-set compounding in ONE launch (the
+ * reference's hybrid / multi-j acquisitions, cli.py:100-107,257-266, with
+ * compound_incoherent, beamform.py:405-411): the plan is built over the
+ * concatenated receive angles of n_sets (<= 8) sets, set j being angles
+ * [set_begin_host[j], set_begin_host[j+1]) (0 = first < ... < last = M).
+ * Each set's image B_j is summed in the order a plan over that set alone
+ * uses (bit-identical to it when both run the tiled kernel), stored at out + j*out_set_stride (+ f*out_frame_stride,
+ * complex elements; out may be NULL), and intensity = sum_j |B_j|^2 in set
+ * order (+ the existing intensity with KKB_RUN_ACCUMULATE_INTENSITY);
+ * frame_max (zeroed) gets its per-frame max.  The tables are staged once
+ * for all sets. */
+int kkb_kk_plan_run_sets(kkb_kk_plan *p, const void *data, int n_frames,
+                         long long data_frame_stride, int n_sets, const int *set_begin_host,
+                         void *out, int out_kind, long long out_frame_stride,
+                         long long out_set_stride, float *intensity, unsigned int *frame_max,
+                         int flags, void *stream);
 /* Fused row-block all-gather: run the plan (whose
  * tables are this rank's lateral rows) and store every IQ pixel straight into
  * each of the n_dst (<= 8) full-image buffers dst_host[d] (device pointers:
@@ -119,7 +135,8 @@ int kkb_kk_plan_run_scatter(kkb_kk_plan *p, const void *data, int n_frames,
                             long long dst_offset, int out_kind, long long out_frame_stride,
                             void *stream);
 /* kkb_kk_plan_run_ex on a receive subset of a larger trace array: transmit n's
- * traces start at data + n*data_tx_stride (complex elements; 0 = M*T), so a
+ * traces start at data + n*data_tx_stride (complex elements, a multiple of T;
+ * 0 = M*T), so a
  * plan over M receive angles can read M consecutive rows of (N, M_total, T)
  * traces decomposed once for several receive sets (multi-set compounding). */
 int kkb_kk_plan_run_strided(kkb_kk_plan *p, const void *data, int n_frames,

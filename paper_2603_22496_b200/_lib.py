@@ -15,7 +15,8 @@ from .errors import DeviceError, raise_for_status
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 # KKB_LIB selects an alternative in-tree build (tuning variants under variants/)
-LIB_PATH = os.environ.get("KKB_LIB") or os.path.join(_HERE, "libkkb.so")
+_DEFAULT_LIB_PATH = os.path.join(_HERE, "libkkb.so")
+LIB_PATH = os.environ.get("KKB_LIB") or _DEFAULT_LIB_PATH
 
 P = ctypes.c_void_p
 I = ctypes.c_int
@@ -37,6 +38,7 @@ SIGNATURES = {
     "kkb_kk_plan_run_ex": [P, P, I, LL, P, I, LL, P, P, I, P],
     "kkb_kk_plan_run_strided": [P, P, I, LL, LL, P, I, LL, P, P, I, P],
     "kkb_kk_plan_run_scatter": [P, P, I, LL, P, I, LL, I, LL, P],
+    "kkb_kk_plan_run_sets": [P, P, I, LL, I, P, P, I, LL, LL, P, P, I, P],
     "kkb_kk_plan_window": [P],
     "kkb_kk_plan_destroy": [P],
     "kkb_kk_taps": [P, P, P, P, I, I, I, I, I, D, D, I, P, P],
@@ -97,6 +99,7 @@ class KKRFHeader(ctypes.Structure):
 KKB_OUT_C64 = 0
 KKB_RUN_ACCUMULATE_INTENSITY = 1
 KKB_MAX_DST = 8  # destinations of kkb_kk_plan_run_scatter
+KKB_MAX_SETS = 8  # receive sets of kkb_kk_plan_run_sets
 KKB_OUT_C128 = 1
 
 _lib = None
@@ -112,7 +115,10 @@ def load() -> ctypes.CDLL:
             f"{LIB_PATH} is missing: run __graft_entry__.build() (nvcc, sm_100a); "
             "this package has no CPU fallback")
     lib = ctypes.CDLL(LIB_PATH)
+    variant = LIB_PATH != _DEFAULT_LIB_PATH  # tuning builds may predate newer entry points
     for name, args in SIGNATURES.items():
+        if variant and not hasattr(lib, name):
+            continue
         fn = getattr(lib, name)
         fn.argtypes = args
         fn.restype = _RESTYPES.get(name, I)

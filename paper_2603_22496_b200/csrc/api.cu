@@ -212,8 +212,8 @@ extern "C" int kkb_kk_plan_run_strided(kkb_kk_plan *p, const void *data, int n_f
                                        float *intensity, unsigned int *frame_max, int flags,
                                        void *stream) {
     if (!p || (flags & ~KKB_RUN_ACCUMULATE_INTENSITY) ||
-        (data_tx_stride != 0 && data_tx_stride < (long long)p->M * p->T)) {
-        set_error("kk_plan_run: bad flags or transmit stride");
+        (data_tx_stride != 0 && (data_tx_stride < (long long)p->M * p->T || data_tx_stride % p->T))) {
+        set_error("kk_plan_run: bad flags or transmit stride (a multiple of T, >= M*T)");
         return KKB_ERR_ARG;
     }
     int st = check_kk_args(p->N, p->M, p->T, p->nx, p->nz, out_kind);
@@ -234,6 +234,39 @@ extern "C" int kkb_kk_plan_run_ex(kkb_kk_plan *p, const void *data, int n_frames
                                   unsigned int *frame_max, int flags, void *stream) {
     return kkb_kk_plan_run_strided(p, data, n_frames, data_frame_stride, 0, out, out_kind,
                                    out_frame_stride, intensity, frame_max, flags, stream);
+}
+
+extern "C" int kkb_kk_plan_run_sets(kkb_kk_plan *p, const void *data, int n_frames,
+                                    long long data_frame_stride, int n_sets,
+                                    const int *set_begin_host, void *out, int out_kind,
+                                    long long out_frame_stride, long long out_set_stride,
+                                    float *intensity, unsigned int *frame_max, int flags,
+                                    void *stream) {
+    if (!p || !set_begin_host || n_sets < 1 || n_sets > KKB_MAX_SETS ||
+        (flags & ~KKB_RUN_ACCUMULATE_INTENSITY)) {
+        set_error("kk_plan_run_sets: 1 <= n_sets <= %d, known flags", KKB_MAX_SETS);
+        return KKB_ERR_ARG;
+    }
+    KKSets sets{};
+    sets.nsets = n_sets;
+    sets.out_set_stride = out_set_stride;
+    for (int j = 0; j <= n_sets; ++j) sets.m0[j] = set_begin_host[j];
+    bool ok = sets.m0[0] == 0 && sets.m0[n_sets] == p->M;
+    for (int j = 0; j < n_sets; ++j) ok = ok && sets.m0[j + 1] > sets.m0[j];
+    if (!ok) {
+        set_error("kk_plan_run_sets: set bounds must rise strictly from 0 to M=%d", p->M);
+        return KKB_ERR_ARG;
+    }
+    int st = check_kk_args(p->N, p->M, p->T, p->nx, p->nz, out_kind);
+    if (st) return st;
+    if (frame_max)
+        KKB_TRY_CUDA(cudaMemsetAsync(frame_max, 0, sizeof(unsigned) * (size_t)n_frames, as_stream(stream)),
+                     "zero frame_max");
+    return kk_gather(reinterpret_cast<const float2 *>(data), p->N, p->M, p->T, p->ltx, p->ltzT,
+                     p->lrx, p->lrzT, p->nx, p->nz, p->w, p->fs, p->shift, p->linear, out,
+                     out_kind, n_frames, data_frame_stride, out_frame_stride, intensity, frame_max,
+                     p->W, as_stream(stream), (flags & KKB_RUN_ACCUMULATE_INTENSITY) ? 1 : 0,
+                     nullptr, p->W_small, 0, &sets);
 }
 
 extern "C" int kkb_kk_plan_run_scatter(kkb_kk_plan *p, const void *data, int n_frames,

@@ -62,12 +62,25 @@ struct KKScatter {
     void *dst[KKB_MAX_DST];
 };
 
+#define KKB_MAX_SETS 8
+// incoherent multi-set compounding in one launch: receive angles
+// [m0[j], m0[j+1]) form set j (m0[0] = 0, m0[nsets] = M); each set's image B_j
+// is summed separately (pairs n asc, m asc within the set, as a launch over
+// that set alone), stored at out + j * out_set_stride when out is set, and
+// intensity = sum_j |B_j|^2 in set order
+struct KKSets {
+    int nsets;
+    int m0[KKB_MAX_SETS + 1];
+    long long out_set_stride;
+};
+
 int kk_gather(const float2 *data, int N, int M, int T, const double *ltx, const double *ltzT,
               const double *lrx, const double *lrzT, int nx, int nz, const double *w, double fs,
               double shift, int linear, void *out, int out_kind, int n_frames, long long data_fs,
               long long out_fs, float *inten, unsigned *fmax, int W, cudaStream_t s,
               int accum = 0, const KKScatter *sc = nullptr, int W_small = 0,
-              long long data_ns = 0);  // 0: M*T (dense (N, M, T) traces)
+              long long data_ns = 0,  // 0: M*T (dense (N, M, T) traces)
+              const KKSets *sets = nullptr);
 
 int kk_taps(const double *ltx, const double *ltz, const double *lrx, const double *lrz, int N, int M,
             int T, int nx, int nz, double fs, double shift, int linear, int *idx, cudaStream_t s);

@@ -239,8 +239,8 @@ int kk_window(const double *ltx, const double *ltz, const double *lrx, const dou
 struct KKArgs {
     const float2 *data;
     long long data_fs;  // frame stride, complex elements
-    long long data_ns;  // transmit stride (M*T, or wider for a receive subset of a larger trace set)
     int N, M, T;
+    int data_nr;  // transmit stride in rows of T (M, or more for a receive subset of a larger trace set)
     const double *ltx;   // (X, N)
     const double *ltzT;  // (N, Z)
     const double *lrx;   // (X, M)
@@ -263,6 +263,10 @@ struct KKArgs {
     long long dst_off;
     void *dst[KKB_MAX_DST];
     int n_frames;  // frames in the batch (the multi-frame instance skips the tail)
+    // incoherent multi-set compounding (KKSets; the MS kernel instances only)
+    int nsets;
+    int set_m0[KKB_MAX_SETS + 1];
+    long long out_set_stride;
 };
 
 // packed LUT index: tile row r -> (r/8)*4 + r%4 pair slot, a = (r/4)&1
@@ -274,9 +278,21 @@ __device__ __forceinline__ int pcol(int c) {
     return (c / (8 * CX)) * (8 * CX) + (c & 7) * CX + ((c >> 3) % CX);
 }
 
-template <int WZ, int WX, int CX, bool LINEAR, int FR>
+// IQ pixel store (complex64 or complex128)
+__device__ __forceinline__ void store_iq(void *out, int kind, long long px, float vr, float vi) {
+    if (kind == KKB_OUT_C128)
+        reinterpret_cast<double2 *>(out)[px] = make_double2(vr, vi);
+    else
+        reinterpret_cast<float2 *>(out)[px] = make_float2(vr, vi);
+}
+
+// MS: the stage sequence runs set by set (set j: transmits n asc, receive
+// chunks of [set_m0[j], set_m0[j+1]) asc); at the end of each set its image is
+// stored, |B_j|^2 added to a per-pixel running intensity and the sums reset.
+template <int WZ, int WX, int CX, bool LINEAR, int FR, bool MS = false>
 __global__ void __launch_bounds__(WZ *WX * 32, KKB_KK_MIN_CTAS)
 k_kk_gather(const KKArgs a) {
+    static_assert(!MS || FR == 1, "multi-set instances run one frame per CTA");
     constexpr int TZ = 8 * WZ;
     constexpr int TX = 8 * CX * WX;
     constexpr int NT = WZ * WX * 32;
@@ -284,8 +300,15 @@ k_kk_gather(const KKArgs a) {
     constexpr int EPT = KKB_KK_STAGE_ELEMS / (32 * KKB_KK_WZ * KKB_KK_WX);
     using Entry = typename std::conditional<LINEAR, float4, float2>::type;
     const int N = a.N, M = a.M, T = a.T, W = a.W, MCH = a.MCH, nx = a.nx, nz = a.nz;
-    const int nchunk = (M + MCH - 1) / MCH;
-    const int nstage = N * nchunk;
+    int nchunk = (M + MCH - 1) / MCH;
+    int nstage = N * nchunk;
+    int set = 0, set_end = M;  // MS: current set and its receive range end
+    if constexpr (MS) {
+        nstage = 0;
+        for (int j = 0; j < a.nsets; ++j) nstage += N * ((a.set_m0[j + 1] - a.set_m0[j] + MCH - 1) / MCH);
+        set_end = a.set_m0[1];
+        nchunk = (set_end + MCH - 1) / MCH;
+    }
 
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Entry *win = reinterpret_cast<Entry *>(smem_raw);                  // [2][FR][MCH][W]
@@ -356,10 +379,11 @@ k_kk_gather(const KKArgs a) {
         qe[i] = (fr << 26) | (q << 16) | (rem - q * W);
     }
     // stage (n, m0): receive angles m0 .. m0+mc-1 of transmit n, all FR frames
-    auto load_stage = [&](int n, int m0) {
-        const int mc = min(MCH, M - m0);
+    auto load_stage = [&](int n, int m0, int mend) {
+        const int mc = min(MCH, mend - m0);
         const int2 *lo_q = lw_s + n * M + m0;
-        const float2 *base0 = a.data + (long long)f0 * a.data_fs + n * a.data_ns + (long long)m0 * T;
+        const int NR = a.data_nr;
+        const float2 *base0 = a.data + (long long)f0 * a.data_fs + (long long)(n * NR + m0) * T;
 #pragma unroll
         for (int i = 0; i < EPT; ++i) {
             s0[i] = s1[i] = make_float2(0.f, 0.f);
@@ -369,7 +393,7 @@ k_kk_gather(const KKArgs a) {
                 if constexpr (FR > 1) {
                     // frames past the batch re-read the first frame (results discarded)
                     const int fe = f0 + fr < a.n_frames ? f0 + fr : f0;
-                    base = a.data + (long long)fe * a.data_fs + n * a.data_ns + (long long)m0 * T;
+                    base = a.data + (long long)fe * a.data_fs + (long long)(n * NR + m0) * T;
                 }
                 const int smp = lo_q[q].x + e;
                 const float2 *tr = base + q * T;
@@ -382,8 +406,8 @@ k_kk_gather(const KKArgs a) {
             }
         }
     };
-    auto store_stage = [&](int m0, int buf) {
-        const int mc = min(MCH, M - m0);
+    auto store_stage = [&](int m0, int mend, int buf) {
+        const int mc = min(MCH, mend - m0);
         Entry *wb = win + buf * FR * MCH * W;
 #pragma unroll
         for (int i = 0; i < EPT; ++i) {
@@ -408,23 +432,45 @@ k_kk_gather(const KKArgs a) {
         for (int p = 0; p < 2; ++p)
 #pragma unroll
             for (int q = 0; q < CX; ++q) accr[fr][p][q] = acci[fr][p][q] = 0.f;
+    float isum[2][CX];  // MS: running sum_j |B_j|^2
+#pragma unroll
+    for (int p = 0; p < 2; ++p)
+#pragma unroll
+        for (int q = 0; q < CX; ++q) isum[p][q] = 0.f;
 
-    load_stage(0, 0);
-    store_stage(0, 0);
+    load_stage(0, 0, set_end);
+    store_stage(0, set_end, 0);
     __syncthreads();
     int n = 0, ch = 0;           // current stage
     int n1 = 0, ch1 = 0;         // next stage
+    int mb = 0, mb1 = 0;         // first receive angle of the current / next stage's set
+    int set_end1 = set_end, nchunk1 = nchunk;
     for (int s = 0; s < nstage; ++s) {
         const int buf = s & 1;
-        const int m0 = ch * MCH;
-        const int mc = min(MCH, M - m0);
+        const int m0 = mb + ch * MCH;
+        const int mc = min(MCH, set_end - m0);
         n1 = n;
         ch1 = ch + 1;
+        mb1 = mb;
+        set_end1 = set_end;
+        nchunk1 = nchunk;
+        bool set_done = false;
         if (ch1 == nchunk) {
             ch1 = 0;
             ++n1;
+            if constexpr (MS) {
+                if (n1 == N) {  // next set
+                    set_done = true;
+                    n1 = 0;
+                    if (set + 1 < a.nsets) {
+                        mb1 = set_end;
+                        set_end1 = a.set_m0[set + 2];
+                        nchunk1 = (set_end1 - mb1 + MCH - 1) / MCH;
+                    }
+                }
+            }
         }
-        if (s + 1 < nstage) load_stage(n1, ch1 * MCH);  // in flight during this stage's sums
+        if (s + 1 < nstage) load_stage(n1, mb1 + ch1 * MCH, set_end1);  // in flight during this stage's sums
         if (ch == 0) {
             const double2 tz = reinterpret_cast<const double2 *>(ltz_p + n * TZ)[zq];
             double txv[CX];
@@ -485,12 +531,60 @@ k_kk_gather(const KKArgs a) {
                 }
             }
         }
+        if constexpr (MS) {
+            if (set_done) {  // image of this set, |B|^2 into the running intensity, reset
+#pragma unroll
+                for (int p = 0; p < 2; ++p) {
+                    const int iz = iz0 + wz * 8 + p * 4 + zt;
+#pragma unroll
+                    for (int r = 0; r < CX; ++r) {
+                        const int ix = ix0 + wx * 8 * CX + r * 8 + xt;
+                        const float vr = accr[0][p][r], vi = acci[0][p][r];
+                        const long long px = (long long)f0 * a.out_fs + (long long)ix * nz + iz;
+                        if (iz < nz && ix < nx) {
+                            if (a.out) store_iq(a.out, a.out_kind, set * a.out_set_stride + px, vr, vi);
+                            float base = isum[p][r];
+                            if (set == 0) base = (a.accum && a.inten) ? a.inten[px] : 0.f;
+                            isum[p][r] = vr * vr + vi * vi + base;
+                        }
+                        accr[0][p][r] = acci[0][p][r] = 0.f;
+                    }
+                }
+                ++set;
+            }
+        }
         // buffer buf^1 was last read in stage s-1, which every thread finished
         // before the barrier that ended it
-        if (s + 1 < nstage) store_stage(ch1 * MCH, buf ^ 1);
+        if (s + 1 < nstage) store_stage(mb1 + ch1 * MCH, set_end1, buf ^ 1);
         __syncthreads();
         n = n1;
         ch = ch1;
+        mb = mb1;
+        set_end = set_end1;
+        nchunk = nchunk1;
+    }
+
+    if constexpr (MS) {  // running intensity and its frame max
+        if (f0 >= a.n_frames) return;
+        float fmx = 0.f;
+#pragma unroll
+        for (int p = 0; p < 2; ++p) {
+            const int iz = iz0 + wz * 8 + p * 4 + zt;
+#pragma unroll
+            for (int r = 0; r < CX; ++r) {
+                const int ix = ix0 + wx * 8 * CX + r * 8 + xt;
+                if (iz < nz && ix < nx) {
+                    const long long px = (long long)f0 * a.out_fs + (long long)ix * nz + iz;
+                    if (a.inten) a.inten[px] = isum[p][r];
+                    fmx = fmaxf(fmx, isum[p][r]);
+                }
+            }
+        }
+        if (a.fmax) {
+            for (int o = 16; o > 0; o >>= 1) fmx = fmaxf(fmx, __shfl_xor_sync(0xffffffffu, fmx, o));
+            if (lane == 0) atomicMax(a.fmax + f0, __float_as_uint(fmx));
+        }
+        return;
     }
 
     // epilogue: IQ (+ fused intensity and frame max), per frame
@@ -540,7 +634,7 @@ k_kk_gather(const KKArgs a) {
 // fit the staging buffer (very coarse grids / steep delays): one thread per
 // (frame, pixel), taps read through L1, the same index math (kk_delay +
 // tap_index), lerp, accumulation order and epilogue as the tiled kernel.
-template <bool LINEAR>
+template <bool LINEAR, bool MS = false>
 __global__ void __launch_bounds__(256)
 k_kk_direct(const KKArgs a) {
     const long long P = (long long)a.nx * a.nz;
@@ -550,51 +644,71 @@ k_kk_direct(const KKArgs a) {
     if (i < P) {
         const int ix = (int)(i / a.nz), iz = (int)(i % a.nz);
         const float2 *dframe = a.data + (long long)f * a.data_fs;
-        double tr_ = 0.0, ti_ = 0.0;  // per-transmit float32 partials, float64 total
-        for (int n = 0; n < a.N; ++n) {
-            float ar = 0.f, ai = 0.f;
-            const double t1 = __dadd_rn(a.ltx[(long long)ix * a.N + n], a.ltzT[(long long)n * a.nz + iz]);
-            for (int m = 0; m < a.M; ++m) {
-                const double fi = kk_delay(t1, a.lrzT[(long long)m * a.nz + iz], a.lrx[(long long)ix * a.M + m],
-                                           a.fs, a.shift);
-                int F;
-                double sv;
-                if (!tap_index<LINEAR>(fi, a.T, F, sv)) continue;
-                const float wm = a.w ? (float)a.w[m] : 1.0f;
-                const float2 *tr = dframe + n * a.data_ns + (long long)m * a.T;
-                const float2 d0 = __ldg(tr + F);
-                if (LINEAR) {
-                    const float2 d1 = __ldg(tr + F + 1);
-                    const float fr = __uint_as_float(((unsigned)__double2loint(sv) >> 9) | 0x3F800000u) - 1.0f;
-                    ar = fmaf(wm, fmaf(fr, d1.x - d0.x, d0.x), ar);
-                    ai = fmaf(wm, fmaf(fr, d1.y - d0.y, d0.y), ai);
-                } else {
-                    ar = fmaf(wm, d0.x, ar);
-                    ai = fmaf(wm, d0.y, ai);
-                }
-            }
-            tr_ += (double)ar;
-            ti_ += (double)ai;
-        }
-        const float ar = (float)tr_, ai = (float)ti_;
         const long long px = (long long)f * a.out_fs + i;
-        if (a.out) {
-            if (a.out_kind == KKB_OUT_C128)
-                reinterpret_cast<double2 *>(a.out)[px] = make_double2(tr_, ti_);
-            else
-                reinterpret_cast<float2 *>(a.out)[px] = make_float2(ar, ai);
+        const int nsets = MS ? a.nsets : 1;
+        float isum = 0.f;  // MS: running sum_j |B_j|^2
+        for (int j = 0; j < nsets; ++j) {
+            const int mb = MS ? a.set_m0[j] : 0, me = MS ? a.set_m0[j + 1] : a.M;
+            double tr_ = 0.0, ti_ = 0.0;  // per-transmit float32 partials, float64 total
+            for (int n = 0; n < a.N; ++n) {
+                float ar = 0.f, ai = 0.f;
+                const double t1 = __dadd_rn(a.ltx[(long long)ix * a.N + n], a.ltzT[(long long)n * a.nz + iz]);
+                for (int m = mb; m < me; ++m) {
+                    const double fi = kk_delay(t1, a.lrzT[(long long)m * a.nz + iz], a.lrx[(long long)ix * a.M + m],
+                                               a.fs, a.shift);
+                    int F;
+                    double sv;
+                    if (!tap_index<LINEAR>(fi, a.T, F, sv)) continue;
+                    const float wm = a.w ? (float)a.w[m] : 1.0f;
+                    const float2 *tr = dframe + (long long)(n * a.data_nr + m) * a.T;
+                    const float2 d0 = __ldg(tr + F);
+                    if (LINEAR) {
+                        const float2 d1 = __ldg(tr + F + 1);
+                        const float fr = __uint_as_float(((unsigned)__double2loint(sv) >> 9) | 0x3F800000u) - 1.0f;
+                        ar = fmaf(wm, fmaf(fr, d1.x - d0.x, d0.x), ar);
+                        ai = fmaf(wm, fmaf(fr, d1.y - d0.y, d0.y), ai);
+                    } else {
+                        ar = fmaf(wm, d0.x, ar);
+                        ai = fmaf(wm, d0.y, ai);
+                    }
+                }
+                tr_ += (double)ar;
+                ti_ += (double)ai;
+            }
+            const float ar = (float)tr_, ai = (float)ti_;
+            if constexpr (MS) {
+                if (a.out) {
+                    if (a.out_kind == KKB_OUT_C128)
+                        reinterpret_cast<double2 *>(a.out)[j * a.out_set_stride + px] = make_double2(tr_, ti_);
+                    else
+                        reinterpret_cast<float2 *>(a.out)[j * a.out_set_stride + px] = make_float2(ar, ai);
+                }
+                const float base = j ? isum : ((a.accum && a.inten) ? a.inten[px] : 0.f);
+                isum = ar * ar + ai * ai + base;
+                continue;
+            }
+            if (a.out) {
+                if (a.out_kind == KKB_OUT_C128)
+                    reinterpret_cast<double2 *>(a.out)[px] = make_double2(tr_, ti_);
+                else
+                    reinterpret_cast<float2 *>(a.out)[px] = make_float2(ar, ai);
+            }
+            for (int d = 0; d < a.ndst; ++d) {
+                if (a.out_kind == KKB_OUT_C128)
+                    reinterpret_cast<double2 *>(a.dst[d])[a.dst_off + px] = make_double2(tr_, ti_);
+                else
+                    reinterpret_cast<float2 *>(a.dst[d])[a.dst_off + px] = make_float2(ar, ai);
+            }
+            if (a.inten) {
+                float I = ar * ar + ai * ai;
+                if (a.accum) I += a.inten[px];
+                a.inten[px] = I;
+                fmx = I;
+            }
         }
-        for (int d = 0; d < a.ndst; ++d) {
-            if (a.out_kind == KKB_OUT_C128)
-                reinterpret_cast<double2 *>(a.dst[d])[a.dst_off + px] = make_double2(tr_, ti_);
-            else
-                reinterpret_cast<float2 *>(a.dst[d])[a.dst_off + px] = make_float2(ar, ai);
-        }
-        if (a.inten) {
-            float I = ar * ar + ai * ai;
-            if (a.accum) I += a.inten[px];
-            a.inten[px] = I;
-            fmx = I;
+        if constexpr (MS) {
+            if (a.inten) a.inten[px] = isum;
+            fmx = isum;
         }
     }
     if (a.fmax) {
@@ -610,19 +724,19 @@ static size_t kk_smem_bytes(int N, int M, int W, int MCH, bool linear, int tz = 
            sizeof(int2) * (size_t)N * M;
 }
 
-template <int WZ, int WX, int CX, int FR>
+template <int WZ, int WX, int CX, int FR, bool MS = false>
 static int launch_tiled(const KKArgs &a, int n_frames, size_t sm, bool linear, cudaStream_t s) {
     constexpr int TZ = 8 * WZ, TX = 8 * CX * WX;
     dim3 grid((unsigned)ceil_div(a.nz, TZ), (unsigned)ceil_div(a.nx, TX),
               (unsigned)ceil_div(n_frames, FR));
     dim3 block(WZ * WX * 32);
     if (linear) {
-        auto fn = k_kk_gather<WZ, WX, CX, true, FR>;
+        auto fn = k_kk_gather<WZ, WX, CX, true, FR, MS>;
         KKB_TRY_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm),
                      "smem attr kk");
         fn<<<grid, block, sm, s>>>(a);
     } else {
-        auto fn = k_kk_gather<WZ, WX, CX, false, FR>;
+        auto fn = k_kk_gather<WZ, WX, CX, false, FR, MS>;
         KKB_TRY_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm),
                      "smem attr kk");
         fn<<<grid, block, sm, s>>>(a);
@@ -635,16 +749,25 @@ int kk_gather(const float2 *data, int N, int M, int T, const double *ltx, const 
               const double *lrx, const double *lrzT, int nx, int nz, const double *w, double fs,
               double shift, int linear, void *out, int out_kind, int n_frames, long long data_fs,
               long long out_fs, float *inten, unsigned *fmax, int W, cudaStream_t s, int accum,
-              const KKScatter *sc, int W_small, long long data_ns) {
+              const KKScatter *sc, int W_small, long long data_ns, const KKSets *sets) {
     if (n_frames <= 0 || nx <= 0 || nz <= 0) return KKB_OK;
+    const bool ms = sets != nullptr;
     if (W < 2) W = 2;
-    KKArgs a{data, data_fs, data_ns > 0 ? data_ns : (long long)M * T, N, M, T, ltx, ltzT, lrx,
+    if (data_ns > 0 && (data_ns % T || data_ns / T < M || (data_ns / T) * (long long)N > 0x7fffffffLL))
+        return KKB_ERR_ARG;
+    KKArgs a{data, data_fs, N, M, T, data_ns > 0 ? (int)(data_ns / T) : M, ltx, ltzT, lrx,
              lrzT, w, fs, shift, nx, nz, W, 0,
              out, out_kind, out_fs, inten, fmax, accum, 0, 0, {}, n_frames};
     if (sc) {
         a.ndst = sc->ndst;
         a.dst_off = sc->dst_off;
         for (int d = 0; d < sc->ndst; ++d) a.dst[d] = sc->dst[d];
+    }
+    if (ms) {
+        if (sc || sets->nsets < 1 || sets->nsets > KKB_MAX_SETS) return KKB_ERR_ARG;
+        a.nsets = sets->nsets;
+        for (int j = 0; j <= sets->nsets; ++j) a.set_m0[j] = sets->m0[j];
+        a.out_set_stride = sets->out_set_stride;
     }
     // instance: big tiles; small tiles when the big grid cannot fill the SMs
     // (or the big tile's window overflows its stage); else the per-pixel kernel
@@ -661,7 +784,12 @@ int kk_gather(const float2 *data, int N, int M, int T, const double *ltx, const 
     if ((force && force[0] == '1') || (!big_ok && !use_small)) {
         // steep geometry or huge pair tables: per-pixel kernel
         dim3 grid((unsigned)ceil_div((long long)nx * nz, 256), (unsigned)n_frames);
-        if (linear)
+        if (ms) {
+            if (linear)
+                k_kk_direct<true, true><<<grid, 256, 0, s>>>(a);
+            else
+                k_kk_direct<false, true><<<grid, 256, 0, s>>>(a);
+        } else if (linear)
             k_kk_direct<true><<<grid, 256, 0, s>>>(a);
         else
             k_kk_direct<false><<<grid, 256, 0, s>>>(a);
@@ -674,7 +802,7 @@ int kk_gather(const float2 *data, int N, int M, int T, const double *ltx, const 
     // big tiles over a batch: KKB_KK_FR frames per CTA share the tables and the
     // index math of every tap (when a window block of FR frames fits a stage)
     const char *ffr = getenv("KKB_KK_FR1");  // test hook: one frame per CTA
-    const int FR = (!use_small && n_frames > 1 && KKB_KK_FR > 1 && KKB_KK_FR * Wc <= stage &&
+    const int FR = (!ms && !use_small && n_frames > 1 && KKB_KK_FR > 1 && KKB_KK_FR * Wc <= stage &&
                     !(ffr && ffr[0] == '1')) ? KKB_KK_FR : 1;
     // receive angles per stage: bounded by the register staging and shared memory
     int MCH = std::max(1, std::min(M, stage / (FR * Wc)));
@@ -682,6 +810,11 @@ int kk_gather(const float2 *data, int N, int M, int T, const double *ltx, const 
     const size_t sm = kk_smem_bytes(N, M, Wc, MCH, linear, tz, tx, FR);
     a.W = Wc;
     a.MCH = MCH;
+    if (ms) {
+        if (use_small)
+            return launch_tiled<KKB_KK_S_WZ, KKB_KK_S_WX, KKB_KK_S_CX, 1, true>(a, n_frames, sm, linear != 0, s);
+        return launch_tiled<KKB_KK_WZ, KKB_KK_WX, KKB_KK_CX, 1, true>(a, n_frames, sm, linear != 0, s);
+    }
     if (use_small)
         return launch_tiled<KKB_KK_S_WZ, KKB_KK_S_WX, KKB_KK_S_CX, 1>(a, n_frames, sm, linear != 0, s);
     if (FR > 1)

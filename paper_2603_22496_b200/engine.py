@@ -279,10 +279,10 @@ class MultiSetEngine:
     The RF is decomposed ONCE over the concatenated angle list (the sets laid
     out one after another along the receive axis), so the element FFTs are
     shared by all sets.
-    mode "incoherent": one gather per set over its rows of the shared traces
-      (``kkb_kk_plan_run_strided``); each adds its |IQ_j|^2 to one intensity
-      buffer (KKB_RUN_ACCUMULATE_INTENSITY), so sum_j |B_j|^2 and its per-frame
-      max come out of the last launch; per-set IQ in ``iq[j]``.
+    mode "incoherent": ONE gather launch over the shared traces
+      (``kkb_kk_plan_run_sets``): each CTA stages the tables once and sums the
+      sets one after another, storing B_j in ``iq[j]`` and sum_j |B_j|^2 (and
+      its per-frame max) in ``inten``.
     mode "coherent": |sum_j B_j|^2 is the kk image over the whole list (kk sums
       over every receive angle): one gather over all rows.
     """
@@ -290,8 +290,6 @@ class MultiSetEngine:
     def __init__(self, array: TransducerArray, params: AcquisitionParams, receive_sets,
                  grid: ImageGrid, frames: int, mode: str = "incoherent", want_db: bool = True,
                  floor_db: float = -60.0, **kw):
-        import ctypes
-
         from .sampling import explicit_angles
 
         sets = [rs[1] if isinstance(rs, tuple) else rs for rs in receive_sets]
@@ -299,9 +297,12 @@ class MultiSetEngine:
             raise ConfigError("need at least one receive set")
         if mode not in ("incoherent", "coherent"):
             raise ConfigError(f"unknown compounding mode {mode!r}")
+        if mode == "incoherent" and len(sets) > _lib.KKB_MAX_SETS:
+            raise ConfigError(f"at most {_lib.KKB_MAX_SETS} receive sets per launch")
         self.mode, self.want_db, self.floor_db = mode, want_db, float(floor_db)
+        self.sets = sets
         union = explicit_angles(np.concatenate([s.angles for s in sets]), sets[0].delta_theta_i)
-        # the union engine: shared decomposition; in coherent mode also the gather
+        # the union engine: shared decomposition and the plan over all angles
         self.engine = KKEngine(array, params, union, grid, frames,
                                want_db=want_db and mode == "coherent", floor_db=floor_db, **kw)
         self.engines = [self.engine]
@@ -312,24 +313,11 @@ class MultiSetEngine:
         t = e.t
         self.inten, self.fmax = e.inten, e.fmax
         self.db = t.empty_like(e.inten) if want_db else None
-        self.sets = sets
-        self._plans, self._luts, self.iq = [], [], []
-        self._m_off = np.concatenate([[0], np.cumsum([s.num_angles for s in sets])[:-1]]).astype(int)
-        w_all = kw.get("channel_weights")
-        for j, rs in enumerate(sets):
-            luts = build_kk_luts_device(grid, params.transmit_angles, rs.angles, e.c)
-            w = None
-            if w_all is not None:
-                w = dev.to_device(np.asarray(w_all, dtype=np.float64)[
-                    self._m_off[j]:self._m_off[j] + rs.num_angles])
-            kp = ctypes.c_void_p()
-            _lib.call("kkb_kk_plan_create", dev.ptr(luts["lut_tx_x"]), dev.ptr(luts["lut_tx_z"]),
-                      dev.ptr(luts["lut_rx_x"]), dev.ptr(luts["lut_rx_z"]), e.N, rs.num_angles,
-                      e.T, grid.nx, grid.nz, dev.ptr(w), float(e.fs), float(e.shift),
-                      int(e.linear), dev.stream_handle(), ctypes.byref(kp))
-            self._plans.append(kp)
-            self._luts.append((luts, w))
-            self.iq.append(t.empty((e.F, grid.nx, grid.nz), dtype=t.complex64, device="cuda"))
+        bounds = np.concatenate([[0], np.cumsum([s.num_angles for s in sets])]).astype(np.int32)
+        self._m_off = bounds[:-1].astype(int)
+        self._bounds = (ctypes.c_int * len(bounds))(*[int(b) for b in bounds])
+        # per-set IQ, (S, F, X, Z): iq[j] is set j's images
+        self.iq = t.empty((len(sets), e.F, grid.nx, grid.nz), dtype=t.complex64, device="cuda")
 
     @property
     def pixel_pairs_per_frame(self) -> int:
@@ -339,32 +327,23 @@ class MultiSetEngine:
         """Compounded intensity (F, X, Z) float32 for a (F, N, L, T) RF batch;
         asynchronous."""
         e = self.engine
+        if tuple(rf.shape[:1]) != (e.F,):
+            raise ConfigError(f"expected RF of shape {(e.F, e.N, e.L, e.T)}")
         if self.mode == "coherent":
             e.run(rf, stream=stream, groups=1)
             return self.inten
-        if tuple(rf.shape[:1]) != (e.F,):
-            raise ConfigError(f"expected RF of shape {(e.F, e.N, e.L, e.T)}")
         e.decompose(rf, stream=stream)
         s = dev.stream_handle(stream)
         P = e.grid.nx * e.grid.nz
-        Mu = e.M
-        last = len(self.sets) - 1
-        for j, (rs, kp) in enumerate(zip(self.sets, self._plans)):
-            base = dev.ptr(e.traces) + int(self._m_off[j]) * e.T * 8  # complex64 rows m_off..
-            _lib.call("kkb_kk_plan_run_strided", kp, base, e.F, e.N * Mu * e.T, Mu * e.T,
-                      dev.ptr(self.iq[j]), _lib.KKB_OUT_C64, P, dev.ptr(self.inten),
-                      dev.ptr(self.fmax) if j == last else None,
-                      _lib.KKB_RUN_ACCUMULATE_INTENSITY if j > 0 else 0, s)
+        _lib.call("kkb_kk_plan_run_sets", e._kk, dev.ptr(e.traces), e.F, e.N * e.M * e.T,
+                  len(self.sets), self._bounds, dev.ptr(self.iq), _lib.KKB_OUT_C64, P, e.F * P,
+                  dev.ptr(self.inten), dev.ptr(self.fmax), 0, s)
         if self.want_db:
             _lib.call("kkb_log_compress", dev.ptr(self.inten), dev.ptr(self.fmax), e.F, P,
                       self.floor_db, dev.ptr(self.db), s)
         return self.inten
 
     def close(self):
-        lib = _lib.load()
-        for kp in getattr(self, "_plans", []):
-            lib.kkb_kk_plan_destroy(kp)
-        self._plans = []
         self.engine.close()
 
     def __del__(self):

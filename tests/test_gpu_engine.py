@@ -254,3 +254,75 @@ def test_multiset_compounding_matches_oracle(oracle, config1_rf, mode):
         for j, img in enumerate(imgs):
             assert rel_l2(eng.iq[j][1].cpu().numpy(), img) <= 1e-5, j
     eng.close()
+
+
+@pytest.mark.parametrize("interp,direct", [("linear", "0"), ("nearest", "0"), ("linear", "1")])
+def test_multiset_one_launch_equals_per_set_launches(monkeypatch, interp, direct):
+    """kkb_kk_plan_run_sets (one launch, tables staged once) against one
+    strided launch per set over the same shared traces, accumulating the
+    intensity: IQ of every set, the compounded intensity and its max are
+    bit-identical (tiled kernels; and the per-pixel kernels, KKB_KK_DIRECT=1)."""
+    import ctypes
+
+    torch = _torch()
+    from paper_2603_22496_b200 import _device as dev
+    from paper_2603_22496_b200 import _lib
+    from paper_2603_22496_b200.beamform import build_kk_luts_device
+
+    monkeypatch.setenv("KKB_KK_DIRECT", direct)
+    w = configs.config1()
+    p, arr, g = w.params, w.array, w.grid
+    tmax = 10 * np.pi / 180
+    sets = [kb.uniform_vernier_angles(11, 5, tmax, 0), kb.confocal_angles(11, 3, tmax),
+            kb.uniform_vernier_angles(11, 2, tmax, 1)]
+    frames = 3
+    rf = torch.from_numpy(np.stack([configs.noise_rf(p.num_transmits, arr.num_elements,
+                                                     p.num_samples, seed=50 + f)
+                                    for f in range(frames)])).cuda()
+    weights = np.linspace(0.5, 1.5, sum(s.num_angles for s in sets))
+    eng = kb.MultiSetEngine(arr, p, sets, g, frames, mode="incoherent", interpolation=interp,
+                            channel_weights=weights)
+    eng.run(rf)
+    torch.cuda.synchronize()
+    e = eng.engine
+    P = g.nx * g.nz
+    inten = torch.empty_like(eng.inten)
+    fmax = torch.zeros_like(eng.fmax)
+    off = 0
+    for j, rs in enumerate(sets):
+        luts = build_kk_luts_device(g, p.transmit_angles, rs.angles, p.sound_speed)
+        wj = dev.to_device(weights[off:off + rs.num_angles].copy())
+        kp = ctypes.c_void_p()
+        _lib.call("kkb_kk_plan_create", dev.ptr(luts["lut_tx_x"]), dev.ptr(luts["lut_tx_z"]),
+                  dev.ptr(luts["lut_rx_x"]), dev.ptr(luts["lut_rx_z"]), e.N, rs.num_angles, e.T,
+                  g.nx, g.nz, dev.ptr(wj), float(e.fs), float(e.shift), int(interp == "linear"),
+                  dev.stream_handle(), ctypes.byref(kp))
+        iq = torch.empty((frames, g.nx, g.nz), dtype=torch.complex64, device="cuda")
+        _lib.call("kkb_kk_plan_run_strided", kp, dev.ptr(e.traces) + off * e.T * 8, frames,
+                  e.N * e.M * e.T, e.M * e.T, dev.ptr(iq), _lib.KKB_OUT_C64, P, dev.ptr(inten),
+                  dev.ptr(fmax) if j == len(sets) - 1 else None,
+                  _lib.KKB_RUN_ACCUMULATE_INTENSITY if j else 0, dev.stream_handle())
+        torch.cuda.synchronize()
+        _lib.load().kkb_kk_plan_destroy(kp)
+        assert torch.equal(iq, eng.iq[j]), j
+        off += rs.num_angles
+    assert torch.equal(inten, eng.inten)
+    assert torch.equal(fmax, eng.fmax)
+    eng.close()
+
+
+def test_run_sets_rejects_bad_bounds():
+    import ctypes
+
+    from paper_2603_22496_b200 import _lib
+    from paper_2603_22496_b200.errors import ConfigError
+
+    w = configs.config1()
+    eng = _engine(w, 1)
+    M = eng.M
+    for b in ([0, M - 1], [1, M], [0, 5, 5, M], [0] + list(range(1, 10)) + [M]):
+        arr = (ctypes.c_int * len(b))(*b)
+        with pytest.raises(ConfigError):
+            _lib.call("kkb_kk_plan_run_sets", eng._kk, None, 1, 0, len(b) - 1, arr, None, 0, 0, 0,
+                      None, None, 0, None)
+    eng.close()
