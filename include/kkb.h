@@ -138,7 +138,10 @@ int kkb_kk_plan_run_scatter(kkb_kk_plan *p, const void *data, int n_frames,
  * traces start at data + n*data_tx_stride (complex elements, a multiple of T;
  * 0 = M*T), so a
  * plan over M receive angles can read M consecutive rows of (N, M_total, T)
- * traces decomposed once for several receive sets (multi-set compounding). */
+ * traces decomposed once for several receive sets.  The subset rows are
+ * copied into dense stream-ordered scratch before the gather (the kernels
+ * keep dense row arithmetic); kkb_kk_plan_run_sets is the one-launch form of
+ * multi-set compounding. */
 int kkb_kk_plan_run_strided(kkb_kk_plan *p, const void *data, int n_frames,
                             long long data_frame_stride, long long data_tx_stride, void *out,
                             int out_kind, long long out_frame_stride, float *intensity,

@@ -240,7 +240,6 @@ struct KKArgs {
     const float2 *data;
     long long data_fs;  // frame stride, complex elements
     int N, M, T;
-    int data_nr;  // transmit stride in rows of T (M, or more for a receive subset of a larger trace set)
     const double *ltx;   // (X, N)
     const double *ltzT;  // (N, Z)
     const double *lrx;   // (X, M)
@@ -382,8 +381,7 @@ k_kk_gather(const KKArgs a) {
     auto load_stage = [&](int n, int m0, int mend) {
         const int mc = min(MCH, mend - m0);
         const int2 *lo_q = lw_s + n * M + m0;
-        const int NR = a.data_nr;
-        const float2 *base0 = a.data + (long long)f0 * a.data_fs + (long long)(n * NR + m0) * T;
+        const float2 *base0 = a.data + (long long)f0 * a.data_fs + (long long)(n * M + m0) * T;
 #pragma unroll
         for (int i = 0; i < EPT; ++i) {
             s0[i] = s1[i] = make_float2(0.f, 0.f);
@@ -393,7 +391,7 @@ k_kk_gather(const KKArgs a) {
                 if constexpr (FR > 1) {
                     // frames past the batch re-read the first frame (results discarded)
                     const int fe = f0 + fr < a.n_frames ? f0 + fr : f0;
-                    base = a.data + (long long)fe * a.data_fs + (long long)(n * NR + m0) * T;
+                    base = a.data + (long long)fe * a.data_fs + (long long)(n * M + m0) * T;
                 }
                 const int smp = lo_q[q].x + e;
                 const float2 *tr = base + q * T;
@@ -443,22 +441,23 @@ k_kk_gather(const KKArgs a) {
     __syncthreads();
     int n = 0, ch = 0;           // current stage
     int n1 = 0, ch1 = 0;         // next stage
-    int mb = 0, mb1 = 0;         // first receive angle of the current / next stage's set
+    int mb = 0, mb1 = 0;         // MS: first receive angle of the current / next stage's set
     int set_end1 = set_end, nchunk1 = nchunk;
     for (int s = 0; s < nstage; ++s) {
         const int buf = s & 1;
-        const int m0 = mb + ch * MCH;
-        const int mc = min(MCH, set_end - m0);
+        int m0, mc;
+        bool set_done = false;
         n1 = n;
         ch1 = ch + 1;
-        mb1 = mb;
-        set_end1 = set_end;
-        nchunk1 = nchunk;
-        bool set_done = false;
-        if (ch1 == nchunk) {
-            ch1 = 0;
-            ++n1;
-            if constexpr (MS) {
+        if constexpr (MS) {
+            m0 = mb + ch * MCH;
+            mc = min(MCH, set_end - m0);
+            mb1 = mb;
+            set_end1 = set_end;
+            nchunk1 = nchunk;
+            if (ch1 == nchunk) {
+                ch1 = 0;
+                ++n1;
                 if (n1 == N) {  // next set
                     set_done = true;
                     n1 = 0;
@@ -469,8 +468,16 @@ k_kk_gather(const KKArgs a) {
                     }
                 }
             }
+            if (s + 1 < nstage) load_stage(n1, mb1 + ch1 * MCH, set_end1);  // in flight during this stage's sums
+        } else {
+            m0 = ch * MCH;
+            mc = min(MCH, M - m0);
+            if (ch1 == nchunk) {
+                ch1 = 0;
+                ++n1;
+            }
+            if (s + 1 < nstage) load_stage(n1, ch1 * MCH, M);  // in flight during this stage's sums
         }
-        if (s + 1 < nstage) load_stage(n1, mb1 + ch1 * MCH, set_end1);  // in flight during this stage's sums
         if (ch == 0) {
             const double2 tz = reinterpret_cast<const double2 *>(ltz_p + n * TZ)[zq];
             double txv[CX];
@@ -555,13 +562,17 @@ k_kk_gather(const KKArgs a) {
         }
         // buffer buf^1 was last read in stage s-1, which every thread finished
         // before the barrier that ended it
-        if (s + 1 < nstage) store_stage(mb1 + ch1 * MCH, set_end1, buf ^ 1);
+        if constexpr (MS) {
+            if (s + 1 < nstage) store_stage(mb1 + ch1 * MCH, set_end1, buf ^ 1);
+            mb = mb1;
+            set_end = set_end1;
+            nchunk = nchunk1;
+        } else {
+            if (s + 1 < nstage) store_stage(ch1 * MCH, M, buf ^ 1);
+        }
         __syncthreads();
         n = n1;
         ch = ch1;
-        mb = mb1;
-        set_end = set_end1;
-        nchunk = nchunk1;
     }
 
     if constexpr (MS) {  // running intensity and its frame max
@@ -660,7 +671,7 @@ k_kk_direct(const KKArgs a) {
                     double sv;
                     if (!tap_index<LINEAR>(fi, a.T, F, sv)) continue;
                     const float wm = a.w ? (float)a.w[m] : 1.0f;
-                    const float2 *tr = dframe + (long long)(n * a.data_nr + m) * a.T;
+                    const float2 *tr = dframe + (long long)(n * a.M + m) * a.T;
                     const float2 d0 = __ldg(tr + F);
                     if (LINEAR) {
                         const float2 d1 = __ldg(tr + F + 1);
@@ -753,9 +764,34 @@ int kk_gather(const float2 *data, int N, int M, int T, const double *ltx, const 
     if (n_frames <= 0 || nx <= 0 || nz <= 0) return KKB_OK;
     const bool ms = sets != nullptr;
     if (W < 2) W = 2;
-    if (data_ns > 0 && (data_ns % T || data_ns / T < M || (data_ns / T) * (long long)N > 0x7fffffffLL))
-        return KKB_ERR_ARG;
-    KKArgs a{data, data_fs, N, M, T, data_ns > 0 ? (int)(data_ns / T) : M, ltx, ltzT, lrx,
+    // a receive subset of a larger trace array (transmit stride data_ns > M*T):
+    // gathered into dense (F, N, M, T) scratch first, so the kernels keep the
+    // dense row arithmetic (a runtime transmit stride costs K5 0.5-8%)
+    float2 *dense = nullptr;
+    if (data_ns > 0 && data_ns != (long long)M * T) {
+        if (data_ns < (long long)M * T) return KKB_ERR_ARG;
+        const size_t row = sizeof(float2) * (size_t)M * T;
+        KKB_TRY_CUDA(cudaMallocAsync(&dense, row * (size_t)n_frames * N, s), "cudaMallocAsync(dense traces)");
+        for (int f = 0; f < n_frames; ++f) {
+            cudaError_t e = cudaMemcpy2DAsync(dense + (size_t)f * N * M * T, row, data + f * data_fs,
+                                              sizeof(float2) * (size_t)data_ns, row, (size_t)N,
+                                              cudaMemcpyDeviceToDevice, s);
+            if (e != cudaSuccess) {
+                cudaFreeAsync(dense, s);
+                return cuda_status(e, "copy trace subset");
+            }
+        }
+        data = dense;
+        data_fs = (long long)N * M * T;
+    }
+    struct FreeDense {
+        float2 *p;
+        cudaStream_t s;
+        ~FreeDense() {
+            if (p) cudaFreeAsync(p, s);
+        }
+    } free_dense{dense, s};
+    KKArgs a{data, data_fs, N, M, T, ltx, ltzT, lrx,
              lrzT, w, fs, shift, nx, nz, W, 0,
              out, out_kind, out_fs, inten, fmax, accum, 0, 0, {}, n_frames};
     if (sc) {

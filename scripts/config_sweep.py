@@ -39,6 +39,30 @@ def device_rate(w, params, rx, frames, reps=5):
     return ms, pp
 
 
+def multiset_rate(w, params, sets, frames, reps=5):
+    """Incoherent compounding of several receive sets (MultiSetEngine: one
+    decomposition over the union, one gather launch for all sets)."""
+    import torch
+
+    eng = kb.MultiSetEngine(w.array, params, sets, w.grid, frames, mode="incoherent")
+    N, L, T = params.num_transmits, w.array.num_elements, params.num_samples
+    base = configs.noise_rf(N, L, T, seed=0)
+    rf = torch.from_numpy(np.broadcast_to(base, (frames,) + base.shape).copy()).cuda()
+    for _ in range(3):
+        eng.run(rf)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        eng.run(rf)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    pp = eng.pixel_pairs_per_frame
+    eng.close()
+    return ms, pp
+
+
 def cpu_frame_ms(w, params, rx, seconds=4.0):
     from oracle import kkbeam_oracle as O
 
@@ -84,6 +108,19 @@ def main():
                "cpu_port_ms_per_frame": cpu, "cpu_threads": os.cpu_count()}
         out.append(row)
         print(json.dumps(row), flush=True)
+    # config 3 hybrid compounded incoherently (cli.py:257-266): confocal(25, 3)
+    # and vernier(25, 2) images, sum of |B_j|^2, one gather launch
+    hp = w3.extra_receive["hybrid"][0]
+    d = hp.transmit_angles[1] - hp.transmit_angles[0]
+    sets = [kb.confocal_angles(25, 3, 12 * d), kb.uniform_vernier_angles(25, 2, 12 * d, 0)]
+    ms_b, pp = multiset_rate(w3, hp, sets, 16)
+    ms_1, _ = multiset_rate(w3, hp, sets, 1, reps=10)
+    row = {"workload": "config3_hybrid_incoherent", "pairs": pp // (w3.grid.nx * w3.grid.nz),
+           "grid": [w3.grid.nx, w3.grid.nz], "T": hp.num_samples,
+           "gpu_ms_per_frame_batched": ms_b / 16, "batch": 16, "gpu_ms_single_frame": ms_1,
+           "pixel_pairs_per_s": pp / (ms_b / 16 / 1e3), "cpu_port_ms_per_frame": None,
+           "cpu_threads": os.cpu_count()}
+    print(json.dumps(row), flush=True)
 
 
 if __name__ == "__main__":
