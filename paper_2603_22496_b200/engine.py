@@ -215,6 +215,25 @@ class KKEngine:
         main.wait_stream(side)
         return self.iq
 
+    def capture(self, rf, groups: int = 1):
+        """CUDA graph of the whole hot path (``run``) on the static RF buffer
+        ``rf``: returns a ``KKGraph`` whose ``replay()`` reruns every launch
+        with no host work, for low-latency frame-by-frame imaging (refill
+        ``rf`` in place between replays; outputs land in ``iq`` / ``inten`` /
+        ``db`` as for ``run``)."""
+        t = self.t
+        self._check_rf(rf, self.F)
+        s = t.cuda.Stream()
+        s.wait_stream(t.cuda.current_stream())
+        with t.cuda.stream(s):  # warm-up: attributes, allocator pools
+            self.run(rf, stream=s, groups=groups)
+        s.synchronize()
+        g = t.cuda.CUDAGraph()
+        with t.cuda.graph(g, stream=s):
+            self.run(rf, stream=s, groups=groups)
+        t.cuda.current_stream().wait_stream(s)
+        return KKGraph(g, self, rf)
+
     # ------------------------------------------------------------------ end-to-end path
     def run_host(self, rf_host, iq_host, chunk_frames: int = 16, streams=None, staging=None):
         """Pinned host RF (F, N, L, T) float32 -> pinned host IQ (F, X, Z) complex64.
@@ -269,6 +288,19 @@ class KKEngine:
             self.close()
         except Exception:
             pass
+
+
+class KKGraph:
+    """A captured ``KKEngine.run`` (see ``KKEngine.capture``)."""
+
+    def __init__(self, graph, engine, rf):
+        self.graph, self.engine, self.rf = graph, engine, rf
+
+    def replay(self):
+        """Rerun the captured hot path on the current contents of ``rf``;
+        asynchronous on the current stream.  Returns the IQ images."""
+        self.graph.replay()
+        return self.engine.iq
 
 
 class MultiSetEngine:

@@ -1,31 +1,44 @@
-import sys, os, time, json
-sys.path.insert(0, '/root/repo' if os.path.exists('/root/repo') else '.')
-import numpy as np, torch
-import paper_2603_22496_b200 as kb
-from paper_2603_22496_b200 import configs
+"""Single-frame latency of the whole hot path: eager launches vs one CUDA
+graph replay (KKEngine.capture), host wall clock per frame incl. sync."""
+import json
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_2603_22496_b200 as kb  # noqa: E402
+from paper_2603_22496_b200 import configs  # noqa: E402
+
 res = {}
-for cfg in (1, 2, 4):
+for cfg in (1, 2, 4, 5):
     w = configs.CONFIGS[cfg]()
-    eng = kb.KKEngine(w.array, w.params, w.receive, w.grid, frames=1)
     p = w.params
-    rf = torch.from_numpy(configs.noise_rf(p.num_transmits, w.array.num_elements, p.num_samples)[None]).cuda()
-    s = torch.cuda.Stream()
-    with torch.cuda.stream(s):
-        for _ in range(3):
-            eng.run(rf)
-    torch.cuda.synchronize()
-    g = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(g, stream=s):
+    eng = kb.KKEngine(w.array, p, w.receive, w.grid, frames=1)
+    rf = torch.from_numpy(configs.noise_rf(p.num_transmits, w.array.num_elements,
+                                           p.num_samples)[None]).cuda()
+    for _ in range(3):
         eng.run(rf)
     torch.cuda.synchronize()
     ref = eng.iq.clone()
-    g.replay(); torch.cuda.synchronize()
+    g = eng.capture(rf)
+    g.replay()
+    torch.cuda.synchronize()
     same = bool(torch.equal(ref, eng.iq))
-    def t(fn, n=200):
-        torch.cuda.synchronize(); t0 = time.perf_counter()
-        for _ in range(n): fn()
-        torch.cuda.synchronize(); return (time.perf_counter() - t0) / n * 1e3
-    eager = t(lambda: eng.run(rf))
-    graph = t(lambda: g.replay())
-    res[w.name] = {"eager_ms": eager, "graph_ms": graph, "bit_identical": same}
+
+    def per_frame(fn, n):
+        fn()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(n):
+            fn()
+            torch.cuda.synchronize()
+        return (time.perf_counter() - t0) / n * 1e3
+
+    n = 20 if cfg == 5 else 300
+    res[w.name] = {"eager_ms": per_frame(lambda: eng.run(rf), n),
+                   "graph_ms": per_frame(g.replay, n), "bit_identical": same}
+    eng.close()
 print(json.dumps(res))

@@ -326,3 +326,33 @@ def test_run_sets_rejects_bad_bounds():
             _lib.call("kkb_kk_plan_run_sets", eng._kk, None, 1, 0, len(b) - 1, arr, None, 0, 0, 0,
                       None, None, 0, None)
     eng.close()
+
+
+@pytest.mark.parametrize("cfg", [1, 4])
+def test_engine_graph_replay_equals_eager(cfg):
+    """KKEngine.capture: one CUDA graph of the whole path; replays on new RF
+    written into the static buffer give the eager result bit for bit."""
+    torch = _torch()
+    w = configs.CONFIGS[cfg]()
+    p, arr = w.params, w.array
+    frames = 2
+    eng = _engine(w, frames)
+    rf = torch.empty((frames, p.num_transmits, arr.num_elements, p.num_samples),
+                     dtype=torch.float32, device="cuda")
+    rf.copy_(torch.from_numpy(np.stack([configs.noise_rf(p.num_transmits, arr.num_elements,
+                                                         p.num_samples, seed=70 + f)
+                                        for f in range(frames)])))
+    g = eng.capture(rf)
+    for seed in (80, 90):
+        new = torch.from_numpy(np.stack([configs.noise_rf(p.num_transmits, arr.num_elements,
+                                                          p.num_samples, seed=seed + f)
+                                         for f in range(frames)])).cuda()
+        ref = eng.run(new).clone()
+        ref_db = eng.db.clone()
+        torch.cuda.synchronize()
+        rf.copy_(new)
+        got = g.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(got, ref)
+        assert torch.equal(eng.db, ref_db)
+    eng.close()
