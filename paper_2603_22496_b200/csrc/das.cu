@@ -134,6 +134,9 @@ typedef double das_total_t;
 #endif
 #define KKB_DAS_NT 256
 #define KKB_DAS_STAGE 1024
+#ifndef KKB_DAS_QUNROLL
+#define KKB_DAS_QUNROLL 1  // transmits per unrolled step of the tap loop
+#endif
 #ifndef KKB_DAS_MINB
 #define KKB_DAS_MINB 2  // CTAs per SM (register cap 128)
 #endif
@@ -400,6 +403,8 @@ k_das_tile(const DasArgs a) {
         const int nc = min(NCH, N - n0);
         const Entry *wb = win + buf * NCH * W;
         const int *lo_b = lo_s + buf * NCH;
+        constexpr int kQU = KKB_DAS_QUNROLL;
+#pragma unroll kQU
         for (int q = 0; q < nc; ++q) {
             const int n = n0 + q;
             const double2 tz = reinterpret_cast<const double2 *>(ltz_p + n * TZ)[zq];
