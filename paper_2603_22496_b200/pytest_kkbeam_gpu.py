@@ -20,6 +20,14 @@ def pytest_configure(config):
     _handle = install()
 
 
+def pytest_terminal_summary(terminalreporter):
+    from . import _lib
+
+    terminalreporter.write_line(
+        f"kkbeam kernels on the GPU: libkkb {_lib.version()}, "
+        f"{_lib.launch_count()} kernel launches ({_lib.LIB_PATH})")
+
+
 def pytest_unconfigure(config):
     if _handle is not None:
         _handle.restore()
