@@ -256,12 +256,16 @@ def test_multiset_compounding_matches_oracle(oracle, config1_rf, mode):
     eng.close()
 
 
-@pytest.mark.parametrize("interp,direct", [("linear", "0"), ("nearest", "0"), ("linear", "1")])
-def test_multiset_one_launch_equals_per_set_launches(monkeypatch, interp, direct):
+@pytest.mark.parametrize("cfg,interp,direct", [(1, "linear", "0"), (1, "nearest", "0"),
+                                                (1, "linear", "1"), (3, "linear", "0"),
+                                                (3, "nearest", "0")])
+def test_multiset_one_launch_equals_per_set_launches(monkeypatch, cfg, interp, direct):
     """kkb_kk_plan_run_sets (one launch, tables staged once) against one
     strided launch per set over the same shared traces, accumulating the
     intensity: IQ of every set, the compounded intensity and its max are
-    bit-identical (tiled kernels; and the per-pixel kernels, KKB_KK_DIRECT=1)."""
+    bit-identical (tiled kernels; and the per-pixel kernels, KKB_KK_DIRECT=1).
+    Config 1 x 3 frames runs the small-tile instance, config 3's hybrid sets x
+    4 frames the big-tile one (whose per-set launches run two frames per CTA)."""
     import ctypes
 
     torch = _torch()
@@ -270,12 +274,19 @@ def test_multiset_one_launch_equals_per_set_launches(monkeypatch, interp, direct
     from paper_2603_22496_b200.beamform import build_kk_luts_device
 
     monkeypatch.setenv("KKB_KK_DIRECT", direct)
-    w = configs.config1()
-    p, arr, g = w.params, w.array, w.grid
-    tmax = 10 * np.pi / 180
-    sets = [kb.uniform_vernier_angles(11, 5, tmax, 0), kb.confocal_angles(11, 3, tmax),
-            kb.uniform_vernier_angles(11, 2, tmax, 1)]
-    frames = 3
+    if cfg == 1:
+        w = configs.config1()
+        p, arr, g = w.params, w.array, w.grid
+        tmax = 10 * np.pi / 180
+        sets = [kb.uniform_vernier_angles(11, 5, tmax, 0), kb.confocal_angles(11, 3, tmax),
+                kb.uniform_vernier_angles(11, 2, tmax, 1)]
+        frames = 3
+    else:
+        w = configs.config3()
+        p, arr, g = w.extra_receive["hybrid"][0], w.array, w.grid
+        d = p.transmit_angles[1] - p.transmit_angles[0]
+        sets = [kb.confocal_angles(25, 3, 12 * d), kb.uniform_vernier_angles(25, 2, 12 * d, 0)]
+        frames = 4
     rf = torch.from_numpy(np.stack([configs.noise_rf(p.num_transmits, arr.num_elements,
                                                      p.num_samples, seed=50 + f)
                                     for f in range(frames)])).cuda()
