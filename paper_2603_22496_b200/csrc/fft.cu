@@ -31,7 +31,7 @@ namespace kkb {
 namespace {
 
 std::mutex g_fft_mu;
-std::map<int, FftPlan> g_fft_plans;  // per device 0 only; libkkb is one-device-per-process
+std::map<int, FftPlan> g_fft_plans;  // keyed by (T, device)
 
 }  // namespace
 
