@@ -866,6 +866,15 @@ __device__ __forceinline__ float db_of(float v, float mx, float floor_db) {
     return fmaxf(d, floor_db);
 }
 
+// 10 log10(v / mx) = 10 log10(2) (log2 v - log2 mx) with the MUFU log2 (abs
+// error ~2^-22 in log2, ~1e-6 dB); the same approximation on both terms keeps
+// the frame maximum at exactly 0 dB.  Frames whose max is not a normal float
+// take db_of.
+__device__ __forceinline__ float db_fast(float v, float l2mx, float floor_db) {
+    const float d = v > 0.f ? 3.01029995663981195f * (__log2f(v) - l2mx) : floor_db;
+    return fmaxf(d, floor_db);
+}
+
 __global__ void __launch_bounds__(256)
 k_log_compress(const float *__restrict__ inten, const unsigned *__restrict__ fmax, long long P,
                float floor_db, float *db, bool vec) {
@@ -875,13 +884,14 @@ k_log_compress(const float *__restrict__ inten, const unsigned *__restrict__ fma
     float *dst = db + (long long)f * P;
     const long long stride = (long long)gridDim.x * blockDim.x;
     const long long t0 = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-    if (vec) {
+    if (vec && mx >= 1.17549435e-38f) {
+        const float l2mx = __log2f(mx);
         const float4 *s4 = reinterpret_cast<const float4 *>(src);
         float4 *d4 = reinterpret_cast<float4 *>(dst);
         for (long long i = t0; i < P / 4; i += stride) {
             const float4 v = __ldcs(s4 + i);  // read once: stream past L2
-            __stcs(d4 + i, make_float4(db_of(v.x, mx, floor_db), db_of(v.y, mx, floor_db),
-                                       db_of(v.z, mx, floor_db), db_of(v.w, mx, floor_db)));
+            __stcs(d4 + i, make_float4(db_fast(v.x, l2mx, floor_db), db_fast(v.y, l2mx, floor_db),
+                                       db_fast(v.z, l2mx, floor_db), db_fast(v.w, l2mx, floor_db)));
         }
     } else {
         for (long long i = t0; i < P; i += stride) dst[i] = db_of(src[i], mx, floor_db);
