@@ -386,6 +386,8 @@ def run_gpu(args):
                "h2d_bytes_per_step": int(host_rf.numel() * 4),
                "d2h_bytes_per_step": int(host_iq.numel() * 8),
                "path": "KKEngine.run_host: pinned H2D float32 RF, decompose+kk on 2 streams, D2H IQ"}
+        # the leg's bound: host->device bytes per second it sustains (PCIe)
+        e2e["h2d_GBps_per_gpu"] = e2e["h2d_bytes_per_step"] / (world * F / e2e["value"]) / 1e9
         # same path fed int16-quantised RF (BASELINE config 2 sample format; exact)
         del host_rf
         scale = float(np.abs(base).max()) / 32767.0
