@@ -843,6 +843,8 @@ int kk_gather(const float2 *data, int N, int M, int T, const double *ltx, const 
     // receive angles per stage: bounded by the register staging and shared memory
     int MCH = std::max(1, std::min(M, stage / (FR * Wc)));
     while (MCH > 1 && kk_smem_bytes(N, M, Wc, MCH, linear, tz, tx, FR) > 200 * 1024) MCH = (MCH + 1) / 2;
+    if (const char *fm = getenv("KKB_KK_MCH"))  // test hook: fewer receive angles per stage
+        MCH = std::max(1, std::min(MCH, atoi(fm)));
     const size_t sm = kk_smem_bytes(N, M, Wc, MCH, linear, tz, tx, FR);
     a.W = Wc;
     a.MCH = MCH;

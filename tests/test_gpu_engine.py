@@ -256,10 +256,11 @@ def test_multiset_compounding_matches_oracle(oracle, config1_rf, mode):
     eng.close()
 
 
-@pytest.mark.parametrize("cfg,interp,direct", [(1, "linear", "0"), (1, "nearest", "0"),
-                                                (1, "linear", "1"), (3, "linear", "0"),
-                                                (3, "nearest", "0")])
-def test_multiset_one_launch_equals_per_set_launches(monkeypatch, cfg, interp, direct):
+@pytest.mark.parametrize("cfg,interp,direct,mch", [(1, "linear", "0", ""), (1, "nearest", "0", ""),
+                                                    (1, "linear", "1", ""), (1, "linear", "0", "2"),
+                                                    (3, "linear", "0", ""), (3, "nearest", "0", "1"),
+                                                    (5, "linear", "0", "")])
+def test_multiset_one_launch_equals_per_set_launches(monkeypatch, cfg, interp, direct, mch):
     """kkb_kk_plan_run_sets (one launch, tables staged once) against one
     strided launch per set over the same shared traces, accumulating the
     intensity: IQ of every set, the compounded intensity and its max are
@@ -274,6 +275,8 @@ def test_multiset_one_launch_equals_per_set_launches(monkeypatch, cfg, interp, d
     from paper_2603_22496_b200.beamform import build_kk_luts_device
 
     monkeypatch.setenv("KKB_KK_DIRECT", direct)
+    if mch:  # sets spanning several receive chunks per stage
+        monkeypatch.setenv("KKB_KK_MCH", mch)
     if cfg == 1:
         w = configs.config1()
         p, arr, g = w.params, w.array, w.grid
@@ -281,12 +284,18 @@ def test_multiset_one_launch_equals_per_set_launches(monkeypatch, cfg, interp, d
         sets = [kb.uniform_vernier_angles(11, 5, tmax, 0), kb.confocal_angles(11, 3, tmax),
                 kb.uniform_vernier_angles(11, 2, tmax, 1)]
         frames = 3
-    else:
+    elif cfg == 3:
         w = configs.config3()
         p, arr, g = w.extra_receive["hybrid"][0], w.array, w.grid
         d = p.transmit_angles[1] - p.transmit_angles[0]
         sets = [kb.confocal_angles(25, 3, 12 * d), kb.uniform_vernier_angles(25, 2, 12 * d, 0)]
         frames = 4
+    else:  # config 5 geometry: wide windows, so each set spans several receive chunks
+        w = configs.config5()
+        p, arr, g = w.params, w.array, w.grid
+        tmax = 15 * np.pi / 180
+        sets = [kb.confocal_angles(31, 9, tmax), kb.uniform_vernier_angles(31, 7, tmax, 0)]
+        frames = 1
     rf = torch.from_numpy(np.stack([configs.noise_rf(p.num_transmits, arr.num_elements,
                                                      p.num_samples, seed=50 + f)
                                     for f in range(frames)])).cuda()
