@@ -645,17 +645,17 @@ static int decomposer_run(kkb_decomposer *p, const void *rf, int in_kind, int n_
             rf_c = (const char *)conv;
         }
         if (i16_direct) {
-            st = fft_r2c_ct(rf_c, 1, (long long)F * N * L, T, X, ldk, K, nullptr, plan.tws, cs);
+            st = fft_r2c_ct(rf_c, 1, (long long)F * N * L, T, X, ldk, K, nullptr, plan.tws, cs, L);
         } else if (plan.direct || plan.large) {
             // lengths without a single-CTA real plan: promote to complex first
             float2 *promo = nullptr;
             KKB_TRY_CUDA(cudaMallocAsync(&promo, sizeof(float2) * (size_t)F * N * L * T, cs),
                          "cudaMallocAsync(promote)");
-            st = fft_r2c((const float *)rf_c, (long long)F * N * L, T, X, ldk, K, nullptr, cs, promo);
+            st = fft_r2c((const float *)rf_c, (long long)F * N * L, T, X, ldk, K, nullptr, cs, promo, L);
             cudaFreeAsync(promo, cs);
         } else {
             st = fft_r2c((const float *)rf_c, (long long)F * N * L, T, X, ldk, K, nullptr, cs,
-                         nullptr);
+                         nullptr, L);
         }
         if (conv) cudaFreeAsync(conv, cs);
         if (st) return st;

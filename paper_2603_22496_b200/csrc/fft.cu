@@ -349,7 +349,7 @@ k_fft_c2c(const float2 *__restrict__ in, long long in_stride, int in_len,
 __global__ void __launch_bounds__(KKB_FFT_THREADS)
 k_fft_r2c_pairs(const float *__restrict__ in, long long ntraces, float2 *__restrict__ out,
                 long long out_stride, int K, const float *__restrict__ bin_scale, int G,
-                FftPlan p) {
+                FftPlan p, int grp) {
     extern __shared__ float2 smem[];
     const int T = p.T;
     float2 *a = smem;
@@ -358,9 +358,11 @@ k_fft_r2c_pairs(const float *__restrict__ in, long long ntraces, float2 *__restr
     load_twiddles(tw, p);
     const long long pair0 = (long long)blockIdx.x * G;
     const bool vec4 = (T & 3) == 0;
+    const long long ppg = (grp + 1) / 2;  // pairs per group (k_r2c's pairing rule)
     for (int g = 0; g < G; ++g) {
-        const long long r0 = 2 * (pair0 + g);
-        const bool l0 = r0 < ntraces, l1 = r0 + 1 < ntraces;
+        const long long pi = pair0 + g, gi = pi / ppg, q = pi - gi * ppg;
+        const long long r0 = gi * grp + 2 * q;
+        const bool l0 = r0 < ntraces, l1 = l0 && 2 * q + 1 < grp && r0 + 1 < ntraces;
         const float *x0 = in + (l0 ? r0 : 0) * T;
         const float *x1 = in + (l1 ? r0 + 1 : 0) * T;
         if (vec4) {
@@ -381,9 +383,10 @@ k_fft_r2c_pairs(const float *__restrict__ in, long long ntraces, float2 *__restr
     __syncthreads();
     float2 *res = stockham(a, b, G, p, tw);
     for (int g = 0; g < G; ++g) {
-        const long long r0 = 2 * (pair0 + g);
+        const long long pi = pair0 + g, gi = pi / ppg, q = pi - gi * ppg;
+        const long long r0 = gi * grp + 2 * q;
         if (r0 >= ntraces) break;
-        const bool has1 = r0 + 1 < ntraces;
+        const bool has1 = 2 * q + 1 < grp && r0 + 1 < ntraces;
         float2 *o0 = out + r0 * out_stride;
         float2 *o1 = out + (r0 + 1) * out_stride;
         for (int k = threadIdx.x; k < K; k += blockDim.x) {
@@ -589,8 +592,10 @@ int fft_c2c_scatter(const float2 *in, long long in_stride, int in_len, int out_l
 }
 
 int fft_r2c(const float *in, long long ntraces, int T, float2 *out, long long out_stride, int K,
-            const float *bin_scale, cudaStream_t s, float2 *scratch_c2c) {
+            const float *bin_scale, cudaStream_t s, float2 *scratch_c2c, long long group_rows) {
     if (ntraces <= 0) return KKB_OK;
+    // pairing groups; the whole batch as one group pairs like groups of 2
+    const int grp = group_rows > 0 && group_rows <= 0x7fffffffLL ? (int)group_rows : 2;
     FftPlan p;
     int st = get_fft_plan(T, &p);
     if (st) return st;
@@ -609,14 +614,14 @@ int fft_r2c(const float *in, long long ntraces, int T, float2 *out, long long ou
         return fft_c2c(scratch_c2c, T, T, out, out_stride, K, ntraces, T, false, 1.0f, s);
     }
     if (fft_ct_supported(T) && g_use_ct)
-        return fft_r2c_ct(in, 0, ntraces, T, out, out_stride, K, bin_scale, p.tws, s);
+        return fft_r2c_ct(in, 0, ntraces, T, out, out_stride, K, bin_scale, p.tws, s, grp);
     int G = traces_per_cta(T);
     int sm = smem_bytes(T, G);
     st = ensure_smem((const void *)k_fft_r2c_pairs, sm);
     if (st) return st;
-    long long npairs = (ntraces + 1) / 2;
+    long long npairs = ceil_div(ntraces, grp) * ((grp + 1) / 2);
     k_fft_r2c_pairs<<<(unsigned)ceil_div(npairs, G), KKB_FFT_THREADS, sm, s>>>(
-        in, ntraces, out, out_stride, K, bin_scale, G, p);
+        in, ntraces, out, out_stride, K, bin_scale, G, p, grp);
     KKB_CHECK_LAUNCH("k_fft_r2c_pairs");
     return KKB_OK;
 }

@@ -44,8 +44,10 @@ int fft_c2c(const float2 *in, long long in_stride, int in_len, float2 *out, long
             int out_len, long long ntraces, int T, bool inverse, float scale, cudaStream_t s);
 
 // Batched real-input FFT: bins [0, K) of each row, times bin_scale[k].
+// Rows are paired (two real rows per complex transform) only within groups of
+// group_rows consecutive rows (0: the whole batch is one group).
 int fft_r2c(const float *in, long long ntraces, int T, float2 *out, long long out_stride, int K,
-            const float *bin_scale, cudaStream_t s, float2 *scratch_c2c);
+            const float *bin_scale, cudaStream_t s, float2 *scratch_c2c, long long group_rows = 0);
 
 // compile-time-specialised twins (fft_ct.cu)
 bool fft_ct_supported(int T);
@@ -54,7 +56,7 @@ void fft_ct_twiddles(int T, std::vector<float2> &out);
 // in_kind 0: float32 rows, 1: int16 rows (converted exactly to float32)
 int fft_r2c_ct(const void *in, int in_kind, long long ntraces, int T, float2 *out,
                long long out_stride, int K, const float *bin_scale, const float2 *tws,
-               cudaStream_t s);
+               cudaStream_t s, long long group_rows = 0);
 int fft_c2c_ct(const float2 *in, long long in_stride, int in_len, float2 *out, long long out_stride,
                int out_len, long long ntraces, int T, bool inverse, float scale, const float2 *tw,
                cudaStream_t s, const RowScatter *sc = nullptr);

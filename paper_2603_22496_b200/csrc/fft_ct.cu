@@ -259,17 +259,32 @@ __device__ __forceinline__ void stages12(float2 *buf, const float2 *__restrict__
 __device__ __forceinline__ float to_f(float x) { return x; }
 __device__ __forceinline__ float to_f(short x) { return (float)x; }  // exact
 
-// Real-pair forward FFT: rows 2p, 2p+1 of `in` (length T) -> bins [0, K) of
-// each row's spectrum at out + row*out_stride, times bin_scale[k].
-template <int T, typename InT>
+// Real-pair forward FFT: rows r0, r0+1 of `in` (length T) -> bins [0, K) of
+// each row's spectrum at out + row*out_stride, times bin_scale[k].  Rows are
+// paired only inside groups of `grp` rows (the L element traces of one
+// (frame, transmit)); an odd group's last row pairs with zeros.  A row's
+// rounding depends on its partner, so this keeps every trace independent of
+// batch size, frame position and the transmit split across GPUs.
+// Even groups pair exactly like the whole batch (rows 2p, 2p+1), so only odd
+// groups take the GROUPED instance.
+template <int T, typename InT, bool GROUPED = false>
 __global__ void __launch_bounds__(Plan<T>::NT)
 k_r2c(const InT *__restrict__ in, long long ntraces, float2 *__restrict__ out,
       long long out_stride, int K, const float *__restrict__ bin_scale,
-      const float2 *__restrict__ tw) {
+      const float2 *__restrict__ tw, int grp) {
     using P = Plan<T>;
     __shared__ __align__(16) float2 buf[T];
-    const long long r0 = 2 * (long long)blockIdx.x;
-    const bool l1 = r0 + 1 < ntraces;
+    long long r0;
+    bool l1;
+    if constexpr (GROUPED) {
+        const unsigned ppg = (unsigned)(grp + 1) >> 1, gi = blockIdx.x / ppg, q = blockIdx.x - gi * ppg;
+        r0 = (long long)gi * grp + 2 * q;
+        if (r0 >= ntraces) return;
+        l1 = (int)(2 * q + 1) < grp && r0 + 1 < ntraces;
+    } else {
+        r0 = 2 * (long long)blockIdx.x;
+        l1 = r0 + 1 < ntraces;
+    }
     const InT *x0 = in + r0 * T;
     const InT *x1 = in + (l1 ? r0 + 1 : r0) * T;
     using S0 = Stage<T, P::NT, P::R0>;
@@ -426,14 +441,18 @@ void fft_ct_twiddles(int T, std::vector<float2> &out) {
 template <int T>
 static int launch_r2c(const void *in, int in_kind, long long ntraces, float2 *out,
                       long long out_stride, int K, const float *bin_scale, const float2 *tw,
-                      cudaStream_t s) {
-    const unsigned npairs = (unsigned)((ntraces + 1) / 2);
-    if (in_kind)
-        ct::k_r2c<T, short><<<npairs, ct::Plan<T>::NT, 0, s>>>(
-            reinterpret_cast<const short *>(in), ntraces, out, out_stride, K, bin_scale, tw);
-    else
-        ct::k_r2c<T, float><<<npairs, ct::Plan<T>::NT, 0, s>>>(
-            reinterpret_cast<const float *>(in), ntraces, out, out_stride, K, bin_scale, tw);
+                      cudaStream_t s, int grp) {
+    const unsigned npairs = (unsigned)(ceil_div(ntraces, grp) * ((grp + 1) / 2));
+    const bool g = grp & 1;
+    if (in_kind) {
+        auto fn = g ? ct::k_r2c<T, short, true> : ct::k_r2c<T, short, false>;
+        fn<<<npairs, ct::Plan<T>::NT, 0, s>>>(reinterpret_cast<const short *>(in), ntraces, out,
+                                              out_stride, K, bin_scale, tw, grp);
+    } else {
+        auto fn = g ? ct::k_r2c<T, float, true> : ct::k_r2c<T, float, false>;
+        fn<<<npairs, ct::Plan<T>::NT, 0, s>>>(reinterpret_cast<const float *>(in), ntraces, out,
+                                              out_stride, K, bin_scale, tw, grp);
+    }
     KKB_CHECK_LAUNCH("k_fft_r2c_ct");
     return KKB_OK;
 }
@@ -461,14 +480,16 @@ static int launch_c2c(const float2 *in, long long in_stride, int in_len, float2 
 
 int fft_r2c_ct(const void *in, int in_kind, long long ntraces, int T, float2 *out,
                long long out_stride, int K, const float *bin_scale, const float2 *tw,
-               cudaStream_t s) {
+               cudaStream_t s, long long group_rows) {
     if (ntraces <= 0) return KKB_OK;
-    if ((ntraces + 1) / 2 > 0x7fffffffLL) return KKB_ERR_UNSUPPORTED;
+    // pairing groups; the whole batch as one group pairs like groups of 2
+    const int grp = group_rows > 0 && group_rows <= 0x7fffffffLL ? (int)group_rows : 2;
+    if (ceil_div(ntraces, grp) * ((grp + 1) / 2) > 0x7fffffffLL) return KKB_ERR_UNSUPPORTED;
     switch (T) {
-        case 1024: return launch_r2c<1024>(in, in_kind, ntraces, out, out_stride, K, bin_scale, tw, s);
-        case 1536: return launch_r2c<1536>(in, in_kind, ntraces, out, out_stride, K, bin_scale, tw, s);
-        case 2048: return launch_r2c<2048>(in, in_kind, ntraces, out, out_stride, K, bin_scale, tw, s);
-        case 4096: return launch_r2c<4096>(in, in_kind, ntraces, out, out_stride, K, bin_scale, tw, s);
+        case 1024: return launch_r2c<1024>(in, in_kind, ntraces, out, out_stride, K, bin_scale, tw, s, grp);
+        case 1536: return launch_r2c<1536>(in, in_kind, ntraces, out, out_stride, K, bin_scale, tw, s, grp);
+        case 2048: return launch_r2c<2048>(in, in_kind, ntraces, out, out_stride, K, bin_scale, tw, s, grp);
+        case 4096: return launch_r2c<4096>(in, in_kind, ntraces, out, out_stride, K, bin_scale, tw, s, grp);
     }
     return KKB_ERR_UNSUPPORTED;
 }

@@ -376,3 +376,25 @@ def test_engine_graph_replay_equals_eager(cfg):
         assert torch.equal(got, ref)
         assert torch.equal(eng.db, ref_db)
     eng.close()
+
+
+@pytest.mark.parametrize("T", [1536, 1000, 4099])
+def test_decomposition_odd_element_count_is_position_independent(T):
+    """Odd element counts: the real-pair FFT pairs rows only within one
+    (frame, transmit), so every frame of a batch equals its own single-frame
+    decomposition bit for bit, whatever its position."""
+    torch = _torch()
+    arr = kb.TransducerArray(63, 0.3e-3, 5e6, 20e6, 0.6)
+    params = kb.AcquisitionParams(C, np.linspace(-0.15, 0.15, 5), T)
+    rx = kb.uniform_vernier_angles(5, 3, 0.15, 0)
+    grid = kb.ImageGrid(-2e-3, 3e-3, 0.1e-3, 0.1e-3, 8, 8)
+    frames = 3
+    rf = torch.from_numpy(np.stack([configs.noise_rf(5, 63, T, seed=60 + f)
+                                    for f in range(frames)])).cuda()
+    eng = kb.KKEngine(arr, params, rx, grid, frames=frames, want_db=False)
+    batch = eng.decompose(rf).clone()
+    for f in range(frames):
+        one = eng.decompose(rf[f:f + 1].contiguous(), n_frames=1).clone()
+        torch.cuda.synchronize()
+        assert torch.equal(one[0], batch[f]), f
+    eng.close()

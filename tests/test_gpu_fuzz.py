@@ -4,6 +4,8 @@ modes and weights drawn at random (edge sizes included: 1 transmit, 1 receive
 angle, 1-pixel rows), so the tiled kernels, their fallbacks and the window
 sizing meet geometries the fixed configs do not."""
 
+import os
+
 import numpy as np
 import pytest
 
@@ -13,6 +15,9 @@ pytestmark = pytest.mark.gpu
 
 import paper_2603_22496_b200 as kb  # noqa: E402
 
+# KKB_FUZZ_SCALE=k multiplies every case count (a long sweep: scripts/README)
+_SCALE = max(1, int(os.environ.get("KKB_FUZZ_SCALE", "1")))
+
 
 def _sym(rng, m, amax):
     half = np.sort(rng.uniform(0.0, amax, m // 2))
@@ -20,7 +25,7 @@ def _sym(rng, m, amax):
     return ang
 
 
-@pytest.mark.parametrize("seed", range(40))
+@pytest.mark.parametrize("seed", range(40 * _SCALE))
 def test_kk_random_geometry(oracle, seed):
     rng = np.random.default_rng(1000 + seed)
     n_tx = int(rng.integers(1, 10))
@@ -52,7 +57,7 @@ def test_kk_random_geometry(oracle, seed):
         assert rel_l2(got, ref) <= 1e-5, (seed, n_tx, m_rx, T, nx, nz)
 
 
-@pytest.mark.parametrize("seed", range(20))
+@pytest.mark.parametrize("seed", range(20 * _SCALE))
 def test_das_random_geometry(oracle, seed):
     rng = np.random.default_rng(2000 + seed)
     n_tx = int(rng.integers(1, 8))
@@ -85,7 +90,7 @@ def test_das_random_geometry(oracle, seed):
         assert rel_l2(got, ref) <= 1e-5, (seed, n_tx, L, T, nx, nz)
 
 
-@pytest.mark.parametrize("seed", range(10))
+@pytest.mark.parametrize("seed", range(10 * _SCALE))
 def test_decomposition_random_geometry(oracle, seed):
     # analytic_signal + compress (the accuracy path) and the batched engine
     # decomposition on random element counts, lengths and angle sets
@@ -103,7 +108,13 @@ def test_decomposition_random_geometry(oracle, seed):
     rf = rng.standard_normal((n_tx, L, T)).astype(np.float32)
     ref = oracle.decompose_f64(rf, fs, arr.positions, rx.angles, C)
     an = kb.analytic_signal(kb.RFVolume(rf, arr, params))
-    got = kb.compress(an, rx, last_used_sample=0).data
+    guard = kb.guard_band_samples(arr.aperture, float(np.abs(rx.angles).max()), fs, C)
+    if guard > T:  # the reference's guard-band check fires even for sample 0
+        from paper_2603_22496_b200.errors import GuardBandError
+
+        with pytest.raises(GuardBandError):
+            kb.compress(an, rx, last_used_sample=0)
+    got = kb.compress(an, rx, last_used_sample=0 if guard <= T else None).data
     assert rel_l2(got, ref) <= 1e-5, (seed, n_tx, L, T, m_rx)
     grid = kb.ImageGrid(-1e-3, 2e-3, 0.1e-3, 0.1e-3, 4, 4)
     eng = kb.KKEngine(arr, params, rx, grid, frames=2, want_db=False)
@@ -112,3 +123,84 @@ def test_decomposition_random_geometry(oracle, seed):
     tr = eng.traces.cpu().numpy()
     assert rel_l2(tr[0], ref) <= 1e-5 and np.array_equal(tr[0], tr[1]), (seed, n_tx, L, T, m_rx)
     eng.close()
+
+
+@pytest.mark.parametrize("seed", range(16 * _SCALE))
+def test_kk_batched_and_multiset_random(seed):
+    """Kernel-level properties on random geometries large enough for the
+    big-tile, two-frames-per-CTA instance: a batch of F frames equals F
+    single-frame launches bit for bit, and one multi-set launch over a random
+    partition of the receive angles equals one launch per set (per-set tables,
+    intensities accumulated) bit for bit."""
+    import ctypes
+
+    import torch
+
+    from paper_2603_22496_b200 import _device as dev
+    from paper_2603_22496_b200 import _lib
+    from paper_2603_22496_b200.beamform import build_kk_luts_device
+
+    rng = np.random.default_rng(4000 + seed)
+    n_tx = int(rng.integers(1, 12))
+    m_rx = int(rng.integers(2, 14))
+    T = int(rng.choice([256, 1000, 1024, 1536, 2048]))
+    nx, nz = int(rng.integers(60, 300)), int(rng.integers(60, 300))
+    frames = int(rng.integers(2, 6))
+    fs = float(rng.uniform(10e6, 40e6))
+    tx = rng.uniform(-0.3, 0.3, n_tx)
+    rx = rng.uniform(-0.35, 0.35, m_rx)
+    dx, dz = float(rng.uniform(0.02e-3, 0.15e-3)), float(rng.uniform(0.02e-3, 0.15e-3))
+    grid = kb.ImageGrid(float(rng.uniform(-5e-3, 0)), float(rng.uniform(1e-3, 10e-3)), dx, dz, nx, nz)
+    linear = int(rng.integers(0, 2))
+    shift = float(rng.uniform(-40, 10))
+    w = rng.uniform(0.2, 2.0, m_rx)
+    data = torch.complex(torch.randn(frames, n_tx, m_rx, T, generator=torch.Generator().manual_seed(seed)),
+                         torch.randn(frames, n_tx, m_rx, T)).to(torch.complex64).cuda()
+    P = nx * nz
+    s = dev.stream_handle()
+
+    def plan(angles, weights):
+        luts = build_kk_luts_device(grid, tx, angles, C)
+        wd = dev.to_device(np.ascontiguousarray(weights))
+        kp = ctypes.c_void_p()
+        _lib.call("kkb_kk_plan_create", dev.ptr(luts["lut_tx_x"]), dev.ptr(luts["lut_tx_z"]),
+                  dev.ptr(luts["lut_rx_x"]), dev.ptr(luts["lut_rx_z"]), n_tx, len(angles), T, nx,
+                  nz, dev.ptr(wd), fs, shift, linear, s, ctypes.byref(kp))
+        return kp, (luts, wd)
+
+    kp, keep = plan(rx, w)
+    batch = torch.empty((frames, nx, nz), dtype=torch.complex64, device="cuda")
+    _lib.call("kkb_kk_plan_run", kp, dev.ptr(data), frames, n_tx * m_rx * T, dev.ptr(batch),
+              _lib.KKB_OUT_C64, P, None, None, s)
+    single = torch.empty_like(batch)
+    for f in range(frames):
+        _lib.call("kkb_kk_plan_run", kp, dev.ptr(data[f]), 1, 0, dev.ptr(single[f]),
+                  _lib.KKB_OUT_C64, P, None, None, s)
+    torch.cuda.synchronize()
+    assert torch.equal(batch, single), (seed, n_tx, m_rx, T, nx, nz, frames)
+
+    # random partition of the receive angles into 1..4 contiguous sets
+    nsets = int(rng.integers(1, min(4, m_rx) + 1))
+    cuts = np.sort(rng.choice(np.arange(1, m_rx), nsets - 1, replace=False)) if nsets > 1 else []
+    bounds = [0, *[int(c) for c in cuts], m_rx]
+    iq_sets = torch.empty((nsets, frames, nx, nz), dtype=torch.complex64, device="cuda")
+    inten = torch.empty((frames, nx, nz), dtype=torch.float32, device="cuda")
+    fmax = torch.zeros(frames, dtype=torch.int32, device="cuda")
+    b = (ctypes.c_int * len(bounds))(*bounds)
+    _lib.call("kkb_kk_plan_run_sets", kp, dev.ptr(data), frames, n_tx * m_rx * T, nsets, b,
+              dev.ptr(iq_sets), _lib.KKB_OUT_C64, P, frames * P, dev.ptr(inten), dev.ptr(fmax), 0, s)
+    ref_i = torch.empty_like(inten)
+    ref_m = torch.zeros_like(fmax)
+    for j in range(nsets):
+        a0, a1 = bounds[j], bounds[j + 1]
+        kj, kjk = plan(rx[a0:a1], w[a0:a1])
+        iq = torch.empty((frames, nx, nz), dtype=torch.complex64, device="cuda")
+        _lib.call("kkb_kk_plan_run_strided", kj, dev.ptr(data) + a0 * T * 8, frames,
+                  n_tx * m_rx * T, m_rx * T, dev.ptr(iq), _lib.KKB_OUT_C64, P, dev.ptr(ref_i),
+                  dev.ptr(ref_m) if j == nsets - 1 else None,
+                  _lib.KKB_RUN_ACCUMULATE_INTENSITY if j else 0, s)
+        torch.cuda.synchronize()
+        _lib.load().kkb_kk_plan_destroy(kj)
+        assert torch.equal(iq, iq_sets[j]), (seed, j, bounds)
+    assert torch.equal(ref_i, inten) and torch.equal(ref_m, fmax), (seed, bounds)
+    _lib.load().kkb_kk_plan_destroy(kp)

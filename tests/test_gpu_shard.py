@@ -93,8 +93,10 @@ def _full_traces(w, rf, frames):
     return tr
 
 
-@pytest.mark.parametrize("cfg,T,frames,world", [(4, None, 2, 3), (5, None, 1, 8), (1, 1000, 2, 3)])
-def test_transmit_sharded_stage1_scatter_assembles_every_trace_buffer(cfg, T, frames, world):
+@pytest.mark.parametrize("cfg,T,frames,world,odd_l", [(4, None, 2, 3, False), (5, None, 1, 8, False),
+                                                      (1, 1000, 2, 3, False), (1, None, 2, 3, True),
+                                                      (1, 1000, 3, 2, True)])
+def test_transmit_sharded_stage1_scatter_assembles_every_trace_buffer(cfg, T, frames, world, odd_l):
     # transmit-sharded stage 1 on one GPU: `world` "ranks" each decompose their
     # transmit block and the inverse FFT's epilogue stores the rows into all
     # ranks' full trace buffers (fused for the compile-time lengths, strided
@@ -111,6 +113,10 @@ def test_transmit_sharded_stage1_scatter_assembles_every_trace_buffer(cfg, T, fr
     p, arr = w.params, w.array
     if T is not None:
         p = kb.AcquisitionParams(p.sound_speed, p.transmit_angles, T, start_time=p.start_time)
+        w = configs.Workload(w.name, arr, p, w.receive, w.grid)
+    if odd_l:  # 63 elements: rows pair only within one (frame, transmit)
+        arr = kb.TransducerArray(63, arr.pitch, arr.center_frequency, arr.sampling_frequency,
+                                 arr.fractional_bandwidth)
         w = configs.Workload(w.name, arr, p, w.receive, w.grid)
     N, M, L, TT = p.num_transmits, w.receive.num_angles, arr.num_elements, p.num_samples
     rf = torch.from_numpy(np.stack([configs.noise_rf(N, L, TT, seed=30 + f)
