@@ -204,3 +204,40 @@ def test_kk_batched_and_multiset_random(seed):
         assert torch.equal(iq, iq_sets[j]), (seed, j, bounds)
     assert torch.equal(ref_i, inten) and torch.equal(ref_m, fmax), (seed, bounds)
     _lib.load().kkb_kk_plan_destroy(kp)
+
+
+@pytest.mark.parametrize("seed", range(12 * _SCALE))
+def test_simulator_random_geometry(oracle, seed):
+    """K8 forward simulator bit-identical to the C restatement of
+    _render_traces on random arrays, angles, windows, pulses and point sets
+    (echoes clipped at the window start included); a WindowOverflowError must
+    name a geometry whose latest echo really runs past the window."""
+    from paper_2603_22496_b200.errors import WindowOverflowError
+
+    rng = np.random.default_rng(5000 + seed)
+    L = int(rng.integers(2, 40))
+    fs = float(rng.uniform(10e6, 40e6))
+    fc = fs * float(rng.uniform(0.15, 0.3))
+    arr = kb.TransducerArray(L, float(rng.uniform(0.1e-3, 0.4e-3)), fc, fs, float(rng.uniform(0.3, 0.9)))
+    n_tx = int(rng.integers(1, 8))
+    tx = _sym(rng, n_tx, 0.3) if n_tx > 1 else np.array([float(rng.uniform(-0.2, 0.2))])
+    T = int(rng.choice([256, 500, 1024, 2048]))
+    t0 = float(rng.uniform(0, 4e-6))
+    params = kb.AcquisitionParams(C, tx, T, start_time=t0)
+    n_pts = int(rng.integers(1, 200))
+    zmax = (t0 + 0.8 * T / fs) * C / 2.2
+    ph = kb.Phantom(rng.uniform(-arr.aperture / 2, arr.aperture / 2, n_pts),
+                    rng.uniform(0.5e-3, max(1e-3, zmax), n_pts), rng.standard_normal(n_pts))
+    pulse = kb.make_pulse(fc, arr.fractional_bandwidth, fs)
+    spread = bool(rng.integers(0, 2))
+    try:
+        rf = kb.simulate_rf(arr, params, ph, pulse, geometric_spreading=spread)
+    except WindowOverflowError:
+        # an echo ends past the window: confirm one does (two-way path + half pulse)
+        two_way = max(((x * np.sin(a) + z * np.cos(a)) + np.hypot(x - u, z)) / C
+                      for x, z in zip(ph.x, ph.z) for a in tx for u in arr.positions)
+        assert (two_way - t0) * fs + (pulse.waveform.size - 1) // 2 > T - 2, seed
+        return
+    ref = oracle.simulate_rf(arr.positions, params.transmit_angles, C, T, t0, fs, ph.x, ph.z,
+                             ph.reflectivity, pulse.waveform, spread=spread)
+    assert np.array_equal(rf.data, ref), (seed, L, n_tx, T, n_pts)
