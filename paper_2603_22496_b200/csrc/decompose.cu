@@ -243,7 +243,9 @@ static int launch_contract(const float2 *X, long long ldx, const float2 *R, long
 #ifndef KKB_CS_NB6
 #define KKB_CS_NB6 2   // rows per thread of the 6-class instance (config 4: M = 11)
 #endif
-#define KKB_CS_LC 4
+#ifndef KKB_CS_LC
+#define KKB_CS_LC 4    // element pairs per cp.async stage
+#endif
 
 struct SymClasses {
     int P;
