@@ -138,7 +138,9 @@ def cpu_model() -> str:
 
 def cpu_pipeline_rate(w, seconds: float = 12.0, min_frames: int = 2, threads: int = 0):
     """Oracle port of the reference path on the host: frames/s over a bounded
-    sample (>= min_frames, ~`seconds` of work)."""
+    sample (>= min_frames, ~`seconds` of work).  The kk loop uses every host
+    core (threads=0), explicitly: torchrun exports OMP_NUM_THREADS=1."""
+    threads = threads or (os.cpu_count() or 1)
     from oracle import kkbeam_oracle as O
     from paper_2603_22496_b200 import configs
 
@@ -198,6 +200,22 @@ def run_reference(args):
 
 
 # ----------------------------------------------------------------- GPU arm
+def _init_dist(torch, dist, world, local):
+    """One process per GPU over NCCL.  KKB_DIST_BACKEND=gloo (a functional
+    check of the multi-rank code path on a one-GPU box: ranks share cuda:0,
+    their timings are not measurements) also wraps the device index."""
+    backend = os.environ.get("KKB_DIST_BACKEND", "nccl")
+    if backend != "nccl":
+        local = local % torch.cuda.device_count()
+    torch.cuda.set_device(local)
+    if world > 1:
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
+    return local
+
+
 def run_gpu(args):
     import torch
     import torch.distributed as dist
@@ -208,9 +226,7 @@ def run_gpu(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    local = _init_dist(torch, dist, world, local)
 
     w = _workload(args.config, args.frames)
     F = w.frames if args.config == 4 else args.frames
@@ -485,9 +501,7 @@ def run_gpu_rowblock(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    local = _init_dist(torch, dist, world, local)
     w = configs.config5()
     arr, p, rx, g = w.array, w.params, w.receive, w.grid
     rf = torch.from_numpy(configs.noise_rf(p.num_transmits, arr.num_elements, p.num_samples,
