@@ -84,16 +84,20 @@ int get_fft_plan(int T, FftPlan *out) {
         double a = -2.0 * M_PI * (double)k / (double)T;
         tw[k] = make_float2((float)cos(a), (float)sin(a));
     }
-    KKB_TRY_CUDA(cudaMalloc(&p.tw, sizeof(float2) * T), "cudaMalloc(twiddles)");
-    KKB_TRY_CUDA(cudaMemcpy(p.tw, tw.data(), sizeof(float2) * T, cudaMemcpyHostToDevice),
-                 "cudaMemcpy(twiddles)");
-    if (fft_ct_supported(T)) {
+    cudaError_t e = cudaMalloc(&p.tw, sizeof(float2) * T);
+    if (e == cudaSuccess)
+        e = cudaMemcpy(p.tw, tw.data(), sizeof(float2) * T, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess && fft_ct_supported(T)) {
         std::vector<float2> tws;
         fft_ct_twiddles(T, tws);
-        KKB_TRY_CUDA(cudaMalloc(&p.tws, sizeof(float2) * tws.size()), "cudaMalloc(stage twiddles)");
-        KKB_TRY_CUDA(cudaMemcpy(p.tws, tws.data(), sizeof(float2) * tws.size(),
-                                cudaMemcpyHostToDevice),
-                     "cudaMemcpy(stage twiddles)");
+        e = cudaMalloc(&p.tws, sizeof(float2) * tws.size());
+        if (e == cudaSuccess)
+            e = cudaMemcpy(p.tws, tws.data(), sizeof(float2) * tws.size(), cudaMemcpyHostToDevice);
+    }
+    if (e != cudaSuccess) {  // nothing cached: free what was allocated
+        cudaFree(p.tw);
+        cudaFree(p.tws);
+        return cuda_status(e, "FFT plan twiddles");
     }
     g_fft_plans[key] = p;
     *out = p;
