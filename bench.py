@@ -216,6 +216,22 @@ def _init_dist(torch, dist, world, local):
     return local
 
 
+def _l2_roofline(achieved_taps):
+    """SURVEY 8(d)'s gather roofline: 16 B of taps per pixel-pair over the
+    measured L2 read bandwidth (profiles/r01g_l2_bw.json, scripts/ubench/
+    l2_bw.cu; the driver's MEASURED_PEAKS.json has no L2 figure)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01g_l2_bw.json")) as f:
+            peak = float(json.load(f)["peak_L2_read_GBps"])
+    except (OSError, KeyError, ValueError):
+        return None
+    return {"kernel": "k_kk_gather", "bound": "l2", "achieved": achieved_taps, "peak": peak,
+            "unit": "GB/s", "frac": achieved_taps / peak,
+            "peak_kind": "measured (scripts/ubench/l2_bw.cu, 48 MB L2-resident set)",
+            "note": "frac > 1: the taps come from shared memory, each staged trace sample "
+                    "serving every pixel of the tile that reads it"}
+
+
 def run_gpu(args):
     import torch
     import torch.distributed as dist
@@ -458,6 +474,7 @@ def run_gpu(args):
                                 "algorithmic_bytes": "16 B of taps per pixel-pair (SURVEY 8d)",
                                 "pixel_pairs_per_s": pp_frame * fl / (kk_launch_ms / 1e3),
                                 "pixel_pairs_per_s_isolated": pp_frame * F / (kk_ms / 1e3)},
+            "l2_roofline": _l2_roofline(achieved_taps),
             "frame_roofline": {"bound": "hbm", "bytes_per_frame": frame_bytes,
                                "achieved": value / world * frame_bytes / 1e9, "peak": hbm_peak,
                                "unit": "GB/s", "frac": value / world * frame_bytes / 1e9 / hbm_peak,
