@@ -288,6 +288,15 @@ int kkb_kkrf_read_header(const char *path, kkb_kkrf_header *header);
 /* Reads `bytes` at `offset` into dst (host, or device when dst_is_device). */
 int kkb_kkrf_read_bytes(const char *path, long long offset, long long bytes, void *dst,
                         int dst_is_device, void *stream);
+/* Ensemble ingest (cli.py:110-128 reads one container per frame): frame f's
+ * frame_bytes payload at offsets_host[f] of paths_host[f] lands in device
+ * memory at dst + f*frame_bytes.  `threads` (1..64) reader threads, each with
+ * its own pinned double-buffered staging and stream, overlap the file reads
+ * with the H2D copies; the copies wait for work already queued on `stream`
+ * and are complete on return (synchronous). */
+int kkb_kkrf_read_ensemble(const char *const *paths_host, const long long *offsets_host,
+                           int n_files, long long frame_bytes, void *dst, int threads,
+                           void *stream);
 /* Writes head, angle tables (rx_host only for kind 2) and the payload
  * (host, or device when payload_is_device), replacing `path`. */
 int kkb_kkrf_write(const char *path, const kkb_kkrf_header *header, const double *tx_host,

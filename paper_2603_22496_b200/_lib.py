@@ -58,6 +58,7 @@ SIGNATURES = {
     "kkb_render_traces": [P, I, I, I, P, P, P, LL, P, P, P, D, D, D, P, I, D, I, P],
     "kkb_kkrf_read_header": [ctypes.c_char_p, P],
     "kkb_kkrf_read_bytes": [ctypes.c_char_p, LL, LL, P, I, P],
+    "kkb_kkrf_read_ensemble": [P, P, I, LL, P, I, P],
     "kkb_kkrf_write": [ctypes.c_char_p, P, P, P, P, LL, I, P],
     "kkb_max_f64": [P, LL, P, P],
     "kkb_gamma_match": [P, P, LL, D, D, D, P, P, P],

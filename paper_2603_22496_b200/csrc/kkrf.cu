@@ -19,9 +19,13 @@
 #include <sys/stat.h>
 #include <unistd.h>
 
+#include <atomic>
 #include <cerrno>
 #include <cstring>
 #include <mutex>
+#include <string>
+#include <thread>
+#include <vector>
 
 #include "common.cuh"
 
@@ -170,6 +174,100 @@ extern "C" int kkb_kkrf_read_bytes(const char *path, long long offset, long long
         done += (long long)n;
     }
     KKB_TRY_CUDA(cudaStreamSynchronize(s), "kkrf H2D sync");
+    return KKB_OK;
+}
+
+// Parallel ensemble ingest: `threads` reader threads, each with its own pair
+// of pinned 16 MiB staging buffers and its own stream, take files round-robin
+// (pread from the page cache / disk into pinned memory, async H2D into the
+// frame's slot).  Slots persist across calls (one ensemble read at a time).
+namespace {
+struct ReadSlot {
+    void *pinned[2] = {nullptr, nullptr};
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+    cudaStream_t st = nullptr;
+};
+std::mutex g_ens_mu;
+std::vector<ReadSlot> g_slots;
+
+int ensure_slots(int n, int dev) {
+    while ((int)g_slots.size() < n) {
+        ReadSlot r;
+        cudaSetDevice(dev);
+        for (int i = 0; i < 2; ++i) {
+            KKB_TRY_CUDA(cudaHostAlloc(&r.pinned[i], kChunk, cudaHostAllocDefault), "cudaHostAlloc(kkrf slot)");
+            KKB_TRY_CUDA(cudaEventCreateWithFlags(&r.ev[i], cudaEventDisableTiming), "event(kkrf slot)");
+        }
+        KKB_TRY_CUDA(cudaStreamCreateWithFlags(&r.st, cudaStreamNonBlocking), "stream(kkrf slot)");
+        g_slots.push_back(r);
+    }
+    return KKB_OK;
+}
+
+int read_one(ReadSlot &r, int &i, const char *path, long long offset, long long bytes, char *d) {
+    Fd f;
+    f.fd = open(path, O_RDONLY);
+    if (f.fd < 0) return io_error("open", path);
+    for (long long done = 0; done < bytes; ++i) {
+        const int k = i & 1;
+        const size_t n = (size_t)std::min<long long>((long long)kChunk, bytes - done);
+        if (i >= 2) KKB_TRY_CUDA(cudaEventSynchronize(r.ev[k]), "kkrf slot wait");
+        int rc = pread_full(f.fd, r.pinned[k], n, offset + done, path);
+        if (rc) return rc;
+        KKB_TRY_CUDA(cudaMemcpyAsync(d + done, r.pinned[k], n, cudaMemcpyHostToDevice, r.st), "kkrf H2D");
+        KKB_TRY_CUDA(cudaEventRecord(r.ev[k], r.st), "kkrf record");
+        done += (long long)n;
+    }
+    return KKB_OK;
+}
+}  // namespace
+
+extern "C" int kkb_kkrf_read_ensemble(const char *const *paths, const long long *offsets_host,
+                                      int n_files, long long frame_bytes, void *dst, int threads,
+                                      void *stream) {
+    if (!paths || !offsets_host || n_files < 0 || frame_bytes < 0 || (n_files && frame_bytes && !dst) ||
+        threads < 1 || threads > 64) {
+        set_error("kkrf_read_ensemble: bad argument (1 <= threads <= 64)");
+        return KKB_ERR_ARG;
+    }
+    if (!n_files || !frame_bytes) return KKB_OK;
+    std::lock_guard<std::mutex> lk(g_ens_mu);
+    int dev = 0;
+    KKB_TRY_CUDA(cudaGetDevice(&dev), "cudaGetDevice");
+    threads = std::min(threads, n_files);
+    int rc = ensure_slots(threads, dev);
+    if (rc) return rc;
+    // the destination may still be in use by work queued on the caller's stream
+    cudaEvent_t ready;
+    KKB_TRY_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming), "event(kkrf ready)");
+    cudaEventRecord(ready, as_stream(stream));
+    std::atomic<int> next{0}, first_err{0};
+    std::vector<std::string> err_msg(threads);
+    auto worker = [&](int t) {
+        cudaSetDevice(dev);
+        ReadSlot &r = g_slots[t];
+        cudaStreamWaitEvent(r.st, ready, 0);
+        int i = 0;
+        for (int f; (f = next.fetch_add(1)) < n_files && !first_err.load();) {
+            const int e = read_one(r, i, paths[f], offsets_host[f], frame_bytes,
+                                   static_cast<char *>(dst) + (size_t)f * frame_bytes);
+            if (e) {
+                int z = 0;
+                if (first_err.compare_exchange_strong(z, e)) err_msg[t] = kkb_last_error();
+            }
+        }
+        cudaStreamSynchronize(r.st);
+    };
+    std::vector<std::thread> pool;
+    for (int t = 1; t < threads; ++t) pool.emplace_back(worker, t);
+    worker(0);
+    for (auto &th : pool) th.join();
+    cudaEventDestroy(ready);
+    if (first_err.load()) {
+        for (auto &m : err_msg)
+            if (!m.empty()) set_error("%s", m.c_str());
+        return first_err.load();
+    }
     return KKB_OK;
 }
 

@@ -224,10 +224,12 @@ def read_container_device(path, stream=None) -> DeviceContainer:
     return DeviceContainer(ps.kind, out, params, array, receive, ps.fs)
 
 
-def read_ensemble_device(paths, stream=None):
+def read_ensemble_device(paths, stream=None, threads: int | None = None):
     """Frames stored one per KKRF file (same kind and geometry) -> one
     (F, N, channels, T) device tensor, e.g. the input of KKEngine.run.
-    Returns (tensor, metadata of the first file)."""
+    ``threads`` parallel readers (default: up to 8, one per file at most)
+    stream the files through pinned staging into HBM
+    (``kkb_kkrf_read_ensemble``).  Returns (tensor, metadata of the first file)."""
     from . import _device as dev
 
     paths = list(paths)
@@ -242,10 +244,13 @@ def read_ensemble_device(paths, stream=None):
     params, array, receive = _metadata(paths[0], first)
     out = _payload_tensor((len(paths),) + first.shape, first.dtype)
     frame_bytes = int(np.prod(first.shape)) * first.dtype.itemsize
-    base = dev.ptr(out)
-    for f, (p, ps) in enumerate(zip(paths, parsed)):
-        _lib.call("kkb_kkrf_read_bytes", os.fsencode(p), ps.payload_offset, frame_bytes,
-                  base + f * frame_bytes, 1, dev.stream_handle(stream))
+    names = [ctypes.c_char_p(os.fsencode(p)) for p in paths]
+    arr_p = (ctypes.c_char_p * len(names))(*names)
+    offs = (ctypes.c_longlong * len(parsed))(*[ps.payload_offset for ps in parsed])
+    n_threads = int(threads) if threads else min(8, len(paths), os.cpu_count() or 1)
+    _lib.call("kkb_kkrf_read_ensemble", ctypes.cast(arr_p, ctypes.c_void_p),
+              ctypes.cast(offs, ctypes.c_void_p), len(paths), frame_bytes, dev.ptr(out),
+              max(1, n_threads), dev.stream_handle(stream))
     return out, DeviceContainer(first.kind, None, params, array, receive, first.fs)
 
 

@@ -31,17 +31,28 @@ def test_device_read_write_roundtrip(tmp_path):
     assert open(out, "rb").read() == open(path, "rb").read()
 
 
-def test_ensemble_into_one_tensor(tmp_path):
+@pytest.mark.parametrize("threads", [None, 1, 2, 5])
+def test_ensemble_into_one_tensor(tmp_path, threads):
+    # several reader threads (kkb_kkrf_read_ensemble); frames larger than one
+    # 16 MiB staging chunk (T = 20011) exercise the double buffering per thread
     paths = []
     frames = []
-    for f in range(3):
+    for f in range(5):
         v = _volume(f, T=2048)
         paths.append(str(tmp_path / f"f{f}.kkrf"))
         rffile.write_container(paths[-1], v)
         frames.append(v.data)
-    t, meta = rffile.read_ensemble_device(paths)
-    assert tuple(t.shape) == (3, 2, 128, 2048)
+    t, meta = rffile.read_ensemble_device(paths, threads=threads)
+    assert tuple(t.shape) == (5, 2, 128, 2048)
     assert np.array_equal(dev.to_host(t), np.stack(frames))
+    big = []
+    for f in range(3):
+        v = _volume(10 + f, T=20011)
+        big.append(str(tmp_path / f"b{f}.kkrf"))
+        rffile.write_container(big[-1], v)
+        frames.append(v.data)
+    tb, _ = rffile.read_ensemble_device(big, threads=threads)
+    assert np.array_equal(dev.to_host(tb), np.stack(frames[5:]))
     other = _volume(9, T=1024)
     rffile.write_container(str(tmp_path / "odd.kkrf"), other)
     with pytest.raises(kb.FileFormatError, match="geometry differs"):
