@@ -186,7 +186,8 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * t / args.steps, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f32/f64 (complex64 traces, float64 index math, complex128 image)",
+        "vs_baseline": None, "dtype": "f32",
+        "dtype_detail": "complex64 stage 1 and traces, float64 delay-index math, complex128 image accumulation",
         "data": "synthetic (seeded noise RF, reference bench.noise_volume)",
         "config": {"workload": w.name, "frames_per_step": 2, "pixel_pairs_per_frame": pp},
         "pixel_pair_samples_per_s": value * pp,
@@ -446,7 +447,8 @@ def run_gpu(args):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None,
-            "dtype": "f32 (complex64 traces/IQ; float64 delay-index math)",
+            "dtype": "f32",
+            "dtype_detail": "complex64 spectra/traces/IQ, float32 taps and sums, float64 delay-index math",
             "data": "synthetic (seeded noise RF, shapes of BASELINE config 4)",
             "config": {"workload": w.name, "frames_per_rank": F, "N_tx": N, "M_rx": M,
                        "L_el": L, "T": T, "grid": [g.nx, g.nz],
@@ -563,7 +565,8 @@ def run_gpu_rowblock(args):
             "metric": METRIC, "value": 1e3 / ms_step, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-            "dtype": "f32 (complex64 traces/IQ; float64 delay-index math)",
+            "dtype": "f32",
+            "dtype_detail": "complex64 spectra/traces/IQ, float32 taps and sums, float64 delay-index math",
             "data": "synthetic (seeded noise RF, shapes of BASELINE config 5)",
             "config": {"workload": w.name, "frames_per_step": 1, "pixel_pairs_per_frame": pp,
                        "parallelism": f"row-block x{world}, stage 1 {args.stage1}"
