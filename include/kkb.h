@@ -114,7 +114,7 @@ int kkb_kk_plan_run_ex(kkb_kk_plan *p, const void *data, int n_frames, long long
  * [set_begin_host[j], set_begin_host[j+1]) (0 = first < ... < last = M).
  * Each set's image B_j is summed in the order a plan over that set alone
  * uses (bit-identical to it when both run the tiled kernel), stored at out + j*out_set_stride (+ f*out_frame_stride,
- * complex elements; out may be NULL), and intensity = sum_j |B_j|^2 in set
+ * complex elements; out may be NULL), and intensity (required) = sum_j |B_j|^2 in set
  * order (+ the existing intensity with KKB_RUN_ACCUMULATE_INTENSITY);
  * frame_max (zeroed) gets its per-frame max.  The tables are staged once
  * for all sets. */

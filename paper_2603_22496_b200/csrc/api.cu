@@ -242,9 +242,9 @@ extern "C" int kkb_kk_plan_run_sets(kkb_kk_plan *p, const void *data, int n_fram
                                     long long out_frame_stride, long long out_set_stride,
                                     float *intensity, unsigned int *frame_max, int flags,
                                     void *stream) {
-    if (!p || !set_begin_host || n_sets < 1 || n_sets > KKB_MAX_SETS ||
+    if (!p || !set_begin_host || !intensity || n_sets < 1 || n_sets > KKB_MAX_SETS ||
         (flags & ~KKB_RUN_ACCUMULATE_INTENSITY)) {
-        set_error("kk_plan_run_sets: 1 <= n_sets <= %d, known flags", KKB_MAX_SETS);
+        set_error("kk_plan_run_sets: intensity buffer, 1 <= n_sets <= %d, known flags", KKB_MAX_SETS);
         return KKB_ERR_ARG;
     }
     KKSets sets{};

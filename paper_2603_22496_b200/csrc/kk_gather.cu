@@ -291,7 +291,6 @@ __device__ __forceinline__ void store_iq(void *out, int kind, long long px, floa
 template <int WZ, int WX, int CX, bool LINEAR, int FR, bool MS = false>
 __global__ void __launch_bounds__(WZ *WX * 32, KKB_KK_MIN_CTAS)
 k_kk_gather(const KKArgs a) {
-    static_assert(!MS || FR == 1, "multi-set instances run one frame per CTA");
     constexpr int TZ = 8 * WZ;
     constexpr int TX = 8 * CX * WX;
     constexpr int NT = WZ * WX * 32;
@@ -430,12 +429,6 @@ k_kk_gather(const KKArgs a) {
         for (int p = 0; p < 2; ++p)
 #pragma unroll
             for (int q = 0; q < CX; ++q) accr[fr][p][q] = acci[fr][p][q] = 0.f;
-    float isum[2][CX];  // MS: running sum_j |B_j|^2
-#pragma unroll
-    for (int p = 0; p < 2; ++p)
-#pragma unroll
-        for (int q = 0; q < CX; ++q) isum[p][q] = 0.f;
-
     load_stage(0, 0, set_end);
     store_stage(0, set_end, 0);
     __syncthreads();
@@ -539,23 +532,42 @@ k_kk_gather(const KKArgs a) {
             }
         }
         if constexpr (MS) {
-            if (set_done) {  // image of this set, |B|^2 into the running intensity, reset
+            if (set_done) {
+                // image of this set; |B|^2 added to the intensity in global memory
+                // (the same float op order as one accumulating launch per set);
+                // after the last set, the frame max
+                const bool last = set + 1 == a.nsets;
 #pragma unroll
-                for (int p = 0; p < 2; ++p) {
-                    const int iz = iz0 + wz * 8 + p * 4 + zt;
+                for (int fr = 0; fr < FR; ++fr) {
+                    const int f = f0 + fr;
+                    float fmx = 0.f;
+                    if (f < a.n_frames) {
 #pragma unroll
-                    for (int r = 0; r < CX; ++r) {
-                        const int ix = ix0 + wx * 8 * CX + r * 8 + xt;
-                        const float vr = accr[0][p][r], vi = acci[0][p][r];
-                        const long long px = (long long)f0 * a.out_fs + (long long)ix * nz + iz;
-                        if (iz < nz && ix < nx) {
-                            if (a.out) store_iq(a.out, a.out_kind, set * a.out_set_stride + px, vr, vi);
-                            float base = isum[p][r];
-                            if (set == 0) base = (a.accum && a.inten) ? a.inten[px] : 0.f;
-                            isum[p][r] = vr * vr + vi * vi + base;
+                        for (int p = 0; p < 2; ++p) {
+                            const int iz = iz0 + wz * 8 + p * 4 + zt;
+#pragma unroll
+                            for (int r = 0; r < CX; ++r) {
+                                const int ix = ix0 + wx * 8 * CX + r * 8 + xt;
+                                if (iz < nz && ix < nx) {
+                                    const float vr = accr[fr][p][r], vi = acci[fr][p][r];
+                                    const long long px = (long long)f * a.out_fs + (long long)ix * nz + iz;
+                                    if (a.out) store_iq(a.out, a.out_kind, set * a.out_set_stride + px, vr, vi);
+                                    float I = vr * vr + vi * vi;
+                                    if (set > 0 || a.accum) I += a.inten[px];
+                                    a.inten[px] = I;
+                                    fmx = fmaxf(fmx, I);
+                                }
+                            }
                         }
-                        accr[0][p][r] = acci[0][p][r] = 0.f;
                     }
+                    if (last && a.fmax && f0 + fr < a.n_frames) {
+                        for (int o = 16; o > 0; o >>= 1) fmx = fmaxf(fmx, __shfl_xor_sync(0xffffffffu, fmx, o));
+                        if (lane == 0) atomicMax(a.fmax + f, __float_as_uint(fmx));
+                    }
+#pragma unroll
+                    for (int p = 0; p < 2; ++p)
+#pragma unroll
+                        for (int r = 0; r < CX; ++r) accr[fr][p][r] = acci[fr][p][r] = 0.f;
                 }
                 ++set;
             }
@@ -575,28 +587,7 @@ k_kk_gather(const KKArgs a) {
         ch = ch1;
     }
 
-    if constexpr (MS) {  // running intensity and its frame max
-        if (f0 >= a.n_frames) return;
-        float fmx = 0.f;
-#pragma unroll
-        for (int p = 0; p < 2; ++p) {
-            const int iz = iz0 + wz * 8 + p * 4 + zt;
-#pragma unroll
-            for (int r = 0; r < CX; ++r) {
-                const int ix = ix0 + wx * 8 * CX + r * 8 + xt;
-                if (iz < nz && ix < nx) {
-                    const long long px = (long long)f0 * a.out_fs + (long long)ix * nz + iz;
-                    if (a.inten) a.inten[px] = isum[p][r];
-                    fmx = fmaxf(fmx, isum[p][r]);
-                }
-            }
-        }
-        if (a.fmax) {
-            for (int o = 16; o > 0; o >>= 1) fmx = fmaxf(fmx, __shfl_xor_sync(0xffffffffu, fmx, o));
-            if (lane == 0) atomicMax(a.fmax + f0, __float_as_uint(fmx));
-        }
-        return;
-    }
+    if constexpr (MS) return;  // every set's epilogue ran inside the loop
 
     // epilogue: IQ (+ fused intensity and frame max), per frame
 #pragma unroll
@@ -838,7 +829,7 @@ int kk_gather(const float2 *data, int N, int M, int T, const double *ltx, const 
     // big tiles over a batch: KKB_KK_FR frames per CTA share the tables and the
     // index math of every tap (when a window block of FR frames fits a stage)
     const char *ffr = getenv("KKB_KK_FR1");  // test hook: one frame per CTA
-    const int FR = (!ms && !use_small && n_frames > 1 && KKB_KK_FR > 1 && KKB_KK_FR * Wc <= stage &&
+    const int FR = (!use_small && n_frames > 1 && KKB_KK_FR > 1 && KKB_KK_FR * Wc <= stage &&
                     !(ffr && ffr[0] == '1')) ? KKB_KK_FR : 1;
     // receive angles per stage: bounded by the register staging and shared memory
     int MCH = std::max(1, std::min(M, stage / (FR * Wc)));
@@ -851,6 +842,9 @@ int kk_gather(const float2 *data, int N, int M, int T, const double *ltx, const 
     if (ms) {
         if (use_small)
             return launch_tiled<KKB_KK_S_WZ, KKB_KK_S_WX, KKB_KK_S_CX, 1, true>(a, n_frames, sm, linear != 0, s);
+        if (FR > 1)
+            return launch_tiled<KKB_KK_WZ, KKB_KK_WX, KKB_KK_CX, KKB_KK_FR, true>(a, n_frames, sm,
+                                                                                linear != 0, s);
         return launch_tiled<KKB_KK_WZ, KKB_KK_WX, KKB_KK_CX, 1, true>(a, n_frames, sm, linear != 0, s);
     }
     if (use_small)
