@@ -127,7 +127,7 @@ static int das_gather_direct(const float2 *data, int n_tx, int n_el, int n_t, co
 #define KKB_DAS_CX 2  // pixel columns per lane
 #endif
 #define KKB_DAS_TX (16 * KKB_DAS_CX)
-#if KKB_DAS_CX > 2
+#if KKB_DAS_CX > 2 || defined(KKB_DAS_FLOAT_TOTAL)
 typedef float das_total_t;  // 8 pixels per lane: float totals keep registers < 128
 #else
 typedef double das_total_t;
