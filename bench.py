@@ -20,6 +20,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import statistics
 import subprocess
@@ -385,6 +386,10 @@ def run_gpu(args):
     s1_bytes = F * (4.0 * N * L * T + 2 * 8.0 * N * L * ldk + 2 * 8.0 * N * M * ldk + 8.0 * N * M * T)
     s1_min = F * (4.0 * N * L * T + 8.0 * N * M * T)
     s1_achieved = s1_bytes / (dec_ms / 1e3) / 1e9
+    # SURVEY 8(d) flop units: contraction 8*N*L*M*K, FFTs 2.5*N*L*T*log2 T + 5*N*M*T*log2 T
+    K = T // 2 + 1
+    s1_flops = F * (8.0 * N * L * M * K + 2.5 * N * L * T * math.log2(T) + 5.0 * N * M * T * math.log2(T))
+    fp32_peak = 148 * 128 * 2 * (clk.get("sm_mhz") or 1965.0) * 1e6 / 1e12  # TFLOP/s, derived
     frame_bytes = 4.0 * N * L * T + 2 * 8.0 * N * M * T + 8.0 * P + 8.0 * (g.nx + g.nz) * (N + M)
 
     # ---- end to end through the public API: pinned host RF in, host IQ out ----
@@ -487,6 +492,9 @@ def run_gpu(args):
                                 "frac": s1_achieved / hbm_peak, "ms": dec_ms,
                                 "bytes_per_step": s1_bytes,
                                 "compulsory_frac": s1_min / (dec_ms / 1e3) / 1e9 / hbm_peak,
+                                "tflops": s1_flops / (dec_ms / 1e3) / 1e12,
+                                "fp32_peak_tflops": fp32_peak,
+                                "flop_frac": s1_flops / (dec_ms / 1e3) / 1e12 / fp32_peak,
                                 "algorithmic_bytes": "RF in + spectra write/read + contracted "
                                                      "bins write/read + traces out (three-kernel "
                                                      "structure); compulsory_frac counts RF in + "
