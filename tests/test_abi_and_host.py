@@ -234,3 +234,18 @@ def test_no_device_means_loud_failure(monkeypatch):
     with pytest.raises(DeviceError):
         kb.analytic_signal(kb.RFVolume(np.zeros((1, 4, 64)), kb.TransducerArray(
             4, 0.23e-3, 5.2e6, 20.83e6, 0.67), kb.AcquisitionParams(C, [0.0], 64)))
+
+
+def test_bench_roofline_helpers_read_the_committed_profiles():
+    """bench.py's roofline denominators come from committed measurements
+    (profiles/): the L2 read bandwidth and the gather's ncu DRAM traffic."""
+    import importlib.util
+
+    spec = importlib.util.spec_from_file_location("bench_mod", os.path.join(ROOT, "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    l2 = bench._l2_roofline(24000.0)
+    assert l2["bound"] == "l2" and 16000 < l2["peak"] < 20000 and 1.2 < l2["frac"] < 1.6
+    t = bench._gather_traffic(400)
+    assert 0.3e9 < t < 0.9e9
+    assert bench._gather_traffic(200) == t / 2
