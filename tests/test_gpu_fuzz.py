@@ -233,10 +233,13 @@ def test_simulator_random_geometry(oracle, seed):
     try:
         rf = kb.simulate_rf(arr, params, ph, pulse, geometric_spreading=spread)
     except WindowOverflowError:
-        # an echo ends past the window: confirm one does (two-way path + half pulse)
-        two_way = max(((x * np.sin(a) + z * np.cos(a)) + np.hypot(x - u, z)) / C
-                      for x, z in zip(ph.x, ph.z) for a in tx for u in arr.positions)
-        assert (two_way - t0) * fs + (pulse.waveform.size - 1) // 2 > T - 2, seed
+        # the reference's rule (simulate.py:246-264): latest transmit arrival +
+        # farther aperture edge, minus t0, in samples, plus the whole pulse >= T
+        tau = max((x * np.sin(a) + z * np.cos(a)) / C for x, z in zip(ph.x, ph.z) for a in tx)
+        need = max((max((x * np.sin(a) + z * np.cos(a)) / C for a in tx)
+                    + max(np.hypot(x - arr.positions[0], z), np.hypot(x - arr.positions[-1], z)) / C
+                    - t0) * fs + pulse.waveform.size for x, z in zip(ph.x, ph.z))
+        assert tau > 0 and need >= T, (seed, need, T)
         return
     ref = oracle.simulate_rf(arr.positions, params.transmit_angles, C, T, t0, fs, ph.x, ph.z,
                              ph.reflectivity, pulse.waveform, spread=spread)
