@@ -50,8 +50,13 @@ const char *kkb_last_error(void);
 int kkb_device_info(int *sm_count, int *cc_major, int *cc_minor);
 /* Number of kernel launches this library issued since load (all threads). */
 long long kkb_launch_count(void);
-/* Reads and clears the device-side error word (synchronous). */
+/* Reads and clears the device-side error word (synchronous): a bit mask of
+ * KKB_DEVERR_* raised by kernels since the last call (0 = none). */
 int kkb_take_device_error(int *flag);
+/* K5: a tap's window index fell outside the trace window staged for its tile
+ * (the index is clamped to the last staged entry; the image is then wrong).
+ * The window sizing makes this impossible; the flag proves it at run time. */
+#define KKB_DEVERR_KK_WINDOW 1
 
 /* ------------------------------------------------------------ K4: delay tables
  * Replaces build_kk_luts / _tx_tables (beamform.py:121-126,159-175):
@@ -148,6 +153,19 @@ int kkb_kk_plan_run_strided(kkb_kk_plan *p, const void *data, int n_frames,
                             unsigned int *frame_max, int flags, void *stream);
 /* trace window (samples per pair) the plan stages in shared memory */
 int kkb_kk_plan_window(const kkb_kk_plan *p);
+/* K5 instance the last kk launch of this process dispatched to (any plan,
+ * any thread): the per-pixel kernel, or the tiled kernel with 16x16 / 32x32
+ * / 32x64 pixel tiles, the last one with one or KKB_KK_FR (2) frames per CTA;
+ * KKB_KK_INST_SETS is or-ed in for the multi-set form.  -1 before any launch.
+ * Selection: the largest tile whose grid fills the SMs, environment override
+ * KKB_KK_INST=direct|small|mid|big|big_fr (tests, measurements). */
+#define KKB_KK_INST_DIRECT 0
+#define KKB_KK_INST_SMALL 1
+#define KKB_KK_INST_MID 2
+#define KKB_KK_INST_BIG 3
+#define KKB_KK_INST_BIG_FR 4
+#define KKB_KK_INST_SETS 16
+int kkb_kk_last_instance(void);
 int kkb_kk_plan_destroy(kkb_kk_plan *p);
 
 /* Diagnostic twin of K5's index math (same device function): writes the tap

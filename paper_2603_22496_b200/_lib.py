@@ -40,6 +40,7 @@ SIGNATURES = {
     "kkb_kk_plan_run_scatter": [P, P, I, LL, P, I, LL, I, LL, P],
     "kkb_kk_plan_run_sets": [P, P, I, LL, I, P, P, I, LL, LL, P, P, I, P],
     "kkb_kk_plan_window": [P],
+    "kkb_kk_last_instance": [],
     "kkb_kk_plan_destroy": [P],
     "kkb_kk_taps": [P, P, P, P, I, I, I, I, I, D, D, I, P, P],
     "kkb_das": [P, I, I, I, P, P, P, I, P, P, P, P, P, D, P, D, D, I, I, I, P, I, P],
@@ -102,6 +103,11 @@ KKB_RUN_ACCUMULATE_INTENSITY = 1
 KKB_MAX_DST = 8  # destinations of kkb_kk_plan_run_scatter
 KKB_MAX_SETS = 8  # receive sets of kkb_kk_plan_run_sets
 KKB_OUT_C128 = 1
+KKB_DEVERR_KK_WINDOW = 1
+# K5 instances (kkb_kk_last_instance)
+KKB_KK_INST_DIRECT, KKB_KK_INST_SMALL, KKB_KK_INST_MID, KKB_KK_INST_BIG, KKB_KK_INST_BIG_FR = range(5)
+KKB_KK_INST_SETS = 16
+KKB_KK_INST_NAMES = {0: "direct", 1: "small", 2: "mid", 3: "big", 4: "big_fr"}
 
 _lib = None
 
@@ -142,6 +148,19 @@ def last_error() -> str:
 def launch_count() -> int:
     """Kernel launches issued by libkkb in this process so far."""
     return int(load().kkb_launch_count())
+
+
+def last_instance() -> int:
+    """K5 instance the last gather launch of this process dispatched to
+    (KKB_KK_INST_*; or-ed with KKB_KK_INST_SETS for the multi-set form)."""
+    return int(load().kkb_kk_last_instance())
+
+
+def take_device_error() -> int:
+    """Read and clear the device-side error word (KKB_DEVERR_* bits)."""
+    v = ctypes.c_int(0)
+    call("kkb_take_device_error", ctypes.byref(v))
+    return int(v.value)
 
 
 def version() -> str:

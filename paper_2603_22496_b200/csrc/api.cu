@@ -147,7 +147,8 @@ static int check_kk_args(int n_tx, int n_rx, int n_t, int nx, int nz, int out_ki
 }
 
 struct kkb_kk_plan {
-    int N, M, T, nx, nz, linear, W, W_small;  // trace windows of the big / small tiles
+    int N, M, T, nx, nz, linear;
+    KKWindows win;  // trace windows of the big / mid / small tiles
     double fs, shift;
     double *ltx, *ltzT, *lrx, *lrzT, *w;  // one allocation
 };
@@ -196,15 +197,14 @@ extern "C" int kkb_kk_plan_create(const double *ltx, const double *ltz, const do
         return fail(cuda_status(e, "copy weights"));
     if ((st = transpose_f64(ltz, nz, n_tx, p->ltzT, s))) return fail(st);
     if ((st = transpose_f64(lrz, nz, n_rx, p->lrzT, s))) return fail(st);
-    if ((st = kk_window(ltx, ltz, lrx, lrz, n_tx, n_rx, nx, nz, fs, shift, &p->W, s))) return fail(st);
-    if ((st = kk_window(ltx, ltz, lrx, lrz, n_tx, n_rx, nx, nz, fs, shift, &p->W_small, s,
-                        KKB_KK_S_TX, KKB_KK_S_TZ)))
-        return fail(st);
+    if ((st = kk_window(ltx, ltz, lrx, lrz, n_tx, n_rx, nx, nz, fs, shift, &p->win, s))) return fail(st);
     *out = p;
     return KKB_OK;
 }
 
-extern "C" int kkb_kk_plan_window(const kkb_kk_plan *p) { return p ? p->W : -1; }
+extern "C" int kkb_kk_plan_window(const kkb_kk_plan *p) { return p ? p->win.big : -1; }
+
+extern "C" int kkb_kk_last_instance(void) { return kk_last_instance(); }
 
 extern "C" int kkb_kk_plan_run_strided(kkb_kk_plan *p, const void *data, int n_frames,
                                        long long data_frame_stride, long long data_tx_stride,
@@ -224,8 +224,8 @@ extern "C" int kkb_kk_plan_run_strided(kkb_kk_plan *p, const void *data, int n_f
     return kk_gather(reinterpret_cast<const float2 *>(data), p->N, p->M, p->T, p->ltx, p->ltzT,
                      p->lrx, p->lrzT, p->nx, p->nz, p->w, p->fs, p->shift, p->linear, out,
                      out_kind, n_frames, data_frame_stride, out_frame_stride, intensity, frame_max,
-                     p->W, as_stream(stream), (flags & KKB_RUN_ACCUMULATE_INTENSITY) ? 1 : 0,
-                     nullptr, p->W_small, data_tx_stride);
+                     p->win, as_stream(stream), (flags & KKB_RUN_ACCUMULATE_INTENSITY) ? 1 : 0,
+                     nullptr, data_tx_stride);
 }
 
 extern "C" int kkb_kk_plan_run_ex(kkb_kk_plan *p, const void *data, int n_frames,
@@ -265,8 +265,8 @@ extern "C" int kkb_kk_plan_run_sets(kkb_kk_plan *p, const void *data, int n_fram
     return kk_gather(reinterpret_cast<const float2 *>(data), p->N, p->M, p->T, p->ltx, p->ltzT,
                      p->lrx, p->lrzT, p->nx, p->nz, p->w, p->fs, p->shift, p->linear, out,
                      out_kind, n_frames, data_frame_stride, out_frame_stride, intensity, frame_max,
-                     p->W, as_stream(stream), (flags & KKB_RUN_ACCUMULATE_INTENSITY) ? 1 : 0,
-                     nullptr, p->W_small, 0, &sets);
+                     p->win, as_stream(stream), (flags & KKB_RUN_ACCUMULATE_INTENSITY) ? 1 : 0,
+                     nullptr, 0, &sets);
 }
 
 extern "C" int kkb_kk_plan_run_scatter(kkb_kk_plan *p, const void *data, int n_frames,
@@ -292,7 +292,7 @@ extern "C" int kkb_kk_plan_run_scatter(kkb_kk_plan *p, const void *data, int n_f
     return kk_gather(reinterpret_cast<const float2 *>(data), p->N, p->M, p->T, p->ltx, p->ltzT,
                      p->lrx, p->lrzT, p->nx, p->nz, p->w, p->fs, p->shift, p->linear, nullptr,
                      out_kind, n_frames, data_frame_stride, out_frame_stride, nullptr, nullptr,
-                     p->W, as_stream(stream), 0, &sc, p->W_small);
+                     p->win, as_stream(stream), 0, &sc);
 }
 
 // ------------------------------------------------------------- CUDA IPC (row-block P2P)

@@ -24,6 +24,13 @@
 #define KKB_KK_S_CX 2
 #define KKB_KK_S_TZ (8 * KKB_KK_S_WZ)
 #define KKB_KK_S_TX (8 * KKB_KK_S_CX * KKB_KK_S_WX)
+// mid-size instance: 32 x 32 pixels, 4 warps (2 x 4 pixels per lane like the
+// big one) for grids between the two, e.g. config-5 row blocks at 4-8 ranks
+#define KKB_KK_M_WZ 4
+#define KKB_KK_M_WX 1
+#define KKB_KK_M_CX 4
+#define KKB_KK_M_TZ (8 * KKB_KK_M_WZ)
+#define KKB_KK_M_TX (8 * KKB_KK_M_CX * KKB_KK_M_WX)
 #ifndef KKB_KK_STAGE_ELEMS
 #define KKB_KK_STAGE_ELEMS 1024  // window entries staged per pipeline stage
 #endif
@@ -48,11 +55,13 @@ int build_kk_luts(double x0, double dx, int nx, double z0, double dz, int nz, co
 
 int transpose_f64(const double *in, int rows, int cols, double *out, cudaStream_t s);
 
-// Synchronises `s`: returns the shared-memory window length (samples) one
-// gather tile needs for these tables.
+// shared-memory trace window (samples) one tile of each instance needs
+struct KKWindows {
+    int big, mid, small;
+};
+// Synchronises `s` (one launch for the three tile sizes).
 int kk_window(const double *ltx, const double *ltz, const double *lrx, const double *lrz, int N,
-              int M, int nx, int nz, double fs, double shift, int *window_out, cudaStream_t s,
-              int tile_x = KKB_KK_TX, int tile_z = KKB_KK_TZ);
+              int M, int nx, int nz, double fs, double shift, KKWindows *win, cudaStream_t s);
 
 #define KKB_MAX_DST 8
 // fused row-block all-gather targets of the gather epilogue (device pointers)
@@ -77,10 +86,13 @@ struct KKSets {
 int kk_gather(const float2 *data, int N, int M, int T, const double *ltx, const double *ltzT,
               const double *lrx, const double *lrzT, int nx, int nz, const double *w, double fs,
               double shift, int linear, void *out, int out_kind, int n_frames, long long data_fs,
-              long long out_fs, float *inten, unsigned *fmax, int W, cudaStream_t s,
-              int accum = 0, const KKScatter *sc = nullptr, int W_small = 0,
+              long long out_fs, float *inten, unsigned *fmax, const KKWindows &win, cudaStream_t s,
+              int accum = 0, const KKScatter *sc = nullptr,
               long long data_ns = 0,  // 0: M*T (dense (N, M, T) traces)
               const KKSets *sets = nullptr);
+
+// instance the last kk_gather dispatch launched (KKB_KK_INST_*, include/kkb.h)
+int kk_last_instance();
 
 int kk_taps(const double *ltx, const double *ltz, const double *lrx, const double *lrz, int N, int M,
             int T, int nx, int nz, double fs, double shift, int linear, int *idx, cudaStream_t s);

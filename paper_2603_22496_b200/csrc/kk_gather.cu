@@ -31,6 +31,8 @@
 // (fused row-block all-gather, kkb_kk_plan_run_scatter).
 
 #include <algorithm>
+#include <atomic>
+#include <cstring>
 #include <cstdlib>
 #include <type_traits>
 #include <vector>
@@ -177,19 +179,30 @@ int kk_taps(const double *ltx, const double *ltz, const double *lrx, const doubl
 }
 
 // ------------------------------------------------------------- window size pre-pass
-// One thread per (tile, n, m): taps the tile can touch span
-// [floor(min corner fi) - 1, floor(max corner fi) + 2]; record the maximum length.
+// One thread per (tile, n, m) of each tile size: taps the tile can touch span
+// [floor(min corner fi) - 1, floor(max corner fi) + 2]; wmax[s] = the largest
+// length over the tiles of size s (big, mid, small) — one launch, one sync.
+struct KKTileSizes {
+    int tx[3], tz[3];
+};
+
 __global__ void k_kk_window(const double *__restrict__ ltx, const double *__restrict__ ltz,
                             const double *__restrict__ lrx, const double *__restrict__ lrz, int N,
-                            int M, int nx, int nz, int TX, int TZ, double fs, double shift,
+                            int M, int nx, int nz, KKTileSizes ts, double fs, double shift,
                             int *wmax) {
-    const int tiles_z = (nz + TZ - 1) / TZ, tiles_x = (nx + TX - 1) / TX;
-    const long long total = (long long)tiles_z * tiles_x * N * M;
-    int best = 0;
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+    long long cum[4] = {0, 0, 0, 0};
+    for (int s = 0; s < 3; ++s)
+        cum[s + 1] = cum[s] + (long long)((nz + ts.tz[s] - 1) / ts.tz[s]) *
+                                  ((nx + ts.tx[s] - 1) / ts.tx[s]) * N * M;
+    int best[3] = {0, 0, 0};
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < cum[3];
          i += (long long)gridDim.x * blockDim.x) {
-        int m = (int)(i % M);
-        long long r = i / M;
+        const int sz = i < cum[1] ? 0 : (i < cum[2] ? 1 : 2);
+        const int TX = ts.tx[sz], TZ = ts.tz[sz];
+        const int tiles_x = (nx + TX - 1) / TX;
+        long long r = i - cum[sz];
+        int m = (int)(r % M);
+        r /= M;
         int n = (int)(r % N);
         r /= N;
         int tx = (int)(r % tiles_x), tz = (int)(r / tiles_x);
@@ -207,26 +220,28 @@ __global__ void k_kk_window(const double *__restrict__ ltx, const double *__rest
             }
         double span = floor(hi) - floor(lo) + 4.0;
         int w = span > 1e9 ? 1000000000 : (int)span;
-        best = max(best, w);
+        best[sz] = max(best[sz], w);
     }
-    atomicMax(wmax, best);
+    for (int s = 0; s < 3; ++s)
+        if (best[s]) atomicMax(wmax + s, best[s]);
 }
 
 int kk_window(const double *ltx, const double *ltz, const double *lrx, const double *lrz, int N,
-              int M, int nx, int nz, double fs, double shift, int *window_out, cudaStream_t s,
-              int tile_x, int tile_z) {
+              int M, int nx, int nz, double fs, double shift, KKWindows *win, cudaStream_t s) {
     int *d = nullptr;
-    KKB_TRY_CUDA(cudaMallocAsync(&d, sizeof(int), s), "cudaMallocAsync(window)");
-    KKB_TRY_CUDA(cudaMemsetAsync(d, 0, sizeof(int), s), "memset(window)");
-    k_kk_window<<<512, 256, 0, s>>>(ltx, ltz, lrx, lrz, N, M, nx, nz, tile_x, tile_z, fs, shift,
-                                    d);
+    KKB_TRY_CUDA(cudaMallocAsync(&d, 3 * sizeof(int), s), "cudaMallocAsync(window)");
+    KKB_TRY_CUDA(cudaMemsetAsync(d, 0, 3 * sizeof(int), s), "memset(window)");
+    KKTileSizes ts{{KKB_KK_TX, KKB_KK_M_TX, KKB_KK_S_TX}, {KKB_KK_TZ, KKB_KK_M_TZ, KKB_KK_S_TZ}};
+    k_kk_window<<<512, 256, 0, s>>>(ltx, ltz, lrx, lrz, N, M, nx, nz, ts, fs, shift, d);
     KKB_CHECK_LAUNCH("k_kk_window");
-    int h = 0;
-    KKB_TRY_CUDA(cudaMemcpyAsync(&h, d, sizeof(int), cudaMemcpyDeviceToHost, s), "copy window");
+    int h[3] = {0, 0, 0};
+    KKB_TRY_CUDA(cudaMemcpyAsync(h, d, sizeof(h), cudaMemcpyDeviceToHost, s), "copy window");
     KKB_TRY_CUDA(cudaStreamSynchronize(s), "sync window");
     cudaFreeAsync(d, s);
     // round up to a multiple of 2 samples (16 B) for tidy cp.async rows
-    *window_out = (h + 1) & ~1;
+    win->big = (h[0] + 1) & ~1;
+    win->mid = (h[1] + 1) & ~1;
+    win->small = (h[2] + 1) & ~1;
     return KKB_OK;
 }
 
@@ -277,6 +292,10 @@ __device__ __forceinline__ int pcol(int c) {
     return (c / (8 * CX)) * (8 * CX) + (c & 7) * CX + ((c >> 3) % CX);
 }
 
+// |IQ|^2 as one explicit float sequence (no contraction choice left to the
+// compiler), shared by the tiled and per-pixel kernels
+__device__ __forceinline__ float mag2(float vr, float vi) { return __fmaf_rn(vr, vr, __fmul_rn(vi, vi)); }
+
 // IQ pixel store (complex64 or complex128)
 __device__ __forceinline__ void store_iq(void *out, int kind, long long px, float vr, float vi) {
     if (kind == KKB_OUT_C128)
@@ -289,7 +308,7 @@ __device__ __forceinline__ void store_iq(void *out, int kind, long long px, floa
 // chunks of [set_m0[j], set_m0[j+1]) asc); at the end of each set its image is
 // stored, |B_j|^2 added to a per-pixel running intensity and the sums reset.
 template <int WZ, int WX, int CX, bool LINEAR, int FR, bool MS = false>
-__global__ void __launch_bounds__(WZ *WX * 32, KKB_KK_MIN_CTAS)
+__global__ void __launch_bounds__(WZ *WX * 32, KKB_KK_MIN_CTAS * KKB_KK_WZ * KKB_KK_WX / (WZ * WX))
 k_kk_gather(const KKArgs a) {
     constexpr int TZ = 8 * WZ;
     constexpr int TX = 8 * CX * WX;
@@ -423,6 +442,7 @@ k_kk_gather(const KKArgs a) {
 
     float accr[FR][2][CX], acci[FR][2][CX];  // float32 per-pixel sums, fixed order
     double t1[2][CX];
+    unsigned emax = 0;  // largest raw window index over live pairs (must stay in the window)
 #pragma unroll
     for (int fr = 0; fr < FR; ++fr)
 #pragma unroll
@@ -492,6 +512,7 @@ k_kk_gather(const KKArgs a) {
 #pragma unroll kQUnroll
         for (int q = 0; q < mc; ++q) {
             const int m = m0 + q;
+            unsigned eq = 0;  // largest raw window index of this pair's taps (clamp check)
             const double2 lz = reinterpret_cast<const double2 *>(lrz_p + m * TZ)[zq];
             double lxv[CX];
 #pragma unroll
@@ -512,8 +533,9 @@ k_kk_gather(const KKArgs a) {
                 for (int r = 0; r < CX; ++r) {
                     const double fi = kk_delay(t1[p][r], p ? lz.y : lz.x, lxv[r], fs, shift);
                     const double sv = __dadd_rd(LINEAR ? fi : __dadd_rn(fi, 0.5), KKB_FLOOR_MAGIC2);
-                    const unsigned e = min((unsigned)(__double2hiint(sv) - loC),
-                                           (unsigned)(LINEAR ? W - 2 : W - 1));
+                    const unsigned raw = (unsigned)(__double2hiint(sv) - loC);
+                    eq = max(eq, raw);
+                    const unsigned e = min(raw, (unsigned)(LINEAR ? W - 2 : W - 1));
                     const float f1 = __uint_as_float(((unsigned)__double2loint(sv) >> 9) + 0x3F800000u);
 #pragma unroll
                     for (int fr = 0; fr < FR; ++fr) {
@@ -530,6 +552,9 @@ k_kk_gather(const KKArgs a) {
                     }
                 }
             }
+            // a clamped index reads a wrong entry unless the pair's whole window
+            // lies outside the trace (every entry zero, e.g. |fi| >= 2^19)
+            if (lw.x <= (LINEAR ? T - 2 : T - 1) && lw.x + W > 0) emax = max(emax, eq);
         }
         if constexpr (MS) {
             if (set_done) {
@@ -552,8 +577,8 @@ k_kk_gather(const KKArgs a) {
                                     const float vr = accr[fr][p][r], vi = acci[fr][p][r];
                                     const long long px = (long long)f * a.out_fs + (long long)ix * nz + iz;
                                     if (a.out) store_iq(a.out, a.out_kind, set * a.out_set_stride + px, vr, vi);
-                                    float I = vr * vr + vi * vi;
-                                    if (set > 0 || a.accum) I += a.inten[px];
+                                    float I = mag2(vr, vi);
+                                    if (set > 0 || a.accum) I = __fadd_rn(I, a.inten[px]);
                                     a.inten[px] = I;
                                     fmx = fmaxf(fmx, I);
                                 }
@@ -587,6 +612,7 @@ k_kk_gather(const KKArgs a) {
         ch = ch1;
     }
 
+    if (emax > (unsigned)(LINEAR ? W - 2 : W - 1)) atomicOr(&g_device_error, KKB_DEVERR_KK_WINDOW);
     if constexpr (MS) return;  // every set's epilogue ran inside the loop
 
     // epilogue: IQ (+ fused intensity and frame max), per frame
@@ -604,21 +630,11 @@ k_kk_gather(const KKArgs a) {
                 if (iz < nz && ix < nx) {
                     const float vr = accr[fr][p][r], vi = acci[fr][p][r];
                     const long long px = (long long)f * a.out_fs + (long long)ix * nz + iz;
-                    if (a.out) {
-                        if (a.out_kind == KKB_OUT_C128)
-                            reinterpret_cast<double2 *>(a.out)[px] = make_double2(vr, vi);
-                        else
-                            reinterpret_cast<float2 *>(a.out)[px] = make_float2(vr, vi);
-                    }
-                    for (int d = 0; d < a.ndst; ++d) {
-                        if (a.out_kind == KKB_OUT_C128)
-                            reinterpret_cast<double2 *>(a.dst[d])[a.dst_off + px] = make_double2(vr, vi);
-                        else
-                            reinterpret_cast<float2 *>(a.dst[d])[a.dst_off + px] = make_float2(vr, vi);
-                    }
+                    if (a.out) store_iq(a.out, a.out_kind, px, vr, vi);
+                    for (int d = 0; d < a.ndst; ++d) store_iq(a.dst[d], a.out_kind, a.dst_off + px, vr, vi);
                     if (a.inten) {
-                        float I = vr * vr + vi * vi;
-                        if (a.accum) I += a.inten[px];  // sets compounded in call order
+                        float I = mag2(vr, vi);
+                        if (a.accum) I = __fadd_rn(I, a.inten[px]);  // sets compounded in call order
                         a.inten[px] = I;
                         fmx = fmaxf(fmx, I);
                     }
@@ -634,8 +650,12 @@ k_kk_gather(const KKArgs a) {
 
 // Per-pixel fallback of K5 for geometries whose per-tile trace window does not
 // fit the staging buffer (very coarse grids / steep delays): one thread per
-// (frame, pixel), taps read through L1, the same index math (kk_delay +
-// tap_index), lerp, accumulation order and epilogue as the tiled kernel.
+// (frame, pixel), taps read through L1.  Every float operation is the tiled
+// kernel's: the same index math (kk_delay + tap_index), the lerp as
+// (2 d0 - d1) + (1 + frac) (d1 - d0), one float32 accumulator over the pairs
+// in (n, m) order, and the same intensity / accumulation expressions — so the
+// two kernels give bit-identical images (tested), whichever one a plan, a
+// row block of it or a batch size dispatches to.
 template <bool LINEAR, bool MS = false>
 __global__ void __launch_bounds__(256)
 k_kk_direct(const KKArgs a) {
@@ -648,12 +668,10 @@ k_kk_direct(const KKArgs a) {
         const float2 *dframe = a.data + (long long)f * a.data_fs;
         const long long px = (long long)f * a.out_fs + i;
         const int nsets = MS ? a.nsets : 1;
-        float isum = 0.f;  // MS: running sum_j |B_j|^2
         for (int j = 0; j < nsets; ++j) {
             const int mb = MS ? a.set_m0[j] : 0, me = MS ? a.set_m0[j + 1] : a.M;
-            double tr_ = 0.0, ti_ = 0.0;  // per-transmit float32 partials, float64 total
+            float ar = 0.f, ai = 0.f;
             for (int n = 0; n < a.N; ++n) {
-                float ar = 0.f, ai = 0.f;
                 const double t1 = __dadd_rn(a.ltx[(long long)ix * a.N + n], a.ltzT[(long long)n * a.nz + iz]);
                 for (int m = mb; m < me; ++m) {
                     const double fi = kk_delay(t1, a.lrzT[(long long)m * a.nz + iz], a.lrx[(long long)ix * a.M + m],
@@ -666,51 +684,26 @@ k_kk_direct(const KKArgs a) {
                     const float2 d0 = __ldg(tr + F);
                     if (LINEAR) {
                         const float2 d1 = __ldg(tr + F + 1);
-                        const float fr = __uint_as_float(((unsigned)__double2loint(sv) >> 9) | 0x3F800000u) - 1.0f;
-                        ar = fmaf(wm, fmaf(fr, d1.x - d0.x, d0.x), ar);
-                        ai = fmaf(wm, fmaf(fr, d1.y - d0.y, d0.y), ai);
+                        const float f1 = __uint_as_float(((unsigned)__double2loint(sv) >> 9) + 0x3F800000u);
+                        const float vx = fmaf(f1, d1.x - d0.x, fmaf(2.f, d0.x, -d1.x));
+                        const float vy = fmaf(f1, d1.y - d0.y, fmaf(2.f, d0.y, -d1.y));
+                        ar = fmaf(wm, vx, ar);
+                        ai = fmaf(wm, vy, ai);
                     } else {
                         ar = fmaf(wm, d0.x, ar);
                         ai = fmaf(wm, d0.y, ai);
                     }
                 }
-                tr_ += (double)ar;
-                ti_ += (double)ai;
             }
-            const float ar = (float)tr_, ai = (float)ti_;
-            if constexpr (MS) {
-                if (a.out) {
-                    if (a.out_kind == KKB_OUT_C128)
-                        reinterpret_cast<double2 *>(a.out)[j * a.out_set_stride + px] = make_double2(tr_, ti_);
-                    else
-                        reinterpret_cast<float2 *>(a.out)[j * a.out_set_stride + px] = make_float2(ar, ai);
-                }
-                const float base = j ? isum : ((a.accum && a.inten) ? a.inten[px] : 0.f);
-                isum = ar * ar + ai * ai + base;
-                continue;
-            }
-            if (a.out) {
-                if (a.out_kind == KKB_OUT_C128)
-                    reinterpret_cast<double2 *>(a.out)[px] = make_double2(tr_, ti_);
-                else
-                    reinterpret_cast<float2 *>(a.out)[px] = make_float2(ar, ai);
-            }
-            for (int d = 0; d < a.ndst; ++d) {
-                if (a.out_kind == KKB_OUT_C128)
-                    reinterpret_cast<double2 *>(a.dst[d])[a.dst_off + px] = make_double2(tr_, ti_);
-                else
-                    reinterpret_cast<float2 *>(a.dst[d])[a.dst_off + px] = make_float2(ar, ai);
-            }
+            if (a.out) store_iq(a.out, a.out_kind, (MS ? j * a.out_set_stride : 0) + px, ar, ai);
+            if (!MS)
+                for (int d = 0; d < a.ndst; ++d) store_iq(a.dst[d], a.out_kind, a.dst_off + px, ar, ai);
             if (a.inten) {
-                float I = ar * ar + ai * ai;
-                if (a.accum) I += a.inten[px];
+                float I = mag2(ar, ai);
+                if ((MS && j > 0) || a.accum) I = __fadd_rn(I, a.inten[px]);
                 a.inten[px] = I;
                 fmx = I;
             }
-        }
-        if constexpr (MS) {
-            if (a.inten) a.inten[px] = isum;
-            fmx = isum;
         }
     }
     if (a.fmax) {
@@ -747,14 +740,80 @@ static int launch_tiled(const KKArgs &a, int n_frames, size_t sm, bool linear, c
     return KKB_OK;
 }
 
+// ------------------------------------------------------------- instance selection
+static std::atomic<int> g_last_instance{-1};
+int kk_last_instance() { return g_last_instance.load(); }
+
+// window entries each instance stages per pipeline stage: EPT per thread
+constexpr int kKKEPT = KKB_KK_STAGE_ELEMS / (32 * KKB_KK_WZ * KKB_KK_WX);
+
+struct InstanceShape {
+    int tz, tx, stage, W, resident;  // resident: CTAs per SM the launch bounds aim for
+};
+
+static InstanceShape instance_shape(int inst, const KKWindows &win) {
+    switch (inst) {
+        case KKB_KK_INST_SMALL:
+            return {KKB_KK_S_TZ, KKB_KK_S_TX, kKKEPT * 32 * KKB_KK_S_WZ * KKB_KK_S_WX,
+                    std::max(2, win.small), KKB_KK_MIN_CTAS * KKB_KK_WZ * KKB_KK_WX / (KKB_KK_S_WZ * KKB_KK_S_WX)};
+        case KKB_KK_INST_MID:
+            return {KKB_KK_M_TZ, KKB_KK_M_TX, kKKEPT * 32 * KKB_KK_M_WZ * KKB_KK_M_WX,
+                    std::max(2, win.mid), KKB_KK_MIN_CTAS * KKB_KK_WZ * KKB_KK_WX / (KKB_KK_M_WZ * KKB_KK_M_WX)};
+        default:
+            return {KKB_KK_TZ, KKB_KK_TX, KKB_KK_STAGE_ELEMS, std::max(2, win.big), KKB_KK_MIN_CTAS};
+    }
+}
+
+static bool instance_fits(int inst, int N, int M, bool linear, const KKWindows &win, int n_frames) {
+    if (inst == KKB_KK_INST_DIRECT) return true;
+    const InstanceShape sh = instance_shape(inst, win);
+    const int fr = inst == KKB_KK_INST_BIG_FR ? KKB_KK_FR : 1;
+    if (inst == KKB_KK_INST_BIG_FR && (n_frames < 2 || KKB_KK_FR < 2)) return false;
+    return sh.W <= sh.stage && fr * sh.W <= sh.stage &&
+           kk_smem_bytes(N, M, sh.W, 1, linear, sh.tz, sh.tx, fr) <= 200 * 1024;
+}
+
+// The largest tile whose grid fills every SM with the CTAs its launch bounds
+// aim for (big tiles share the tables and index setup over more pixels; two
+// frames per CTA also share every tap's index math); below that, the largest
+// tile that fits at all.  KKB_KK_INST forces an instance when it fits
+// (KKB_KK_DIRECT=1 / KKB_KK_SMALL=1 / KKB_KK_FR1=1: older test hooks).
+static int select_instance(int N, int M, int nx, int nz, int n_frames, bool linear, const KKWindows &win) {
+    static const int order[4] = {KKB_KK_INST_BIG_FR, KKB_KK_INST_BIG, KKB_KK_INST_MID, KKB_KK_INST_SMALL};
+    auto fits = [&](int i) { return instance_fits(i, N, M, linear, win, n_frames); };
+    auto env1 = [](const char *k) {
+        const char *v = getenv(k);
+        return v && v[0] == '1';
+    };
+    if (const char *f = getenv("KKB_KK_INST")) {
+        const char *names[5] = {"direct", "small", "mid", "big", "big_fr"};
+        for (int i = 0; i < 5; ++i)
+            if (!strcmp(f, names[i]) && fits(i)) return i;
+    }
+    if (env1("KKB_KK_DIRECT")) return KKB_KK_INST_DIRECT;
+    if (env1("KKB_KK_SMALL") && fits(KKB_KK_INST_SMALL)) return KKB_KK_INST_SMALL;
+    const bool no_fr = env1("KKB_KK_FR1");
+    const long long sms = sm_count();
+    int largest_fit = KKB_KK_INST_DIRECT;
+    for (int inst : order) {
+        if ((inst == KKB_KK_INST_BIG_FR && no_fr) || !fits(inst)) continue;
+        if (largest_fit == KKB_KK_INST_DIRECT) largest_fit = inst;
+        const InstanceShape sh = instance_shape(inst, win);
+        const int fr = inst == KKB_KK_INST_BIG_FR ? KKB_KK_FR : 1;
+        const long long ctas = ceil_div(nz, sh.tz) * ceil_div(nx, sh.tx) * ceil_div(n_frames, fr);
+        if (ctas >= sh.resident * sms) return inst;
+    }
+    return largest_fit == KKB_KK_INST_DIRECT ? KKB_KK_INST_DIRECT
+           : (fits(KKB_KK_INST_SMALL) ? KKB_KK_INST_SMALL : largest_fit);
+}
+
 int kk_gather(const float2 *data, int N, int M, int T, const double *ltx, const double *ltzT,
               const double *lrx, const double *lrzT, int nx, int nz, const double *w, double fs,
               double shift, int linear, void *out, int out_kind, int n_frames, long long data_fs,
-              long long out_fs, float *inten, unsigned *fmax, int W, cudaStream_t s, int accum,
-              const KKScatter *sc, int W_small, long long data_ns, const KKSets *sets) {
+              long long out_fs, float *inten, unsigned *fmax, const KKWindows &win, cudaStream_t s,
+              int accum, const KKScatter *sc, long long data_ns, const KKSets *sets) {
     if (n_frames <= 0 || nx <= 0 || nz <= 0) return KKB_OK;
     const bool ms = sets != nullptr;
-    if (W < 2) W = 2;
     // a receive subset of a larger trace array (transmit stride data_ns > M*T):
     // gathered into dense (F, N, M, T) scratch first, so the kernels keep the
     // dense row arithmetic (a runtime transmit stride costs K5 0.5-8%)
@@ -783,7 +842,7 @@ int kk_gather(const float2 *data, int N, int M, int T, const double *ltx, const 
         }
     } free_dense{dense, s};
     KKArgs a{data, data_fs, N, M, T, ltx, ltzT, lrx,
-             lrzT, w, fs, shift, nx, nz, W, 0,
+             lrzT, w, fs, shift, nx, nz, 2, 0,
              out, out_kind, out_fs, inten, fmax, accum, 0, 0, {}, n_frames};
     if (sc) {
         a.ndst = sc->ndst;
@@ -796,19 +855,9 @@ int kk_gather(const float2 *data, int N, int M, int T, const double *ltx, const 
         for (int j = 0; j <= sets->nsets; ++j) a.set_m0[j] = sets->m0[j];
         a.out_set_stride = sets->out_set_stride;
     }
-    // instance: big tiles; small tiles when the big grid cannot fill the SMs
-    // (or the big tile's window overflows its stage); else the per-pixel kernel
-    constexpr int EPT = KKB_KK_STAGE_ELEMS / (32 * KKB_KK_WZ * KKB_KK_WX);
-    constexpr int STAGE_S = EPT * 32 * KKB_KK_S_WZ * KKB_KK_S_WX;
-    const long long tiles_big = ceil_div(nz, KKB_KK_TZ) * ceil_div(nx, KKB_KK_TX);
-    const bool small_ok = W_small >= 2 && W_small <= STAGE_S &&
-                          kk_smem_bytes(N, M, W_small, 1, linear, KKB_KK_S_TZ, KKB_KK_S_TX) <= 200 * 1024;
-    const bool big_ok = W <= KKB_KK_STAGE_ELEMS && kk_smem_bytes(N, M, W, 1, linear) <= 227 * 1024;
-    const char *force = getenv("KKB_KK_DIRECT");  // test hooks: per-pixel / small-tile kernels
-    const char *fsmall = getenv("KKB_KK_SMALL");
-    bool use_small = small_ok && (!big_ok || tiles_big * n_frames < 2LL * sm_count() ||
-                                  (fsmall && fsmall[0] == '1'));
-    if ((force && force[0] == '1') || (!big_ok && !use_small)) {
+    const int inst = select_instance(N, M, nx, nz, n_frames, linear != 0, win);
+    g_last_instance.store(inst | (ms ? KKB_KK_INST_SETS : 0));
+    if (inst == KKB_KK_INST_DIRECT) {
         // steep geometry or huge pair tables: per-pixel kernel
         dim3 grid((unsigned)ceil_div((long long)nx * nz, 256), (unsigned)n_frames);
         if (ms) {
@@ -823,35 +872,31 @@ int kk_gather(const float2 *data, int N, int M, int T, const double *ltx, const 
         KKB_CHECK_LAUNCH("k_kk_direct");
         return KKB_OK;
     }
-    const int Wc = use_small ? W_small : W;
-    const int stage = use_small ? STAGE_S : KKB_KK_STAGE_ELEMS;
-    const int tz = use_small ? KKB_KK_S_TZ : KKB_KK_TZ, tx = use_small ? KKB_KK_S_TX : KKB_KK_TX;
-    // big tiles over a batch: KKB_KK_FR frames per CTA share the tables and the
-    // index math of every tap (when a window block of FR frames fits a stage)
-    const char *ffr = getenv("KKB_KK_FR1");  // test hook: one frame per CTA
-    const int FR = (!use_small && n_frames > 1 && KKB_KK_FR > 1 && KKB_KK_FR * Wc <= stage &&
-                    !(ffr && ffr[0] == '1')) ? KKB_KK_FR : 1;
+    const InstanceShape sh = instance_shape(inst, win);
+    const int FR = inst == KKB_KK_INST_BIG_FR ? KKB_KK_FR : 1;
     // receive angles per stage: bounded by the register staging and shared memory
-    int MCH = std::max(1, std::min(M, stage / (FR * Wc)));
-    while (MCH > 1 && kk_smem_bytes(N, M, Wc, MCH, linear, tz, tx, FR) > 200 * 1024) MCH = (MCH + 1) / 2;
+    int MCH = std::max(1, std::min(M, sh.stage / (FR * sh.W)));
+    while (MCH > 1 && kk_smem_bytes(N, M, sh.W, MCH, linear, sh.tz, sh.tx, FR) > 200 * 1024) MCH = (MCH + 1) / 2;
     if (const char *fm = getenv("KKB_KK_MCH"))  // test hook: fewer receive angles per stage
         MCH = std::max(1, std::min(MCH, atoi(fm)));
-    const size_t sm = kk_smem_bytes(N, M, Wc, MCH, linear, tz, tx, FR);
-    a.W = Wc;
+    const size_t sm = kk_smem_bytes(N, M, sh.W, MCH, linear, sh.tz, sh.tx, FR);
+    a.W = sh.W;
     a.MCH = MCH;
-    if (ms) {
-        if (use_small)
-            return launch_tiled<KKB_KK_S_WZ, KKB_KK_S_WX, KKB_KK_S_CX, 1, true>(a, n_frames, sm, linear != 0, s);
-        if (FR > 1)
-            return launch_tiled<KKB_KK_WZ, KKB_KK_WX, KKB_KK_CX, KKB_KK_FR, true>(a, n_frames, sm,
-                                                                                linear != 0, s);
-        return launch_tiled<KKB_KK_WZ, KKB_KK_WX, KKB_KK_CX, 1, true>(a, n_frames, sm, linear != 0, s);
+    const bool lin = linear != 0;
+    switch (inst) {
+        case KKB_KK_INST_SMALL:
+            return ms ? launch_tiled<KKB_KK_S_WZ, KKB_KK_S_WX, KKB_KK_S_CX, 1, true>(a, n_frames, sm, lin, s)
+                      : launch_tiled<KKB_KK_S_WZ, KKB_KK_S_WX, KKB_KK_S_CX, 1>(a, n_frames, sm, lin, s);
+        case KKB_KK_INST_MID:
+            return ms ? launch_tiled<KKB_KK_M_WZ, KKB_KK_M_WX, KKB_KK_M_CX, 1, true>(a, n_frames, sm, lin, s)
+                      : launch_tiled<KKB_KK_M_WZ, KKB_KK_M_WX, KKB_KK_M_CX, 1>(a, n_frames, sm, lin, s);
+        case KKB_KK_INST_BIG_FR:
+            return ms ? launch_tiled<KKB_KK_WZ, KKB_KK_WX, KKB_KK_CX, KKB_KK_FR, true>(a, n_frames, sm, lin, s)
+                      : launch_tiled<KKB_KK_WZ, KKB_KK_WX, KKB_KK_CX, KKB_KK_FR>(a, n_frames, sm, lin, s);
+        default:
+            return ms ? launch_tiled<KKB_KK_WZ, KKB_KK_WX, KKB_KK_CX, 1, true>(a, n_frames, sm, lin, s)
+                      : launch_tiled<KKB_KK_WZ, KKB_KK_WX, KKB_KK_CX, 1>(a, n_frames, sm, lin, s);
     }
-    if (use_small)
-        return launch_tiled<KKB_KK_S_WZ, KKB_KK_S_WX, KKB_KK_S_CX, 1>(a, n_frames, sm, linear != 0, s);
-    if (FR > 1)
-        return launch_tiled<KKB_KK_WZ, KKB_KK_WX, KKB_KK_CX, KKB_KK_FR>(a, n_frames, sm, linear != 0, s);
-    return launch_tiled<KKB_KK_WZ, KKB_KK_WX, KKB_KK_CX, 1>(a, n_frames, sm, linear != 0, s);
 }
 
 // ------------------------------------------------------------- K6 epilogues

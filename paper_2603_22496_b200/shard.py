@@ -171,7 +171,11 @@ class RowBlockKK:
     Image assembly (``transport``): "p2p" — the K5 epilogue writes the rows
     straight into every rank's full-image buffer (CUDA IPC over NVLink);
     ``gather()`` then only waits (stream sync + barrier) and returns the local
-    image, valid until the next ``beamform_block``.  "nccl" — the blocks (and,
+    image.  The IPC image is double-buffered: call i writes half i % 2, so a
+    fast rank's call i + 1 never overwrites the image a slow rank is still
+    reading after gather() i; a rank can only reach call i + 2 (the same half
+    again) after every rank has passed gather() i + 1, i.e. has finished with
+    image i.  The returned image is valid until the next gather().  "nccl" — the blocks (and,
     sharded, the traces) are all-gathered with NCCL after the kernels.  Per-row
     and per-pixel arithmetic does not depend on the split, so the image is
     bit-identical to the single-GPU image for any world size, stage-1 mode
@@ -253,9 +257,10 @@ class RowBlockKK:
         """Full-image (and, sharded, full-trace) buffer per rank; IPC handles
         exchanged, peers mapped."""
         t = self.t
-        self._img = _IpcBuffer(self.grid.nx * self.grid.nz * 8, (self.grid.nx, self.grid.nz),
+        self._img = _IpcBuffer(2 * self.grid.nx * self.grid.nz * 8, (2, self.grid.nx, self.grid.nz),
                                t.complex64, self.rank, self.world, self.group)
-        self.image = self._img.tensor
+        self._half = 1  # half written by the latest beamform_block (0 after the first call)
+        self.image = self._img.tensor[self._half]
         if self.stage1 == "sharded":
             self._tr = _IpcBuffer(self.N * self.M * self.T * 8, (self.N, self.M, self.T),
                                   t.complex64, self.rank, self.world, self.group)
@@ -325,8 +330,12 @@ class RowBlockKK:
         if self._plan is None:
             return self.block[:0]
         if self.transport == "p2p":
+            # alternate halves: peers may still read the other one (class doc)
+            self._half ^= 1
+            self.image = self._img.tensor[self._half]
             _lib.call("kkb_kk_plan_run_scatter", self._plan, dev.ptr(traces), 1, 0,
-                      self._img.dsts, len(self._img.dsts), self.ix0 * self.grid.nz,
+                      self._img.dsts, len(self._img.dsts),
+                      (self._half * self.grid.nx + self.ix0) * self.grid.nz,
                       _lib.KKB_OUT_C64, 0, dev.stream_handle(stream))
             return self.image[self.ix0:self.ix1]
         _lib.call("kkb_kk_plan_run", self._plan, dev.ptr(traces), 1, 0,

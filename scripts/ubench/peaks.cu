@@ -1,0 +1,143 @@
+// Measured on-chip peaks for the rooflines MEASURED_PEAKS.json lacks:
+//   * shared-memory load bandwidth with conflict-free 128-bit warp loads
+//     (LDS.128, lane-consecutive: 4 wavefronts of 128 B per warp load) — the
+//     K5 gather's binding resource (16 B of taps per pixel-pair from SMEM);
+//   * FP32 FMA throughput (K2 contraction, FFT butterflies);
+//   * FP64 add/mul throughput (K5's per-tap delay math: 4 DADD/DMUL + 1 DADD.RD).
+// Every SM runs many resident warps of independent chains; time with CUDA
+// events; the effective SM clock comes from clock64() deltas over the same
+// run (cycles / elapsed time).  Prints one JSON object.
+#include <cstdio>
+#include <cuda_runtime.h>
+
+__device__ unsigned long long g_cycles[4096];
+
+__global__ void k_lds128(int iters, float *out) {
+    __shared__ __align__(16) float4 s[2048];
+    for (int i = threadIdx.x; i < 2048; i += blockDim.x) s[i] = make_float4(i, i + 1, i + 2, i + 3);
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    unsigned a = (unsigned)__cvta_generic_to_shared(s) + ((warp * 32 + lane) & 511) * 16;
+    float acc0 = 0.f, acc1 = 0.f;
+    const unsigned long long c0 = clock64();
+    for (int i = 0; i < iters; ++i) {
+        const unsigned ai = a ^ ((i & 1) << 13);
+        float x, y, z, w, x1, y1, z1, w1;
+        asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(x), "=f"(y), "=f"(z), "=f"(w) : "r"(ai) : "memory");
+        asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4+16384];" : "=f"(x1), "=f"(y1), "=f"(z1), "=f"(w1) : "r"(ai) : "memory");
+        acc0 += (x + y) + (z + w);
+        acc1 += (x1 + y1) + (z1 + w1);
+    }
+    const unsigned long long c1 = clock64();
+    if (threadIdx.x == 0) g_cycles[blockIdx.x] = c1 - c0;
+    if (acc0 + acc1 == -1.f) out[0] = acc0;
+}
+
+template <int CH>
+__global__ void k_ffma(int iters, float *out) {
+    float a[CH];
+#pragma unroll
+    for (int j = 0; j < CH; ++j) a[j] = threadIdx.x * 1e-7f + j;
+    const float b = 0.999999f, c = 1e-7f;
+    const unsigned long long c0 = clock64();
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int j = 0; j < CH; ++j) a[j] = fmaf(a[j], b, c);
+    }
+    const unsigned long long c1 = clock64();
+    float s = 0.f;
+#pragma unroll
+    for (int j = 0; j < CH; ++j) s += a[j];
+    if (threadIdx.x == 0) g_cycles[blockIdx.x] = c1 - c0;
+    if (s == -1.f) out[0] = s;
+}
+
+template <int CH>
+__global__ void k_dadd(int iters, double *out) {
+    double a[CH];
+#pragma unroll
+    for (int j = 0; j < CH; ++j) a[j] = threadIdx.x * 1e-7 + j;
+    const double b = 1e-9;
+    const unsigned long long c0 = clock64();
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int j = 0; j < CH; ++j) a[j] = __dadd_rn(a[j], b);
+    }
+    const unsigned long long c1 = clock64();
+    double s = 0.0;
+#pragma unroll
+    for (int j = 0; j < CH; ++j) s += a[j];
+    if (threadIdx.x == 0) g_cycles[blockIdx.x] = c1 - c0;
+    if (s == -1.0) out[0] = s;
+}
+
+static double mean_cycles(int blocks) {
+    static unsigned long long h[4096];
+    cudaMemcpyFromSymbol(h, g_cycles, sizeof(unsigned long long) * blocks);
+    double s = 0;
+    for (int i = 0; i < blocks; ++i) s += (double)h[i];
+    return s / blocks;
+}
+
+template <class F>
+static float timed(F launch) {
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    launch();  // warm-up
+    cudaDeviceSynchronize();
+    float best = 1e30f;
+    for (int r = 0; r < 5; ++r) {
+        cudaEventRecord(e0);
+        launch();
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float ms;
+        cudaEventElapsedTime(&ms, e0, e1);
+        if (ms < best) best = ms;
+    }
+    return best;
+}
+
+int main() {
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    float *outf;
+    double *outd;
+    cudaMalloc(&outf, 16);
+    cudaMalloc(&outd, 16);
+    printf("{\n \"tool\": \"scripts/ubench/peaks.cu\",\n \"sm_count\": %d,\n", sms);
+
+    {   // LDS.128: 2 CTAs x 1024 threads per SM, 2 loads of 16 B per thread per iteration
+        const int threads = 1024, blocks = sms * 2, iters = 1 << 15;
+        float ms = timed([&] { k_lds128<<<blocks, threads>>>(iters, outf); });
+        double bytes = (double)blocks * threads * iters * 2 * 16;
+        double cyc = mean_cycles(blocks);
+        double mhz = cyc / (ms * 1e3);
+        printf(" \"smem_lds128\": {\"GBps\": %.1f, \"bytes_per_clk_per_sm\": %.2f, \"sm_mhz_effective\": %.0f, "
+               "\"ms\": %.3f, \"what\": \"conflict-free LDS.128, 2048 threads/SM\", \"err\": \"%s\"},\n",
+               bytes / (ms * 1e-3) / 1e9, bytes / (cyc * sms), mhz, ms, cudaGetErrorString(cudaGetLastError()));
+    }
+    {   // FFMA: 8 independent chains, 2 x 1024 threads per SM
+        const int threads = 1024, blocks = sms * 2, iters = 1 << 14;
+        float ms = timed([&] { k_ffma<8><<<blocks, threads>>>(iters, outf); });
+        double flops = 2.0 * blocks * threads * (double)iters * 8;
+        double cyc = mean_cycles(blocks);
+        printf(" \"fp32_fma\": {\"TFLOPs\": %.2f, \"flops_per_clk_per_sm\": %.1f, \"sm_mhz_effective\": %.0f, "
+               "\"ms\": %.3f, \"err\": \"%s\"},\n",
+               flops / (ms * 1e-3) / 1e12, flops / (cyc * sms), cyc / (ms * 1e3), ms,
+               cudaGetErrorString(cudaGetLastError()));
+    }
+    {   // DADD: 8 independent chains
+        const int threads = 1024, blocks = sms * 2, iters = 1 << 12;
+        float ms = timed([&] { k_dadd<8><<<blocks, threads>>>(iters, outd); });
+        double ops = (double)blocks * threads * iters * 8;
+        double cyc = mean_cycles(blocks);
+        printf(" \"fp64_add\": {\"Gops\": %.1f, \"ops_per_clk_per_sm\": %.2f, \"sm_mhz_effective\": %.0f, "
+               "\"ms\": %.3f, \"err\": \"%s\"}\n",
+               ops / (ms * 1e-3) / 1e9, ops / (cyc * sms), cyc / (ms * 1e3), ms,
+               cudaGetErrorString(cudaGetLastError()));
+    }
+    printf("}\n");
+    return 0;
+}

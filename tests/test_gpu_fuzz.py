@@ -126,12 +126,15 @@ def test_decomposition_random_geometry(oracle, seed):
 
 
 @pytest.mark.parametrize("seed", range(16 * _SCALE))
-def test_kk_batched_and_multiset_random(seed):
-    """Kernel-level properties on random geometries large enough for the
-    big-tile, two-frames-per-CTA instance: a batch of F frames equals F
-    single-frame launches bit for bit, and one multi-set launch over a random
-    partition of the receive angles equals one launch per set (per-set tables,
-    intensities accumulated) bit for bit."""
+def test_kk_batched_and_multiset_random(seed, monkeypatch):
+    """Kernel-level properties on random geometries: a batch of F frames
+    equals F single-frame launches bit for bit through every tiled instance
+    (forced with KKB_KK_INST — these grids are too small for the default
+    dispatch to pick the 32 x 64 tiles with two frames per CTA — and checked
+    with kkb_kk_last_instance whenever the instance's window fits), and one
+    multi-set launch over a random partition of the receive angles equals
+    one launch per set (per-set tables, intensities accumulated) bit for bit,
+    the multi-set launch also forced onto the two-frames-per-CTA instance."""
     import ctypes
 
     import torch
@@ -169,15 +172,24 @@ def test_kk_batched_and_multiset_random(seed):
         return kp, (luts, wd)
 
     kp, keep = plan(rx, w)
-    batch = torch.empty((frames, nx, nz), dtype=torch.complex64, device="cuda")
-    _lib.call("kkb_kk_plan_run", kp, dev.ptr(data), frames, n_tx * m_rx * T, dev.ptr(batch),
-              _lib.KKB_OUT_C64, P, None, None, s)
-    single = torch.empty_like(batch)
+    single = torch.empty((frames, nx, nz), dtype=torch.complex64, device="cuda")
     for f in range(frames):
         _lib.call("kkb_kk_plan_run", kp, dev.ptr(data[f]), 1, 0, dev.ptr(single[f]),
                   _lib.KKB_OUT_C64, P, None, None, s)
-    torch.cuda.synchronize()
-    assert torch.equal(batch, single), (seed, n_tx, m_rx, T, nx, nz, frames)
+    ran = set()
+    for inst in ("natural", "big_fr", "big", "mid", "direct"):
+        if inst != "natural":
+            monkeypatch.setenv("KKB_KK_INST", inst)
+        batch = torch.empty((frames, nx, nz), dtype=torch.complex64, device="cuda")
+        _lib.call("kkb_kk_plan_run", kp, dev.ptr(data), frames, n_tx * m_rx * T, dev.ptr(batch),
+                  _lib.KKB_OUT_C64, P, None, None, s)
+        torch.cuda.synchronize()
+        ran.add(_lib.KKB_KK_INST_NAMES[_lib.last_instance()])
+        monkeypatch.delenv("KKB_KK_INST", raising=False)
+        assert torch.equal(batch, single), (seed, inst, n_tx, m_rx, T, nx, nz, frames)
+    assert "direct" in ran, ran
+    assert _lib.take_device_error() == 0
+    monkeypatch.setenv("KKB_KK_INST", "big_fr")
 
     # random partition of the receive angles into 1..4 contiguous sets
     nsets = int(rng.integers(1, min(4, m_rx) + 1))
@@ -189,6 +201,7 @@ def test_kk_batched_and_multiset_random(seed):
     b = (ctypes.c_int * len(bounds))(*bounds)
     _lib.call("kkb_kk_plan_run_sets", kp, dev.ptr(data), frames, n_tx * m_rx * T, nsets, b,
               dev.ptr(iq_sets), _lib.KKB_OUT_C64, P, frames * P, dev.ptr(inten), dev.ptr(fmax), 0, s)
+    monkeypatch.delenv("KKB_KK_INST")
     ref_i = torch.empty_like(inten)
     ref_m = torch.zeros_like(fmax)
     for j in range(nsets):
@@ -204,6 +217,7 @@ def test_kk_batched_and_multiset_random(seed):
         assert torch.equal(iq, iq_sets[j]), (seed, j, bounds)
     assert torch.equal(ref_i, inten) and torch.equal(ref_m, fmax), (seed, bounds)
     _lib.load().kkb_kk_plan_destroy(kp)
+    assert _lib.take_device_error() == 0
 
 
 @pytest.mark.parametrize("seed", range(12 * _SCALE))

@@ -472,8 +472,10 @@ def test_analytic_signal_rejects_too_long_traces():
 
 
 def test_small_and_big_tile_instances_are_bit_identical(monkeypatch):
-    # a single small frame runs the 16 x 16 tile instance, a batch the 32 x 64
-    # one; the per-pixel sums run in the same order, so the images agree bit for bit
+    # the 16 x 16 and the 32 x 64 tile instances (forced, and checked with
+    # kkb_kk_last_instance: a 4-frame config-4 batch alone dispatches to the
+    # 32 x 64 tiles with one frame per CTA); the per-pixel sums run in the
+    # same order, so the images agree bit for bit
     import torch
 
     w = configs.config4(frames=4)
@@ -481,9 +483,13 @@ def test_small_and_big_tile_instances_are_bit_identical(monkeypatch):
     rf = np.stack([configs.noise_rf(p.num_transmits, arr.num_elements, p.num_samples, seed=s)
                    for s in range(4)])
     eng = kb.KKEngine(arr, p, w.receive, w.grid, frames=4, want_db=False)
+    monkeypatch.setenv("KKB_KK_INST", "big")
     big = eng.run(torch.from_numpy(rf).cuda()).clone()
-    monkeypatch.setenv("KKB_KK_SMALL", "1")
+    torch.cuda.synchronize()
+    assert _lib.last_instance() == _lib.KKB_KK_INST_BIG
+    monkeypatch.setenv("KKB_KK_INST", "small")
     small = eng.run(torch.from_numpy(rf).cuda()).clone()
     torch.cuda.synchronize()
+    assert _lib.last_instance() == _lib.KKB_KK_INST_SMALL
     assert torch.equal(big, small)
     eng.close()

@@ -81,6 +81,18 @@ def test_p2p_transport_single_rank_is_the_full_image():
     rb = shard.RowBlockKK(arr, p, w.receive, w.grid, 0, 1, transport="p2p")
     assert rb.transport == "p2p"
     rb.beamform_block(rf)
+    first = rb.gather()
+    assert torch.equal(first, full)
+    # the next frame lands in the other half of the double-buffered IPC image,
+    # so the previous image stays intact until the next gather()
+    rf2 = torch.from_numpy(configs.noise_rf(p.num_transmits, arr.num_elements, p.num_samples,
+                                            seed=5)).cuda()
+    full2 = full_eng.run(rf2[None]).clone()[0]
+    rb.beamform_block(rf2)
+    torch.cuda.synchronize()
+    assert torch.equal(first, full)
+    assert torch.equal(rb.gather(), full2)
+    rb.beamform_block(rf)
     assert torch.equal(rb.gather(), full)
     rb.close()
     full_eng.close()
