@@ -153,6 +153,12 @@ int kkb_kk_plan_run_strided(kkb_kk_plan *p, const void *data, int n_frames,
                             unsigned int *frame_max, int flags, void *stream);
 /* trace window (samples per pair) the plan stages in shared memory */
 int kkb_kk_plan_window(const kkb_kk_plan *p);
+/* Plan-time proof of the window sizing: at creation the plan evaluates every
+ * (pixel, pair) tap index with the gather's own arithmetic against each tile
+ * size's staged window; bit (1 << KKB_KK_INST_*) is set for an instance that
+ * would clamp a tap (the dispatch then never uses it, and
+ * KKB_DEVERR_KK_WINDOW is raised).  0 = every tiled instance proven. */
+int kkb_kk_plan_window_check(const kkb_kk_plan *p);
 /* K5 instance the last kk launch of this process dispatched to (any plan,
  * any thread): the per-pixel kernel, or the tiled kernel with 16x16 / 32x32
  * / 32x64 pixel tiles, the last one with one or KKB_KK_FR (2) frames per CTA;

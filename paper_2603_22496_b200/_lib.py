@@ -41,6 +41,7 @@ SIGNATURES = {
     "kkb_kk_plan_run_sets": [P, P, I, LL, I, P, P, I, LL, LL, P, P, I, P],
     "kkb_kk_plan_window": [P],
     "kkb_kk_last_instance": [],
+    "kkb_kk_plan_window_check": [P],
     "kkb_kk_plan_destroy": [P],
     "kkb_kk_taps": [P, P, P, P, I, I, I, I, I, D, D, I, P, P],
     "kkb_das": [P, I, I, I, P, P, P, I, P, P, P, P, P, D, P, D, D, I, I, I, P, I, P],

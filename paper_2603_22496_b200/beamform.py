@@ -185,6 +185,88 @@ def kk_device(data, luts: DelayLUTSet, fs: float, shift: float, linear: bool = T
     return out
 
 
+class _KKPlanCache:
+    """K5 plans of the drop-in path, reused across calls on the same tables.
+
+    The reference builds its delay tables once and calls ``kk`` /
+    ``_kk_kernel`` per frame (beamform.py:340-375), with plain writeable
+    numpy arrays.  A plan (device tables, depth-major copies, window sizes:
+    one synchronising setup) is keyed by the identity and shape of the four
+    host arrays plus (weights, fs, shift, interpolation) and is reused only
+    while the arrays still hold the bytes it was built from (compared with
+    the cached copies: ~memcmp cost, so in-place edits of a table are never
+    missed).  Each entry also keeps pinned staging for the traces and the
+    complex128 image, so a call is H2D + one gather launch + D2H."""
+
+    def __init__(self, capacity: int = 8):
+        from collections import OrderedDict
+
+        self._d = OrderedDict()
+        self.capacity = capacity
+        self.hits = self.misses = 0
+
+    def _build(self, luts, n, m, T, nx, nz, weights, fs, shift, linear):
+        import ctypes
+
+        t = dev.require_cuda()
+        dl = [dev.to_device(np.ascontiguousarray(a, dtype=np.float64)) for a in luts]
+        wd = dev.to_device(np.ascontiguousarray(weights, dtype=np.float64)) if weights is not None else None
+        kp = ctypes.c_void_p()
+        _lib.call("kkb_kk_plan_create", *[x.data_ptr() for x in dl], n, m, T, nx, nz, dev.ptr(wd),
+                  float(fs), float(shift), int(bool(linear)), dev.stream_handle(), ctypes.byref(kp))
+        return {"plan": kp, "keep": (dl, wd), "copies": [np.array(a, dtype=np.float64) for a in luts],
+                "in_d": t.empty((n, m, T), dtype=t.complex64, device="cuda"),
+                "out_d": t.empty((nx, nz), dtype=t.complex128, device="cuda"),
+                "in_h": t.empty((n, m, T), dtype=t.complex64).pin_memory(),
+                "out_h": t.empty((nx, nz), dtype=t.complex128).pin_memory()}
+
+    def entry(self, luts, n, m, T, nx, nz, weights, fs, shift, linear):
+        wkey = None if weights is None else np.asarray(weights, dtype=np.float64).tobytes()
+        key = (tuple((id(a), np.shape(a)) for a in luts), n, m, T, nx, nz, wkey, float(fs),
+               float(shift), bool(linear))
+        e = self._d.get(key)
+        if e is not None and all(np.array_equal(c, a) for c, a in zip(e["copies"], luts)):
+            self._d.move_to_end(key)
+            self.hits += 1
+            return e
+        if e is not None:
+            self._drop(key)
+        self.misses += 1
+        e = self._build(luts, n, m, T, nx, nz, weights, fs, shift, linear)
+        self._d[key] = e
+        while len(self._d) > self.capacity:
+            self._drop(next(iter(self._d)))
+        return e
+
+    def _drop(self, key):
+        e = self._d.pop(key)
+        dev.synchronize()
+        _lib.load().kkb_kk_plan_destroy(e["plan"])
+
+    def clear(self):
+        while self._d:
+            self._drop(next(iter(self._d)))
+
+    def run_host(self, data, luts, weights, fs, shift, linear, out):
+        """(N, M, T) complex64 host traces -> `out` (X, Z) complex128, in place."""
+        t = dev.require_cuda()
+        n, m, T = (int(x) for x in data.shape)
+        nx, nz = out.shape
+        e = self.entry(luts, n, m, T, nx, nz, weights, fs, shift, linear)
+        np.copyto(e["in_h"].numpy(), data, casting="same_kind")
+        s = t.cuda.current_stream()
+        e["in_d"].copy_(e["in_h"], non_blocking=True)
+        _lib.call("kkb_kk_plan_run", e["plan"], dev.ptr(e["in_d"]), 1, 0, dev.ptr(e["out_d"]),
+                  _lib.KKB_OUT_C128, 0, None, None, dev.stream_handle(s))
+        e["out_h"].copy_(e["out_d"], non_blocking=True)
+        s.synchronize()
+        out[...] = e["out_h"].numpy()
+        return out
+
+
+kk_plans = _KKPlanCache()
+
+
 def kk(rfc: CompressedRF, luts: DelayLUTSet, config: BeamformConfig = BeamformConfig()) -> ComplexImage:
     """Beamform decomposed plane-wave traces onto the LUT grid (beamform.py:340-375)."""
     _check_common(luts, rfc.params, "kk")
@@ -193,10 +275,10 @@ def kk(rfc: CompressedRF, luts: DelayLUTSet, config: BeamformConfig = BeamformCo
     w = _resolve_weights(config, rfc.receive_angles.num_angles, "kk")
     fs = rfc.sampling_frequency
     shift = (config.pulse_delay - rfc.params.start_time) * fs
-    out = kk_device(dev.to_device(rfc.data), luts, fs, shift,
-                    linear=config.interpolation == "linear", weights=w)
-    dev.synchronize()
-    return ComplexImage(dev.to_host(out), luts.grid)
+    out = np.empty((luts.grid.nx, luts.grid.nz), dtype=np.complex128)
+    kk_plans.run_host(rfc.data, (luts.lut_tx_x, luts.lut_tx_z, luts.lut_rx_x, luts.lut_rx_z), w, fs,
+                      shift, config.interpolation == "linear", out)
+    return ComplexImage(out, luts.grid)
 
 
 def das(rf: AnalyticRF, luts: DelayLUTSet, config: BeamformConfig = BeamformConfig()) -> ComplexImage:

@@ -198,11 +198,15 @@ extern "C" int kkb_kk_plan_create(const double *ltx, const double *ltz, const do
     if ((st = transpose_f64(ltz, nz, n_tx, p->ltzT, s))) return fail(st);
     if ((st = transpose_f64(lrz, nz, n_rx, p->lrzT, s))) return fail(st);
     if ((st = kk_window(ltx, ltz, lrx, lrz, n_tx, n_rx, nx, nz, fs, shift, &p->win, s))) return fail(st);
+    if ((st = kk_check_windows(ltx, ltz, lrx, lrz, n_tx, n_rx, n_t, nx, nz, fs, shift, linear, &p->win, s)))
+        return fail(st);
     *out = p;
     return KKB_OK;
 }
 
 extern "C" int kkb_kk_plan_window(const kkb_kk_plan *p) { return p ? p->win.big : -1; }
+
+extern "C" int kkb_kk_plan_window_check(const kkb_kk_plan *p) { return p ? p->win.bad : -1; }
 
 extern "C" int kkb_kk_last_instance(void) { return kk_last_instance(); }
 

@@ -40,6 +40,10 @@
 #ifndef KKB_KK_FR
 #define KKB_KK_FR 2              // frames per CTA of the batched (big-tile) gather
 #endif
+#ifndef KKB_KK_CHECK
+#define KKB_KK_CHECK 0           // 1: K5 also checks every tap's window index in the loop (debug;
+                                 // +11% K5 time; kk_check_windows proves it per plan instead)
+#endif
 #ifndef KKB_KK_QUNROLL
 #define KKB_KK_QUNROLL 1         // receive-loop unroll of the gather
 #endif
@@ -58,6 +62,7 @@ int transpose_f64(const double *in, int rows, int cols, double *out, cudaStream_
 // shared-memory trace window (samples) one tile of each instance needs
 struct KKWindows {
     int big, mid, small;
+    int bad;  // bit (1 << KKB_KK_INST_*): instance whose window failed kk_check_windows
 };
 // Synchronises `s` (one launch for the three tile sizes).
 int kk_window(const double *ltx, const double *ltz, const double *lrx, const double *lrz, int N,
@@ -90,6 +95,13 @@ int kk_gather(const float2 *data, int N, int M, int T, const double *ltx, const 
               int accum = 0, const KKScatter *sc = nullptr,
               long long data_ns = 0,  // 0: M*T (dense (N, M, T) traces)
               const KKSets *sets = nullptr);
+
+// Plan-time proof that no tap of these tables leaves its tile's staged window
+// (every tile size whose window fits; synchronises `s`): sets win->bad, and
+// the device error word on a failure.
+int kk_check_windows(const double *ltx, const double *ltz, const double *lrx, const double *lrz,
+                     int N, int M, int T, int nx, int nz, double fs, double shift, int linear,
+                     KKWindows *win, cudaStream_t s);
 
 // instance the last kk_gather dispatch launched (KKB_KK_INST_*, include/kkb.h)
 int kk_last_instance();

@@ -242,6 +242,13 @@ int kk_window(const double *ltx, const double *ltz, const double *lrx, const dou
     win->big = (h[0] + 1) & ~1;
     win->mid = (h[1] + 1) & ~1;
     win->small = (h[2] + 1) & ~1;
+    win->bad = 0;
+    if (const char *k = getenv("KKB_KK_WINDOW_SHRINK")) {  // fault injection (tests): undersized windows
+        const int d = atoi(k);
+        win->big = std::max(2, win->big - d);
+        win->mid = std::max(2, win->mid - d);
+        win->small = std::max(2, win->small - d);
+    }
     return KKB_OK;
 }
 
@@ -442,7 +449,9 @@ k_kk_gather(const KKArgs a) {
 
     float accr[FR][2][CX], acci[FR][2][CX];  // float32 per-pixel sums, fixed order
     double t1[2][CX];
+#if KKB_KK_CHECK
     unsigned emax = 0;  // largest raw window index over live pairs (must stay in the window)
+#endif
 #pragma unroll
     for (int fr = 0; fr < FR; ++fr)
 #pragma unroll
@@ -512,7 +521,9 @@ k_kk_gather(const KKArgs a) {
 #pragma unroll kQUnroll
         for (int q = 0; q < mc; ++q) {
             const int m = m0 + q;
+#if KKB_KK_CHECK
             unsigned eq = 0;  // largest raw window index of this pair's taps (clamp check)
+#endif
             const double2 lz = reinterpret_cast<const double2 *>(lrz_p + m * TZ)[zq];
             double lxv[CX];
 #pragma unroll
@@ -534,7 +545,9 @@ k_kk_gather(const KKArgs a) {
                     const double fi = kk_delay(t1[p][r], p ? lz.y : lz.x, lxv[r], fs, shift);
                     const double sv = __dadd_rd(LINEAR ? fi : __dadd_rn(fi, 0.5), KKB_FLOOR_MAGIC2);
                     const unsigned raw = (unsigned)(__double2hiint(sv) - loC);
+#if KKB_KK_CHECK
                     eq = max(eq, raw);
+#endif
                     const unsigned e = min(raw, (unsigned)(LINEAR ? W - 2 : W - 1));
                     const float f1 = __uint_as_float(((unsigned)__double2loint(sv) >> 9) + 0x3F800000u);
 #pragma unroll
@@ -554,7 +567,9 @@ k_kk_gather(const KKArgs a) {
             }
             // a clamped index reads a wrong entry unless the pair's whole window
             // lies outside the trace (every entry zero, e.g. |fi| >= 2^19)
+#if KKB_KK_CHECK
             if (lw.x <= (LINEAR ? T - 2 : T - 1) && lw.x + W > 0) emax = max(emax, eq);
+#endif
         }
         if constexpr (MS) {
             if (set_done) {
@@ -612,7 +627,9 @@ k_kk_gather(const KKArgs a) {
         ch = ch1;
     }
 
+#if KKB_KK_CHECK
     if (emax > (unsigned)(LINEAR ? W - 2 : W - 1)) atomicOr(&g_device_error, KKB_DEVERR_KK_WINDOW);
+#endif
     if constexpr (MS) return;  // every set's epilogue ran inside the loop
 
     // epilogue: IQ (+ fused intensity and frame max), per frame
@@ -748,24 +765,28 @@ int kk_last_instance() { return g_last_instance.load(); }
 constexpr int kKKEPT = KKB_KK_STAGE_ELEMS / (32 * KKB_KK_WZ * KKB_KK_WX);
 
 struct InstanceShape {
-    int tz, tx, stage, W, resident;  // resident: CTAs per SM the launch bounds aim for
+    int tz, tx, stage, W, resident, warps;  // resident: CTAs per SM the launch bounds aim for
 };
 
 static InstanceShape instance_shape(int inst, const KKWindows &win) {
     switch (inst) {
         case KKB_KK_INST_SMALL:
             return {KKB_KK_S_TZ, KKB_KK_S_TX, kKKEPT * 32 * KKB_KK_S_WZ * KKB_KK_S_WX,
-                    std::max(2, win.small), KKB_KK_MIN_CTAS * KKB_KK_WZ * KKB_KK_WX / (KKB_KK_S_WZ * KKB_KK_S_WX)};
+                    std::max(2, win.small), KKB_KK_MIN_CTAS * KKB_KK_WZ * KKB_KK_WX / (KKB_KK_S_WZ * KKB_KK_S_WX),
+                    KKB_KK_S_WZ * KKB_KK_S_WX};
         case KKB_KK_INST_MID:
             return {KKB_KK_M_TZ, KKB_KK_M_TX, kKKEPT * 32 * KKB_KK_M_WZ * KKB_KK_M_WX,
-                    std::max(2, win.mid), KKB_KK_MIN_CTAS * KKB_KK_WZ * KKB_KK_WX / (KKB_KK_M_WZ * KKB_KK_M_WX)};
+                    std::max(2, win.mid), KKB_KK_MIN_CTAS * KKB_KK_WZ * KKB_KK_WX / (KKB_KK_M_WZ * KKB_KK_M_WX),
+                    KKB_KK_M_WZ * KKB_KK_M_WX};
         default:
-            return {KKB_KK_TZ, KKB_KK_TX, KKB_KK_STAGE_ELEMS, std::max(2, win.big), KKB_KK_MIN_CTAS};
+            return {KKB_KK_TZ, KKB_KK_TX, KKB_KK_STAGE_ELEMS, std::max(2, win.big), KKB_KK_MIN_CTAS,
+                    KKB_KK_WZ * KKB_KK_WX};
     }
 }
 
 static bool instance_fits(int inst, int N, int M, bool linear, const KKWindows &win, int n_frames) {
     if (inst == KKB_KK_INST_DIRECT) return true;
+    if (win.bad & (1 << inst)) return false;  // kk_check_windows found a tap outside its window
     const InstanceShape sh = instance_shape(inst, win);
     const int fr = inst == KKB_KK_INST_BIG_FR ? KKB_KK_FR : 1;
     if (inst == KKB_KK_INST_BIG_FR && (n_frames < 2 || KKB_KK_FR < 2)) return false;
@@ -773,11 +794,111 @@ static bool instance_fits(int inst, int N, int M, bool linear, const KKWindows &
            kk_smem_bytes(N, M, sh.W, 1, linear, sh.tz, sh.tx, fr) <= 200 * 1024;
 }
 
-// The largest tile whose grid fills every SM with the CTAs its launch bounds
-// aim for (big tiles share the tables and index setup over more pixels; two
-// frames per CTA also share every tap's index math); below that, the largest
-// tile that fits at all.  KKB_KK_INST forces an instance when it fits
-// (KKB_KK_DIRECT=1 / KKB_KK_SMALL=1 / KKB_KK_FR1=1: older test hooks).
+// Wave model of one launch (profiles/r02a_instance_sweep.jsonl: config-5 row
+// blocks at 1-8 ranks, config-4 batches of 1-400 frames, configs 1-3): the
+// busiest SM runs ceil(CTAs / SMs) CTAs; with k of them resident at once it
+// sustains eff(k x warps) of its full-occupancy rate (a lone 8-warp CTA
+// reaches ~0.88: the shared-memory pipe is the limiter, not latency); the
+// full-occupancy cost per pixel-pair differs by instance (measured at 400
+// frames: two frames per CTA 1.00, one 1.02, 32 x 32 tiles 1.07, 16 x 16
+// tiles 1.42 — smaller tiles stage the same windows and tables for fewer
+// pixels).  The dispatch takes the instance with the smallest modelled time.
+static double instance_cost(int inst, long long ctas, long long sms) {
+    static const double rel[5] = {0.0, 1.42, 1.07, 1.02, 1.00};
+    const InstanceShape sh = instance_shape(inst, KKWindows{2, 2, 2, 0});
+    const int fr = inst == KKB_KK_INST_BIG_FR ? KKB_KK_FR : 1;
+    const long long per_sm = ceil_div(ctas, sms);
+    const double resident = (double)std::min<long long>(per_sm, sh.resident);
+    const double eff = std::min(1.0, 0.75 + resident * sh.warps / 64.0);
+    return (double)per_sm * sh.tz * sh.tx * fr * rel[inst] / eff;
+}
+
+// ------------------------------------------------------------- plan-time window proof
+// Every (pixel, pair) of one tile size, evaluated with the gather's own index
+// arithmetic (kk_delay, the round-down magic add, the window start from the
+// tile's corner delays): flags the tile size in *bad (and the device error
+// word) if any tap's window index would leave [0, W-2] (linear) / [0, W-1]
+// (nearest) while the pair's window overlaps the trace.  The tables are fixed
+// per plan and the index math is frame-independent, so one pass at plan
+// creation proves the clamp in k_kk_gather (e = min(raw, W-2)) never changes
+// a tap for any launch of the plan; an instance that fails is not dispatched.
+template <bool LINEAR>
+__global__ void __launch_bounds__(256)
+k_kk_window_check(const double *__restrict__ ltx, const double *__restrict__ ltz,
+                  const double *__restrict__ lrx, const double *__restrict__ lrz, int N, int M,
+                  int T, int nx, int nz, int TX, int TZ, int W, double fs, double shift, int bit,
+                  int *bad) {
+    extern __shared__ int lo_s[];  // [M]
+    const int tiles_z = (nz + TZ - 1) / TZ;
+    const int tz = blockIdx.x % tiles_z, tx = blockIdx.x / tiles_z, n = blockIdx.y;
+    const int iz0 = tz * TZ, ix0 = tx * TX;
+    const int rzb = min(TZ - 1, nz - 1 - iz0), cxb = min(TX - 1, nx - 1 - ix0);
+    for (int m = threadIdx.x; m < M; m += blockDim.x) {
+        double lo = 1e300;
+        for (int cr = 0; cr < 2; ++cr)
+            for (int cc = 0; cc < 2; ++cc) {
+                const int iz = iz0 + (cr ? rzb : 0), ix = ix0 + (cc ? cxb : 0);
+                const double t1 = __dadd_rn(ltx[(long long)ix * N + n], ltz[(long long)iz * N + n]);
+                lo = fmin(lo, kk_delay(t1, lrz[(long long)iz * M + m], lrx[(long long)ix * M + m], fs, shift));
+            }
+        lo_s[m] = (int)fmax(fmin(floor(lo) - 1.0, 1.0e9), -1.0e9);
+    }
+    __syncthreads();
+    const unsigned lim = (unsigned)(LINEAR ? W - 2 : W - 1);
+    const int rows = rzb + 1, total = rows * (cxb + 1) * M;
+    bool badf = false;
+    for (int i = threadIdx.x; i < total; i += blockDim.x) {
+        const int m = i % M, px = i / M, r = px % rows, c = px / rows;
+        const int iz = iz0 + r, ix = ix0 + c, lo = lo_s[m];
+        const double t1 = __dadd_rn(ltx[(long long)ix * N + n], ltz[(long long)iz * N + n]);
+        const double fi = kk_delay(t1, lrz[(long long)iz * M + m], lrx[(long long)ix * M + m], fs, shift);
+        const double sv = __dadd_rd(LINEAR ? fi : __dadd_rn(fi, 0.5), KKB_FLOOR_MAGIC2);
+        const unsigned raw = (unsigned)(__double2hiint(sv) - (lo + KKB_MAGIC2_HI));
+        const bool live = lo <= (LINEAR ? T - 2 : T - 1) && lo + W > 0;
+        badf |= live && raw > lim;
+    }
+    if (__syncthreads_or(badf) && threadIdx.x == 0) {
+        atomicOr(bad, bit);
+        atomicOr(&g_device_error, KKB_DEVERR_KK_WINDOW);
+    }
+}
+
+int kk_check_windows(const double *ltx, const double *ltz, const double *lrx, const double *lrz,
+                     int N, int M, int T, int nx, int nz, double fs, double shift, int linear,
+                     KKWindows *win, cudaStream_t s) {
+    win->bad = 0;
+    if ((size_t)M * sizeof(int) > 48 * 1024) return KKB_OK;  // huge pair tables: no tile fits anyway
+    int *d = nullptr;
+    KKB_TRY_CUDA(cudaMallocAsync(&d, sizeof(int), s), "cudaMallocAsync(window check)");
+    KKB_TRY_CUDA(cudaMemsetAsync(d, 0, sizeof(int), s), "memset(window check)");
+    const int insts[3] = {KKB_KK_INST_BIG, KKB_KK_INST_MID, KKB_KK_INST_SMALL};
+    for (int k = 0; k < 3; ++k) {
+        const InstanceShape sh = instance_shape(insts[k], *win);
+        if (sh.W > sh.stage) continue;  // this tile size never runs (per-pixel kernel instead)
+        const long long tiles = ceil_div(nz, sh.tz) * ceil_div(nx, sh.tx);
+        if (tiles > 0x7fffffffLL || N > 65535) continue;
+        dim3 grid((unsigned)tiles, (unsigned)N);
+        const size_t smem = sizeof(int) * (size_t)M;
+        if (linear)
+            k_kk_window_check<true><<<grid, 256, smem, s>>>(ltx, ltz, lrx, lrz, N, M, T, nx, nz, sh.tx,
+                                                            sh.tz, sh.W, fs, shift, 1 << insts[k], d);
+        else
+            k_kk_window_check<false><<<grid, 256, smem, s>>>(ltx, ltz, lrx, lrz, N, M, T, nx, nz, sh.tx,
+                                                             sh.tz, sh.W, fs, shift, 1 << insts[k], d);
+        KKB_CHECK_LAUNCH("k_kk_window_check");
+    }
+    int h = 0;
+    KKB_TRY_CUDA(cudaMemcpyAsync(&h, d, sizeof(int), cudaMemcpyDeviceToHost, s), "copy window check");
+    KKB_TRY_CUDA(cudaStreamSynchronize(s), "sync window check");
+    cudaFreeAsync(d, s);
+    // a tile size that failed disables its instances (big covers both frame counts)
+    win->bad = h | ((h & (1 << KKB_KK_INST_BIG)) ? (1 << KKB_KK_INST_BIG_FR) : 0);
+    return KKB_OK;
+}
+
+// KKB_KK_INST forces an instance when it fits (KKB_KK_DIRECT=1 /
+// KKB_KK_SMALL=1 / KKB_KK_FR1=1: older test hooks); the per-pixel kernel
+// runs when no tile's window fits its stage.
 static int select_instance(int N, int M, int nx, int nz, int n_frames, bool linear, const KKWindows &win) {
     static const int order[4] = {KKB_KK_INST_BIG_FR, KKB_KK_INST_BIG, KKB_KK_INST_MID, KKB_KK_INST_SMALL};
     auto fits = [&](int i) { return instance_fits(i, N, M, linear, win, n_frames); };
@@ -794,17 +915,20 @@ static int select_instance(int N, int M, int nx, int nz, int n_frames, bool line
     if (env1("KKB_KK_SMALL") && fits(KKB_KK_INST_SMALL)) return KKB_KK_INST_SMALL;
     const bool no_fr = env1("KKB_KK_FR1");
     const long long sms = sm_count();
-    int largest_fit = KKB_KK_INST_DIRECT;
+    int best = KKB_KK_INST_DIRECT;
+    double best_cost = 0.0;
     for (int inst : order) {
         if ((inst == KKB_KK_INST_BIG_FR && no_fr) || !fits(inst)) continue;
-        if (largest_fit == KKB_KK_INST_DIRECT) largest_fit = inst;
         const InstanceShape sh = instance_shape(inst, win);
         const int fr = inst == KKB_KK_INST_BIG_FR ? KKB_KK_FR : 1;
         const long long ctas = ceil_div(nz, sh.tz) * ceil_div(nx, sh.tx) * ceil_div(n_frames, fr);
-        if (ctas >= sh.resident * sms) return inst;
+        const double c = instance_cost(inst, ctas, sms);
+        if (best == KKB_KK_INST_DIRECT || c < best_cost) {
+            best = inst;
+            best_cost = c;
+        }
     }
-    return largest_fit == KKB_KK_INST_DIRECT ? KKB_KK_INST_DIRECT
-           : (fits(KKB_KK_INST_SMALL) ? KKB_KK_INST_SMALL : largest_fit);
+    return best;
 }
 
 int kk_gather(const float2 *data, int N, int M, int T, const double *ltx, const double *ltzT,

@@ -31,17 +31,11 @@ from . import _lib
 
 
 def _launch_kk(data, ltx, ltz, lrx, lrz, weights, fs, shift, linear, out):
-    t = dev.require_cuda()
-    d = [dev.to_device(np.ascontiguousarray(a)) for a in (data, ltx, ltz, lrx, lrz)]
-    n, m, T = data.shape
-    nx, nz = out.shape
-    w = dev.to_device(np.ascontiguousarray(weights, dtype=np.float64))
-    o = t.empty((nx, nz), dtype=t.complex128, device="cuda")
-    _lib.call("kkb_kk", dev.ptr(d[0]), n, m, T, dev.ptr(d[1]), dev.ptr(d[2]), dev.ptr(d[3]),
-              dev.ptr(d[4]), nx, nz, dev.ptr(w), float(fs), float(shift), int(bool(linear)),
-              dev.ptr(o), _lib.KKB_OUT_C128, 1, 0, 0, None, None, dev.stream_handle())
-    dev.synchronize()
-    out[...] = dev.to_host(o)
+    # plan cached across calls on the same tables (beamform._KKPlanCache):
+    # one H2D of the traces, one gather launch, one D2H of the image per call
+    from .beamform import kk_plans
+
+    kk_plans.run_host(data, (ltx, ltz, lrx, lrz), weights, fs, shift, linear, out)
 
 
 def kk_kernel(data, ltx, ltz, lrx, lrz, weights, fs, shift, linear, out):

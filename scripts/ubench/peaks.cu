@@ -23,8 +23,8 @@ __global__ void k_lds128(int iters, float *out) {
     for (int i = 0; i < iters; ++i) {
         const unsigned ai = a ^ ((i & 1) << 13);
         float x, y, z, w, x1, y1, z1, w1;
-        asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(x), "=f"(y), "=f"(z), "=f"(w) : "r"(ai) : "memory");
-        asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4+16384];" : "=f"(x1), "=f"(y1), "=f"(z1), "=f"(w1) : "r"(ai) : "memory");
+        asm volatile("ld.volatile.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(x), "=f"(y), "=f"(z), "=f"(w) : "r"(ai) : "memory");
+        asm volatile("ld.volatile.shared.v4.f32 {%0,%1,%2,%3}, [%4+16384];" : "=f"(x1), "=f"(y1), "=f"(z1), "=f"(w1) : "r"(ai) : "memory");
         acc0 += (x + y) + (z + w);
         acc1 += (x1 + y1) + (z1 + w1);
     }
@@ -85,7 +85,11 @@ static float timed(F launch) {
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
     launch();  // warm-up
-    cudaDeviceSynchronize();
+    cudaError_t le = cudaGetLastError();
+    if (le != cudaSuccess || (le = cudaDeviceSynchronize()) != cudaSuccess) {
+        fprintf(stderr, "launch failed: %s\n", cudaGetErrorString(le));
+        return -1.f;
+    }
     float best = 1e30f;
     for (int r = 0; r < 5; ++r) {
         cudaEventRecord(e0);
@@ -108,8 +112,8 @@ int main() {
     cudaMalloc(&outd, 16);
     printf("{\n \"tool\": \"scripts/ubench/peaks.cu\",\n \"sm_count\": %d,\n", sms);
 
-    {   // LDS.128: 2 CTAs x 1024 threads per SM, 2 loads of 16 B per thread per iteration
-        const int threads = 1024, blocks = sms * 2, iters = 1 << 15;
+    {   // LDS.128: 4 CTAs x 512 threads per SM, 2 loads of 16 B per thread per iteration
+        const int threads = 512, blocks = sms * 4, iters = 1 << 13;
         float ms = timed([&] { k_lds128<<<blocks, threads>>>(iters, outf); });
         double bytes = (double)blocks * threads * iters * 2 * 16;
         double cyc = mean_cycles(blocks);
@@ -118,8 +122,8 @@ int main() {
                "\"ms\": %.3f, \"what\": \"conflict-free LDS.128, 2048 threads/SM\", \"err\": \"%s\"},\n",
                bytes / (ms * 1e-3) / 1e9, bytes / (cyc * sms), mhz, ms, cudaGetErrorString(cudaGetLastError()));
     }
-    {   // FFMA: 8 independent chains, 2 x 1024 threads per SM
-        const int threads = 1024, blocks = sms * 2, iters = 1 << 14;
+    {   // FFMA: 8 independent chains, 4 x 512 threads per SM
+        const int threads = 512, blocks = sms * 4, iters = 1 << 14;
         float ms = timed([&] { k_ffma<8><<<blocks, threads>>>(iters, outf); });
         double flops = 2.0 * blocks * threads * (double)iters * 8;
         double cyc = mean_cycles(blocks);
@@ -129,7 +133,7 @@ int main() {
                cudaGetErrorString(cudaGetLastError()));
     }
     {   // DADD: 8 independent chains
-        const int threads = 1024, blocks = sms * 2, iters = 1 << 12;
+        const int threads = 512, blocks = sms * 4, iters = 1 << 12;
         float ms = timed([&] { k_dadd<8><<<blocks, threads>>>(iters, outd); });
         double ops = (double)blocks * threads * iters * 8;
         double cyc = mean_cycles(blocks);

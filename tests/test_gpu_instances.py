@@ -1,10 +1,11 @@
 """The K5 instance bench.py times, pinned to the oracle.
 
 bench.py's step gathers 400 config-4 frames per launch, which dispatches to
-the 32 x 64-tile instance with two frames per CTA (KKB_KK_INST_BIG_FR).  The
-batches here are large enough to reach it through the normal dispatch (the
-test asserts that they did, via kkb_kk_last_instance), one with an odd frame
-count so the last CTA runs the one-frame tail.  Every frame is compared with
+the 32 x 64-tile instance with two frames per CTA (KKB_KK_INST_BIG_FR).  A
+63-frame batch reaches it through the normal dispatch, 16- and 11-frame
+batches are forced onto it; the test asserts which instance ran (via
+kkb_kk_last_instance), and the odd frame counts make the last CTA run the
+one-frame tail.  Every frame is compared with
 the oracle (reference kk on the oracle's own decomposition) and with a
 single-frame launch of the same traces, which dispatches to the 16 x 16
 instance: the per-pixel sums run in the same order, so they must agree bit
@@ -32,8 +33,11 @@ def _frames(w, F, seed0):
                      for f in range(F)])
 
 
-@pytest.mark.parametrize("F", [21, 24])
-def test_bench_instance_matches_oracle_every_frame(oracle, F):
+@pytest.mark.parametrize("F,force", [(63, None), (16, "big_fr"), (11, "big_fr")])
+def test_bench_instance_matches_oracle_every_frame(oracle, monkeypatch, F, force):
+    """63 frames reach the two-frames-per-CTA instance through the default
+    dispatch (odd: the last CTA runs the one-frame tail); 16 and 11 frames are
+    forced onto it (KKB_KK_INST=big_fr)."""
     import torch
 
     w = configs.config4(frames=F)
@@ -41,8 +45,11 @@ def test_bench_instance_matches_oracle_every_frame(oracle, F):
     fs, c = arr.sampling_frequency, p.sound_speed
     rf = _frames(w, F, 700)
     eng = kb.KKEngine(arr, p, rx, g, frames=F, want_db=False)
+    if force:
+        monkeypatch.setenv("KKB_KK_INST", force)
     iq = eng.run(torch.from_numpy(rf).cuda()).clone()
     torch.cuda.synchronize()
+    monkeypatch.delenv("KKB_KK_INST", raising=False)
     assert _lib.last_instance() == _lib.KKB_KK_INST_BIG_FR
     assert _lib.take_device_error() == 0
     # every frame again as a one-frame launch (16 x 16 instance): bit-identical
@@ -94,10 +101,10 @@ def test_every_instance_bit_identical(monkeypatch):
     eng.close()
 
 
-def test_dispatch_fills_the_sms():
-    """The default dispatch picks the largest tile whose grid fills every SM
-    (bench workload: two frames per CTA; one config-1 frame: 16 x 16 tiles;
-    one config-5 frame: 32 x 64 tiles)."""
+def test_dispatch_follows_the_wave_model():
+    """The default dispatch (wave model, kk_gather.cu select_instance) on the
+    measured shapes: bench workload -> two frames per CTA; one config-1 frame
+    -> 16 x 16 tiles; one config-5 frame -> 32 x 64 tiles."""
     import torch
 
     for cfg, F, want in ((4, 400, _lib.KKB_KK_INST_BIG_FR), (1, 1, _lib.KKB_KK_INST_SMALL),

@@ -11,8 +11,12 @@ and window rule (beamform.py:225-235), so a bit-exact image proves, for every
 addressing (per-frame window blocks of the two-frames-per-CTA instance, the
 odd-frame tail, the clamp at the window end) of the kernel that runs in the
 benchmark — not of the kk_taps diagnostic twin.  One frame per pair puts all
-N*M pairs in one batched launch.  The device error word must stay clear
-(KKB_DEVERR_KK_WINDOW: a tap index clamped at the window end).
+N*M pairs in one batched launch.  Every plan also proves at creation
+(kk_check_windows: every (pixel, pair) through the gather's own index
+arithmetic against each tile size's staged window) that no tap can be
+clamped at its window's end: kkb_kk_plan_window_check must be 0 and the
+device error word (KKB_DEVERR_KK_WINDOW) clear; a fault-injection test shows
+the proof catching undersized windows and the dispatch routing around them.
 
 Tolerance: bit-exact (torch.equal / np.array_equal).
 """
@@ -27,7 +31,7 @@ pytestmark = pytest.mark.gpu
 from paper_2603_22496_b200 import _device as dev  # noqa: E402
 from paper_2603_22496_b200 import _lib, configs  # noqa: E402
 
-INSTANCES = ["natural", "big", "mid", "small", "direct"]
+INSTANCES = ["natural", "big_fr", "big", "mid", "small", "direct"]
 CODE = {"big_fr": _lib.KKB_KK_INST_BIG_FR, "big": _lib.KKB_KK_INST_BIG, "mid": _lib.KKB_KK_INST_MID,
         "small": _lib.KKB_KK_INST_SMALL, "direct": _lib.KKB_KK_INST_DIRECT}
 
@@ -94,12 +98,11 @@ def test_production_gather_taps_bit_exact(oracle, monkeypatch, cfg, linear):
     ref = torch.from_numpy(np.ascontiguousarray(np.moveaxis(exp.reshape(g.nx, g.nz, N * M), -1, 0)))
     data = _encoded(pairs, N, M, T)
     kp, keep = _plan(luts, N, M, T, g.nx, g.nz, fs, shift, linear)
+    assert _lib.load().kkb_kk_plan_window_check(kp) == 0   # every tile size proven at plan time
     try:
         for inst in INSTANCES:
             out, code = _run(kp, data, g.nx, g.nz, monkeypatch, inst)
-            if inst == "natural":
-                assert code == _lib.KKB_KK_INST_BIG_FR, code   # 121 frames fill the SMs with 2/CTA
-            else:
+            if inst != "natural":
                 assert code == CODE[inst], (inst, code)
             bad = (out.cpu() != ref)
             assert not bool(bad.any()), (cfg, linear, inst, int(bad.sum()))
@@ -183,4 +186,35 @@ def test_production_gather_taps_config5_row_block(oracle, monkeypatch, linear):
                 assert not bool(bad.any()), (n, linear, inst, int(bad.sum()))
             del data
     finally:
+        _lib.load().kkb_kk_plan_destroy(kp)
+
+
+def test_window_proof_catches_undersized_windows(oracle, monkeypatch):
+    """Fault injection: KKB_KK_WINDOW_SHRINK makes every staged window too
+    short.  The plan-time proof must flag the tile sizes whose taps would be
+    clamped (and raise the device error word), the dispatch must then avoid
+    them, and the image must stay identical to the correctly sized plan's."""
+    import torch
+
+    w = configs.config4(frames=1)
+    arr, p, rx, g = w.array, w.params, w.receive, w.grid
+    N, M, T, fs = p.num_transmits, rx.num_angles, p.num_samples, arr.sampling_frequency
+    shift = (0.0 - p.start_time) * fs
+    luts = _luts(oracle, w)
+    pairs = [(n, m) for n in range(N) for m in range(M)]
+    data = _encoded(pairs, N, M, T)
+    good, keep_g = _plan(luts, N, M, T, g.nx, g.nz, fs, shift, True)
+    assert _lib.take_device_error() == 0
+    ref, _ = _run(good, data, g.nx, g.nz, monkeypatch, "natural")
+    monkeypatch.setenv("KKB_KK_WINDOW_SHRINK", "6")
+    bad, keep_b = _plan(luts, N, M, T, g.nx, g.nz, fs, shift, True)
+    monkeypatch.delenv("KKB_KK_WINDOW_SHRINK")
+    flags = _lib.load().kkb_kk_plan_window_check(bad)
+    assert flags != 0
+    assert _lib.take_device_error() & _lib.KKB_DEVERR_KK_WINDOW
+    for inst in INSTANCES:
+        out, code = _run(bad, data, g.nx, g.nz, monkeypatch, inst)
+        assert not (flags & (1 << code)), (inst, code, flags)   # a flagged instance never runs
+        assert torch.equal(out, ref), inst
+    for kp in (good, bad):
         _lib.load().kkb_kk_plan_destroy(kp)
