@@ -167,6 +167,16 @@ def cpu_pipeline_rate(w, seconds: float = 12.0, min_frames: int = 2, threads: in
     return n / dt, n, dt
 
 
+def _config(w, frames, world):
+    """The `config` object of both arms (identical keys and values)."""
+    g, p = w.grid, w.params
+    return {"workload": w.name, "frames_per_rank": frames, "N_tx": p.num_transmits,
+            "M_rx": w.receive.num_angles, "L_el": w.array.num_elements, "T": p.num_samples,
+            "grid": [g.nx, g.nz], "pixel_pairs_per_frame": g.nx * g.nz * w.pairs,
+            "l2": "inputs larger than L2 (3.46 GB RF per rank), no flush",
+            "parallelism": f"frame-sharded x{world}"}
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -190,11 +200,12 @@ def run_reference(args):
         "vs_baseline": None, "dtype": "f32",
         "dtype_detail": "complex64 stage 1 and traces, float64 delay-index math, complex128 image accumulation",
         "data": "synthetic (seeded noise RF, reference bench.noise_volume)",
-        "config": {"workload": w.name, "frames_per_step": 2, "pixel_pairs_per_frame": pp},
+        "config": _config(w, args.frames, int(os.environ.get("WORLD_SIZE", "1"))),
         "pixel_pair_samples_per_s": value * pp,
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "cpu": cpu_model(),
-                         "sample": "2 frames per step of the workload: numpy/scipy complex64 "
-                                   "stage 1 (bench.py:113-138 form) + C/OpenMP kk loop (all cores)"},
+                         "sample": f"2 frames per step of the {args.frames}-frame workload: numpy/scipy "
+                                   "complex64 stage 1 (bench.py:113-138 form) + C/OpenMP kk loop "
+                                   "(all cores)"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
@@ -216,6 +227,18 @@ def _init_dist(torch, dist, world, local):
         else:
             dist.init_process_group(backend)
     return local
+
+
+def _onchip_peaks():
+    """Measured shared-memory (LDS.128) and FP32 FMA peaks of this B200
+    (scripts/ubench/peaks.cu, profiles/r02_onchip_peaks.json); the driver's
+    MEASURED_PEAKS.json has only HBM and bf16 tensor figures."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r02_onchip_peaks.json")) as f:
+            d = json.load(f)
+        return float(d["smem_lds128_GBps"]), float(d["fp32_fma_TFLOPs"]), "measured"
+    except (OSError, KeyError, ValueError):
+        return None, None, "missing"
 
 
 def _l2_roofline(achieved_taps):
@@ -377,7 +400,9 @@ def run_gpu(args):
     compulsory = fl * (N * M * T * 8 + P * (8 + 4)) + 8 * (g.nx + g.nz) * (N + M)
     achieved_hbm = compulsory / (kk_launch_ms / 1e3) / 1e9
     sm_mhz = clk.get("sm_mhz") or 1965.0
-    smem_peak = sm_count * 128 * sm_mhz * 1e6 / 1e9           # GB/s, 128 B/clk/SM crossbar
+    smem_meas, fp32_meas, onchip_kind = _onchip_peaks()
+    smem_derived = sm_count * 128 * sm_mhz * 1e6 / 1e9          # GB/s, 128 B/clk/SM crossbar
+    smem_peak = smem_meas or smem_derived
     achieved_taps = gather_bytes_alg / (kk_launch_ms / 1e3) / 1e9
     # stage 1 (K1-K3) is HBM-bound: bytes its three kernels must move per batch
     # (RF in, spectra written then read, contracted bins written then read,
@@ -389,7 +414,7 @@ def run_gpu(args):
     # SURVEY 8(d) flop units: contraction 8*N*L*M*K, FFTs 2.5*N*L*T*log2 T + 5*N*M*T*log2 T
     K = T // 2 + 1
     s1_flops = F * (8.0 * N * L * M * K + 2.5 * N * L * T * math.log2(T) + 5.0 * N * M * T * math.log2(T))
-    fp32_peak = 148 * 128 * 2 * (clk.get("sm_mhz") or 1965.0) * 1e6 / 1e12  # TFLOP/s, derived
+    fp32_peak = fp32_meas or sm_count * 128 * 2 * sm_mhz * 1e6 / 1e12  # TFLOP/s
     frame_bytes = 4.0 * N * L * T + 2 * 8.0 * N * M * T + 8.0 * P + 8.0 * (g.nx + g.nz) * (N + M)
 
     # ---- end to end through the public API: pinned host RF in, host IQ out ----
@@ -455,11 +480,7 @@ def run_gpu(args):
             "dtype": "f32",
             "dtype_detail": "complex64 spectra/traces/IQ, float32 taps and sums, float64 delay-index math",
             "data": "synthetic (seeded noise RF, shapes of BASELINE config 4)",
-            "config": {"workload": w.name, "frames_per_rank": F, "N_tx": N, "M_rx": M,
-                       "L_el": L, "T": T, "grid": [g.nx, g.nz],
-                       "pixel_pairs_per_frame": pp_frame,
-                       "l2": "inputs larger than L2 (3.46 GB RF per rank), no flush",
-                       "parallelism": f"frame-sharded x{world}"},
+            "config": _config(w, F, world),
             "pixel_pair_samples_per_s": value * pp_frame,
             "stage_ms_sequential": {"decompose(K1-K3)": dec_ms, "kk_gather(K5)": kk_ms,
                                     "db_map(K6)": det_ms},
@@ -467,20 +488,31 @@ def run_gpu(args):
             "value_int16_ingest": {"value": world * F / (q_ms / 1e3), "unit": UNIT, "ms_per_step": q_ms,
                                    "note": "same device-resident step on int16-quantised RF "
                                            "(converted exactly in the FFT load)"},
-            "roofline": {"kernel": "k_kk_gather", "bound": "hbm",
-                         "achieved": achieved_hbm, "peak": hbm_peak, "unit": "GB/s",
-                         "frac": achieved_hbm / hbm_peak, "traffic": _gather_traffic(fl),
+            # the binding roofline of the dominant kernel: K5's taps come from
+            # shared memory (16 B of taps per pixel-pair), against the
+            # measured LDS.128 peak; HBM and L2 figures are secondary
+            "roofline": {"kernel": "k_kk_gather", "bound": "smem",
+                         "achieved": achieved_taps, "peak": smem_peak, "unit": "GB/s",
+                         "frac": achieved_taps / smem_peak, "traffic": _gather_traffic(fl),
                          "launch_ms": kk_launch_ms, "frames_per_launch": fl,
-                         "algorithmic_bytes_per_launch": compulsory,
-                         "peak_kind": peak_kind,
-                         "algorithmic_bytes": "compulsory HBM per launch: traces read + IQ/intensity "
-                                              "write + tables (SURVEY 8d)"},
-            "onchip_roofline": {"kernel": "k_kk_gather", "bound": "smem",
-                                "achieved": achieved_taps, "peak": smem_peak, "unit": "GB/s",
-                                "frac": achieved_taps / smem_peak,
-                                "algorithmic_bytes": "16 B of taps per pixel-pair (SURVEY 8d)",
-                                "pixel_pairs_per_s": pp_frame * fl / (kk_launch_ms / 1e3),
-                                "pixel_pairs_per_s_isolated": pp_frame * F / (kk_ms / 1e3)},
+                         "algorithmic_bytes_per_launch": gather_bytes_alg,
+                         "algorithmic_bytes": "16 B of taps (two complex64 samples) per pixel-pair "
+                                              "(SURVEY 8d) x pixel-pairs per launch",
+                         "peak_kind": (f"{onchip_kind} (scripts/ubench/peaks.cu: conflict-free LDS.128 "
+                                       "on every SM, profiles/r02_onchip_peaks.json)") if smem_meas else
+                                      "derived (148 SMs x 128 B/clk x sampled SM clock)",
+                         "peak_derived_at_sampled_clock": smem_derived,
+                         "pixel_pairs_per_s": pp_frame * fl / (kk_launch_ms / 1e3),
+                         "pixel_pairs_per_s_isolated": pp_frame * F / (kk_ms / 1e3),
+                         "traffic_note": "ncu dram read+write per launch (newest profiles/r*_gather_traffic.json); "
+                                         "below the compulsory HBM bytes because the gather reads only "
+                                         "the trace samples the image's delays reach"},
+            "hbm_roofline": {"kernel": "k_kk_gather", "bound": "hbm",
+                             "achieved": achieved_hbm, "peak": hbm_peak, "unit": "GB/s",
+                             "frac": achieved_hbm / hbm_peak, "peak_kind": peak_kind,
+                             "algorithmic_bytes_per_launch": compulsory,
+                             "algorithmic_bytes": "compulsory HBM per launch: traces read + IQ/intensity "
+                                                  "write + tables (SURVEY 8d); not the binding bound"},
             "l2_roofline": _l2_roofline(achieved_taps),
             "frame_roofline": {"bound": "hbm", "bytes_per_frame": frame_bytes,
                                "achieved": value / world * frame_bytes / 1e9, "peak": hbm_peak,
@@ -488,17 +520,20 @@ def run_gpu(args):
                                "algorithmic_bytes": "SURVEY 8(d) compulsory HBM per frame: RF in "
                                                     "+ traces write/read + IQ out + tables"},
             "stage1_roofline": {"kernels": "k_r2c + k_contract_sym + k_c2c", "bound": "hbm",
-                                "achieved": s1_achieved, "peak": hbm_peak, "unit": "GB/s",
-                                "frac": s1_achieved / hbm_peak, "ms": dec_ms,
-                                "bytes_per_step": s1_bytes,
-                                "compulsory_frac": s1_min / (dec_ms / 1e3) / 1e9 / hbm_peak,
+                                "achieved": s1_min / (dec_ms / 1e3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
+                                "frac": s1_min / (dec_ms / 1e3) / 1e9 / hbm_peak, "ms": dec_ms,
+                                "algorithmic_bytes_per_step": s1_min,
+                                "algorithmic_bytes": "compulsory: RF in (float32) + decomposed traces out "
+                                                     "(complex64)",
+                                "structure_bytes_per_step": s1_bytes,
+                                "structure_frac": s1_achieved / hbm_peak,
+                                "structure_note": "bytes the three-kernel structure moves (RF in, spectra "
+                                                  "written and read back, contracted bins written and read "
+                                                  "back, traces out) over the same time",
                                 "tflops": s1_flops / (dec_ms / 1e3) / 1e12,
                                 "fp32_peak_tflops": fp32_peak,
-                                "flop_frac": s1_flops / (dec_ms / 1e3) / 1e12 / fp32_peak,
-                                "algorithmic_bytes": "RF in + spectra write/read + contracted "
-                                                     "bins write/read + traces out (three-kernel "
-                                                     "structure); compulsory_frac counts RF in + "
-                                                     "traces out only"},
+                                "fp32_peak_kind": onchip_kind if fp32_meas else "derived",
+                                "flop_frac": s1_flops / (dec_ms / 1e3) / 1e12 / fp32_peak},
             "gpu_launches": int(launches),
             "clocks": clk,
         }

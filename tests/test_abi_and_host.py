@@ -238,7 +238,8 @@ def test_no_device_means_loud_failure(monkeypatch):
 
 def test_bench_roofline_helpers_read_the_committed_profiles():
     """bench.py's roofline denominators come from committed measurements
-    (profiles/): the L2 read bandwidth and the gather's ncu DRAM traffic."""
+    (profiles/): the shared-memory (LDS.128) and FP32 peaks, the L2 read
+    bandwidth and the gather's ncu DRAM traffic."""
     import importlib.util
 
     spec = importlib.util.spec_from_file_location("bench_mod", os.path.join(ROOT, "bench.py"))
@@ -249,3 +250,11 @@ def test_bench_roofline_helpers_read_the_committed_profiles():
     t = bench._gather_traffic(400)
     assert 0.3e9 < t < 0.9e9
     assert bench._gather_traffic(200) == t / 2
+    smem, fp32, kind = bench._onchip_peaks()
+    assert kind == "measured" and 30000 < smem < 40000 and 60 < fp32 < 80
+    # both arms report the same config object
+    from paper_2603_22496_b200 import configs
+
+    w = configs.config4(frames=400)
+    c = bench._config(w, 400, 1)
+    assert c["workload"] == w.name and c["pixel_pairs_per_frame"] == 256 * 256 * 121
