@@ -18,6 +18,16 @@ Resolutions of BASELINE.json ambiguities (also recorded in DESIGN.md):
 * config 4: ``transmit_angles(11, 10 deg)``; grid z from 5 mm at lambda/4 so
   the image fits the T=1536 window; 400 frames per rank.
 * config 5: ``transmit_angles(31, 15 deg)`` x ``confocal_angles(31, 31, 15 deg)``.
+
+Media (``config2_medium``, ``config4_vessel_frame``): the BASELINE phantoms
+re-expressed with the reference's own phantom objects (simulate.py:136-184)
+and rendered by the GPU forward simulator (bit-identical to the reference's
+``_render_traces``): speckle at 10 scatterers per resolution cell with real
+N(0, 1) amplitudes (``Phantom.reflectivity`` is real, so BASELINE's "complex
+Gaussian amplitudes" are not representable), two anechoic 2 mm cysts, a row
+of six amplitude-20 wires, int16 quantisation (``quantize_int16``); the
+config-4 ensemble adds a 2 mm vessel whose scatterers move 50 um per frame
+(RF linearity: static background + per-frame vessel echoes).
 """
 
 from __future__ import annotations
@@ -142,3 +152,74 @@ CONFIGS = {1: config1, 2: config2, 3: config3, 4: config4, 5: config5}
 def noise_rf(n_tx: int, n_el: int, n_t: int, seed: int = 0) -> np.ndarray:
     """Seeded float32 white-noise RF (the reference's bench.noise_volume)."""
     return np.random.default_rng(seed).standard_normal((n_tx, n_el, n_t), dtype=np.float32)
+
+
+# ------------------------------------------------------------------ media
+def speckle_density(array: TransducerArray, z_mid: float) -> float:
+    """10 scatterers per resolution cell: cell = (lambda z /
+    aperture) x (pulse length / 2), pulse length c / (bw fc); per m^2."""
+    lam = C / array.center_frequency
+    lateral = lam * z_mid / array.aperture
+    axial = C / (array.fractional_bandwidth * array.center_frequency) / 2.0
+    return 10.0 / (lateral * axial)
+
+
+CYSTS_C2 = ((-8e-3, 14e-3), (7e-3, 24e-3))      # (x, z) of the two 2 mm anechoic cysts
+WIRES_C2_DEPTH = 19e-3                           # six wires, 5 mm apart, amplitude 20
+
+
+def config2_medium(seed: int = 0, z_range=(5e-3, 33e-3)):
+    """Config-2 calibration-phantom medium: speckle over
+    the aperture width x z_range, two 2 mm anechoic cysts, six wires."""
+    from .simulate import Phantom, merge_phantoms, speckle_phantom, wire_phantom
+
+    arr = config2().array
+    a = arr.aperture
+    z0, z1 = z_range
+    sp = speckle_phantom((-a / 2, a / 2, z0, z1), speckle_density(arr, 0.5 * (z0 + z1)), seed,
+                         inclusion_center=CYSTS_C2[0], inclusion_radius=2e-3)
+    cx, cz = CYSTS_C2[1]
+    keep = (sp.x - cx) ** 2 + (sp.z - cz) ** 2 > (2e-3) ** 2
+    sp = Phantom(sp.x[keep], sp.z[keep], sp.reflectivity[keep])
+    wires = wire_phantom([5e-3] * 5, WIRES_C2_DEPTH, 20.0)
+    return merge_phantoms(sp, wires)
+
+
+def quantize_int16(rf: np.ndarray):
+    """BASELINE config 2's sample format: q = clip(round(rf / s), +-32767)
+    with s = max|rf| / 32767 (the oracle consumes q.astype(float32))."""
+    s = float(np.abs(rf).max()) / 32767.0
+    return np.clip(np.round(rf / s), -32767, 32767).astype(np.int16), s
+
+
+VESSEL_Z = 15e-3          # centre depth of the config-4 vessel (2 mm diameter, lateral)
+VESSEL_STEP = 50e-6       # lateral displacement of its scatterers per frame
+
+
+def config4_background(seed: int = 0):
+    """Static config-4 medium: the config-2 speckle cropped to z <= 24 mm
+    (T = 1536 window), the vessel lumen carved out."""
+    from .simulate import Phantom, speckle_phantom
+
+    arr = config4().array
+    a = arr.aperture
+    sp = speckle_phantom((-a / 2, a / 2, 5e-3, 24e-3), speckle_density(arr, 14.5e-3), seed)
+    keep = np.abs(sp.z - VESSEL_Z) > 1e-3
+    return Phantom(sp.x[keep], sp.z[keep], sp.reflectivity[keep])
+
+
+def config4_vessel_frame(frame: int, seed: int = 1, amplitude: float = 0.5):
+    """Moving scatterers of the 2 mm vessel in frame `frame`: seeded positions
+    inside the lumen, shifted laterally by 50 um per frame and wrapped over
+    the aperture width."""
+    from .simulate import Phantom
+
+    arr = config4().array
+    a = arr.aperture
+    rng = np.random.default_rng(seed)
+    count = int(round(speckle_density(arr, VESSEL_Z) * a * 2e-3))
+    x = rng.uniform(-a / 2, a / 2, count)
+    z = rng.uniform(VESSEL_Z - 1e-3, VESSEL_Z + 1e-3, count)
+    r = amplitude * rng.standard_normal(count)
+    x = (x + a / 2 + VESSEL_STEP * frame) % a - a / 2
+    return Phantom(x, z, r)
