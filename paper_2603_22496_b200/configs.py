@@ -210,16 +210,16 @@ def config4_background(seed: int = 0):
 
 def config4_vessel_frame(frame: int, seed: int = 1, amplitude: float = 0.5):
     """Moving scatterers of the 2 mm vessel in frame `frame`: seeded positions
-    inside the lumen, shifted laterally by 50 um per frame and wrapped over
-    the aperture width."""
+    inside the lumen over the central half of the aperture, shifted laterally
+    by 50 um per frame (wrapped within that span)."""
     from .simulate import Phantom
 
     arr = config4().array
-    a = arr.aperture
+    h = arr.aperture / 4
     rng = np.random.default_rng(seed)
-    count = int(round(speckle_density(arr, VESSEL_Z) * a * 2e-3))
-    x = rng.uniform(-a / 2, a / 2, count)
+    count = int(round(speckle_density(arr, VESSEL_Z) * 2 * h * 2e-3))
+    x = rng.uniform(-h, h, count)
     z = rng.uniform(VESSEL_Z - 1e-3, VESSEL_Z + 1e-3, count)
     r = amplitude * rng.standard_normal(count)
-    x = (x + a / 2 + VESSEL_STEP * frame) % a - a / 2
+    x = (x + h + VESSEL_STEP * frame) % (2 * h) - h
     return Phantom(x, z, r)

@@ -64,13 +64,9 @@ def test_config2_medium_int16_kk_vs_oracle(oracle, config2_rf75):
     ref_tr, ref = _oracle_image(oracle, w, p, rx, q.astype(np.float32))
     assert rel_l2(got_tr, ref_tr) <= 1e-5
     assert rel_l2(got, ref) <= 1e-5
-    # the medium is what it claims: anechoic cysts, bright wires
+    # the medium is what it claims: the brightest echo is a wire (the 15 x 5
+    # vernier image is too coarse for the 2 mm cysts; the DAS test checks them)
     I = np.abs(ref) ** 2
-    X, Z = np.meshgrid(g.x, g.z, indexing="ij")
-    bg = I[(Z > 8e-3) & (Z < 30e-3)].mean()
-    for cx, cz in configs.CYSTS_C2:
-        inside = (X - cx) ** 2 + (Z - cz) ** 2 < (1.2e-3) ** 2
-        assert I[inside].mean() < 0.1 * bg, (cx, cz)
     ix, iz = np.unravel_index(np.argmax(I), I.shape)
     assert abs(g.z[iz] - configs.WIRES_C2_DEPTH) < 0.5e-3
     eng.close()
@@ -88,6 +84,14 @@ def test_config2_das_full_size_vs_oracle(oracle, config2_rf75):
                             luts.rx_frac, g.x, g.z, arr.positions, np.inf,
                             np.ones(arr.num_elements), arr.sampling_frequency, 0.0)
     assert rel_l2(got, ref) <= 1e-5
+    # the medium is what it claims: both 2 mm cysts anechoic in the
+    # full-aperture image (> 10 dB below the speckle around them)
+    I = np.abs(got) ** 2
+    X, Z = np.meshgrid(g.x, g.z, indexing="ij")
+    for cx, cz in configs.CYSTS_C2:
+        r2 = (X - cx) ** 2 + (Z - cz) ** 2
+        inside, ring = r2 < (1.2e-3) ** 2, (r2 > (3e-3) ** 2) & (r2 < (5e-3) ** 2)
+        assert I[inside].mean() < 0.1 * I[ring].mean(), (cx, cz)
 
 
 def test_config4_vessel_ensemble_vs_oracle(oracle):
@@ -110,9 +114,13 @@ def test_config4_vessel_ensemble_vs_oracle(oracle):
     for f in range(F):
         _, ref = _oracle_image(oracle, w, p, rx, rf_h[f])
         assert rel_l2(iq[f], ref) <= 1e-5, f
+    # frame-to-frame changes: in the vessel band, not in the static tissue
+    # above it (echoes arrive after the vessel's, so the plane-wave
+    # decomposition's aperture-truncation tails only reach deeper pixels)
     d = np.abs(np.diff(iq, axis=0)) ** 2
     in_vessel = np.abs(g.z - configs.VESSEL_Z) < 1.5e-3
-    assert d[:, :, in_vessel].mean() > 10 * d[:, :, ~in_vessel].mean()
+    above = g.z < configs.VESSEL_Z - 3e-3
+    assert d[:, :, in_vessel].mean() > 100 * d[:, :, above].mean()
     eng.close()
 
 
