@@ -268,6 +268,11 @@ def run_gpu(args):
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     local = _init_dist(torch, dist, world, local)
+    host_cpus = None
+    if world > 1:  # pinned host buffers on the GPU's own NUMA node (first touch)
+        from paper_2603_22496_b200._numa import bind_to_device
+
+        host_cpus = bind_to_device(local)
 
     w = _workload(args.config, args.frames)
     F = w.frames if args.config == 4 else args.frames
@@ -536,6 +541,7 @@ def run_gpu(args):
                                 "flop_frac": s1_flops / (dec_ms / 1e3) / 1e12 / fp32_peak},
             "gpu_launches": int(launches),
             "clocks": clk,
+            "host_binding": (f"{len(host_cpus)} CPUs local to the GPU" if host_cpus else "unbound"),
         }
         if e2e:
             line["e2e"] = e2e

@@ -258,3 +258,15 @@ def test_bench_roofline_helpers_read_the_committed_profiles():
     w = configs.config4(frames=400)
     c = bench._config(w, 400, 1)
     assert c["workload"] == w.name and c["pixel_pairs_per_frame"] == 256 * 256 * 121
+
+
+def test_numa_cpulist_parsing_and_pci_address():
+    from types import SimpleNamespace
+
+    from paper_2603_22496_b200._numa import parse_cpulist, pci_address
+
+    assert parse_cpulist("0-3,8,10-11\n") == [0, 1, 2, 3, 8, 10, 11]
+    assert parse_cpulist("5") == [5]
+    assert parse_cpulist("") == []
+    props = SimpleNamespace(pci_domain_id=0, pci_bus_id=0x1b, pci_device_id=0)
+    assert pci_address(props) == "0000:1b:00.0"
