@@ -255,6 +255,18 @@ int kkb_decomposer_run_scatter(kkb_decomposer *p, const void *rf, int rf_is_i16,
  * uses (0: general contraction).  The reference guarantees the symmetry
  * (ReceiveAngleSet, sampling.py:55-57; centred positions, core.py:32-38). */
 int kkb_decomposer_symmetric_classes(const kkb_decomposer *p);
+/* Contraction form of the plan's K2 (north star: "complex fp32 via split real
+ * GEMM or fp32 FMA, whichever ncu shows faster"): KKB_CONTRACT_FMA, the
+ * symmetric FP32-FMA kernel (default), or KKB_CONTRACT_TENSOR, the same
+ * symmetric contraction as one real GEMM per bin on the tcgen05 tensor cores
+ * in split precision (3xTF32: hi*hi + hi*lo + lo*hi, fp32 accumulation in
+ * TMEM).  The tensor form needs the symmetric geometry with <= 8 angle
+ * classes (KKB_ERR_UNSUPPORTED otherwise).  Environment KKB_CONTRACT=tc
+ * selects it at creation. */
+#define KKB_CONTRACT_FMA 0
+#define KKB_CONTRACT_TENSOR 1
+int kkb_decomposer_set_contraction(kkb_decomposer *p, int form);
+int kkb_decomposer_contraction(const kkb_decomposer *p);
 /* bytes of device scratch held by the plan */
 long long kkb_decomposer_workspace_bytes(const kkb_decomposer *p);
 int kkb_decomposer_destroy(kkb_decomposer *p);

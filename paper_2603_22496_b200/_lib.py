@@ -53,6 +53,8 @@ SIGNATURES = {
     "kkb_decomposer_run_scatter": [P, P, I, I, P, I, LL, LL, P],
     "kkb_decomposer_set_pipeline": [P, I, I],
     "kkb_decomposer_symmetric_classes": [P],
+    "kkb_decomposer_set_contraction": [P, I],
+    "kkb_decomposer_contraction": [P],
     "kkb_decomposer_workspace_bytes": [P],
     "kkb_decomposer_destroy": [P],
     "kkb_log_compress": [P, P, I, LL, F, P, P],
@@ -105,6 +107,7 @@ KKB_MAX_DST = 8  # destinations of kkb_kk_plan_run_scatter
 KKB_MAX_SETS = 8  # receive sets of kkb_kk_plan_run_sets
 KKB_OUT_C128 = 1
 KKB_DEVERR_KK_WINDOW = 1
+KKB_CONTRACT_FMA, KKB_CONTRACT_TENSOR = 0, 1
 # K5 instances (kkb_kk_last_instance)
 KKB_KK_INST_DIRECT, KKB_KK_INST_SMALL, KKB_KK_INST_MID, KKB_KK_INST_BIG, KKB_KK_INST_BIG_FR = range(5)
 KKB_KK_INST_SETS = 16

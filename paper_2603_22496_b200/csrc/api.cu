@@ -492,6 +492,10 @@ struct kkb_decomposer {
     int P = 0;
     float2 *cs = nullptr;
     std::vector<short> mp, mm;
+    // tensor-core contraction (k_contract_tc, kkb_decomposer_set_contraction):
+    // 3xTF32 class tables in the UMMA operand layout, built on first use
+    int form = KKB_CONTRACT_FMA;
+    float *tctab = nullptr;
 };
 
 // Pair receive angles into +/- classes and build the cos/sin table; P = 0
@@ -589,6 +593,11 @@ extern "C" int kkb_decomposer_create(int n_tx, int n_el, int n_t, const double *
     scale.resize(ldk, 0.0);
     st = build_ramps(tau.data(), n_el, n_rx, freq.data(), scale.data(), ldk, p->ramps, 0);
     if (!st) st = build_symmetric_classes(p, positions_host, angles_host, c, freq, scale);
+    if (!st) {  // KKB_CONTRACT=tc: tensor-core contraction by default (falls back if unsupported)
+        const char *f = getenv("KKB_CONTRACT");
+        if (f && !strcmp(f, "tc") && p->P >= 1 && p->P <= 8)
+            st = kkb_decomposer_set_contraction(p, KKB_CONTRACT_TENSOR);
+    }
     if (st) {
         cudaFree(p->ramps);
         cudaFree(p->X);
@@ -602,6 +611,30 @@ extern "C" int kkb_decomposer_create(int n_tx, int n_el, int n_t, const double *
 }
 
 extern "C" int kkb_decomposer_symmetric_classes(const kkb_decomposer *p) { return p ? p->P : -1; }
+
+extern "C" int kkb_decomposer_set_contraction(kkb_decomposer *p, int form) {
+    if (!p || (form != KKB_CONTRACT_FMA && form != KKB_CONTRACT_TENSOR)) {
+        set_error("set_contraction: form must be KKB_CONTRACT_FMA or KKB_CONTRACT_TENSOR");
+        return KKB_ERR_ARG;
+    }
+    if (form == KKB_CONTRACT_TENSOR) {
+        if (p->P < 1 || p->P > 8) {
+            set_error("tensor-core contraction needs a symmetric geometry with 1..8 angle classes (P=%d)", p->P);
+            return KKB_ERR_UNSUPPORTED;
+        }
+        if (!p->tctab) {
+            long long bytes = 0;
+            int st = build_tc_table(p->cs, p->ldk, p->P, p->L, p->K, &p->tctab, &bytes, 0);
+            if (st) return st;
+            KKB_TRY_CUDA(cudaStreamSynchronize(0), "sync tc table");
+            p->bytes += bytes;
+        }
+    }
+    p->form = form;
+    return KKB_OK;
+}
+
+extern "C" int kkb_decomposer_contraction(const kkb_decomposer *p) { return p ? p->form : -1; }
 
 extern "C" long long kkb_decomposer_workspace_bytes(const kkb_decomposer *p) { return p ? p->bytes : 0; }
 
@@ -663,7 +696,10 @@ static int decomposer_run(kkb_decomposer *p, const void *rf, int in_kind, int n_
         }
         if (conv) cudaFreeAsync(conv, cs);
         if (st) return st;
-        if (p->P > 0)
+        if (p->form == KKB_CONTRACT_TENSOR)
+            st = contract_tc(X, ldk, p->tctab, Y, ldk, (long long)F * N, L, M, K, p->P, p->mp.data(),
+                             p->mm.data(), cs);
+        else if (p->P > 0)
             st = contract_sym(X, ldk, p->cs, ldk, Y, ldk, (long long)F * N, L, M, K, p->P,
                               p->mp.data(), p->mm.data(), cs);
         else
@@ -767,6 +803,7 @@ extern "C" int kkb_decomposer_destroy(kkb_decomposer *p) {
     cudaFree(p->X);
     cudaFree(p->Y);
     cudaFree(p->cs);
+    cudaFree(p->tctab);
     delete p;
     return KKB_OK;
 }

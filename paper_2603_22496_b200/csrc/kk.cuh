@@ -129,6 +129,11 @@ int contract_sym(const float2 *X, long long ldx, const float2 *CS, long long ldc
                  const short *mm, cudaStream_t s);
 int contract(const float2 *X, long long ldx, const float2 *R, long long ldr, float2 *Y,
              long long ldy, long long B, int L, int M, int Kb, cudaStream_t s);
+// tensor-core (tcgen05, 3xTF32) form of contract_sym (contract_tc.cu)
+int build_tc_table(const float2 *cs, long long ldc, int P, int L, int Kb, float **tab, long long *bytes,
+                   cudaStream_t s);
+int contract_tc(const float2 *X, long long ldx, const float *tab, float2 *Y, long long ldy, long long B,
+                int L, int M, int Kb, int P, const short *mp, const short *mm, cudaStream_t s);
 
 // K8 forward simulator (simulate.cu)
 int render_traces(float *out, int n_tx, int n_el, int n_t, const double *sx, const double *sz,
