@@ -260,7 +260,7 @@ int kkb_decomposer_symmetric_classes(const kkb_decomposer *p);
  * symmetric FP32-FMA kernel (default), or KKB_CONTRACT_TENSOR, the same
  * symmetric contraction as one real GEMM per bin on the tcgen05 tensor cores
  * in split precision (3xTF32: hi*hi + hi*lo + lo*hi, fp32 accumulation in
- * TMEM).  The tensor form needs the symmetric geometry with <= 8 angle
+ * TMEM).  The tensor form needs the symmetric geometry with <= 16 angle
  * classes (KKB_ERR_UNSUPPORTED otherwise).  Environment KKB_CONTRACT=tc
  * selects it at creation. */
 #define KKB_CONTRACT_FMA 0

@@ -595,7 +595,7 @@ extern "C" int kkb_decomposer_create(int n_tx, int n_el, int n_t, const double *
     if (!st) st = build_symmetric_classes(p, positions_host, angles_host, c, freq, scale);
     if (!st) {  // KKB_CONTRACT=tc: tensor-core contraction by default (falls back if unsupported)
         const char *f = getenv("KKB_CONTRACT");
-        if (f && !strcmp(f, "tc") && p->P >= 1 && p->P <= 8)
+        if (f && !strcmp(f, "tc") && p->P >= 1 && p->P <= 16)
             st = kkb_decomposer_set_contraction(p, KKB_CONTRACT_TENSOR);
     }
     if (st) {
@@ -618,8 +618,8 @@ extern "C" int kkb_decomposer_set_contraction(kkb_decomposer *p, int form) {
         return KKB_ERR_ARG;
     }
     if (form == KKB_CONTRACT_TENSOR) {
-        if (p->P < 1 || p->P > 8) {
-            set_error("tensor-core contraction needs a symmetric geometry with 1..8 angle classes (P=%d)", p->P);
+        if (p->P < 1 || p->P > 16) {
+            set_error("tensor-core contraction needs a symmetric geometry with 1..16 angle classes (P=%d)", p->P);
             return KKB_ERR_UNSUPPORTED;
         }
         if (!p->tctab) {
