@@ -109,9 +109,9 @@ KKB_OUT_C128 = 1
 KKB_DEVERR_KK_WINDOW = 1
 KKB_CONTRACT_FMA, KKB_CONTRACT_TENSOR = 0, 1
 # K5 instances (kkb_kk_last_instance)
-KKB_KK_INST_DIRECT, KKB_KK_INST_SMALL, KKB_KK_INST_MID, KKB_KK_INST_BIG, KKB_KK_INST_BIG_FR = range(5)
+KKB_KK_INST_DIRECT, KKB_KK_INST_SMALL, KKB_KK_INST_MID, KKB_KK_INST_BIG, KKB_KK_INST_BIG_FR, KKB_KK_INST_TC = range(6)
 KKB_KK_INST_SETS = 16
-KKB_KK_INST_NAMES = {0: "direct", 1: "small", 2: "mid", 3: "big", 4: "big_fr"}
+KKB_KK_INST_NAMES = {0: "direct", 1: "small", 2: "mid", 3: "big", 4: "big_fr", 5: "tc"}
 
 _lib = None
 

@@ -63,6 +63,7 @@ int transpose_f64(const double *in, int rows, int cols, double *out, cudaStream_
 struct KKWindows {
     int big, mid, small;
     int bad;  // bit (1 << KKB_KK_INST_*): instance whose window failed kk_check_windows
+    int tc;   // window of the tensor-core gather's 8 x 16 tile
 };
 // Synchronises `s` (one launch for the three tile sizes).
 int kk_window(const double *ltx, const double *ltz, const double *lrx, const double *lrz, int N,
@@ -102,6 +103,15 @@ int kk_gather(const float2 *data, int N, int M, int T, const double *ltx, const 
 int kk_check_windows(const double *ltx, const double *ltz, const double *lrx, const double *lrz,
                      int N, int M, int T, int nx, int nz, double fs, double shift, int linear,
                      KKWindows *win, cudaStream_t s);
+
+// tensor-core (tcgen05) form of K5 (kk_gather_tc.cu): 8 x 16-pixel tiles,
+// up to 128 frames per CTA; W = the tile window (<= 64)
+int kk_gather_tc(const float2 *data, int N, int M, int T, const double *ltx, const double *ltzT,
+                 const double *lrx, const double *lrzT, int nx, int nz, const double *w, double fs,
+                 double shift, int linear, void *out, int out_kind, int n_frames, long long data_fs,
+                 long long out_fs, float *inten, unsigned *fmax, int W, int accum, cudaStream_t s);
+#define KKB_KK_TC_TZ 8
+#define KKB_KK_TC_TX 16
 
 // instance the last kk_gather dispatch launched (KKB_KK_INST_*, include/kkb.h)
 int kk_last_instance();

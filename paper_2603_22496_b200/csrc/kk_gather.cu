@@ -183,21 +183,21 @@ int kk_taps(const double *ltx, const double *ltz, const double *lrx, const doubl
 // [floor(min corner fi) - 1, floor(max corner fi) + 2]; wmax[s] = the largest
 // length over the tiles of size s (big, mid, small) — one launch, one sync.
 struct KKTileSizes {
-    int tx[3], tz[3];
+    int tx[4], tz[4];
 };
 
 __global__ void k_kk_window(const double *__restrict__ ltx, const double *__restrict__ ltz,
                             const double *__restrict__ lrx, const double *__restrict__ lrz, int N,
                             int M, int nx, int nz, KKTileSizes ts, double fs, double shift,
                             int *wmax) {
-    long long cum[4] = {0, 0, 0, 0};
-    for (int s = 0; s < 3; ++s)
+    long long cum[5] = {0, 0, 0, 0, 0};
+    for (int s = 0; s < 4; ++s)
         cum[s + 1] = cum[s] + (long long)((nz + ts.tz[s] - 1) / ts.tz[s]) *
                                   ((nx + ts.tx[s] - 1) / ts.tx[s]) * N * M;
-    int best[3] = {0, 0, 0};
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < cum[3];
+    int best[4] = {0, 0, 0, 0};
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < cum[4];
          i += (long long)gridDim.x * blockDim.x) {
-        const int sz = i < cum[1] ? 0 : (i < cum[2] ? 1 : 2);
+        const int sz = i < cum[1] ? 0 : (i < cum[2] ? 1 : (i < cum[3] ? 2 : 3));
         const int TX = ts.tx[sz], TZ = ts.tz[sz];
         const int tiles_x = (nx + TX - 1) / TX;
         long long r = i - cum[sz];
@@ -222,19 +222,20 @@ __global__ void k_kk_window(const double *__restrict__ ltx, const double *__rest
         int w = span > 1e9 ? 1000000000 : (int)span;
         best[sz] = max(best[sz], w);
     }
-    for (int s = 0; s < 3; ++s)
+    for (int s = 0; s < 4; ++s)
         if (best[s]) atomicMax(wmax + s, best[s]);
 }
 
 int kk_window(const double *ltx, const double *ltz, const double *lrx, const double *lrz, int N,
               int M, int nx, int nz, double fs, double shift, KKWindows *win, cudaStream_t s) {
     int *d = nullptr;
-    KKB_TRY_CUDA(cudaMallocAsync(&d, 3 * sizeof(int), s), "cudaMallocAsync(window)");
-    KKB_TRY_CUDA(cudaMemsetAsync(d, 0, 3 * sizeof(int), s), "memset(window)");
-    KKTileSizes ts{{KKB_KK_TX, KKB_KK_M_TX, KKB_KK_S_TX}, {KKB_KK_TZ, KKB_KK_M_TZ, KKB_KK_S_TZ}};
+    KKB_TRY_CUDA(cudaMallocAsync(&d, 4 * sizeof(int), s), "cudaMallocAsync(window)");
+    KKB_TRY_CUDA(cudaMemsetAsync(d, 0, 4 * sizeof(int), s), "memset(window)");
+    KKTileSizes ts{{KKB_KK_TX, KKB_KK_M_TX, KKB_KK_S_TX, KKB_KK_TC_TX},
+                   {KKB_KK_TZ, KKB_KK_M_TZ, KKB_KK_S_TZ, KKB_KK_TC_TZ}};
     k_kk_window<<<512, 256, 0, s>>>(ltx, ltz, lrx, lrz, N, M, nx, nz, ts, fs, shift, d);
     KKB_CHECK_LAUNCH("k_kk_window");
-    int h[3] = {0, 0, 0};
+    int h[4] = {0, 0, 0, 0};
     KKB_TRY_CUDA(cudaMemcpyAsync(h, d, sizeof(h), cudaMemcpyDeviceToHost, s), "copy window");
     KKB_TRY_CUDA(cudaStreamSynchronize(s), "sync window");
     cudaFreeAsync(d, s);
@@ -242,12 +243,14 @@ int kk_window(const double *ltx, const double *ltz, const double *lrx, const dou
     win->big = (h[0] + 1) & ~1;
     win->mid = (h[1] + 1) & ~1;
     win->small = (h[2] + 1) & ~1;
+    win->tc = (h[3] + 1) & ~1;
     win->bad = 0;
     if (const char *k = getenv("KKB_KK_WINDOW_SHRINK")) {  // fault injection (tests): undersized windows
         const int d = atoi(k);
         win->big = std::max(2, win->big - d);
         win->mid = std::max(2, win->mid - d);
         win->small = std::max(2, win->small - d);
+        win->tc = std::max(2, win->tc - d);
     }
     return KKB_OK;
 }
@@ -805,7 +808,7 @@ static bool instance_fits(int inst, int N, int M, bool linear, const KKWindows &
 // pixels).  The dispatch takes the instance with the smallest modelled time.
 static double instance_cost(int inst, long long ctas, long long sms) {
     static const double rel[5] = {0.0, 1.42, 1.07, 1.02, 1.00};
-    const InstanceShape sh = instance_shape(inst, KKWindows{2, 2, 2, 0});
+    const InstanceShape sh = instance_shape(inst, KKWindows{2, 2, 2, 0, 2});
     const int fr = inst == KKB_KK_INST_BIG_FR ? KKB_KK_FR : 1;
     const long long per_sm = ceil_div(ctas, sms);
     const double resident = (double)std::min<long long>(per_sm, sh.resident);
@@ -885,6 +888,18 @@ int kk_check_windows(const double *ltx, const double *ltz, const double *lrx, co
         else
             k_kk_window_check<false><<<grid, 256, smem, s>>>(ltx, ltz, lrx, lrz, N, M, T, nx, nz, sh.tx,
                                                              sh.tz, sh.W, fs, shift, 1 << insts[k], d);
+        KKB_CHECK_LAUNCH("k_kk_window_check");
+    }
+    if (win->tc >= 2 && win->tc <= 64 && ceil_div(nz, KKB_KK_TC_TZ) * ceil_div(nx, KKB_KK_TC_TX) <= 0x7fffffffLL &&
+        N <= 65535) {  // the tensor-core gather's 8 x 16 tile
+        dim3 grid((unsigned)(ceil_div(nz, KKB_KK_TC_TZ) * ceil_div(nx, KKB_KK_TC_TX)), (unsigned)N);
+        const size_t smem = sizeof(int) * (size_t)M;
+        if (linear)
+            k_kk_window_check<true><<<grid, 256, smem, s>>>(ltx, ltz, lrx, lrz, N, M, T, nx, nz, KKB_KK_TC_TX,
+                                                            KKB_KK_TC_TZ, win->tc, fs, shift, 1 << KKB_KK_INST_TC, d);
+        else
+            k_kk_window_check<false><<<grid, 256, smem, s>>>(ltx, ltz, lrx, lrz, N, M, T, nx, nz, KKB_KK_TC_TX,
+                                                             KKB_KK_TC_TZ, win->tc, fs, shift, 1 << KKB_KK_INST_TC, d);
         KKB_CHECK_LAUNCH("k_kk_window_check");
     }
     int h = 0;
@@ -978,6 +993,22 @@ int kk_gather(const float2 *data, int N, int M, int T, const double *ltx, const 
         a.nsets = sets->nsets;
         for (int j = 0; j <= sets->nsets; ++j) a.set_m0[j] = sets->m0[j];
         a.out_set_stride = sets->out_set_stride;
+    }
+    // tensor-core gather (kk_gather_tc.cu): single-set, no peer scatter, a
+    // proven window of <= 64 samples on its 8 x 16 tile; forced with
+    // KKB_KK_INST=tc, default-on for batches with KKB_KK_TC=1
+    {
+        const char *fi = getenv("KKB_KK_INST");
+        const char *ft = getenv("KKB_KK_TC");
+        const bool forced = fi && !strcmp(fi, "tc");
+        const bool want = forced || (ft && ft[0] == '1' && n_frames >= 16 && !fi);
+        const bool tc_ok = !ms && !sc && win.tc >= 2 && win.tc <= 64 && !(win.bad & (1 << KKB_KK_INST_TC)) &&
+                           (size_t)N * M * sizeof(int) <= 32 * 1024;
+        if (want && tc_ok) {
+            g_last_instance.store(KKB_KK_INST_TC);
+            return kk_gather_tc(data, N, M, T, ltx, ltzT, lrx, lrzT, nx, nz, w, fs, shift, linear, out, out_kind,
+                                n_frames, data_fs, out_fs, inten, fmax, win.tc, accum, s);
+        }
     }
     const int inst = select_instance(N, M, nx, nz, n_frames, linear != 0, win);
     g_last_instance.store(inst | (ms ? KKB_KK_INST_SETS : 0));
