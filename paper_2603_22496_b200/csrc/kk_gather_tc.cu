@@ -48,6 +48,7 @@ __device__ __forceinline__ double tc_kk_delay(double t1, double lz, double lx, d
 #define TCG_MAGIC2_HI 0x41380000
 
 #define TCG_PRODUCERS 256
+#define TCG_WSCALE 4096.0f      // weights x 2^12: their fp16 low halves stay normal
 #define TCG_TZ 8
 #define TCG_TX 16
 
@@ -153,38 +154,70 @@ k_kk_gather_tc(const TcgArgs a) {
 
     if (warp < 8) {
         // ------------------------------------------------------------ producers
+        // Loads of pair pr + PD are issued before pair pr's operands are
+        // built (register prefetch, PD pairs deep), so the L2 latency of the
+        // trace windows and delay tables overlaps the conversion work.
+        constexpr int UPT = (128 * KC + TCG_PRODUCERS - 1) / TCG_PRODUCERS;  // window units per thread
+        constexpr int PD = KW <= 32 ? 2 : 1;
+        struct PairRegs {
+            float2 v[UPT][8];
+            double tx, tz, lz, lx;
+        };
         const int r = t & 127;                        // weight row (threads 0..127)
         const int ix = min(ix0 + r / TCG_TZ, nx - 1), iz = min(iz0 + r % TCG_TZ, nz - 1);
-        double t1 = 0.0;
+        auto fetch = [&](int pr, PairRegs &R) {
+            const int n = pr / M, m = pr - n * M;
+            const int lo = lo_s[pr];
+            const float2 *base = a.data + (long long)f0 * a.data_fs + (long long)(n * M + m) * T;
+#pragma unroll
+            for (int i = 0; i < UPT; ++i) {
+                const int u = t + i * TCG_PRODUCERS, f = u / KC, c = u - f * KC;
+                const int s0 = lo + 8 * c;
+                const float2 *tr = base + (long long)f * a.data_fs;
+                const bool fok = u < NH * KC && f < FB;
+#pragma unroll
+                for (int e = 0; e < 8; ++e)
+                    R.v[i][e] = fok && (unsigned)(s0 + e) < (unsigned)T ? __ldg(tr + s0 + e) : make_float2(0.f, 0.f);
+            }
+            if (t < 128) {
+                R.tx = __ldg(a.ltx + (long long)ix * N + n);
+                R.tz = __ldg(a.ltzT + (long long)n * nz + iz);
+                R.lz = __ldg(a.lrzT + (long long)m * nz + iz);
+                R.lx = __ldg(a.lrx + (long long)ix * M + m);
+            }
+        };
+        PairRegs cur, nx1, nx2;
+        fetch(0, cur);
+        if (PD > 1 && npairs > 1) fetch(1, nx1);
         for (int pr = 0; pr < npairs; ++pr) {
             const int st = pr % NSTAGE, use = pr / NSTAGE;
-            const int n = pr / M, m = pr - n * M;
+            const int m = pr % M;
+            if (PD > 1) {
+                if (pr + 2 < npairs) fetch(pr + 2, nx2);
+            } else if (pr + 1 < npairs) {
+                fetch(pr + 1, nx1);
+            }
             if (use > 0) tc::mbar_wait(&empty_bar[st], (use - 1) & 1);
             unsigned char *Ab = sm + st * STAGE;
             unsigned char *Bb = Ab + 2 * A_PLANE;
             const int lo = lo_s[pr];
-            // trace windows: unit u = (frame, 8-sample chunk)
-            const float2 *base = a.data + (long long)f0 * a.data_fs + (long long)(n * M + m) * T;
-            for (int u = t; u < NH * KC; u += TCG_PRODUCERS) {
-                const int f = u / KC, c = u - f * KC;
-                uint32_t rh[4] = {0, 0, 0, 0}, rl[4] = {0, 0, 0, 0}, ih[4] = {0, 0, 0, 0}, il[4] = {0, 0, 0, 0};
-                if (f < FB) {
-                    const float sc = fscale[f];
-                    const float2 *tr = base + (long long)f * a.data_fs;
-                    const int s0 = lo + 8 * c;
+            // trace windows: unit u = (frame f, 8-sample chunk c), scaled, split, stored
 #pragma unroll
-                    for (int i = 0; i < 8; i += 2) {
-                        float2 v0 = make_float2(0.f, 0.f), v1 = v0;
-                        if ((unsigned)(s0 + i) < (unsigned)T) v0 = __ldg(tr + s0 + i);
-                        if ((unsigned)(s0 + i + 1) < (unsigned)T) v1 = __ldg(tr + s0 + i + 1);
-                        const float x0 = v0.x * sc, y0 = v0.y * sc, x1 = v1.x * sc, y1 = v1.y * sc;
-                        const __half hx0 = __float2half_rn(x0), hx1 = __float2half_rn(x1);
-                        const __half hy0 = __float2half_rn(y0), hy1 = __float2half_rn(y1);
-                        rh[i / 2] = pack_h2(hx0, hx1);
-                        ih[i / 2] = pack_h2(hy0, hy1);
-                        rl[i / 2] = pack_h2(__float2half_rn(x0 - __half2float(hx0)), __float2half_rn(x1 - __half2float(hx1)));
-                        il[i / 2] = pack_h2(__float2half_rn(y0 - __half2float(hy0)), __float2half_rn(y1 - __half2float(hy1)));
-                    }
+            for (int i = 0; i < UPT; ++i) {
+                const int u = t + i * TCG_PRODUCERS, f = u / KC, c = u - f * KC;
+                if (u >= NH * KC) break;
+                const float sc = f < FB ? fscale[f] : 1.0f;
+                uint32_t rh[4], rl[4], ih[4], il[4];
+#pragma unroll
+                for (int e = 0; e < 8; e += 2) {
+                    const float x0 = cur.v[i][e].x * sc, y0 = cur.v[i][e].y * sc;
+                    const float x1 = cur.v[i][e + 1].x * sc, y1 = cur.v[i][e + 1].y * sc;
+                    const __half hx0 = __float2half_rn(x0), hx1 = __float2half_rn(x1);
+                    const __half hy0 = __float2half_rn(y0), hy1 = __float2half_rn(y1);
+                    rh[e / 2] = pack_h2(hx0, hx1);
+                    ih[e / 2] = pack_h2(hy0, hy1);
+                    rl[e / 2] = pack_h2(__float2half_rn(x0 - __half2float(hx0)), __float2half_rn(x1 - __half2float(hx1)));
+                    il[e / 2] = pack_h2(__float2half_rn(y0 - __half2float(hy0)), __float2half_rn(y1 - __half2float(hy1)));
                 }
                 unsigned char *bre = Bb + c * NCOLS * 16 + f * 16, *bim = Bb + c * NCOLS * 16 + (NH + f) * 16;
                 *reinterpret_cast<uint4 *>(bre) = make_uint4(rh[0], rh[1], rh[2], rh[3]);
@@ -192,15 +225,15 @@ k_kk_gather_tc(const TcgArgs a) {
                 *reinterpret_cast<uint4 *>(bre + B_PLANE) = make_uint4(rl[0], rl[1], rl[2], rl[3]);
                 *reinterpret_cast<uint4 *>(bim + B_PLANE) = make_uint4(il[0], il[1], il[2], il[3]);
             }
-            // weight rows
+            // weight rows (scaled by 2^12 so the fp16 low halves stay normal)
             if (t < 128) {
-                if (m == 0) t1 = __dadd_rn(a.ltx[(long long)ix * N + n], a.ltzT[(long long)n * nz + iz]);
-                const double fi = tc_kk_delay(t1, a.lrzT[(long long)m * nz + iz], a.lrx[(long long)ix * M + m], fs, shift);
+                const double t1 = __dadd_rn(cur.tx, cur.tz);
+                const double fi = tc_kk_delay(t1, cur.lz, cur.lx, fs, shift);
                 const double sv = __dadd_rd(LINEAR ? fi : __dadd_rn(fi, 0.5), TCG_MAGIC2);
                 const int F = __double2hiint(sv) - TCG_MAGIC2_HI;
                 const bool ok = (unsigned)F <= (unsigned)(LINEAR ? T - 2 : T - 1);
                 const int e = F - lo;
-                const float wm = a.w ? (float)a.w[m] : 1.0f;
+                const float wm = (a.w ? (float)a.w[m] : 1.0f) * TCG_WSCALE;
                 float w0 = 0.f, w1 = 0.f;
                 if (ok) {
                     if (LINEAR) {
@@ -239,6 +272,8 @@ k_kk_gather_tc(const TcgArgs a) {
             tc::fence_smem_to_async();
             asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"((uint32_t)__cvta_generic_to_shared(&full_bar[st]))
                          : "memory");
+            cur = nx1;
+            if (PD > 1) nx1 = nx2;
         }
     } else if (lane == 0) {
         // ------------------------------------------------------------ MMA issue
@@ -281,7 +316,7 @@ k_kk_gather_tc(const TcgArgs a) {
             for (int i = 0; i < 8; ++i) {
                 const int f = fc + i;
                 if (f >= fb1) break;
-                const float inv = 1.0f / fscale[f];   // exact: a power of two
+                const float inv = 1.0f / (fscale[f] * TCG_WSCALE);   // exact: a power of two
                 const float vr = re[i] * inv, vi = im[i] * inv;
                 float I = 0.f;
                 if (pix) {
