@@ -104,7 +104,7 @@ k_kk_gather_tc(const TcgArgs a) {
     constexpr int KC = KW / 8;                    // 16-byte K chunks (8 fp16) per row
     constexpr int NCOLS = 256;                    // B columns (re of 128 frames | im of 128 frames)
     constexpr int A_PLANE = KC * 128 * 16;        // one split half of the weight operand
-    constexpr int B_PLANE = KC * NCOLS * 16;      // one split half of the trace operand
+    constexpr int B_PLANE = KC * NCOLS * 16;      // one split half of the trace operand (MN-major)
     constexpr int STAGE = 2 * A_PLANE + 2 * B_PLANE;
     extern __shared__ __align__(1024) unsigned char sm[];
     __shared__ uint64_t full_bar[NSTAGE], empty_bar[NSTAGE], done_bar;
@@ -157,10 +157,15 @@ k_kk_gather_tc(const TcgArgs a) {
         // Loads of pair pr + PD are issued before pair pr's operands are
         // built (register prefetch, PD pairs deep), so the L2 latency of the
         // trace windows and delay tables overlaps the conversion work.
-        constexpr int UPT = (128 * KC + TCG_PRODUCERS - 1) / TCG_PRODUCERS;  // window units per thread
+        // trace operand: warp w fills 8-frame groups g = w, w + 8, ...; lane k
+        // holds window sample k (k + 32 for KW = 64) of the group's 8 frames, so
+        // every load instruction reads one frame's window contiguously and
+        // every store writes 8 frames of one sample (16 B, MN-major layout)
+        constexpr int KP = KW / 32;                   // samples per lane
+        constexpr int GPW = 2;                        // 8-frame groups per warp (NH <= 128)
         constexpr int PD = KW <= 32 ? 2 : 1;
         struct PairRegs {
-            float2 v[UPT][8];
+            float2 v[GPW][KP][8];
             double tx, tz, lz, lx;
         };
         const int r = t & 127;                        // weight row (threads 0..127)
@@ -170,15 +175,17 @@ k_kk_gather_tc(const TcgArgs a) {
             const int lo = lo_s[pr];
             const float2 *base = a.data + (long long)f0 * a.data_fs + (long long)(n * M + m) * T;
 #pragma unroll
-            for (int i = 0; i < UPT; ++i) {
-                const int u = t + i * TCG_PRODUCERS, f = u / KC, c = u - f * KC;
-                const int s0 = lo + 8 * c;
-                const float2 *tr = base + (long long)f * a.data_fs;
-                const bool fok = u < NH * KC && f < FB;
+            for (int g = 0; g < GPW; ++g)
 #pragma unroll
-                for (int e = 0; e < 8; ++e)
-                    R.v[i][e] = fok && (unsigned)(s0 + e) < (unsigned)T ? __ldg(tr + s0 + e) : make_float2(0.f, 0.f);
-            }
+                for (int kp = 0; kp < KP; ++kp) {
+                    const int smp = lo + lane + 32 * kp;
+                    const bool sok = (unsigned)smp < (unsigned)T;
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        const int f = (warp + 8 * g) * 8 + j;
+                        R.v[g][kp][j] = sok && f < FB ? __ldg(base + (long long)f * a.data_fs + smp) : make_float2(0.f, 0.f);
+                    }
+                }
             if (t < 128) {
                 R.tx = __ldg(a.ltx + (long long)ix * N + n);
                 R.tz = __ldg(a.ltzT + (long long)n * nz + iz);
@@ -201,29 +208,36 @@ k_kk_gather_tc(const TcgArgs a) {
             unsigned char *Ab = sm + st * STAGE;
             unsigned char *Bb = Ab + 2 * A_PLANE;
             const int lo = lo_s[pr];
-            // trace windows: unit u = (frame f, 8-sample chunk c), scaled, split, stored
+            // trace operand (MN-major): (k, n) at (n/8) KC*128 + (k/8) 128 + (k%8) 16 + (n%8) 2
 #pragma unroll
-            for (int i = 0; i < UPT; ++i) {
-                const int u = t + i * TCG_PRODUCERS, f = u / KC, c = u - f * KC;
-                if (u >= NH * KC) break;
-                const float sc = f < FB ? fscale[f] : 1.0f;
-                uint32_t rh[4], rl[4], ih[4], il[4];
+            for (int g = 0; g < GPW; ++g) {
+                const int gg = warp + 8 * g;          // 8-frame group
+                if (gg * 8 >= NH) break;              // uniform per warp
 #pragma unroll
-                for (int e = 0; e < 8; e += 2) {
-                    const float x0 = cur.v[i][e].x * sc, y0 = cur.v[i][e].y * sc;
-                    const float x1 = cur.v[i][e + 1].x * sc, y1 = cur.v[i][e + 1].y * sc;
-                    const __half hx0 = __float2half_rn(x0), hx1 = __float2half_rn(x1);
-                    const __half hy0 = __float2half_rn(y0), hy1 = __float2half_rn(y1);
-                    rh[e / 2] = pack_h2(hx0, hx1);
-                    ih[e / 2] = pack_h2(hy0, hy1);
-                    rl[e / 2] = pack_h2(__float2half_rn(x0 - __half2float(hx0)), __float2half_rn(x1 - __half2float(hx1)));
-                    il[e / 2] = pack_h2(__float2half_rn(y0 - __half2float(hy0)), __float2half_rn(y1 - __half2float(hy1)));
+                for (int kp = 0; kp < KP; ++kp) {
+                    const int k = lane + 32 * kp;
+                    uint32_t rh[4], rl[4], ih[4], il[4];
+#pragma unroll
+                    for (int j = 0; j < 8; j += 2) {
+                        const int f = gg * 8 + j;
+                        const float s0 = f < FB ? fscale[f] : 1.0f, s1 = f + 1 < FB ? fscale[f + 1] : 1.0f;
+                        const float x0 = cur.v[g][kp][j].x * s0, y0 = cur.v[g][kp][j].y * s0;
+                        const float x1 = cur.v[g][kp][j + 1].x * s1, y1 = cur.v[g][kp][j + 1].y * s1;
+                        const __half hx0 = __float2half_rn(x0), hx1 = __float2half_rn(x1);
+                        const __half hy0 = __float2half_rn(y0), hy1 = __float2half_rn(y1);
+                        rh[j / 2] = pack_h2(hx0, hx1);
+                        ih[j / 2] = pack_h2(hy0, hy1);
+                        rl[j / 2] = pack_h2(__float2half_rn(x0 - __half2float(hx0)), __float2half_rn(x1 - __half2float(hx1)));
+                        il[j / 2] = pack_h2(__float2half_rn(y0 - __half2float(hy0)), __float2half_rn(y1 - __half2float(hy1)));
+                    }
+                    const int off_k = (k >> 3) * 128 + (k & 7) * 16;
+                    unsigned char *bre = Bb + gg * (KC * 128) + off_k;
+                    unsigned char *bim = Bb + (NH / 8 + gg) * (KC * 128) + off_k;
+                    *reinterpret_cast<uint4 *>(bre) = make_uint4(rh[0], rh[1], rh[2], rh[3]);
+                    *reinterpret_cast<uint4 *>(bim) = make_uint4(ih[0], ih[1], ih[2], ih[3]);
+                    *reinterpret_cast<uint4 *>(bre + B_PLANE) = make_uint4(rl[0], rl[1], rl[2], rl[3]);
+                    *reinterpret_cast<uint4 *>(bim + B_PLANE) = make_uint4(il[0], il[1], il[2], il[3]);
                 }
-                unsigned char *bre = Bb + c * NCOLS * 16 + f * 16, *bim = Bb + c * NCOLS * 16 + (NH + f) * 16;
-                *reinterpret_cast<uint4 *>(bre) = make_uint4(rh[0], rh[1], rh[2], rh[3]);
-                *reinterpret_cast<uint4 *>(bim) = make_uint4(ih[0], ih[1], ih[2], ih[3]);
-                *reinterpret_cast<uint4 *>(bre + B_PLANE) = make_uint4(rl[0], rl[1], rl[2], rl[3]);
-                *reinterpret_cast<uint4 *>(bim + B_PLANE) = make_uint4(il[0], il[1], il[2], il[3]);
             }
             // weight rows (scaled by 2^12 so the fp16 low halves stay normal)
             if (t < 128) {
@@ -277,18 +291,18 @@ k_kk_gather_tc(const TcgArgs a) {
         }
     } else if (lane == 0) {
         // ------------------------------------------------------------ MMA issue
-        const uint32_t idesc = tc::instr_desc(0, 128, 2 * NH);
+        const uint32_t idesc = tc::instr_desc(0, 128, 2 * NH, 1);
         const uint32_t s0 = (uint32_t)__cvta_generic_to_shared(sm);
         for (int pr = 0; pr < npairs; ++pr) {
             const int st = pr % NSTAGE, use = pr / NSTAGE;
             tc::mbar_wait(&full_bar[st], use & 1);
             tc::fence_after_sync();
             const uint32_t sa = s0 + st * STAGE, sb = sa + 2 * A_PLANE;
-            const uint64_t da = tc::smem_desc(sa, 128 * 16, 128), db = tc::smem_desc(sb, NCOLS * 16, 128);
+            const uint64_t da = tc::smem_desc(sa, 128 * 16, 128), db = tc::smem_desc(sb, 128, KC * 128);
 #pragma unroll
             for (int ks = 0; ks < KW / 16; ++ks) {
                 const uint64_t ah = da + ((ks * 2 * 128 * 16) >> 4), al = ah + (A_PLANE >> 4);
-                const uint64_t bh = db + ((ks * 2 * NCOLS * 16) >> 4), bl = bh + (B_PLANE >> 4);
+                const uint64_t bh = db + ((ks * 2 * 128) >> 4), bl = bh + (B_PLANE >> 4);
                 tc::mma_f16(tmem, ah, bh, idesc, pr > 0 || ks > 0);
                 tc::mma_f16(tmem, ah, bl, idesc, true);
                 tc::mma_f16(tmem, al, bh, idesc, true);
@@ -391,8 +405,7 @@ int kk_gather_tc(const float2 *data, int N, int M, int T, const double *ltx, con
     FB = std::min(FB, std::max(1, n_frames));
     TcgArgs a{data, data_fs, N, M, T, ltx, ltzT, lrx, lrzT, w, fs, shift, nx, nz,
               out, out_kind, out_fs, inten, fmax, accum, n_frames, mx, FB};
-    const int KW = W <= 16 ? 16 : (W <= 32 ? 32 : 64);
-    if (KW == 16) return linear ? launch_tc<16, true>(a, s) : launch_tc<16, false>(a, s);
+    const int KW = W <= 32 ? 32 : 64;  // one window sample per lane (two for 64)
     if (KW == 32) return linear ? launch_tc<32, true>(a, s) : launch_tc<32, false>(a, s);
     return linear ? launch_tc<64, true>(a, s) : launch_tc<64, false>(a, s);
 }

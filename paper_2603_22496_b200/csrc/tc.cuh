@@ -1,9 +1,11 @@
 // tcgen05 / TMEM / mbarrier helpers (sm_100a inline PTX) for the tensor-core
 // kernels of libkkb.  Operands live in shared memory in the canonical
-// K-major, no-swizzle UMMA layout: 8-row x 16-byte core matrices, rows of a
+// no-swizzle UMMA layouts.  K-major: 8-row x 16-byte core matrices, rows of a
 // core matrix 16 B apart; the descriptor's SBO is the byte stride between
 // 8-row groups, LBO the byte stride between the two 16-byte K halves of one
-// MMA's 32-byte K step.  Accumulators are fp32 in TMEM: row i of an M = 128
+// MMA's 32-byte K step.  MN-major: core matrices of 8 K-rows x 16 bytes of
+// consecutive M/N values; LBO = stride between 8-deep K groups, SBO = stride
+// between 16-byte M/N groups.  Accumulators are fp32 in TMEM: row i of an M = 128
 // tile is TMEM lane i, column j is TMEM column base + j.
 #pragma once
 
@@ -25,10 +27,10 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t saddr, uint32_t lbo, uint
 }
 
 // Instruction descriptor: fp32 accumulate, A/B format (0 f16, 1 bf16, 2 tf32),
-// both K-major, dense.
-__host__ __device__ constexpr uint32_t instr_desc(int ab_format, int M, int N) {
+// A K-major, B K-major (b_mn_major = 0) or MN-major (1), dense.
+__host__ __device__ constexpr uint32_t instr_desc(int ab_format, int M, int N, int b_mn_major = 0) {
     return (1u << 4) | ((uint32_t)ab_format << 7) | ((uint32_t)ab_format << 10) |
-           ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+           ((uint32_t)b_mn_major << 16) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 
 // D[tmem] (+)= A[smem] * B[smem]^T, issued by ONE thread.
