@@ -163,15 +163,15 @@ int kkb_kk_plan_window_check(const kkb_kk_plan *p);
  * any thread): the per-pixel kernel, or the tiled kernel with 16x16 / 32x32
  * / 32x64 pixel tiles, the last one with one or KKB_KK_FR (2) frames per CTA;
  * KKB_KK_INST_SETS is or-ed in for the multi-set form.  -1 before any launch.
- * Selection: a wave model over the tiled instances; the tensor-core gather
- * for batches when KKB_KK_TC=1; environment override
+ * Selection: a wave model over the tiled FMA instances; environment override
  * KKB_KK_INST=direct|small|mid|big|big_fr|tc (tests, measurements). */
 #define KKB_KK_INST_DIRECT 0
 #define KKB_KK_INST_SMALL 1
 #define KKB_KK_INST_MID 2
 #define KKB_KK_INST_BIG 3
 #define KKB_KK_INST_BIG_FR 4
-#define KKB_KK_INST_TC 5     /* tensor-core gather (tcgen05, split fp16): 8 x 16 tiles, <= 128 frames per CTA */
+#define KKB_KK_INST_TC 5     /* tensor-core gather (tcgen05, split fp16): 8 x 16 tiles, <= 128 frames per
+                                per CTA, <= 128 pairs; an experiment, only when forced (slower, see DESIGN) */
 #define KKB_KK_INST_SETS 16
 int kkb_kk_last_instance(void);
 int kkb_kk_plan_destroy(kkb_kk_plan *p);

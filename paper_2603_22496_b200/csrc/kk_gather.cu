@@ -994,16 +994,18 @@ int kk_gather(const float2 *data, int N, int M, int T, const double *ltx, const 
         for (int j = 0; j <= sets->nsets; ++j) a.set_m0[j] = sets->m0[j];
         a.out_set_stride = sets->out_set_stride;
     }
-    // tensor-core gather (kk_gather_tc.cu): single-set, no peer scatter, a
-    // proven window of <= 64 samples on its 8 x 16 tile; forced with
-    // KKB_KK_INST=tc, default-on for batches with KKB_KK_TC=1
+    // tensor-core gather (kk_gather_tc.cu), an experiment measured slower than
+    // the FMA instances (profiles/r02_gather_tc_experiment.json): only when
+    // forced with KKB_KK_INST=tc, for single-set launches without peer
+    // scatter, a proven window of <= 64 samples on its 8 x 16 tile and at most
+    // 128 pairs (the tensor core's accumulator adds truncate: ~3e-8 relative
+    // bias per MMA, scripts/ubench/tc_accum.cu, so longer pair chains would
+    // leave the 1e-5 parity bound)
     {
         const char *fi = getenv("KKB_KK_INST");
-        const char *ft = getenv("KKB_KK_TC");
-        const bool forced = fi && !strcmp(fi, "tc");
-        const bool want = forced || (ft && ft[0] == '1' && n_frames >= 16 && !fi);
+        const bool want = fi && !strcmp(fi, "tc");
         const bool tc_ok = !ms && !sc && win.tc >= 2 && win.tc <= 64 && !(win.bad & (1 << KKB_KK_INST_TC)) &&
-                           (size_t)N * M * sizeof(int) <= 32 * 1024;
+                           N * M <= 128;
         if (want && tc_ok) {
             g_last_instance.store(KKB_KK_INST_TC);
             return kk_gather_tc(data, N, M, T, ltx, ltzT, lrx, lrzT, nx, nz, w, fs, shift, linear, out, out_kind,
