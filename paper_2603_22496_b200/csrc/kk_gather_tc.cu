@@ -379,8 +379,6 @@ static int launch_tc(const TcgArgs &a, cudaStream_t s) {
     return KKB_OK;
 }
 
-int kk_gather_tc_window_limit() { return 64; }
-
 int kk_gather_tc(const float2 *data, int N, int M, int T, const double *ltx, const double *ltzT,
                  const double *lrx, const double *lrzT, int nx, int nz, const double *w, double fs,
                  double shift, int linear, void *out, int out_kind, int n_frames, long long data_fs,
