@@ -213,6 +213,15 @@ int kkb_analytic_signal(const float *rf, long long n_traces, int n_t, void *out,
 int kkb_shear_and_sum(const void *data, int n_tx, int n_el, int n_t,
                       const double *positions_host, const double *angles_host, int n_rx,
                       double fs, double c, void *out, void *stream);
+/* Plan form of kkb_shear_and_sum for repeated calls on one geometry (the
+ * reference's compress per frame): the phase ramps are built once.
+ * kkb_shear_plan_run is asynchronous on `stream`; same arithmetic as
+ * kkb_shear_and_sum (which is create + run + destroy). */
+typedef struct kkb_shear_plan kkb_shear_plan;
+int kkb_shear_plan_create(const double *positions_host, const double *angles_host, int n_el, int n_rx,
+                          int n_t, double fs, double c, kkb_shear_plan **out);
+int kkb_shear_plan_run(kkb_shear_plan *p, const void *data, int n_tx, void *out, void *stream);
+int kkb_shear_plan_destroy(kkb_shear_plan *p);
 
 /* ------------------------------------------------------------ fused stage 1 plan
  * Device-resident, batched form of analytic_signal + compress — the data

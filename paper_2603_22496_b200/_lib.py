@@ -47,6 +47,9 @@ SIGNATURES = {
     "kkb_das": [P, I, I, I, P, P, P, I, P, P, P, P, P, D, P, D, D, I, I, I, P, I, P],
     "kkb_analytic_signal": [P, LL, I, P, P],
     "kkb_shear_and_sum": [P, I, I, I, P, P, I, D, D, P, P],
+    "kkb_shear_plan_create": [P, P, I, I, I, D, D, P],
+    "kkb_shear_plan_run": [P, P, I, P, P],
+    "kkb_shear_plan_destroy": [P],
     "kkb_decomposer_create": [I, I, I, P, P, I, D, D, I, P],
     "kkb_decomposer_run": [P, P, I, P, P],
     "kkb_decomposer_run_i16": [P, P, I, P, P],

@@ -36,6 +36,39 @@ def guard_band_samples(aperture: float, max_abs_angle: float, sampling_frequency
     return int(math.ceil(aperture * math.sin(abs(max_abs_angle)) * sampling_frequency / sound_speed))
 
 
+class _ShearPlanCache:
+    """Shear plans (the phase ramps of one geometry, built once in float64)
+    keyed by the bytes of (positions, angles, fs, c, T): a reference loop that
+    compresses frame after frame pays the ramp build once."""
+
+    def __init__(self, capacity: int = 4):
+        from collections import OrderedDict
+
+        self._d = OrderedDict()
+        self.capacity = capacity
+
+    def get(self, pos: np.ndarray, ang: np.ndarray, fs: float, c: float, T: int):
+        import ctypes
+
+        key = (pos.tobytes(), ang.tobytes(), float(fs), float(c), int(T))
+        h = self._d.get(key)
+        if h is not None:
+            self._d.move_to_end(key)
+            return h
+        h = ctypes.c_void_p()
+        _lib.call("kkb_shear_plan_create", pos.ctypes.data, ang.ctypes.data, int(pos.size), int(ang.size),
+                  int(T), float(fs), float(c), ctypes.byref(h))
+        self._d[key] = h
+        while len(self._d) > self.capacity:
+            _, old = self._d.popitem(last=False)
+            dev.synchronize()
+            _lib.load().kkb_shear_plan_destroy(old)
+        return h
+
+
+shear_plans = _ShearPlanCache()
+
+
 def shear_and_sum_device(data, sampling_frequency, positions, angles, sound_speed, out=None,
                          stream=None):
     """complex64 CUDA tensor (N, L, T) -> complex64 CUDA tensor (N, M, T)."""
@@ -52,9 +85,8 @@ def shear_and_sum_device(data, sampling_frequency, positions, angles, sound_spee
     n, l, T = (int(s) for s in data.shape)
     if out is None:
         out = t.empty((n, ang.size, T), dtype=t.complex64, device=data.device)
-    _lib.call("kkb_shear_and_sum", dev.ptr(data), n, l, T, pos.ctypes.data, ang.ctypes.data,
-              int(ang.size), float(sampling_frequency), float(sound_speed), dev.ptr(out),
-              dev.stream_handle(stream))
+    plan = shear_plans.get(pos, ang, sampling_frequency, sound_speed, T)
+    _lib.call("kkb_shear_plan_run", plan, dev.ptr(data), n, dev.ptr(out), dev.stream_handle(stream))
     return out
 
 

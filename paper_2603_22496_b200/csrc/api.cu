@@ -441,6 +441,69 @@ extern "C" int kkb_analytic_signal(const float *rf, long long n_traces, int n_t,
 
 // =====================================================================
 // K1-K3: shear_and_sum on complex input, all T bins
+struct kkb_shear_plan {
+    int L, M, T;
+    float2 *ramps;  // (M, L, T): exp(2 pi i f_k u_l sin(theta_m) / c) / T, float64-built
+};
+
+extern "C" int kkb_shear_plan_create(const double *positions_host, const double *angles_host, int n_el,
+                                     int n_rx, int n_t, double fs, double c, kkb_shear_plan **out) {
+    if (!out || n_el < 1 || n_rx < 1 || n_t < 1 || n_t > KKB_FFT_MAX_T_TOTAL || !(c > 0)) {
+        set_error("shear_plan: bad sizes");
+        return KKB_ERR_ARG;
+    }
+    const int T = n_t;
+    std::vector<double> tau((size_t)n_el * n_rx), freq(T), scale(T, 1.0 / T);
+    for (int m = 0; m < n_rx; ++m) {
+        double q = sin(angles_host[m]) / c;  // compress.py:79  positions * (sin(theta) / c)
+        for (int l = 0; l < n_el; ++l) tau[(size_t)l * n_rx + m] = positions_host[l] * q;
+    }
+    for (int k = 0; k < T; ++k) freq[k] = fftfreq(k, T, fs);
+    kkb_shear_plan *p = new (std::nothrow) kkb_shear_plan();
+    if (!p) return KKB_ERR_NOMEM;
+    p->L = n_el;
+    p->M = n_rx;
+    p->T = T;
+    cudaError_t e = cudaMalloc(&p->ramps, sizeof(float2) * (size_t)n_rx * n_el * T);
+    if (e != cudaSuccess) {
+        delete p;
+        return cuda_status(e, "cudaMalloc(shear ramps)");
+    }
+    int st = build_ramps(tau.data(), n_el, n_rx, freq.data(), scale.data(), T, p->ramps, 0);
+    if (st) {
+        cudaFree(p->ramps);
+        delete p;
+        return st;
+    }
+    *out = p;
+    return KKB_OK;
+}
+
+extern "C" int kkb_shear_plan_run(kkb_shear_plan *p, const void *data, int n_tx, void *out, void *stream) {
+    if (!p || n_tx < 1) {
+        set_error("shear_plan_run: bad plan or transmit count");
+        return KKB_ERR_ARG;
+    }
+    cudaStream_t s = as_stream(stream);
+    const int T = p->T, L = p->L, M = p->M;
+    const long long ntr = (long long)n_tx * L;
+    Scratch xs(s), ys(s);
+    int st;
+    if ((st = xs.alloc(sizeof(float2) * (size_t)ntr * T))) return st;
+    if ((st = ys.alloc(sizeof(float2) * (size_t)n_tx * M * T))) return st;
+    float2 *X = (float2 *)xs.p, *Y = (float2 *)ys.p;
+    if ((st = fft_c2c((const float2 *)data, T, T, X, T, T, ntr, T, false, 1.0f, s))) return st;
+    if ((st = contract(X, T, p->ramps, T, Y, T, n_tx, L, M, T, s))) return st;
+    return fft_c2c(Y, T, T, (float2 *)out, T, T, (long long)n_tx * M, T, true, 1.0f, s);
+}
+
+extern "C" int kkb_shear_plan_destroy(kkb_shear_plan *p) {
+    if (!p) return KKB_OK;
+    cudaFree(p->ramps);
+    delete p;
+    return KKB_OK;
+}
+
 extern "C" int kkb_shear_and_sum(const void *data, int n_tx, int n_el, int n_t,
                                  const double *positions_host, const double *angles_host, int n_rx,
                                  double fs, double c, void *out, void *stream) {
@@ -448,26 +511,12 @@ extern "C" int kkb_shear_and_sum(const void *data, int n_tx, int n_el, int n_t,
         set_error("shear_and_sum: bad sizes");
         return KKB_ERR_ARG;
     }
-    cudaStream_t s = as_stream(stream);
-    const int T = n_t;
-    const long long ntr = (long long)n_tx * n_el;
-    std::vector<double> tau((size_t)n_el * n_rx), freq(T), scale(T, 1.0 / T);
-    for (int m = 0; m < n_rx; ++m) {
-        double q = sin(angles_host[m]) / c;  // compress.py:79  positions * (sin(theta) / c)
-        for (int l = 0; l < n_el; ++l) tau[(size_t)l * n_rx + m] = positions_host[l] * q;
-    }
-    for (int k = 0; k < T; ++k) freq[k] = fftfreq(k, T, fs);
-    Scratch xs(s), ys(s), rs(s);
-    int st;
-    if ((st = xs.alloc(sizeof(float2) * (size_t)ntr * T))) return st;
-    if ((st = ys.alloc(sizeof(float2) * (size_t)n_tx * n_rx * T))) return st;
-    if ((st = rs.alloc(sizeof(float2) * (size_t)n_rx * n_el * T))) return st;
-    if ((st = build_ramps(tau.data(), n_el, n_rx, freq.data(), scale.data(), T, (float2 *)rs.p, s)))
-        return st;
-    float2 *X = (float2 *)xs.p, *Y = (float2 *)ys.p;
-    if ((st = fft_c2c((const float2 *)data, T, T, X, T, T, ntr, T, false, 1.0f, s))) return st;
-    if ((st = contract(X, T, (const float2 *)rs.p, T, Y, T, n_tx, n_el, n_rx, T, s))) return st;
-    st = fft_c2c(Y, T, T, (float2 *)out, T, T, (long long)n_tx * n_rx, T, true, 1.0f, s);
+    kkb_shear_plan *p = nullptr;
+    int st = kkb_shear_plan_create(positions_host, angles_host, n_el, n_rx, n_t, fs, c, &p);
+    if (st) return st;
+    st = kkb_shear_plan_run(p, data, n_tx, out, stream);
+    cudaStreamSynchronize(as_stream(stream));
+    kkb_shear_plan_destroy(p);
     return st;
 }
 

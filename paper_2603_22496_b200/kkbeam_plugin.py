@@ -6,6 +6,8 @@ globals at call time:
 * ``kkbeam.beamform._kk_kernel``   (beamform.py:212-236, called at 363-374)
 * ``kkbeam.beamform._das_kernel``  (beamform.py:178-209, called at 281-297)
 * ``kkbeam.compress.shear_and_sum`` (compress.py:54-82, called at 120)
+* ``analytic_signal`` (spectral.py:84-93; bound by name in ``kkbeam``,
+  ``kkbeam.spectral`` and ``kkbeam.cli``)
 * ``kkbeam.simulate._render_traces`` (simulate.py:187-220, called at 280-293;
   the forward simulator, §8(f) row 4 — bit-identical on the GPU)
 * ``kkbeam.metrics.gamma_match`` and the CLI's imported name
@@ -65,6 +67,23 @@ def das_kernel(data, ltx, ltz, hyp, base, frac, xcoord, zcoord, upos, tan_max, w
     out[...] = dev.to_host(o)
 
 
+def analytic_signal(rf):
+    """Drop-in for kkbeam.spectral.analytic_signal (spectral.py:84-93): the
+    one-sided FFT -> weights -> inverse FFT on the GPU (K1 + K3), returned
+    in the reference's own AnalyticRF container (so its validation and
+    isinstance checks are unchanged)."""
+    from .spectral import analytic_signal_device
+
+    core = sys.modules.get("kkbeam.core")
+    x = dev.to_device(np.ascontiguousarray(rf.data, dtype=np.float32))
+    out = dev.to_host(analytic_signal_device(x))
+    if core is None:  # not installed against the reference: this package's container
+        from .core import AnalyticRF
+    else:
+        AnalyticRF = core.AnalyticRF
+    return AnalyticRF(out, rf.array, rf.params)
+
+
 def shear_and_sum(data, sampling_frequency, positions, angles, sound_speed):
     """Drop-in for kkbeam.compress.shear_and_sum (complex128 (N, M, T) out)."""
     from .compress import shear_and_sum as gpu_shear
@@ -115,8 +134,10 @@ class Installed:
         self._saved = {}
 
 
-def install(kkbeam_pkg=None) -> Installed:
-    """Rebind the reference's kernel globals to the GPU shims.
+def install(kkbeam_pkg=None, spectral: bool = True) -> Installed:
+    """Rebind the reference's kernel globals to the GPU shims (and, with
+    `spectral`, its analytic_signal: the whole README pipeline
+    analytic_signal -> compress -> kk then runs on the GPU).
 
     Note kkbeam/__init__.py:34 binds ``kkbeam.compress`` to the *function*,
     so the submodule is taken from sys.modules."""
@@ -129,6 +150,12 @@ def install(kkbeam_pkg=None) -> Installed:
     bf._kk_kernel = kk_kernel
     bf._das_kernel = das_kernel
     cp.shear_and_sum = shear_and_sum
+    if spectral:  # analytic_signal is imported by name into kkbeam and kkbeam.cli too
+        for name in ("kkbeam.spectral", "kkbeam", "kkbeam.cli"):
+            mod = sys.modules.get(name)
+            if mod is not None and hasattr(mod, "analytic_signal"):
+                saved[(mod, "analytic_signal")] = mod.analytic_signal
+                mod.analytic_signal = analytic_signal
     sim = sys.modules.get("kkbeam.simulate")
     if sim is not None and hasattr(sim, "_render_traces"):
         saved[(sim, "_render_traces")] = sim._render_traces

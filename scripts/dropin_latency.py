@@ -8,7 +8,10 @@ What an unmodified kkbeam caller gets:
 * ``kk``: this package's ``kk(CompressedRF, DelayLUTSet)`` (same signature
   as the reference's, container validation included);
 * ``pipeline``: ``analytic_signal -> compress -> kk`` through the public API,
-  numpy at every boundary (the reference's README flow).
+  numpy at every boundary (the reference's README flow);
+* with the reference installed in baseline/_ref: its own README pipeline,
+  unmodified, on the host (numba / numpy) and with ``kkbeam_plugin``
+  installed (its kernels and analytic_signal rebound to libkkb).
 Beside them, on the same host: the oracle's C/OpenMP restatement of
 ``_kk_kernel`` (all cores) and the reference benchmark's complex64 stage 1
 (numpy/scipy) — the CPU cost each call replaces.
@@ -78,6 +81,41 @@ def main():
         r["pixel_pairs"] = g.nx * g.nz * w.pairs
         res["configs"][w.name] = r
         print(w.name, json.dumps(r), flush=True)
+    # the unmodified reference's README pipeline, numba/numpy on the host vs
+    # the same calls with kkbeam_plugin installed (when baseline/_ref holds it)
+    ref_root = os.path.join(ROOT, "baseline", "_ref")
+    if os.path.isdir(os.path.join(ref_root, "kkbeam")):
+        os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache_dropin")
+        sys.path.insert(0, ref_root)
+        import kkbeam as rk
+
+        for cfg in (1, 4):
+            w = configs.CONFIGS[cfg]() if cfg == 1 else configs.config4(frames=1)
+            arr, p, rx, g = w.array, w.params, w.receive, w.grid
+            rarr = rk.TransducerArray(arr.num_elements, arr.pitch, arr.center_frequency,
+                                      arr.sampling_frequency, arr.fractional_bandwidth)
+            rp = rk.AcquisitionParams(p.sound_speed, p.transmit_angles, p.num_samples, start_time=p.start_time)
+            rrx = rk.explicit_angles(rx.angles, rx.delta_theta_i)
+            rg = rk.ImageGrid(g.x0, g.z0, g.dx, g.dz, g.nx, g.nz)
+            rf = rk.RFVolume(configs.noise_rf(p.num_transmits, arr.num_elements, p.num_samples, seed=3), rarr, rp)
+            luts = rk.build_kk_luts(rg, rp, rrx)
+
+            def pipe():
+                return rk.kk(rk.compress(rk.analytic_signal(rf), rrx), luts)
+
+            cpu_ms = med(pipe, reps=5, warm=3)
+            cpu_img = pipe().pixels
+            h = kkbeam_plugin.install(rk)
+            try:
+                gpu_ms = med(pipe, reps=20, warm=3)
+                gpu_img = pipe().pixels
+            finally:
+                h.restore()
+            r = {"reference_pipeline_cpu_ms": cpu_ms, "reference_pipeline_with_plugin_ms": gpu_ms,
+                 "speedup": cpu_ms / gpu_ms,
+                 "rel_l2_plugin_vs_cpu": float(np.linalg.norm(gpu_img - cpu_img) / np.linalg.norm(cpu_img))}
+            res["configs"][w.name]["unmodified_reference_readme_pipeline"] = r
+            print(w.name, "reference pipeline", json.dumps(r), flush=True)
     if len(sys.argv) > 1:
         with open(sys.argv[1], "w") as f:
             json.dump(res, f, indent=1)
