@@ -278,6 +278,17 @@ int kkb_decomposer_symmetric_classes(const kkb_decomposer *p);
 #define KKB_CONTRACT_TENSOR 1
 int kkb_decomposer_set_contraction(kkb_decomposer *p, int form);
 int kkb_decomposer_contraction(const kkb_decomposer *p);
+/* Stage-1 ring mode: K1 (real FFT) and a persistent K2 (contraction, FMA
+ * form) run concurrently, the spectra handed over through `slots` row-tile
+ * slots of an L2-resident ring (16 (frame, transmit) rows each) instead of a
+ * full spectra array in HBM; `consumer_ctas` persistent K2 CTAs (0: half the
+ * SMs).  Used for float32 / int16 RF with a compile-time FFT length, an even
+ * element count and <= 6 symmetric classes; otherwise the three-kernel path
+ * runs.  slots = 0 turns it off.  Environment KKB_S1_RING=slots[,ctas] sets
+ * it at creation.  kkb_decomposer_ring_error (synchronous) reports a bounded
+ * spin that timed out (1), which would mean a scheduling failure. */
+int kkb_decomposer_set_ring(kkb_decomposer *p, int slots, int consumer_ctas);
+int kkb_decomposer_ring_error(kkb_decomposer *p, int *flag);
 /* bytes of device scratch held by the plan */
 long long kkb_decomposer_workspace_bytes(const kkb_decomposer *p);
 int kkb_decomposer_destroy(kkb_decomposer *p);

@@ -58,6 +58,8 @@ SIGNATURES = {
     "kkb_decomposer_symmetric_classes": [P],
     "kkb_decomposer_set_contraction": [P, I],
     "kkb_decomposer_contraction": [P],
+    "kkb_decomposer_set_ring": [P, I, I],
+    "kkb_decomposer_ring_error": [P, P],
     "kkb_decomposer_workspace_bytes": [P],
     "kkb_decomposer_destroy": [P],
     "kkb_log_compress": [P, P, I, LL, F, P, P],

@@ -520,6 +520,8 @@ extern "C" int kkb_shear_and_sum(const void *data, int n_tx, int n_el, int n_t,
     return st;
 }
 
+#define KKB_RING_TILE_ROWS 16  // rows of one contraction tile (k_contract_sym<6, 2>)
+
 // =====================================================================
 // fused stage-1 plan
 struct kkb_decomposer {
@@ -545,6 +547,14 @@ struct kkb_decomposer {
     // 3xTF32 class tables in the UMMA operand layout, built on first use
     int form = KKB_CONTRACT_FMA;
     float *tctab = nullptr;
+    // stage-1 ring mode (kkb_decomposer_set_ring): K1 and a persistent K2 run
+    // concurrently, the spectra passing through R L2-resident row-tile slots
+    int ring_R = 0, ring_ctas = 0;
+    float2 *ring = nullptr;
+    int *ring_cnt = nullptr;  // fft_done[tiles] | con_done[tiles] | queue | started | err
+    long long ring_tiles = 0;
+    cudaStream_t ring_side = nullptr;
+    cudaEvent_t ring_ev[2] = {};
 };
 
 // Pair receive angles into +/- classes and build the cos/sin table; P = 0
@@ -647,6 +657,13 @@ extern "C" int kkb_decomposer_create(int n_tx, int n_el, int n_t, const double *
         if (f && !strcmp(f, "tc") && p->P >= 1 && p->P <= 16)
             st = kkb_decomposer_set_contraction(p, KKB_CONTRACT_TENSOR);
     }
+    if (!st) {  // KKB_S1_RING=R[,ctas]: stage-1 ring mode by default
+        if (const char *r = getenv("KKB_S1_RING")) {
+            int R = atoi(r), ctas = 0;
+            if (const char *c2 = strchr(r, ',')) ctas = atoi(c2 + 1);
+            if (R >= 2) st = kkb_decomposer_set_ring(p, R, ctas);
+        }
+    }
     if (st) {
         cudaFree(p->ramps);
         cudaFree(p->X);
@@ -685,6 +702,39 @@ extern "C" int kkb_decomposer_set_contraction(kkb_decomposer *p, int form) {
 
 extern "C" int kkb_decomposer_contraction(const kkb_decomposer *p) { return p ? p->form : -1; }
 
+extern "C" int kkb_decomposer_set_ring(kkb_decomposer *p, int slots, int consumer_ctas) {
+    if (!p || slots < 0 || slots == 1 || consumer_ctas < 0) {
+        set_error("set_ring: slots 0 (off) or >= 2, consumer_ctas >= 0");
+        return KKB_ERR_ARG;
+    }
+    KKB_TRY_CUDA(cudaDeviceSynchronize(), "sync before ring realloc");
+    cudaFree(p->ring);
+    p->ring = nullptr;
+    p->ring_R = 0;
+    if (slots == 0) return KKB_OK;
+    const size_t bytes = sizeof(float2) * (size_t)slots * KKB_RING_TILE_ROWS * p->L * p->ldk;
+    KKB_TRY_CUDA(cudaMalloc(&p->ring, bytes), "cudaMalloc(ring)");
+    if (!p->ring_side) {
+        KKB_TRY_CUDA(cudaStreamCreateWithFlags(&p->ring_side, cudaStreamNonBlocking), "ring stream");
+        for (int i = 0; i < 2; ++i)
+            KKB_TRY_CUDA(cudaEventCreateWithFlags(&p->ring_ev[i], cudaEventDisableTiming), "ring event");
+    }
+    p->ring_R = slots;
+    p->ring_ctas = consumer_ctas > 0 ? consumer_ctas : sm_count() / 2;
+    return KKB_OK;
+}
+
+extern "C" int kkb_decomposer_ring_error(kkb_decomposer *p, int *flag) {
+    if (!p || !flag) return KKB_ERR_ARG;
+    *flag = 0;
+    if (!p->ring_cnt) return KKB_OK;
+    KKB_TRY_CUDA(cudaDeviceSynchronize(), "sync ring error");
+    unsigned e = 0;
+    KKB_TRY_CUDA(cudaMemcpy(&e, p->ring_cnt + 2 * p->ring_tiles + 2, sizeof(e), cudaMemcpyDeviceToHost), "read ring error");
+    *flag = (int)e;
+    return KKB_OK;
+}
+
 extern "C" long long kkb_decomposer_workspace_bytes(const kkb_decomposer *p) { return p ? p->bytes : 0; }
 
 // exact int16 -> float32 widening (the reference consumes q.astype(float32))
@@ -692,6 +742,51 @@ __global__ void k_i16_to_f32(const short *__restrict__ in, long long n, float *_
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
          i += (long long)gridDim.x * blockDim.x)
         out[i] = (float)in[i];
+}
+
+__global__ void k_wait_started(const int *started, unsigned *err) {
+    if (threadIdx.x == 0) ring_wait_geq(started, 1, err);
+}
+
+// K1 -> K2 through the L2 ring for F frames (one pass), then K3 on `s`.
+static int decomposer_run_ring(kkb_decomposer *p, const void *rf_c, int in_kind, int F, float2 *tr_c,
+                               cudaStream_t s) {
+    const int N = p->N, L = p->L, T = p->T, M = p->M, K = p->K, ldk = p->ldk;
+    const long long B = (long long)F * N;
+    const long long tiles = (B + KKB_RING_TILE_ROWS - 1) / KKB_RING_TILE_ROWS;
+    if (tiles > p->ring_tiles) {
+        cudaFree(p->ring_cnt);
+        p->ring_cnt = nullptr;
+        KKB_TRY_CUDA(cudaMalloc(&p->ring_cnt, sizeof(int) * (size_t)(2 * tiles + 3)), "cudaMalloc(ring counters)");
+        p->ring_tiles = tiles;
+    }
+    int *fft_done = p->ring_cnt, *con_done = p->ring_cnt + tiles, *queue = con_done + tiles, *started = queue + 1;
+    unsigned *err = reinterpret_cast<unsigned *>(started + 1);
+    KKB_TRY_CUDA(cudaMemsetAsync(p->ring_cnt, 0, sizeof(int) * (size_t)(2 * tiles + 2), s), "zero ring counters");
+    Stage1Ring rs;
+    rs.fft_done = fft_done;
+    rs.con_done = con_done;
+    rs.R = p->ring_R;
+    rs.con_per_tile = (K + 31) / 32;
+    rs.traces_per_tile = (long long)KKB_RING_TILE_ROWS * L;
+    rs.err = err;
+    FftPlan plan;
+    int st = get_fft_plan(T, &plan);
+    if (st) return st;
+    float2 *Y = p->Y;
+    // the persistent consumer first (side stream), K1 once it is resident
+    KKB_TRY_CUDA(cudaEventRecord(p->ring_ev[0], s), "record ring fork");
+    KKB_TRY_CUDA(cudaStreamWaitEvent(p->ring_side, p->ring_ev[0], 0), "wait ring fork");
+    st = contract_sym_ring(p->ring, ldk, p->cs, ldk, Y, ldk, B, L, M, K, p->P, p->mp.data(), p->mm.data(), rs,
+                           queue, started, p->ring_ctas, p->ring_side);
+    if (st) return st;
+    k_wait_started<<<1, 32, 0, s>>>(started, err);
+    KKB_CHECK_LAUNCH("k_wait_started");
+    st = fft_r2c_ct_ring(rf_c, in_kind, B * L, T, p->ring, ldk, K, nullptr, plan.tws, s, rs);
+    if (st) return st;
+    KKB_TRY_CUDA(cudaEventRecord(p->ring_ev[1], p->ring_side), "record ring join");
+    KKB_TRY_CUDA(cudaStreamWaitEvent(s, p->ring_ev[1], 0), "wait ring join");
+    return fft_c2c(Y, ldk, K, tr_c, T, T, B * M, T, true, 1.0f, s);
 }
 
 static int decomposer_run(kkb_decomposer *p, const void *rf, int in_kind, int n_frames,
@@ -729,6 +824,11 @@ static int decomposer_run(kkb_decomposer *p, const void *rf, int in_kind, int n_
                 (const short *)rf_c, n, conv);
             KKB_CHECK_LAUNCH("k_i16_to_f32");
             rf_c = (const char *)conv;
+        }
+        if (p->ring_R > 0 && !scatter && !piped && !(in_kind && !i16_direct) && fft_ct_supported(T) &&
+            !(L & 1) && p->P >= 1 && p->P <= 6 && p->form == KKB_CONTRACT_FMA) {
+            if ((st = decomposer_run_ring(p, rf_c, in_kind, F, tr_c, cs))) return st;
+            continue;
         }
         if (i16_direct) {
             st = fft_r2c_ct(rf_c, 1, (long long)F * N * L, T, X, ldk, K, nullptr, plan.tws, cs, L);
@@ -853,6 +953,11 @@ extern "C" int kkb_decomposer_destroy(kkb_decomposer *p) {
     cudaFree(p->Y);
     cudaFree(p->cs);
     cudaFree(p->tctab);
+    cudaFree(p->ring);
+    cudaFree(p->ring_cnt);
+    if (p->ring_side) cudaStreamDestroy(p->ring_side);
+    for (int i = 0; i < 2; ++i)
+        if (p->ring_ev[i]) cudaEventDestroy(p->ring_ev[i]);
     delete p;
     return KKB_OK;
 }

@@ -22,6 +22,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "fft.cuh"
 #include "kk.cuh"
 
 namespace kkb {
@@ -253,22 +254,21 @@ struct SymClasses {
     short mm[KKB_MAX_CLASSES];  // output receive index of -theta, -1 for theta = 0
 };
 
+// One tile: KT bins from k0, BT rows from b0 (X rows counted from X, Y rows
+// from Y; rows >= B are not read or written), classes from p0.
 template <int PC, int NB>
-__global__ void __launch_bounds__(256, 2)
-k_contract_sym(const float2 *__restrict__ X, long long ldx, const float2 *__restrict__ CS,
-               long long ldc, float2 *__restrict__ Y, long long ldy, long long B, int L, int M,
-               int Kb, const SymClasses cls) {
+__device__ __forceinline__ void contract_sym_tile(const float2 *__restrict__ X, long long ldx,
+                                                  const float2 *__restrict__ CS, long long ldc,
+                                                  float2 *__restrict__ Y, long long ldy, long long B, int L,
+                                                  int M, int Kb, const SymClasses &cls, int k0, long long b0,
+                                                  int p0, float2 *csm) {
     constexpr int KT = KKB_CT_KT, BT = 8 * NB, LC = KKB_CS_LC;
     static_assert(BT == 16 || BT == 32, "staging covers 16 or 2 x 16 rows");
-    extern __shared__ __align__(16) float2 csm[];
     float2 *Xl = csm;                     // [2][LC][BT][KT]
     float2 *Xr = Xl + 2 * LC * BT * KT;   // [2][LC][BT][KT] mirrored elements
     float2 *Cs = Xr + 2 * LC * BT * KT;   // [2][LC][PC][KT]
     const int tid = threadIdx.x;
     const int kx = tid % KT, bg = tid / KT;
-    const int k0 = blockIdx.x * KT;
-    const long long b0 = (long long)blockIdx.y * BT;
-    const int p0 = blockIdx.z * PC;
     const int Lp = (L + 1) / 2;
     const int nlc = (Lp + LC - 1) / LC;
     const int kc = tid & 15, bbA = tid >> 4;
@@ -368,6 +368,55 @@ k_contract_sym(const float2 *__restrict__ X, long long ldx, const float2 *__rest
 }
 
 template <int PC, int NB>
+__global__ void __launch_bounds__(256, 2)
+k_contract_sym(const float2 *__restrict__ X, long long ldx, const float2 *__restrict__ CS,
+               long long ldc, float2 *__restrict__ Y, long long ldy, long long B, int L, int M,
+               int Kb, const SymClasses cls) {
+    extern __shared__ __align__(16) float2 csm[];
+    contract_sym_tile<PC, NB>(X, ldx, CS, ldc, Y, ldy, B, L, M, Kb, cls, blockIdx.x * KKB_CT_KT,
+                              (long long)blockIdx.y * (8 * NB), blockIdx.z * PC, csm);
+}
+
+// Persistent consumer of the stage-1 ring (Stage1Ring, fft.cuh): work item
+// i = (row-tile t, bin tile) taken from a global queue in order; waits until
+// K1 has written all of tile t's spectra into ring slot t % R, contracts them
+// (X read from the slot with L2-only cp.async.cg loads), writes Y rows of the
+// tile, and releases the slot for K1's tile t + R.  `started` tells the
+// launcher this kernel is resident before K1 floods the SMs.
+template <int PC, int NB>
+__global__ void __launch_bounds__(256, 2)
+k_contract_sym_ring(const float2 *__restrict__ ring, long long ldx, const float2 *__restrict__ CS,
+                    long long ldc, float2 *__restrict__ Y, long long ldy, long long B, int L, int M,
+                    int Kb, const SymClasses cls, const Stage1Ring rs, int *queue, int *started) {
+    constexpr int BT = 8 * NB;
+    extern __shared__ __align__(16) float2 csm[];
+    __shared__ int item_s;
+    if (threadIdx.x == 0) atomicAdd(started, 1);
+    const int nkt = (Kb + KKB_CT_KT - 1) / KKB_CT_KT;
+    const long long ntiles = (B + BT - 1) / BT;
+    const long long nitems = ntiles * nkt;
+    for (;;) {
+        if (threadIdx.x == 0) item_s = atomicAdd(queue, 1);
+        __syncthreads();
+        const long long item = item_s;
+        if (item >= nitems) return;
+        const long long t = item / nkt;
+        const int kt = (int)(item - t * nkt);
+        const long long rows = B - t * BT < BT ? B - t * BT : BT;
+        if (threadIdx.x == 0) ring_wait_geq(rs.fft_done + t, (int)(rows * L / 2), rs.err);
+        __syncthreads();
+        const float2 *Xs = ring + (t % rs.R) * (long long)BT * L * ldx;
+        contract_sym_tile<PC, NB>(Xs, ldx, CS, ldc, Y + t * BT * M * ldy, ldy, rows, L, M, Kb, cls,
+                                  kt * KKB_CT_KT, 0, 0, csm);
+        __syncthreads();  // every read of the slot done (and item_s reusable)
+        if (threadIdx.x == 0) {
+            __threadfence();
+            atomicAdd(rs.con_done + t, 1);
+        }
+    }
+}
+
+template <int PC, int NB>
 static int launch_contract_sym(const float2 *X, long long ldx, const float2 *CS, long long ldc,
                                float2 *Y, long long ldy, long long B, int L, int M, int Kb,
                                const SymClasses &cls, cudaStream_t s) {
@@ -404,6 +453,32 @@ int contract_sym(const float2 *X, long long ldx, const float2 *CS, long long ldc
     if (P <= 3) return launch_contract_sym<3, 4>(X, ldx, CS, ldc, Y, ldy, B, L, M, Kb, cls, s);
     if (P <= 6) return launch_contract_sym<6, KKB_CS_NB6>(X, ldx, CS, ldc, Y, ldy, B, L, M, Kb, cls, s);
     return launch_contract_sym<8, 2>(X, ldx, CS, ldc, Y, ldy, B, L, M, Kb, cls, s);
+}
+
+int contract_sym_ring(const float2 *ring, long long ldx, const float2 *CS, long long ldc, float2 *Y,
+                      long long ldy, long long B, int L, int M, int Kb, int P, const short *mp,
+                      const short *mm, const Stage1Ring &rs, int *queue, int *started, int nctas,
+                      cudaStream_t s) {
+    if (B <= 0 || Kb <= 0) return KKB_OK;
+    if (P < 1 || P > 6 || ((ldx | ldc) & 1)) {
+        set_error("contract_sym_ring: 1..6 classes and even row strides");
+        return KKB_ERR_ARG;
+    }
+    SymClasses cls{};
+    cls.P = P;
+    for (int p = 0; p < P; ++p) {
+        cls.mp[p] = mp[p];
+        cls.mm[p] = mm[p];
+    }
+    constexpr int BT = 8 * KKB_CS_NB6;
+    const int sm = (int)sizeof(float2) * 2 * KKB_CS_LC * KKB_CT_KT * (2 * BT + 6);
+    KKB_TRY_CUDA(cudaFuncSetAttribute(k_contract_sym_ring<6, KKB_CS_NB6>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, sm),
+                 "smem attr contract_sym_ring");
+    k_contract_sym_ring<6, KKB_CS_NB6><<<nctas, 256, sm, s>>>(ring, ldx, CS, ldc, Y, ldy, B, L, M, Kb, cls, rs,
+                                                               queue, started);
+    KKB_CHECK_LAUNCH("k_contract_sym_ring");
+    return KKB_OK;
 }
 
 int contract(const float2 *X, long long ldx, const float2 *R, long long ldr, float2 *Y,

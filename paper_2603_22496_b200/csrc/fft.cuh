@@ -26,6 +26,36 @@ struct RowScatter {
     float2 *dst[KKB_ROW_SCATTER_MAX] = {};
 };
 
+// Stage-1 handoff through an L2-resident ring (decomposer "ring" mode): K1
+// writes the spectra of global row-tile t (tile_rows (frame, transmit) rows)
+// into ring slot t % R once the persistent contraction has released the slot
+// (con_done[t - R] == con_per_tile) and counts its transform pairs into
+// fft_done[t]; the contraction consumes a tile when fft_done[t] reaches the
+// tile's pair count.  Spins are bounded: on a timeout the kernel raises *err
+// and proceeds (no hang; the result is then wrong and the caller fails).
+struct Stage1Ring {
+    int *fft_done = nullptr;
+    int *con_done = nullptr;
+    int R = 0;
+    int con_per_tile = 0;
+    long long traces_per_tile = 0;  // tile_rows * L
+    unsigned *err = nullptr;
+};
+
+// wait until *p >= target (acquire); false after ~0.5 s (sets *err)
+__device__ __forceinline__ bool ring_wait_geq(const int *p, int target, unsigned *err) {
+    for (long long it = 0;; ++it) {
+        int v;
+        asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+        if (v >= target) return true;
+        if (it > (1LL << 21)) {
+            atomicOr(err, 1u);
+            return false;
+        }
+        __nanosleep(256);
+    }
+}
+
 struct FftPlan {
     int T;
     int nstages;
@@ -57,6 +87,11 @@ void fft_ct_twiddles(int T, std::vector<float2> &out);
 int fft_r2c_ct(const void *in, int in_kind, long long ntraces, int T, float2 *out,
                long long out_stride, int K, const float *bin_scale, const float2 *tws,
                cudaStream_t s, long long group_rows = 0);
+// fft_r2c_ct writing through the stage-1 ring (even group_rows: pairs never
+// straddle a (frame, transmit) row, so a row-tile's pairs are contiguous CTAs)
+int fft_r2c_ct_ring(const void *in, int in_kind, long long ntraces, int T, float2 *ring,
+                    long long out_stride, int K, const float *bin_scale, const float2 *tws,
+                    cudaStream_t s, const Stage1Ring &rs);
 int fft_c2c_ct(const float2 *in, long long in_stride, int in_len, float2 *out, long long out_stride,
                int out_len, long long ntraces, int T, bool inverse, float scale, const float2 *tw,
                cudaStream_t s, const RowScatter *sc = nullptr);

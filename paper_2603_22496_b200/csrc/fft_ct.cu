@@ -267,15 +267,24 @@ __device__ __forceinline__ float to_f(short x) { return (float)x; }  // exact
 // batch size, frame position and the transmit split across GPUs.
 // Even groups pair exactly like the whole batch (rows 2p, 2p+1), so only odd
 // groups take the GROUPED instance.
-template <int T, typename InT, bool GROUPED = false>
+template <int T, typename InT, bool GROUPED = false, bool RING = false>
 __global__ void __launch_bounds__(Plan<T>::NT)
 k_r2c(const InT *__restrict__ in, long long ntraces, float2 *__restrict__ out,
       long long out_stride, int K, const float *__restrict__ bin_scale,
-      const float2 *__restrict__ tw, int grp) {
+      const float2 *__restrict__ tw, int grp, const Stage1Ring rs = Stage1Ring{}) {
     using P = Plan<T>;
     __shared__ __align__(16) float2 buf[T];
     long long r0;
     bool l1;
+    long long tile = 0;
+    if constexpr (RING) {
+        // wait until the contraction released this row-tile's ring slot
+        tile = 2 * (long long)blockIdx.x / rs.traces_per_tile;
+        if (tile >= rs.R) {
+            if (threadIdx.x == 0) ring_wait_geq(rs.con_done + (tile - rs.R), rs.con_per_tile, rs.err);
+            __syncthreads();
+        }
+    }
     if constexpr (GROUPED) {
         const unsigned ppg = (unsigned)(grp + 1) >> 1, gi = blockIdx.x / ppg, q = blockIdx.x - gi * ppg;
         r0 = (long long)gi * grp + 2 * q;
@@ -317,8 +326,10 @@ k_r2c(const InT *__restrict__ in, long long ntraces, float2 *__restrict__ out,
         }
     }
     __syncthreads();
-    float2 *o0 = out + r0 * out_stride;
-    float2 *o1 = out + (r0 + 1) * out_stride;
+    long long orow = r0;
+    if constexpr (RING) orow = (tile % rs.R) * rs.traces_per_tile + (r0 - tile * rs.traces_per_tile);
+    float2 *o0 = out + orow * out_stride;
+    float2 *o1 = out + (orow + 1) * out_stride;
 #pragma unroll
     for (int t = 0; t < S2::ITER; ++t) {
         const int j = S2::lane_j(t);
@@ -333,6 +344,13 @@ k_r2c(const InT *__restrict__ in, long long ntraces, float2 *__restrict__ out,
                 o0[k] = make_float2(s * (zk.x + zn.x), s * (zk.y - zn.y));
                 if (l1) o1[k] = make_float2(s * (zk.y + zn.y), -s * (zk.x - zn.x));
             }
+        }
+    }
+    if constexpr (RING) {  // this pair's spectra are in the slot: count it (release)
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            atomicAdd(rs.fft_done + tile, 1);
         }
     }
 }
@@ -447,11 +465,11 @@ static int launch_r2c(const void *in, int in_kind, long long ntraces, float2 *ou
     if (in_kind) {
         auto fn = g ? ct::k_r2c<T, short, true> : ct::k_r2c<T, short, false>;
         fn<<<npairs, ct::Plan<T>::NT, 0, s>>>(reinterpret_cast<const short *>(in), ntraces, out,
-                                              out_stride, K, bin_scale, tw, grp);
+                                              out_stride, K, bin_scale, tw, grp, Stage1Ring{});
     } else {
         auto fn = g ? ct::k_r2c<T, float, true> : ct::k_r2c<T, float, false>;
         fn<<<npairs, ct::Plan<T>::NT, 0, s>>>(reinterpret_cast<const float *>(in), ntraces, out,
-                                              out_stride, K, bin_scale, tw, grp);
+                                              out_stride, K, bin_scale, tw, grp, Stage1Ring{});
     }
     KKB_CHECK_LAUNCH("k_fft_r2c_ct");
     return KKB_OK;
@@ -490,6 +508,34 @@ int fft_r2c_ct(const void *in, int in_kind, long long ntraces, int T, float2 *ou
         case 1536: return launch_r2c<1536>(in, in_kind, ntraces, out, out_stride, K, bin_scale, tw, s, grp);
         case 2048: return launch_r2c<2048>(in, in_kind, ntraces, out, out_stride, K, bin_scale, tw, s, grp);
         case 4096: return launch_r2c<4096>(in, in_kind, ntraces, out, out_stride, K, bin_scale, tw, s, grp);
+    }
+    return KKB_ERR_UNSUPPORTED;
+}
+
+template <int T>
+static int launch_r2c_ring(const void *in, int in_kind, long long ntraces, float2 *ring, long long out_stride,
+                           int K, const float *bin_scale, const float2 *tw, cudaStream_t s, const Stage1Ring &rs) {
+    const unsigned npairs = (unsigned)ceil_div(ntraces, 2);
+    if (in_kind)
+        ct::k_r2c<T, short, false, true><<<npairs, ct::Plan<T>::NT, 0, s>>>(
+            reinterpret_cast<const short *>(in), ntraces, ring, out_stride, K, bin_scale, tw, 2, rs);
+    else
+        ct::k_r2c<T, float, false, true><<<npairs, ct::Plan<T>::NT, 0, s>>>(
+            reinterpret_cast<const float *>(in), ntraces, ring, out_stride, K, bin_scale, tw, 2, rs);
+    KKB_CHECK_LAUNCH("k_fft_r2c_ct_ring");
+    return KKB_OK;
+}
+
+int fft_r2c_ct_ring(const void *in, int in_kind, long long ntraces, int T, float2 *ring,
+                    long long out_stride, int K, const float *bin_scale, const float2 *tws,
+                    cudaStream_t s, const Stage1Ring &rs) {
+    if (ntraces <= 0) return KKB_OK;
+    if ((ntraces & 1) || (rs.traces_per_tile & 1) || ceil_div(ntraces, 2) > 0x7fffffffLL) return KKB_ERR_UNSUPPORTED;
+    switch (T) {
+        case 1024: return launch_r2c_ring<1024>(in, in_kind, ntraces, ring, out_stride, K, bin_scale, tws, s, rs);
+        case 1536: return launch_r2c_ring<1536>(in, in_kind, ntraces, ring, out_stride, K, bin_scale, tws, s, rs);
+        case 2048: return launch_r2c_ring<2048>(in, in_kind, ntraces, ring, out_stride, K, bin_scale, tws, s, rs);
+        case 4096: return launch_r2c_ring<4096>(in, in_kind, ntraces, ring, out_stride, K, bin_scale, tws, s, rs);
     }
     return KKB_ERR_UNSUPPORTED;
 }

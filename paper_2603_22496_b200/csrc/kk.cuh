@@ -139,6 +139,12 @@ int contract_sym(const float2 *X, long long ldx, const float2 *CS, long long ldc
                  const short *mm, cudaStream_t s);
 int contract(const float2 *X, long long ldx, const float2 *R, long long ldr, float2 *Y,
              long long ldy, long long B, int L, int M, int Kb, cudaStream_t s);
+struct Stage1Ring;
+// persistent ring consumer of contract_sym (decomposer ring mode), nctas CTAs
+int contract_sym_ring(const float2 *ring, long long ldx, const float2 *CS, long long ldc, float2 *Y,
+                      long long ldy, long long B, int L, int M, int Kb, int P, const short *mp,
+                      const short *mm, const Stage1Ring &rs, int *queue, int *started, int nctas,
+                      cudaStream_t s);
 // tensor-core (tcgen05, 3xTF32) form of contract_sym (contract_tc.cu)
 int build_tc_table(const float2 *cs, long long ldc, int P, int L, int Kb, float **tab, long long *bytes,
                    cudaStream_t s);
