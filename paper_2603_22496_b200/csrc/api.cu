@@ -720,7 +720,9 @@ extern "C" int kkb_decomposer_set_ring(kkb_decomposer *p, int slots, int consume
             KKB_TRY_CUDA(cudaEventCreateWithFlags(&p->ring_ev[i], cudaEventDisableTiming), "ring event");
     }
     p->ring_R = slots;
-    p->ring_ctas = consumer_ctas > 0 ? consumer_ctas : sm_count() / 2;
+    // consumers must leave every SM room for K1 (a consumer CTA takes half an
+    // SM's registers): at most one per SM
+    p->ring_ctas = std::min(consumer_ctas > 0 ? consumer_ctas : sm_count() / 2, sm_count());
     return KKB_OK;
 }
 
@@ -762,7 +764,7 @@ static int decomposer_run_ring(kkb_decomposer *p, const void *rf_c, int in_kind,
     }
     int *fft_done = p->ring_cnt, *con_done = p->ring_cnt + tiles, *queue = con_done + tiles, *started = queue + 1;
     unsigned *err = reinterpret_cast<unsigned *>(started + 1);
-    KKB_TRY_CUDA(cudaMemsetAsync(p->ring_cnt, 0, sizeof(int) * (size_t)(2 * tiles + 2), s), "zero ring counters");
+    KKB_TRY_CUDA(cudaMemsetAsync(p->ring_cnt, 0, sizeof(int) * (size_t)(2 * tiles + 3), s), "zero ring counters");
     Stage1Ring rs;
     rs.fft_done = fft_done;
     rs.con_done = con_done;

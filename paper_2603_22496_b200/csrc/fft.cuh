@@ -42,17 +42,21 @@ struct Stage1Ring {
     unsigned *err = nullptr;
 };
 
-// wait until *p >= target (acquire); false after ~0.5 s (sets *err)
+// wait until *p >= target (acquire); false after 2 s of %globaltimer (sets *err)
 __device__ __forceinline__ bool ring_wait_geq(const int *p, int target, unsigned *err) {
-    for (long long it = 0;; ++it) {
+    unsigned long long t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    for (;;) {
         int v;
         asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
         if (v >= target) return true;
-        if (it > (1LL << 21)) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        if (t - t0 > 2000000000ull) {
             atomicOr(err, 1u);
             return false;
         }
-        __nanosleep(256);
+        __nanosleep(128);
     }
 }
 

@@ -35,7 +35,7 @@ def main():
     t_ref = timed()
     ref = eng.traces.clone()
     print(json.dumps({"mode": "three-kernel", "frames": F, "decompose_ms": t_ref}), flush=True)
-    for R, ctas in ((4, 74), (4, 148), (8, 74), (8, 148), (2, 148), (4, 37), (4, 296)):
+    for R, ctas in ((4, 74), (8, 74), (8, 148), (4, 148), (4, 37), (6, 110)):
         _lib.call("kkb_decomposer_set_ring", eng._dec, R, ctas)
         eng.traces.zero_()
         t = timed()
