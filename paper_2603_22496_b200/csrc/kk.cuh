@@ -105,13 +105,14 @@ int kk_check_windows(const double *ltx, const double *ltz, const double *lrx, co
                      KKWindows *win, cudaStream_t s);
 
 // tensor-core (tcgen05) form of K5 (kk_gather_tc.cu): 8 x 16-pixel tiles,
-// up to 128 frames per CTA; W = the tile window (<= 64)
+// 64 frames per CTA; W = the tile window (<= KKB_KK_TC_W)
 int kk_gather_tc(const float2 *data, int N, int M, int T, const double *ltx, const double *ltzT,
                  const double *lrx, const double *lrzT, int nx, int nz, const double *w, double fs,
                  double shift, int linear, void *out, int out_kind, int n_frames, long long data_fs,
                  long long out_fs, float *inten, unsigned *fmax, int W, int accum, cudaStream_t s);
 #define KKB_KK_TC_TZ 8
 #define KKB_KK_TC_TX 16
+#define KKB_KK_TC_W 32    // window samples per (tile, pair)
 
 // instance the last kk_gather dispatch launched (KKB_KK_INST_*, include/kkb.h)
 int kk_last_instance();

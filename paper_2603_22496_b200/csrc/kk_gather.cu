@@ -890,7 +890,7 @@ int kk_check_windows(const double *ltx, const double *ltz, const double *lrx, co
                                                              sh.tz, sh.W, fs, shift, 1 << insts[k], d);
         KKB_CHECK_LAUNCH("k_kk_window_check");
     }
-    if (win->tc >= 2 && win->tc <= 64 && ceil_div(nz, KKB_KK_TC_TZ) * ceil_div(nx, KKB_KK_TC_TX) <= 0x7fffffffLL &&
+    if (win->tc >= 2 && win->tc <= KKB_KK_TC_W && ceil_div(nz, KKB_KK_TC_TZ) * ceil_div(nx, KKB_KK_TC_TX) <= 0x7fffffffLL &&
         N <= 65535) {  // the tensor-core gather's 8 x 16 tile
         dim3 grid((unsigned)(ceil_div(nz, KKB_KK_TC_TZ) * ceil_div(nx, KKB_KK_TC_TX)), (unsigned)N);
         const size_t smem = sizeof(int) * (size_t)M;
@@ -1004,8 +1004,8 @@ int kk_gather(const float2 *data, int N, int M, int T, const double *ltx, const 
     {
         const char *fi = getenv("KKB_KK_INST");
         const bool want = fi && !strcmp(fi, "tc");
-        const bool tc_ok = !ms && !sc && win.tc >= 2 && win.tc <= 64 && !(win.bad & (1 << KKB_KK_INST_TC)) &&
-                           N * M <= 128;
+        const bool tc_ok = !ms && !sc && win.tc >= 2 && win.tc <= KKB_KK_TC_W && !(win.bad & (1 << KKB_KK_INST_TC)) &&
+                           N * M <= 8192;
         if (want && tc_ok) {
             g_last_instance.store(KKB_KK_INST_TC);
             return kk_gather_tc(data, N, M, T, ltx, ltzT, lrx, lrzT, nx, nz, w, fs, shift, linear, out, out_kind,

@@ -52,6 +52,40 @@ __device__ __forceinline__ void mma_f16(uint32_t d_tmem, uint64_t a, uint64_t b,
         "l"(a), "l"(b), "r"(idesc), "r"((uint32_t)accumulate));
 }
 
+// One K = 32 step of a split-fp16 product, hi*hi + hi*lo + lo*hi over two
+// K = 16 MMAs each (6 MMAs, one asm block): a = A hi descriptor (A lo at
+// +APL bytes, next K half at +AK), b = B hi descriptor (B lo at +BPL, next K
+// half at +BK).  accumulate = false overwrites D with the first product.
+template <int APL, int BPL, int AK, int BK>
+__device__ __forceinline__ void mma_f16_split_pair(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc,
+                                                   bool accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p, q;\n\t.reg .b64 a1, a2, a3, b1, b2, b3;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "setp.eq.b32 q, 0, 0;\n\t"
+        "add.s64 b1, %2, %6;\n\t"
+        "add.s64 a1, %1, %5;\n\t"
+        "add.s64 a2, %1, %7;\n\t"
+        "add.s64 b2, %2, %8;\n\t"
+        "add.s64 a3, a2, %5;\n\t"
+        "add.s64 b3, b2, %6;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, b1, %3, q;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], a1, %2, %3, q;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], a2, b2, %3, q;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], a2, b3, %3, q;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], a3, b2, %3, q;\n\t}\n" ::"r"(d_tmem),
+        "l"(a), "l"(b), "r"(idesc), "r"((uint32_t)accumulate), "n"((long long)(APL >> 4)),
+        "n"((long long)(BPL >> 4)), "n"((long long)(AK >> 4)), "n"((long long)(BK >> 4)));
+}
+
+// one lane of the (converged) warp
+__device__ __forceinline__ bool elect_one() {
+    uint32_t p = 0;
+    asm volatile("{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.b32 %0, 1, 0, P;\n\t}" : "=r"(p));
+    return p != 0;
+}
+
 // Arrive on an mbarrier once every MMA this thread issued so far completes.
 __device__ __forceinline__ void commit(uint64_t *bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
