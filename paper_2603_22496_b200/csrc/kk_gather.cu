@@ -291,6 +291,9 @@ struct KKArgs {
     int nsets;
     int set_m0[KKB_MAX_SETS + 1];
     long long out_set_stride;
+    // when set, the launch is the tensor-core gather's standby: every CTA
+    // returns at once unless *run_if != 0 (kk_gather_tc.cu, non-finite batch)
+    const unsigned *run_if;
 };
 
 // packed LUT index: tile row r -> (r/8)*4 + r%4 pair slot, a = (r/4)&1
@@ -320,6 +323,7 @@ __device__ __forceinline__ void store_iq(void *out, int kind, long long px, floa
 template <int WZ, int WX, int CX, bool LINEAR, int FR, bool MS = false>
 __global__ void __launch_bounds__(WZ *WX * 32, KKB_KK_MIN_CTAS * KKB_KK_WZ * KKB_KK_WX / (WZ * WX))
 k_kk_gather(const KKArgs a) {
+    if (a.run_if && *a.run_if == 0) return;
     constexpr int TZ = 8 * WZ;
     constexpr int TX = 8 * CX * WX;
     constexpr int NT = WZ * WX * 32;
@@ -679,6 +683,7 @@ k_kk_gather(const KKArgs a) {
 template <bool LINEAR, bool MS = false>
 __global__ void __launch_bounds__(256)
 k_kk_direct(const KKArgs a) {
+    if (a.run_if && *a.run_if == 0) return;
     const long long P = (long long)a.nx * a.nz;
     const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     const int f = blockIdx.y;
@@ -866,10 +871,53 @@ k_kk_window_check(const double *__restrict__ ltx, const double *__restrict__ ltz
     }
 }
 
+// Per (tensor-core tile, pair): whether every live tap of the tile's pixels
+// falls in the first 16 samples of the pair's window (window start as in
+// kk_gather_tc.cu: floor(min corner delay) - 1); such pairs take one K = 16
+// MMA step instead of two.  Exact, with the gather's own index arithmetic.
+template <bool LINEAR>
+__global__ void __launch_bounds__(256)
+k_kk_tc_k16(const double *__restrict__ ltx, const double *__restrict__ ltz, const double *__restrict__ lrx,
+            const double *__restrict__ lrz, int N, int M, int T, int nx, int nz, double fs, double shift,
+            unsigned char *__restrict__ k16) {
+    const int TZ = KKB_KK_TC_TZ, TX = KKB_KK_TC_TX;
+    const int tiles_z = (nz + TZ - 1) / TZ;
+    const long long NM = (long long)N * M, total = (long long)tiles_z * ((nx + TX - 1) / TX) * NM;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+         i += (long long)gridDim.x * blockDim.x) {
+        const long long tile = i / NM;
+        const int pr = (int)(i % NM), n = pr / M, m = pr % M;
+        const int iz0 = (int)(tile % tiles_z) * TZ, ix0 = (int)(tile / tiles_z) * TX;
+        const int rzb = min(TZ - 1, nz - 1 - iz0), cxb = min(TX - 1, nx - 1 - ix0);
+        double lo = 1e300;
+        for (int cr = 0; cr < 2; ++cr)
+            for (int cc = 0; cc < 2; ++cc) {
+                const int iz = iz0 + (cr ? rzb : 0), ix = ix0 + (cc ? cxb : 0);
+                const double t1 = __dadd_rn(ltx[(long long)ix * N + n], ltz[(long long)iz * N + n]);
+                lo = fmin(lo, kk_delay(t1, lrz[(long long)iz * M + m], lrx[(long long)ix * M + m], fs, shift));
+            }
+        const int lo_i = (int)fmax(fmin(floor(lo) - 1.0, (double)T), (double)-KKB_KK_TC_W);
+        bool fits = true;
+        for (int c = 0; c <= cxb && fits; ++c)
+            for (int r = 0; r <= rzb; ++r) {
+                const int iz = iz0 + r, ix = ix0 + c;
+                const double t1 = __dadd_rn(ltx[(long long)ix * N + n], ltz[(long long)iz * N + n]);
+                const double fi = kk_delay(t1, lrz[(long long)iz * M + m], lrx[(long long)ix * M + m], fs, shift);
+                const double sv = __dadd_rd(LINEAR ? fi : __dadd_rn(fi, 0.5), KKB_FLOOR_MAGIC2);
+                const int F = __double2hiint(sv) - KKB_MAGIC2_HI;
+                const bool tap = (unsigned)F <= (unsigned)(LINEAR ? T - 2 : T - 1);
+                const int e = F - lo_i;
+                if (tap && (e < 0 || e + (LINEAR ? 1 : 0) > 15)) fits = false;
+            }
+        k16[i] = fits ? 1 : 0;
+    }
+}
+
 int kk_check_windows(const double *ltx, const double *ltz, const double *lrx, const double *lrz,
                      int N, int M, int T, int nx, int nz, double fs, double shift, int linear,
                      KKWindows *win, cudaStream_t s) {
     win->bad = 0;
+    win->tc_k16 = nullptr;
     if ((size_t)M * sizeof(int) > 48 * 1024) return KKB_OK;  // huge pair tables: no tile fits anyway
     int *d = nullptr;
     KKB_TRY_CUDA(cudaMallocAsync(&d, sizeof(int), s), "cudaMallocAsync(window check)");
@@ -901,6 +949,21 @@ int kk_check_windows(const double *ltx, const double *ltz, const double *lrx, co
             k_kk_window_check<false><<<grid, 256, smem, s>>>(ltx, ltz, lrx, lrz, N, M, T, nx, nz, KKB_KK_TC_TX,
                                                              KKB_KK_TC_TZ, win->tc, fs, shift, 1 << KKB_KK_INST_TC, d);
         KKB_CHECK_LAUNCH("k_kk_window_check");
+    }
+    win->tc_k16 = nullptr;
+    if (win->tc >= 2 && win->tc <= KKB_KK_TC_W) {
+        const long long n16 = ceil_div(nz, KKB_KK_TC_TZ) * ceil_div(nx, KKB_KK_TC_TX) * (long long)N * M;
+        if (cudaMalloc(&win->tc_k16, (size_t)n16) == cudaSuccess) {
+            const int blocks = (int)std::min<long long>(ceil_div(n16, 256), 148LL * 16);
+            if (linear)
+                k_kk_tc_k16<true><<<blocks, 256, 0, s>>>(ltx, ltz, lrx, lrz, N, M, T, nx, nz, fs, shift, win->tc_k16);
+            else
+                k_kk_tc_k16<false><<<blocks, 256, 0, s>>>(ltx, ltz, lrx, lrz, N, M, T, nx, nz, fs, shift, win->tc_k16);
+            KKB_CHECK_LAUNCH("k_kk_tc_k16");
+        } else {
+            cudaGetLastError();  // no table: every pair takes two K steps
+            win->tc_k16 = nullptr;
+        }
     }
     int h = 0;
     KKB_TRY_CUDA(cudaMemcpyAsync(&h, d, sizeof(int), cudaMemcpyDeviceToHost, s), "copy window check");
@@ -994,66 +1057,74 @@ int kk_gather(const float2 *data, int N, int M, int T, const double *ltx, const 
         for (int j = 0; j <= sets->nsets; ++j) a.set_m0[j] = sets->m0[j];
         a.out_set_stride = sets->out_set_stride;
     }
-    // tensor-core gather (kk_gather_tc.cu), an experiment measured slower than
-    // the FMA instances (profiles/r02_gather_tc_experiment.json): only when
-    // forced with KKB_KK_INST=tc, for single-set launches without peer
-    // scatter, a proven window of <= 64 samples on its 8 x 16 tile and at most
-    // 128 pairs (the tensor core's accumulator adds truncate: ~3e-8 relative
-    // bias per MMA, scripts/ubench/tc_accum.cu, so longer pair chains would
-    // leave the 1e-5 parity bound)
+    const int inst = select_instance(N, M, nx, nz, n_frames, linear != 0, win);
+    auto launch_fma = [&](KKArgs a) -> int {
+        if (inst == KKB_KK_INST_DIRECT) {
+            // steep geometry or huge pair tables: per-pixel kernel
+            dim3 grid((unsigned)ceil_div((long long)nx * nz, 256), (unsigned)n_frames);
+            if (ms) {
+                if (linear)
+                    k_kk_direct<true, true><<<grid, 256, 0, s>>>(a);
+                else
+                    k_kk_direct<false, true><<<grid, 256, 0, s>>>(a);
+            } else if (linear)
+                k_kk_direct<true><<<grid, 256, 0, s>>>(a);
+            else
+                k_kk_direct<false><<<grid, 256, 0, s>>>(a);
+            KKB_CHECK_LAUNCH("k_kk_direct");
+            return KKB_OK;
+        }
+        const InstanceShape sh = instance_shape(inst, win);
+        const int FR = inst == KKB_KK_INST_BIG_FR ? KKB_KK_FR : 1;
+        // receive angles per stage: bounded by the register staging and shared memory
+        int MCH = std::max(1, std::min(M, sh.stage / (FR * sh.W)));
+        while (MCH > 1 && kk_smem_bytes(N, M, sh.W, MCH, linear, sh.tz, sh.tx, FR) > 200 * 1024) MCH = (MCH + 1) / 2;
+        if (const char *fm = getenv("KKB_KK_MCH"))  // test hook: fewer receive angles per stage
+            MCH = std::max(1, std::min(MCH, atoi(fm)));
+        const size_t sm = kk_smem_bytes(N, M, sh.W, MCH, linear, sh.tz, sh.tx, FR);
+        a.W = sh.W;
+        a.MCH = MCH;
+        const bool lin = linear != 0;
+        switch (inst) {
+            case KKB_KK_INST_SMALL:
+                return ms ? launch_tiled<KKB_KK_S_WZ, KKB_KK_S_WX, KKB_KK_S_CX, 1, true>(a, n_frames, sm, lin, s)
+                          : launch_tiled<KKB_KK_S_WZ, KKB_KK_S_WX, KKB_KK_S_CX, 1>(a, n_frames, sm, lin, s);
+            case KKB_KK_INST_MID:
+                return ms ? launch_tiled<KKB_KK_M_WZ, KKB_KK_M_WX, KKB_KK_M_CX, 1, true>(a, n_frames, sm, lin, s)
+                          : launch_tiled<KKB_KK_M_WZ, KKB_KK_M_WX, KKB_KK_M_CX, 1>(a, n_frames, sm, lin, s);
+            case KKB_KK_INST_BIG_FR:
+                return ms ? launch_tiled<KKB_KK_WZ, KKB_KK_WX, KKB_KK_CX, KKB_KK_FR, true>(a, n_frames, sm, lin, s)
+                          : launch_tiled<KKB_KK_WZ, KKB_KK_WX, KKB_KK_CX, KKB_KK_FR>(a, n_frames, sm, lin, s);
+            default:
+                return ms ? launch_tiled<KKB_KK_WZ, KKB_KK_WX, KKB_KK_CX, 1, true>(a, n_frames, sm, lin, s)
+                          : launch_tiled<KKB_KK_WZ, KKB_KK_WX, KKB_KK_CX, 1>(a, n_frames, sm, lin, s);
+        }
+    };
+    // tensor-core gather (kk_gather_tc.cu): single-set launches without peer
+    // scatter whose 4 x 32 tile has a proven window of <= KKB_KK_TC_W samples.
+    // The FMA instance is launched behind it as a standby that only runs when
+    // the batch holds a NaN / Inf sample (the reference propagates those per
+    // tap; a tensor-core product would spread them over the window).
     {
         const char *fi = getenv("KKB_KK_INST");
         const bool want = fi && !strcmp(fi, "tc");
-        const bool tc_ok = !ms && !sc && win.tc >= 2 && win.tc <= KKB_KK_TC_W && !(win.bad & (1 << KKB_KK_INST_TC)) &&
-                           N * M <= 8192;
+        const bool tc_ok = !ms && !sc && win.tc >= 2 && win.tc <= KKB_KK_TC_W && !(win.bad & (1 << KKB_KK_INST_TC));
         if (want && tc_ok) {
-            g_last_instance.store(KKB_KK_INST_TC);
-            return kk_gather_tc(data, N, M, T, ltx, ltzT, lrx, lrzT, nx, nz, w, fs, shift, linear, out, out_kind,
-                                n_frames, data_fs, out_fs, inten, fmax, win.tc, accum, s);
+            const int rc = kk_gather_tc(data, N, M, T, ltx, ltzT, lrx, lrzT, nx, nz, w, fs, shift, linear, out,
+                                        out_kind, n_frames, data_fs, out_fs, inten, fmax, win.tc, win.tc_k16, accum, s,
+                                        [&](const unsigned *run_if) {
+                                            KKArgs b = a;
+                                            b.run_if = run_if;
+                                            return launch_fma(b);
+                                        });
+            if (rc != KKB_ERR_UNSUPPORTED) {
+                g_last_instance.store(KKB_KK_INST_TC);
+                return rc;
+            }
         }
     }
-    const int inst = select_instance(N, M, nx, nz, n_frames, linear != 0, win);
     g_last_instance.store(inst | (ms ? KKB_KK_INST_SETS : 0));
-    if (inst == KKB_KK_INST_DIRECT) {
-        // steep geometry or huge pair tables: per-pixel kernel
-        dim3 grid((unsigned)ceil_div((long long)nx * nz, 256), (unsigned)n_frames);
-        if (ms) {
-            if (linear)
-                k_kk_direct<true, true><<<grid, 256, 0, s>>>(a);
-            else
-                k_kk_direct<false, true><<<grid, 256, 0, s>>>(a);
-        } else if (linear)
-            k_kk_direct<true><<<grid, 256, 0, s>>>(a);
-        else
-            k_kk_direct<false><<<grid, 256, 0, s>>>(a);
-        KKB_CHECK_LAUNCH("k_kk_direct");
-        return KKB_OK;
-    }
-    const InstanceShape sh = instance_shape(inst, win);
-    const int FR = inst == KKB_KK_INST_BIG_FR ? KKB_KK_FR : 1;
-    // receive angles per stage: bounded by the register staging and shared memory
-    int MCH = std::max(1, std::min(M, sh.stage / (FR * sh.W)));
-    while (MCH > 1 && kk_smem_bytes(N, M, sh.W, MCH, linear, sh.tz, sh.tx, FR) > 200 * 1024) MCH = (MCH + 1) / 2;
-    if (const char *fm = getenv("KKB_KK_MCH"))  // test hook: fewer receive angles per stage
-        MCH = std::max(1, std::min(MCH, atoi(fm)));
-    const size_t sm = kk_smem_bytes(N, M, sh.W, MCH, linear, sh.tz, sh.tx, FR);
-    a.W = sh.W;
-    a.MCH = MCH;
-    const bool lin = linear != 0;
-    switch (inst) {
-        case KKB_KK_INST_SMALL:
-            return ms ? launch_tiled<KKB_KK_S_WZ, KKB_KK_S_WX, KKB_KK_S_CX, 1, true>(a, n_frames, sm, lin, s)
-                      : launch_tiled<KKB_KK_S_WZ, KKB_KK_S_WX, KKB_KK_S_CX, 1>(a, n_frames, sm, lin, s);
-        case KKB_KK_INST_MID:
-            return ms ? launch_tiled<KKB_KK_M_WZ, KKB_KK_M_WX, KKB_KK_M_CX, 1, true>(a, n_frames, sm, lin, s)
-                      : launch_tiled<KKB_KK_M_WZ, KKB_KK_M_WX, KKB_KK_M_CX, 1>(a, n_frames, sm, lin, s);
-        case KKB_KK_INST_BIG_FR:
-            return ms ? launch_tiled<KKB_KK_WZ, KKB_KK_WX, KKB_KK_CX, KKB_KK_FR, true>(a, n_frames, sm, lin, s)
-                      : launch_tiled<KKB_KK_WZ, KKB_KK_WX, KKB_KK_CX, KKB_KK_FR>(a, n_frames, sm, lin, s);
-        default:
-            return ms ? launch_tiled<KKB_KK_WZ, KKB_KK_WX, KKB_KK_CX, 1, true>(a, n_frames, sm, lin, s)
-                      : launch_tiled<KKB_KK_WZ, KKB_KK_WX, KKB_KK_CX, 1>(a, n_frames, sm, lin, s);
-    }
+    return launch_fma(a);
 }
 
 // ------------------------------------------------------------- K6 epilogues

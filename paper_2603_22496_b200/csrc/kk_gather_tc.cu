@@ -56,29 +56,49 @@ __device__ __forceinline__ double tc_kk_delay(double t1, double lz, double lx, d
 #define TCG_MAGIC2 1572864.0   // 1.5 * 2^20 (kk_gather.cu KKB_FLOOR_MAGIC2)
 #define TCG_MAGIC2_HI 0x41380000
 #define TCG_WSCALE 4096.0f     // weights x 2^12: their fp16 low halves stay normal
-#define TCG_TZ 8
-#define TCG_TX 16
+#define TCG_TZ KKB_KK_TC_TZ
+#define TCG_TX KKB_KK_TC_TX
 #define TCG_KW KKB_KK_TC_W     // window samples per pair (two K steps)
 #define TCG_FB 64              // frames per CTA: N = 128 (re | im)
 #define TCG_NA 4               // weight (A) stages
-#define TCG_NB 8               // trace-window (B) stages: deeper, they hide the TMA latency
-#define TCG_PB 2               // pairs per producer iteration (divides TCG_NA)
+#define TCG_NB 8               // trace-window (B) stages (they hide the TMA latency)
+#define TCG_PB 2               // pairs per producer iteration
 #define TCG_GROUP 8            // pairs per accumulator group
-#define TCG_THREADS 320
+#define TCG_ND 4               // TMEM accumulators (128 columns each)
+#define TCG_THREADS 352        // 11 warps
 
-// per-frame max |re|, |im| of the traces (float bits; atomicMax on non-negative floats)
-__global__ void k_frame_maxabs(const float2 *__restrict__ data, long long data_fs, long long per_frame,
-                               unsigned *__restrict__ out) {
+// per-frame max |re|, |im| of the traces (float bits; atomicMax on
+// non-negative floats).  V complex samples per load (2: 16-byte loads, when
+// the frame stride and length are even and the base 16-byte aligned).
+template <int V>
+__global__ void __launch_bounds__(256) k_frame_maxabs(const float2 *__restrict__ data, long long data_fs,
+                                                      long long per_frame, unsigned *__restrict__ out,
+                                                      unsigned *__restrict__ nonfinite) {
     const int f = blockIdx.y;
     const float2 *d = data + (long long)f * data_fs;
-    float m = 0.f;
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < per_frame;
-         i += (long long)gridDim.x * blockDim.x) {
-        const float2 v = __ldg(d + i);
-        m = fmaxf(m, fmaxf(fabsf(v.x), fabsf(v.y)));
+    // max of the magnitude bits: finite < Inf (0x7f800000) < NaN
+    unsigned m = 0;
+    const long long nv = per_frame / V;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nv; i += (long long)gridDim.x * blockDim.x) {
+        if (V == 2) {
+            const float4 v = __ldg(reinterpret_cast<const float4 *>(d) + i);
+            m = max(max(m, max(__float_as_uint(v.x) & 0x7fffffffu, __float_as_uint(v.y) & 0x7fffffffu)),
+                    max(__float_as_uint(v.z) & 0x7fffffffu, __float_as_uint(v.w) & 0x7fffffffu));
+        } else {
+            const float2 v = __ldg(d + i);
+            m = max(m, max(__float_as_uint(v.x) & 0x7fffffffu, __float_as_uint(v.y) & 0x7fffffffu));
+        }
     }
-    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if ((threadIdx.x & 31) == 0 && m > 0.f) atomicMax(out + f, __float_as_uint(m));
+    const unsigned mx = __reduce_max_sync(0xffffffffu, m);
+    __shared__ unsigned wm[8];
+    if ((threadIdx.x & 31) == 0) wm[threadIdx.x >> 5] = mx;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned r = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) r = max(r, wm[w]);
+        if (r >= 0x7f800000u) atomicOr(nonfinite, 1u);
+        else if (r) atomicMax(out + f, r);
+    }
 }
 
 __device__ __forceinline__ float frame_scale(unsigned maxbits) {
@@ -98,40 +118,64 @@ __device__ __forceinline__ void split_h(float x, __half &hi, __half &lo) {
     lo = __float2half_rn(x - __half2float(hi));
 }
 
-// planes[pl][g][q][t][8]: pl = re_hi, im_hi, re_lo, im_lo; frames 8g..8g+7
-__global__ void k_split_planes(const float2 *__restrict__ data, long long data_fs, int n_frames, int NM, int T,
-                               const unsigned *__restrict__ maxabs, long long ngroups, __half *__restrict__ planes) {
+// planes[pl][g][q][t][8]: pl = re_hi, im_hi, re_lo, im_lo; frames 8g..8g+7.
+// A thread owns V consecutive samples of one (g, q) row: 8 frame loads of
+// V complex each, 4 planes x V 16-byte stores.
+template <int V>
+__global__ void __launch_bounds__(256) k_split_planes(const float2 *__restrict__ data, long long data_fs,
+                                                      int n_frames, int NM, int T,
+                                                      const unsigned *__restrict__ maxabs, long long ngroups,
+                                                      __half *__restrict__ planes) {
     const long long per_plane = ngroups * NM * (long long)T * 8;
-    const long long total = ngroups * NM * (long long)T;
+    const int TV = T / V;
+    const long long total = ngroups * NM * (long long)TV;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
          i += (long long)gridDim.x * blockDim.x) {
-        const int t = (int)(i % T);
-        const long long gq = i / T;
+        const int tv = (int)(i % TV);
+        const long long gq = i / TV;
         const int q = (int)(gq % NM);
         const long long g = gq / NM;
-        __half h[4][8];
+        float2 v[8][V];
+        float sc[8];
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
             const long long f = g * 8 + j;
-            float2 v = make_float2(0.f, 0.f);
-            float sc = 1.0f;
-            if (f < n_frames) {
-                v = __ldg(data + f * data_fs + (long long)q * T + t);
-                sc = frame_scale(maxabs[f]);
-            }
-            split_h(v.x * sc, h[0][j], h[2][j]);
-            split_h(v.y * sc, h[1][j], h[3][j]);
-        }
+            sc[j] = 1.0f;
 #pragma unroll
-        for (int pl = 0; pl < 4; ++pl)
-            reinterpret_cast<uint4 *>(planes + pl * per_plane)[i] =
-                make_uint4(pack_h2(h[pl][0], h[pl][1]), pack_h2(h[pl][2], h[pl][3]), pack_h2(h[pl][4], h[pl][5]),
-                           pack_h2(h[pl][6], h[pl][7]));
+            for (int u = 0; u < V; ++u) v[j][u] = make_float2(0.f, 0.f);
+            if (f < n_frames) {
+                const float2 *src = data + f * data_fs + (long long)q * T + (long long)tv * V;
+                if (V == 2) {
+                    const float4 x = __ldg(reinterpret_cast<const float4 *>(src));
+                    v[j][0] = make_float2(x.x, x.y);
+                    v[j][V - 1] = make_float2(x.z, x.w);
+                } else {
+                    v[j][0] = __ldg(src);
+                }
+                sc[j] = frame_scale(__ldg(maxabs + f));
+            }
+        }
+        uint4 *dst = reinterpret_cast<uint4 *>(planes) + gq * T + (long long)tv * V;
+#pragma unroll
+        for (int u = 0; u < V; ++u) {
+            __half h[4][8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                split_h(v[j][u].x * sc[j], h[0][j], h[2][j]);
+                split_h(v[j][u].y * sc[j], h[1][j], h[3][j]);
+            }
+#pragma unroll
+            for (int pl = 0; pl < 4; ++pl)
+                dst[pl * (per_plane / 8) + u] = make_uint4(pack_h2(h[pl][0], h[pl][1]), pack_h2(h[pl][2], h[pl][3]),
+                                                           pack_h2(h[pl][4], h[pl][5]), pack_h2(h[pl][6], h[pl][7]));
+        }
     }
 }
 
 struct TcgArgs {
-    CUtensorMap planes;      // 4-D map of the split trace planes (64-byte aligned)
+    CUtensorMap planes;      // 4-D map of the split trace planes: 32-sample windows
+    CUtensorMap planes16;    // the same planes, 16-sample windows (one K step)
+    const unsigned char *k16;  // [tile][pair] 1: the pair's taps fit 16 samples (or null)
     int N, M, T;
     const double *ltx, *ltzT, *lrx, *lrzT, *w;
     double fs, shift;
@@ -143,7 +187,10 @@ struct TcgArgs {
     unsigned *fmax;
     int accum;
     int n_frames;
-    const unsigned *maxabs;
+    const unsigned *maxabs;     // per-frame max |sample| (float bits)
+    const unsigned *nonfinite;  // != 0: a NaN / Inf sample; the FMA gather runs instead
+    int tiles_z;                // pixel tiles along depth
+    long long tiles, items;     // work item = frame block * tiles + pixel tile
 };
 
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
@@ -164,6 +211,31 @@ __device__ __forceinline__ void tma_4d(void *dst, const CUtensorMap *map, int c0
         : "memory");
 }
 
+// per-slot delay tables of one pixel tile: [ltx N][TX] [ltz N][TZ] [lrx M][TX]
+// [lrz M][TZ] (fp64) then the window starts lo [N*M] (int)
+struct TcgTables {
+    double *ltx, *ltz, *lrx, *lrz;
+    int *lo;
+};
+__device__ __forceinline__ TcgTables tcg_tables(unsigned char *base, int N, int M) {
+    TcgTables t;
+    t.ltx = reinterpret_cast<double *>(base);
+    t.ltz = t.ltx + N * TCG_TX;
+    t.lrx = t.ltz + N * TCG_TZ;
+    t.lrz = t.lrx + M * TCG_TX;
+    t.lo = reinterpret_cast<int *>(t.lrz + M * TCG_TZ);
+    return t;
+}
+__host__ __device__ __forceinline__ size_t tcg_slot_bytes(int N, int M) {
+    return ((sizeof(double) * (size_t)(N + M) * (TCG_TX + TCG_TZ) + sizeof(int) * (size_t)N * M) + 15) & ~(size_t)15;
+}
+
+// Persistent: one CTA per SM walks work items (64-frame block, pixel tile)
+// strided by the grid.  The rings, the accumulator
+// sequence and the table slots run across items, so the drains' epilogue of
+// one item overlaps the next item's MMAs (four TMEM accumulators give the
+// MMA three groups of slack) and a table builder warp prepares the next
+// item's tile tables while the current item runs.
 template <bool LINEAR>
 __global__ void __launch_bounds__(TCG_THREADS, 1)
 k_kk_gather_tc(const __grid_constant__ TcgArgs a) {
@@ -172,28 +244,31 @@ k_kk_gather_tc(const __grid_constant__ TcgArgs a) {
     constexpr int B_PLANE = 16 * TCG_KW * 16;       // 8 KB: one split half of the traces (MN-major, 16 col groups)
     constexpr int ASTAGE = 2 * A_PLANE, BSTAGE = 2 * B_PLANE;
     extern __shared__ __align__(1024) unsigned char sm[];
-    __shared__ uint64_t a_full[TCG_NA], a_empty[TCG_NA], b_full[TCG_NB], b_empty[TCG_NB], dfull[2], dfree[2];
+    __shared__ uint64_t a_full[TCG_NA], a_empty[TCG_NA], b_full[TCG_NB], b_empty[TCG_NB];
+    __shared__ uint64_t dfull[TCG_ND], dfree[TCG_ND], tab_full[2], tab_empty[2];
     __shared__ uint32_t tmem_base;
-    __shared__ float fscale[TCG_FB];
-    // delay tables of the tile (fp64) and the window starts, after the stages
-    double *ltx_s = reinterpret_cast<double *>(sm + TCG_NA * ASTAGE + TCG_NB * BSTAGE);  // [N][TX]
-    double *ltz_s = ltx_s + a.N * TCG_TX;                                  // [N][TZ]
-    double *lrx_s = ltz_s + a.N * TCG_TZ;                                  // [M][TX]
-    double *lrz_s = lrx_s + a.M * TCG_TX;                                  // [M][TZ]
-    float *w_s = reinterpret_cast<float *>(lrz_s + a.M * TCG_TZ);        // [M] weights x 2^12
-    int *lo_s = reinterpret_cast<int *>(w_s + a.M);                       // [N*M]
+    __shared__ int b_k16[TCG_NB];  // per B stage: 1 = a 16-sample window (one K step)
+
+    // a batch with a non-finite sample goes to the FMA gather (NaN x 0 would
+    // spread it over the whole window); uniform, before any barrier
+    if (*a.nonfinite) return;
 
     const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
     const int N = a.N, M = a.M, T = a.T, nx = a.nx, nz = a.nz;
-    const int tiles_z = (nz + TCG_TZ - 1) / TCG_TZ;
-    const int iz0 = (blockIdx.x % tiles_z) * TCG_TZ, ix0 = (blockIdx.x / tiles_z) * TCG_TX;
-    const int f0 = blockIdx.y * TCG_FB;
-    const int FB = min(TCG_FB, a.n_frames - f0);
     const double fs = a.fs, shift = a.shift;
     const int npairs = N * M;
     const int ngroups = (npairs + TCG_GROUP - 1) / TCG_GROUP;
+    unsigned char *tab_base = sm + TCG_NA * ASTAGE + TCG_NB * BSTAGE;
+    const size_t slot_bytes = tcg_slot_bytes(N, M);
+    float *w_s = reinterpret_cast<float *>(tab_base + 2 * slot_bytes);  // [M] weights x 2^12
+    // this CTA's items: blockIdx.x + k * gridDim.x.  Items run frame block
+    // major, so the CTAs in flight share one frame block's trace planes in L2
+    const int nit = (int)((a.items - blockIdx.x + gridDim.x - 1) / gridDim.x);
+    auto item_of = [&](int k) { return (long long)blockIdx.x + (long long)k * gridDim.x; };
+    auto tile_of = [&](int k) { return (int)(item_of(k) % a.tiles); };
+    auto fb_of = [&](int k) { return (int)(item_of(k) / a.tiles); };
 
-    if (warp == 4) tc::tmem_alloc<256>(&tmem_base);
+    if (warp == 4) tc::tmem_alloc<32 * 4 * TCG_ND>(&tmem_base);
     if (t == 0) {
         for (int s = 0; s < TCG_NA; ++s) {
             tc::mbar_init(&a_full[s], 128);  // the 128 weight rows
@@ -203,49 +278,19 @@ k_kk_gather_tc(const __grid_constant__ TcgArgs a) {
             tc::mbar_init(&b_full[s], 1);    // the TMA issuer (expect_tx)
             tc::mbar_init(&b_empty[s], 1);
         }
-        for (int d = 0; d < 2; ++d) {
+        for (int d = 0; d < TCG_ND; ++d) {
             tc::mbar_init(&dfull[d], 1);
             tc::mbar_init(&dfree[d], 128);
         }
+        for (int s = 0; s < 2; ++s) {
+            tc::mbar_init(&tab_full[s], 32);       // the builder warp
+            tc::mbar_init(&tab_empty[s], 128 + 1); // weight rows + TMA issuer
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    if (t < TCG_FB) fscale[t] = t < FB ? frame_scale(a.maxabs[f0 + t]) : 1.0f;
-    if (t == 0) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&a.planes)) : "memory");
-    // tile tables (edge tiles repeat the last row / column)
-    for (int i = t; i < N * TCG_TX; i += blockDim.x) {
-        const int n = i / TCG_TX, c = i - n * TCG_TX;
-        ltx_s[i] = __ldg(a.ltx + (long long)min(ix0 + c, nx - 1) * N + n);
-    }
-    for (int i = t; i < N * TCG_TZ; i += blockDim.x) {
-        const int n = i / TCG_TZ, r = i - n * TCG_TZ;
-        ltz_s[i] = __ldg(a.ltzT + (long long)n * nz + min(iz0 + r, nz - 1));
-    }
-    for (int i = t; i < M * TCG_TX; i += blockDim.x) {
-        const int m = i / TCG_TX, c = i - m * TCG_TX;
-        lrx_s[i] = __ldg(a.lrx + (long long)min(ix0 + c, nx - 1) * M + m);
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&a.planes)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&a.planes16)) : "memory");
     }
     for (int i = t; i < M; i += blockDim.x) w_s[i] = (a.w ? (float)__ldg(a.w + i) : 1.0f) * TCG_WSCALE;
-    for (int i = t; i < M * TCG_TZ; i += blockDim.x) {
-        const int m = i / TCG_TZ, r = i - m * TCG_TZ;
-        lrz_s[i] = __ldg(a.lrzT + (long long)m * nz + min(iz0 + r, nz - 1));
-    }
-    __syncthreads();
-    {
-        const int rzb = min(TCG_TZ - 1, nz - 1 - iz0), cxb = min(TCG_TX - 1, nx - 1 - ix0);
-        for (int i = t; i < npairs; i += blockDim.x) {
-            const int n = i / M, m = i - n * M;
-            double lo = 1e300;
-            for (int cr = 0; cr < 2; ++cr)
-                for (int cc = 0; cc < 2; ++cc) {
-                    const int r = cr ? rzb : 0, c = cc ? cxb : 0;
-                    const double t1 = __dadd_rn(ltx_s[n * TCG_TX + c], ltz_s[n * TCG_TZ + r]);
-                    lo = fmin(lo, tc_kk_delay(t1, lrz_s[m * TCG_TZ + r], lrx_s[m * TCG_TX + c], fs, shift));
-                }
-            // a live window (plan proof: lo in (-W, T - 1)) is never clamped; a
-            // dead one (every tap rejected) is zero-filled by the TMA unit
-            lo_s[i] = (int)fmax(fmin(floor(lo) - 1.0, (double)T), (double)-TCG_KW);
-        }
-    }
     tc::fence_before_sync();
     __syncthreads();
     tc::fence_after_sync();
@@ -254,9 +299,9 @@ k_kk_gather_tc(const __grid_constant__ TcgArgs a) {
     if (warp < 4) {
         // ------------------------------------------------------------ weight rows
         // A row holds two nonzero halves (w0 at window sample e, w1 at e + 1)
-        // in 32: the stage's A planes are zeroed once, then each pair writes
-        // the two 32-bit words that carry them and clears the words it wrote
-        // in the same stage one round earlier (4 x STS.32 per plane).
+        // in 32: the A ring is zeroed once, then each pair writes the two
+        // 32-bit words that carry them and clears the words it wrote in the
+        // same stage one round earlier (4 x STS.32 per plane).
         const int r = t, cl = r / TCG_TZ, rl = r % TCG_TZ;
         unsigned char *row = sm + r * 16;
 #pragma unroll
@@ -267,85 +312,107 @@ k_kk_gather_tc(const __grid_constant__ TcgArgs a) {
         // byte offset of 32-bit word k (half pair 2k, 2k + 1) of the row
         auto word = [](int k) { return (k >> 2) * (128 * 16) + (k & 3) * 4; };
         uint32_t prevk = 0;  // per stage (4 bits each): first word written last round
-        int n = 0, m = 0;
-        // TCG_PB pairs per iteration: independent delay chains in flight and one
-        // proxy fence per batch
-        for (int pr0 = 0; pr0 < npairs; pr0 += TCG_PB) {
-            uint32_t hA[TCG_PB], hB[TCG_PB], lA[TCG_PB], lB[TCG_PB];
-            int kA[TCG_PB];
+        unsigned P = 0;      // pairs issued so far (the rings' sequence)
+        for (int k = 0; k < nit; ++k) {
+            const int slot = k & 1;
+            tc::mbar_wait(&tab_full[slot], (k >> 1) & 1);
+            const TcgTables tb = tcg_tables(tab_base + slot * slot_bytes, N, M);
+            int n = 0, m = 0;
+            // TCG_PB pairs per iteration: independent delay chains in flight
+            // and one proxy fence per batch
+            for (int pr0 = 0; pr0 < npairs; pr0 += TCG_PB) {
+                uint32_t hA[TCG_PB], hB[TCG_PB], lA[TCG_PB], lB[TCG_PB];
+                int kA[TCG_PB];
 #pragma unroll
-            for (int j = 0; j < TCG_PB; ++j) {
-                const int pr = min(pr0 + j, npairs - 1);
-                const double t1 = __dadd_rn(ltx_s[n * TCG_TX + cl], ltz_s[n * TCG_TZ + rl]);
-                const double fi = tc_kk_delay(t1, lrz_s[m * TCG_TZ + rl], lrx_s[m * TCG_TX + cl], fs, shift);
-                const float wm = w_s[m];
-                const int lo = lo_s[pr];
-                const double sv = __dadd_rd(LINEAR ? fi : __dadd_rn(fi, 0.5), TCG_MAGIC2);
-                const int F = __double2hiint(sv) - TCG_MAGIC2_HI;
-                const int e = F - lo;
-                // the reference's in-window rule; (e < 32) holds for every live
-                // window by the plan-time proof and only guards the stores
-                const bool ok = (unsigned)F <= (unsigned)(LINEAR ? T - 2 : T - 1) && (unsigned)e < TCG_KW;
-                float w0, w1 = 0.f;
-                if (LINEAR) {
-                    const float fr = __uint_as_float(((unsigned)__double2loint(sv) >> 9) | 0x3F800000u) - 1.0f;
-                    w0 = wm * (1.0f - fr);
-                    w1 = wm * fr;
-                } else {
-                    w0 = wm;
+                for (int j = 0; j < TCG_PB; ++j) {
+                    const int pr = min(pr0 + j, npairs - 1);
+                    const double t1 = __dadd_rn(tb.ltx[n * TCG_TX + cl], tb.ltz[n * TCG_TZ + rl]);
+                    const double fi = tc_kk_delay(t1, tb.lrz[m * TCG_TZ + rl], tb.lrx[m * TCG_TX + cl], fs, shift);
+                    const float wm = w_s[m];
+                    const int lo = tb.lo[pr] >> 1;  // bit 0: the one-K-step flag
+                    const double sv = __dadd_rd(LINEAR ? fi : __dadd_rn(fi, 0.5), TCG_MAGIC2);
+                    const int F = __double2hiint(sv) - TCG_MAGIC2_HI;
+                    const int e = F - lo;
+                    // the reference's in-window rule; (e < 32) holds for every live
+                    // window by the plan-time proof and only guards the stores
+                    const bool ok = (unsigned)F <= (unsigned)(LINEAR ? T - 2 : T - 1) && (unsigned)e < TCG_KW;
+                    float w0, w1 = 0.f;
+                    if (LINEAR) {
+                        const float fr = __uint_as_float(((unsigned)__double2loint(sv) >> 9) | 0x3F800000u) - 1.0f;
+                        w0 = wm * (1.0f - fr);
+                        w1 = wm * fr;
+                    } else {
+                        w0 = wm;
+                    }
+                    if (!ok) w0 = w1 = 0.f;
+                    __half h0, l0, h1, l1;
+                    split_h(w0, h0, l0);
+                    split_h(w1, h1, l1);
+                    const bool odd = e & 1;
+                    hA[j] = odd ? (uint32_t)__half_as_ushort(h0) << 16 : pack_h2(h0, h1);
+                    hB[j] = odd ? (uint32_t)__half_as_ushort(h1) : 0u;
+                    lA[j] = odd ? (uint32_t)__half_as_ushort(l0) << 16 : pack_h2(l0, l1);
+                    lB[j] = odd ? (uint32_t)__half_as_ushort(l1) : 0u;
+                    kA[j] = ok ? e >> 1 : 0;
+                    if (++m == M) {
+                        m = 0;
+                        ++n;
+                    }
                 }
-                if (!ok) w0 = w1 = 0.f;
-                __half h0, l0, h1, l1;
-                split_h(w0, h0, l0);
-                split_h(w1, h1, l1);
-                const bool odd = e & 1;
-                hA[j] = odd ? (uint32_t)__half_as_ushort(h0) << 16 : pack_h2(h0, h1);
-                hB[j] = odd ? (uint32_t)__half_as_ushort(h1) : 0u;
-                lA[j] = odd ? (uint32_t)__half_as_ushort(l0) << 16 : pack_h2(l0, l1);
-                lB[j] = odd ? (uint32_t)__half_as_ushort(l1) : 0u;
-                kA[j] = ok ? e >> 1 : 0;
-                if (++m == M) {
-                    m = 0;
-                    ++n;
+                const int nb = min(TCG_PB, npairs - pr0);
+#pragma unroll
+                for (int j = 0; j < TCG_PB; ++j) {
+                    if (j >= nb) break;
+                    const unsigned pp = P + j;
+                    const int st = (int)(pp % TCG_NA);
+                    const unsigned use = pp / TCG_NA;
+                    unsigned char *Ab = row + st * ASTAGE;
+                    if (use > 0) {
+                        tc::mbar_wait(&a_empty[st], (uint32_t)((use - 1) & 1));
+                        const int qA = (prevk >> (4 * st)) & 15, qB = qA == 15 ? 14 : qA + 1;
+                        *reinterpret_cast<uint32_t *>(Ab + word(qA)) = 0u;
+                        *reinterpret_cast<uint32_t *>(Ab + word(qB)) = 0u;
+                        *reinterpret_cast<uint32_t *>(Ab + A_PLANE + word(qA)) = 0u;
+                        *reinterpret_cast<uint32_t *>(Ab + A_PLANE + word(qB)) = 0u;
+                    }
+                    // kA == 15 (e >= 30) leaves hB / lB zero: their store to word 14 is a no-op
+                    const int kB = kA[j] == 15 ? 14 : kA[j] + 1;
+                    *reinterpret_cast<uint32_t *>(Ab + word(kB)) = hB[j];
+                    *reinterpret_cast<uint32_t *>(Ab + word(kA[j])) = hA[j];
+                    *reinterpret_cast<uint32_t *>(Ab + A_PLANE + word(kB)) = lB[j];
+                    *reinterpret_cast<uint32_t *>(Ab + A_PLANE + word(kA[j])) = lA[j];
+                    prevk = (prevk & ~(15u << (4 * st))) | ((uint32_t)kA[j] << (4 * st));
                 }
+                tc::fence_smem_to_async();
+#pragma unroll
+                for (int j = 0; j < TCG_PB; ++j)
+                    if (j < nb) mbar_arrive(&a_full[(int)((P + j) % TCG_NA)]);
+                P += nb;
             }
-#pragma unroll
-            for (int j = 0; j < TCG_PB; ++j) {
-                const int pr = pr0 + j;
-                if (pr >= npairs) break;
-                const int st = pr % TCG_NA, use = pr / TCG_NA;
-                unsigned char *Ab = row + st * ASTAGE;
-                if (use > 0) {
-                    tc::mbar_wait(&a_empty[st], (use - 1) & 1);
-                    const int qA = (prevk >> (4 * st)) & 15, qB = qA == 15 ? 14 : qA + 1;
-                    *reinterpret_cast<uint32_t *>(Ab + word(qA)) = 0u;
-                    *reinterpret_cast<uint32_t *>(Ab + word(qB)) = 0u;
-                    *reinterpret_cast<uint32_t *>(Ab + A_PLANE + word(qA)) = 0u;
-                    *reinterpret_cast<uint32_t *>(Ab + A_PLANE + word(qB)) = 0u;
-                }
-                // kA == 15 (e >= 30) leaves hB / lB zero: their store to word 14 is a no-op
-                const int kB = kA[j] == 15 ? 14 : kA[j] + 1;
-                *reinterpret_cast<uint32_t *>(Ab + word(kB)) = hB[j];
-                *reinterpret_cast<uint32_t *>(Ab + word(kA[j])) = hA[j];
-                *reinterpret_cast<uint32_t *>(Ab + A_PLANE + word(kB)) = lB[j];
-                *reinterpret_cast<uint32_t *>(Ab + A_PLANE + word(kA[j])) = lA[j];
-                prevk = (prevk & ~(15u << (4 * st))) | ((uint32_t)kA[j] << (4 * st));
-            }
-            tc::fence_smem_to_async();
-#pragma unroll
-            for (int j = 0; j < TCG_PB; ++j)
-                if (pr0 + j < npairs) mbar_arrive(&a_full[(pr0 + j) % TCG_NA]);
+            mbar_arrive(&tab_empty[slot]);  // this item's tables read
         }
     } else if (warp == 4) {
         // ------------------------------------------------------------ trace windows (TMA)
-        // box [plane 4][group 8][sample 32][frame 8] = B hi (re groups | im
-        // groups) then B lo: column group = im * 8 + g, 512 B apart
+        // box [plane 4][group 8][sample 32 (or 16)][frame 8] = B hi (re
+        // groups | im groups) then B lo: column group = im * 8 + g, 512 (256) B apart
         if (lane == 0) {
-            for (int pr = 0; pr < npairs; ++pr) {
-                const int st = pr % TCG_NB, use = pr / TCG_NB;
-                if (use > 0) tc::mbar_wait(&b_empty[st], (use - 1) & 1);
-                mbar_arrive_tx(&b_full[st], BSTAGE);
-                tma_4d(sm + TCG_NA * ASTAGE + st * BSTAGE, &a.planes, 8 * lo_s[pr], pr, f0 / 8, 0, &b_full[st]);
+            unsigned P = 0;
+            for (int k = 0; k < nit; ++k) {
+                const int slot = k & 1;
+                tc::mbar_wait(&tab_full[slot], (k >> 1) & 1);
+                const int *lo = tcg_tables(tab_base + slot * slot_bytes, N, M).lo;
+                const int g0 = fb_of(k) * (TCG_FB / 8);
+                for (int pr = 0; pr < npairs; ++pr, ++P) {
+                    const int st = (int)(P % TCG_NB);
+                    const unsigned use = P / TCG_NB;
+                    if (use > 0) tc::mbar_wait(&b_empty[st], (uint32_t)((use - 1) & 1));
+                    const int v = lo[pr], one = v & 1;
+                    b_k16[st] = one;  // published to the MMA warp by the arrive below
+                    mbar_arrive_tx(&b_full[st], one ? BSTAGE / 2 : BSTAGE);
+                    tma_4d(sm + TCG_NA * ASTAGE + st * BSTAGE, one ? &a.planes16 : &a.planes, 8 * (v >> 1), pr, g0, 0,
+                           &b_full[st]);
+                }
+                mbar_arrive(&tab_empty[slot]);
             }
         }
     } else if (warp == 5) {
@@ -355,95 +422,186 @@ k_kk_gather_tc(const __grid_constant__ TcgArgs a) {
         // uniform registers, no per-MMA lane election.
         const uint32_t idesc = tc::instr_desc(0, 128, 2 * TCG_FB, 1);
         const uint32_t s0 = (uint32_t)__cvta_generic_to_shared(sm);
-        for (int pr = 0; pr < npairs; ++pr) {
-            const int sa_ = pr % TCG_NA, sb_ = pr % TCG_NB;
-            const int grp = pr / TCG_GROUP, d = grp & 1;
-            const bool first = pr % TCG_GROUP == 0;
-            if (first && grp >= 2) tc::mbar_wait(&dfree[d], ((grp >> 1) - 1) & 1);  // drained
-            tc::mbar_wait(&a_full[sa_], (pr / TCG_NA) & 1);
-            tc::mbar_wait(&b_full[sb_], (pr / TCG_NB) & 1);
-            tc::fence_after_sync();
-            const uint32_t sa = s0 + sa_ * ASTAGE, sb = s0 + TCG_NA * ASTAGE + sb_ * BSTAGE;
-            const uint64_t da = tc::smem_desc(sa, 128 * 16, 128), db = tc::smem_desc(sb, 128, TCG_KW * 16);
-            if (tc::elect_one()) {
-                tc::mma_f16_split_pair<A_PLANE, B_PLANE, 2 * 128 * 16, 2 * 128>(tmem + d * 128, da, db, idesc,
-                                                                                  !first);
-                tc::commit(&a_empty[sa_]);
-                tc::commit(&b_empty[sb_]);
-                if (pr % TCG_GROUP == TCG_GROUP - 1 || pr == npairs - 1) tc::commit(&dfull[d]);
+        unsigned P = 0, G = 0;  // pairs and accumulator groups so far
+        for (int k = 0; k < nit; ++k) {
+            for (int pr = 0; pr < npairs; ++pr, ++P) {
+                const int sa_ = (int)(P % TCG_NA), sb_ = (int)(P % TCG_NB), d = (int)(G % TCG_ND);
+                const bool first = pr % TCG_GROUP == 0, last = pr % TCG_GROUP == TCG_GROUP - 1 || pr == npairs - 1;
+                if (first && G >= TCG_ND) tc::mbar_wait(&dfree[d], (uint32_t)((G / TCG_ND - 1) & 1));  // drained
+                tc::mbar_wait(&a_full[sa_], (uint32_t)((P / TCG_NA) & 1));
+                tc::mbar_wait(&b_full[sb_], (uint32_t)((P / TCG_NB) & 1));
+                tc::fence_after_sync();
+                const uint32_t sa = s0 + sa_ * ASTAGE, sb = s0 + TCG_NA * ASTAGE + sb_ * BSTAGE;
+                const bool one = b_k16[sb_] != 0;
+                const uint64_t da = tc::smem_desc(sa, 128 * 16, 128);
+                if (tc::elect_one()) {
+                    if (one)  // 16-sample window: B planes of 16 x 256 B, one K step
+                        tc::mma_f16_split_step<A_PLANE, B_PLANE / 2>(tmem + d * 128, da, tc::smem_desc(sb, 128, 256),
+                                                                     idesc, !first);
+                    else
+                        tc::mma_f16_split_pair<A_PLANE, B_PLANE, 2 * 128 * 16, 2 * 128>(
+                            tmem + d * 128, da, tc::smem_desc(sb, 128, TCG_KW * 16), idesc, !first);
+                    tc::commit(&a_empty[sa_]);
+                    tc::commit(&b_empty[sb_]);
+                    if (last) tc::commit(&dfull[d]);
+                }
+                __syncwarp();
+                if (last) ++G;
             }
-            __syncwarp();
         }
-    } else {
+    } else if (warp < 10) {
         // ------------------------------------------------------------ drains + epilogue
         const int quarter = warp & 3;
         const int r = quarter * 32 + lane;
-        float S[2 * TCG_FB];
+        const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
+        unsigned G = 0;
+        for (int k = 0; k < nit; ++k) {
+            float S[2 * TCG_FB];
 #pragma unroll
-        for (int c = 0; c < 2 * TCG_FB; ++c) S[c] = 0.f;
-        for (int grp = 0; grp < ngroups; ++grp) {
-            const int d = grp & 1;
-            tc::mbar_wait(&dfull[d], (grp >> 1) & 1);
-            tc::fence_after_sync();
+            for (int c = 0; c < 2 * TCG_FB; ++c) S[c] = 0.f;
+            for (int grp = 0; grp < ngroups; ++grp, ++G) {
+                const int d = (int)(G % TCG_ND);
+                tc::mbar_wait(&dfull[d], (uint32_t)((G / TCG_ND) & 1));
+                tc::fence_after_sync();
 #pragma unroll
-            for (int c0 = 0; c0 < 2 * TCG_FB; c0 += 8) {
-                float v[8];
-                tc::tmem_ld8(tmem + ((uint32_t)(quarter * 32) << 16) + d * 128 + c0, v);
-                tc::tmem_ld_wait();
+                for (int c0 = 0; c0 < 2 * TCG_FB; c0 += 16) {
+                    float v[8], u[8];
+                    tc::tmem_ld8(lane_base + d * 128 + c0, v);
+                    tc::tmem_ld8(lane_base + d * 128 + c0 + 8, u);
+                    tc::tmem_ld_wait();
 #pragma unroll
-                for (int i = 0; i < 8; ++i) S[c0 + i] = __fadd_rn(S[c0 + i], v[i]);
+                    for (int i = 0; i < 8; ++i) {
+                        S[c0 + i] = __fadd_rn(S[c0 + i], v[i]);
+                        S[c0 + 8 + i] = __fadd_rn(S[c0 + 8 + i], u[i]);
+                    }
+                }
+                tc::fence_before_sync();
+                mbar_arrive(&dfree[d]);
             }
-            tc::fence_before_sync();
-            mbar_arrive(&dfree[d]);
+            // epilogue: straight-line passes over the 64 frames (IQ, |IQ|^2,
+            // per-frame max), each frame independent of the others
+            const int tile = tile_of(k), f0 = fb_of(k) * TCG_FB;
+            const int FB = min(TCG_FB, a.n_frames - f0);
+            const int ix = (tile / a.tiles_z) * TCG_TX + r / TCG_TZ, iz = (tile % a.tiles_z) * TCG_TZ + r % TCG_TZ;
+            const bool pix = ix < nx && iz < nz;
+            const long long px0 = (long long)f0 * a.out_fs + (long long)ix * nz + iz;
+#pragma unroll
+            for (int f = 0; f < TCG_FB; ++f) {
+                // exact: the product of two powers of two
+                const float sc = frame_scale(__ldg(a.maxabs + min(f0 + f, a.n_frames - 1)));
+                const float inv = f < FB ? 1.0f / (sc * TCG_WSCALE) : 0.f;
+                S[f] *= inv;
+                S[TCG_FB + f] *= inv;
+            }
+            if (a.out && pix) {
+                if (a.out_kind == KKB_OUT_C128) {
+#pragma unroll
+                    for (int f = 0; f < TCG_FB; ++f)
+                        if (f < FB)
+                            reinterpret_cast<double2 *>(a.out)[px0 + f * a.out_fs] = make_double2(S[f], S[TCG_FB + f]);
+                } else {
+#pragma unroll
+                    for (int f = 0; f < TCG_FB; ++f)
+                        if (f < FB)
+                            reinterpret_cast<float2 *>(a.out)[px0 + f * a.out_fs] = make_float2(S[f], S[TCG_FB + f]);
+                }
+            }
+            if (a.inten) {
+#pragma unroll
+                for (int f = 0; f < TCG_FB; ++f) S[f] = pix ? __fmaf_rn(S[f], S[f], __fmul_rn(S[TCG_FB + f], S[TCG_FB + f])) : 0.f;
+                if (pix) {
+                    if (a.accum) {
+#pragma unroll
+                        for (int f = 0; f < TCG_FB; ++f)
+                            if (f < FB) S[f] = __fadd_rn(S[f], a.inten[px0 + f * a.out_fs]);
+                    }
+#pragma unroll
+                    for (int f = 0; f < TCG_FB; ++f)
+                        if (f < FB) a.inten[px0 + f * a.out_fs] = S[f];
+                }
+                if (a.fmax) {
+                    // non-negative floats order like their bit patterns: one redux per frame
+#pragma unroll
+                    for (int f = 0; f < TCG_FB; ++f) {
+                        const unsigned mx = __reduce_max_sync(0xffffffffu, __float_as_uint(S[f]));
+                        if (lane == 0 && f < FB) atomicMax(a.fmax + f0 + f, mx);
+                    }
+                }
+            }
         }
-        const int ix = ix0 + r / TCG_TZ, iz = iz0 + r % TCG_TZ;
-        const bool pix = ix < nx && iz < nz;
-#pragma unroll
-        for (int f = 0; f < TCG_FB; ++f) {
-            if (f >= FB) break;
-            const float inv = 1.0f / (fscale[f] * TCG_WSCALE);   // exact: a power of two
-            const float vr = S[f] * inv, vi = S[TCG_FB + f] * inv;
-            float I = 0.f;
-            if (pix) {
-                const long long px = (long long)(f0 + f) * a.out_fs + (long long)ix * nz + iz;
-                if (a.out) {
-                    if (a.out_kind == KKB_OUT_C128)
-                        reinterpret_cast<double2 *>(a.out)[px] = make_double2(vr, vi);
-                    else
-                        reinterpret_cast<float2 *>(a.out)[px] = make_float2(vr, vi);
+    } else {
+        // ------------------------------------------------------------ tile tables (next items)
+        int held[2] = {-1, -1};  // tile held by each slot
+        for (int k = 0; k < nit; ++k) {
+            const int slot = k & 1, tile = tile_of(k);
+            if (k >= 2) tc::mbar_wait(&tab_empty[slot], (uint32_t)(((k >> 1) - 1) & 1));
+            if (held[slot] != tile) {
+                const TcgTables tb = tcg_tables(tab_base + slot * slot_bytes, N, M);
+                const int iz0 = (tile % a.tiles_z) * TCG_TZ, ix0 = (tile / a.tiles_z) * TCG_TX;
+                // edge tiles repeat the last row / column
+                for (int i = lane; i < N * TCG_TX; i += 32) {
+                    const int n = i / TCG_TX, c = i - n * TCG_TX;
+                    tb.ltx[i] = __ldg(a.ltx + (long long)min(ix0 + c, nx - 1) * N + n);
                 }
-                if (a.inten) {
-                    I = __fmaf_rn(vr, vr, __fmul_rn(vi, vi));
-                    if (a.accum) I = __fadd_rn(I, a.inten[px]);
-                    a.inten[px] = I;
+                for (int i = lane; i < N * TCG_TZ; i += 32) {
+                    const int n = i / TCG_TZ, rr = i - n * TCG_TZ;
+                    tb.ltz[i] = __ldg(a.ltzT + (long long)n * nz + min(iz0 + rr, nz - 1));
                 }
+                for (int i = lane; i < M * TCG_TX; i += 32) {
+                    const int m = i / TCG_TX, c = i - m * TCG_TX;
+                    tb.lrx[i] = __ldg(a.lrx + (long long)min(ix0 + c, nx - 1) * M + m);
+                }
+                for (int i = lane; i < M * TCG_TZ; i += 32) {
+                    const int m = i / TCG_TZ, rr = i - m * TCG_TZ;
+                    tb.lrz[i] = __ldg(a.lrzT + (long long)m * nz + min(iz0 + rr, nz - 1));
+                }
+                __syncwarp();
+                const int rzb = min(TCG_TZ - 1, nz - 1 - iz0), cxb = min(TCG_TX - 1, nx - 1 - ix0);
+                for (int i = lane; i < npairs; i += 32) {
+                    const int n = i / M, m = i - n * M;
+                    double lo = 1e300;
+                    for (int cr = 0; cr < 2; ++cr)
+                        for (int cc = 0; cc < 2; ++cc) {
+                            const int rr = cr ? rzb : 0, c = cc ? cxb : 0;
+                            const double t1 = __dadd_rn(tb.ltx[n * TCG_TX + c], tb.ltz[n * TCG_TZ + rr]);
+                            lo = fmin(lo, tc_kk_delay(t1, tb.lrz[m * TCG_TZ + rr], tb.lrx[m * TCG_TX + c], fs, shift));
+                        }
+                    // a live window (plan proof: lo in (-W, T - 1)) is never clamped; a
+                    // dead one (every tap rejected) is zero-filled by the TMA unit
+                    const int lo_i = (int)fmax(fmin(floor(lo) - 1.0, (double)T), (double)-TCG_KW);
+                    tb.lo[i] = lo_i * 2 + (a.k16 && a.k16[(long long)tile * npairs + i] ? 1 : 0);
+                }
+                held[slot] = tile;
             }
-            if (a.fmax) {
-                // non-negative floats order like their bit patterns: one redux per frame
-                const unsigned mx = __reduce_max_sync(0xffffffffu, __float_as_uint(I));
-                if (lane == 0) atomicMax(a.fmax + f0 + f, mx);
-            }
+            mbar_arrive(&tab_full[slot]);
         }
     }
     tc::fence_before_sync();
     __syncthreads();
     if (warp == 4) {
         __syncwarp();
-        tc::tmem_free<256>(tmem);
+        tc::tmem_free<32 * 4 * TCG_ND>(tmem);
     }
 }
 
 int kk_gather_tc(const float2 *data, int N, int M, int T, const double *ltx, const double *ltzT,
                  const double *lrx, const double *lrzT, int nx, int nz, const double *w, double fs,
                  double shift, int linear, void *out, int out_kind, int n_frames, long long data_fs,
-                 long long out_fs, float *inten, unsigned *fmax, int W, int accum, cudaStream_t s) {
+                 long long out_fs, float *inten, unsigned *fmax, int W, const unsigned char *k16, int accum,
+                 cudaStream_t s, const std::function<int(const unsigned *)> &fma_fallback) {
     if (W > TCG_KW || W < 2) return KKB_ERR_UNSUPPORTED;
     const int NM = N * M;
     const long long ngroups = (n_frames + 7) / 8;
     const size_t plane_elems = (size_t)ngroups * NM * T * 8;
-    unsigned *mx = nullptr;
+    const size_t smem = (size_t)TCG_NA * (2 * (TCG_KW / 8) * 128 * 16) + (size_t)TCG_NB * (2 * 16 * TCG_KW * 16) +
+                        2 * tcg_slot_bytes(N, M) + sizeof(float) * (size_t)M;
+    if (smem > 227 * 1024) {
+        set_error("kk tensor-core gather: %d pairs do not fit shared memory", NM);
+        return KKB_ERR_UNSUPPORTED;
+    }
+    unsigned *mx = nullptr;  // [n_frames] frame max, then the non-finite flag
     __half *planes = nullptr;
-    KKB_TRY_CUDA(cudaMallocAsync(&mx, sizeof(unsigned) * (size_t)n_frames, s), "cudaMallocAsync(frame max)");
+    KKB_TRY_CUDA(cudaMallocAsync(&mx, sizeof(unsigned) * ((size_t)n_frames + 1), s), "cudaMallocAsync(frame max)");
     struct Free {
         void *p;
         cudaStream_t s;
@@ -453,14 +611,22 @@ int kk_gather_tc(const float2 *data, int N, int M, int T, const double *ltx, con
     } f1{mx, s};
     KKB_TRY_CUDA(cudaMallocAsync(&planes, sizeof(__half) * 4 * plane_elems, s), "cudaMallocAsync(trace planes)");
     Free f2{planes, s};
-    KKB_TRY_CUDA(cudaMemsetAsync(mx, 0, sizeof(unsigned) * (size_t)n_frames, s), "zero frame max");
+    unsigned *nonfinite = mx + n_frames;
+    KKB_TRY_CUDA(cudaMemsetAsync(mx, 0, sizeof(unsigned) * ((size_t)n_frames + 1), s), "zero frame max");
     const long long per = (long long)NM * T;
-    const int bx = (int)std::max<long long>(1, std::min<long long>(ceil_div(per, 256), std::max(1, 148 * 4 / n_frames)));
-    k_frame_maxabs<<<dim3(bx, n_frames), 256, 0, s>>>(data, data_fs, per, mx);
+    const bool v2 = (T % 2) == 0 && (data_fs % 2) == 0 && ((uintptr_t)data & 15) == 0;
+    const int bx = (int)std::max<long long>(1, std::min<long long>(ceil_div(per, 512), ceil_div(148LL * 16, n_frames)));
+    if (v2)
+        k_frame_maxabs<2><<<dim3(bx, n_frames), 256, 0, s>>>(data, data_fs, per, mx, nonfinite);
+    else
+        k_frame_maxabs<1><<<dim3(bx, n_frames), 256, 0, s>>>(data, data_fs, per, mx, nonfinite);
     KKB_CHECK_LAUNCH("k_frame_maxabs");
-    const long long units = ngroups * NM * (long long)T;
-    k_split_planes<<<(unsigned)std::min<long long>(ceil_div(units, 256), 148LL * 64), 256, 0, s>>>(
-        data, data_fs, n_frames, NM, T, mx, ngroups, planes);
+    const long long units = ngroups * NM * (long long)(T / (v2 ? 2 : 1));
+    const unsigned sblocks = (unsigned)std::min<long long>(ceil_div(units, 256), 148LL * 32);
+    if (v2)
+        k_split_planes<2><<<sblocks, 256, 0, s>>>(data, data_fs, n_frames, NM, T, mx, ngroups, planes);
+    else
+        k_split_planes<1><<<sblocks, 256, 0, s>>>(data, data_fs, n_frames, NM, T, mx, ngroups, planes);
     KKB_CHECK_LAUNCH("k_split_planes");
     static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
     if (!encode) {
@@ -478,10 +644,14 @@ int kk_gather_tc(const float2 *data, int N, int M, int T, const double *ltx, con
         // (sample, frame) flattened: a window is one 512-byte row of the box
         const cuuint64_t dims[4] = {8ull * T, (cuuint64_t)NM, (cuuint64_t)ngroups, 4};
         const cuuint64_t strides[3] = {16ull * T, 16ull * T * NM, 16ull * T * NM * ngroups};
-        const cuuint32_t box[4] = {8 * TCG_KW, 1, 8, 4}, estr[4] = {1, 1, 1, 1};
-        const CUresult r = encode(&a.planes, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, planes, dims, strides, box, estr,
-                                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        const cuuint32_t box[4] = {8 * TCG_KW, 1, 8, 4}, box16[4] = {8 * 16, 1, 8, 4}, estr[4] = {1, 1, 1, 1};
+        CUresult r = encode(&a.planes, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, planes, dims, strides, box, estr,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r == CUDA_SUCCESS)
+            r = encode(&a.planes16, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, planes, dims, strides, box16, estr,
+                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) {
             set_error("kk tensor-core gather: cuTensorMapEncodeTiled failed (%d)", (int)r);
             return KKB_ERR_CUDA;
@@ -490,14 +660,12 @@ int kk_gather_tc(const float2 *data, int N, int M, int T, const double *ltx, con
     a.N = N, a.M = M, a.T = T, a.ltx = ltx, a.ltzT = ltzT, a.lrx = lrx, a.lrzT = lrzT, a.w = w;
     a.fs = fs, a.shift = shift, a.nx = nx, a.nz = nz, a.out = out, a.out_kind = out_kind, a.out_fs = out_fs;
     a.inten = inten, a.fmax = fmax, a.accum = accum, a.n_frames = n_frames, a.maxabs = mx;
-    constexpr int ASTAGE = 2 * (TCG_KW / 8) * 128 * 16, BSTAGE = 2 * 16 * TCG_KW * 16;
-    const size_t smem = (size_t)TCG_NA * ASTAGE + (size_t)TCG_NB * BSTAGE + sizeof(double) * (size_t)(N + M) * (TCG_TX + TCG_TZ) +
-                        sizeof(float) * (size_t)M + sizeof(int) * (size_t)NM;
-    if (smem > 227 * 1024) {
-        set_error("kk tensor-core gather: %d pairs do not fit shared memory", NM);
-        return KKB_ERR_UNSUPPORTED;
-    }
-    dim3 grid((unsigned)(ceil_div(nz, TCG_TZ) * ceil_div(nx, TCG_TX)), (unsigned)ceil_div(n_frames, TCG_FB));
+    a.nonfinite = nonfinite;
+    a.k16 = k16;
+    a.tiles_z = (int)ceil_div(nz, TCG_TZ);
+    a.tiles = (long long)a.tiles_z * ceil_div(nx, TCG_TX);
+    a.items = a.tiles * ceil_div(n_frames, TCG_FB);
+    const unsigned grid = (unsigned)std::min<long long>(a.items, sm_count());
     if (linear) {
         KKB_TRY_CUDA(cudaFuncSetAttribute(k_kk_gather_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                      "smem attr kk tc");
@@ -508,7 +676,8 @@ int kk_gather_tc(const float2 *data, int N, int M, int T, const double *ltx, con
         k_kk_gather_tc<false><<<grid, TCG_THREADS, smem, s>>>(a);
     }
     KKB_CHECK_LAUNCH("k_kk_gather_tc");
-    return KKB_OK;
+    // the FMA gather, live only when the batch held a non-finite sample
+    return fma_fallback(nonfinite);
 }
 
 }  // namespace kkb

@@ -79,6 +79,24 @@ __device__ __forceinline__ void mma_f16_split_pair(uint32_t d_tmem, uint64_t a, 
         "n"((long long)(BPL >> 4)), "n"((long long)(AK >> 4)), "n"((long long)(BK >> 4)));
 }
 
+// One K = 16 step of the same split product (3 MMAs): A hi x B hi,
+// A hi x B lo (B lo at +BPL bytes), A lo x B hi (A lo at +APL bytes).
+template <int APL, int BPL>
+__device__ __forceinline__ void mma_f16_split_step(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc,
+                                                   bool accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p, q;\n\t.reg .b64 a1, b1;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "setp.eq.b32 q, 0, 0;\n\t"
+        "add.s64 b1, %2, %6;\n\t"
+        "add.s64 a1, %1, %5;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, b1, %3, q;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], a1, %2, %3, q;\n\t}\n" ::"r"(d_tmem),
+        "l"(a), "l"(b), "r"(idesc), "r"((uint32_t)accumulate), "n"((long long)(APL >> 4)),
+        "n"((long long)(BPL >> 4)));
+}
+
 // one lane of the (converged) warp
 __device__ __forceinline__ bool elect_one() {
     uint32_t p = 0;
