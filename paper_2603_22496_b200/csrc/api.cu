@@ -185,7 +185,7 @@ extern "C" int kkb_kk_plan_create(const double *ltx, const double *ltz, const do
     p->w = weights ? p->lrzT + n_lrz : nullptr;
     auto fail = [&](int code) {
         cudaFree(buf);
-        if (p->win.tc_k16) cudaFree(p->win.tc_k16);
+        if (p->win.tc_lo) cudaFree(p->win.tc_lo);
         delete p;
         return code;
     };
@@ -350,7 +350,7 @@ extern "C" int kkb_kk_plan_run(kkb_kk_plan *p, const void *data, int n_frames,
 extern "C" int kkb_kk_plan_destroy(kkb_kk_plan *p) {
     if (!p) return KKB_OK;
     cudaFree(p->ltx);
-    if (p->win.tc_k16) cudaFree(p->win.tc_k16);
+    if (p->win.tc_lo) cudaFree(p->win.tc_lo);
     delete p;
     return KKB_OK;
 }

@@ -66,9 +66,11 @@ struct KKWindows {
     int big, mid, small;
     int bad;  // bit (1 << KKB_KK_INST_*): instance whose window failed kk_check_windows
     int tc;   // window of the tensor-core gather's tile (KKB_KK_TC_TZ x KKB_KK_TC_TX)
-    // per (tensor-core tile, pair): 1 when every live tap of the tile sits in
-    // the first 16 window samples (one K = 16 step); device, owned by the plan
-    unsigned char *tc_k16;
+    // per (tensor-core tile, pair): the exact window start (the smallest live
+    // tap index of the tile's pixels) * 2 + 1 when every live tap sits in its
+    // first 16 samples (one K = 16 step); device, owned by the plan; null when
+    // the tensor-core gather cannot take the plan
+    int *tc_lo;
 };
 // Synchronises `s` (one launch for the three tile sizes).
 int kk_window(const double *ltx, const double *ltz, const double *lrx, const double *lrz, int N,
@@ -110,14 +112,13 @@ int kk_check_windows(const double *ltx, const double *ltz, const double *lrx, co
                      KKWindows *win, cudaStream_t s);
 
 // tensor-core (tcgen05) form of K5 (kk_gather_tc.cu): 4 x 32-pixel tiles,
-// 64 frames per work item, persistent CTAs; W = the tile window (<=
-// KKB_KK_TC_W).  fma_fallback(run_if) launches the FMA instance as a standby
+// 64 frames per work item, persistent CTAs; tc_lo = KKWindows::tc_lo.  fma_fallback(run_if) launches the FMA instance as a standby
 // that runs only when *run_if != 0 (a non-finite sample in the batch).
 // KKB_ERR_UNSUPPORTED (nothing launched) when the shape does not fit.
 int kk_gather_tc(const float2 *data, int N, int M, int T, const double *ltx, const double *ltzT,
                  const double *lrx, const double *lrzT, int nx, int nz, const double *w, double fs,
                  double shift, int linear, void *out, int out_kind, int n_frames, long long data_fs,
-                 long long out_fs, float *inten, unsigned *fmax, int W, const unsigned char *k16, int accum,
+                 long long out_fs, float *inten, unsigned *fmax, const int *tc_lo, int accum,
                  cudaStream_t s, const std::function<int(const unsigned *)> &fma_fallback);
 #define KKB_KK_TC_TZ 4   // tensor-core tile: 4 depth rows x 32 columns (128 pixels = M)
 #define KKB_KK_TC_TX 32

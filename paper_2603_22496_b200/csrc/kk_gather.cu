@@ -871,57 +871,58 @@ k_kk_window_check(const double *__restrict__ ltx, const double *__restrict__ ltz
     }
 }
 
-// Per (tensor-core tile, pair): whether every live tap of the tile's pixels
-// falls in the first 16 samples of the pair's window (window start as in
-// kk_gather_tc.cu: floor(min corner delay) - 1); such pairs take one K = 16
-// MMA step instead of two.  Exact, with the gather's own index arithmetic.
+// Tensor-core gather windows, per (tile, pair) of its 4 x 32 tile: the
+// smallest and largest live tap index over the tile's pixels, with the
+// gather's own index arithmetic (exact: every pixel is evaluated).  The
+// window starts at the smallest; it takes one K = 16 MMA step when the taps
+// span <= 16 samples (linear: F + 1 included), else two; a span beyond 32
+// makes the plan ineligible (the table is dropped, the FMA gather runs).
 template <bool LINEAR>
 __global__ void __launch_bounds__(256)
-k_kk_tc_k16(const double *__restrict__ ltx, const double *__restrict__ ltz, const double *__restrict__ lrx,
-            const double *__restrict__ lrz, int N, int M, int T, int nx, int nz, double fs, double shift,
-            unsigned char *__restrict__ k16) {
+k_kk_tc_windows(const double *__restrict__ ltx, const double *__restrict__ ltz, const double *__restrict__ lrx,
+                const double *__restrict__ lrz, int N, int M, int T, int nx, int nz, double fs, double shift,
+                int *__restrict__ tc_lo, int *over_flag) {
     const int TZ = KKB_KK_TC_TZ, TX = KKB_KK_TC_TX;
     const int tiles_z = (nz + TZ - 1) / TZ;
     const long long NM = (long long)N * M, total = (long long)tiles_z * ((nx + TX - 1) / TX) * NM;
+    bool over = false;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
          i += (long long)gridDim.x * blockDim.x) {
         const long long tile = i / NM;
         const int pr = (int)(i % NM), n = pr / M, m = pr % M;
         const int iz0 = (int)(tile % tiles_z) * TZ, ix0 = (int)(tile / tiles_z) * TX;
         const int rzb = min(TZ - 1, nz - 1 - iz0), cxb = min(TX - 1, nx - 1 - ix0);
-        double lo = 1e300;
-        for (int cr = 0; cr < 2; ++cr)
-            for (int cc = 0; cc < 2; ++cc) {
-                const int iz = iz0 + (cr ? rzb : 0), ix = ix0 + (cc ? cxb : 0);
-                const double t1 = __dadd_rn(ltx[(long long)ix * N + n], ltz[(long long)iz * N + n]);
-                lo = fmin(lo, kk_delay(t1, lrz[(long long)iz * M + m], lrx[(long long)ix * M + m], fs, shift));
-            }
-        const int lo_i = (int)fmax(fmin(floor(lo) - 1.0, (double)T), (double)-KKB_KK_TC_W);
-        bool fits = true;
-        for (int c = 0; c <= cxb && fits; ++c)
+        int fmin_ = 0x7fffffff, fmax_ = -1;
+        for (int c = 0; c <= cxb; ++c)
             for (int r = 0; r <= rzb; ++r) {
                 const int iz = iz0 + r, ix = ix0 + c;
                 const double t1 = __dadd_rn(ltx[(long long)ix * N + n], ltz[(long long)iz * N + n]);
                 const double fi = kk_delay(t1, lrz[(long long)iz * M + m], lrx[(long long)ix * M + m], fs, shift);
                 const double sv = __dadd_rd(LINEAR ? fi : __dadd_rn(fi, 0.5), KKB_FLOOR_MAGIC2);
                 const int F = __double2hiint(sv) - KKB_MAGIC2_HI;
-                const bool tap = (unsigned)F <= (unsigned)(LINEAR ? T - 2 : T - 1);
-                const int e = F - lo_i;
-                if (tap && (e < 0 || e + (LINEAR ? 1 : 0) > 15)) fits = false;
+                if ((unsigned)F <= (unsigned)(LINEAR ? T - 2 : T - 1)) {
+                    fmin_ = min(fmin_, F);
+                    fmax_ = max(fmax_, F);
+                }
             }
-        k16[i] = fits ? 1 : 0;
+        const int lo = fmax_ < 0 ? 0 : fmin_;                          // no live tap: any window
+        const int span = fmax_ < 0 ? 1 : fmax_ - fmin_ + 1 + (LINEAR ? 1 : 0);  // samples touched
+        over |= span > KKB_KK_TC_W;
+        tc_lo[i] = lo * 2 + (span <= 16 ? 1 : 0);
     }
+    if (__syncthreads_or(over) && threadIdx.x == 0) atomicOr(over_flag, 1);
 }
 
 int kk_check_windows(const double *ltx, const double *ltz, const double *lrx, const double *lrz,
                      int N, int M, int T, int nx, int nz, double fs, double shift, int linear,
                      KKWindows *win, cudaStream_t s) {
     win->bad = 0;
-    win->tc_k16 = nullptr;
+    win->tc_lo = nullptr;
     if ((size_t)M * sizeof(int) > 48 * 1024) return KKB_OK;  // huge pair tables: no tile fits anyway
     int *d = nullptr;
-    KKB_TRY_CUDA(cudaMallocAsync(&d, sizeof(int), s), "cudaMallocAsync(window check)");
-    KKB_TRY_CUDA(cudaMemsetAsync(d, 0, sizeof(int), s), "memset(window check)");
+    // d[0]: failed tile sizes; d[1]: the tensor-core windows exceed 32 samples
+    KKB_TRY_CUDA(cudaMallocAsync(&d, 2 * sizeof(int), s), "cudaMallocAsync(window check)");
+    KKB_TRY_CUDA(cudaMemsetAsync(d, 0, 2 * sizeof(int), s), "memset(window check)");
     const int insts[3] = {KKB_KK_INST_BIG, KKB_KK_INST_MID, KKB_KK_INST_SMALL};
     for (int k = 0; k < 3; ++k) {
         const InstanceShape sh = instance_shape(insts[k], *win);
@@ -938,39 +939,33 @@ int kk_check_windows(const double *ltx, const double *ltz, const double *lrx, co
                                                              sh.tz, sh.W, fs, shift, 1 << insts[k], d);
         KKB_CHECK_LAUNCH("k_kk_window_check");
     }
-    if (win->tc >= 2 && win->tc <= KKB_KK_TC_W && ceil_div(nz, KKB_KK_TC_TZ) * ceil_div(nx, KKB_KK_TC_TX) <= 0x7fffffffLL &&
-        N <= 65535) {  // the tensor-core gather's 8 x 16 tile
-        dim3 grid((unsigned)(ceil_div(nz, KKB_KK_TC_TZ) * ceil_div(nx, KKB_KK_TC_TX)), (unsigned)N);
-        const size_t smem = sizeof(int) * (size_t)M;
-        if (linear)
-            k_kk_window_check<true><<<grid, 256, smem, s>>>(ltx, ltz, lrx, lrz, N, M, T, nx, nz, KKB_KK_TC_TX,
-                                                            KKB_KK_TC_TZ, win->tc, fs, shift, 1 << KKB_KK_INST_TC, d);
-        else
-            k_kk_window_check<false><<<grid, 256, smem, s>>>(ltx, ltz, lrx, lrz, N, M, T, nx, nz, KKB_KK_TC_TX,
-                                                             KKB_KK_TC_TZ, win->tc, fs, shift, 1 << KKB_KK_INST_TC, d);
-        KKB_CHECK_LAUNCH("k_kk_window_check");
-    }
-    win->tc_k16 = nullptr;
-    if (win->tc >= 2 && win->tc <= KKB_KK_TC_W) {
-        const long long n16 = ceil_div(nz, KKB_KK_TC_TZ) * ceil_div(nx, KKB_KK_TC_TX) * (long long)N * M;
-        if (cudaMalloc(&win->tc_k16, (size_t)n16) == cudaSuccess) {
-            const int blocks = (int)std::min<long long>(ceil_div(n16, 256), 148LL * 16);
+    {  // the tensor-core gather's exact per (tile, pair) windows
+        const long long ntc = ceil_div(nz, KKB_KK_TC_TZ) * ceil_div(nx, KKB_KK_TC_TX) * (long long)N * M;
+        if (cudaMalloc(&win->tc_lo, sizeof(int) * (size_t)ntc) == cudaSuccess) {
+            const int blocks = (int)std::min<long long>(ceil_div(ntc, 256), 148LL * 16);
             if (linear)
-                k_kk_tc_k16<true><<<blocks, 256, 0, s>>>(ltx, ltz, lrx, lrz, N, M, T, nx, nz, fs, shift, win->tc_k16);
+                k_kk_tc_windows<true><<<blocks, 256, 0, s>>>(ltx, ltz, lrx, lrz, N, M, T, nx, nz, fs, shift,
+                                                             win->tc_lo, d + 1);
             else
-                k_kk_tc_k16<false><<<blocks, 256, 0, s>>>(ltx, ltz, lrx, lrz, N, M, T, nx, nz, fs, shift, win->tc_k16);
-            KKB_CHECK_LAUNCH("k_kk_tc_k16");
+                k_kk_tc_windows<false><<<blocks, 256, 0, s>>>(ltx, ltz, lrx, lrz, N, M, T, nx, nz, fs, shift,
+                                                              win->tc_lo, d + 1);
+            KKB_CHECK_LAUNCH("k_kk_tc_windows");
         } else {
-            cudaGetLastError();  // no table: every pair takes two K steps
-            win->tc_k16 = nullptr;
+            cudaGetLastError();  // no table: the tensor-core gather is not dispatched
+            win->tc_lo = nullptr;
         }
     }
-    int h = 0;
-    KKB_TRY_CUDA(cudaMemcpyAsync(&h, d, sizeof(int), cudaMemcpyDeviceToHost, s), "copy window check");
+    int hh[2] = {0, 0};
+    KKB_TRY_CUDA(cudaMemcpyAsync(hh, d, sizeof(hh), cudaMemcpyDeviceToHost, s), "copy window check");
     KKB_TRY_CUDA(cudaStreamSynchronize(s), "sync window check");
     cudaFreeAsync(d, s);
     // a tile size that failed disables its instances (big covers both frame counts)
+    const int h = hh[0];
     win->bad = h | ((h & (1 << KKB_KK_INST_BIG)) ? (1 << KKB_KK_INST_BIG_FR) : 0);
+    if (hh[1] && win->tc_lo) {  // too steep for the tensor-core tile: not eligible (not an error)
+        cudaFree(win->tc_lo);
+        win->tc_lo = nullptr;
+    }
     return KKB_OK;
 }
 
@@ -1101,17 +1096,17 @@ int kk_gather(const float2 *data, int N, int M, int T, const double *ltx, const 
         }
     };
     // tensor-core gather (kk_gather_tc.cu): single-set launches without peer
-    // scatter whose 4 x 32 tile has a proven window of <= KKB_KK_TC_W samples.
+    // scatter whose plan holds exact tile windows of <= KKB_KK_TC_W samples.
     // The FMA instance is launched behind it as a standby that only runs when
     // the batch holds a NaN / Inf sample (the reference propagates those per
     // tap; a tensor-core product would spread them over the window).
     {
         const char *fi = getenv("KKB_KK_INST");
         const bool want = fi && !strcmp(fi, "tc");
-        const bool tc_ok = !ms && !sc && win.tc >= 2 && win.tc <= KKB_KK_TC_W && !(win.bad & (1 << KKB_KK_INST_TC));
+        const bool tc_ok = !ms && !sc && win.tc_lo && !(win.bad & (1 << KKB_KK_INST_TC));
         if (want && tc_ok) {
             const int rc = kk_gather_tc(data, N, M, T, ltx, ltzT, lrx, lrzT, nx, nz, w, fs, shift, linear, out,
-                                        out_kind, n_frames, data_fs, out_fs, inten, fmax, win.tc, win.tc_k16, accum, s,
+                                        out_kind, n_frames, data_fs, out_fs, inten, fmax, win.tc_lo, accum, s,
                                         [&](const unsigned *run_if) {
                                             KKArgs b = a;
                                             b.run_if = run_if;

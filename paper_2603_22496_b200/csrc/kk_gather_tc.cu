@@ -1,17 +1,18 @@
 // K5 on the 5th-generation tensor cores: the kk pixel gather (_kk_kernel,
 // beamform.py:212-236) as a sequence of small GEMMs, one per (tx, rx) pair.
 //
-// For a tile of 128 pixels (8 depth rows x 16 lateral columns) and a batch of
+// For a tile of 128 pixels (4 depth rows x 32 lateral columns) and a block of
 // 64 frames, the linear interpolation of pair (n, m) is
-//     IQ[px, f] += sum_e  W_nm[px, e] * trace_nm[f, lo_nm + e],   e < 32
+//     IQ[px, f] += sum_e  W_nm[px, e] * trace_nm[f, lo_nm + e],   e < 16 or 32
 // where W_nm has at most two nonzeros per pixel row: w_m (1 - frac) at
 // e = floor(fi) - lo and w_m frac at e + 1 (nearest: w_m at floor(fi + 0.5) - lo),
 // and the row is all zero when the reference's in-window rule rejects the tap
 // (beamform.py:226-235) — so the rule costs nothing in the product.  fi is the
 // reference's float64 delay in its exact operation order (the FMA kernels'
-// index arithmetic, bit for bit), frac its 23-bit weight.  The window
-// [lo_nm, lo_nm + 32) comes from the tile's corner delays and is proven for
-// every (pixel, pair) at plan creation (kk_check_windows).
+// index arithmetic, bit for bit), frac its 23-bit weight.  The window start
+// lo_nm and its length (16 or 32 samples: one or two K = 16 steps) come from
+// the plan (k_kk_tc_windows, kk_gather.cu): every pixel of the tile evaluated
+// with this same arithmetic, so the window provably holds every live tap.
 //
 // Operands: one tcgen05.mma (kind::f16, M = 128 pixels, N = 128 = re | im of
 // 64 frames, K = 16 samples) per 16 window samples and split term.  Every
@@ -175,7 +176,7 @@ __global__ void __launch_bounds__(256) k_split_planes(const float2 *__restrict__
 struct TcgArgs {
     CUtensorMap planes;      // 4-D map of the split trace planes: 32-sample windows
     CUtensorMap planes16;    // the same planes, 16-sample windows (one K step)
-    const unsigned char *k16;  // [tile][pair] 1: the pair's taps fit 16 samples (or null)
+    const int *tc_lo;        // [tile][pair] window start * 2 + one-K-step flag (plan time, exact)
     int N, M, T;
     const double *ltx, *ltzT, *lrx, *lrzT, *w;
     double fs, shift;
@@ -555,22 +556,8 @@ k_kk_gather_tc(const __grid_constant__ TcgArgs a) {
                     const int m = i / TCG_TZ, rr = i - m * TCG_TZ;
                     tb.lrz[i] = __ldg(a.lrzT + (long long)m * nz + min(iz0 + rr, nz - 1));
                 }
-                __syncwarp();
-                const int rzb = min(TCG_TZ - 1, nz - 1 - iz0), cxb = min(TCG_TX - 1, nx - 1 - ix0);
-                for (int i = lane; i < npairs; i += 32) {
-                    const int n = i / M, m = i - n * M;
-                    double lo = 1e300;
-                    for (int cr = 0; cr < 2; ++cr)
-                        for (int cc = 0; cc < 2; ++cc) {
-                            const int rr = cr ? rzb : 0, c = cc ? cxb : 0;
-                            const double t1 = __dadd_rn(tb.ltx[n * TCG_TX + c], tb.ltz[n * TCG_TZ + rr]);
-                            lo = fmin(lo, tc_kk_delay(t1, tb.lrz[m * TCG_TZ + rr], tb.lrx[m * TCG_TX + c], fs, shift));
-                        }
-                    // a live window (plan proof: lo in (-W, T - 1)) is never clamped; a
-                    // dead one (every tap rejected) is zero-filled by the TMA unit
-                    const int lo_i = (int)fmax(fmin(floor(lo) - 1.0, (double)T), (double)-TCG_KW);
-                    tb.lo[i] = lo_i * 2 + (a.k16 && a.k16[(long long)tile * npairs + i] ? 1 : 0);
-                }
+                const int *src = a.tc_lo + (long long)tile * npairs;
+                for (int i = lane; i < npairs; i += 32) tb.lo[i] = __ldg(src + i);
                 held[slot] = tile;
             }
             mbar_arrive(&tab_full[slot]);
@@ -587,9 +574,9 @@ k_kk_gather_tc(const __grid_constant__ TcgArgs a) {
 int kk_gather_tc(const float2 *data, int N, int M, int T, const double *ltx, const double *ltzT,
                  const double *lrx, const double *lrzT, int nx, int nz, const double *w, double fs,
                  double shift, int linear, void *out, int out_kind, int n_frames, long long data_fs,
-                 long long out_fs, float *inten, unsigned *fmax, int W, const unsigned char *k16, int accum,
+                 long long out_fs, float *inten, unsigned *fmax, const int *tc_lo, int accum,
                  cudaStream_t s, const std::function<int(const unsigned *)> &fma_fallback) {
-    if (W > TCG_KW || W < 2) return KKB_ERR_UNSUPPORTED;
+    if (!tc_lo) return KKB_ERR_UNSUPPORTED;
     const int NM = N * M;
     const long long ngroups = (n_frames + 7) / 8;
     const size_t plane_elems = (size_t)ngroups * NM * T * 8;
@@ -661,7 +648,7 @@ int kk_gather_tc(const float2 *data, int N, int M, int T, const double *ltx, con
     a.fs = fs, a.shift = shift, a.nx = nx, a.nz = nz, a.out = out, a.out_kind = out_kind, a.out_fs = out_fs;
     a.inten = inten, a.fmax = fmax, a.accum = accum, a.n_frames = n_frames, a.maxabs = mx;
     a.nonfinite = nonfinite;
-    a.k16 = k16;
+    a.tc_lo = tc_lo;
     a.tiles_z = (int)ceil_div(nz, TCG_TZ);
     a.tiles = (long long)a.tiles_z * ceil_div(nx, TCG_TX);
     a.items = a.tiles * ceil_div(n_frames, TCG_FB);
