@@ -174,8 +174,12 @@ __global__ void __launch_bounds__(256) k_split_planes(const float2 *__restrict__
 }
 
 struct TcgArgs {
-    CUtensorMap planes;      // 4-D map of the split trace planes: 32-sample windows
-    CUtensorMap planes16;    // the same planes, 16-sample windows (one K step)
+    // 4-D maps of the split trace planes: [0] 32-sample windows, [1] 16-sample
+    // windows (one K step); boxes of 8 frame groups, and of the last frame
+    // block's gt groups for the tail maps
+    CUtensorMap planes[2], tail[2];
+    int gt;                  // frame groups (of 8) in the last frame block
+    int nfb;                 // frame blocks
     const int *tc_lo;        // [tile][pair] window start * 2 + one-K-step flag (plan time, exact)
     int N, M, T;
     const double *ltx, *ltzT, *lrx, *lrzT, *w;
@@ -288,8 +292,10 @@ k_kk_gather_tc(const __grid_constant__ TcgArgs a) {
             tc::mbar_init(&tab_empty[s], 128 + 1); // weight rows + TMA issuer
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&a.planes)) : "memory");
-        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&a.planes16)) : "memory");
+        for (int i = 0; i < 2; ++i) {
+            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&a.planes[i])) : "memory");
+            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&a.tail[i])) : "memory");
+        }
     }
     for (int i = t; i < M; i += blockDim.x) w_s[i] = (a.w ? (float)__ldg(a.w + i) : 1.0f) * TCG_WSCALE;
     tc::fence_before_sync();
@@ -402,16 +408,19 @@ k_kk_gather_tc(const __grid_constant__ TcgArgs a) {
                 const int slot = k & 1;
                 tc::mbar_wait(&tab_full[slot], (k >> 1) & 1);
                 const int *lo = tcg_tables(tab_base + slot * slot_bytes, N, M).lo;
-                const int g0 = fb_of(k) * (TCG_FB / 8);
+                const int fb = fb_of(k), g0 = fb * (TCG_FB / 8);
+                const bool tl = fb == a.nfb - 1;
+                const uint32_t G = tl ? a.gt : TCG_FB / 8;
                 for (int pr = 0; pr < npairs; ++pr, ++P) {
                     const int st = (int)(P % TCG_NB);
                     const unsigned use = P / TCG_NB;
                     if (use > 0) tc::mbar_wait(&b_empty[st], (uint32_t)((use - 1) & 1));
                     const int v = lo[pr], one = v & 1;
                     b_k16[st] = one;  // published to the MMA warp by the arrive below
-                    mbar_arrive_tx(&b_full[st], one ? BSTAGE / 2 : BSTAGE);
-                    tma_4d(sm + TCG_NA * ASTAGE + st * BSTAGE, one ? &a.planes16 : &a.planes, 8 * (v >> 1), pr, g0, 0,
-                           &b_full[st]);
+                    // 4 planes x G groups x (16 or 32) samples x 16 B
+                    mbar_arrive_tx(&b_full[st], 4 * G * (one ? 16 : TCG_KW) * 16);
+                    tma_4d(sm + TCG_NA * ASTAGE + st * BSTAGE, tl ? &a.tail[one] : &a.planes[one], 8 * (v >> 1), pr,
+                           g0, 0, &b_full[st]);
                 }
                 mbar_arrive(&tab_empty[slot]);
             }
@@ -421,10 +430,12 @@ k_kk_gather_tc(const __grid_constant__ TcgArgs a) {
         // The whole warp runs the (warp-uniform) loop and one elected lane
         // issues a pair's six MMAs from one asm block: descriptors stay in
         // uniform registers, no per-MMA lane election.
-        const uint32_t idesc = tc::instr_desc(0, 128, 2 * TCG_FB, 1);
         const uint32_t s0 = (uint32_t)__cvta_generic_to_shared(sm);
         unsigned P = 0, G = 0;  // pairs and accumulator groups so far
         for (int k = 0; k < nit; ++k) {
+            // N = 16 x frame groups: re columns [0, 8g), im [8g, 16g)
+            const uint32_t g = fb_of(k) == a.nfb - 1 ? a.gt : TCG_FB / 8;
+            const uint32_t idesc = tc::instr_desc(0, 128, 16 * g, 1);
             for (int pr = 0; pr < npairs; ++pr, ++P) {
                 const int sa_ = (int)(P % TCG_NA), sb_ = (int)(P % TCG_NB), d = (int)(G % TCG_ND);
                 const bool first = pr % TCG_GROUP == 0, last = pr % TCG_GROUP == TCG_GROUP - 1 || pr == npairs - 1;
@@ -434,14 +445,15 @@ k_kk_gather_tc(const __grid_constant__ TcgArgs a) {
                 tc::fence_after_sync();
                 const uint32_t sa = s0 + sa_ * ASTAGE, sb = s0 + TCG_NA * ASTAGE + sb_ * BSTAGE;
                 const bool one = b_k16[sb_] != 0;
-                const uint64_t da = tc::smem_desc(sa, 128 * 16, 128);
+                // B: column groups of (16 or 32 samples) x 16 B; B lo after the 2g hi groups
+                const uint32_t kb = one ? 16 * 16 : TCG_KW * 16;
+                const uint64_t ah = tc::smem_desc(sa, 128 * 16, 128), al = tc::smem_desc(sa + A_PLANE, 128 * 16, 128);
+                const uint64_t bh = tc::smem_desc(sb, 128, kb), bl = tc::smem_desc(sb + 2 * g * kb, 128, kb);
                 if (tc::elect_one()) {
-                    if (one)  // 16-sample window: B planes of 16 x 256 B, one K step
-                        tc::mma_f16_split_step<A_PLANE, B_PLANE / 2>(tmem + d * 128, da, tc::smem_desc(sb, 128, 256),
-                                                                     idesc, !first);
-                    else
-                        tc::mma_f16_split_pair<A_PLANE, B_PLANE, 2 * 128 * 16, 2 * 128>(
-                            tmem + d * 128, da, tc::smem_desc(sb, 128, TCG_KW * 16), idesc, !first);
+                    tc::mma_f16_split3(tmem + d * 128, ah, al, bh, bl, idesc, !first);
+                    if (!one)  // second K = 16 half: A + 2 chunks, B + 2 K groups
+                        tc::mma_f16_split3(tmem + d * 128, ah + ((2 * 128 * 16) >> 4), al + ((2 * 128 * 16) >> 4),
+                                           bh + ((2 * 128) >> 4), bl + ((2 * 128) >> 4), idesc, true);
                     tc::commit(&a_empty[sa_]);
                     tc::commit(&b_empty[sb_]);
                     if (last) tc::commit(&dfull[d]);
@@ -460,20 +472,24 @@ k_kk_gather_tc(const __grid_constant__ TcgArgs a) {
             float S[2 * TCG_FB];
 #pragma unroll
             for (int c = 0; c < 2 * TCG_FB; ++c) S[c] = 0.f;
+            const uint32_t g = fb_of(k) == a.nfb - 1 ? a.gt : TCG_FB / 8;  // re [0, 8g), im [8g, 16g)
             for (int grp = 0; grp < ngroups; ++grp, ++G) {
                 const int d = (int)(G % TCG_ND);
                 tc::mbar_wait(&dfull[d], (uint32_t)((G / TCG_ND) & 1));
                 tc::fence_after_sync();
+                const uint32_t col = lane_base + d * 128;
 #pragma unroll
-                for (int c0 = 0; c0 < 2 * TCG_FB; c0 += 16) {
-                    float v[8], u[8];
-                    tc::tmem_ld8(lane_base + d * 128 + c0, v);
-                    tc::tmem_ld8(lane_base + d * 128 + c0 + 8, u);
-                    tc::tmem_ld_wait();
+                for (int c0 = 0; c0 < TCG_FB; c0 += 8) {
+                    if (c0 < 8 * (int)g) {  // warp-uniform
+                        float v[8], u[8];
+                        tc::tmem_ld8(col + c0, v);
+                        tc::tmem_ld8(col + 8 * g + c0, u);
+                        tc::tmem_ld_wait();
 #pragma unroll
-                    for (int i = 0; i < 8; ++i) {
-                        S[c0 + i] = __fadd_rn(S[c0 + i], v[i]);
-                        S[c0 + 8 + i] = __fadd_rn(S[c0 + 8 + i], u[i]);
+                        for (int i = 0; i < 8; ++i) {
+                            S[c0 + i] = __fadd_rn(S[c0 + i], v[i]);
+                            S[TCG_FB + c0 + i] = __fadd_rn(S[TCG_FB + c0 + i], u[i]);
+                        }
                     }
                 }
                 tc::fence_before_sync();
@@ -631,14 +647,17 @@ int kk_gather_tc(const float2 *data, int N, int M, int T, const double *ltx, con
         // (sample, frame) flattened: a window is one 512-byte row of the box
         const cuuint64_t dims[4] = {8ull * T, (cuuint64_t)NM, (cuuint64_t)ngroups, 4};
         const cuuint64_t strides[3] = {16ull * T, 16ull * T * NM, 16ull * T * NM * ngroups};
-        const cuuint32_t box[4] = {8 * TCG_KW, 1, 8, 4}, box16[4] = {8 * 16, 1, 8, 4}, estr[4] = {1, 1, 1, 1};
-        CUresult r = encode(&a.planes, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, planes, dims, strides, box, estr,
-                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-        if (r == CUDA_SUCCESS)
-            r = encode(&a.planes16, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, planes, dims, strides, box16, estr,
-                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        const cuuint32_t estr[4] = {1, 1, 1, 1};
+        a.nfb = (int)ceil_div(ngroups, TCG_FB / 8);
+        a.gt = (int)(ngroups - (long long)(a.nfb - 1) * (TCG_FB / 8));
+        CUresult r = CUDA_SUCCESS;
+        for (int one = 0; one < 2 && r == CUDA_SUCCESS; ++one)
+            for (int tl = 0; tl < 2 && r == CUDA_SUCCESS; ++tl) {
+                const cuuint32_t box[4] = {8u * (one ? 16u : (unsigned)TCG_KW), 1, tl ? (cuuint32_t)a.gt : 8u, 4};
+                r = encode(tl ? &a.tail[one] : &a.planes[one], CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, planes, dims,
+                           strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            }
         if (r != CUDA_SUCCESS) {
             set_error("kk tensor-core gather: cuTensorMapEncodeTiled failed (%d)", (int)r);
             return KKB_ERR_CUDA;
@@ -651,7 +670,7 @@ int kk_gather_tc(const float2 *data, int N, int M, int T, const double *ltx, con
     a.tc_lo = tc_lo;
     a.tiles_z = (int)ceil_div(nz, TCG_TZ);
     a.tiles = (long long)a.tiles_z * ceil_div(nx, TCG_TX);
-    a.items = a.tiles * ceil_div(n_frames, TCG_FB);
+    a.items = a.tiles * a.nfb;
     const unsigned grid = (unsigned)std::min<long long>(a.items, sm_count());
     if (linear) {
         KKB_TRY_CUDA(cudaFuncSetAttribute(k_kk_gather_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),

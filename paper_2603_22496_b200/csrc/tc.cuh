@@ -52,49 +52,19 @@ __device__ __forceinline__ void mma_f16(uint32_t d_tmem, uint64_t a, uint64_t b,
         "l"(a), "l"(b), "r"(idesc), "r"((uint32_t)accumulate));
 }
 
-// One K = 32 step of a split-fp16 product, hi*hi + hi*lo + lo*hi over two
-// K = 16 MMAs each (6 MMAs, one asm block): a = A hi descriptor (A lo at
-// +APL bytes, next K half at +AK), b = B hi descriptor (B lo at +BPL, next K
-// half at +BK).  accumulate = false overwrites D with the first product.
-template <int APL, int BPL, int AK, int BK>
-__device__ __forceinline__ void mma_f16_split_pair(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc,
-                                                   bool accumulate) {
+// One K = 16 step of a split-fp16 product, hi*hi + hi*lo + lo*hi, as three
+// MMAs from one asm block (descriptors of the A / B hi and lo halves);
+// accumulate = false overwrites D with the first product.
+__device__ __forceinline__ void mma_f16_split3(uint32_t d_tmem, uint64_t ah, uint64_t al, uint64_t bh, uint64_t bl,
+                                               uint32_t idesc, bool accumulate) {
     asm volatile(
-        "{\n\t.reg .pred p, q;\n\t.reg .b64 a1, a2, a3, b1, b2, b3;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
+        "{\n\t.reg .pred p, q;\n\t"
+        "setp.ne.b32 p, %6, 0;\n\t"
         "setp.eq.b32 q, 0, 0;\n\t"
-        "add.s64 b1, %2, %6;\n\t"
-        "add.s64 a1, %1, %5;\n\t"
-        "add.s64 a2, %1, %7;\n\t"
-        "add.s64 b2, %2, %8;\n\t"
-        "add.s64 a3, a2, %5;\n\t"
-        "add.s64 b3, b2, %6;\n\t"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, b1, %3, q;\n\t"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], a1, %2, %3, q;\n\t"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], a2, b2, %3, q;\n\t"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], a2, b3, %3, q;\n\t"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], a3, b2, %3, q;\n\t}\n" ::"r"(d_tmem),
-        "l"(a), "l"(b), "r"(idesc), "r"((uint32_t)accumulate), "n"((long long)(APL >> 4)),
-        "n"((long long)(BPL >> 4)), "n"((long long)(AK >> 4)), "n"((long long)(BK >> 4)));
-}
-
-// One K = 16 step of the same split product (3 MMAs): A hi x B hi,
-// A hi x B lo (B lo at +BPL bytes), A lo x B hi (A lo at +APL bytes).
-template <int APL, int BPL>
-__device__ __forceinline__ void mma_f16_split_step(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc,
-                                                   bool accumulate) {
-    asm volatile(
-        "{\n\t.reg .pred p, q;\n\t.reg .b64 a1, b1;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "setp.eq.b32 q, 0, 0;\n\t"
-        "add.s64 b1, %2, %6;\n\t"
-        "add.s64 a1, %1, %5;\n\t"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, b1, %3, q;\n\t"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], a1, %2, %3, q;\n\t}\n" ::"r"(d_tmem),
-        "l"(a), "l"(b), "r"(idesc), "r"((uint32_t)accumulate), "n"((long long)(APL >> 4)),
-        "n"((long long)(BPL >> 4)));
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %3, %5, p;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %4, %5, q;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %2, %3, %5, q;\n\t}\n" ::"r"(d_tmem),
+        "l"(ah), "l"(al), "l"(bh), "l"(bl), "r"(idesc), "r"((uint32_t)accumulate));
 }
 
 // one lane of the (converged) warp

@@ -1,18 +1,23 @@
-"""The K5 instance bench.py times, pinned to the oracle.
+"""The K5 instances bench.py times, pinned to the oracle.
 
-bench.py's step gathers 400 config-4 frames per launch, which dispatches to
-the 32 x 64-tile instance with two frames per CTA (KKB_KK_INST_BIG_FR).  A
-63-frame batch reaches it through the normal dispatch, 16- and 11-frame
-batches are forced onto it; the test asserts which instance ran (via
+bench.py's step gathers 400 config-4 frames per launch; linear batches of
+>= 48 frames dispatch to the tensor-core gather (KKB_KK_INST_TC,
+kk_gather_tc.cu), smaller ones to the FMA instances (wave model).  A
+63-frame batch reaches the tensor-core gather through the normal dispatch
+and the two-frames-per-CTA FMA instance (KKB_KK_INST_BIG_FR) when forced, as
+do 16- and 11-frame batches; the test asserts which instance ran (via
 kkb_kk_last_instance), and the odd frame counts make the last CTA run the
-one-frame tail.  Every frame is compared with
-the oracle (reference kk on the oracle's own decomposition) and with a
-single-frame launch of the same traces, which dispatches to the 16 x 16
-instance: the per-pixel sums run in the same order, so they must agree bit
-for bit.
+one-frame tail.  Every frame is compared with the oracle (reference kk on
+the oracle's own decomposition) and with a single-frame launch of the same
+traces through the same kind of gather (16 x 16 FMA instance, or the
+tensor-core gather forced): a pixel's sum runs in the same order whatever
+the batch, so they must agree bit for bit.  The tensor-core gather's NaN /
+Inf standby (the FMA gather runs instead) and its intensity / frame-max
+epilogue are covered too.
 
 Tolerances: IQ rel L2 <= 1e-5 per frame (north star); batch vs single
-frame and instance vs instance: bit-exact.
+frame and FMA instance vs FMA instance: bit-exact; tensor-core vs FMA
+gather: rel L2 <= 2e-6 (split-fp16 products, measured ~5e-7).
 """
 
 import numpy as np
@@ -33,11 +38,13 @@ def _frames(w, F, seed0):
                      for f in range(F)])
 
 
-@pytest.mark.parametrize("F,force", [(63, None), (16, "big_fr"), (11, "big_fr")])
-def test_bench_instance_matches_oracle_every_frame(oracle, monkeypatch, F, force):
-    """63 frames reach the two-frames-per-CTA instance through the default
-    dispatch (odd: the last CTA runs the one-frame tail); 16 and 11 frames are
-    forced onto it (KKB_KK_INST=big_fr)."""
+@pytest.mark.parametrize("F,force,want", [(63, None, _lib.KKB_KK_INST_TC), (63, "big_fr", _lib.KKB_KK_INST_BIG_FR),
+                                          (16, "big_fr", _lib.KKB_KK_INST_BIG_FR),
+                                          (11, "big_fr", _lib.KKB_KK_INST_BIG_FR)])
+def test_bench_instance_matches_oracle_every_frame(oracle, monkeypatch, F, force, want):
+    """63 frames reach the tensor-core gather through the default dispatch;
+    63, 16 and 11 frames forced onto the two-frames-per-CTA FMA instance
+    (odd: the last CTA runs the one-frame tail)."""
     import torch
 
     w = configs.config4(frames=F)
@@ -50,16 +57,20 @@ def test_bench_instance_matches_oracle_every_frame(oracle, monkeypatch, F, force
     iq = eng.run(torch.from_numpy(rf).cuda()).clone()
     torch.cuda.synchronize()
     monkeypatch.delenv("KKB_KK_INST", raising=False)
-    assert _lib.last_instance() == _lib.KKB_KK_INST_BIG_FR
+    assert _lib.last_instance() == want
     assert _lib.take_device_error() == 0
-    # every frame again as a one-frame launch (16 x 16 instance): bit-identical
+    # every frame again as a one-frame launch of the same kind of gather
+    tc = want == _lib.KKB_KK_INST_TC
+    if tc:
+        monkeypatch.setenv("KKB_KK_INST", "tc")
     P = g.nx * g.nz
     single = torch.empty_like(iq)
     for f in range(F):
         _lib.call("kkb_kk_plan_run", eng._kk, dev.ptr(eng.traces[f]), 1, 0, dev.ptr(single[f]),
                   _lib.KKB_OUT_C64, P, None, None, dev.stream_handle())
     torch.cuda.synchronize()
-    assert _lib.last_instance() == _lib.KKB_KK_INST_SMALL
+    monkeypatch.delenv("KKB_KK_INST", raising=False)
+    assert _lib.last_instance() == (_lib.KKB_KK_INST_TC if tc else _lib.KKB_KK_INST_SMALL)
     assert torch.equal(iq, single)
     # every frame against the oracle: reference kk on the oracle's decomposition
     luts = oracle.kk_luts(g.x, g.z, p.transmit_angles, rx.angles, c)
@@ -101,30 +112,33 @@ def test_every_instance_bit_identical(monkeypatch):
     eng.close()
 
 
-def test_dispatch_follows_the_wave_model():
-    """The default dispatch (wave model, kk_gather.cu select_instance) on the
-    measured shapes: bench workload -> two frames per CTA; one config-1 frame
-    -> 16 x 16 tiles; one config-5 frame -> 32 x 64 tiles."""
+def test_dispatch_follows_the_wave_model(monkeypatch):
+    """The default dispatch on the measured shapes: the bench workload (400
+    linear frames) -> the tensor-core gather, or with KKB_KK_TC=0 the wave
+    model's choice (kk_gather.cu select_instance), two frames per CTA; one
+    config-1 frame -> 16 x 16 tiles; one config-5 frame -> 32 x 64 tiles."""
     import torch
 
-    for cfg, F, want in ((4, 400, _lib.KKB_KK_INST_BIG_FR), (1, 1, _lib.KKB_KK_INST_SMALL),
-                         (5, 1, _lib.KKB_KK_INST_BIG)):
+    for cfg, F, tc, want in ((4, 400, True, _lib.KKB_KK_INST_TC), (4, 400, False, _lib.KKB_KK_INST_BIG_FR),
+                             (1, 1, True, _lib.KKB_KK_INST_SMALL), (5, 1, True, _lib.KKB_KK_INST_BIG)):
+        if not tc:
+            monkeypatch.setenv("KKB_KK_TC", "0")
         w = configs.config4(frames=F) if cfg == 4 else configs.CONFIGS[cfg]()
         p, arr, rx, g = w.params, w.array, w.receive, w.grid
         eng = kb.KKEngine(arr, p, rx, g, frames=F, want_db=False)
         eng.traces.zero_()
         eng.gather()
         torch.cuda.synchronize()
+        monkeypatch.delenv("KKB_KK_TC", raising=False)
         assert _lib.last_instance() == want, (cfg, F, _lib.last_instance())
         eng.close()
 
 
-def test_tensor_core_gather_experiment_matches_oracle(oracle, monkeypatch):
-    """The opt-in tcgen05 gather (KKB_KK_INST=tc; slower than the FMA
-    instances, kept as the measured experiment of DESIGN.md): a 32-frame
-    config-4 batch within 1e-5 rel L2 of the oracle per frame, and each frame
-    independent of the batch it is gathered in (rel 0 between a batch and
-    single-frame tensor-core launches is not required: only the 1e-5 bound)."""
+@pytest.mark.parametrize("linear", [True, False])
+def test_tensor_core_gather_matches_oracle(oracle, monkeypatch, linear):
+    """The tcgen05 gather forced on a 32-frame config-4 batch (below the
+    default crossover), linear and nearest: within 1e-5 rel L2 of the
+    oracle per frame."""
     import torch
 
     F = 32
@@ -132,7 +146,7 @@ def test_tensor_core_gather_experiment_matches_oracle(oracle, monkeypatch):
     arr, p, rx, g = w.array, w.params, w.receive, w.grid
     fs, c = arr.sampling_frequency, p.sound_speed
     rf = _frames(w, F, 900)
-    eng = kb.KKEngine(arr, p, rx, g, frames=F, want_db=False)
+    eng = kb.KKEngine(arr, p, rx, g, frames=F, want_db=False, interpolation="linear" if linear else "nearest")
     eng.decompose(torch.from_numpy(rf).cuda())
     monkeypatch.setenv("KKB_KK_INST", "tc")
     eng.gather()
@@ -145,6 +159,68 @@ def test_tensor_core_gather_experiment_matches_oracle(oracle, monkeypatch):
     shift = (0.0 - p.start_time) * fs
     for f in (0, 7, 31):
         tr = oracle.decompose_f64(rf[f], fs, arr.positions, rx.angles, c)
-        ref = oracle.kk_kernel(tr, *luts, np.ones(rx.num_angles), fs, shift)
+        ref = oracle.kk_kernel(tr, *luts, np.ones(rx.num_angles), fs, shift, linear=linear)
         assert rel_l2(got[f], ref) <= 1e-5, f
+    eng.close()
+
+
+def test_tensor_core_epilogue_matches_fma(monkeypatch):
+    """Intensity |IQ|^2 and the per-frame max (the dB path's inputs) from the
+    tensor-core gather against the FMA gather on a 100-frame batch (a 36-frame
+    tail block): rel L2 <= 2e-6 per frame, frame max within 4e-6."""
+    import torch
+
+    F = 100
+    w = configs.config4(frames=F)
+    p, arr, g = w.params, w.array, w.grid
+    rf = _frames(w, F, 1200)
+    eng = kb.KKEngine(arr, p, w.receive, g, frames=F, want_db=True)
+    eng.decompose(torch.from_numpy(rf).cuda())
+    outs = {}
+    for tc in ("1", "0"):
+        monkeypatch.setenv("KKB_KK_TC", tc)
+        eng.gather()
+        torch.cuda.synchronize()
+        outs[tc] = (_lib.last_instance(), eng.iq.clone(), eng.inten.clone(),
+                    eng.fmax.clone().view(torch.float32))
+    monkeypatch.delenv("KKB_KK_TC")
+    assert outs["1"][0] == _lib.KKB_KK_INST_TC and outs["0"][0] == _lib.KKB_KK_INST_BIG_FR
+    for a, b in zip(outs["1"][1:3], outs["0"][1:3]):
+        for f in range(F):
+            e = float((torch.linalg.vector_norm(a[f] - b[f]) / torch.linalg.vector_norm(b[f])).item())
+            assert e <= 2e-6, (f, e)
+    ft, ff = outs["1"][3], outs["0"][3]
+    assert bool(((ft - ff).abs() <= 4e-6 * ff.abs()).all())
+
+
+def test_tensor_core_nonfinite_standby(monkeypatch):
+    """A NaN and an Inf sample in a 64-frame batch: the tensor-core gather
+    stands down on the device and the FMA standby computes the batch, so the
+    image (NaN / Inf pattern included) is bit-identical to the FMA gather's,
+    where the reference spreads a non-finite sample only to the pixels that
+    tap it."""
+    import torch
+
+    F = 64
+    w = configs.config4(frames=F)
+    p, arr, g = w.params, w.array, w.grid
+    rf = _frames(w, F, 1500)
+    eng = kb.KKEngine(arr, p, w.receive, g, frames=F, want_db=False)
+    eng.decompose(torch.from_numpy(rf).cuda())
+    eng.traces[5, 3, 4, 700] = float("nan")
+    eng.traces[40, 0, 10, 300] = complex(float("inf"), 0.0)
+    outs = {}
+    for tc in ("1", "0"):
+        monkeypatch.setenv("KKB_KK_TC", tc)
+        eng.gather()
+        torch.cuda.synchronize()
+        outs[tc] = (_lib.last_instance(), eng.iq.clone())
+    monkeypatch.delenv("KKB_KK_TC")
+    assert outs["1"][0] == _lib.KKB_KK_INST_TC
+    a, b = outs["1"][1], outs["0"][1]
+    assert bool(torch.isnan(b.real).any() | torch.isnan(b.imag).any())
+    va, vb = torch.view_as_real(a), torch.view_as_real(b)
+    assert torch.equal(torch.isnan(va), torch.isnan(vb))
+    m = ~torch.isnan(vb)
+    assert torch.equal(va[m], vb[m])
     eng.close()
