@@ -602,6 +602,21 @@ int kk_gather_tc(const float2 *data, int N, int M, int T, const double *ltx, con
         set_error("kk tensor-core gather: %d pairs do not fit shared memory", NM);
         return KKB_ERR_UNSUPPORTED;
     }
+    // The split planes are the size of the traces (~600 MB for the bench
+    // batch).  Keep freed stream-ordered blocks in the device's pool across
+    // synchronisations (default release threshold 0 hands them back to the
+    // driver at every sync, and remapping them costs milliseconds per call).
+    static int pool_kept = -1;
+    if (pool_kept < 0) {
+        int dev = 0;
+        cudaMemPool_t pool;
+        pool_kept = cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess;
+        if (pool_kept) {
+            unsigned long long keep = ~0ull;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        }
+        cudaGetLastError();
+    }
     unsigned *mx = nullptr;  // [n_frames] frame max, then the non-finite flag
     __half *planes = nullptr;
     KKB_TRY_CUDA(cudaMallocAsync(&mx, sizeof(unsigned) * ((size_t)n_frames + 1), s), "cudaMallocAsync(frame max)");
