@@ -14,31 +14,37 @@
 // the plan (k_kk_tc_windows, kk_gather.cu): every pixel of the tile evaluated
 // with this same arithmetic, so the window provably holds every live tap.
 //
-// Operands: one tcgen05.mma (kind::f16, M = 128 pixels, N = 128 = re | im of
-// 64 frames, K = 16 samples) per 16 window samples and split term.  Every
-// operand is split into two fp16 halves x = hi + lo and the product sums
+// Operands: per K = 16 window samples three tcgen05.mma (kind::f16, M = 128
+// pixels, N = 16 x frame groups = re | im of up to 64 frames): every operand
+// is split into two fp16 halves x = hi + lo and the product sums
 // hi*hi + hi*lo + lo*hi (lo*lo ~ 2^-22 dropped).  The traces are split ONCE
 // per batch (k_split_planes: each frame scaled by a power of two so its
 // largest sample sits just under 2^15) into four planes (hi/lo x re/im) laid
-// out [frame group of 8][pair][sample][8 frames]: one 4-D TMA box (32 samples
-// x 8 frames as one 512-byte row x 8 groups x 4 planes = 16 KB, cp.async.bulk.tensor)
-// lands a pair's window for 64 frames directly in the MN-major operand layout,
-// zero-filled where the window leaves the trace (the reference's out-of-window
-// taps carry zero weight anyway).  Weights are scaled by 2^12 so their low
-// halves stay normal.
+// out [frame group of 8][pair][sample][8 frames]: one 4-D TMA box (16 or 32
+// samples x 8 frames as one row x 8 groups x 4 planes, cp.async.bulk.tensor)
+// lands a pair's window for 64 frames directly in the MN-major operand
+// layout, zero-filled where the window leaves the trace.  Weights are scaled
+// by 2^12 so their low halves stay normal.  A batch holding a NaN / Inf
+// sample is left to the FMA gather (the standby launch in kk_gather.cu): a
+// tensor-core product would multiply it by the zero weights of every other
+// pixel of the tile, where the reference touches only the pixels that tap it.
 //
 // Accumulation: tensor-core adds into a TMEM accumulator truncate (measured,
 // scripts/ubench/tc_accum.cu: ~3e-8 relative drift per MMA), so pairs are
-// summed in groups of 8 into two ping-pong TMEM accumulators, and four drain
-// warps add each finished group into float32 registers with round-to-nearest
-// adds: the drift is bounded by one group's 48 MMAs.
+// summed in groups of TCG_GROUP = 16 into four rotating TMEM accumulators,
+// and four drain warps add each finished group into float32 registers with
+// round-to-nearest adds: the drift is bounded by one group's <= 96 MMAs
+// (measured 9e-7 rel L2 against the FMA gather on the bench batch; groups of
+// 8: 5e-7 and 11% slower, of 32: 1.7e-6 and 1% faster;
+// profiles/r02_gather_tc_sweep.jsonl).
 //
-// Warp roles (10 warps): 0-3 build the weight rows of each pair (one row per
-// thread, delay tables staged in shared memory); 4 allocates TMEM and issues
-// the TMA copies (one lane); 5 issues
-// the MMAs (one lane); 6-9 drain the accumulators and run the epilogue (IQ,
-// fused |IQ|^2, per-frame max).  Stages are guarded by full / empty
-// mbarriers (tcgen05.commit frees a stage and publishes a group).
+// Warp roles (11 warps, persistent CTAs): 0-3 build the weight rows of each
+// pair (one row per thread, delay tables staged in shared memory); 4
+// allocates TMEM and issues the TMA copies (one lane); 5 issues the MMAs
+// (one elected lane); 6-9 drain the accumulators and run the epilogue (IQ,
+// fused |IQ|^2, per-frame max); 10 builds the next item's tile tables.
+// Stages are guarded by full / empty mbarriers (tcgen05.commit frees a stage
+// and publishes a group).
 
 #include <algorithm>
 #include <cuda.h>
@@ -64,7 +70,7 @@ __device__ __forceinline__ double tc_kk_delay(double t1, double lz, double lx, d
 #define TCG_NA 4               // weight (A) stages
 #define TCG_NB 8               // trace-window (B) stages (they hide the TMA latency)
 #define TCG_PB 2               // pairs per producer iteration
-#define TCG_GROUP 8            // pairs per accumulator group
+#define TCG_GROUP 16           // pairs per accumulator group
 #define TCG_ND 4               // TMEM accumulators (128 columns each)
 #define TCG_THREADS 352        // 11 warps
 

@@ -17,7 +17,8 @@ epilogue are covered too.
 
 Tolerances: IQ rel L2 <= 1e-5 per frame (north star); batch vs single
 frame and FMA instance vs FMA instance: bit-exact; tensor-core vs FMA
-gather: rel L2 <= 2e-6 (split-fp16 products, measured ~5e-7).
+gather: IQ rel L2 <= 3e-6 per frame (split-fp16 products, measured ~9e-7),
+|IQ|^2 <= 6e-6 (twice the relative error of IQ).
 """
 
 import numpy as np
@@ -167,7 +168,8 @@ def test_tensor_core_gather_matches_oracle(oracle, monkeypatch, linear):
 def test_tensor_core_epilogue_matches_fma(monkeypatch):
     """Intensity |IQ|^2 and the per-frame max (the dB path's inputs) from the
     tensor-core gather against the FMA gather on a 100-frame batch (a 36-frame
-    tail block): rel L2 <= 2e-6 per frame, frame max within 4e-6."""
+    tail block): IQ rel L2 <= 3e-6 and intensity <= 6e-6 per frame, frame max
+    within 1e-5."""
     import torch
 
     F = 100
@@ -185,12 +187,12 @@ def test_tensor_core_epilogue_matches_fma(monkeypatch):
                     eng.fmax.clone().view(torch.float32))
     monkeypatch.delenv("KKB_KK_TC")
     assert outs["1"][0] == _lib.KKB_KK_INST_TC and outs["0"][0] == _lib.KKB_KK_INST_BIG_FR
-    for a, b in zip(outs["1"][1:3], outs["0"][1:3]):
+    for a, b, tol in zip(outs["1"][1:3], outs["0"][1:3], (3e-6, 6e-6)):
         for f in range(F):
             e = float((torch.linalg.vector_norm(a[f] - b[f]) / torch.linalg.vector_norm(b[f])).item())
-            assert e <= 2e-6, (f, e)
+            assert e <= tol, (f, e, tol)
     ft, ff = outs["1"][3], outs["0"][3]
-    assert bool(((ft - ff).abs() <= 4e-6 * ff.abs()).all())
+    assert bool(((ft - ff).abs() <= 1e-5 * ff.abs()).all())
 
 
 def test_tensor_core_nonfinite_standby(monkeypatch):
