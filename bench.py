@@ -257,6 +257,17 @@ def _l2_roofline(achieved_taps):
                     "serving every pixel of the tile that reads it"}
 
 
+def _tensor_peak():
+    """Dense bf16/f16 tensor peak (MEASURED_PEAKS.json, driver-written): the
+    sustained figure, the gather being timed inside a multi-kernel step."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p.get("bf16_tflops_sustained") or p["bf16_tflops"]), "measured (sustained bf16 matmul)"
+    except Exception:
+        return 2250.0, "fallback (nominal dense bf16)"
+
+
 def run_gpu(args):
     import torch
     import torch.distributed as dist
@@ -409,6 +420,13 @@ def run_gpu(args):
     smem_derived = sm_count * 128 * sm_mhz * 1e6 / 1e9          # GB/s, 128 B/clk/SM crossbar
     smem_peak = smem_meas or smem_derived
     achieved_taps = gather_bytes_alg / (kk_launch_ms / 1e3) / 1e9
+    # which K5 ran (the sequential passes above): the tensor-core gather's work
+    # is its split-fp16 MMAs, 3 per K = 16 step of 128 pixels x 16 columns
+    # (re | im of 8 frames) x 16 samples, ksteps per group of 8 frames
+    k5_inst = _lib.KKB_KK_INST_NAMES.get(_lib.last_instance() & 15, "?")
+    tc_ksteps = int(_lib.load().kkb_kk_plan_tc_ksteps(eng._kk)) if k5_inst == "tc" else -1
+    tc_flops = tc_ksteps * math.ceil(fl / 8) * 3 * 2.0 * 128 * 16 * 16 if tc_ksteps > 0 else None
+    tensor_peak, tensor_kind = _tensor_peak()
     # stage 1 (K1-K3) is HBM-bound: bytes its three kernels must move per batch
     # (RF in, spectra written then read, contracted bins written then read,
     # traces out) and the two-array compulsory minimum (RF in + traces out)
@@ -493,10 +511,26 @@ def run_gpu(args):
             "value_int16_ingest": {"value": world * F / (q_ms / 1e3), "unit": UNIT, "ms_per_step": q_ms,
                                    "note": "same device-resident step on int16-quantised RF "
                                            "(converted exactly in the FFT load)"},
-            # the binding roofline of the dominant kernel: K5's taps come from
-            # shared memory (16 B of taps per pixel-pair), against the
-            # measured LDS.128 peak; HBM and L2 figures are secondary
-            "roofline": {"kernel": "k_kk_gather", "bound": "smem",
+            # the dominant kernel's roofline.  The tensor-core gather (the bench
+            # dispatch): its split-fp16 MMA work against the measured tensor
+            # peak.  The FMA gather: its taps against the measured LDS.128 peak
+            # (both kept: "taps_roofline" is the algorithmic on-chip figure)
+            "roofline": ({"kernel": "k_kk_gather_tc", "bound": "tensor",
+                          "achieved": tc_flops / (kk_launch_ms / 1e3) / 1e12, "peak": tensor_peak,
+                          "unit": "TFLOP/s", "frac": tc_flops / (kk_launch_ms / 1e3) / 1e12 / tensor_peak,
+                          "traffic": _gather_traffic(fl), "launch_ms": kk_launch_ms,
+                          "frames_per_launch": fl, "flops_per_launch": tc_flops,
+                          "k_steps_per_frame_group": tc_ksteps,
+                          "flops": "issued split-fp16 MMA work of the gather's GEMM form: 3 products "
+                                   "(hi*hi, hi*lo, lo*hi) x 2*128*16*16 per K = 16 step, one or two "
+                                   "steps per (tile, pair) from the plan's exact windows "
+                                   "(kkb_kk_plan_tc_ksteps), per group of 8 frames; the direct form's "
+                                   "algorithmic work is the taps below",
+                          "peak_kind": tensor_kind,
+                          "launch_note": "launch_ms spans the K5 call: the per-frame max and plane "
+                                         "split passes plus the gather (profiles/r02b_launches_"
+                                         "bench_default.csv has each kernel's share)"}
+                         if tc_flops else {"kernel": "k_kk_gather_tc" if tc_flops else "k_kk_gather", "bound": "smem",
                          "achieved": achieved_taps, "peak": smem_peak, "unit": "GB/s",
                          "frac": achieved_taps / smem_peak, "traffic": _gather_traffic(fl),
                          "launch_ms": kk_launch_ms, "frames_per_launch": fl,
@@ -509,10 +543,28 @@ def run_gpu(args):
                          "peak_derived_at_sampled_clock": smem_derived,
                          "pixel_pairs_per_s": pp_frame * fl / (kk_launch_ms / 1e3),
                          "pixel_pairs_per_s_isolated": pp_frame * F / (kk_ms / 1e3),
-                         "traffic_note": "ncu dram read+write per launch (newest profiles/r*_gather_traffic.json); "
-                                         "below the compulsory HBM bytes because the gather reads only "
-                                         "the trace samples the image's delays reach"},
-            "hbm_roofline": {"kernel": "k_kk_gather", "bound": "hbm",
+                         "traffic_note": "ncu dram read+write per launch of the gather kernel (newest "
+                                         "profiles/r*_gather_traffic.json); below the compulsory HBM "
+                                         "bytes because the gather reads only the trace samples the "
+                                         "image's delays reach"}),
+            "taps_roofline": {"kernel": "k_kk_gather_tc" if tc_flops else "k_kk_gather", "bound": "smem",
+                         "achieved": achieved_taps, "peak": smem_peak, "unit": "GB/s",
+                         "frac": achieved_taps / smem_peak, "traffic": _gather_traffic(fl),
+                         "launch_ms": kk_launch_ms, "frames_per_launch": fl,
+                         "algorithmic_bytes_per_launch": gather_bytes_alg,
+                         "algorithmic_bytes": "16 B of taps (two complex64 samples) per pixel-pair "
+                                              "(SURVEY 8d) x pixel-pairs per launch",
+                         "peak_kind": (f"{onchip_kind} (scripts/ubench/peaks.cu: conflict-free LDS.128 "
+                                       "on every SM, profiles/r02_onchip_peaks.json)") if smem_meas else
+                                      "derived (148 SMs x 128 B/clk x sampled SM clock)",
+                         "peak_derived_at_sampled_clock": smem_derived,
+                         "pixel_pairs_per_s": pp_frame * fl / (kk_launch_ms / 1e3),
+                         "pixel_pairs_per_s_isolated": pp_frame * F / (kk_ms / 1e3),
+                         "traffic_note": "ncu dram read+write per launch of the gather kernel (newest "
+                                         "profiles/r*_gather_traffic.json); below the compulsory HBM "
+                                         "bytes because the gather reads only the trace samples the "
+                                         "image's delays reach"},
+            "hbm_roofline": {"kernel": "k_kk_gather_tc" if tc_flops else "k_kk_gather", "bound": "hbm",
                              "achieved": achieved_hbm, "peak": hbm_peak, "unit": "GB/s",
                              "frac": achieved_hbm / hbm_peak, "peak_kind": peak_kind,
                              "algorithmic_bytes_per_launch": compulsory,

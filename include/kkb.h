@@ -159,6 +159,12 @@ int kkb_kk_plan_window(const kkb_kk_plan *p);
  * would clamp a tap (the dispatch then never uses it, and
  * KKB_DEVERR_KK_WINDOW is raised).  0 = every tiled instance proven. */
 int kkb_kk_plan_window_check(const kkb_kk_plan *p);
+/* Tensor-core gather work of the plan: the number of K = 16 MMA steps (1 or 2
+ * per tile and pair, from the plan's exact per-tile windows) one group of 8
+ * frames takes; -1 when the plan is not eligible for the tensor-core gather
+ * (tile windows beyond 32 samples).  A launch of F frames issues
+ * ksteps x ceil(F/8) x 3 MMAs of 128 x 16 x 16 (M x N x K) per group. */
+long long kkb_kk_plan_tc_ksteps(const kkb_kk_plan *p);
 /* K5 instance the last kk launch of this process dispatched to (any plan,
  * any thread): the per-pixel kernel, or the tiled kernel with 16x16 / 32x32
  * / 32x64 pixel tiles, the last one with one or KKB_KK_FR (2) frames per CTA;

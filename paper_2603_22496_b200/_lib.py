@@ -42,6 +42,7 @@ SIGNATURES = {
     "kkb_kk_plan_window": [P],
     "kkb_kk_last_instance": [],
     "kkb_kk_plan_window_check": [P],
+    "kkb_kk_plan_tc_ksteps": [P],
     "kkb_kk_plan_destroy": [P],
     "kkb_kk_taps": [P, P, P, P, I, I, I, I, I, D, D, I, P, P],
     "kkb_das": [P, I, I, I, P, P, P, I, P, P, P, P, P, D, P, D, D, I, I, I, P, I, P],
@@ -79,6 +80,7 @@ SIGNATURES = {
     "kkb_ipc_close_handle": [P],
 }
 _RESTYPES = {
+    "kkb_kk_plan_tc_ksteps": LL,
     "kkb_version": ctypes.c_char_p,
     "kkb_last_error": ctypes.c_char_p,
     "kkb_launch_count": LL,

@@ -209,6 +209,8 @@ extern "C" int kkb_kk_plan_window(const kkb_kk_plan *p) { return p ? p->win.big 
 
 extern "C" int kkb_kk_plan_window_check(const kkb_kk_plan *p) { return p ? p->win.bad : -1; }
 
+extern "C" long long kkb_kk_plan_tc_ksteps(const kkb_kk_plan *p) { return p ? p->win.tc_ksteps : -1; }
+
 extern "C" int kkb_kk_last_instance(void) { return kk_last_instance(); }
 
 extern "C" int kkb_kk_plan_run_strided(kkb_kk_plan *p, const void *data, int n_frames,

@@ -71,6 +71,9 @@ struct KKWindows {
     // first 16 samples (one K = 16 step); device, owned by the plan; null when
     // the tensor-core gather cannot take the plan
     int *tc_lo;
+    // sum over (tile, pair) of the K = 16 steps one frame group takes (1 or 2
+    // each): the tensor-core work of a launch (-1: not eligible)
+    long long tc_ksteps;
 };
 // Synchronises `s` (one launch for the three tile sizes).
 int kk_window(const double *ltx, const double *ltz, const double *lrx, const double *lrz, int N,

@@ -918,6 +918,7 @@ int kk_check_windows(const double *ltx, const double *ltz, const double *lrx, co
                      KKWindows *win, cudaStream_t s) {
     win->bad = 0;
     win->tc_lo = nullptr;
+    win->tc_ksteps = -1;
     if ((size_t)M * sizeof(int) > 48 * 1024) return KKB_OK;  // huge pair tables: no tile fits anyway
     int *d = nullptr;
     // d[0]: failed tile sizes; d[1]: the tensor-core windows exceed 32 samples
@@ -962,9 +963,19 @@ int kk_check_windows(const double *ltx, const double *ltz, const double *lrx, co
     // a tile size that failed disables its instances (big covers both frame counts)
     const int h = hh[0];
     win->bad = h | ((h & (1 << KKB_KK_INST_BIG)) ? (1 << KKB_KK_INST_BIG_FR) : 0);
+    win->tc_ksteps = -1;
     if (hh[1] && win->tc_lo) {  // too steep for the tensor-core tile: not eligible (not an error)
         cudaFree(win->tc_lo);
         win->tc_lo = nullptr;
+    }
+    if (win->tc_lo) {  // the K-step count (bench's tensor roofline, kkb_kk_plan_tc_ksteps)
+        const size_t ntc = (size_t)(ceil_div(nz, KKB_KK_TC_TZ) * ceil_div(nx, KKB_KK_TC_TX)) * N * M;
+        std::vector<int> h(ntc);
+        if (cudaMemcpy(h.data(), win->tc_lo, sizeof(int) * ntc, cudaMemcpyDeviceToHost) == cudaSuccess) {
+            long long k = 0;
+            for (int v : h) k += (v & 1) ? 1 : 2;
+            win->tc_ksteps = k;
+        }
     }
     return KKB_OK;
 }

@@ -5,6 +5,6 @@ if [ "$1" = launches ]; then
   ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launch.log 2>&1
 else
   ncu --set full --clock-control none --import-source on \
-      -k regex:"k_kk_gather|k_r2c|k_contract|k_c2c|k_log_compress" -s 15 -c 5 -f -o gpurun_out/prof_round $CMD > gpurun_out/ncu_full.log 2>&1
+      -k regex:"k_kk_gather|k_r2c|k_contract|k_c2c|k_log_compress|k_split_planes|k_frame_maxabs" -s 24 -c 8 -f -o gpurun_out/prof_round $CMD > gpurun_out/ncu_full.log 2>&1
 fi
 echo "ncu rc=$?"

@@ -226,3 +226,46 @@ def test_tensor_core_nonfinite_standby(monkeypatch):
     m = ~torch.isnan(vb)
     assert torch.equal(va[m], vb[m])
     eng.close()
+
+
+def test_bench_workload_tensor_core_gather(oracle, monkeypatch):
+    """The exact configuration bench.py times: 400 config-4 frames in one
+    launch (seven 64-frame blocks, the last of 2 frame groups), through the
+    default dispatch -> the tensor-core gather.  Every frame against the
+    oracle-pinned FMA gather (KKB_KK_TC=0 -> big_fr), sampled frames against
+    the oracle itself, and repeated input frames (8 distinct frames tiled, as
+    in bench.py) bit-identical wherever they sit in the batch."""
+    import torch
+
+    F, D = 400, 8
+    w = configs.config4(frames=F)
+    arr, p, rx, g = w.array, w.params, w.receive, w.grid
+    fs, c = arr.sampling_frequency, p.sound_speed
+    base = _frames(w, D, 2000)
+    eng = kb.KKEngine(arr, p, rx, g, frames=F, want_db=True)
+    rf = torch.from_numpy(base).cuda().repeat(F // D, 1, 1, 1)
+    eng.decompose(rf)
+    del rf
+    outs = {}
+    for tc in ("1", "0"):
+        monkeypatch.setenv("KKB_KK_TC", tc)
+        eng.gather()
+        torch.cuda.synchronize()
+        outs[tc] = (_lib.last_instance(), eng.iq.clone())
+    monkeypatch.delenv("KKB_KK_TC")
+    assert outs["1"][0] == _lib.KKB_KK_INST_TC and outs["0"][0] == _lib.KKB_KK_INST_BIG_FR
+    assert _lib.take_device_error() == 0
+    a, b = outs["1"][1], outs["0"][1]
+    for f in range(F):
+        e = float((torch.linalg.vector_norm(a[f] - b[f]) / torch.linalg.vector_norm(b[f])).item())
+        assert e <= 3e-6, (f, e)
+    for f in range(D, F):
+        assert torch.equal(a[f], a[f % D]), f
+    luts = oracle.kk_luts(g.x, g.z, p.transmit_angles, rx.angles, c)
+    shift = (0.0 - p.start_time) * fs
+    got = a.cpu().numpy()
+    for f in (0, 63, 64, 383, 384, 399):
+        tr = oracle.decompose_f64(base[f % D], fs, arr.positions, rx.angles, c)
+        ref = oracle.kk_kernel(tr, *luts, np.ones(rx.num_angles), fs, shift)
+        assert rel_l2(got[f], ref) <= 1e-5, f
+    eng.close()
