@@ -295,6 +295,22 @@ int kkb_decomposer_contraction(const kkb_decomposer *p);
  * spin that timed out (1), which would mean a scheduling failure. */
 int kkb_decomposer_set_ring(kkb_decomposer *p, int slots, int consumer_ctas);
 int kkb_decomposer_ring_error(kkb_decomposer *p, int *flag);
+/* One stage of stage 1 at a time, for the reference's staged benchmark
+ * (kkbeam.bench._kk_stage_fns, bench.py:113-153): stage 0 the real FFT of rf
+ * ((F, N, L, T) float32) into the plan's spectra ("reorg_fft"), 1 the
+ * contraction with the one-sided weights folded into the cached ramps
+ * ("hilbert_compress"), 2 the inverse FFT into traces ((F, N, M, T)
+ * complex64, "ifft").  Same launches and results as kkb_decomposer_run;
+ * F <= the plan's max_frames, stages in order 0, 1, 2 on one stream. */
+int kkb_decomposer_run_stage(kkb_decomposer *p, int stage, const float *rf, int n_frames, void *traces,
+                             void *stream);
+/* analytic_signal one stage at a time (the staged DAS benchmark,
+ * kkbeam.bench._das_stage_fns, bench.py:91-110): stage 0 real FFT of rf
+ * ((n_traces, T) float32) into spec ((n_traces, T/2 + 1) complex64, caller
+ * scratch), 1 one-sided weights / T applied to spec in place, 2 inverse FFT
+ * into out ((n_traces, T) complex64).  0 + 1 + 2 == kkb_analytic_signal. */
+int kkb_analytic_signal_stage(int stage, const float *rf, long long n_traces, int n_t, void *spec, void *out,
+                              void *stream);
 /* bytes of device scratch held by the plan */
 long long kkb_decomposer_workspace_bytes(const kkb_decomposer *p);
 int kkb_decomposer_destroy(kkb_decomposer *p);

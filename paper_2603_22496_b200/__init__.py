@@ -11,6 +11,8 @@ There is no CPU fallback: without the CUDA library or a GPU the compute
 entry points raise ``DeviceError``.
 """
 
+from .bench import (STAGES, StageTimings, bench_csv_text, bench_das, bench_kk, format_bench_table,
+                    noise_volume, write_bench_csv)
 from .beamform import (BeamformConfig, DelayLUTSet, build_das_luts, build_kk_luts,
                        cache_model_entries, compound_coherent, compound_incoherent, das,
                        intensity, kk)

@@ -43,6 +43,8 @@ SIGNATURES = {
     "kkb_kk_last_instance": [],
     "kkb_kk_plan_window_check": [P],
     "kkb_kk_plan_tc_ksteps": [P],
+    "kkb_decomposer_run_stage": [P, I, P, I, P, P],
+    "kkb_analytic_signal_stage": [I, P, LL, I, P, P, P],
     "kkb_kk_plan_destroy": [P],
     "kkb_kk_taps": [P, P, P, P, I, I, I, I, I, D, D, I, P, P],
     "kkb_das": [P, I, I, I, P, P, P, I, P, P, P, P, P, D, P, D, D, I, I, I, P, I, P],

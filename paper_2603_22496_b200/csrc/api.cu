@@ -8,6 +8,7 @@
 #include <new>
 #include <string>
 #include <vector>
+#include <map>
 
 #include "common.cuh"
 #include "fft.cuh"
@@ -877,6 +878,107 @@ static int decomposer_run(kkb_decomposer *p, const void *rf, int in_kind, int n_
         }
     }
     return KKB_OK;
+}
+
+// One stage of the plan's stage 1 at a time, for the reference's staged
+// benchmark (bench.py:113-153 reorg_fft / hilbert_compress / ifft): stage 0
+// real FFT of rf into the plan's spectra, 1 contraction (one-sided weights
+// folded into the ramps) into its contracted bins, 2 inverse FFT to traces.
+// The stages are the three-kernel path's own launches (same results as
+// kkb_decomposer_run); n_frames <= the plan's frames per pass.
+extern "C" int kkb_decomposer_run_stage(kkb_decomposer *p, int stage, const float *rf, int n_frames,
+                                        void *traces, void *stream) {
+    if (!p || n_frames < 0 || stage < 0 || stage > 2) return KKB_ERR_ARG;
+    if (n_frames > p->chunk) {
+        set_error("decomposer stage: %d frames exceed the plan's %d per pass", n_frames, p->chunk);
+        return KKB_ERR_ARG;
+    }
+    if (n_frames == 0) return KKB_OK;
+    cudaStream_t s = as_stream(stream);
+    const int N = p->N, L = p->L, T = p->T, M = p->M, K = p->K, ldk = p->ldk;
+    FftPlan plan;
+    int st = get_fft_plan(T, &plan);
+    if (st) return st;
+    const long long F = n_frames;
+    if (stage == 0) {
+        if (!rf) return KKB_ERR_ARG;
+        if (plan.direct || plan.large) {
+            float2 *promo = nullptr;
+            KKB_TRY_CUDA(cudaMallocAsync(&promo, sizeof(float2) * (size_t)F * N * L * T, s), "cudaMallocAsync(promote)");
+            st = fft_r2c(rf, F * N * L, T, p->X, ldk, K, nullptr, s, promo, L);
+            cudaFreeAsync(promo, s);
+            return st;
+        }
+        return fft_r2c(rf, F * N * L, T, p->X, ldk, K, nullptr, s, nullptr, L);
+    }
+    if (stage == 1) {
+        if (p->form == KKB_CONTRACT_TENSOR)
+            return contract_tc(p->X, ldk, p->tctab, p->Y, ldk, F * N, L, M, K, p->P, p->mp.data(), p->mm.data(), s);
+        if (p->P > 0)
+            return contract_sym(p->X, ldk, p->cs, ldk, p->Y, ldk, F * N, L, M, K, p->P, p->mp.data(),
+                                p->mm.data(), s);
+        return contract(p->X, ldk, p->ramps, ldk, p->Y, ldk, F * N, L, M, K, s);
+    }
+    if (!traces) return KKB_ERR_ARG;
+    return fft_c2c(p->Y, ldk, K, (float2 *)traces, T, T, F * N * M, T, true, 1.0f, s);
+}
+
+// One stage of analytic_signal (spectral.py:84-93) at a time, for the
+// reference's staged DAS benchmark (bench.py:91-110): stage 0 real FFT of the
+// rows into spec ((n_traces, T/2 + 1) complex64, caller scratch), 1 the
+// one-sided weights / T on spec in place, 2 inverse FFT of spec into out
+// ((n_traces, T) complex64).  Stages 0 + 1 + 2 equal kkb_analytic_signal.
+extern "C" int kkb_analytic_signal_stage(int stage, const float *rf, long long n_traces, int n_t, void *spec,
+                                         void *out, void *stream) {
+    if (n_traces < 0 || n_t < 1 || n_t > KKB_FFT_MAX_T_TOTAL || stage < 0 || stage > 2 || !spec) {
+        set_error("analytic_signal_stage: bad arguments (stage %d, T=%d)", stage, n_t);
+        return n_t > KKB_FFT_MAX_T_TOTAL ? KKB_ERR_UNSUPPORTED : KKB_ERR_ARG;
+    }
+    if (n_traces == 0) return KKB_OK;
+    cudaStream_t s = as_stream(stream);
+    const int T = n_t, K = T / 2 + 1;
+    FftPlan plan;
+    int st = get_fft_plan(T, &plan);
+    if (st) return st;
+    float2 *X = (float2 *)spec;
+    if (stage == 0) {
+        if (!rf) return KKB_ERR_ARG;
+        if (plan.direct || plan.large) {
+            Scratch promo(s);
+            if ((st = promo.alloc(sizeof(float2) * (size_t)n_traces * T))) return st;
+            return fft_r2c(rf, n_traces, T, X, K, K, nullptr, s, (float2 *)promo.p);
+        }
+        return fft_r2c(rf, n_traces, T, X, K, K, nullptr, s, nullptr);
+    }
+    if (stage == 1) {
+        // one-sided weights / T per length, built once per process (device
+        // tables, kept for the process lifetime: a staged benchmark calls this
+        // per repetition)
+        static std::mutex mu;
+        static std::map<std::pair<int, int>, float *> tables;  // (device, T) -> weights
+        int devid = 0;
+        KKB_TRY_CUDA(cudaGetDevice(&devid), "get device");
+        float *w = nullptr;
+        {
+            std::lock_guard<std::mutex> lock(mu);
+            auto it = tables.find({devid, T});
+            if (it != tables.end()) {
+                w = it->second;
+            } else {
+                std::vector<float> sc(K);
+                for (int k = 0; k < K; ++k) sc[k] = (float)(one_sided(k, T) / T);
+                KKB_TRY_CUDA(cudaMalloc(&w, sizeof(float) * K), "cudaMalloc(one-sided weights)");
+                KKB_TRY_CUDA(cudaMemcpy(w, sc.data(), sizeof(float) * K, cudaMemcpyHostToDevice), "copy weights");
+                tables[{devid, T}] = w;
+            }
+        }
+        const long long total = n_traces * K;
+        k_scale_bins<<<(unsigned)std::min<long long>(ceil_div(total, 256), 4096), 256, 0, s>>>(X, n_traces, K, K, w);
+        KKB_CHECK_LAUNCH("k_scale_bins");
+        return KKB_OK;
+    }
+    if (!out) return KKB_ERR_ARG;
+    return fft_c2c(X, K, K, (float2 *)out, T, T, n_traces, T, true, 1.0f, s);
 }
 
 // Pipelined mode: `chunk_frames` per pass, passes rotated over `slots` (1..4)

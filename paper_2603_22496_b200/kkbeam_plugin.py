@@ -13,6 +13,9 @@ globals at call time:
 * ``kkbeam.metrics.gamma_match`` and the CLI's imported name
   ``kkbeam.cli.gamma_match`` (metrics.py:175-202, called at cli.py:167; the
   display map, §8(f) row 2)
+* ``kkbeam.bench._kk_stage_fns`` / ``_das_stage_fns`` (bench.py:113-153,
+  91-110; used by ``bench_kk`` / ``bench_das`` and ``kkbeam bench``): the
+  staged benchmark's stages on the device (``paper_2603_22496_b200.bench``)
 
 The shims below have exactly those signatures (flat numpy arrays in, the
 caller's ``out`` array filled in place) and run the sm_100a kernels through
@@ -165,4 +168,15 @@ def install(kkbeam_pkg=None, spectral: bool = True) -> Installed:
         if mod is not None and hasattr(mod, "gamma_match"):
             saved[(mod, "gamma_match")] = mod.gamma_match
             mod.gamma_match = gamma_match
+    # the staged benchmark (bench.py:91-185, `kkbeam bench`): its private
+    # stage builders call scipy / numpy directly, so they are rebound to the
+    # device stages (paper_2603_22496_b200.bench)
+    bm = sys.modules.get("kkbeam.bench")
+    if bm is not None and hasattr(bm, "_kk_stage_fns"):
+        from . import bench as gpu_bench
+
+        saved[(bm, "_kk_stage_fns")] = bm._kk_stage_fns
+        saved[(bm, "_das_stage_fns")] = bm._das_stage_fns
+        bm._kk_stage_fns = gpu_bench.kk_stage_fns
+        bm._das_stage_fns = gpu_bench.das_stage_fns
     return Installed(saved)
