@@ -259,6 +259,7 @@ k_kk_gather_tc(const __grid_constant__ TcgArgs a) {
     __shared__ uint64_t dfull[TCG_ND], dfree[TCG_ND], tab_full[2], tab_empty[2];
     __shared__ uint32_t tmem_base;
     __shared__ int b_k16[TCG_NB];  // per B stage: 1 = a 16-sample window (one K step)
+    __shared__ unsigned fm_s[2][4][TCG_FB];  // per item parity: each drain warp's frame maxima
 
     // a batch with a non-finite sample goes to the FMA gather (NaN x 0 would
     // spread it over the whole window); uniform, before any barrier
@@ -543,11 +544,22 @@ k_kk_gather_tc(const __grid_constant__ TcgArgs a) {
                         if (f < FB) a.inten[px0 + f * a.out_fs] = S[f];
                 }
                 if (a.fmax) {
-                    // non-negative floats order like their bit patterns: one redux per frame
+                    // non-negative floats order like their bit patterns: one redux per
+                    // frame and warp, the four drain warps combined in shared memory,
+                    // then one atomic per frame and item (the CTAs in flight share a
+                    // frame block, so per-warp atomics contend on 64 addresses)
+                    unsigned *fm = fm_s[k & 1][quarter];
 #pragma unroll
                     for (int f = 0; f < TCG_FB; ++f) {
                         const unsigned mx = __reduce_max_sync(0xffffffffu, __float_as_uint(S[f]));
-                        if (lane == 0 && f < FB) atomicMax(a.fmax + f0 + f, mx);
+                        if (lane == 0) fm[f] = mx;
+                    }
+                    asm volatile("bar.sync 1, 128;" ::: "memory");  // the four drain warps
+                    const int dr = (warp - 6) * 32 + lane;  // 0..127
+                    if (dr < FB) {
+                        const unsigned m4 = max(max(fm_s[k & 1][0][dr], fm_s[k & 1][1][dr]),
+                                                max(fm_s[k & 1][2][dr], fm_s[k & 1][3][dr]));
+                        atomicMax(a.fmax + f0 + dr, m4);
                     }
                 }
             }
