@@ -126,7 +126,8 @@ int kk_gather_tc(const float2 *data, int N, int M, int T, const double *ltx, con
 #define KKB_KK_TC_TZ 4   // tensor-core tile: 4 depth rows x 32 columns (128 pixels = M)
 #define KKB_KK_TC_TX 32
 #define KKB_KK_TC_W 32    // window samples per (tile, pair)
-#define KKB_KK_TC_MIN_FRAMES 48  // default dispatch: linear batches of at least this many frames
+#define KKB_KK_TC_MIN_FRAMES 48          // default dispatch: linear batches of at least this many frames
+#define KKB_KK_TC_MIN_FRAMES_NEAREST 128 // ... and nearest-tap batches of at least this many
 
 // instance the last kk_gather dispatch launched (KKB_KK_INST_*, include/kkb.h)
 int kk_last_instance();

@@ -1112,15 +1112,16 @@ int kk_gather(const float2 *data, int N, int M, int T, const double *ltx, const 
     // the batch holds a NaN / Inf sample (the reference propagates those per
     // tap; a tensor-core product would spread them over the window).
     {
-        // default: linear interpolation on batches of >= KKB_KK_TC_MIN_FRAMES
-        // frames (measured crossover, profiles/r02_gather_tc_sweep.jsonl: below
-        // it the per-pair weight rows dominate; nearest taps stay on the FMA
-        // gather, which wins there at every batch size); KKB_KK_INST forces
-        // an instance either way, KKB_KK_TC=0 disables it
+        // default: batches of >= KKB_KK_TC_MIN_FRAMES frames with linear taps,
+        // >= KKB_KK_TC_MIN_FRAMES_NEAREST with nearest taps (the FMA gather's
+        // cheaper taps hold out longer) — the measured crossovers,
+        // profiles/r02_gather_tc_sweep.jsonl: below them the per-pair weight
+        // rows do not amortise; KKB_KK_INST forces an instance either way,
+        // KKB_KK_TC=0 disables it
         const char *fi = getenv("KKB_KK_INST");
         const char *tcv = getenv("KKB_KK_TC");
-        const bool want = fi ? !strcmp(fi, "tc")
-                             : !(tcv && tcv[0] == '0') && linear && n_frames >= KKB_KK_TC_MIN_FRAMES;
+        const int min_frames = linear ? KKB_KK_TC_MIN_FRAMES : KKB_KK_TC_MIN_FRAMES_NEAREST;
+        const bool want = fi ? !strcmp(fi, "tc") : !(tcv && tcv[0] == '0') && n_frames >= min_frames;
         const bool tc_ok = !ms && !sc && win.tc_lo && !(win.bad & (1 << KKB_KK_INST_TC));
         if (want && tc_ok) {
             const int rc = kk_gather_tc(data, N, M, T, ltx, ltzT, lrx, lrzT, nx, nz, w, fs, shift, linear, out,
