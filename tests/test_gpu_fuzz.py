@@ -258,3 +258,75 @@ def test_simulator_random_geometry(oracle, seed):
     ref = oracle.simulate_rf(arr.positions, params.transmit_angles, C, T, t0, fs, ph.x, ph.z,
                              ph.reflectivity, pulse.waveform, spread=spread)
     assert np.array_equal(rf.data, ref), (seed, L, n_tx, T, n_pts)
+
+
+@pytest.mark.parametrize("seed", range(30 * _SCALE))
+def test_tensor_core_gather_random(seed, monkeypatch):
+    """Random geometries and batch sizes through the tensor-core gather
+    (forced, KKB_KK_INST=tc) against the FMA gather (KKB_KK_TC=0): partial
+    tiles, tail frame blocks, both tap modes, channel weights, complex64 /
+    complex128 IQ, fused intensity (optionally accumulated) and frame max.
+    Plans too steep for its 4 x 32 tile must fall back to an FMA instance."""
+    import ctypes
+
+    import torch
+
+    from paper_2603_22496_b200 import _device as dev
+    from paper_2603_22496_b200 import _lib
+
+    rng = np.random.default_rng(7000 + seed)
+    n_tx = int(rng.integers(1, 8))
+    m_rx = int(rng.integers(1, 12))
+    T = int(rng.choice([128, 256, 777, 1024, 1536]))
+    nx, nz = int(rng.integers(1, 80)), int(rng.integers(1, 80))
+    F = int(rng.integers(1, 140))
+    fs = float(rng.uniform(10e6, 40e6))
+    tx = _sym(rng, n_tx, 0.3) if n_tx > 1 else np.array([float(rng.uniform(-0.2, 0.2))])
+    params = kb.AcquisitionParams(C, tx, T, start_time=float(rng.uniform(0, 3e-6)))
+    rx = kb.explicit_angles(_sym(rng, m_rx, 0.35))
+    dx, dz = float(rng.uniform(0.02e-3, 0.3e-3)), float(rng.uniform(0.02e-3, 0.3e-3))
+    grid = kb.ImageGrid(float(rng.uniform(-5e-3, 0)), float(rng.uniform(1e-3, 10e-3)), dx, dz, nx, nz)
+    luts = kb.build_kk_luts(grid, params, rx)
+    linear = bool(rng.integers(0, 2))
+    w = rng.uniform(0.2, 2.0, m_rx) if rng.integers(0, 2) else None
+    c128 = bool(rng.integers(0, 2))
+    accum = bool(rng.integers(0, 2))
+    d = [dev.to_device(np.ascontiguousarray(a)) for a in (luts.lut_tx_x, luts.lut_tx_z, luts.lut_rx_x, luts.lut_rx_z)]
+    wd = dev.to_device(w) if w is not None else None
+    kp = ctypes.c_void_p()
+    shift = (0.0 - params.start_time) * fs
+    _lib.call("kkb_kk_plan_create", *[x.data_ptr() for x in d], n_tx, m_rx, T, nx, nz, dev.ptr(wd), fs, shift,
+              int(linear), dev.stream_handle(), ctypes.byref(kp))
+    try:
+        g = torch.Generator(device="cuda").manual_seed(seed)
+        traces = torch.view_as_complex(torch.randn((F, n_tx, m_rx, T, 2), generator=g, device="cuda"))
+        P = nx * nz
+        base = torch.rand((F, P), generator=g, device="cuda")
+        outs = {}
+        for mode in ("tc", "fma"):
+            if mode == "tc":
+                monkeypatch.setenv("KKB_KK_INST", "tc")
+            else:
+                monkeypatch.setenv("KKB_KK_TC", "0")
+            iq = torch.zeros((F, P), dtype=torch.complex128 if c128 else torch.complex64, device="cuda")
+            inten = base.clone()
+            fmax = torch.zeros(F, dtype=torch.int32, device="cuda")
+            _lib.call("kkb_kk_plan_run_ex", kp, dev.ptr(traces), F, n_tx * m_rx * T, dev.ptr(iq),
+                      _lib.KKB_OUT_C128 if c128 else _lib.KKB_OUT_C64, P, dev.ptr(inten), dev.ptr(fmax),
+                      _lib.KKB_RUN_ACCUMULATE_INTENSITY if accum else 0, dev.stream_handle())
+            torch.cuda.synchronize()
+            monkeypatch.delenv("KKB_KK_INST", raising=False)
+            monkeypatch.delenv("KKB_KK_TC", raising=False)
+            outs[mode] = (_lib.last_instance(), iq, inten, fmax.view(torch.float32))
+        assert _lib.take_device_error() == 0
+        eligible = int(_lib.load().kkb_kk_plan_tc_ksteps(kp)) > 0
+        assert (outs["tc"][0] == _lib.KKB_KK_INST_TC) == eligible, (seed, outs["tc"][0], eligible)
+        a, b = outs["tc"], outs["fma"]
+        for x, y, tol in ((a[1], b[1], 3e-6), (a[2], b[2], 6e-6)):
+            for f in range(F):
+                ny = float(torch.linalg.vector_norm(y[f]).item())
+                e = float(torch.linalg.vector_norm(x[f] - y[f]).item())
+                assert e <= tol * ny + 1e-30, (seed, f, e / max(ny, 1e-30))
+        assert bool(((a[3] - b[3]).abs() <= 1e-5 * b[3].abs() + 1e-30).all()), seed
+    finally:
+        _lib.load().kkb_kk_plan_destroy(kp)
