@@ -26,6 +26,13 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t saddr, uint32_t lbo, uint
     return d;                // base offset 0, lbo mode 0, layout SWIZZLE_NONE
 }
 
+// Swizzled K-major shared-memory descriptor (layout 4 = 64-byte swizzle: rows
+// of 64 bytes, 8-row atoms of 512; 6 = 32-byte swizzle: rows of 32 bytes,
+// atoms of 256): sbo = the atom stride; the leading offset is unused.
+__device__ __forceinline__ uint64_t smem_desc_sw(uint32_t saddr, uint32_t sbo, uint32_t layout) {
+    return smem_desc(saddr, 16, sbo) | ((uint64_t)layout << 61);
+}
+
 // Instruction descriptor: fp32 accumulate, A/B format (0 f16, 1 bf16, 2 tf32),
 // A K-major, B K-major (b_mn_major = 0) or MN-major (1), dense.
 __host__ __device__ constexpr uint32_t instr_desc(int ab_format, int M, int N, int b_mn_major = 0) {
