@@ -304,7 +304,8 @@ def run_gpu(args):
     del src
 
     pipeline = (args.pipe_chunk, args.pipe_slots) if args.pipe_slots > 1 else None
-    eng = kb.KKEngine(arr, p, rx, g, frames=F, chunk_frames=args.chunk, pipeline=pipeline)
+    eng = kb.KKEngine(arr, p, rx, g, frames=F, chunk_frames=args.chunk, pipeline=pipeline,
+                      fuse_tc=not args.no_fuse)
     stream = torch.cuda.current_stream()
 
     G = max(1, args.groups)
@@ -508,6 +509,9 @@ def run_gpu(args):
             "stage_ms_sequential": {"decompose(K1-K3)": dec_ms, "kk_gather(K5)": kk_ms,
                                     "db_map(K6)": det_ms},
             "overlap_groups": G,
+            "stage1_to_k5": ("fused: K3 writes the tensor-core gather's split fp16 planes "
+                             "(kkb_decomposer_run_planes -> kkb_kk_plan_run_planes)") if eng.fused else
+                            "complex64 traces (K5 splits them itself when it runs on the tensor cores)",
             "value_int16_ingest": {"value": world * F / (q_ms / 1e3), "unit": UNIT, "ms_per_step": q_ms,
                                    "note": "same device-resident step on int16-quantised RF "
                                            "(converted exactly in the FFT load)"},
@@ -695,6 +699,8 @@ def main():
     ap.add_argument("--chunk", type=int, default=None, help="frames per decomposition pass")
     ap.add_argument("--pipe-chunk", type=int, default=8, help="frames per pipelined pass")
     ap.add_argument("--pipe-slots", type=int, default=1, help="decomposition streams (1 = off)")
+    ap.add_argument("--no-fuse", action="store_true",
+                    help="K3 writes complex64 traces and the gather splits them (no fused planes)")
     ap.add_argument("--groups", type=int, default=1,
                     help="frame groups: decomposition of group g+1 overlaps the gather of group g")
     ap.add_argument("--e2e-chunk", type=int, default=16)

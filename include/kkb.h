@@ -159,6 +159,15 @@ int kkb_kk_plan_window(const kkb_kk_plan *p);
  * would clamp a tap (the dispatch then never uses it, and
  * KKB_DEVERR_KK_WINDOW is raised).  0 = every tiled instance proven. */
 int kkb_kk_plan_window_check(const kkb_kk_plan *p);
+/* kkb_kk_plan_run_ex on traces already split by kkb_decomposer_run_planes:
+ * the tensor-core gather reads the planes and frame bounds; traces (dense
+ * (F, N, M, T) complex64) are read only by the FMA standby when *nonfinite is
+ * set.  KKB_ERR_UNSUPPORTED when the plan cannot run the tensor-core gather
+ * (kkb_kk_plan_tc_ksteps < 0): no other instance reads planes. */
+int kkb_kk_plan_run_planes(kkb_kk_plan *p, const void *planes, const unsigned *frame_bound,
+                           const unsigned *nonfinite, const void *traces, int n_frames, void *out, int out_kind,
+                           long long out_frame_stride, float *intensity, unsigned int *frame_max, int flags,
+                           void *stream);
 /* Tensor-core gather work of the plan: the number of K = 16 MMA steps (1 or 2
  * per tile and pair, from the plan's exact per-tile windows) one group of 8
  * frames takes; -1 when the plan is not eligible for the tensor-core gather
@@ -311,6 +320,20 @@ int kkb_decomposer_run_stage(kkb_decomposer *p, int stage, const float *rf, int 
  * into out ((n_traces, T) complex64).  0 + 1 + 2 == kkb_analytic_signal. */
 int kkb_analytic_signal_stage(int stage, const float *rf, long long n_traces, int n_t, void *spec, void *out,
                               void *stream);
+/* Stage 1 emitting the tensor-core gather's split trace planes instead of
+ * complex64 traces (the fused bench path; kkb_kk_plan_run_planes consumes
+ * them): K1, K2, a per-frame bound (max over the frame's traces of the L1
+ * norm of their bins, >= every |sample|) into frame_bound[F], then K3
+ * writes each trace scaled by its frame's power of two and split into fp16
+ * halves (hi + lo) as planes (kkb_tc_planes_bytes(F, N*M, T) bytes, layout
+ * in the library's tcplanes.cuh).  A NaN / Inf bin sets *nonfinite, and only
+ * then are the complex64 traces ((F, N, M, T)) written too — for the FMA
+ * gather, which then runs instead.  T in {1024, 1536, 2048}; F <= the plan's
+ * max_frames. */
+int kkb_decomposer_run_planes(kkb_decomposer *p, const float *rf, int n_frames, void *planes,
+                              unsigned *frame_bound, unsigned *nonfinite, void *traces, void *stream);
+/* bytes of the split planes of F frames of `pairs` traces of T samples */
+long long kkb_tc_planes_bytes(int n_frames, int pairs, int n_t);
 /* bytes of device scratch held by the plan */
 long long kkb_decomposer_workspace_bytes(const kkb_decomposer *p);
 int kkb_decomposer_destroy(kkb_decomposer *p);

@@ -44,6 +44,9 @@ SIGNATURES = {
     "kkb_kk_plan_window_check": [P],
     "kkb_kk_plan_tc_ksteps": [P],
     "kkb_decomposer_run_stage": [P, I, P, I, P, P],
+    "kkb_decomposer_run_planes": [P, P, I, P, P, P, P, P],
+    "kkb_kk_plan_run_planes": [P, P, P, P, P, I, P, I, LL, P, P, I, P],
+    "kkb_tc_planes_bytes": [I, I, I],
     "kkb_analytic_signal_stage": [I, P, LL, I, P, P, P],
     "kkb_kk_plan_destroy": [P],
     "kkb_kk_taps": [P, P, P, P, I, I, I, I, I, D, D, I, P, P],
@@ -83,6 +86,7 @@ SIGNATURES = {
 }
 _RESTYPES = {
     "kkb_kk_plan_tc_ksteps": LL,
+    "kkb_tc_planes_bytes": LL,
     "kkb_version": ctypes.c_char_p,
     "kkb_last_error": ctypes.c_char_p,
     "kkb_launch_count": LL,

@@ -244,6 +244,26 @@ extern "C" int kkb_kk_plan_run_ex(kkb_kk_plan *p, const void *data, int n_frames
                                    out_frame_stride, intensity, frame_max, flags, stream);
 }
 
+extern "C" int kkb_kk_plan_run_planes(kkb_kk_plan *p, const void *planes, const unsigned *frame_bound,
+                                      const unsigned *nonfinite, const void *traces, int n_frames, void *out,
+                                      int out_kind, long long out_frame_stride, float *intensity,
+                                      unsigned int *frame_max, int flags, void *stream) {
+    if (!p || !planes || !frame_bound || !nonfinite || !traces || (flags & ~KKB_RUN_ACCUMULATE_INTENSITY)) {
+        set_error("kk_plan_run_planes: planes, bounds, flag and traces are required");
+        return KKB_ERR_ARG;
+    }
+    int st = check_kk_args(p->N, p->M, p->T, p->nx, p->nz, out_kind);
+    if (st) return st;
+    if (frame_max)
+        KKB_TRY_CUDA(cudaMemsetAsync(frame_max, 0, sizeof(unsigned) * (size_t)n_frames, as_stream(stream)),
+                     "zero frame_max");
+    const TcPlanes tcp{reinterpret_cast<const __half *>(planes), frame_bound, nonfinite};
+    return kk_gather(reinterpret_cast<const float2 *>(traces), p->N, p->M, p->T, p->ltx, p->ltzT, p->lrx, p->lrzT,
+                     p->nx, p->nz, p->w, p->fs, p->shift, p->linear, out, out_kind, n_frames,
+                     (long long)p->N * p->M * p->T, out_frame_stride, intensity, frame_max, p->win, as_stream(stream),
+                     (flags & KKB_RUN_ACCUMULATE_INTENSITY) ? 1 : 0, nullptr, 0, nullptr, &tcp);
+}
+
 extern "C" int kkb_kk_plan_run_sets(kkb_kk_plan *p, const void *data, int n_frames,
                                     long long data_frame_stride, int n_sets,
                                     const int *set_begin_host, void *out, int out_kind,
@@ -979,6 +999,40 @@ extern "C" int kkb_analytic_signal_stage(int stage, const float *rf, long long n
     }
     if (!out) return KKB_ERR_ARG;
     return fft_c2c(X, K, K, (float2 *)out, T, T, n_traces, T, true, 1.0f, s);
+}
+
+extern "C" long long kkb_tc_planes_bytes(int n_frames, int pairs, int n_t) {
+    if (n_frames < 0 || pairs < 0 || n_t < 0) return -1;
+    return 4LL * 2 * ((n_frames + 7) / 8) * 8 * (long long)pairs * n_t;
+}
+
+// Stage 1 emitting the tensor-core gather's split planes (K1, K2, the frame
+// bounds, K3 into planes; traces written only for a batch with a non-finite
+// bin).  One pass: n_frames <= the plan's frames per pass.
+extern "C" int kkb_decomposer_run_planes(kkb_decomposer *p, const float *rf, int n_frames, void *planes,
+                                         unsigned *fbound, unsigned *nonfinite, void *traces, void *stream) {
+    if (!p || !rf || !planes || !fbound || !nonfinite || !traces || n_frames < 0) return KKB_ERR_ARG;
+    if (n_frames > p->chunk) {
+        set_error("decomposer planes: %d frames exceed the plan's %d per pass", n_frames, p->chunk);
+        return KKB_ERR_ARG;
+    }
+    if (!(p->T == 1024 || p->T == 1536 || p->T == 2048)) {
+        set_error("decomposer planes: T = %d (1024, 1536 or 2048)", p->T);
+        return KKB_ERR_UNSUPPORTED;
+    }
+    cudaStream_t s = as_stream(stream);
+    KKB_TRY_CUDA(cudaMemsetAsync(fbound, 0, sizeof(unsigned) * (size_t)n_frames, s), "zero frame bounds");
+    KKB_TRY_CUDA(cudaMemsetAsync(nonfinite, 0, sizeof(unsigned), s), "zero flag");
+    if (n_frames == 0) return KKB_OK;
+    int st;
+    if ((st = kkb_decomposer_run_stage(p, 0, rf, n_frames, nullptr, stream))) return st;
+    if ((st = kkb_decomposer_run_stage(p, 1, rf, n_frames, nullptr, stream))) return st;
+    FftPlan plan;
+    if ((st = get_fft_plan(p->T, &plan))) return st;
+    const long long rows = (long long)n_frames * p->N * p->M;
+    if ((st = frame_bound(p->Y, p->ldk, p->K, rows, p->N * p->M, 1.0f, fbound, nonfinite, s))) return st;
+    return fft_c2c_planes(p->Y, p->ldk, p->K, p->T, n_frames, p->N * p->M, 1.0f, plan.tws, fbound, nonfinite,
+                          (float2 *)traces, (__half *)planes, s);
 }
 
 // Pipelined mode: `chunk_frames` per pass, passes rotated over `slots` (1..4)

@@ -1,6 +1,7 @@
 // FFT plan and launchers shared by the spectral / decomposition paths.
 #pragma once
 
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include <vector>
@@ -99,6 +100,16 @@ int fft_r2c_ct_ring(const void *in, int in_kind, long long ntraces, int T, float
 int fft_c2c_ct(const float2 *in, long long in_stride, int in_len, float2 *out, long long out_stride,
                int out_len, long long ntraces, int T, bool inverse, float scale, const float2 *tw,
                cudaStream_t s, const RowScatter *sc = nullptr);
+// K3 into the tensor-core gather's split planes (tcplanes.cuh) for rows
+// (frame, pair) of the contracted bins Y; T in {1024, 1536, 2048}.  traces
+// are written too when *nonfinite != 0.  planes: 4 x ceil(F/8)*8 x NM x T fp16.
+int fft_c2c_planes(const float2 *Y, long long ldy, int K, int T, int n_frames, int NM, float scale,
+                   const float2 *tws, const unsigned *fbound, const unsigned *nonfinite, float2 *traces,
+                   __half *planes, cudaStream_t s);
+// the per-frame bounds fft_c2c_planes scales by (max over rows of scale x the
+// L1 norm of the row's bins), and the non-finite flag
+int frame_bound(const float2 *Y, long long ldy, int K, long long rows, int rows_per_frame, float scale,
+                unsigned *fbound, unsigned *nonfinite, cudaStream_t s);
 // fft_c2c whose rows are stored through `sc` (out_stride = row pitch inside a
 // frame): fused into the compile-time kernels' epilogue, otherwise one
 // transform into scratch followed by a strided copy per destination.

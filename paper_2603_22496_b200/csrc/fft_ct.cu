@@ -31,6 +31,7 @@
 
 #include "common.cuh"
 #include "fft.cuh"
+#include "tcplanes.cuh"
 
 namespace kkb {
 namespace ct {
@@ -194,7 +195,9 @@ struct Stage {
     static constexpr int ITER = (TR + NT - 1) / NT;
     float2 v[ITER][R];
 
-    __device__ __forceinline__ static int lane_j(int t) { return (int)threadIdx.x + t * NT; }
+    // NT is a power of two; a CTA may run several transforms side by side
+    // (k_c2c_planes: threads [i NT, (i + 1) NT) take transform i)
+    __device__ __forceinline__ static int lane_j(int t) { return (int)(threadIdx.x & (NT - 1)) + t * NT; }
     __device__ __forceinline__ static bool ok(int j) { return TR % NT == 0 || j < TR; }
     __device__ __forceinline__ static int swz(int e) { return e ^ ((e >> 4) & 15); }
 
@@ -241,17 +244,27 @@ struct Stage {
     }
 };
 
+// barrier of one transform's NT threads: the CTA-wide __syncthreads (BAR 0)
+// for one transform per CTA, named barrier 1 + i for transform i of several
+template <int NT>
+__device__ __forceinline__ void xform_sync(int bar) {
+    if (bar == 0)
+        __syncthreads();
+    else
+        asm volatile("bar.sync %0, %1;" ::"r"(bar), "n"(NT) : "memory");
+}
+
 // stages 1 and 2 of the plan on `buf` holding stage 0's swizzled output;
 // returns with stage 2's outputs (bins j + r T/R2) in `c`
 template <int T, typename S2>
-__device__ __forceinline__ void stages12(float2 *buf, const float2 *__restrict__ tw, S2 &c) {
+__device__ __forceinline__ void stages12(float2 *buf, const float2 *__restrict__ tw, S2 &c, int bar = 0) {
     using P = Plan<T>;
     Stage<T, P::NT, P::R1> b;
     b.template load<true>(buf);
-    __syncthreads();
+    xform_sync<P::NT>(bar);
     b.template compute<P::R0, 0>(tw);
     b.template store<P::R0, false>(buf);
-    __syncthreads();
+    xform_sync<P::NT>(bar);
     c.template load<false>(buf);
     c.template compute<P::R0 * P::R1, (P::R1 - 1) * P::R0>(tw);
 }
@@ -361,15 +374,13 @@ k_r2c(const InT *__restrict__ in, long long ntraces, float2 *__restrict__ out,
 // buffers mapped over NVLink) at sc.off + (row / rpf) * frame_stride +
 // (row % rpf) * out_stride instead of `out` -- the fused trace all-gather of
 // transmit-sharded stage 1.
-template <int T, bool INV, bool SC = false>
-__global__ void __launch_bounds__(Plan<T>::NT)
-k_c2c(const float2 *__restrict__ in, long long in_stride, int in_len, float2 *__restrict__ out,
-      long long out_stride, int out_len, float scale, const float2 *__restrict__ tw,
-      RowScatter sc = RowScatter{}) {
+// One complex transform of the row at src (bins [0, in_len), the rest zero)
+// through buf; returns with the outputs (points j + r T/R2 of lane j) in c,
+// conjugated on input for the inverse (the caller conjugates the output).
+template <int T, bool INV, typename S2>
+__device__ __forceinline__ void c2c_row(const float2 *__restrict__ src, int in_len, const float2 *__restrict__ tw,
+                                        float2 *buf, S2 &c, int bar = 0) {
     using P = Plan<T>;
-    __shared__ __align__(16) float2 buf[T];
-    const long long row = blockIdx.x;
-    const float2 *src = in + row * in_stride;
     const float sg = INV ? -1.f : 1.f;
     using S0 = Stage<T, P::NT, P::R0>;
     S0 a;
@@ -388,10 +399,22 @@ k_c2c(const float2 *__restrict__ in, long long in_stride, int in_len, float2 *__
     }
     a.template compute<1, 0>(tw);
     a.template store<1, true>(buf);
-    __syncthreads();
+    xform_sync<P::NT>(bar);
+    stages12<T>(buf, tw, c, bar);
+}
+
+template <int T, bool INV, bool SC = false>
+__global__ void __launch_bounds__(Plan<T>::NT)
+k_c2c(const float2 *__restrict__ in, long long in_stride, int in_len, float2 *__restrict__ out,
+      long long out_stride, int out_len, float scale, const float2 *__restrict__ tw,
+      RowScatter sc = RowScatter{}) {
+    using P = Plan<T>;
+    __shared__ __align__(16) float2 buf[T];
+    const long long row = blockIdx.x;
+    const float sg = INV ? -1.f : 1.f;
     using S2 = Stage<T, P::NT, P::R2>;
     S2 c;
-    stages12<T>(buf, tw, c);
+    c2c_row<T, INV>(in + row * in_stride, in_len, tw, buf, c);
     const float sy = sg * scale;
     if constexpr (SC) {
         const long long o = sc.off + (row / sc.rows_per_frame) * sc.frame_stride +
@@ -420,6 +443,101 @@ k_c2c(const float2 *__restrict__ in, long long in_stride, int in_len, float2 *__
                 if (S2::ok(j) && k < out_len) dst[k] = make_float2(c.v[t][r].x * scale, c.v[t][r].y * sy);
             }
         }
+    }
+}
+
+// K3 into the tensor-core gather's split planes (tcplanes.cuh): inverse
+// transforms of the contracted bins Y (rows (frame, pair), row stride ldy,
+// bins [0, K)).  A CTA takes the 8 frames of one frame group of one pair q:
+// eight transforms side by side (threads [i NT, (i + 1) NT) take frame i,
+// each in its own T-point buffer), each output scaled by its frame's power
+// of two (from the frame bound fbound[f]) and split into fp16 halves, staged
+// in the freed buffers as [plane][sample][8 frames] and stored as coalesced
+// 16-byte rows.  Frames past n_frames stage zeros.  When *nonfinite is set
+// the complex64 traces are written too (the FMA gather, which then runs
+// instead, reads them).
+template <int T>
+__global__ void __launch_bounds__(8 * Plan<T>::NT)
+k_c2c_planes(const float2 *__restrict__ Y, long long ldy, int K, int n_frames, int NM, float scale,
+             const float2 *__restrict__ tw, const unsigned *__restrict__ fbound,
+             const unsigned *__restrict__ nonfinite, float2 *__restrict__ traces, __half *__restrict__ planes,
+             long long per_plane) {
+    using P = Plan<T>;
+    extern __shared__ __align__(16) unsigned char dsm[];
+    float2 *bufs = reinterpret_cast<float2 *>(dsm);  // [8][T]; then the stage [8 frames][T][4 planes] fp16
+    uint2 *stage = reinterpret_cast<uint2 *>(dsm);
+    const int q = blockIdx.x % NM;
+    const long long g = blockIdx.x / NM;
+    const int i = threadIdx.x / P::NT;  // frame of the group
+    const long long f = g * 8 + i, row = f * NM + q;
+    const bool live = f < n_frames;
+    using S2 = Stage<T, P::NT, P::R2>;
+    S2 c;
+    c2c_row<T, true>(live ? Y + row * ldy : Y, live ? K : 0, tw, bufs + (size_t)i * T, c, 1 + i);  // own barrier
+    const bool flag = *nonfinite != 0;
+    const float sc = live ? frame_scale(__ldg(fbound + f)) : 0.f;
+    __syncthreads();  // every transform's buffer read: reuse them as the stage
+#pragma unroll
+    for (int t = 0; t < S2::ITER; ++t) {
+        const int j = S2::lane_j(t);
+#pragma unroll
+        for (int r = 0; r < P::R2; ++r) {
+            const int k = j + r * S2::TR;
+            if (S2::ok(j)) {
+                const float2 x = make_float2(c.v[t][r].x * scale, c.v[t][r].y * -scale);
+                if (flag && live) traces[row * T + k] = x;
+                __half h0, l0, h1, l1;
+                split_h(x.x * sc, h0, l0);
+                split_h(x.y * sc, h1, l1);
+                stage[i * T + k] = make_uint2(pack_h2(h0, h1), pack_h2(l0, l1));  // consecutive k: conflict-free
+            }
+        }
+    }
+    __syncthreads();
+    // per sample k: the 8 frames' 8-byte entries in, the four planes' 16-byte
+    // rows out (conflict-free 64-bit loads, coalesced 128-bit stores)
+    uint4 *dst = reinterpret_cast<uint4 *>(planes) + (g * NM + q) * T;
+    for (int k = threadIdx.x; k < T; k += blockDim.x) {
+        uint2 e[8];
+#pragma unroll
+        for (int fi = 0; fi < 8; ++fi) e[fi] = stage[fi * T + k];
+        // e.x = (re hi, im hi), e.y = (re lo, im lo) of one frame
+        auto lo16 = [](uint32_t v) { return v & 0xffffu; };
+        auto hi16 = [](uint32_t v) { return v >> 16; };
+        dst[0 * (per_plane / 8) + k] = make_uint4(lo16(e[0].x) | lo16(e[1].x) << 16, lo16(e[2].x) | lo16(e[3].x) << 16,
+                                                  lo16(e[4].x) | lo16(e[5].x) << 16, lo16(e[6].x) | lo16(e[7].x) << 16);
+        dst[1 * (per_plane / 8) + k] = make_uint4(hi16(e[0].x) | hi16(e[1].x) << 16, hi16(e[2].x) | hi16(e[3].x) << 16,
+                                                  hi16(e[4].x) | hi16(e[5].x) << 16, hi16(e[6].x) | hi16(e[7].x) << 16);
+        dst[2 * (per_plane / 8) + k] = make_uint4(lo16(e[0].y) | lo16(e[1].y) << 16, lo16(e[2].y) | lo16(e[3].y) << 16,
+                                                  lo16(e[4].y) | lo16(e[5].y) << 16, lo16(e[6].y) | lo16(e[7].y) << 16);
+        dst[3 * (per_plane / 8) + k] = make_uint4(hi16(e[0].y) | hi16(e[1].y) << 16, hi16(e[2].y) | hi16(e[3].y) << 16,
+                                                  hi16(e[4].y) | hi16(e[5].y) << 16, hi16(e[6].y) | hi16(e[7].y) << 16);
+    }
+}
+
+// Per-frame bound for the plane scale: max over the frame's rows of
+// scale * sum_k (|Re Y_k| + |Im Y_k|) >= max_t |x_t| (the inverse transform
+// of bins [0, K)), as float bits; a non-finite bin sets *nonfinite.  One warp
+// per row.
+__global__ void __launch_bounds__(256) k_frame_bound(const float2 *__restrict__ Y, long long ldy, int K,
+                                                     long long rows, int rows_per_frame, float scale,
+                                                     unsigned *__restrict__ fbound, unsigned *__restrict__ nonfinite) {
+    const long long row = (long long)blockIdx.x * 8 + (threadIdx.x >> 5);
+    if (row >= rows) return;
+    const int lane = threadIdx.x & 31;
+    const float2 *y = Y + row * ldy;
+    float s = 0.f;
+    for (int k = lane; k < K; k += 32) {
+        const float2 v = __ldg(y + k);
+        s += fabsf(v.x) + fabsf(v.y);
+    }
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) {
+        // rounding margin: the sum and the transform's own roundings stay far
+        // below 2^-10 relative, and a bound twice too large costs nothing
+        const float b = s * fabsf(scale) * 1.001f;
+        if (!(b <= 3.0e38f)) atomicOr(nonfinite, 1u);  // NaN or Inf
+        else atomicMax(fbound + row / rows_per_frame, __float_as_uint(b));
     }
 }
 
@@ -538,6 +656,42 @@ int fft_r2c_ct_ring(const void *in, int in_kind, long long ntraces, int T, float
         case 4096: return launch_r2c_ring<4096>(in, in_kind, ntraces, ring, out_stride, K, bin_scale, tws, s, rs);
     }
     return KKB_ERR_UNSUPPORTED;
+}
+
+template <int T>
+static int launch_c2c_planes(const float2 *Y, long long ldy, int K, int n_frames, int NM, float scale,
+                             const float2 *tw, const unsigned *fbound, const unsigned *nonfinite, float2 *traces,
+                             __half *planes, cudaStream_t s) {
+    const long long groups = (n_frames + 7) / 8;
+    const long long per_plane = groups * 8 * NM * (long long)T;
+    const size_t smem = sizeof(float2) * 8 * (size_t)T;  // 8 transform buffers, then the fp16 stage
+    KKB_TRY_CUDA(cudaFuncSetAttribute(ct::k_c2c_planes<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+                 "smem attr c2c planes");
+    ct::k_c2c_planes<T><<<(unsigned)(groups * NM), 8 * ct::Plan<T>::NT, smem, s>>>(
+        Y, ldy, K, n_frames, NM, scale, tw, fbound, nonfinite, traces, planes, per_plane);
+    KKB_CHECK_LAUNCH("k_c2c_planes");
+    return KKB_OK;
+}
+
+int fft_c2c_planes(const float2 *Y, long long ldy, int K, int T, int n_frames, int NM, float scale,
+                   const float2 *tws, const unsigned *fbound, const unsigned *nonfinite, float2 *traces,
+                   __half *planes, cudaStream_t s) {
+    if (n_frames <= 0) return KKB_OK;
+    switch (T) {
+        case 1024: return launch_c2c_planes<1024>(Y, ldy, K, n_frames, NM, scale, tws, fbound, nonfinite, traces, planes, s);
+        case 1536: return launch_c2c_planes<1536>(Y, ldy, K, n_frames, NM, scale, tws, fbound, nonfinite, traces, planes, s);
+        case 2048: return launch_c2c_planes<2048>(Y, ldy, K, n_frames, NM, scale, tws, fbound, nonfinite, traces, planes, s);
+    }
+    return KKB_ERR_UNSUPPORTED;
+}
+
+int frame_bound(const float2 *Y, long long ldy, int K, long long rows, int rows_per_frame, float scale,
+                unsigned *fbound, unsigned *nonfinite, cudaStream_t s) {
+    if (rows <= 0) return KKB_OK;
+    ct::k_frame_bound<<<(unsigned)ceil_div(rows, 8), 256, 0, s>>>(Y, ldy, K, rows, rows_per_frame, scale, fbound,
+                                                                   nonfinite);
+    KKB_CHECK_LAUNCH("k_frame_bound");
+    return KKB_OK;
 }
 
 int fft_c2c_ct(const float2 *in, long long in_stride, int in_len, float2 *out, long long out_stride,

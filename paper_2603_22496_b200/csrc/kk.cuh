@@ -3,6 +3,7 @@
 
 #include <functional>
 
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 // kk gather tile: TZ = 8*WZ depth rows x TX = 8*CX*WX lateral columns per CTA
@@ -105,7 +106,7 @@ int kk_gather(const float2 *data, int N, int M, int T, const double *ltx, const 
               long long out_fs, float *inten, unsigned *fmax, const KKWindows &win, cudaStream_t s,
               int accum = 0, const KKScatter *sc = nullptr,
               long long data_ns = 0,  // 0: M*T (dense (N, M, T) traces)
-              const KKSets *sets = nullptr);
+              const KKSets *sets = nullptr, const struct TcPlanes *tcp = nullptr);
 
 // Plan-time proof that no tap of these tables leaves its tile's staged window
 // (every tile size whose window fits; synchronises `s`): sets win->bad, and
@@ -123,6 +124,21 @@ int kk_gather_tc(const float2 *data, int N, int M, int T, const double *ltx, con
                  double shift, int linear, void *out, int out_kind, int n_frames, long long data_fs,
                  long long out_fs, float *inten, unsigned *fmax, const int *tc_lo, int accum,
                  cudaStream_t s, const std::function<int(const unsigned *)> &fma_fallback);
+// Traces already split into the tensor-core gather's planes (tcplanes.cuh) by
+// K3 (fft_c2c_planes), with their per-frame bounds and non-finite flag; the
+// complex64 traces passed beside them are read only by the FMA standby (when
+// the flag is set).  kk_gather then runs the tensor-core gather or fails with
+// KKB_ERR_UNSUPPORTED: no FMA instance can read planes.
+struct TcPlanes {
+    const __half *planes;
+    const unsigned *fbound;
+    const unsigned *nonfinite;
+};
+int kk_gather_tc_planes(const __half *planes, const unsigned *fbound, const unsigned *nonfinite, int N, int M,
+                        int T, const double *ltx, const double *ltzT, const double *lrx, const double *lrzT, int nx,
+                        int nz, const double *w, double fs, double shift, int linear, void *out, int out_kind,
+                        int n_frames, long long out_fs, float *inten, unsigned *fmax, const int *tc_lo, int accum,
+                        cudaStream_t s, const std::function<int(const unsigned *)> &fma_fallback);
 #define KKB_KK_TC_TZ 4   // tensor-core tile: 4 depth rows x 32 columns (128 pixels = M)
 #define KKB_KK_TC_TX 32
 #define KKB_KK_TC_W 32    // window samples per (tile, pair)

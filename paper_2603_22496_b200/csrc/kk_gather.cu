@@ -1019,7 +1019,7 @@ int kk_gather(const float2 *data, int N, int M, int T, const double *ltx, const 
               const double *lrx, const double *lrzT, int nx, int nz, const double *w, double fs,
               double shift, int linear, void *out, int out_kind, int n_frames, long long data_fs,
               long long out_fs, float *inten, unsigned *fmax, const KKWindows &win, cudaStream_t s,
-              int accum, const KKScatter *sc, long long data_ns, const KKSets *sets) {
+              int accum, const KKScatter *sc, long long data_ns, const KKSets *sets, const TcPlanes *tcp) {
     if (n_frames <= 0 || nx <= 0 || nz <= 0) return KKB_OK;
     const bool ms = sets != nullptr;
     // a receive subset of a larger trace array (transmit stride data_ns > M*T):
@@ -1123,6 +1123,21 @@ int kk_gather(const float2 *data, int N, int M, int T, const double *ltx, const 
         const int min_frames = linear ? KKB_KK_TC_MIN_FRAMES : KKB_KK_TC_MIN_FRAMES_NEAREST;
         const bool want = fi ? !strcmp(fi, "tc") : !(tcv && tcv[0] == '0') && n_frames >= min_frames;
         const bool tc_ok = !ms && !sc && win.tc_lo && !(win.bad & (1 << KKB_KK_INST_TC));
+        if (tcp) {  // traces split by K3: the tensor-core gather or nothing
+            if (!tc_ok || ms || sc) {
+                set_error("kk: split-plane traces need the tensor-core gather, which this plan cannot run");
+                return KKB_ERR_UNSUPPORTED;
+            }
+            const int rc = kk_gather_tc_planes(tcp->planes, tcp->fbound, tcp->nonfinite, N, M, T, ltx, ltzT, lrx,
+                                               lrzT, nx, nz, w, fs, shift, linear, out, out_kind, n_frames, out_fs,
+                                               inten, fmax, win.tc_lo, accum, s, [&](const unsigned *run_if) {
+                                                   KKArgs b = a;
+                                                   b.run_if = run_if;
+                                                   return launch_fma(b);
+                                               });
+            if (rc == KKB_OK) g_last_instance.store(KKB_KK_INST_TC);
+            return rc;
+        }
         if (want && tc_ok) {
             const int rc = kk_gather_tc(data, N, M, T, ltx, ltzT, lrx, lrzT, nx, nz, w, fs, shift, linear, out,
                                         out_kind, n_frames, data_fs, out_fs, inten, fmax, win.tc_lo, accum, s,

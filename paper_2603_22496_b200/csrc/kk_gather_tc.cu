@@ -54,6 +54,7 @@
 #include "common.cuh"
 #include "kk.cuh"
 #include "tc.cuh"
+#include "tcplanes.cuh"
 
 namespace kkb {
 
@@ -106,23 +107,6 @@ __global__ void __launch_bounds__(256) k_frame_maxabs(const float2 *__restrict__
         if (r >= 0x7f800000u) atomicOr(nonfinite, 1u);
         else if (r) atomicMax(out + f, r);
     }
-}
-
-__device__ __forceinline__ float frame_scale(unsigned maxbits) {
-    // 2^(14 - e) with e = floor(log2(max)): max * scale < 2^15 (fp16 max 65504)
-    if (maxbits == 0u) return 1.0f;
-    const int e = (int)((maxbits >> 23) & 0xff) - 127;
-    const int s = min(max(14 - e, -120), 120);
-    return __uint_as_float((unsigned)(127 + s) << 23);
-}
-
-__device__ __forceinline__ uint32_t pack_h2(__half a, __half b) {
-    return (uint32_t)__half_as_ushort(a) | ((uint32_t)__half_as_ushort(b) << 16);
-}
-
-__device__ __forceinline__ void split_h(float x, __half &hi, __half &lo) {
-    hi = __float2half_rn(x);
-    lo = __float2half_rn(x - __half2float(hi));
 }
 
 // planes[pl][g][q][t][8]: pl = re_hi, im_hi, re_lo, im_lo; frames 8g..8g+7.
@@ -605,25 +589,79 @@ k_kk_gather_tc(const __grid_constant__ TcgArgs a) {
     }
 }
 
-int kk_gather_tc(const float2 *data, int N, int M, int T, const double *ltx, const double *ltzT,
-                 const double *lrx, const double *lrzT, int nx, int nz, const double *w, double fs,
-                 double shift, int linear, void *out, int out_kind, int n_frames, long long data_fs,
-                 long long out_fs, float *inten, unsigned *fmax, const int *tc_lo, int accum,
-                 cudaStream_t s, const std::function<int(const unsigned *)> &fma_fallback) {
-    if (!tc_lo) return KKB_ERR_UNSUPPORTED;
+static size_t tcg_smem_bytes(int N, int M) {
+    return (size_t)TCG_NA * (2 * (TCG_KW / 8) * 128 * 16) + (size_t)TCG_NB * (2 * 16 * TCG_KW * 16) +
+           2 * tcg_slot_bytes(N, M) + sizeof(float) * (size_t)M;
+}
+
+// The gather proper on split planes (tcplanes.cuh) with per-frame scale bounds
+// mx and the non-finite flag (the kernel stands down when it is set).
+static int tcg_launch(const __half *planes, const unsigned *mx, const unsigned *nonfinite, int N, int M, int T,
+                      const double *ltx, const double *ltzT, const double *lrx, const double *lrzT, int nx, int nz,
+                      const double *w, double fs, double shift, int linear, void *out, int out_kind, int n_frames,
+                      long long out_fs, float *inten, unsigned *fmax, const int *tc_lo, int accum, cudaStream_t s) {
     const int NM = N * M;
     const long long ngroups = (n_frames + 7) / 8;
-    const size_t plane_elems = (size_t)ngroups * NM * T * 8;
-    const size_t smem = (size_t)TCG_NA * (2 * (TCG_KW / 8) * 128 * 16) + (size_t)TCG_NB * (2 * 16 * TCG_KW * 16) +
-                        2 * tcg_slot_bytes(N, M) + sizeof(float) * (size_t)M;
-    if (smem > 227 * 1024) {
-        set_error("kk tensor-core gather: %d pairs do not fit shared memory", NM);
-        return KKB_ERR_UNSUPPORTED;
+    const size_t smem = tcg_smem_bytes(N, M);
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    if (!encode) {
+        cudaDriverEntryPointQueryResult q;
+        void *fn = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess || !fn) {
+            set_error("kk tensor-core gather: cuTensorMapEncodeTiled unavailable");
+            return KKB_ERR_CUDA;
+        }
+        encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
     }
-    // The split planes are the size of the traces (~600 MB for the bench
-    // batch).  Keep freed stream-ordered blocks in the device's pool across
-    // synchronisations (default release threshold 0 hands them back to the
-    // driver at every sync, and remapping them costs milliseconds per call).
+    TcgArgs a{};
+    {
+        // (sample, frame) flattened: a window is one 512-byte row of the box
+        const cuuint64_t dims[4] = {8ull * T, (cuuint64_t)NM, (cuuint64_t)ngroups, 4};
+        const cuuint64_t strides[3] = {16ull * T, 16ull * T * NM, 16ull * T * NM * ngroups};
+        const cuuint32_t estr[4] = {1, 1, 1, 1};
+        a.nfb = (int)ceil_div(ngroups, TCG_FB / 8);
+        a.gt = (int)(ngroups - (long long)(a.nfb - 1) * (TCG_FB / 8));
+        CUresult r = CUDA_SUCCESS;
+        for (int one = 0; one < 2 && r == CUDA_SUCCESS; ++one)
+            for (int tl = 0; tl < 2 && r == CUDA_SUCCESS; ++tl) {
+                const cuuint32_t box[4] = {8u * (one ? 16u : (unsigned)TCG_KW), 1, tl ? (cuuint32_t)a.gt : 8u, 4};
+                r = encode(tl ? &a.tail[one] : &a.planes[one], CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, const_cast<__half *>(planes), dims,
+                           strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            }
+        if (r != CUDA_SUCCESS) {
+            set_error("kk tensor-core gather: cuTensorMapEncodeTiled failed (%d)", (int)r);
+            return KKB_ERR_CUDA;
+        }
+    }
+    a.N = N, a.M = M, a.T = T, a.ltx = ltx, a.ltzT = ltzT, a.lrx = lrx, a.lrzT = lrzT, a.w = w;
+    a.fs = fs, a.shift = shift, a.nx = nx, a.nz = nz, a.out = out, a.out_kind = out_kind, a.out_fs = out_fs;
+    a.inten = inten, a.fmax = fmax, a.accum = accum, a.n_frames = n_frames, a.maxabs = mx;
+    a.nonfinite = nonfinite;
+    a.tc_lo = tc_lo;
+    a.tiles_z = (int)ceil_div(nz, TCG_TZ);
+    a.tiles = (long long)a.tiles_z * ceil_div(nx, TCG_TX);
+    a.items = a.tiles * a.nfb;
+    const unsigned grid = (unsigned)std::min<long long>(a.items, sm_count());
+    if (linear) {
+        KKB_TRY_CUDA(cudaFuncSetAttribute(k_kk_gather_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+                     "smem attr kk tc");
+        k_kk_gather_tc<true><<<grid, TCG_THREADS, smem, s>>>(a);
+    } else {
+        KKB_TRY_CUDA(cudaFuncSetAttribute(k_kk_gather_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+                     "smem attr kk tc");
+        k_kk_gather_tc<false><<<grid, TCG_THREADS, smem, s>>>(a);
+    }
+    KKB_CHECK_LAUNCH("k_kk_gather_tc");
+    return KKB_OK;
+}
+
+// The split planes are the size of the traces (~600 MB for the bench batch).
+// Keep freed stream-ordered blocks in the device's pool across
+// synchronisations (default release threshold 0 hands them back to the
+// driver at every sync, and remapping them costs milliseconds per call).
+static void keep_pool_blocks() {
     static int pool_kept = -1;
     if (pool_kept < 0) {
         int dev = 0;
@@ -635,6 +673,22 @@ int kk_gather_tc(const float2 *data, int N, int M, int T, const double *ltx, con
         }
         cudaGetLastError();
     }
+}
+
+int kk_gather_tc(const float2 *data, int N, int M, int T, const double *ltx, const double *ltzT,
+                 const double *lrx, const double *lrzT, int nx, int nz, const double *w, double fs,
+                 double shift, int linear, void *out, int out_kind, int n_frames, long long data_fs,
+                 long long out_fs, float *inten, unsigned *fmax, const int *tc_lo, int accum,
+                 cudaStream_t s, const std::function<int(const unsigned *)> &fma_fallback) {
+    if (!tc_lo) return KKB_ERR_UNSUPPORTED;
+    const int NM = N * M;
+    const long long ngroups = (n_frames + 7) / 8;
+    const size_t plane_elems = (size_t)ngroups * NM * T * 8;
+    if (tcg_smem_bytes(N, M) > 227 * 1024) {
+        set_error("kk tensor-core gather: %d pairs do not fit shared memory", NM);
+        return KKB_ERR_UNSUPPORTED;
+    }
+    keep_pool_blocks();
     unsigned *mx = nullptr;  // [n_frames] frame max, then the non-finite flag
     __half *planes = nullptr;
     KKB_TRY_CUDA(cudaMallocAsync(&mx, sizeof(unsigned) * ((size_t)n_frames + 1), s), "cudaMallocAsync(frame max)");
@@ -664,58 +718,22 @@ int kk_gather_tc(const float2 *data, int N, int M, int T, const double *ltx, con
     else
         k_split_planes<1><<<sblocks, 256, 0, s>>>(data, data_fs, n_frames, NM, T, mx, ngroups, planes);
     KKB_CHECK_LAUNCH("k_split_planes");
-    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
-    if (!encode) {
-        cudaDriverEntryPointQueryResult q;
-        void *fn = nullptr;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
-            q != cudaDriverEntryPointSuccess || !fn) {
-            set_error("kk tensor-core gather: cuTensorMapEncodeTiled unavailable");
-            return KKB_ERR_CUDA;
-        }
-        encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
-    }
-    TcgArgs a{};
-    {
-        // (sample, frame) flattened: a window is one 512-byte row of the box
-        const cuuint64_t dims[4] = {8ull * T, (cuuint64_t)NM, (cuuint64_t)ngroups, 4};
-        const cuuint64_t strides[3] = {16ull * T, 16ull * T * NM, 16ull * T * NM * ngroups};
-        const cuuint32_t estr[4] = {1, 1, 1, 1};
-        a.nfb = (int)ceil_div(ngroups, TCG_FB / 8);
-        a.gt = (int)(ngroups - (long long)(a.nfb - 1) * (TCG_FB / 8));
-        CUresult r = CUDA_SUCCESS;
-        for (int one = 0; one < 2 && r == CUDA_SUCCESS; ++one)
-            for (int tl = 0; tl < 2 && r == CUDA_SUCCESS; ++tl) {
-                const cuuint32_t box[4] = {8u * (one ? 16u : (unsigned)TCG_KW), 1, tl ? (cuuint32_t)a.gt : 8u, 4};
-                r = encode(tl ? &a.tail[one] : &a.planes[one], CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, planes, dims,
-                           strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-            }
-        if (r != CUDA_SUCCESS) {
-            set_error("kk tensor-core gather: cuTensorMapEncodeTiled failed (%d)", (int)r);
-            return KKB_ERR_CUDA;
-        }
-    }
-    a.N = N, a.M = M, a.T = T, a.ltx = ltx, a.ltzT = ltzT, a.lrx = lrx, a.lrzT = lrzT, a.w = w;
-    a.fs = fs, a.shift = shift, a.nx = nx, a.nz = nz, a.out = out, a.out_kind = out_kind, a.out_fs = out_fs;
-    a.inten = inten, a.fmax = fmax, a.accum = accum, a.n_frames = n_frames, a.maxabs = mx;
-    a.nonfinite = nonfinite;
-    a.tc_lo = tc_lo;
-    a.tiles_z = (int)ceil_div(nz, TCG_TZ);
-    a.tiles = (long long)a.tiles_z * ceil_div(nx, TCG_TX);
-    a.items = a.tiles * a.nfb;
-    const unsigned grid = (unsigned)std::min<long long>(a.items, sm_count());
-    if (linear) {
-        KKB_TRY_CUDA(cudaFuncSetAttribute(k_kk_gather_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
-                     "smem attr kk tc");
-        k_kk_gather_tc<true><<<grid, TCG_THREADS, smem, s>>>(a);
-    } else {
-        KKB_TRY_CUDA(cudaFuncSetAttribute(k_kk_gather_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
-                     "smem attr kk tc");
-        k_kk_gather_tc<false><<<grid, TCG_THREADS, smem, s>>>(a);
-    }
-    KKB_CHECK_LAUNCH("k_kk_gather_tc");
+    int st = tcg_launch(planes, mx, nonfinite, N, M, T, ltx, ltzT, lrx, lrzT, nx, nz, w, fs, shift, linear, out,
+                        out_kind, n_frames, out_fs, inten, fmax, tc_lo, accum, s);
+    if (st) return st;
     // the FMA gather, live only when the batch held a non-finite sample
+    return fma_fallback(nonfinite);
+}
+
+int kk_gather_tc_planes(const __half *planes, const unsigned *fbound, const unsigned *nonfinite, int N, int M,
+                        int T, const double *ltx, const double *ltzT, const double *lrx, const double *lrzT, int nx,
+                        int nz, const double *w, double fs, double shift, int linear, void *out, int out_kind,
+                        int n_frames, long long out_fs, float *inten, unsigned *fmax, const int *tc_lo, int accum,
+                        cudaStream_t s, const std::function<int(const unsigned *)> &fma_fallback) {
+    if (!tc_lo || tcg_smem_bytes(N, M) > 227 * 1024) return KKB_ERR_UNSUPPORTED;
+    int st = tcg_launch(planes, fbound, nonfinite, N, M, T, ltx, ltzT, lrx, lrzT, nx, nz, w, fs, shift, linear, out,
+                        out_kind, n_frames, out_fs, inten, fmax, tc_lo, accum, s);
+    if (st) return st;
     return fma_fallback(nonfinite);
 }
 

@@ -39,7 +39,7 @@ class KKEngine:
                  chunk_frames: int | None = None, pipeline: tuple | None = None,
                  interpolation: str = "linear",
                  pulse_delay: float = 0.0, channel_weights=None, floor_db: float = -60.0,
-                 want_db: bool = True, groups: int = 1):
+                 want_db: bool = True, groups: int = 1, fuse_tc: bool = False):
         t = dev.require_cuda()
         self.t = t
         self.array, self.params, self.receive, self.grid = array, params, receive, grid
@@ -88,6 +88,21 @@ class KKEngine:
         self.inten = t.empty((F, X, Z), dtype=t.float32, device="cuda")
         self.fmax = t.zeros((F,), dtype=t.int32, device="cuda")
         self.db = t.empty((F, X, Z), dtype=t.float32, device="cuda") if want_db else None
+        # fused stage 1 -> tensor-core gather (fuse_tc): K3 writes the gather's
+        # split fp16 planes (kkb_decomposer_run_planes) instead of complex64
+        # traces, so the gather skips its own frame-max and split passes.  Used
+        # for whole float32 batches the tensor-core gather takes; self.traces
+        # then holds traces only for a batch with a NaN / Inf bin.
+        self.fused = False
+        self._planes_frames = 0
+        min_f = 48 if self.linear else 128   # kk.cuh KKB_KK_TC_MIN_FRAMES(_NEAREST)
+        if (fuse_tc and self.T in (1024, 1536, 2048) and pipeline is None and self.chunk == F and F >= min_f
+                and int(lib.kkb_kk_plan_tc_ksteps(kp)) > 0):
+            nb = int(lib.kkb_tc_planes_bytes(F, N * M, T))
+            self._planes = t.empty((nb,), dtype=t.uint8, device="cuda")
+            self._fbound = t.zeros((F,), dtype=t.int32, device="cuda")
+            self._nonfinite = t.zeros((1,), dtype=t.int32, device="cuda")
+            self.fused = True
         self._closed = False
 
     def _new_decomposer(self, chunk: int):
@@ -129,8 +144,21 @@ class KKEngine:
     def decompose(self, rf, n_frames: int | None = None, stream=None):
         F = self.F if n_frames is None else n_frames
         self._check_rf(rf, F)
+        if self.fused and F == self.F and rf.dtype == self.t.float32:
+            _lib.call("kkb_decomposer_run_planes", self._dec, dev.ptr(rf), F, dev.ptr(self._planes),
+                      dev.ptr(self._fbound), dev.ptr(self._nonfinite), dev.ptr(self.traces),
+                      dev.stream_handle(stream))
+            self._planes_frames = F
+            return self.traces[:F]
+        self._planes_frames = 0
         self._run_decomposer(self._dec, rf, F, self.traces, dev.stream_handle(stream))
         return self.traces[:F]
+
+    def _run_planes(self, F, iq, inten, fmax, accumulate, s):
+        P = self.grid.nx * self.grid.nz
+        _lib.call("kkb_kk_plan_run_planes", self._kk, dev.ptr(self._planes), dev.ptr(self._fbound),
+                  dev.ptr(self._nonfinite), dev.ptr(self.traces), F, dev.ptr(iq), _lib.KKB_OUT_C64, P,
+                  dev.ptr(inten), dev.ptr(fmax), _lib.KKB_RUN_ACCUMULATE_INTENSITY if accumulate else 0, s)
 
     def beamform(self, traces=None, n_frames: int | None = None, stream=None, out_offset: int = 0,
                  inten=None, fmax=None, accumulate: bool = False, want_db: bool | None = None):
@@ -144,9 +172,12 @@ class KKEngine:
         iq = self.iq[out_offset:out_offset + F]
         inten = (self.inten if inten is None else inten)[out_offset:out_offset + F]
         fmax = None if fmax is False else (self.fmax if fmax is None else fmax)[out_offset:out_offset + F]
-        _lib.call("kkb_kk_plan_run_ex", self._kk, dev.ptr(traces), F, self.N * self.M * self.T,
-                  dev.ptr(iq), _lib.KKB_OUT_C64, P, dev.ptr(inten), dev.ptr(fmax),
-                  _lib.KKB_RUN_ACCUMULATE_INTENSITY if accumulate else 0, s)
+        if traces is self.traces and out_offset == 0 and F == self._planes_frames:
+            self._run_planes(F, iq, inten, fmax, accumulate, s)
+        else:
+            _lib.call("kkb_kk_plan_run_ex", self._kk, dev.ptr(traces), F, self.N * self.M * self.T,
+                      dev.ptr(iq), _lib.KKB_OUT_C64, P, dev.ptr(inten), dev.ptr(fmax),
+                      _lib.KKB_RUN_ACCUMULATE_INTENSITY if accumulate else 0, s)
         if self.want_db if want_db is None else want_db:
             db = self.db[out_offset:out_offset + F]
             _lib.call("kkb_log_compress", dev.ptr(inten), dev.ptr(fmax), F, P, self.floor_db,
@@ -158,6 +189,9 @@ class KKEngine:
         F = self.F if n_frames is None else n_frames
         P = self.grid.nx * self.grid.nz
         fmax = self.fmax[:F]
+        if F == self._planes_frames:
+            self._run_planes(F, self.iq, self.inten, fmax, False, dev.stream_handle(stream))
+            return self.iq[:F]
         _lib.call("kkb_kk_plan_run", self._kk, dev.ptr(self.traces), F, self.N * self.M * self.T,
                   dev.ptr(self.iq), _lib.KKB_OUT_C64, P, dev.ptr(self.inten), dev.ptr(fmax),
                   dev.stream_handle(stream))
@@ -196,6 +230,7 @@ class KKEngine:
             self._side = t.cuda.Stream()
         side = self._side
         side.wait_stream(main)  # outputs may still be read by earlier work on main
+        self._planes_frames = 0
         NMT = self.N * self.M * self.T
         for g in range(groups):
             f0, f1 = balanced_range(self.F, g, groups)
@@ -249,6 +284,7 @@ class KKEngine:
                 iq_host.dtype != t.complex64:
             raise ConfigError(f"expected a host complex64 IQ buffer of shape {(F, self.grid.nx, self.grid.nz)}")
         C = max(1, min(chunk_frames, self.chunk, F))
+        self._planes_frames = 0
         if streams is None:
             streams = [t.cuda.Stream(), t.cuda.Stream()]
         cur = t.cuda.current_stream()
