@@ -448,32 +448,34 @@ k_c2c(const float2 *__restrict__ in, long long in_stride, int in_len, float2 *__
 
 // K3 into the tensor-core gather's split planes (tcplanes.cuh): inverse
 // transforms of the contracted bins Y (rows (frame, pair), row stride ldy,
-// bins [0, K)).  A CTA takes the 8 frames of one frame group of one pair q:
-// eight transforms side by side (threads [i NT, (i + 1) NT) take frame i,
-// each in its own T-point buffer), each output scaled by its frame's power
-// of two (from the frame bound fbound[f]) and split into fp16 halves, staged
-// in the freed buffers as [plane][sample][8 frames] and stored as coalesced
-// 16-byte rows.  Frames past n_frames stage zeros.  When *nonfinite is set
-// the complex64 traces are written too (the FMA gather, which then runs
-// instead, reads them).
+// bins [0, K)).  A CTA takes 4 frames (half a frame group) of one pair q:
+// four transforms side by side (threads [i NT, (i + 1) NT) take frame i, each
+// in its own T-point buffer with its own named barrier), each output scaled
+// by its frame's power of two (from the frame bound fbound[f]) and split into
+// fp16 halves, staged in the freed buffers as [frame][sample] 8-byte entries
+// (the four planes' halves) and stored as the 8-byte halves of the planes'
+// 16-byte rows (two CTAs fill a row; two CTAs per SM overlap their phases).
+// Frames past n_frames stage zeros.  When *nonfinite is set the complex64
+// traces are written too (the FMA gather, which then runs instead, reads them).
 template <int T>
-__global__ void __launch_bounds__(8 * Plan<T>::NT)
+__global__ void __launch_bounds__(4 * Plan<T>::NT, 2)
 k_c2c_planes(const float2 *__restrict__ Y, long long ldy, int K, int n_frames, int NM, float scale,
              const float2 *__restrict__ tw, const unsigned *__restrict__ fbound,
              const unsigned *__restrict__ nonfinite, float2 *__restrict__ traces, __half *__restrict__ planes,
              long long per_plane) {
     using P = Plan<T>;
     extern __shared__ __align__(16) unsigned char dsm[];
-    float2 *bufs = reinterpret_cast<float2 *>(dsm);  // [8][T]; then the stage [8 frames][T][4 planes] fp16
+    float2 *bufs = reinterpret_cast<float2 *>(dsm);  // [4][T]; then the stage [4 frames][T] uint2
     uint2 *stage = reinterpret_cast<uint2 *>(dsm);
     const int q = blockIdx.x % NM;
-    const long long g = blockIdx.x / NM;
-    const int i = threadIdx.x / P::NT;  // frame of the group
-    const long long f = g * 8 + i, row = f * NM + q;
+    const long long gh = blockIdx.x / NM, g = gh >> 1;
+    const int half = (int)(gh & 1);
+    const int i = threadIdx.x / P::NT;  // frame of the half group
+    const long long f = g * 8 + half * 4 + i, row = f * NM + q;
     const bool live = f < n_frames;
     using S2 = Stage<T, P::NT, P::R2>;
     S2 c;
-    c2c_row<T, true>(live ? Y + row * ldy : Y, live ? K : 0, tw, bufs + (size_t)i * T, c, 1 + i);  // own barrier
+    c2c_row<T, true>(live ? Y + row * ldy : Y, live ? K : 0, tw, bufs + (size_t)i * T, c, 1 + i);
     const bool flag = *nonfinite != 0;
     const float sc = live ? frame_scale(__ldg(fbound + f)) : 0.f;
     __syncthreads();  // every transform's buffer read: reuse them as the stage
@@ -494,24 +496,19 @@ k_c2c_planes(const float2 *__restrict__ Y, long long ldy, int K, int n_frames, i
         }
     }
     __syncthreads();
-    // per sample k: the 8 frames' 8-byte entries in, the four planes' 16-byte
-    // rows out (conflict-free 64-bit loads, coalesced 128-bit stores)
-    uint4 *dst = reinterpret_cast<uint4 *>(planes) + (g * NM + q) * T;
+    // per sample k: the 4 frames' 8-byte entries in, the four planes' 8-byte
+    // half rows out (conflict-free 64-bit loads, coalesced 64-bit stores)
+    uint2 *dst = reinterpret_cast<uint2 *>(planes) + ((g * NM + q) * T) * 2 + half;
     for (int k = threadIdx.x; k < T; k += blockDim.x) {
-        uint2 e[8];
+        uint2 e[4];
 #pragma unroll
-        for (int fi = 0; fi < 8; ++fi) e[fi] = stage[fi * T + k];
+        for (int fi = 0; fi < 4; ++fi) e[fi] = stage[fi * T + k];
         // e.x = (re hi, im hi), e.y = (re lo, im lo) of one frame
-        auto lo16 = [](uint32_t v) { return v & 0xffffu; };
-        auto hi16 = [](uint32_t v) { return v >> 16; };
-        dst[0 * (per_plane / 8) + k] = make_uint4(lo16(e[0].x) | lo16(e[1].x) << 16, lo16(e[2].x) | lo16(e[3].x) << 16,
-                                                  lo16(e[4].x) | lo16(e[5].x) << 16, lo16(e[6].x) | lo16(e[7].x) << 16);
-        dst[1 * (per_plane / 8) + k] = make_uint4(hi16(e[0].x) | hi16(e[1].x) << 16, hi16(e[2].x) | hi16(e[3].x) << 16,
-                                                  hi16(e[4].x) | hi16(e[5].x) << 16, hi16(e[6].x) | hi16(e[7].x) << 16);
-        dst[2 * (per_plane / 8) + k] = make_uint4(lo16(e[0].y) | lo16(e[1].y) << 16, lo16(e[2].y) | lo16(e[3].y) << 16,
-                                                  lo16(e[4].y) | lo16(e[5].y) << 16, lo16(e[6].y) | lo16(e[7].y) << 16);
-        dst[3 * (per_plane / 8) + k] = make_uint4(hi16(e[0].y) | hi16(e[1].y) << 16, hi16(e[2].y) | hi16(e[3].y) << 16,
-                                                  hi16(e[4].y) | hi16(e[5].y) << 16, hi16(e[6].y) | hi16(e[7].y) << 16);
+        const long long o = 2LL * k;
+        dst[0 * (per_plane / 4) + o] = make_uint2((e[0].x & 0xffffu) | (e[1].x << 16), (e[2].x & 0xffffu) | (e[3].x << 16));
+        dst[1 * (per_plane / 4) + o] = make_uint2((e[0].x >> 16) | (e[1].x & 0xffff0000u), (e[2].x >> 16) | (e[3].x & 0xffff0000u));
+        dst[2 * (per_plane / 4) + o] = make_uint2((e[0].y & 0xffffu) | (e[1].y << 16), (e[2].y & 0xffffu) | (e[3].y << 16));
+        dst[3 * (per_plane / 4) + o] = make_uint2((e[0].y >> 16) | (e[1].y & 0xffff0000u), (e[2].y >> 16) | (e[3].y & 0xffff0000u));
     }
 }
 
@@ -664,10 +661,10 @@ static int launch_c2c_planes(const float2 *Y, long long ldy, int K, int n_frames
                              __half *planes, cudaStream_t s) {
     const long long groups = (n_frames + 7) / 8;
     const long long per_plane = groups * 8 * NM * (long long)T;
-    const size_t smem = sizeof(float2) * 8 * (size_t)T;  // 8 transform buffers, then the fp16 stage
+    const size_t smem = sizeof(float2) * 4 * (size_t)T;  // 4 transform buffers, then the fp16 stage
     KKB_TRY_CUDA(cudaFuncSetAttribute(ct::k_c2c_planes<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                  "smem attr c2c planes");
-    ct::k_c2c_planes<T><<<(unsigned)(groups * NM), 8 * ct::Plan<T>::NT, smem, s>>>(
+    ct::k_c2c_planes<T><<<(unsigned)(groups * 2 * NM), 4 * ct::Plan<T>::NT, smem, s>>>(
         Y, ldy, K, n_frames, NM, scale, tw, fbound, nonfinite, traces, planes, per_plane);
     KKB_CHECK_LAUNCH("k_c2c_planes");
     return KKB_OK;
