@@ -104,3 +104,45 @@ def test_fused_nonfinite_standby(monkeypatch):
     assert torch.equal(a[m], b[m])
     fused.close()
     plain.close()
+
+
+@pytest.mark.parametrize("cfg", [2, 3])
+def test_fused_other_lengths(oracle, cfg):
+    """T = 2048 workloads (config 2: 15 x 5 pairs on 256 x 400 px; config 3's
+    dense vernier set, 81 pairs on 384 x 512): the fused path against the
+    unfused engine (every frame) and the oracle (first and last frame)."""
+    import torch
+
+    F = 56
+    w = configs.CONFIGS[cfg]()
+    arr, p, rx, g = w.array, w.params, w.receive, w.grid
+    base, rf = _rf(w, F, 900 + cfg, distinct=4)
+    fused = kb.KKEngine(arr, p, rx, g, frames=F, fuse_tc=True, want_db=False)
+    plain = kb.KKEngine(arr, p, rx, g, frames=F, want_db=False)
+    assert fused.fused
+    fused.run(rf)
+    plain.run(rf)
+    torch.cuda.synchronize()
+    for f in range(F):
+        assert _rel(fused.iq[f], plain.iq[f]) <= 3e-6, f
+    got = fused.iq.cpu().numpy()
+    fs, c = arr.sampling_frequency, p.sound_speed
+    luts = oracle.kk_luts(g.x, g.z, p.transmit_angles, rx.angles, c)
+    shift = (0.0 - p.start_time) * fs
+    for f in (0, F - 1):
+        tr = oracle.decompose_f64(base[f % len(base)], fs, arr.positions, rx.angles, c)
+        ref = oracle.kk_kernel(tr, *luts, np.ones(rx.num_angles), fs, shift)
+        assert rel_l2(got[f], ref) <= 1e-5, (cfg, f)
+    fused.close()
+    plain.close()
+
+
+def test_fused_falls_back_when_ineligible():
+    """Config 1's steep delays exceed the tensor-core tile's 32-sample
+    windows: fuse_tc quietly keeps the complex64 path (and small batches, or
+    batches below the crossover, never fuse)."""
+    w = configs.config1()
+    arr, p, rx, g = w.array, w.params, w.receive, w.grid
+    assert not kb.KKEngine(arr, p, rx, g, frames=64, fuse_tc=True).fused
+    w4 = configs.config4(frames=16)
+    assert not kb.KKEngine(w4.array, w4.params, w4.receive, w4.grid, frames=16, fuse_tc=True).fused
