@@ -17,10 +17,10 @@ import paper_2603_22496_b200 as kb  # noqa: E402
 from paper_2603_22496_b200 import configs  # noqa: E402
 
 
-def device_rate(w, params, rx, frames, reps=5):
+def device_rate(w, params, rx, frames, reps=5, fuse_tc=False):
     import torch
 
-    eng = kb.KKEngine(w.array, params, rx, w.grid, frames=frames)
+    eng = kb.KKEngine(w.array, params, rx, w.grid, frames=frames, fuse_tc=fuse_tc)
     N, L, T = params.num_transmits, w.array.num_elements, params.num_samples
     base = configs.noise_rf(N, L, T, seed=0)
     rf = torch.from_numpy(np.broadcast_to(base, (frames,) + base.shape).copy()).cuda()
@@ -35,6 +35,9 @@ def device_rate(w, params, rx, frames, reps=5):
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / reps
     pp = eng.pixel_pairs_per_frame
+    if fuse_tc:
+        from paper_2603_22496_b200 import _lib
+        pp = (pp, eng.fused, _lib.KKB_KK_INST_NAMES[_lib.last_instance() & 15])
     eng.close()
     return ms, pp
 
@@ -106,6 +109,10 @@ def main():
                "gpu_ms_per_frame_batched": ms_b / F, "batch": F,
                "gpu_ms_single_frame": ms_1, "pixel_pairs_per_s": pp / (ms_b / F / 1e3),
                "cpu_port_ms_per_frame": cpu, "cpu_threads": os.cpu_count()}
+        if not big:  # large batches: the tensor-core gather (fused from stage 1 where eligible)
+            ms_l, (_, fused, inst) = device_rate(w, p, rx, 128, reps=3, fuse_tc=True)
+            row.update({"gpu_ms_per_frame_batch128": ms_l / 128, "batch128_gather": inst,
+                        "batch128_fused_stage1": fused, "pixel_pairs_per_s_batch128": pp / (ms_l / 128 / 1e3)})
         out.append(row)
         print(json.dumps(row), flush=True)
     # config 3 hybrid compounded incoherently (cli.py:257-266): confocal(25, 3)
