@@ -146,3 +146,29 @@ def test_fused_falls_back_when_ineligible():
     assert not kb.KKEngine(arr, p, rx, g, frames=64, fuse_tc=True).fused
     w4 = configs.config4(frames=16)
     assert not kb.KKEngine(w4.array, w4.params, w4.receive, w4.grid, frames=16, fuse_tc=True).fused
+
+
+@pytest.mark.parametrize("fuse", [True, False])
+def test_tensor_core_path_graph_replay(fuse):
+    """KKEngine.capture on a 64-frame config-4 batch (the tcgen05 gather, with
+    and without the fused planes): replays on new RF equal the eager run bit
+    for bit (the gather's scratch is stream-ordered, so it lives in the graph)."""
+    import torch
+
+    F = 64
+    w = configs.config4(frames=F)
+    arr, p, rx, g = w.array, w.params, w.receive, w.grid
+    eng = kb.KKEngine(arr, p, rx, g, frames=F, fuse_tc=fuse)
+    _, rf0 = _rf(w, F, 40, distinct=2)
+    rf = rf0.clone()
+    graph = eng.capture(rf)
+    for seed in (50, 60):
+        _, new = _rf(w, F, seed, distinct=2)
+        ref = eng.run(new).clone()
+        torch.cuda.synchronize()
+        assert _lib.last_instance() == _lib.KKB_KK_INST_TC
+        rf.copy_(new)
+        got = graph.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(got, ref)
+    eng.close()
