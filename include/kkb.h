@@ -293,6 +293,24 @@ int kkb_decomposer_symmetric_classes(const kkb_decomposer *p);
 #define KKB_CONTRACT_TENSOR 1
 int kkb_decomposer_set_contraction(kkb_decomposer *p, int form);
 int kkb_decomposer_contraction(const kkb_decomposer *p);
+/* Fused stage 1 (opt-in): the real FFT (K1) and the symmetric FMA
+ * contraction (K2) as ONE warp-specialised kernel per (frame, transmit) row,
+ * the per-element spectra kept in shared memory instead of round-tripping
+ * through HBM (replaces rfft * one_sided / T and the compress einsum,
+ * spectral.py:84-93, compress.py:78-81): 3.8 instead of 11.6 GB of DRAM
+ * traffic per 400 config-4 frames, but measured slower than K1 -> K2 on the
+ * B200 (issue- and latency-bound), so plans default to K1 -> K2.
+ * Its phase factors come from float64 phases anchored every four element
+ * pairs and stepped by the per-element rotation, so it needs a uniform array
+ * (the reference's TransducerArray, core.py:32-38); eligible plans: T = 1536,
+ * L a multiple of 8 up to 256, symmetric receive set with <= 6 classes
+ * (M <= 12).  Traces differ from the unfused path by ~1e-7 relative (both
+ * within the 1e-5 bound).  set_fused(p, 1) selects it (environment
+ * KKB_S1_FUSED=1 at creation); set_fused(p, 1) on an ineligible plan is
+ * KKB_ERR_UNSUPPORTED.  fused() reports whether the plan's stage 1 runs
+ * fused. */
+int kkb_decomposer_set_fused(kkb_decomposer *p, int on);
+int kkb_decomposer_fused(const kkb_decomposer *p);
 /* Stage-1 ring mode: K1 (real FFT) and a persistent K2 (contraction, FMA
  * form) run concurrently, the spectra handed over through `slots` row-tile
  * slots of an L2-resident ring (16 (frame, transmit) rows each) instead of a

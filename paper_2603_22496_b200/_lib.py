@@ -64,6 +64,8 @@ SIGNATURES = {
     "kkb_decomposer_symmetric_classes": [P],
     "kkb_decomposer_set_contraction": [P, I],
     "kkb_decomposer_contraction": [P],
+    "kkb_decomposer_set_fused": [P, I],
+    "kkb_decomposer_fused": [P],
     "kkb_decomposer_set_ring": [P, I, I],
     "kkb_decomposer_ring_error": [P, P],
     "kkb_decomposer_workspace_bytes": [P],

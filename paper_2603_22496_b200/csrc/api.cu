@@ -551,6 +551,7 @@ extern "C" int kkb_shear_and_sum(const void *data, int n_tx, int n_el, int n_t,
 // fused stage-1 plan
 struct kkb_decomposer {
     int N, L, T, M, K, ldk, chunk;  // ldk: spectral row stride (K rounded up to even)
+    double fs = 0.0;
     float2 *ramps = nullptr;
     float2 *X = nullptr;            // slots x chunk frames of spectra
     float2 *Y = nullptr;            // slots x chunk frames of contracted bins
@@ -574,6 +575,10 @@ struct kkb_decomposer {
     float *tctab = nullptr;
     // stage-1 ring mode (kkb_decomposer_set_ring): K1 and a persistent K2 run
     // concurrently, the spectra passing through R L2-resident row-tile slots
+    // fused stage 1 (stage1_fused.cu, kkb_decomposer_set_fused): K1 + K2 in one
+    // kernel for a uniform symmetric array
+    int s1f_ok = 0, s1f_on = 0;
+    float2 *s1f_gam = nullptr;  // (P, L/8 + 1) split phase slopes (stage1_fused_table)
     int ring_R = 0, ring_ctas = 0;
     float2 *ring = nullptr;
     int *ring_cnt = nullptr;  // fft_done[tiles] | con_done[tiles] | queue | started | err
@@ -626,6 +631,32 @@ static int build_symmetric_classes(kkb_decomposer *p, const double *pos, const d
     p->mp = mp;
     p->mm = mm;
     p->bytes += (long long)(sizeof(float2) * (size_t)P * Lp * p->ldk);
+    // fused stage 1: needs a uniform array (the phase is linear in the element
+    // index) and a length / class count the kernel is built for
+    if (stage1_fused_supported(p->T, L, P)) {
+        const double step = (pos[L - 1] - pos[0]) / (L - 1);
+        bool uniform = step > 0;
+        for (int l = 0; l + 1 < L && uniform; ++l)
+            uniform = fabs((pos[l + 1] - pos[l]) - step) <= 1e-9 * step;
+        if (uniform) {
+            const int Lh = L / 2;
+            std::vector<double> t((size_t)P * (Lh + 1));
+            for (int q = 0; q < P; ++q) {
+                for (int j = 0; j < Lh; ++j) t[(size_t)q * (Lh + 1) + j] = tau[(size_t)j * P + q];
+                t[(size_t)q * (Lh + 1) + Lh] = step * (sin(ang[mp[q]]) / c);
+            }
+            std::vector<float2> gam;
+            stage1_fused_table(t.data(), P, L, 1.0 / (p->T * (1.0 / p->fs)), gam);  // fftfreq's bin spacing
+            KKB_TRY_CUDA(cudaMalloc(&p->s1f_gam, sizeof(float2) * gam.size()), "cudaMalloc(s1f table)");
+            KKB_TRY_CUDA(cudaMemcpy(p->s1f_gam, gam.data(), sizeof(float2) * gam.size(), cudaMemcpyHostToDevice),
+                         "copy s1f table");
+            p->bytes += (long long)(sizeof(float2) * gam.size());
+            p->s1f_ok = 1;
+            // opt-in: measured slower than K1 -> K2 at config 4
+            const char *e = getenv("KKB_S1_FUSED");
+            p->s1f_on = e && e[0] == '1';
+        }
+    }
     return KKB_OK;
 }
 
@@ -650,6 +681,7 @@ extern "C" int kkb_decomposer_create(int n_tx, int n_el, int n_t, const double *
     p->K = n_t / 2 + 1;
     p->ldk = p->K + (p->K & 1);
     p->chunk = max_frames;
+    p->fs = fs;
     const int K = p->K, ldk = p->ldk;
     std::vector<double> tau((size_t)n_el * n_rx), freq(K), scale(K);
     for (int m = 0; m < n_rx; ++m) {
@@ -694,6 +726,7 @@ extern "C" int kkb_decomposer_create(int n_tx, int n_el, int n_t, const double *
         cudaFree(p->X);
         cudaFree(p->Y);
         cudaFree(p->cs);
+        cudaFree(p->s1f_gam);
         delete p;
         return st;
     }
@@ -726,6 +759,21 @@ extern "C" int kkb_decomposer_set_contraction(kkb_decomposer *p, int form) {
 }
 
 extern "C" int kkb_decomposer_contraction(const kkb_decomposer *p) { return p ? p->form : -1; }
+
+extern "C" int kkb_decomposer_set_fused(kkb_decomposer *p, int on) {
+    if (!p || (on != 0 && on != 1)) return KKB_ERR_ARG;
+    if (on && !p->s1f_ok) {
+        set_error("fused stage 1 needs T = 1536, L a multiple of 8, a uniform symmetric array and <= 6 angle classes");
+        return KKB_ERR_UNSUPPORTED;
+    }
+    p->s1f_on = on;
+    return KKB_OK;
+}
+
+extern "C" int kkb_decomposer_fused(const kkb_decomposer *p) { return p ? (p->s1f_ok && p->s1f_on) : -1; }
+
+// the fused stage-1 kernel runs instead of K1 -> K2 (FMA form, no ring)
+static bool use_s1f(const kkb_decomposer *p) { return p->s1f_ok && p->s1f_on && p->form == KKB_CONTRACT_FMA; }
 
 extern "C" int kkb_decomposer_set_ring(kkb_decomposer *p, int slots, int consumer_ctas) {
     if (!p || slots < 0 || slots == 1 || consumer_ctas < 0) {
@@ -857,7 +905,10 @@ static int decomposer_run(kkb_decomposer *p, const void *rf, int in_kind, int n_
             if ((st = decomposer_run_ring(p, rf_c, in_kind, F, tr_c, cs))) return st;
             continue;
         }
-        if (i16_direct) {
+        if (use_s1f(p) && (in_kind == 0 || i16_direct)) {
+            st = stage1_fused(rf_c, in_kind, (long long)F * N, L, T, p->s1f_gam, Y, ldk, M, p->P,
+                              p->mp.data(), p->mm.data(), plan.tws, cs);
+        } else if (i16_direct) {
             st = fft_r2c_ct(rf_c, 1, (long long)F * N * L, T, X, ldk, K, nullptr, plan.tws, cs, L);
         } else if (plan.direct || plan.large) {
             // lengths without a single-CTA real plan: promote to complex first
@@ -872,7 +923,9 @@ static int decomposer_run(kkb_decomposer *p, const void *rf, int in_kind, int n_
         }
         if (conv) cudaFreeAsync(conv, cs);
         if (st) return st;
-        if (p->form == KKB_CONTRACT_TENSOR)
+        if (use_s1f(p) && (in_kind == 0 || i16_direct))
+            st = KKB_OK;  // Y written by the fused kernel
+        else if (p->form == KKB_CONTRACT_TENSOR)
             st = contract_tc(X, ldk, p->tctab, Y, ldk, (long long)F * N, L, M, K, p->P, p->mp.data(),
                              p->mm.data(), cs);
         else if (p->P > 0)
@@ -1025,10 +1078,16 @@ extern "C" int kkb_decomposer_run_planes(kkb_decomposer *p, const float *rf, int
     KKB_TRY_CUDA(cudaMemsetAsync(nonfinite, 0, sizeof(unsigned), s), "zero flag");
     if (n_frames == 0) return KKB_OK;
     int st;
-    if ((st = kkb_decomposer_run_stage(p, 0, rf, n_frames, nullptr, stream))) return st;
-    if ((st = kkb_decomposer_run_stage(p, 1, rf, n_frames, nullptr, stream))) return st;
     FftPlan plan;
     if ((st = get_fft_plan(p->T, &plan))) return st;
+    if (use_s1f(p)) {
+        if ((st = stage1_fused(rf, 0, (long long)n_frames * p->N, p->L, p->T, p->s1f_gam, p->Y, p->ldk,
+                               p->M, p->P, p->mp.data(), p->mm.data(), plan.tws, s)))
+            return st;
+    } else {
+        if ((st = kkb_decomposer_run_stage(p, 0, rf, n_frames, nullptr, stream))) return st;
+        if ((st = kkb_decomposer_run_stage(p, 1, rf, n_frames, nullptr, stream))) return st;
+    }
     const long long rows = (long long)n_frames * p->N * p->M;
     if ((st = frame_bound(p->Y, p->ldk, p->K, rows, p->N * p->M, 1.0f, fbound, nonfinite, s))) return st;
     return fft_c2c_planes(p->Y, p->ldk, p->K, p->T, n_frames, p->N * p->M, 1.0f, plan.tws, fbound, nonfinite,
@@ -1114,6 +1173,7 @@ extern "C" int kkb_decomposer_destroy(kkb_decomposer *p) {
     cudaFree(p->X);
     cudaFree(p->Y);
     cudaFree(p->cs);
+    cudaFree(p->s1f_gam);
     cudaFree(p->tctab);
     cudaFree(p->ring);
     cudaFree(p->ring_cnt);

@@ -1,6 +1,8 @@
 // Internal declarations of the gather / LUT / epilogue / decomposition kernels.
 #pragma once
 
+#include <vector>
+
 #include <functional>
 
 #include <cuda_fp16.h>
@@ -177,6 +179,15 @@ int contract_sym_ring(const float2 *ring, long long ldx, const float2 *CS, long 
                       long long ldy, long long B, int L, int M, int Kb, int P, const short *mp,
                       const short *mm, const Stage1Ring &rs, int *queue, int *started, int nctas,
                       cudaStream_t s);
+// fused stage 1 (stage1_fused.cu): K1 + K2 in one kernel for uniform
+// symmetric arrays.  stage1_fused_table turns the float64 class delays tau
+// (P, L/2 + 1: tau[q][j] for j < L/2, the per-element step at tau[q][L/2])
+// and the bin spacing fsT into the kernel's split phase slopes gam
+// (P, L/8 + 1 float2)
+bool stage1_fused_supported(int T, int L, int P);
+void stage1_fused_table(const double *tau, int P, int L, double fsT, std::vector<float2> &out);
+int stage1_fused(const void *rf, int in_kind, long long B, int L, int T, const float2 *gam, float2 *Y,
+                 long long ldy, int M, int P, const short *mp, const short *mm, const float2 *tws, cudaStream_t s);
 // tensor-core (tcgen05, 3xTF32) form of contract_sym (contract_tc.cu)
 int build_tc_table(const float2 *cs, long long ldc, int P, int L, int Kb, float **tab, long long *bytes,
                    cudaStream_t s);
