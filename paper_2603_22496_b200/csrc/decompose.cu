@@ -373,8 +373,10 @@ k_contract_sym(const float2 *__restrict__ X, long long ldx, const float2 *__rest
                long long ldc, float2 *__restrict__ Y, long long ldy, long long B, int L, int M,
                int Kb, const SymClasses cls) {
     extern __shared__ __align__(16) float2 csm[];
+    // row tiles last to first: K1 wrote the last rows' spectra most recently,
+    // so the first tiles scheduled find them in L2
     contract_sym_tile<PC, NB>(X, ldx, CS, ldc, Y, ldy, B, L, M, Kb, cls, blockIdx.x * KKB_CT_KT,
-                              (long long)blockIdx.y * (8 * NB), blockIdx.z * PC, csm);
+                              (long long)(gridDim.y - 1 - blockIdx.y) * (8 * NB), blockIdx.z * PC, csm);
 }
 
 // Persistent consumer of the stage-1 ring (Stage1Ring, fft.cuh): work item

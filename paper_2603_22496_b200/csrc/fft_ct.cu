@@ -232,8 +232,11 @@ k_c2c_planes(const float2 *__restrict__ Y, long long ldy, int K, int n_frames, i
     extern __shared__ __align__(16) unsigned char dsm[];
     float2 *bufs = reinterpret_cast<float2 *>(dsm);  // [4][T]; then the stage [4 frames][T] uint2
     uint2 *stage = reinterpret_cast<uint2 *>(dsm);
-    const int q = blockIdx.x % NM;
-    const long long gh = blockIdx.x / NM, g = gh >> 1;
+    // CTAs last to first: the frame bound just read the highest rows of Y
+    // (L2-resident), and the gather starts from the lowest frames' planes
+    const unsigned bid = gridDim.x - 1 - blockIdx.x;
+    const int q = bid % NM;
+    const long long gh = bid / NM, g = gh >> 1;
     const int half = (int)(gh & 1);
     const int i = threadIdx.x / P::NT;  // frame of the half group
     const long long f = g * 8 + half * 4 + i, row = f * NM + q;
@@ -284,6 +287,8 @@ k_c2c_planes(const float2 *__restrict__ Y, long long ldy, int K, int n_frames, i
 __global__ void __launch_bounds__(256) k_frame_bound(const float2 *__restrict__ Y, long long ldy, int K,
                                                      long long rows, int rows_per_frame, float scale,
                                                      unsigned *__restrict__ fbound, unsigned *__restrict__ nonfinite) {
+    // rows first to last: K2 runs its row tiles backwards, so the lowest rows
+    // are the ones still in L2 (and K3 then starts from the highest)
     const long long row = (long long)blockIdx.x * 8 + (threadIdx.x >> 5);
     if (row >= rows) return;
     const int lane = threadIdx.x & 31;
