@@ -573,12 +573,12 @@ struct kkb_decomposer {
     // 3xTF32 class tables in the UMMA operand layout, built on first use
     int form = KKB_CONTRACT_FMA;
     float *tctab = nullptr;
-    // stage-1 ring mode (kkb_decomposer_set_ring): K1 and a persistent K2 run
-    // concurrently, the spectra passing through R L2-resident row-tile slots
     // fused stage 1 (stage1_fused.cu, kkb_decomposer_set_fused): K1 + K2 in one
     // kernel for a uniform symmetric array
     int s1f_ok = 0, s1f_on = 0;
     float2 *s1f_gam = nullptr;  // (P, L/8 + 1) split phase slopes (stage1_fused_table)
+    // stage-1 ring mode (kkb_decomposer_set_ring): K1 and a persistent K2 run
+    // concurrently, the spectra passing through R L2-resident row-tile slots
     int ring_R = 0, ring_ctas = 0;
     float2 *ring = nullptr;
     int *ring_cnt = nullptr;  // fft_done[tiles] | con_done[tiles] | queue | started | err

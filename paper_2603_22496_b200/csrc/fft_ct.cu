@@ -256,10 +256,9 @@ k_c2c_planes(const float2 *__restrict__ Y, long long ldy, int K, int n_frames, i
             if (S2::ok(j)) {
                 const float2 x = make_float2(c.v[t][r].x * scale, c.v[t][r].y * -scale);
                 if (flag && live) traces[row * T + k] = x;
-                __half h0, l0, h1, l1;
-                split_h(x.x * sc, h0, l0);
-                split_h(x.y * sc, h1, l1);
-                stage[i * T + k] = make_uint2(pack_h2(h0, h1), pack_h2(l0, l1));  // consecutive k: conflict-free
+                uint32_t hi, lo;
+                split_h2(x.x * sc, x.y * sc, hi, lo);
+                stage[i * T + k] = make_uint2(hi, lo);  // consecutive k: conflict-free
             }
         }
     }

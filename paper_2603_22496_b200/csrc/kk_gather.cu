@@ -1176,7 +1176,7 @@ __device__ __forceinline__ float db_fast(float v, float l2mx, float floor_db) {
 __global__ void __launch_bounds__(256)
 k_log_compress(const float *__restrict__ inten, const unsigned *__restrict__ fmax, long long P,
                float floor_db, float *db, bool vec) {
-    const int f = blockIdx.y;
+    const int f = gridDim.y - 1 - blockIdx.y;  // last frames first: the gather wrote them last (L2)
     const float mx = __uint_as_float(fmax[f]);
     const float *src = inten + (long long)f * P;
     float *dst = db + (long long)f * P;

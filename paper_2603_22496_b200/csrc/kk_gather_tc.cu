@@ -343,14 +343,13 @@ k_kk_gather_tc(const __grid_constant__ TcgArgs a) {
                         w0 = wm;
                     }
                     if (!ok) w0 = w1 = 0.f;
-                    __half h0, l0, h1, l1;
-                    split_h(w0, h0, l0);
-                    split_h(w1, h1, l1);
+                    uint32_t hw, lw;  // pack_h2(hi(w0), hi(w1)), pack_h2(lo(w0), lo(w1))
+                    split_h2(w0, w1, hw, lw);
                     const bool odd = e & 1;
-                    hA[j] = odd ? (uint32_t)__half_as_ushort(h0) << 16 : pack_h2(h0, h1);
-                    hB[j] = odd ? (uint32_t)__half_as_ushort(h1) : 0u;
-                    lA[j] = odd ? (uint32_t)__half_as_ushort(l0) << 16 : pack_h2(l0, l1);
-                    lB[j] = odd ? (uint32_t)__half_as_ushort(l1) : 0u;
+                    hA[j] = odd ? hw << 16 : hw;
+                    hB[j] = odd ? hw >> 16 : 0u;
+                    lA[j] = odd ? lw << 16 : lw;
+                    lB[j] = odd ? lw >> 16 : 0u;
                     kA[j] = ok ? e >> 1 : 0;
                     if (++m == M) {
                         m = 0;

@@ -27,4 +27,14 @@ __device__ __forceinline__ void split_h(float x, __half &hi, __half &lo) {
     lo = __float2half_rn(x - __half2float(hi));
 }
 
+// split_h of (a, b) with packed conversions (two F2FP instead of four F2F):
+// hi = pack_h2(hi(a), hi(b)), lo = pack_h2(lo(a), lo(b)), bit for bit
+__device__ __forceinline__ void split_h2(float a, float b, uint32_t &hi, uint32_t &lo) {
+    const __half2 h = __floats2half2_rn(a, b);
+    const float2 hf = __half22float2(h);
+    const __half2 l = __floats2half2_rn(a - hf.x, b - hf.y);
+    hi = pack_h2(__low2half(h), __high2half(h));
+    lo = pack_h2(__low2half(l), __high2half(l));
+}
+
 }  // namespace kkb
