@@ -75,6 +75,15 @@ __device__ __forceinline__ double tc_kk_delay(double t1, double lz, double lx, d
 #define TCG_ND 4               // TMEM accumulators (128 columns each)
 #define TCG_THREADS 352        // 11 warps
 
+// A / TMEM row r -> tile pixel (column cl, depth row rl).  Lanes r, r+8,
+// r+16, r+24 of a warp take the four depth rows of one column: their delays
+// differ by a few samples, so the weight-row words they store (rows 16 B
+// apart: the same bank quad) usually land in different banks, where rows 8
+// apart at one depth (r = cl * 4 + rl) mostly collided 4-way.
+static_assert(TCG_TZ == 4 && TCG_TX == 32, "row map assumes 4 x 32 tiles");
+__device__ __forceinline__ int tcg_col(int r) { return (r & 7) + 8 * (r >> 5); }
+__device__ __forceinline__ int tcg_row(int r) { return (r >> 3) & 3; }
+
 // per-frame max |re|, |im| of the traces (float bits; atomicMax on
 // non-negative floats).  V complex samples per load (2: 16-byte loads, when
 // the frame stride and length are even and the base 16-byte aligned).
@@ -300,7 +309,7 @@ k_kk_gather_tc(const __grid_constant__ TcgArgs a) {
         // in 32: the A ring is zeroed once, then each pair writes the two
         // 32-bit words that carry them and clears the words it wrote in the
         // same stage one round earlier (4 x STS.32 per plane).
-        const int r = t, cl = r / TCG_TZ, rl = r % TCG_TZ;
+        const int r = t, cl = tcg_col(r), rl = tcg_row(r);
         unsigned char *row = sm + r * 16;
 #pragma unroll
         for (int st = 0; st < TCG_NA; ++st)
@@ -489,7 +498,7 @@ k_kk_gather_tc(const __grid_constant__ TcgArgs a) {
             // per-frame max), each frame independent of the others
             const int tile = tile_of(k), f0 = fb_of(k) * TCG_FB;
             const int FB = min(TCG_FB, a.n_frames - f0);
-            const int ix = (tile / a.tiles_z) * TCG_TX + r / TCG_TZ, iz = (tile % a.tiles_z) * TCG_TZ + r % TCG_TZ;
+            const int ix = (tile / a.tiles_z) * TCG_TX + tcg_col(r), iz = (tile % a.tiles_z) * TCG_TZ + tcg_row(r);
             const bool pix = ix < nx && iz < nz;
             const long long px0 = (long long)f0 * a.out_fs + (long long)ix * nz + iz;
 #pragma unroll
