@@ -68,12 +68,21 @@ __device__ __forceinline__ double tc_kk_delay(double t1, double lz, double lx, d
 #define TCG_TX KKB_KK_TC_TX
 #define TCG_KW KKB_KK_TC_W     // window samples per pair (two K steps)
 #define TCG_FB 64              // frames per CTA: N = 128 (re | im)
+#ifndef TCG_NA
 #define TCG_NA 4               // weight (A) stages
+#endif
+#ifndef TCG_NB
 #define TCG_NB 8               // trace-window (B) stages (they hide the TMA latency)
+#endif
+#ifndef TCG_PB
 #define TCG_PB 2               // pairs per producer iteration
+#endif
 #define TCG_GROUP 16           // pairs per accumulator group
 #define TCG_ND 4               // TMEM accumulators (128 columns each)
 #define TCG_THREADS 352        // 11 warps
+#ifndef TCG_EXP_SKIP2
+#define TCG_EXP_SKIP2 0        // experiment builds: 1 = skip the second K step of two-step pairs
+#endif
 
 // A / TMEM row r -> tile pixel (column cl, depth row rl).  Lanes r, r+8,
 // r+16, r+24 of a warp take the four depth rows of one column: their delays
@@ -328,6 +337,18 @@ k_kk_gather_tc(const __grid_constant__ TcgArgs a) {
             // TCG_PB pairs per iteration: independent delay chains in flight
             // and one proxy fence per batch
             for (int pr0 = 0; pr0 < npairs; pr0 += TCG_PB) {
+#ifdef TCG_EXP_NO_PROD  // experiment builds: the ring handshakes without weight rows
+                {
+                    const int nb = min(TCG_PB, npairs - pr0);
+                    for (int j = 0; j < nb; ++j) {
+                        const unsigned pp = P + j, use = pp / TCG_NA;
+                        if (use > 0) tc::mbar_wait(&a_empty[(int)(pp % TCG_NA)], (uint32_t)((use - 1) & 1));
+                    }
+                    for (int j = 0; j < nb; ++j) mbar_arrive(&a_full[(int)((P + j) % TCG_NA)]);
+                    P += nb;
+                    continue;
+                }
+#endif
                 uint32_t hA[TCG_PB], hB[TCG_PB], lA[TCG_PB], lB[TCG_PB];
                 int kA[TCG_PB];
 #pragma unroll
@@ -417,9 +438,14 @@ k_kk_gather_tc(const __grid_constant__ TcgArgs a) {
                     const int v = lo[pr], one = v & 1;
                     b_k16[st] = one;  // published to the MMA warp by the arrive below
                     // 4 planes x G groups x (16 or 32) samples x 16 B
+#ifdef TCG_EXP_NO_TMA  // experiment builds: the ring handshakes without the copies
+                    mbar_arrive(&b_full[st]);
+                    (void)G;
+#else
                     mbar_arrive_tx(&b_full[st], 4 * G * (one ? 16 : TCG_KW) * 16);
                     tma_4d(sm + TCG_NA * ASTAGE + st * BSTAGE, tl ? &a.tail[one] : &a.planes[one], 8 * (v >> 1), pr,
                            g0, 0, &b_full[st]);
+#endif
                 }
                 mbar_arrive(&tab_empty[slot]);
             }
@@ -431,6 +457,9 @@ k_kk_gather_tc(const __grid_constant__ TcgArgs a) {
         // uniform registers, no per-MMA lane election.
         const uint32_t s0 = (uint32_t)__cvta_generic_to_shared(sm);
         unsigned P = 0, G = 0;  // pairs and accumulator groups so far
+#ifdef TCG_EXP_PROFILE
+        long long prof[5] = {0, 0, 0, 0, 0};
+#endif
         for (int k = 0; k < nit; ++k) {
             // N = 16 x frame groups: re columns [0, 8g), im [8g, 16g)
             const uint32_t g = fb_of(k) == a.nfb - 1 ? a.gt : TCG_FB / 8;
@@ -438,9 +467,21 @@ k_kk_gather_tc(const __grid_constant__ TcgArgs a) {
             for (int pr = 0; pr < npairs; ++pr, ++P) {
                 const int sa_ = (int)(P % TCG_NA), sb_ = (int)(P % TCG_NB), d = (int)(G % TCG_ND);
                 const bool first = pr % TCG_GROUP == 0, last = pr % TCG_GROUP == TCG_GROUP - 1 || pr == npairs - 1;
+#ifdef TCG_EXP_PROFILE  // experiment builds: where the MMA warp's cycles go
+                long long c_0 = clock64();
+#endif
                 if (first && G >= TCG_ND) tc::mbar_wait(&dfree[d], (uint32_t)((G / TCG_ND - 1) & 1));  // drained
+#ifdef TCG_EXP_PROFILE
+                long long c_1 = clock64();
+#endif
                 tc::mbar_wait(&a_full[sa_], (uint32_t)((P / TCG_NA) & 1));
+#ifdef TCG_EXP_PROFILE
+                long long c_2 = clock64();
+#endif
                 tc::mbar_wait(&b_full[sb_], (uint32_t)((P / TCG_NB) & 1));
+#ifdef TCG_EXP_PROFILE
+                long long c_3 = clock64();
+#endif
                 tc::fence_after_sync();
                 const uint32_t sa = s0 + sa_ * ASTAGE, sb = s0 + TCG_NA * ASTAGE + sb_ * BSTAGE;
                 const bool one = b_k16[sb_] != 0;
@@ -449,8 +490,10 @@ k_kk_gather_tc(const __grid_constant__ TcgArgs a) {
                 const uint64_t ah = tc::smem_desc(sa, 128 * 16, 128), al = tc::smem_desc(sa + A_PLANE, 128 * 16, 128);
                 const uint64_t bh = tc::smem_desc(sb, 128, kb), bl = tc::smem_desc(sb + 2 * g * kb, 128, kb);
                 if (tc::elect_one()) {
+#ifndef TCG_EXP_NO_MMA  // experiment builds: the pipeline without the MMAs
                     tc::mma_f16_split3(tmem + d * 128, ah, al, bh, bl, idesc, !first);
-                    if (!one)  // second K = 16 half: A + 2 chunks, B + 2 K groups
+#endif
+                    if (!one && !TCG_EXP_SKIP2)  // second K = 16 half: A + 2 chunks, B + 2 K groups
                         tc::mma_f16_split3(tmem + d * 128, ah + ((2 * 128 * 16) >> 4), al + ((2 * 128 * 16) >> 4),
                                            bh + ((2 * 128) >> 4), bl + ((2 * 128) >> 4), idesc, true);
                     tc::commit(&a_empty[sa_]);
@@ -458,9 +501,21 @@ k_kk_gather_tc(const __grid_constant__ TcgArgs a) {
                     if (last) tc::commit(&dfull[d]);
                 }
                 __syncwarp();
+#ifdef TCG_EXP_PROFILE
+                long long c_4 = clock64();
+                prof[0] += c_1 - c_0;
+                prof[1] += c_2 - c_1;
+                prof[2] += c_3 - c_2;
+                prof[3] += c_4 - c_3;
+                prof[4] += 1;
+#endif
                 if (last) ++G;
             }
         }
+#ifdef TCG_EXP_PROFILE
+        if (lane == 0)
+            for (int i = 0; i < 5; ++i) atomicAdd(reinterpret_cast<unsigned long long *>(a.fmax) + 220 + i, (unsigned long long)prof[i]);
+#endif
     } else if (warp < 10) {
         // ------------------------------------------------------------ drains + epilogue
         const int quarter = warp & 3;
@@ -477,6 +532,11 @@ k_kk_gather_tc(const __grid_constant__ TcgArgs a) {
                 tc::mbar_wait(&dfull[d], (uint32_t)((G / TCG_ND) & 1));
                 tc::fence_after_sync();
                 const uint32_t col = lane_base + d * 128;
+#ifdef TCG_EXP_NO_DRAIN  // experiment builds: drains hand the accumulator straight back
+                tc::fence_before_sync();
+                mbar_arrive(&dfree[d]);
+                continue;
+#endif
 #pragma unroll
                 for (int c0 = 0; c0 < TCG_FB; c0 += 8) {
                     if (c0 < 8 * (int)g) {  // warp-uniform
@@ -494,6 +554,10 @@ k_kk_gather_tc(const __grid_constant__ TcgArgs a) {
                 tc::fence_before_sync();
                 mbar_arrive(&dfree[d]);
             }
+#ifdef TCG_EXP_NO_EPI  // experiment builds: drains without the epilogue
+            if (S[0] == 12345.f) a.fmax[0] = 1u;  // keep the drains' adds alive
+            continue;
+#endif
             // epilogue: straight-line passes over the 64 frames (IQ, |IQ|^2,
             // per-frame max), each frame independent of the others
             const int tile = tile_of(k), f0 = fb_of(k) * TCG_FB;
