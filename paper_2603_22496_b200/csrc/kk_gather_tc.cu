@@ -626,6 +626,9 @@ k_kk_gather_tc(const __grid_constant__ TcgArgs a) {
         for (int k = 0; k < nit; ++k) {
             const int slot = k & 1, tile = tile_of(k);
             if (k >= 2) tc::mbar_wait(&tab_empty[slot], (uint32_t)(((k >> 1) - 1) & 1));
+#ifdef TCG_EXP_NO_TAB  // experiment builds: stale tables (timing only)
+            if (held[slot] != tile && held[slot] >= 0) held[slot] = tile;
+#endif
             if (held[slot] != tile) {
                 const TcgTables tb = tcg_tables(tab_base + slot * slot_bytes, N, M);
                 const int iz0 = (tile % a.tiles_z) * TCG_TZ, ix0 = (tile / a.tiles_z) * TCG_TX;
