@@ -329,9 +329,19 @@ k_kk_gather_tc(const __grid_constant__ TcgArgs a) {
         auto word = [](int k) { return (k >> 2) * (128 * 16) + (k & 3) * 4; };
         uint32_t prevk = 0;  // per stage (4 bits each): first word written last round
         unsigned P = 0;      // pairs issued so far (the rings' sequence)
+#ifdef TCG_EXP_PROFILE
+        long long pprof[3] = {0, 0, 0};  // loop cycles, a_empty wait cycles, tab_full wait cycles
+        const long long pt0 = clock64();
+#endif
         for (int k = 0; k < nit; ++k) {
             const int slot = k & 1;
+#ifdef TCG_EXP_PROFILE
+            const long long tw0 = clock64();
+#endif
             tc::mbar_wait(&tab_full[slot], (k >> 1) & 1);
+#ifdef TCG_EXP_PROFILE
+            pprof[2] += clock64() - tw0;
+#endif
             const TcgTables tb = tcg_tables(tab_base + slot * slot_bytes, N, M);
             int n = 0, m = 0;
             // TCG_PB pairs per iteration: independent delay chains in flight
@@ -395,7 +405,13 @@ k_kk_gather_tc(const __grid_constant__ TcgArgs a) {
                     const unsigned use = pp / TCG_NA;
                     unsigned char *Ab = row + st * ASTAGE;
                     if (use > 0) {
+#ifdef TCG_EXP_PROFILE
+                        const long long w0 = clock64();
+#endif
                         tc::mbar_wait(&a_empty[st], (uint32_t)((use - 1) & 1));
+#ifdef TCG_EXP_PROFILE
+                        pprof[1] += clock64() - w0;
+#endif
                         const int qA = (prevk >> (4 * st)) & 15, qB = qA == 15 ? 14 : qA + 1;
                         *reinterpret_cast<uint32_t *>(Ab + word(qA)) = 0u;
                         *reinterpret_cast<uint32_t *>(Ab + word(qB)) = 0u;
@@ -410,7 +426,9 @@ k_kk_gather_tc(const __grid_constant__ TcgArgs a) {
                     *reinterpret_cast<uint32_t *>(Ab + A_PLANE + word(kA[j])) = lA[j];
                     prevk = (prevk & ~(15u << (4 * st))) | ((uint32_t)kA[j] << (4 * st));
                 }
+#ifndef TCG_EXP_NO_FENCE  // experiment builds: timing without the proxy fence (unsafe)
                 tc::fence_smem_to_async();
+#endif
 #pragma unroll
                 for (int j = 0; j < TCG_PB; ++j)
                     if (j < nb) mbar_arrive(&a_full[(int)((P + j) % TCG_NA)]);
@@ -418,12 +436,22 @@ k_kk_gather_tc(const __grid_constant__ TcgArgs a) {
             }
             mbar_arrive(&tab_empty[slot]);  // this item's tables read
         }
+#ifdef TCG_EXP_PROFILE
+        pprof[0] = clock64() - pt0;
+        if (t == 0)
+            for (int i = 0; i < 3; ++i)
+                atomicAdd(reinterpret_cast<unsigned long long *>(a.fmax) + 230 + i, (unsigned long long)pprof[i]);
+#endif
     } else if (warp == 4) {
         // ------------------------------------------------------------ trace windows (TMA)
         // box [plane 4][group 8][sample 32 (or 16)][frame 8] = B hi (re
         // groups | im groups) then B lo: column group = im * 8 + g, 512 (256) B apart
         if (lane == 0) {
             unsigned P = 0;
+#ifdef TCG_EXP_PROFILE
+            long long bprof = 0;
+            const long long bt0 = clock64();
+#endif
             for (int k = 0; k < nit; ++k) {
                 const int slot = k & 1;
                 tc::mbar_wait(&tab_full[slot], (k >> 1) & 1);
@@ -434,7 +462,13 @@ k_kk_gather_tc(const __grid_constant__ TcgArgs a) {
                 for (int pr = 0; pr < npairs; ++pr, ++P) {
                     const int st = (int)(P % TCG_NB);
                     const unsigned use = P / TCG_NB;
+#ifdef TCG_EXP_PROFILE
+                    const long long b0 = clock64();
+#endif
                     if (use > 0) tc::mbar_wait(&b_empty[st], (uint32_t)((use - 1) & 1));
+#ifdef TCG_EXP_PROFILE
+                    bprof += clock64() - b0;
+#endif
                     const int v = lo[pr], one = v & 1;
                     b_k16[st] = one;  // published to the MMA warp by the arrive below
                     // 4 planes x G groups x (16 or 32) samples x 16 B
@@ -449,6 +483,10 @@ k_kk_gather_tc(const __grid_constant__ TcgArgs a) {
                 }
                 mbar_arrive(&tab_empty[slot]);
             }
+#ifdef TCG_EXP_PROFILE
+            atomicAdd(reinterpret_cast<unsigned long long *>(a.fmax) + 233, (unsigned long long)(clock64() - bt0));
+            atomicAdd(reinterpret_cast<unsigned long long *>(a.fmax) + 234, (unsigned long long)bprof);
+#endif
         }
     } else if (warp == 5) {
         // ------------------------------------------------------------ MMA issue

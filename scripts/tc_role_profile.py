@@ -17,9 +17,13 @@ P = g.nx * g.nz
 traces = torch.view_as_complex(torch.randn((F, N, M, T, 2), device="cuda"))
 iq = torch.empty((F, P), dtype=torch.complex64, device="cuda")
 inten = torch.empty((F, P), device="cuda")
-fmax = torch.zeros(F + 200, dtype=torch.int32, device="cuda")  # + profile slots (u64 220..224, past the frame maxima)
+fmax = torch.zeros(F + 200, dtype=torch.int32, device="cuda")  # noqa  # + profile slots (u64 220..224, past the frame maxima)
 _lib.call("kkb_kk_plan_run", kp, dev.ptr(traces), F, N * M * T, dev.ptr(iq), _lib.KKB_OUT_C64, P, dev.ptr(inten), dev.ptr(fmax), dev.stream_handle())
 torch.cuda.synchronize()
-v = fmax.cpu().view(torch.int64)[220:225].tolist()
+v = fmax.cpu().view(torch.int64)[220:235].tolist()
 n = v[4]
-print({"pairs": n, "dfree_wait": v[0] / n, "a_full_wait": v[1] / n, "b_full_wait": v[2] / n, "issue": v[3] / n})
+print({"mma_warp": {"pairs": n, "dfree_wait": v[0] / n, "a_full_wait": v[1] / n, "b_full_wait": v[2] / n,
+                    "issue": v[3] / n},
+       "producer_thread0": {"loop": v[10] / n * 148, "a_empty_wait": v[11] / n * 148, "tab_full_wait": v[12] / n * 148},
+       "tma_lane": {"loop": v[13] / n * 148, "b_empty_wait": v[14] / n * 148},
+       "note": "cycles per (tile, pair); producer / TMA sums are per CTA (one thread each), scaled by the 148 CTAs"})
