@@ -39,7 +39,8 @@ class KKEngine:
                  chunk_frames: int | None = None, pipeline: tuple | None = None,
                  interpolation: str = "linear",
                  pulse_delay: float = 0.0, channel_weights=None, floor_db: float = -60.0,
-                 want_db: bool = True, groups: int = 1, fuse_tc: bool = False):
+                 want_db: bool = True, groups: int = 1, fuse_tc: bool = False,
+                 fused_stage1: bool = False):
         t = dev.require_cuda()
         self.t = t
         self.array, self.params, self.receive, self.grid = array, params, receive, grid
@@ -58,6 +59,9 @@ class KKEngine:
         self.want_db = want_db
         self.chunk = int(chunk_frames or self.F)
         self.groups = int(groups)   # >1: overlap decomposition and gather across frame groups
+        # fused_stage1: K1 + K2 as one kernel (opt-in, kkb_decomposer_set_fused;
+        # uniform arrays, T = 1536, <= 6 angle classes; ConfigError otherwise)
+        self.fused_stage1 = bool(fused_stage1)
         self._side = None
         lib = _lib.load()
 
@@ -111,6 +115,11 @@ class KKEngine:
         h = ctypes.c_void_p()
         _lib.call("kkb_decomposer_create", self.N, self.L, self.T, pos.ctypes.data, ang.ctypes.data,
                   self.M, float(self.fs), float(self.c), int(chunk), ctypes.byref(h))
+        if self.fused_stage1:
+            if _lib.load().kkb_decomposer_set_fused(h, 1) != 0:
+                _lib.load().kkb_decomposer_destroy(h)
+                raise ConfigError("fused_stage1 needs a uniform symmetric array, T = 1536, L a multiple of 8 "
+                                  "up to 256 and at most 6 receive-angle classes")
         return h
 
     # ------------------------------------------------------------------ info

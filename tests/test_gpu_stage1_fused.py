@@ -139,3 +139,58 @@ def test_fused_ineligible_plans():
         assert lib.kkb_decomposer_fused(h) == 0
     finally:
         lib.kkb_decomposer_destroy(h)
+
+
+def test_engine_option_whole_path(oracle):
+    """KKEngine(fused_stage1=True): the whole path (decomposition, gather,
+    detection) against the default engine and the oracle's image."""
+    import torch
+
+    F = 2
+    w = configs.config4(frames=F)
+    arr, p, rx, g = w.array, w.params, w.receive, w.grid
+    rf = np.stack([configs.noise_rf(p.num_transmits, arr.num_elements, p.num_samples, seed=110 + f)
+                   for f in range(F)])
+    outs = []
+    for fused in (True, False):
+        eng = kb.KKEngine(arr, p, rx, g, frames=F, want_db=False, fused_stage1=fused)
+        assert _lib.load().kkb_decomposer_fused(eng._dec) == int(fused)
+        outs.append(eng.run(torch.from_numpy(rf).cuda()).cpu().numpy().copy())
+        eng.close()
+    assert rel_l2(outs[0], outs[1]) <= 2e-6
+    ref_tr = oracle.decompose_f64(rf[1], arr.sampling_frequency, arr.positions, rx.angles, p.sound_speed)
+    luts = oracle.kk_luts(g.x, g.z, p.transmit_angles, rx.angles, p.sound_speed)
+    shift = oracle.kk_resolved_shift(0.0, p.start_time, arr.sampling_frequency)
+    ref = oracle.kk_kernel(ref_tr, *luts, np.ones(rx.num_angles), arr.sampling_frequency, shift)
+    assert rel_l2(outs[0][1].reshape(ref.shape), ref) <= 1e-5
+
+
+def test_engine_option_rejects_ineligible():
+    arr = kb.TransducerArray(16, 0.3e-3, 5e6, 20e6, 0.6)
+    params = kb.AcquisitionParams(C, np.linspace(-0.1, 0.1, 3), 1024)     # T != 1536
+    rx = kb.uniform_vernier_angles(3, 3, 0.1, 1)
+    grid = kb.ImageGrid(-1e-3, 2e-3, 0.1e-3, 0.1e-3, 4, 4)
+    with pytest.raises(kb.ConfigError):
+        kb.KKEngine(arr, params, rx, grid, frames=1, fused_stage1=True)
+
+
+def test_fused_random_geometries(oracle):
+    """Seeded random eligible geometries: element counts (multiples of 8),
+    receive sets, pitches and sampling rates."""
+    rng = np.random.default_rng(2026)
+    for case in range(6):
+        L = int(rng.integers(1, 33)) * 8
+        n_tx = int(rng.integers(3, 12))
+        n_rx = int(rng.integers(1, 12))
+        fs = float(rng.uniform(16e6, 40e6))
+        arr = kb.TransducerArray(L, float(rng.uniform(0.1e-3, 0.4e-3)), fs / 5, fs, 0.5)
+        params = kb.AcquisitionParams(C, np.linspace(-12 * DEG, 12 * DEG, n_tx), 1536)
+        rx = kb.uniform_vernier_angles(n_tx, n_rx, 12 * DEG, int(rng.integers(0, n_tx // 2 + 1)))
+        grid = kb.ImageGrid(-2e-3, 5e-3, 0.1e-3, 0.1e-3, 8, 8)
+        w = configs.Workload(f"rand{case}", arr, params, rx, grid)
+        rf = configs.noise_rf(n_tx, L, 1536, seed=200 + case)[None]
+        fused = _traces(w, rf, True)
+        plain = _traces(w, rf, False)
+        assert rel_l2(fused, plain) <= 2e-6, (case, L, n_rx)
+        ref = oracle.decompose_f64(rf[0], fs, arr.positions, rx.angles, C)
+        assert rel_l2(fused[0], ref) <= 1e-5, (case, L, n_rx)
