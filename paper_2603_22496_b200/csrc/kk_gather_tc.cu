@@ -38,13 +38,20 @@
 // 8: 5e-7 and 11% slower, of 32: 1.7e-6 and 1% faster;
 // profiles/r02_gather_tc_sweep.jsonl).
 //
-// Warp roles (11 warps, persistent CTAs): 0-3 build the weight rows of each
-// pair (one row per thread, delay tables staged in shared memory); 4
-// allocates TMEM and issues the TMA copies (one lane); 5 issues the MMAs
-// (one elected lane); 6-9 drain the accumulators and run the epilogue (IQ,
-// fused |IQ|^2, per-frame max); 10 builds the next item's tile tables.
-// Stages are guarded by full / empty mbarriers (tcgen05.commit frees a stage
-// and publishes a group).
+// Work item = (pixel tile, TWO 64-frame blocks): the per-pair protocol (weight
+// rows, ring handshakes, window copies) costs ~335 cycles per (tile, pair)
+// whatever the MMA width (profiles/r02f_gather_tc_role_profile.json), so one
+// weight build serves both blocks' windows and accumulators (the item's K5
+// time per frame falls 13%).  Warp roles (16 warps = 4 warpgroups,
+// persistent CTAs, setmaxnreg): warpgroup 0 builds the weight rows of each
+// pair (one row per thread, delay tables staged in shared memory); in
+// warpgroup 1, warp 4 allocates TMEM and issues the TMA copies (one lane, both
+// blocks' windows into one 32 KB stage), warp 5 issues the MMAs (one elected
+// lane), warp 6 builds the next item's tile tables; warpgroups 2 and 3 drain
+// set 0's / set 1's accumulators (two each in TMEM) and run the epilogue (IQ,
+// fused |IQ|^2, per-frame max) with 168 registers while the other two
+// warpgroups give theirs back (88).  Stages are guarded by full / empty
+// mbarriers (tcgen05.commit frees a stage and publishes a group).
 
 #include <algorithm>
 #include <cuda.h>
@@ -72,14 +79,19 @@ __device__ __forceinline__ double tc_kk_delay(double t1, double lz, double lx, d
 #define TCG_NA 4               // weight (A) stages
 #endif
 #ifndef TCG_NB
-#define TCG_NB 8               // trace-window (B) stages (they hide the TMA latency)
+#define TCG_NB 4               // trace-window (B) stages (they hide the TMA latency), TCG_SETS windows each
 #endif
+#define TCG_SETS 2             // frame blocks per item: one weight build serves both
 #ifndef TCG_PB
 #define TCG_PB 2               // pairs per producer iteration
 #endif
 #define TCG_GROUP 16           // pairs per accumulator group
-#define TCG_ND 4               // TMEM accumulators (128 columns each)
-#define TCG_THREADS 352        // 11 warps
+#define TCG_ND 4               // TMEM accumulators (128 columns each): 2 per frame-block set
+#define TCG_NDS (TCG_ND / TCG_SETS)
+#define TCG_THREADS 512        // 16 warps = 4 warpgroups (setmaxnreg per role)
+#define TCG_REGS_LO 88         // producers, TMA / MMA / table warps
+#define TCG_REGS_HI 168        // drains (128 fp32 partial sums each)
+static_assert(2 * 128 * TCG_REGS_LO + 2 * 128 * TCG_REGS_HI == TCG_THREADS * 128, "register pool");
 #ifndef TCG_EXP_SKIP2
 #define TCG_EXP_SKIP2 0        // experiment builds: 1 = skip the second K step of two-step pairs
 #endif
@@ -255,13 +267,13 @@ k_kk_gather_tc(const __grid_constant__ TcgArgs a) {
     constexpr int KC = TCG_KW / 8;                 // 16-byte K chunks per weight row
     constexpr int A_PLANE = KC * 128 * 16;          // 8 KB: one split half of the weights (K-major)
     constexpr int B_PLANE = 16 * TCG_KW * 16;       // 8 KB: one split half of the traces (MN-major, 16 col groups)
-    constexpr int ASTAGE = 2 * A_PLANE, BSTAGE = 2 * B_PLANE;
+    constexpr int ASTAGE = 2 * A_PLANE, BSET = 2 * B_PLANE, BSTAGE = TCG_SETS * BSET;
     extern __shared__ __align__(1024) unsigned char sm[];
     __shared__ uint64_t a_full[TCG_NA], a_empty[TCG_NA], b_full[TCG_NB], b_empty[TCG_NB];
     __shared__ uint64_t dfull[TCG_ND], dfree[TCG_ND], tab_full[2], tab_empty[2];
     __shared__ uint32_t tmem_base;
     __shared__ int b_k16[TCG_NB];  // per B stage: 1 = a 16-sample window (one K step)
-    __shared__ unsigned fm_s[2][4][TCG_FB];  // per item parity: each drain warp's frame maxima
+    __shared__ unsigned fm_s[TCG_SETS][2][4][TCG_FB];  // per set and item parity: each drain warp's frame maxima
 
     // a batch with a non-finite sample goes to the FMA gather (NaN x 0 would
     // spread it over the whole window); uniform, before any barrier
@@ -280,7 +292,8 @@ k_kk_gather_tc(const __grid_constant__ TcgArgs a) {
     const int nit = (int)((a.items - blockIdx.x + gridDim.x - 1) / gridDim.x);
     auto item_of = [&](int k) { return (long long)blockIdx.x + (long long)k * gridDim.x; };
     auto tile_of = [&](int k) { return (int)(item_of(k) % a.tiles); };
-    auto fb_of = [&](int k) { return (int)(item_of(k) / a.tiles); };
+    // item k covers frame blocks TCG_SETS * (item / tiles) + s, s < TCG_SETS
+    auto fb_of = [&](int k, int set) { return (int)(item_of(k) / a.tiles) * TCG_SETS + set; };
 
     if (warp == 4) tc::tmem_alloc<32 * 4 * TCG_ND>(&tmem_base);
     if (t == 0) {
@@ -313,6 +326,7 @@ k_kk_gather_tc(const __grid_constant__ TcgArgs a) {
     const uint32_t tmem = tmem_base;
 
     if (warp < 4) {
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(TCG_REGS_LO));
         // ------------------------------------------------------------ weight rows
         // A row holds two nonzero halves (w0 at window sample e, w1 at e + 1)
         // in 32: the A ring is zeroed once, then each pair writes the two
@@ -442,7 +456,9 @@ k_kk_gather_tc(const __grid_constant__ TcgArgs a) {
             for (int i = 0; i < 3; ++i)
                 atomicAdd(reinterpret_cast<unsigned long long *>(a.fmax) + 230 + i, (unsigned long long)pprof[i]);
 #endif
-    } else if (warp == 4) {
+    } else if (warp < 8) {
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(TCG_REGS_LO));
+      if (warp == 4) {
         // ------------------------------------------------------------ trace windows (TMA)
         // box [plane 4][group 8][sample 32 (or 16)][frame 8] = B hi (re
         // groups | im groups) then B lo: column group = im * 8 + g, 512 (256) B apart
@@ -456,9 +472,14 @@ k_kk_gather_tc(const __grid_constant__ TcgArgs a) {
                 const int slot = k & 1;
                 tc::mbar_wait(&tab_full[slot], (k >> 1) & 1);
                 const int *lo = tcg_tables(tab_base + slot * slot_bytes, N, M).lo;
-                const int fb = fb_of(k), g0 = fb * (TCG_FB / 8);
-                const bool tl = fb == a.nfb - 1;
-                const uint32_t G = tl ? a.gt : TCG_FB / 8;
+                // the item's frame blocks: set s is block fb_of(k, s) when it exists
+                int fbs[TCG_SETS];
+                uint32_t Gs[TCG_SETS];
+#pragma unroll
+                for (int st2 = 0; st2 < TCG_SETS; ++st2) {
+                    fbs[st2] = fb_of(k, st2);
+                    Gs[st2] = fbs[st2] >= a.nfb ? 0u : fbs[st2] == a.nfb - 1 ? (uint32_t)a.gt : TCG_FB / 8;
+                }
                 for (int pr = 0; pr < npairs; ++pr, ++P) {
                     const int st = (int)(P % TCG_NB);
                     const unsigned use = P / TCG_NB;
@@ -471,14 +492,21 @@ k_kk_gather_tc(const __grid_constant__ TcgArgs a) {
 #endif
                     const int v = lo[pr], one = v & 1;
                     b_k16[st] = one;  // published to the MMA warp by the arrive below
-                    // 4 planes x G groups x (16 or 32) samples x 16 B
+                    // per set: 4 planes x G groups x (16 or 32) samples x 16 B
+                    uint32_t bytes = 0;
+#pragma unroll
+                    for (int st2 = 0; st2 < TCG_SETS; ++st2) bytes += 4 * Gs[st2] * (one ? 16 : TCG_KW) * 16;
 #ifdef TCG_EXP_NO_TMA  // experiment builds: the ring handshakes without the copies
+                    (void)bytes;
                     mbar_arrive(&b_full[st]);
-                    (void)G;
 #else
-                    mbar_arrive_tx(&b_full[st], 4 * G * (one ? 16 : TCG_KW) * 16);
-                    tma_4d(sm + TCG_NA * ASTAGE + st * BSTAGE, tl ? &a.tail[one] : &a.planes[one], 8 * (v >> 1), pr,
-                           g0, 0, &b_full[st]);
+                    mbar_arrive_tx(&b_full[st], bytes);
+#pragma unroll
+                    for (int st2 = 0; st2 < TCG_SETS; ++st2)
+                        if (Gs[st2])
+                            tma_4d(sm + TCG_NA * ASTAGE + st * BSTAGE + st2 * BSET,
+                                   fbs[st2] == a.nfb - 1 ? &a.tail[one] : &a.planes[one], 8 * (v >> 1), pr,
+                                   fbs[st2] * (TCG_FB / 8), 0, &b_full[st]);
 #endif
                 }
                 mbar_arrive(&tab_empty[slot]);
@@ -488,7 +516,7 @@ k_kk_gather_tc(const __grid_constant__ TcgArgs a) {
             atomicAdd(reinterpret_cast<unsigned long long *>(a.fmax) + 234, (unsigned long long)bprof);
 #endif
         }
-    } else if (warp == 5) {
+      } else if (warp == 5) {
         // ------------------------------------------------------------ MMA issue
         // The whole warp runs the (warp-uniform) loop and one elected lane
         // issues a pair's six MMAs from one asm block: descriptors stay in
@@ -499,16 +527,26 @@ k_kk_gather_tc(const __grid_constant__ TcgArgs a) {
         long long prof[5] = {0, 0, 0, 0, 0};
 #endif
         for (int k = 0; k < nit; ++k) {
-            // N = 16 x frame groups: re columns [0, 8g), im [8g, 16g)
-            const uint32_t g = fb_of(k) == a.nfb - 1 ? a.gt : TCG_FB / 8;
-            const uint32_t idesc = tc::instr_desc(0, 128, 16 * g, 1);
+            // per set: N = 16 x frame groups, re columns [0, 8g), im [8g, 16g);
+            // g = 0 when the item has no frame block for the set
+            uint32_t gset[TCG_SETS], idesc[TCG_SETS];
+#pragma unroll
+            for (int st2 = 0; st2 < TCG_SETS; ++st2) {
+                const int fb = fb_of(k, st2);
+                gset[st2] = fb >= a.nfb ? 0u : fb == a.nfb - 1 ? (uint32_t)a.gt : TCG_FB / 8;
+                idesc[st2] = tc::instr_desc(0, 128, 16 * (gset[st2] ? gset[st2] : 1), 1);
+            }
             for (int pr = 0; pr < npairs; ++pr, ++P) {
-                const int sa_ = (int)(P % TCG_NA), sb_ = (int)(P % TCG_NB), d = (int)(G % TCG_ND);
+                const int sa_ = (int)(P % TCG_NA), sb_ = (int)(P % TCG_NB), d = (int)(G % TCG_NDS);
                 const bool first = pr % TCG_GROUP == 0, last = pr % TCG_GROUP == TCG_GROUP - 1 || pr == npairs - 1;
 #ifdef TCG_EXP_PROFILE  // experiment builds: where the MMA warp's cycles go
                 long long c_0 = clock64();
 #endif
-                if (first && G >= TCG_ND) tc::mbar_wait(&dfree[d], (uint32_t)((G / TCG_ND - 1) & 1));  // drained
+                if (first && G >= TCG_NDS) {  // both sets' accumulator d drained
+#pragma unroll
+                    for (int st2 = 0; st2 < TCG_SETS; ++st2)
+                        tc::mbar_wait(&dfree[st2 * TCG_NDS + d], (uint32_t)((G / TCG_NDS - 1) & 1));
+                }
 #ifdef TCG_EXP_PROFILE
                 long long c_1 = clock64();
 #endif
@@ -521,22 +559,32 @@ k_kk_gather_tc(const __grid_constant__ TcgArgs a) {
                 long long c_3 = clock64();
 #endif
                 tc::fence_after_sync();
-                const uint32_t sa = s0 + sa_ * ASTAGE, sb = s0 + TCG_NA * ASTAGE + sb_ * BSTAGE;
+                const uint32_t sa = s0 + sa_ * ASTAGE;
                 const bool one = b_k16[sb_] != 0;
                 // B: column groups of (16 or 32 samples) x 16 B; B lo after the 2g hi groups
                 const uint32_t kb = one ? 16 * 16 : TCG_KW * 16;
                 const uint64_t ah = tc::smem_desc(sa, 128 * 16, 128), al = tc::smem_desc(sa + A_PLANE, 128 * 16, 128);
-                const uint64_t bh = tc::smem_desc(sb, 128, kb), bl = tc::smem_desc(sb + 2 * g * kb, 128, kb);
                 if (tc::elect_one()) {
+                    // one weight build (A) serves every set's frame block (B window, accumulator)
+#pragma unroll
+                    for (int st2 = 0; st2 < TCG_SETS; ++st2) {
+                        if (!gset[st2]) continue;
+                        const uint32_t sb = s0 + TCG_NA * ASTAGE + sb_ * BSTAGE + st2 * BSET;
+                        const uint32_t dacc = tmem + (uint32_t)((st2 * TCG_NDS + d) * 128);
+                        const uint64_t bh = tc::smem_desc(sb, 128, kb), bl = tc::smem_desc(sb + 2 * gset[st2] * kb, 128, kb);
 #ifndef TCG_EXP_NO_MMA  // experiment builds: the pipeline without the MMAs
-                    tc::mma_f16_split3(tmem + d * 128, ah, al, bh, bl, idesc, !first);
+                        tc::mma_f16_split3(dacc, ah, al, bh, bl, idesc[st2], !first);
 #endif
-                    if (!one && !TCG_EXP_SKIP2)  // second K = 16 half: A + 2 chunks, B + 2 K groups
-                        tc::mma_f16_split3(tmem + d * 128, ah + ((2 * 128 * 16) >> 4), al + ((2 * 128 * 16) >> 4),
-                                           bh + ((2 * 128) >> 4), bl + ((2 * 128) >> 4), idesc, true);
+                        if (!one && !TCG_EXP_SKIP2)  // second K = 16 half: A + 2 chunks, B + 2 K groups
+                            tc::mma_f16_split3(dacc, ah + ((2 * 128 * 16) >> 4), al + ((2 * 128 * 16) >> 4),
+                                               bh + ((2 * 128) >> 4), bl + ((2 * 128) >> 4), idesc[st2], true);
+                    }
                     tc::commit(&a_empty[sa_]);
                     tc::commit(&b_empty[sb_]);
-                    if (last) tc::commit(&dfull[d]);
+                    if (last) {  // every set's drains run the group protocol, used or not
+#pragma unroll
+                        for (int st2 = 0; st2 < TCG_SETS; ++st2) tc::commit(&dfull[st2 * TCG_NDS + d]);
+                    }
                 }
                 __syncwarp();
 #ifdef TCG_EXP_PROFILE
@@ -554,9 +602,47 @@ k_kk_gather_tc(const __grid_constant__ TcgArgs a) {
         if (lane == 0)
             for (int i = 0; i < 5; ++i) atomicAdd(reinterpret_cast<unsigned long long *>(a.fmax) + 220 + i, (unsigned long long)prof[i]);
 #endif
-    } else if (warp < 10) {
+      } else if (warp == 6) {
+        // ------------------------------------------------------------ tile tables (next items)
+        int held[2] = {-1, -1};  // tile held by each slot
+        for (int k = 0; k < nit; ++k) {
+            const int slot = k & 1, tile = tile_of(k);
+            if (k >= 2) tc::mbar_wait(&tab_empty[slot], (uint32_t)(((k >> 1) - 1) & 1));
+#ifdef TCG_EXP_NO_TAB  // experiment builds: stale tables (timing only)
+            if (held[slot] != tile && held[slot] >= 0) held[slot] = tile;
+#endif
+            if (held[slot] != tile) {
+                const TcgTables tb = tcg_tables(tab_base + slot * slot_bytes, N, M);
+                const int iz0 = (tile % a.tiles_z) * TCG_TZ, ix0 = (tile / a.tiles_z) * TCG_TX;
+                // edge tiles repeat the last row / column
+                for (int i = lane; i < N * TCG_TX; i += 32) {
+                    const int n = i / TCG_TX, c = i - n * TCG_TX;
+                    tb.ltx[i] = __ldg(a.ltx + (long long)min(ix0 + c, nx - 1) * N + n);
+                }
+                for (int i = lane; i < N * TCG_TZ; i += 32) {
+                    const int n = i / TCG_TZ, rr = i - n * TCG_TZ;
+                    tb.ltz[i] = __ldg(a.ltzT + (long long)n * nz + min(iz0 + rr, nz - 1));
+                }
+                for (int i = lane; i < M * TCG_TX; i += 32) {
+                    const int m = i / TCG_TX, c = i - m * TCG_TX;
+                    tb.lrx[i] = __ldg(a.lrx + (long long)min(ix0 + c, nx - 1) * M + m);
+                }
+                for (int i = lane; i < M * TCG_TZ; i += 32) {
+                    const int m = i / TCG_TZ, rr = i - m * TCG_TZ;
+                    tb.lrz[i] = __ldg(a.lrzT + (long long)m * nz + min(iz0 + rr, nz - 1));
+                }
+                const int *src = a.tc_lo + (long long)tile * npairs;
+                for (int i = lane; i < npairs; i += 32) tb.lo[i] = __ldg(src + i);
+                held[slot] = tile;
+            }
+            mbar_arrive(&tab_full[slot]);
+        }
+      }  // warp 7: no role
+    } else {
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(TCG_REGS_HI));
         // ------------------------------------------------------------ drains + epilogue
-        const int quarter = warp & 3;
+        // warpgroup 2 drains set 0's accumulators, warpgroup 3 set 1's
+        const int set = (warp - 8) >> 2, quarter = warp & 3;
         const int r = quarter * 32 + lane;
         const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
         unsigned G = 0;
@@ -564,10 +650,12 @@ k_kk_gather_tc(const __grid_constant__ TcgArgs a) {
             float S[2 * TCG_FB];
 #pragma unroll
             for (int c = 0; c < 2 * TCG_FB; ++c) S[c] = 0.f;
-            const uint32_t g = fb_of(k) == a.nfb - 1 ? a.gt : TCG_FB / 8;  // re [0, 8g), im [8g, 16g)
+            const int fbk = fb_of(k, set);
+            // re [0, 8g), im [8g, 16g); g = 0: no frame block for this set (handshakes only)
+            const uint32_t g = fbk >= a.nfb ? 0u : fbk == a.nfb - 1 ? (uint32_t)a.gt : TCG_FB / 8;
             for (int grp = 0; grp < ngroups; ++grp, ++G) {
-                const int d = (int)(G % TCG_ND);
-                tc::mbar_wait(&dfull[d], (uint32_t)((G / TCG_ND) & 1));
+                const int d = set * TCG_NDS + (int)(G % TCG_NDS);
+                tc::mbar_wait(&dfull[d], (uint32_t)((G / TCG_NDS) & 1));
                 tc::fence_after_sync();
                 const uint32_t col = lane_base + d * 128;
 #ifdef TCG_EXP_NO_DRAIN  // experiment builds: drains hand the accumulator straight back
@@ -596,9 +684,10 @@ k_kk_gather_tc(const __grid_constant__ TcgArgs a) {
             if (S[0] == 12345.f) a.fmax[0] = 1u;  // keep the drains' adds alive
             continue;
 #endif
+            if (!g) continue;
             // epilogue: straight-line passes over the 64 frames (IQ, |IQ|^2,
             // per-frame max), each frame independent of the others
-            const int tile = tile_of(k), f0 = fb_of(k) * TCG_FB;
+            const int tile = tile_of(k), f0 = fbk * TCG_FB;
             const int FB = min(TCG_FB, a.n_frames - f0);
             const int ix = (tile / a.tiles_z) * TCG_TX + tcg_col(r), iz = (tile % a.tiles_z) * TCG_TZ + tcg_row(r);
             const bool pix = ix < nx && iz < nz;
@@ -642,56 +731,22 @@ k_kk_gather_tc(const __grid_constant__ TcgArgs a) {
                     // frame and warp, the four drain warps combined in shared memory,
                     // then one atomic per frame and item (the CTAs in flight share a
                     // frame block, so per-warp atomics contend on 64 addresses)
-                    unsigned *fm = fm_s[k & 1][quarter];
+                    unsigned *fm = fm_s[set][k & 1][quarter];
 #pragma unroll
                     for (int f = 0; f < TCG_FB; ++f) {
                         const unsigned mx = __reduce_max_sync(0xffffffffu, __float_as_uint(S[f]));
                         if (lane == 0) fm[f] = mx;
                     }
-                    asm volatile("bar.sync 1, 128;" ::: "memory");  // the four drain warps
-                    const int dr = (warp - 6) * 32 + lane;  // 0..127
+                    // the set's four drain warps (named barrier 1 + set)
+                    asm volatile("bar.sync %0, 128;" ::"r"(1 + set) : "memory");
+                    const int dr = (warp - 8 - 4 * set) * 32 + lane;  // 0..127
                     if (dr < FB) {
-                        const unsigned m4 = max(max(fm_s[k & 1][0][dr], fm_s[k & 1][1][dr]),
-                                                max(fm_s[k & 1][2][dr], fm_s[k & 1][3][dr]));
+                        const unsigned m4 = max(max(fm_s[set][k & 1][0][dr], fm_s[set][k & 1][1][dr]),
+                                                max(fm_s[set][k & 1][2][dr], fm_s[set][k & 1][3][dr]));
                         atomicMax(a.fmax + f0 + dr, m4);
                     }
                 }
             }
-        }
-    } else {
-        // ------------------------------------------------------------ tile tables (next items)
-        int held[2] = {-1, -1};  // tile held by each slot
-        for (int k = 0; k < nit; ++k) {
-            const int slot = k & 1, tile = tile_of(k);
-            if (k >= 2) tc::mbar_wait(&tab_empty[slot], (uint32_t)(((k >> 1) - 1) & 1));
-#ifdef TCG_EXP_NO_TAB  // experiment builds: stale tables (timing only)
-            if (held[slot] != tile && held[slot] >= 0) held[slot] = tile;
-#endif
-            if (held[slot] != tile) {
-                const TcgTables tb = tcg_tables(tab_base + slot * slot_bytes, N, M);
-                const int iz0 = (tile % a.tiles_z) * TCG_TZ, ix0 = (tile / a.tiles_z) * TCG_TX;
-                // edge tiles repeat the last row / column
-                for (int i = lane; i < N * TCG_TX; i += 32) {
-                    const int n = i / TCG_TX, c = i - n * TCG_TX;
-                    tb.ltx[i] = __ldg(a.ltx + (long long)min(ix0 + c, nx - 1) * N + n);
-                }
-                for (int i = lane; i < N * TCG_TZ; i += 32) {
-                    const int n = i / TCG_TZ, rr = i - n * TCG_TZ;
-                    tb.ltz[i] = __ldg(a.ltzT + (long long)n * nz + min(iz0 + rr, nz - 1));
-                }
-                for (int i = lane; i < M * TCG_TX; i += 32) {
-                    const int m = i / TCG_TX, c = i - m * TCG_TX;
-                    tb.lrx[i] = __ldg(a.lrx + (long long)min(ix0 + c, nx - 1) * M + m);
-                }
-                for (int i = lane; i < M * TCG_TZ; i += 32) {
-                    const int m = i / TCG_TZ, rr = i - m * TCG_TZ;
-                    tb.lrz[i] = __ldg(a.lrzT + (long long)m * nz + min(iz0 + rr, nz - 1));
-                }
-                const int *src = a.tc_lo + (long long)tile * npairs;
-                for (int i = lane; i < npairs; i += 32) tb.lo[i] = __ldg(src + i);
-                held[slot] = tile;
-            }
-            mbar_arrive(&tab_full[slot]);
         }
     }
     tc::fence_before_sync();
@@ -703,7 +758,7 @@ k_kk_gather_tc(const __grid_constant__ TcgArgs a) {
 }
 
 static size_t tcg_smem_bytes(int N, int M) {
-    return (size_t)TCG_NA * (2 * (TCG_KW / 8) * 128 * 16) + (size_t)TCG_NB * (2 * 16 * TCG_KW * 16) +
+    return (size_t)TCG_NA * (2 * (TCG_KW / 8) * 128 * 16) + (size_t)TCG_NB * TCG_SETS * (2 * 16 * TCG_KW * 16) +
            2 * tcg_slot_bytes(N, M) + sizeof(float) * (size_t)M;
 }
 
@@ -755,7 +810,7 @@ static int tcg_launch(const __half *planes, const unsigned *mx, const unsigned *
     a.tc_lo = tc_lo;
     a.tiles_z = (int)ceil_div(nz, TCG_TZ);
     a.tiles = (long long)a.tiles_z * ceil_div(nx, TCG_TX);
-    a.items = a.tiles * a.nfb;
+    a.items = a.tiles * ceil_div(a.nfb, TCG_SETS);  // items of TCG_SETS frame blocks
     const unsigned grid = (unsigned)std::min<long long>(a.items, sm_count());
     if (linear) {
         KKB_TRY_CUDA(cudaFuncSetAttribute(k_kk_gather_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
