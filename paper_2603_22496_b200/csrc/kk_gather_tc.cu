@@ -85,7 +85,9 @@ __device__ __forceinline__ double tc_kk_delay(double t1, double lz, double lx, d
 #ifndef TCG_PB
 #define TCG_PB 2               // pairs per producer iteration
 #endif
+#ifndef TCG_GROUP
 #define TCG_GROUP 16           // pairs per accumulator group
+#endif
 #define TCG_ND 4               // TMEM accumulators (128 columns each): 2 per frame-block set
 #define TCG_NDS (TCG_ND / TCG_SETS)
 #define TCG_THREADS 512        // 16 warps = 4 warpgroups (setmaxnreg per role)
