@@ -248,7 +248,9 @@ def test_bench_roofline_helpers_read_the_committed_profiles():
     l2 = bench._l2_roofline(24000.0)
     assert l2["bound"] == "l2" and 16000 < l2["peak"] < 20000 and 1.2 < l2["frac"] < 1.6
     t = bench._gather_traffic(400)
-    assert 0.3e9 < t < 0.9e9
+    # between the L2-warm single-block capture (0.55 GB) and the gather's
+    # compulsory bytes plus slack (traces 0.60 GB + IQ 0.21 GB + tables + planes)
+    assert 0.3e9 < t < 1.2e9
     assert bench._gather_traffic(200) == t / 2
     smem, fp32, kind = bench._onchip_peaks()
     assert kind == "measured" and 30000 < smem < 40000 and 60 < fp32 < 80
