@@ -222,8 +222,11 @@ k_c2c(const float2 *__restrict__ in, long long in_stride, int in_len, float2 *__
 // 16-byte rows (two CTAs fill a row; two CTAs per SM overlap their phases).
 // Frames past n_frames stage zeros.  When *nonfinite is set the complex64
 // traces are written too (the FMA gather, which then runs instead, reads them).
+#ifndef KKB_C2C_PLANES_MINB
+#define KKB_C2C_PLANES_MINB 2  // resident CTAs per SM the register budget is sized for
+#endif
 template <int T>
-__global__ void __launch_bounds__(4 * Plan<T>::NT, 2)
+__global__ void __launch_bounds__(4 * Plan<T>::NT, KKB_C2C_PLANES_MINB)
 k_c2c_planes(const float2 *__restrict__ Y, long long ldy, int K, int n_frames, int NM, float scale,
              const float2 *__restrict__ tw, const unsigned *__restrict__ fbound,
              const unsigned *__restrict__ nonfinite, float2 *__restrict__ traces, __half *__restrict__ planes,
