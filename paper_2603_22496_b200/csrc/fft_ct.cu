@@ -26,6 +26,7 @@
 // staging 53% slower (register pressure), so one CTA per transform is kept.
 
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <vector>
 
@@ -142,7 +143,7 @@ k_r2c(const InT *__restrict__ in, long long ntraces, float2 *__restrict__ out,
 // One complex transform of the row at src (bins [0, in_len), the rest zero)
 // through buf; returns with the outputs (points j + r T/R2 of lane j) in c,
 // conjugated on input for the inverse (the caller conjugates the output).
-template <int T, bool INV, typename S2>
+template <int T, bool INV, typename S2, bool SMEM_SRC = false>
 __device__ __forceinline__ void c2c_row(const float2 *__restrict__ src, int in_len, const float2 *__restrict__ tw,
                                         float2 *buf, S2 &c, int bar = 0) {
     using P = Plan<T>;
@@ -157,7 +158,7 @@ __device__ __forceinline__ void c2c_row(const float2 *__restrict__ src, int in_l
             for (int r = 0; r < P::R0; ++r) {
                 const int e = j + r * S0::TR;
                 float2 v = make_float2(0.f, 0.f);
-                if (e < in_len) v = __ldg(src + e);
+                if (e < in_len) v = SMEM_SRC ? src[e] : __ldg(src + e);
                 a.v[t][r] = make_float2(v.x, sg * v.y);
             }
         }
@@ -279,6 +280,116 @@ k_c2c_planes(const float2 *__restrict__ Y, long long ldy, int K, int n_frames, i
         dst[1 * (per_plane / 4) + o] = make_uint2((e[0].x >> 16) | (e[1].x & 0xffff0000u), (e[2].x >> 16) | (e[3].x & 0xffff0000u));
         dst[2 * (per_plane / 4) + o] = make_uint2((e[0].y & 0xffffu) | (e[1].y << 16), (e[2].y & 0xffffu) | (e[3].y << 16));
         dst[3 * (per_plane / 4) + o] = make_uint2((e[0].y >> 16) | (e[1].y & 0xffff0000u), (e[2].y >> 16) | (e[3].y & 0xffff0000u));
+    }
+}
+
+// K3 as a persistent kernel (2 CTAs per SM) whose CTAs walk the same units
+// (4 frames of one pair) in the same order as k_c2c_planes, each unit's four
+// rows of Y arriving by 1D bulk copies (cp.async.bulk, mbarrier complete_tx)
+// into one of two shared slots while the previous unit transforms: the
+// per-CTA load latency the one-shot kernel exposes at every CTA start is
+// hidden behind the FFT.  Arithmetic and store order are those of
+// k_c2c_planes, so the planes and traces are bit-identical.
+template <int T>
+__global__ void __launch_bounds__(4 * Plan<T>::NT, KKB_C2C_PLANES_MINB)
+k_c2c_planes_pf(const float2 *__restrict__ Y, long long ldy, int K, int n_frames, int NM, float scale,
+                const float2 *__restrict__ tw, const unsigned *__restrict__ fbound,
+                const unsigned *__restrict__ nonfinite, float2 *__restrict__ traces, __half *__restrict__ planes,
+                long long per_plane, int n_units, int row_bytes) {
+    using P = Plan<T>;
+    extern __shared__ __align__(128) unsigned char dsm[];
+    float2 *bufs = reinterpret_cast<float2 *>(dsm);
+    uint2 *stage = reinterpret_cast<uint2 *>(dsm);
+    unsigned char *slots = dsm + sizeof(float2) * 4 * T;  // [2 slots][4 rows][row_bytes]
+    uint64_t *mb = reinterpret_cast<uint64_t *>(slots + 8 * (size_t)row_bytes);
+    const int i = threadIdx.x / P::NT;
+    auto sa = [](const void *p) { return (uint32_t)__cvta_generic_to_shared(p); };
+    // thread 0: the four live rows of unit u into slot sl
+    auto fetch = [&](int u, int sl) {
+        const int bid = n_units - 1 - u;
+        const int q = bid % NM, gh = bid / NM, f0 = (gh >> 1) * 8 + (gh & 1) * 4;
+        const int live = min(4, n_frames - f0);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sa(&mb[sl])),
+                     "r"((uint32_t)(live * row_bytes))
+                     : "memory");
+        for (int fi = 0; fi < live; ++fi) {
+            const long long row = (long long)(f0 + fi) * NM + q;
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                    sa(slots + ((size_t)sl * 4 + fi) * row_bytes)),
+                "l"(Y + row * ldy), "r"((uint32_t)row_bytes), "r"(sa(&mb[sl]))
+                : "memory");
+        }
+    };
+    if (threadIdx.x == 0) {
+        for (int k = 0; k < 2; ++k)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sa(&mb[k])) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        if (blockIdx.x < n_units) fetch(blockIdx.x, 0);
+        if (blockIdx.x + gridDim.x < n_units) fetch(blockIdx.x + gridDim.x, 1);
+    }
+    const bool flag = *nonfinite != 0;
+    int it = 0;
+#pragma unroll 1
+    for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++it) {
+        const int sl = it & 1;
+        const int bid = n_units - 1 - u;
+        const int q = bid % NM, gh = bid / NM, g = gh >> 1, half = gh & 1;
+        const int f = g * 8 + half * 4 + i;
+        const long long row = (long long)f * NM + q;
+        const bool live = f < n_frames;
+        {
+            const uint32_t a = sa(&mb[sl]), par = (uint32_t)((it >> 1) & 1);
+            asm volatile(
+                "{\n\t.reg .pred P1;\n\tW_%=:\n\t"
+                "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+                "@!P1 bra W_%=;\n\t}\n" ::"r"(a),
+                "r"(par)
+                : "memory");
+        }
+        using S2 = Stage<T, P::NT, P::R2>;
+        S2 c;
+        c2c_row<T, true, S2, true>(reinterpret_cast<const float2 *>(slots + ((size_t)sl * 4 + i) * row_bytes),
+                                   live ? K : 0, tw, bufs + (size_t)i * T, c, 1 + i);
+        const float sc = live ? frame_scale(__ldg(fbound + f)) : 0.f;
+        __syncthreads();  // every transform's slot and buffer read
+#pragma unroll
+        for (int t = 0; t < S2::ITER; ++t) {
+            const int j = S2::lane_j(t);
+#pragma unroll
+            for (int r = 0; r < P::R2; ++r) {
+                const int k = j + r * S2::TR;
+                if (S2::ok(j)) {
+                    const float2 x = make_float2(c.v[t][r].x * scale, c.v[t][r].y * -scale);
+                    if (flag && live) traces[row * T + k] = x;
+                    uint32_t hi, lo;
+                    split_h2(x.x * sc, x.y * sc, hi, lo);
+                    stage[i * T + k] = make_uint2(hi, lo);
+                }
+            }
+        }
+        __syncthreads();
+        // refill the slot (read before the first barrier above) with the unit
+        // after next, here where the transform outputs are no longer live
+        if (threadIdx.x == 0 && u + 2 * (int)gridDim.x < n_units) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            fetch(u + 2 * (int)gridDim.x, sl);
+        }
+        uint2 *dst = reinterpret_cast<uint2 *>(planes) + (((long long)g * NM + q) * T) * 2 + half;
+        for (int k = threadIdx.x; k < T; k += blockDim.x) {
+            uint2 e[4];
+#pragma unroll
+            for (int fi = 0; fi < 4; ++fi) e[fi] = stage[fi * T + k];
+            const long long o = 2LL * k;
+            dst[0 * (per_plane / 4) + o] = make_uint2((e[0].x & 0xffffu) | (e[1].x << 16), (e[2].x & 0xffffu) | (e[3].x << 16));
+            dst[1 * (per_plane / 4) + o] = make_uint2((e[0].x >> 16) | (e[1].x & 0xffff0000u), (e[2].x >> 16) | (e[3].x & 0xffff0000u));
+            dst[2 * (per_plane / 4) + o] = make_uint2((e[0].y & 0xffffu) | (e[1].y << 16), (e[2].y & 0xffffu) | (e[3].y << 16));
+            dst[3 * (per_plane / 4) + o] = make_uint2((e[0].y >> 16) | (e[1].y & 0xffff0000u), (e[2].y >> 16) | (e[3].y & 0xffff0000u));
+        }
+        __syncthreads();  // stage read before the next unit's transforms reuse the buffers
     }
 }
 
@@ -434,6 +545,34 @@ static int launch_c2c_planes(const float2 *Y, long long ldy, int K, int n_frames
     const long long groups = (n_frames + 7) / 8;
     const long long per_plane = groups * 8 * NM * (long long)T;
     const size_t smem = sizeof(float2) * 4 * (size_t)T;  // 4 transform buffers, then the fp16 stage
+    // the prefetching persistent form, opt-in (KKB_K3_PREFETCH=1): bit-identical
+    // and measured 0.18 ms slower per 400 frames than the one-shot kernel
+    // (profiles/r02h_k3_prefetch_experiment.json: 276 B of spills at 64
+    // registers).  Rows are copied whole in 16-byte units, so Y and its row
+    // pitch must be 16-byte aligned and the pitch hold K rounded up to 2 bins.
+    static const int pf_env = [] {
+        const char *e = getenv("KKB_K3_PREFETCH");
+        return e ? atoi(e) : 0;
+    }();
+    const int row_bytes = (int)(((long long)K * 8 + 15) / 16 * 16);
+    if (pf_env && groups * 2 * NM < (1LL << 31) && ((uintptr_t)Y % 16) == 0 && (ldy * 8) % 16 == 0 && ldy * 8 >= row_bytes) {
+        const int n_units = (int)(groups * 2 * NM);
+        const size_t smem_pf = smem + 8 * (size_t)row_bytes + 16;
+        KKB_TRY_CUDA(cudaFuncSetAttribute(ct::k_c2c_planes_pf<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)smem_pf),
+                     "smem attr c2c planes pf");
+        static int n_sm = 0;
+        if (!n_sm) {
+            int dev = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+        }
+        const int grid = std::min(n_units, n_sm * KKB_C2C_PLANES_MINB);
+        ct::k_c2c_planes_pf<T><<<(unsigned)grid, 4 * ct::Plan<T>::NT, smem_pf, s>>>(
+            Y, ldy, K, n_frames, NM, scale, tw, fbound, nonfinite, traces, planes, per_plane, n_units, row_bytes);
+        KKB_CHECK_LAUNCH("k_c2c_planes_pf");
+        return KKB_OK;
+    }
     KKB_TRY_CUDA(cudaFuncSetAttribute(ct::k_c2c_planes<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                  "smem attr c2c planes");
     ct::k_c2c_planes<T><<<(unsigned)(groups * 2 * NM), 4 * ct::Plan<T>::NT, smem, s>>>(
