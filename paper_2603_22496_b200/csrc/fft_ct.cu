@@ -250,7 +250,9 @@ k_c2c_planes(const float2 *__restrict__ Y, long long ldy, int K, int n_frames, i
     c2c_row<T, true>(live ? Y + row * ldy : Y, live ? K : 0, tw, bufs + (size_t)i * T, c, 1 + i);
     const bool flag = *nonfinite != 0;
     const float sc = live ? frame_scale(__ldg(fbound + f)) : 0.f;
-    __syncthreads();  // every transform's buffer read: reuse them as the stage
+    // transform i's stage entries [i][k] occupy exactly its own buffer: once
+    // its own threads have read it (named barrier 1 + i), the others need not wait
+    xform_sync<P::NT>(1 + i);
 #pragma unroll
     for (int t = 0; t < S2::ITER; ++t) {
         const int j = S2::lane_j(t);
